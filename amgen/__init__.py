@@ -233,3 +233,38 @@ def config(name: str, steps: int | None = None, n: int | None = None) -> Workloa
         x, y = hotspot_positions(N, side, side, seed=2)
         return Workload(name, side, side, None, x, y, 1, steps or 1000, profile="busy", Q=50_000)
     raise KeyError(name)
+
+
+def banded_state(n: int, w: int, h: int, seed: int, band: int = 24, gap: int = 6,
+                 p_running: float = 0.3, p_done: float = 0.0, target: int = 0,
+                 hot_frac: float = 0.5):
+    """A state with a large step spread that satisfies the validity condition P:156
+    by construction (for r_p < gap and v <= band + gap): agents only inside vertical
+    bands of width ``band`` separated by empty gaps of width ``gap``; band k is at
+    step k (steps change by one per band), so agents K bands apart are at least
+    (K-1)(band+gap)+gap > r_p + (K-1)v apart.  Half the agents sit in hotspots.
+    Statuses: RUNNING with p_running, DONE (step = target) with p_done."""
+    rng = np.random.default_rng(seed)
+    period = band + gap
+    nb = max(1, w // period)
+    n_hot = int(n * hot_frac)
+    spots = max(1, n_hot // 250)
+    cx = rng.uniform(0, w, spots)
+    cy = rng.uniform(0, h, spots)
+    sp = np.arange(n_hot) % spots
+    x = np.concatenate([np.rint(cx[sp] + rng.normal(0, 40, n_hot)), rng.integers(0, w, n - n_hot)])
+    y = np.concatenate([np.rint(cy[sp] + rng.normal(0, 40, n_hot)), rng.integers(0, h, n - n_hot)])
+    x = np.clip(x, 0, nb * period - 1).astype(np.int64)
+    y = np.clip(y, 0, h - 1).astype(np.int32)
+    k = x // period
+    off = x % period
+    off = np.where(off >= band, band - 1, off)       # push gap agents to the band's edge
+    x = (k * period + off).astype(np.int32)
+    step = k.astype(np.int32)
+    status = (rng.random(n) < p_running).astype(np.uint8)
+    if p_done > 0 and target > 0:
+        done = rng.random(n) < p_done
+        status[done] = 2
+        step[done] = target
+    perm = rng.permutation(n)
+    return x[perm], y[perm], step[perm], status[perm]

@@ -1,0 +1,92 @@
+/*
+ * am_driver.h -- C ABI of the GPU-resident trace-replay driver (libametro.so).
+ *
+ * The paper evaluates AI Metropolis by replaying recorded GenAgent traces (replay
+ * mode) through its controller/worker loop (Alg. 3).  Those traces
+ * and the LLM are out of scope here: agent actions come from a deterministic
+ * random-walk policy and LLM latencies are sampled from integer tables
+ * (SURVEY 8(c.4)).  LLM capacity is infinite: every ready
+ * cluster starts at once.
+ *
+ * Event rules (integer microseconds), per simulation b with clock t_b (start 0):
+ *   1. commit every RUNNING agent whose cluster completion time <= t_b: apply the
+ *      move computed at dispatch, step += 1 (worker l.20-21, controller l.11-12);
+ *   2. one tracker round (am_update + am_ready, Alg. 3 l.8-9);
+ *   3. each ready cluster C gets completion time t_b + max_{i in C} dur(i, s_i);
+ *      every member's move is computed now from its perception (all perceived agents
+ *      are cluster-mates, so the inputs equal the lock-step run's);
+ *   4. t_b = min pending completion time (quantum 0), else rounded up to a multiple
+ *      of the quantum.
+ * A simulation ends when all its agents are DONE (step == target); T_ooo[b] is the
+ * time of that last commit.  All simulations advance one round per am_replay_round.
+ *
+ * Synthetic model (identical definition implemented independently by the oracle):
+ *   mix64 = splitmix64 finaliser; key3(s,a,b) = mix64(mix64(mix64(s+a)+b))
+ *   digest_i = sum_{j perceived} mix64((j<<32) ^ ((u16)dx<<16) ^ (u16)dy),
+ *              perceived = same-step non-DONE j != i with dist <= radius_p
+ *   h = mix64(key3(policy_seed, i, s) + digest_i); move = {0,+x,-x,+y,-y}[h % 5],
+ *       cancelled if the target tile is a wall or off the map
+ *   K = vals[min{m : (key3(lat_seed,i,s) >> 32) < cdf32[m]}]
+ *   dur(i,s) = base_us + sum_{k<K} lat[key3(lat_seed ^ 0xC0FFEE, (i<<20) ^ s, k) >> 54]
+ *
+ * Ownership: every pointer in am_synth and every array argument is a caller-owned
+ * DEVICE pointer that must stay alive while the replay exists; outputs marked
+ * "host" are host memory.  Errors as in am.h.
+ */
+#ifndef AM_DRIVER_H_
+#define AM_DRIVER_H_
+
+#include <stdint.h>
+#include "am.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    const uint32_t* lat;        /* [1024] per-call latency quantiles, microseconds        */
+    const uint64_t* cdf32;      /* [n_vals] cumulative call-count probability * 2^32      */
+    const int32_t*  vals;       /* [n_vals] call counts                                    */
+    int32_t  n_vals;            /* 1..16                                                   */
+    int32_t  base_us;           /* fixed per-step cost                                     */
+    uint64_t lat_seed;
+    uint64_t policy_seed;
+    const uint8_t* wall;        /* [map_h*map_w] row-major, 1 = wall; NULL = open map      */
+    const int64_t* dur_table;   /* optional explicit durations [n_agents][dur_T]; NULL     */
+    int32_t  dur_T;
+    int32_t  policy;            /* 0 = random walk, 1 = always stay                         */
+} am_synth;
+
+typedef struct am_replay am_replay;
+
+/* Create a replay on ctx (which must have been created with target_step > 0; the
+ * replay sets AM_DIGEST and clears AM_PEEK/AM_ASYNC on it as needed).
+ * positions int32 [n][2] and steps int32 [n] are the world state, updated in place
+ * by commits; the replay starts from the current contents (steps normally all 0). */
+int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* synth,
+                     int64_t quantum_us, int32_t* positions, int32_t* steps);
+
+/* Run up to max_rounds rounds without host synchronisation (CUDA graph of one round
+ * replayed), then synchronise.  *active (host) receives the number of agents not yet
+ * DONE (0 = every simulation finished).  Rounds after a simulation finished are no-ops. */
+int am_replay_run(am_replay* r, int64_t max_rounds, int64_t* active);
+
+/* Exactly one round with its outputs kept for inspection (tests): mask uint8 [n],
+ * order int32 [n], labels int32 [n] device arrays (may be NULL); *n_ready host. */
+int am_replay_step(am_replay* r, uint8_t* mask, int32_t* order, int32_t* labels,
+                   int32_t* n_ready);
+
+/* Results: T_ooo int64 [n_sims] (host), rounds int64 [n_sims] (host; rounds in which
+ * the simulation had at least one active agent), traj uint64 [n] (device, may be NULL:
+ * per-agent trajectory hash chained at every commit). */
+int am_replay_results(am_replay* r, int64_t* T_ooo, int64_t* rounds, uint64_t* traj);
+
+/* Total agent-steps dispatched so far (host). */
+int am_replay_dispatched(am_replay* r, int64_t* agent_steps);
+
+int am_replay_destroy(am_replay* r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AM_DRIVER_H_ */

@@ -1,0 +1,370 @@
+// am_driver.cu -- GPU-resident trace-replay driver (include/am_driver.h).
+//
+// One replay round for every simulation at once (Alg. 3 with infinite LLM capacity,
+// replay mode P:228): k_commit -> am_update -> am_ready -> k_disp_a -> k_disp_b.
+// The synthetic policy/latency model is the same definition the oracle implements
+// independently (am_driver.h); nothing here is shared with oracle/.
+#include <climits>
+#include <cstdio>
+#include <new>
+
+#include "am_driver.h"
+#include "am_internal.cuh"
+
+namespace am {
+
+struct RepDev {
+    Dev d;                      // tracker context (labels, digests, status)
+    am_synth sy;
+    long long Q;
+    int2* pos;                  // world state (caller-owned)
+    int32_t* steps;
+    long long* tcommit;         // [n] completion time of the agent's dispatched step
+    int2* newpos;               // [n] move computed at dispatch
+    unsigned long long* traj;   // [n]
+    long long* tcl;             // [n] cluster completion time, indexed by root label
+    long long* t_sim;           // [S] current event time
+    long long* tnext;           // [S] accumulator: min pending completion (LLONG_MAX)
+    long long* tdone;           // [S] time of the last commit that finished an agent
+    long long* rounds;          // [S]
+    int32_t* active_flag;       // [S]
+    const int32_t* order;       // this round's order (replay-owned)
+    long long* dispatched;      // [1]
+    int32_t* liveness;          // [1]
+    Chain* chain;               // last-block counter of k_disp_b
+};
+
+__device__ __forceinline__ int sim_of(const Dev& d, int i)
+{
+    return d.n_sims == 1 ? 0 : (int)(((long long)i * d.n_sims + d.n_sims - 1) / d.n);
+}
+
+__device__ __forceinline__ unsigned long long traj_step(unsigned long long th, int s, int x, int y)
+{
+    return mix64(th ^ (((unsigned long long)(uint32_t)s << 32) | ((unsigned long long)(uint16_t)x << 16) |
+                       (unsigned long long)(uint16_t)y));
+}
+
+// duration of agent i's step s in integer microseconds
+__device__ __forceinline__ long long duration(const am_synth& sy, int i, int s)
+{
+    if (sy.dur_table) return sy.dur_table[(long long)i * sy.dur_T + s];
+    const unsigned long long u = key3(sy.lat_seed, (uint32_t)i, (uint32_t)s);
+    const unsigned long long hi = u >> 32;
+    int m = 0;
+    while (m < sy.n_vals - 1 && !(hi < sy.cdf32[m])) m++;
+    const int K = sy.vals[m];
+    long long dsum = sy.base_us;
+    for (int k = 0; k < K; k++) {
+        const unsigned long long h =
+            key3(sy.lat_seed ^ 0xC0FFEEULL, ((unsigned long long)(uint32_t)i << 20) ^ (uint32_t)s, (uint32_t)k);
+        dsum += sy.lat[h >> 54];
+    }
+    return dsum;
+}
+
+// commit every RUNNING agent whose cluster completed (tcommit <= t_sim): the move
+// computed at dispatch is applied and the step advances (worker l.20-21).
+__global__ void __launch_bounds__(256) k_commit(RepDev r)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const Dev& d = r.d;
+    if (i >= d.n) return;
+    const uint8_t st = d.status[d.ctl->cur][i];
+    if (st == ST_DONE) return;
+    const int b = sim_of(d, i);
+    const long long t = r.t_sim[b];
+    bool active = true;
+    if (st == ST_RUNNING) {
+        const long long tc = r.tcommit[i];
+        if (tc <= t) {
+            const int2 np = r.newpos[i];
+            const int s = r.steps[i] + 1;
+            r.pos[i] = np;
+            r.steps[i] = s;
+            r.traj[i] = traj_step(r.traj[i], s, np.x, np.y);
+            if (d.target > 0 && s == d.target) {
+                active = false;
+                atomicMax((unsigned long long*)(r.tdone + b), (unsigned long long)t);
+            }
+        } else {
+            // stays RUNNING through this round: bounds the next event
+            atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
+        }
+    }
+    if (active) r.active_flag[b] = 1;
+}
+
+// dispatch, part a: cluster completion time = t + max member duration (atomicMax at
+// the cluster's root label; a stale value is <= t).
+__global__ void __launch_bounds__(256) k_disp_a(RepDev r)
+{
+    const Dev& d = r.d;
+    const int nr = d.ctl->n_ready;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k == 0) *r.dispatched += nr;
+    if (k >= nr) return;
+    const int i = r.order[k];
+    const int b = sim_of(d, i);
+    const long long tc = r.t_sim[b] + duration(r.sy, i, r.steps[i]);
+    atomicMax((unsigned long long*)(r.tcl + d.labels[i]), (unsigned long long)tc);
+}
+
+// dispatch, part b: member completion times and moves (random-walk policy on the
+// perception digest), next event per simulation (last block).
+__global__ void __launch_bounds__(256) k_disp_b(RepDev r)
+{
+    const Dev& d = r.d;
+    const int nr = d.ctl->n_ready;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < nr) {
+        const int i = r.order[k];
+        const int b = sim_of(d, i);
+        const long long tc = r.tcl[d.labels[i]];
+        r.tcommit[i] = tc;
+        const int s = r.steps[i];
+        const int2 p = r.pos[i];
+        int mv = 0;
+        if (r.sy.policy == 0) {
+            const unsigned long long h = mix64(key3(r.sy.policy_seed, (uint32_t)i, (uint32_t)s) + d.digest[i]);
+            mv = (int)(h % 5ull);
+        }
+        const int qx = p.x + (mv == 1) - (mv == 2), qy = p.y + (mv == 3) - (mv == 4);
+        bool ok = qx >= 0 && qx < d.map_w && qy >= 0 && qy < d.map_h;
+        if (ok && r.sy.wall && r.sy.wall[(long long)qy * d.map_w + qx]) ok = false;
+        r.newpos[i] = ok ? make_int2(qx, qy) : p;
+        atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
+    }
+    // (agents still RUNNING from earlier rounds were folded into tnext by k_commit)
+    if (finish_block(r.chain, gridDim.x)) {
+        for (int b = threadIdx.x; b < d.n_sims; b += blockDim.x) {
+            const long long tn = *(volatile long long*)(r.tnext + b);
+            const int act = *(volatile int32_t*)(r.active_flag + b);
+            if (act) {
+                r.rounds[b] += 1;
+                if (tn == LLONG_MAX) {
+                    *r.liveness = 1;
+                } else {
+                    r.t_sim[b] = r.Q > 0 ? ((tn + r.Q - 1) / r.Q) * r.Q : tn;
+                }
+            }
+            r.tnext[b] = LLONG_MAX;
+            r.active_flag[b] = 0;
+        }
+    }
+}
+
+}  // namespace am
+
+using namespace am;
+
+struct am_replay {
+    am_ctx* ctx = nullptr;
+    RepDev r{};
+    void* mem = nullptr;
+    uint8_t* mask = nullptr;
+    int32_t* order = nullptr;
+    cudaStream_t stream = nullptr;      // own stream (graph capture)
+    cudaStream_t user_stream = nullptr;
+    cudaGraphExec_t g1 = nullptr, g8 = nullptr;
+    long long* h_buf = nullptr;         // pinned: dispatched, liveness
+};
+
+static int rp_err(am_replay* rp, cudaError_t e, const char* where)
+{
+    char buf[256];
+    snprintf(buf, sizeof buf, "%s: %s", where, cudaGetErrorString(e));
+    if (rp && rp->ctx) rp->ctx->err = buf;
+    return AM_E_CUDA;
+}
+#define RK(call)                                             \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return rp_err(rp, e_, #call); \
+    } while (0)
+
+static int enqueue_round(am_replay* rp)
+{
+    am_ctx* c = rp->ctx;
+    const int n = c->d.n;
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    k_commit<<<nb, 256, 0, rp->stream>>>(rp->r);
+    int rc = am_update(c, (const int32_t*)rp->r.pos, rp->r.steps);
+    if (rc) return rc;
+    rc = am_ready(c, rp->mask, rp->order, nullptr);
+    if (rc) return rc;
+    rp->r.d = c->d;
+    k_disp_a<<<nb, 256, 0, rp->stream>>>(rp->r);
+    k_disp_b<<<nb, 256, 0, rp->stream>>>(rp->r);
+    RK(cudaGetLastError());
+    return AM_OK;
+}
+
+extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* synth, int64_t quantum_us,
+                                int32_t* positions, int32_t* steps)
+{
+    if (!out || !ctx || !synth || !positions || !steps) return AM_E_ARG;
+    if (ctx->d.target <= 0) {
+        ctx->err = "am_replay_create: the context needs target_step > 0";
+        return AM_E_ARG;
+    }
+    if (synth->n_vals < 1 || synth->n_vals > 16 || !synth->lat || !synth->cdf32 || !synth->vals) {
+        if (!synth->dur_table) {
+            ctx->err = "am_replay_create: bad latency tables";
+            return AM_E_ARG;
+        }
+    }
+    am_replay* rp = new (std::nothrow) am_replay();
+    if (!rp) return AM_E_ARG;
+    rp->ctx = ctx;
+    rp->user_stream = ctx->stream;
+    const long long n = std::max(1, ctx->d.n), S = ctx->d.n_sims;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~size_t(255); return o; };
+    size_t o_tc = take(8 * n), o_np = take(8 * n), o_tr = take(8 * n), o_tcl = take(8 * n);
+    size_t o_ts = take(8 * S), o_tn = take(8 * S), o_td = take(8 * S), o_rd = take(8 * S), o_af = take(4 * S);
+    size_t o_disp = take(8), o_live = take(4), o_chain = take(sizeof(Chain));
+    size_t o_mask = take(n), o_order = take(4 * n);
+    cudaError_t e = cudaMalloc(&rp->mem, off);
+    if (e != cudaSuccess) { delete rp; return rp_err(nullptr, e, "cudaMalloc"); }
+    char* b = (char*)rp->mem;
+    RepDev& r = rp->r;
+    r.sy = *synth;
+    r.Q = quantum_us;
+    r.pos = (int2*)positions;
+    r.steps = steps;
+    r.tcommit = (long long*)(b + o_tc);
+    r.newpos = (int2*)(b + o_np);
+    r.traj = (unsigned long long*)(b + o_tr);
+    r.tcl = (long long*)(b + o_tcl);
+    r.t_sim = (long long*)(b + o_ts);
+    r.tnext = (long long*)(b + o_tn);
+    r.tdone = (long long*)(b + o_td);
+    r.rounds = (long long*)(b + o_rd);
+    r.active_flag = (int32_t*)(b + o_af);
+    r.dispatched = (long long*)(b + o_disp);
+    r.liveness = (int32_t*)(b + o_live);
+    r.chain = (Chain*)(b + o_chain);
+    rp->mask = (uint8_t*)(b + o_mask);
+    rp->order = (int32_t*)(b + o_order);
+    r.order = rp->order;
+    RK(cudaStreamCreateWithFlags(&rp->stream, cudaStreamNonBlocking));
+    RK(cudaMallocHost((void**)&rp->h_buf, 64));
+    RK(cudaStreamSynchronize(rp->user_stream));
+    RK(cudaMemsetAsync(rp->mem, 0, off, rp->stream));
+    RK(cudaMemsetAsync(r.tnext, 0x7F, 8 * S, rp->stream));  // "no pending" marker
+    RK(cudaStreamSynchronize(rp->stream));
+    // tnext must be exactly LLONG_MAX: fill with a tiny copy
+    {
+        long long* h = (long long*)malloc(8 * S);
+        for (long long k = 0; k < S; k++) h[k] = LLONG_MAX;
+        RK(cudaMemcpy(r.tnext, h, 8 * S, cudaMemcpyHostToDevice));
+        free(h);
+    }
+    am_set_stream(ctx, rp->stream);
+    ctx->d.flags = (ctx->d.flags | AM_DIGEST | AM_ASYNC) & ~AM_PEEK;
+    am_reset(ctx);
+    int rc = am_update(ctx, positions, steps);  // initial state (synchronous)
+    if (rc) {
+        am_replay_destroy(rp);
+        return rc;
+    }
+    r.d = ctx->d;
+    *out = rp;
+    return AM_OK;
+}
+
+static int build_graph(am_replay* rp, int rounds, cudaGraphExec_t* exec)
+{
+    cudaGraph_t g;
+    RK(cudaStreamBeginCapture(rp->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = AM_OK;
+    for (int k = 0; k < rounds && rc == AM_OK; k++) rc = enqueue_round(rp);
+    cudaError_t e = cudaStreamEndCapture(rp->stream, &g);
+    if (rc) return rc;
+    if (e != cudaSuccess) return rp_err(rp, e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return rp_err(rp, e, "cudaGraphInstantiate");
+    return AM_OK;
+}
+
+static int finish_check(am_replay* rp, int64_t* active)
+{
+    am_ctx* c = rp->ctx;
+    RK(cudaMemcpyAsync(rp->h_buf, rp->r.liveness, 4, cudaMemcpyDeviceToHost, rp->stream));
+    int rc = am_sync(c);  // reads the control block (n_active) + validation errors
+    if (rc) return rc;
+    if (*(int32_t*)rp->h_buf) {
+        c->err = "replay: agents not DONE but nothing running (liveness)";
+        return AM_E_LIVENESS;
+    }
+    if (active) *active = c->h_ctl->n_active;
+    return AM_OK;
+}
+
+extern "C" int am_replay_run(am_replay* rp, int64_t max_rounds, int64_t* active)
+{
+    if (!rp) return AM_E_ARG;
+    int rc;
+    if (!rp->g8 && (rc = build_graph(rp, 8, &rp->g8))) return rc;
+    if (!rp->g1 && (rc = build_graph(rp, 1, &rp->g1))) return rc;
+    int64_t k = 0;
+    for (; k + 8 <= max_rounds; k += 8) RK(cudaGraphLaunch(rp->g8, rp->stream));
+    for (; k < max_rounds; k++) RK(cudaGraphLaunch(rp->g1, rp->stream));
+    return finish_check(rp, active);
+}
+
+extern "C" int am_replay_step(am_replay* rp, uint8_t* mask, int32_t* order, int32_t* labels, int32_t* n_ready)
+{
+    if (!rp) return AM_E_ARG;
+    int rc = enqueue_round(rp);
+    if (rc) return rc;
+    am_ctx* c = rp->ctx;
+    const size_t n = (size_t)c->d.n;
+    if (mask) RK(cudaMemcpyAsync(mask, rp->mask, n, cudaMemcpyDeviceToDevice, rp->stream));
+    if (order) RK(cudaMemcpyAsync(order, rp->order, 4 * n, cudaMemcpyDeviceToDevice, rp->stream));
+    if (labels) RK(cudaMemcpyAsync(labels, c->d.labels, 4 * n, cudaMemcpyDeviceToDevice, rp->stream));
+    int64_t act = 0;
+    rc = finish_check(rp, &act);
+    if (rc) return rc;
+    if (n_ready) *n_ready = c->h_ctl->n_ready;
+    return AM_OK;
+}
+
+extern "C" int am_replay_results(am_replay* rp, int64_t* T_ooo, int64_t* rounds, uint64_t* traj)
+{
+    if (!rp) return AM_E_ARG;
+    const size_t S = (size_t)rp->ctx->d.n_sims;
+    RK(cudaStreamSynchronize(rp->stream));
+    if (T_ooo) RK(cudaMemcpy(T_ooo, rp->r.tdone, 8 * S, cudaMemcpyDeviceToHost));
+    if (rounds) RK(cudaMemcpy(rounds, rp->r.rounds, 8 * S, cudaMemcpyDeviceToHost));
+    if (traj) RK(cudaMemcpy(traj, rp->r.traj, 8 * (size_t)rp->ctx->d.n, cudaMemcpyDeviceToDevice));
+    return AM_OK;
+}
+
+extern "C" int am_replay_dispatched(am_replay* rp, int64_t* agent_steps)
+{
+    if (!rp || !agent_steps) return AM_E_ARG;
+    RK(cudaMemcpyAsync(rp->h_buf + 1, rp->r.dispatched, 8, cudaMemcpyDeviceToHost, rp->stream));
+    RK(cudaStreamSynchronize(rp->stream));
+    *agent_steps = rp->h_buf[1];
+    return AM_OK;
+}
+
+extern "C" int am_replay_destroy(am_replay* rp)
+{
+    if (!rp) return AM_OK;
+    if (rp->stream) cudaStreamSynchronize(rp->stream);
+    if (rp->g1) cudaGraphExecDestroy(rp->g1);
+    if (rp->g8) cudaGraphExecDestroy(rp->g8);
+    if (rp->ctx) {
+        am_set_stream(rp->ctx, rp->user_stream);
+        rp->ctx->d.flags &= ~AM_ASYNC;
+    }
+    if (rp->stream) cudaStreamDestroy(rp->stream);
+    if (rp->h_buf) cudaFreeHost(rp->h_buf);
+    cudaFree(rp->mem);
+    delete rp;
+    return AM_OK;
+}

@@ -1,0 +1,394 @@
+// am_host.cu -- the C ABI (include/am.h): context, workspace, launch sequence.
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "am_internal.cuh"
+
+namespace am {
+__global__ void k_ingest(Dev d, const int2* npos, const int32_t* nstep, const uint8_t* nstat, int mode);
+__global__ void k_bin(Dev d);
+__global__ void k_cells(Dev d);
+__global__ void k_scatter(Dev d);
+__global__ void k_scan(Dev d);
+__global__ void k_finalize(Dev d);
+__global__ void k_ready(Dev d, uint8_t* mask);
+__global__ void k_sort_hist(Dev d, int max_passes);
+__global__ void k_sort_pass(Dev d, int pass, int32_t* order);
+__global__ void k_small(Dev d, uint8_t* mask, int32_t* order);
+__global__ void k_round_begin(Ctl* ctl);
+
+__global__ void k_copy_status(Dev d, uint8_t* out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < d.n) out[i] = d.status[d.ctl->cur][i];
+}
+}  // namespace am
+
+using namespace am;
+
+static thread_local std::string g_init_err;
+
+static int set_err(am_ctx* c, int code, const char* msg)
+{
+    if (c) c->err = msg; else g_init_err = msg;
+    return code;
+}
+
+static int cuda_err(am_ctx* c, cudaError_t e, const char* where)
+{
+    char buf[256];
+    snprintf(buf, sizeof buf, "%s: %s", where, cudaGetErrorString(e));
+    return set_err(c, AM_E_CUDA, buf);
+}
+
+#define CK(ctx, call)                                         \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return cuda_err(ctx, e_, #call); \
+    } while (0)
+
+static int err_code(int bits)
+{
+    if (bits & ERR_BOUNDS) return AM_E_BOUNDS;
+    if (bits & ERR_PROTOCOL) return AM_E_PROTOCOL;
+    if (bits & ERR_VELOCITY) return AM_E_VELOCITY;
+    return AM_OK;
+}
+
+static int ilog2_ceil(long long x)
+{
+    int l = 0;
+    while ((1LL << l) < x) l++;
+    return l;
+}
+
+static inline unsigned blocks(long long n, int t) { return (unsigned)std::max(1LL, (n + t - 1) / t); }
+
+extern "C" const char* am_version(void) { return "ametro-b200 0.1 (sm_100a)"; }
+
+extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max,
+                       int32_t n_agents, const am_config* cfg)
+{
+    if (!out) return set_err(nullptr, AM_E_ARG, "am_init: out is NULL");
+    *out = nullptr;
+    if (map_w < 1 || map_h < 1 || map_w > 32768 || map_h > 32768)
+        return set_err(nullptr, AM_E_ARG, "am_init: map dims must be in [1, 32768]");
+    if (radius_p < 0 || v_max < 0 || n_agents < 0 || n_agents > (1 << 28))
+        return set_err(nullptr, AM_E_ARG, "am_init: negative radius/speed or bad agent count");
+    am_config c{};
+    c.n_sims = 1;
+    c.flags = AM_VALIDATE;
+    if (cfg) c = *cfg;
+    if (c.n_sims < 1 || (n_agents > 0 && c.n_sims > n_agents))
+        return set_err(nullptr, AM_E_ARG, "am_init: n_sims must be in [1, n_agents]");
+    if (c.metric != AM_METRIC_L2 && c.metric != AM_METRIC_LINF)
+        return set_err(nullptr, AM_E_ARG, "am_init: unknown metric");
+    if (c.cell < 0 || (c.cell & (c.cell - 1)))
+        return set_err(nullptr, AM_E_ARG, "am_init: cell must be 0 or a power of two");
+    if (c.target_step < 0) return set_err(nullptr, AM_E_ARG, "am_init: negative target_step");
+
+    am_ctx* x = new (std::nothrow) am_ctx();
+    if (!x) return set_err(nullptr, AM_E_ARG, "am_init: out of host memory");
+    const long long n = n_agents;
+    const int per_sim_max = (int)((n + c.n_sims - 1) / c.n_sims);
+    Dev& d = x->d;
+    d.n = n_agents;
+    d.n_sims = c.n_sims;
+    d.map_w = map_w;
+    d.map_h = map_h;
+    d.r_p = radius_p;
+    d.v = v_max;
+    d.target = c.target_step;
+    d.metric = c.metric;
+    d.flags = c.flags;
+    x->stream = (cudaStream_t)c.stream;
+
+    // path selection
+    bool small = (c.n_sims > 1) || (n <= kSmallMax);
+    if (c.flags & AM_FORCE_BINNED) small = false;
+    if (c.flags & AM_FORCE_SMALL) small = true;
+    if (small && per_sim_max > kSmallMax) {
+        delete x;
+        return set_err(nullptr, AM_E_ARG, "am_init: fused path needs <= 1024 agents per simulation");
+    }
+    if (!small && c.n_sims > 1) {
+        delete x;
+        return set_err(nullptr, AM_E_ARG, "am_init: the binned path takes one simulation");
+    }
+    x->path = small ? 0 : 1;
+    x->small_threads = std::max(32, ((per_sim_max + 31) / 32) * 32);
+
+    // cell size: >= R_c = r_p + v (coupling needs <= 2x2 cells), grown until the Morton
+    // grid has at most max(4N, 4096) cells and at most 4096 cells per side.
+    long long Rc = (long long)radius_p + v_max;
+    int clog;
+    if (c.cell) {
+        clog = ilog2_ceil(c.cell);
+    } else {
+        clog = ilog2_ceil(std::max(1LL, Rc));
+        for (;;) {
+            long long side = std::max((map_w + (1LL << clog) - 1) >> clog, (map_h + (1LL << clog) - 1) >> clog);
+            long long g = 1LL << ilog2_ceil(std::max(64LL, side));
+            if (g * g <= std::max(4 * n, 4096LL) || clog >= 15) break;
+            clog++;
+        }
+    }
+    for (;;) {  // hard cap on the grid side
+        long long side = std::max((map_w + (1LL << clog) - 1) >> clog, (map_h + (1LL << clog) - 1) >> clog);
+        if (side <= 4096 || clog >= 15) break;
+        clog++;
+    }
+    {
+        long long side = std::max((map_w + (1LL << clog) - 1) >> clog, (map_h + (1LL << clog) - 1) >> clog);
+        d.glog = ilog2_ceil(std::max(64LL, side));
+    }
+    d.clog = clog;
+    d.ncells = 1 << (2 * d.glog);
+    x->cell = 1 << clog;
+    d.idbits = std::max(1, ilog2_ceil(std::max(2LL, n)));
+    {
+        int lagbits = c.target_step > 0 ? ilog2_ceil((long long)c.target_step + 1) : 31;
+        int bits = lagbits + d.idbits;
+        x->sort_passes_max = std::min(kMaxSortPasses, std::max(1, (bits + 7) / 8));
+    }
+    x->ntiles_sort = (int)blocks(n, kSortTile);
+    x->ntiles_ready = (int)blocks(n, kReadyTile);
+    x->ntiles_cells = d.ncells / kCellsPerTile;
+
+    // workspace layout
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    const size_t N = (size_t)std::max(1LL, n);
+    size_t o_ctl = take(sizeof(Ctl));
+    size_t o_pos0 = take(8 * N), o_pos1 = take(8 * N);
+    size_t o_st0 = take(4 * N), o_st1 = take(4 * N);
+    size_t o_ss0 = take(N), o_ss1 = take(N);
+    size_t o_labels = take(4 * N), o_digest = take(8 * N);
+    size_t o_tiles_s = take(8 * (size_t)c.n_sims);
+    size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
+           o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
+           o_tsort = 0, o_gh = 0, o_gs = 0;
+    const size_t NC = (size_t)d.ncells;
+    if (x->path == 1) {
+        o_key = take(4 * N); o_rank = take(4 * N);
+        o_cnt = take(4 * NC); o_cmin = take(4 * NC);
+        o_ctab = take(8 * (NC + 1)); o_l1 = take(4 * (NC / 16)); o_l2 = take(4 * (NC / 256));
+        o_rec = take(16 * N); o_blk = take(4 * (N / 32 + 1));
+        o_par = take(4 * N); o_bad = take(N);
+        o_rk0 = take(8 * N); o_rk1 = take(8 * N); o_rv0 = take(4 * N); o_rv1 = take(4 * N);
+        o_tc = take(8 * (size_t)x->ntiles_cells); o_tr = take(8 * (size_t)x->ntiles_ready);
+        o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * 256);
+        o_gh = take(4 * kMaxSortPasses * 256); o_gs = take(4 * kMaxSortPasses * 256);
+    }
+    x->ws_bytes = off;
+    cudaError_t e = cudaMalloc(&x->ws, off);
+    if (e != cudaSuccess) { delete x; return cuda_err(nullptr, e, "am_init: cudaMalloc"); }
+    e = cudaMallocHost((void**)&x->h_ctl, sizeof(Ctl));
+    if (e != cudaSuccess) { cudaFree(x->ws); delete x; return cuda_err(nullptr, e, "am_init: cudaMallocHost"); }
+    char* b = (char*)x->ws;
+    d.ctl = (Ctl*)(b + o_ctl);
+    d.pos[0] = (int2*)(b + o_pos0); d.pos[1] = (int2*)(b + o_pos1);
+    d.step[0] = (int32_t*)(b + o_st0); d.step[1] = (int32_t*)(b + o_st1);
+    d.status[0] = (uint8_t*)(b + o_ss0); d.status[1] = (uint8_t*)(b + o_ss1);
+    d.labels = (int32_t*)(b + o_labels);
+    d.digest = (unsigned long long*)(b + o_digest);
+    d.tiles_s = (unsigned long long*)(b + o_tiles_s);
+    if (x->path == 1) {
+        d.key = (uint32_t*)(b + o_key); d.rank = (uint32_t*)(b + o_rank);
+        d.cnt = (uint32_t*)(b + o_cnt); d.cmin = (int32_t*)(b + o_cmin);
+        d.ctab = (int2*)(b + o_ctab); d.lmin1 = (int32_t*)(b + o_l1); d.lmin2 = (int32_t*)(b + o_l2);
+        d.rec = (int4*)(b + o_rec); d.blkbits = (uint32_t*)(b + o_blk);
+        d.parent = (uint32_t*)(b + o_par); d.bad = (uint8_t*)(b + o_bad);
+        d.rkey[0] = (unsigned long long*)(b + o_rk0); d.rkey[1] = (unsigned long long*)(b + o_rk1);
+        d.rval[0] = (uint32_t*)(b + o_rv0); d.rval[1] = (uint32_t*)(b + o_rv1);
+        d.tiles_c = (unsigned long long*)(b + o_tc); d.tiles_r = (unsigned long long*)(b + o_tr);
+        d.tiles_sort = (unsigned long long*)(b + o_tsort);
+        d.ghist = (uint32_t*)(b + o_gh); d.gstart = (uint32_t*)(b + o_gs);
+    }
+    // initial contents: everything zero except the min-step table
+    e = cudaMemsetAsync(x->ws, 0, off, x->stream);
+    if (e == cudaSuccess && x->path == 1) e = cudaMemsetAsync(d.cmin, 0x7F, 4 * NC, x->stream);  // ~INT_MAX
+    Ctl h{};
+    h.acc_W = INT_MAX;
+    h.acc_S = INT_MIN;
+    h.W = INT_MAX;
+    h.S = INT_MIN;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d.ctl, &h, sizeof h, cudaMemcpyHostToDevice, x->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
+    if (e != cudaSuccess) {
+        cudaFree(x->ws); cudaFreeHost(x->h_ctl); delete x;
+        return cuda_err(nullptr, e, "am_init: workspace init");
+    }
+    x->stats.path = x->path;
+    x->stats.cell = x->cell;
+    *out = x;
+    return AM_OK;
+}
+
+
+static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, const uint8_t* st, int mode)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (c->d.n == 0) return AM_OK;
+    if (!pos || !steps || (mode == 2 && !st)) return set_err(c, AM_E_ARG, "NULL array");
+    k_ingest<<<blocks(c->d.n, 256), 256, 0, c->stream>>>(c->d, (const int2*)pos, steps, st, mode);
+    CK(c, cudaGetLastError());
+    return AM_OK;
+}
+
+extern "C" int am_update(am_ctx* c, const int32_t* positions, const int32_t* sim_steps)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    const bool first = c->first;
+    int rc = launch_ingest(c, positions, sim_steps, nullptr, first ? 1 : 0);
+    if (rc) return rc;
+    if (first) {
+        rc = am_sync(c);  // the initial state is checked synchronously
+        if (rc == AM_OK) c->first = false;
+    }
+    return rc;
+}
+
+extern "C" int am_set_state(am_ctx* c, const int32_t* positions, const int32_t* sim_steps,
+                            const uint8_t* status)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    int rc = launch_ingest(c, positions, sim_steps, status, 2);
+    if (rc) return rc;
+    rc = am_sync(c);
+    if (rc == AM_OK) c->first = false;
+    return rc;
+}
+
+static void fill_stats(am_ctx* c)
+{
+    const Ctl& h = *c->h_ctl;
+    c->stats.n_ready = h.n_ready;
+    c->stats.n_active = h.n_active;
+    c->stats.n_running = h.n_running;
+    c->stats.watermark = h.W;
+    c->stats.max_step = h.S;
+    c->stats.n_clusters = h.n_clusters;
+}
+
+extern "C" int am_sync(am_ctx* c)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    CK(c, cudaMemcpyAsync(c->h_ctl, c->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    fill_stats(c);
+    const int bits = c->h_ctl->err_sticky;
+    if (bits) {
+        CK(c, cudaMemsetAsync(&c->d.ctl->err_sticky, 0, sizeof(int32_t), c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        const int code = err_code(bits);
+        return set_err(c, code, code == AM_E_BOUNDS ? "update rejected: position out of bounds"
+                              : code == AM_E_PROTOCOL ? "update rejected: protocol violation"
+                                                      : "update rejected: velocity limit exceeded");
+    }
+    return AM_OK;
+}
+
+extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_ready)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (c->first) return set_err(c, AM_E_STATE, "am_ready before the initial am_update");
+    const bool async = (c->d.flags & AM_ASYNC) != 0;
+    if (!async && !n_ready) return set_err(c, AM_E_ARG, "n_ready is NULL");
+    if (c->d.n == 0) {
+        if (n_ready) *n_ready = 0;
+        return AM_OK;
+    }
+    if (!mask || !order) return set_err(c, AM_E_ARG, "NULL mask/order");
+    const Dev& d = c->d;
+    cudaStream_t s = c->stream;
+    k_round_begin<<<1, 1, 0, s>>>(d.ctl);
+    if (c->path == 0) {
+        k_small<<<d.n_sims, c->small_threads, 0, s>>>(d, mask, order);
+    } else {
+        const unsigned nb = blocks(d.n, 256);
+        k_bin<<<nb, 256, 0, s>>>(d);
+        k_cells<<<c->ntiles_cells, 256, 0, s>>>(d);
+        k_scatter<<<nb, 256, 0, s>>>(d);
+        k_scan<<<nb, 256, 0, s>>>(d);
+        k_finalize<<<nb, 256, 0, s>>>(d);
+        k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask);
+        k_sort_hist<<<c->ntiles_sort, 256, 0, s>>>(d, c->sort_passes_max);
+        for (int p = 0; p < c->sort_passes_max; p++)
+            k_sort_pass<<<c->ntiles_sort, 256, 0, s>>>(d, p, order);
+    }
+    CK(c, cudaGetLastError());
+    c->have_round = true;
+    if (async) return AM_OK;
+    int rc = am_sync(c);
+    *n_ready = rc == AM_OK ? c->h_ctl->n_ready : 0;
+    return rc;
+}
+
+extern "C" int am_clusters(am_ctx* c, int32_t* labels)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (!labels) return set_err(c, AM_E_ARG, "NULL labels");
+    if (!c->have_round) return set_err(c, AM_E_STATE, "am_clusters before any am_ready");
+    if (c->d.n == 0) return AM_OK;
+    CK(c, cudaMemcpyAsync(labels, c->d.labels, 4 * (size_t)c->d.n, cudaMemcpyDeviceToDevice, c->stream));
+    return AM_OK;
+}
+
+extern "C" int am_status(am_ctx* c, uint8_t* status)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (!status) return set_err(c, AM_E_ARG, "NULL status");
+    if (c->d.n == 0) return AM_OK;
+    k_copy_status<<<blocks(c->d.n, 256), 256, 0, c->stream>>>(c->d, status);
+    CK(c, cudaGetLastError());
+    return AM_OK;
+}
+
+extern "C" int am_stats(const am_ctx* c, am_round_stats* out)
+{
+    if (!c || !out) return AM_E_ARG;
+    *out = c->stats;
+    return AM_OK;
+}
+
+extern "C" int am_set_flags(am_ctx* c, uint32_t flags)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    c->d.flags = flags;
+    return AM_OK;
+}
+
+extern "C" int am_set_stream(am_ctx* c, void* stream)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    c->stream = (cudaStream_t)stream;
+    return AM_OK;
+}
+
+extern "C" int am_reset(am_ctx* c)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    c->first = true;
+    c->have_round = false;
+    return AM_OK;
+}
+
+extern "C" size_t am_workspace_bytes(const am_ctx* c) { return c ? c->ws_bytes : 0; }
+
+extern "C" const int32_t* am_ready_count_device(const am_ctx* c) { return c ? &c->d.ctl->n_ready : nullptr; }
+
+extern "C" int am_destroy(am_ctx* c)
+{
+    if (!c) return AM_OK;
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->ws);
+    cudaFreeHost(c->h_ctl);
+    delete c;
+    return AM_OK;
+}
+
+extern "C" const char* am_last_error(const am_ctx* c) { return c ? c->err.c_str() : g_init_err.c_str(); }

@@ -1,0 +1,278 @@
+// am_internal.cuh -- context layout and device helpers of libametro (sm_100a).
+//
+// Product code: shares nothing with oracle/ (the CPU oracle is test-only).
+// Citations "P:<line>" refer to /root/reference/PAPER.md.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "am.h"
+
+namespace am {
+
+constexpr int kSmallMax = 1024;           // agents per simulation for the fused kernel
+constexpr int kCellsPerTile = 4096;       // cell-table scan tile (256 threads x 16 cells)
+constexpr int kReadyTile = 2048;          // ready compaction tile (256 threads x 8 agents)
+constexpr int kSortTile = 2048;           // radix pass tile (256 threads x 8 keys)
+constexpr int kMaxSortPasses = 8;
+constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+constexpr uint32_t kRClamp = 46340u;      // >= every distance on a 32768^2 map; R^2 < 2^31
+
+enum : int32_t { ERR_BOUNDS = 1, ERR_PROTOCOL = 2, ERR_VELOCITY = 4 };
+enum : uint8_t { ST_IDLE = 0, ST_RUNNING = 1, ST_DONE = 2 };
+
+// dynamic tile ticket + "last block" counter of one grid-wide pass; the last block
+// to finish resets both, so the next launch starts clean (stream order).
+struct Chain {
+    unsigned ticket;
+    unsigned done;
+};
+
+// device control block (one per context, device memory; mirrored to pinned host)
+struct Ctl {
+    uint32_t cur;          // which of the two state buffers is committed
+    uint32_t epoch;        // bumped by every am_ready; tags chained-scan tile words
+    int32_t  err_new;      // error bits of the running am_update
+    int32_t  err_sticky;   // error bits not yet reported to the host
+    int32_t  W, S;         // watermark (min step of non-DONE) and max step
+    int32_t  n_active, n_running;
+    int32_t  n_ready, n_clusters;
+    int32_t  npasses;      // radix passes needed by this round's ready keys
+    int32_t  pad0;
+    // accumulators of am_update (reset by its last block)
+    int32_t  acc_W, acc_S, acc_active, acc_running;
+    unsigned long long sort_or;   // OR of all ready keys
+    Chain ingest, bin, cells, ready, hist, small_, pass[kMaxSortPasses];
+};
+
+// all device pointers of a context, passed by value to kernels
+struct Dev {
+    Ctl* ctl;
+    int32_t n, n_sims, map_w, map_h, r_p, v, target, metric;
+    uint32_t flags;
+    int32_t clog;          // log2 cell edge
+    int32_t glog;          // log2 cells per side of the Morton grid
+    int32_t ncells;        // (1 << glog)^2
+    int32_t idbits;        // bits to hold an agent id
+    // double-buffered state
+    int2* pos[2];
+    int32_t* step[2];
+    uint8_t* status[2];
+    // binned round
+    uint32_t* key;         // Morton cell key per agent (kSentinel = DONE)
+    uint32_t* rank;        // slot of the agent inside its cell
+    uint32_t* cnt;         // [ncells] agents per cell (zero between rounds)
+    int32_t* cmin;         // [ncells] min step per cell (INT_MAX between rounds)
+    int2* ctab;            // [ncells+1] {start, min step}
+    int32_t* lmin1;        // [ncells/16]  min step per 4x4-cell block
+    int32_t* lmin2;        // [ncells/256] min step per 16x16-cell block
+    int4* rec;             // [n] sorted records {x | y<<16, step, id, status}
+    uint32_t* blkbits;     // [n/32+1] blocked bit per sorted record
+    uint32_t* parent;      // [n] union-find forest in id space (root = min id)
+    uint8_t* bad;          // [n] cluster (root) has a blocked or RUNNING member
+    int32_t* labels;       // [n]
+    unsigned long long* digest;   // [n] perception digests (AM_DIGEST)
+    unsigned long long* rkey[2];  // [n] ready keys (ping-pong)
+    uint32_t* rval[2];            // [n] ready ids (ping-pong)
+    unsigned long long* tiles_c;  // chained-scan tile words: cell table scan
+    unsigned long long* tiles_r;  //   ready compaction
+    unsigned long long* tiles_s;  //   per-simulation (fused path)
+    unsigned long long* tiles_sort;  // [kMaxSortPasses][ntiles_sort][256]
+    uint32_t* ghist;              // [kMaxSortPasses][256]
+    uint32_t* gstart;             // [kMaxSortPasses][256]
+};
+
+}  // namespace am
+
+struct am_ctx {
+    am::Dev d;
+    am::Ctl* h_ctl = nullptr;        // pinned host mirror
+    cudaStream_t stream = nullptr;
+    int path = 0;                    // 0 = fused per-sim kernel, 1 = binned pipeline
+    int cell = 0;
+    int small_threads = 32;
+    int sort_passes_max = 1;
+    int ntiles_sort = 1;
+    int ntiles_ready = 1;
+    int ntiles_cells = 1;
+    bool first = true;
+    bool have_round = false;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    am_round_stats stats{};
+    std::string err;
+};
+
+// ---------------------------------------------------------------- device helpers
+namespace am {
+
+__device__ __forceinline__ uint32_t part1by1(uint32_t x)
+{
+    x &= 0xFFFFu;
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+// Morton (Z-order) key of a cell: every aligned 2^k x 2^k block of cells is a
+// contiguous key range, so the min-step pyramid is a min over contiguous ranges.
+__device__ __forceinline__ uint32_t morton(uint32_t cx, uint32_t cy)
+{
+    return part1by1(cx) | (part1by1(cy) << 1);
+}
+
+// blocking radius clamped so that R^2 fits in 31 bits; exact because the
+// clamp exceeds every distance on a <= 32768^2 map.
+__device__ __forceinline__ uint32_t rb_radius(long long lag, int v, int r_p)
+{
+    long long R = (lag + 1) * (long long)v + r_p;
+    return R > (long long)kRClamp ? kRClamp : (uint32_t)R;
+}
+
+__device__ __forceinline__ bool within(int dx, int dy, uint32_t R, int metric)
+{
+    if (metric == AM_METRIC_LINF) {
+        uint32_t ax = (uint32_t)abs(dx), ay = (uint32_t)abs(dy);
+        return ax <= R && ay <= R;
+    }
+    uint32_t d2 = (uint32_t)(dx * dx) + (uint32_t)(dy * dy);
+    return d2 <= R * R;
+}
+
+// distance from point (x,y) to the tile box [x0,x1] x [y0,y1] within R
+__device__ __forceinline__ bool box_within(int x, int y, int x0, int y0, int x1, int y1,
+                                           uint32_t R, int metric)
+{
+    int dx = x < x0 ? x0 - x : (x > x1 ? x - x1 : 0);
+    int dy = y < y0 ? y0 - y : (y > y1 ? y - y1 : 0);
+    return within(dx, dy, R, metric);
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z)
+{
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ unsigned long long key3(unsigned long long s, unsigned long long a,
+                                                   unsigned long long b)
+{
+    return mix64(mix64(mix64(s + a) + b));
+}
+// one perceived agent's contribution to the perception digest
+__device__ __forceinline__ unsigned long long digest_term(uint32_t j, int dx, int dy)
+{
+    unsigned long long w = ((unsigned long long)j << 32) ^
+                           ((unsigned long long)(uint16_t)dx << 16) ^ (unsigned long long)(uint16_t)dy;
+    return mix64(w);
+}
+
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p); }
+
+// union-find (global, id space): hook the larger root under the smaller, so every
+// root is the minimum id of its tree; find uses intermediate pointer jumping.
+__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x)
+{
+    uint32_t cur = ld_cg(parent + x);
+    if (cur != x) {
+        uint32_t prev = x, next;
+        while (cur > (next = ld_cg(parent + cur))) {
+            parent[prev] = next;
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+__device__ __forceinline__ void uf_unite(uint32_t* parent, uint32_t a, uint32_t b)
+{
+    uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            uint32_t old = atomicCAS(parent + rb, rb, ra);
+            if (old == rb) break;
+            rb = old;
+        } else {
+            uint32_t old = atomicCAS(parent + ra, ra, rb);
+            if (old == ra) break;
+            ra = old;
+        }
+    }
+}
+
+// ------------------------------------------------ chained (decoupled look-back) scan
+// tile word: [tag:30][flag:2][value:32]; flag 1 = aggregate, 2 = inclusive prefix.
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long tile_word(uint32_t tag, uint32_t flag, uint32_t val)
+{
+    return ((unsigned long long)(tag & 0x3FFFFFFFu) << 34) | ((unsigned long long)flag << 32) | val;
+}
+// publish this tile's aggregate, look back, publish the inclusive prefix; returns
+// the exclusive prefix.  Called by ONE thread.  tiles[t] for t < tile must be
+// published eventually (tickets are handed out in launch order).
+__device__ __forceinline__ uint32_t chain_scan(unsigned long long* tiles, uint32_t tile, uint32_t tag,
+                                               uint32_t agg)
+{
+    tag &= 0x3FFFFFFFu;
+    if (tile == 0) {
+        st_relaxed(tiles, tile_word(tag, 2, agg));
+        return 0;
+    }
+    st_relaxed(tiles + tile, tile_word(tag, 1, agg));
+    uint32_t excl = 0;
+    int j = (int)tile - 1;
+    while (j >= 0) {
+        unsigned long long w = ld_relaxed(tiles + j);
+        uint32_t wt = (uint32_t)(w >> 34), fl = (uint32_t)(w >> 32) & 3u;
+        if (wt != tag || fl == 0) continue;   // not yet published in this epoch
+        excl += (uint32_t)w;
+        if (fl == 2) break;
+        --j;
+    }
+    st_relaxed(tiles + tile, tile_word(tag, 2, excl + agg));
+    return excl;
+}
+
+__device__ __forceinline__ uint32_t take_ticket(Chain* c)
+{
+    __shared__ uint32_t t;
+    if (threadIdx.x == 0) t = atomicAdd(&c->ticket, 1u);
+    __syncthreads();
+    uint32_t r = t;
+    __syncthreads();
+    return r;
+}
+// returns true in thread 0 of the last block to finish (after a fence)
+__device__ __forceinline__ bool finish_block(Chain* c, uint32_t nblocks)
+{
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t d = atomicAdd(&c->done, 1u);
+        last = (d == nblocks - 1);
+        if (last) {
+            c->ticket = 0;
+            c->done = 0;
+            __threadfence();
+        }
+    }
+    __syncthreads();
+    return last;
+}
+
+}  // namespace am

@@ -1,0 +1,660 @@
+// am_kernels.cu -- the tracker's kernels for sm_100a.
+//
+// One scheduling round (Alg. 3 controller l.8-9) on the binned path:
+//   k_bin       cell key + slot per agent (counting sort, histogram by atomics)
+//   k_cells     chained scan of cell counts -> cell table {start, min step},
+//               min-step pyramid (4x4 and 16x16 Morton blocks)
+//   k_scatter   agents -> cell-sorted 16-byte records
+//   k_scan      time-dilated neighbour scan: blocked bits, coupling
+//               unions, perception digests
+//   k_finalize  labels = union-find roots (min id), bad[root] |= blocked | RUNNING
+//   k_ready     ready mask, dispatch, ordered compaction of the ready set
+//   k_sort_*    stable LSD radix sort of the ready set by (step, label) -> order
+// and the fused per-simulation path (k_small) for simulations of <= 1024 agents.
+#include <climits>
+
+#include "am_internal.cuh"
+
+namespace am {
+
+// ============================================================== am_update: ingest
+// mode 0 = commit (update_agents, Alg. 3 l.11), 1 = initial state,
+// 2 = full state with statuses (snapshot).  Reads state[cur], writes state[1-cur];
+// the last block flips cur iff no error was raised (all-or-nothing update).
+__global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ npos,
+                                                const int32_t* __restrict__ nstep,
+                                                const uint8_t* __restrict__ nstat, int mode)
+{
+    Ctl* ctl = d.ctl;
+    const uint32_t c = ctl->cur;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int err = 0, act = 0, run = 0;
+    int s = 0;
+    if (i < d.n) {
+        int2 p = npos[i];
+        s = nstep[i];
+        uint8_t st;
+        if (p.x < 0 || p.x >= d.map_w || p.y < 0 || p.y >= d.map_h) err |= ERR_BOUNDS;
+        if (mode == 0) {
+            const int os = d.step[c][i];
+            const uint8_t ost = d.status[c][i];
+            const long long ds = (long long)s - os;
+            st = ost;
+            if (ds == 0) {
+                if (d.flags & AM_VALIDATE) {
+                    int2 op = d.pos[c][i];
+                    if (op.x != p.x || op.y != p.y) err |= ERR_PROTOCOL;
+                }
+            } else if (ds == 1) {
+                if (ost != ST_RUNNING) {
+                    err |= ERR_PROTOCOL;
+                } else {
+                    if (d.flags & AM_VALIDATE) {
+                        int2 op = d.pos[c][i];
+                        if (!within(p.x - op.x, p.y - op.y, (uint32_t)d.v, d.metric)) err |= ERR_VELOCITY;
+                    }
+                    st = (d.target > 0 && s == d.target) ? ST_DONE : ST_IDLE;
+                }
+            } else {
+                err |= ERR_PROTOCOL;
+            }
+        } else if (mode == 1) {
+            if (s < 0 || (d.target > 0 && s > d.target)) err |= ERR_PROTOCOL;
+            st = (d.target > 0 && s == d.target) ? ST_DONE : ST_IDLE;
+        } else {
+            st = nstat[i];
+            if (st > ST_DONE || s < 0) err |= ERR_PROTOCOL;
+        }
+        d.pos[c ^ 1u][i] = p;
+        d.step[c ^ 1u][i] = s;
+        d.status[c ^ 1u][i] = st;
+        act = st != ST_DONE;
+        run = st == ST_RUNNING;
+    }
+    // block reductions
+    const int lane = threadIdx.x & 31;
+    int werr = __reduce_or_sync(0xFFFFFFFFu, (unsigned)err);
+    int wmin = __reduce_min_sync(0xFFFFFFFFu, act ? s : INT_MAX);
+    int wmax = __reduce_max_sync(0xFFFFFFFFu, act ? s : INT_MIN);
+    int wact = __reduce_add_sync(0xFFFFFFFFu, (unsigned)act);
+    int wrun = __reduce_add_sync(0xFFFFFFFFu, (unsigned)run);
+    if (lane == 0) {
+        if (werr) atomicOr(&ctl->err_new, werr);
+        if (wact) {
+            atomicMin(&ctl->acc_W, wmin);
+            atomicMax(&ctl->acc_S, wmax);
+            atomicAdd(&ctl->acc_active, wact);
+        }
+        if (wrun) atomicAdd(&ctl->acc_running, wrun);
+    }
+    if (finish_block(&ctl->ingest, gridDim.x) && threadIdx.x == 0) {
+        const int e = *(volatile int*)&ctl->err_new;
+        if (e == 0) {
+            ctl->cur = c ^ 1u;
+            ctl->W = *(volatile int*)&ctl->acc_W;
+            ctl->S = *(volatile int*)&ctl->acc_S;
+            ctl->n_active = *(volatile int*)&ctl->acc_active;
+            ctl->n_running = *(volatile int*)&ctl->acc_running;
+        } else {
+            ctl->err_sticky |= e;
+        }
+        ctl->err_new = 0;
+        ctl->acc_W = INT_MAX;
+        ctl->acc_S = INT_MIN;
+        ctl->acc_active = 0;
+        ctl->acc_running = 0;
+        __threadfence();
+    }
+}
+
+// ============================================================== binned round
+// k_bin: Morton cell key, slot inside the cell (atomic histogram), per-cell min step;
+// also resets the union-find forest and the per-root bad flags for this round.
+__global__ void __launch_bounds__(256) k_bin(Dev d)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.n) return;
+    const uint32_t c = d.ctl->cur;
+    const uint8_t st = d.status[c][i];
+    uint32_t key = kSentinel, rank = 0;
+    if (st != ST_DONE) {
+        const int2 p = d.pos[c][i];
+        key = morton((uint32_t)p.x >> d.clog, (uint32_t)p.y >> d.clog);
+        rank = atomicAdd(d.cnt + key, 1u);
+        atomicMin(d.cmin + key, d.step[c][i]);
+    }
+    d.key[i] = key;
+    d.rank[i] = rank;
+    d.parent[i] = (uint32_t)i;
+    d.bad[i] = 0;
+}
+
+// k_cells: exclusive scan of the cell counts in Morton order -> ctab{start, min};
+// lmin1 = min over each 16-cell (4x4) block, lmin2 over each 256-cell (16x16) block;
+// resets cnt/cmin for the next round.  256 threads x 16 cells per tile.
+__global__ void __launch_bounds__(256) k_cells(Dev d)
+{
+    Ctl* ctl = d.ctl;
+    __shared__ uint32_t wsum[8];
+    __shared__ uint32_t tile_excl;
+    const uint32_t tile = take_ticket(&ctl->cells);
+    const uint32_t tag = ctl->epoch * 16u + 1u;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const long long base = (long long)tile * kCellsPerTile + t * 16;
+    uint4* cnt4 = reinterpret_cast<uint4*>(d.cnt + base);
+    int4* min4 = reinterpret_cast<int4*>(d.cmin + base);
+    uint32_t cnt[16];
+    int mn[16];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        uint4 a = cnt4[k];
+        int4 b = min4[k];
+        cnt[4 * k] = a.x; cnt[4 * k + 1] = a.y; cnt[4 * k + 2] = a.z; cnt[4 * k + 3] = a.w;
+        mn[4 * k] = b.x; mn[4 * k + 1] = b.y; mn[4 * k + 2] = b.z; mn[4 * k + 3] = b.w;
+        cnt4[k] = make_uint4(0, 0, 0, 0);
+        min4[k] = make_int4(INT_MAX, INT_MAX, INT_MAX, INT_MAX);
+    }
+    uint32_t sum = 0;
+    int m1 = INT_MAX;
+#pragma unroll
+    for (int k = 0; k < 16; k++) { sum += cnt[k]; m1 = min(m1, mn[k]); }
+    d.lmin1[base >> 4] = m1;
+    // 16 consecutive threads = one 256-cell block
+    int m2 = m1;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) m2 = min(m2, __shfl_xor_sync(0xFFFFFFFFu, m2, o));
+    if ((lane & 15) == 0) d.lmin2[base >> 8] = m2;
+    // block exclusive scan of sum
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (t == 0) {
+        uint32_t acc = 0;
+        for (int k = 0; k < 8; k++) { uint32_t v = wsum[k]; wsum[k] = acc; acc += v; }
+        tile_excl = chain_scan(d.tiles_c, tile, tag, acc);
+        if (tile == gridDim.x - 1) {
+            d.ctab[d.ncells] = make_int2((int)(tile_excl + acc), INT_MAX);
+        }
+    }
+    __syncthreads();
+    uint32_t run = tile_excl + wsum[w] + incl - sum;
+    int4* out = reinterpret_cast<int4*>(d.ctab + base);
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        int4 v;
+        v.x = (int)run; v.y = mn[2 * k]; run += cnt[2 * k];
+        v.z = (int)run; v.w = mn[2 * k + 1]; run += cnt[2 * k + 1];
+        out[k] = v;
+    }
+    finish_block(&ctl->cells, gridDim.x);
+}
+
+// k_scatter: agents -> records sorted by cell (the order inside a cell is arbitrary;
+// no output depends on it).
+__global__ void __launch_bounds__(256) k_scatter(Dev d)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.n) return;
+    const uint32_t key = d.key[i];
+    if (key == kSentinel) return;
+    const uint32_t c = d.ctl->cur;
+    const int2 p = d.pos[c][i];
+    const uint32_t r = (uint32_t)d.ctab[key].x + d.rank[i];
+    d.rec[r] = make_int4(p.x | (p.y << 16), d.step[c][i], i, d.status[c][i]);
+}
+
+// test every record of cell `key` against agent A; returns true if A got blocked.
+template <bool kCouple>
+__device__ __forceinline__ bool scan_cell(const Dev& d, uint32_t key, int ax, int ay, int as,
+                                          uint32_t aid, bool blocked, uint32_t Rc,
+                                          unsigned long long& dig)
+{
+    const int beg = d.ctab[key].x, end = d.ctab[key + 1].x;
+    for (int b = beg; b < end; b++) {
+        const int4 B = d.rec[b];
+        const uint32_t bid = (uint32_t)B.z;
+        if (bid == aid) continue;
+        const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+        if (kCouple && B.y == as) {
+            if (within(dx, dy, Rc, d.metric)) {
+                if (aid < bid) uf_unite(d.parent, aid, bid);
+                if ((d.flags & AM_DIGEST) && within(dx, dy, (uint32_t)d.r_p, d.metric))
+                    dig += digest_term(bid, dx, dy);
+            }
+        } else if (!blocked && B.y < as) {
+            if (within(dx, dy, rb_radius((long long)as - B.y, d.v, d.r_p), d.metric)) {
+                blocked = true;
+                if (!kCouple) return true;
+            }
+        }
+    }
+    return blocked;
+}
+
+// k_scan: one thread per sorted record A.
+//   phase 1: cells within box distance R_c = r_p + v: coupling unions + blocking tests;
+//   phase 2: only if not yet blocked and A is ahead of the watermark: blocking tests
+//            over the disk of radius R_b(s_A - W), walking the min-step pyramid:
+//            a block with min step m is skipped if m >= s_A or its box distance
+//            exceeds R_b(s_A - m) (exact pruning: no agent inside can block A).
+__global__ void __launch_bounds__(256) k_scan(Dev d)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nact = d.ctl->n_active;
+    const int W = d.ctl->W;
+    bool blocked = false;
+    if (r < nact) {
+        const int4 A = d.rec[r];
+        const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+        const uint32_t aid = (uint32_t)A.z;
+        const int cl = d.clog, G = 1 << d.glog;
+        const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+        unsigned long long dig = 0;
+        // ---- phase 1
+        {
+            const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
+            const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
+            for (int cy = cy0; cy <= cy1; cy++)
+                for (int cx = cx0; cx <= cx1; cx++) {
+                    if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1,
+                                    ((cy + 1) << cl) - 1, Rc, d.metric))
+                        continue;
+                    const uint32_t key = morton(cx, cy);
+                    if (d.ctab[key].y > as) continue;
+                    blocked = scan_cell<true>(d, key, ax, ay, as, aid, blocked, Rc, dig);
+                }
+        }
+        if (d.flags & AM_DIGEST) d.digest[aid] = dig;
+        // ---- phase 2
+        if (!blocked && as > W) {
+            const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
+            const int l2 = cl + 4;  // 16 cells per side
+            const int G2 = G >> 4;
+            const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
+            const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
+            for (int by = by0; by <= by1 && !blocked; by++)
+                for (int bx = bx0; bx <= bx1 && !blocked; bx++) {
+                    const int m2 = d.lmin2[morton(bx, by)];
+                    if (m2 >= as) continue;
+                    if (!box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
+                                    rb_radius((long long)as - m2, d.v, d.r_p), d.metric))
+                        continue;
+                    for (int sy = 0; sy < 4 && !blocked; sy++)
+                        for (int sx = 0; sx < 4 && !blocked; sx++) {
+                            const int qx = bx * 4 + sx, qy = by * 4 + sy;  // 4x4-cell block
+                            const int l1 = cl + 2;
+                            const int m1 = d.lmin1[morton(qx, qy)];
+                            if (m1 >= as) continue;
+                            if (!box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
+                                            ((qy + 1) << l1) - 1, rb_radius((long long)as - m1, d.v, d.r_p),
+                                            d.metric))
+                                continue;
+                            for (int ty = 0; ty < 4 && !blocked; ty++)
+                                for (int tx = 0; tx < 4 && !blocked; tx++) {
+                                    const int cx = qx * 4 + tx, cy = qy * 4 + ty;
+                                    const int x0 = cx << cl, y0 = cy << cl;
+                                    const int x1 = ((cx + 1) << cl) - 1, y1 = ((cy + 1) << cl) - 1;
+                                    // phase-1 cells were tested completely already
+                                    if (box_within(ax, ay, x0, y0, x1, y1, Rc, d.metric)) continue;
+                                    const uint32_t key = morton(cx, cy);
+                                    const int m0 = d.ctab[key].y;
+                                    if (m0 >= as) continue;
+                                    if (!box_within(ax, ay, x0, y0, x1, y1,
+                                                    rb_radius((long long)as - m0, d.v, d.r_p), d.metric))
+                                        continue;
+                                    blocked = scan_cell<false>(d, key, ax, ay, as, aid, false, Rc, dig);
+                                }
+                        }
+                }
+        }
+    }
+    const unsigned bits = __ballot_sync(0xFFFFFFFFu, blocked);
+    if ((threadIdx.x & 31) == 0 && r < nact) d.blkbits[r >> 5] = bits;
+}
+
+// k_finalize: label = root of the agent's tree (= min id of its cluster, Q10);
+// a blocked or RUNNING member makes its cluster not ready (Q7).
+__global__ void __launch_bounds__(256) k_finalize(Dev d)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= d.ctl->n_active) return;
+    const int4 A = d.rec[r];
+    const uint32_t aid = (uint32_t)A.z;
+    const uint32_t root = uf_find(d.parent, aid);
+    d.labels[aid] = (int32_t)root;
+    const bool blk = (d.blkbits[r >> 5] >> (r & 31)) & 1u;
+    if (blk || A.w == ST_RUNNING) d.bad[root] = 1;
+}
+
+// k_ready: mask, DONE labels, dispatch (IDLE -> RUNNING), and the
+// ordered compaction of the ready set: keys ((step - W) << idbits) | label, values id.
+// 256 threads x 8 consecutive agents per tile; chained scan keeps id order.
+__global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask)
+{
+    Ctl* ctl = d.ctl;
+    __shared__ uint32_t wsum[8];
+    __shared__ uint32_t tile_excl;
+    __shared__ uint32_t ncl;
+    const uint32_t tile = take_ticket(&ctl->ready);
+    const uint32_t tag = ctl->epoch * 16u + 2u;
+    const uint32_t c = ctl->cur;
+    const int W = ctl->W;
+    const bool ok = ctl->err_sticky == 0;
+    const bool peek = (d.flags & AM_PEEK) != 0;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) ncl = 0;
+    const int i0 = tile * kReadyTile + t * 8;
+    uint8_t ready[8];
+    int lab[8];
+    uint32_t cnt = 0, mycl = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int i = i0 + k;
+        ready[k] = 0;
+        lab[k] = -1;
+        if (i < d.n) {
+            const uint8_t st = d.status[c][i];
+            if (st == ST_DONE) {
+                d.labels[i] = -1;
+            } else {
+                lab[k] = d.labels[i];
+                ready[k] = ok && st == ST_IDLE && !d.bad[lab[k]];
+                if (ready[k]) {
+                    if (!peek) d.status[c][i] = ST_RUNNING;
+                    cnt++;
+                    mycl += (lab[k] == i);
+                }
+            }
+            mask[i] = ready[k];
+        }
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (mycl) atomicAdd(&ncl, mycl);
+    if (t == 0) {
+        uint32_t acc = 0;
+        for (int k = 0; k < 8; k++) { uint32_t v = wsum[k]; wsum[k] = acc; acc += v; }
+        tile_excl = chain_scan(d.tiles_r, tile, tag, acc);
+        if (tile == gridDim.x - 1) ctl->n_ready = (int)(tile_excl + acc);
+    }
+    __syncthreads();
+    uint32_t pos = tile_excl + wsum[w] + incl - cnt;
+    unsigned long long kor = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        if (ready[k]) {
+            const int i = i0 + k;
+            const unsigned long long key =
+                ((unsigned long long)(uint32_t)(d.step[c][i] - W) << d.idbits) | (uint32_t)lab[k];
+            d.rkey[0][pos] = key;
+            d.rval[0][pos] = (uint32_t)i;
+            kor |= key;
+            pos++;
+        }
+    }
+    // OR of all keys -> number of radix passes
+    unsigned lo = __reduce_or_sync(0xFFFFFFFFu, (unsigned)kor);
+    unsigned hi = __reduce_or_sync(0xFFFFFFFFu, (unsigned)(kor >> 32));
+    if (lane == 0 && (lo | hi)) atomicOr(&ctl->sort_or, ((unsigned long long)hi << 32) | lo);
+    __syncthreads();
+    if (t == 0 && ncl) atomicAdd(&ctl->n_clusters, (int)ncl);
+    if (finish_block(&ctl->ready, gridDim.x) && t == 0) {
+        unsigned long long o = *(volatile unsigned long long*)&ctl->sort_or;
+        int bits = o ? 64 - __clzll((long long)o) : 0;
+        int np = (bits + 7) / 8;
+        ctl->npasses = np < 1 ? 1 : np;
+        ctl->sort_or = 0;
+    }
+}
+
+// k_sort_hist: global 8-bit digit histograms of the ready keys for every pass; the
+// last block turns them into exclusive digit offsets.
+__global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
+{
+    Ctl* ctl = d.ctl;
+    __shared__ uint32_t h[kMaxSortPasses][256];
+    const int n = ctl->n_ready;
+    const int np = min(ctl->npasses, max_passes);
+    for (int k = threadIdx.x; k < kMaxSortPasses * 256; k += blockDim.x) (&h[0][0])[k] = 0;
+    __syncthreads();
+    const int i0 = blockIdx.x * kSortTile;
+    if (i0 < n) {
+        for (int k = threadIdx.x; k < kSortTile && i0 + k < n; k += blockDim.x) {
+            const unsigned long long key = d.rkey[0][i0 + k];
+            for (int p = 0; p < np; p++) atomicAdd(&h[p][(key >> (8 * p)) & 255u], 1u);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < np * 256; k += blockDim.x) {
+            const uint32_t v = (&h[0][0])[k];
+            if (v) atomicAdd(d.ghist + k, v);
+        }
+    }
+    if (finish_block(&ctl->hist, gridDim.x)) {
+        // thread 0 only: exclusive scans (np x 256)
+        for (int p = 0; p < np; p++) {
+            uint32_t acc = 0;
+            for (int b = 0; b < 256; b++) {
+                const uint32_t v = *(volatile uint32_t*)(d.ghist + p * 256 + b);
+                d.gstart[p * 256 + b] = acc;
+                acc += v;
+                d.ghist[p * 256 + b] = 0;
+            }
+        }
+        __threadfence();
+    }
+}
+
+// k_sort_pass: one stable LSD pass over 8 bits (onesweep: per-digit decoupled
+// look-back across tiles).  Warp w of a tile owns items [256w, 256w+256) and ranks them
+// in index order with __match_any_sync, so the pass is stable.  The last pass writes
+// the ids straight into `order`.
+__global__ void __launch_bounds__(256) k_sort_pass(Dev d, int pass, int32_t* __restrict__ order)
+{
+    Ctl* ctl = d.ctl;
+    __shared__ uint32_t wcnt[8][256];
+    __shared__ uint32_t goff[256];
+    const int n = ctl->n_ready;
+    const int np = ctl->npasses;
+    const uint32_t tile = take_ticket(&ctl->pass[pass]);
+    if (pass >= np || (int)tile * kSortTile >= n) {
+        finish_block(&ctl->pass[pass], gridDim.x);
+        return;
+    }
+    const uint32_t tag = ctl->epoch * 16u + 4u + (uint32_t)pass;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const unsigned long long* kin = d.rkey[pass & 1];
+    const uint32_t* vin = d.rval[pass & 1];
+    unsigned long long* kout = d.rkey[(pass + 1) & 1];
+    uint32_t* vout = d.rval[(pass + 1) & 1];
+    const bool last = pass == np - 1;
+    for (int k = t; k < 8 * 256; k += 256) (&wcnt[0][0])[k] = 0;
+    __syncthreads();
+    const int shift = 8 * pass;
+    unsigned long long key[8];
+    uint32_t val[8], rnk[8];
+    int dig[8];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int i = tile * kSortTile + w * 256 + k * 32 + lane;
+        const bool valid = i < n;
+        key[k] = valid ? kin[i] : 0ull;
+        val[k] = valid ? vin[i] : 0u;
+        dig[k] = valid ? (int)((key[k] >> shift) & 255u) : 256;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, dig[k]);
+        const uint32_t base = valid ? wcnt[w][dig[k]] : 0u;
+        rnk[k] = base + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) wcnt[w][dig[k]] = base + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit (thread t = digit): exclusive prefix over warps, tile total, look-back
+    {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) { uint32_t v = wcnt[q][t]; wcnt[q][t] = acc; acc += v; }
+        unsigned long long* tw = d.tiles_sort + ((size_t)pass * gridDim.x) * 256;
+        uint32_t excl;
+        // column-major tile words: word of (tile, digit) at tw[digit * ntiles + tile]
+        unsigned long long* col = tw + (size_t)t * gridDim.x;
+        excl = chain_scan(col, tile, tag, acc);
+        goff[t] = d.gstart[pass * 256 + t] + excl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        if (dig[k] < 256) {
+            const uint32_t dst = goff[dig[k]] + wcnt[w][dig[k]] + rnk[k];
+            if (last) {
+                order[dst] = (int32_t)val[k];
+            } else {
+                kout[dst] = key[k];
+                vout[dst] = val[k];
+            }
+        }
+    }
+    finish_block(&ctl->pass[pass], gridDim.x);
+}
+
+// ============================================================== fused small path
+// One CTA per simulation (<= 1024 agents): the whole round in shared memory.
+// Simulations take tickets in index order; a chained scan over simulations places
+// each one's ready agents in `order` (sim-major: order = (sim, step, label, id)).
+__device__ __forceinline__ uint32_t suf_find(volatile uint32_t* parent, uint32_t x)
+{
+    uint32_t cur = parent[x];
+    if (cur != x) {
+        uint32_t prev = x, next;
+        while (cur > (next = parent[cur])) {
+            parent[prev] = next;
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+__device__ __forceinline__ void suf_unite(uint32_t* parent, uint32_t a, uint32_t b)
+{
+    volatile uint32_t* vp = parent;
+    uint32_t ra = suf_find(vp, a), rb = suf_find(vp, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            uint32_t old = atomicCAS(parent + rb, rb, ra);
+            if (old == rb) break;
+            rb = old;
+        } else {
+            uint32_t old = atomicCAS(parent + ra, ra, rb);
+            if (old == ra) break;
+            ra = old;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mask,
+                                                 int32_t* __restrict__ order)
+{
+    Ctl* ctl = d.ctl;
+    __shared__ int sx[kSmallMax], sy[kSmallMax], ss[kSmallMax];
+    __shared__ uint8_t sst[kSmallMax], sbad[kSmallMax], srdy[kSmallMax];
+    __shared__ uint32_t par[kSmallMax];
+    __shared__ int slab[kSmallMax];
+    __shared__ uint32_t s_excl, s_ncl;
+    const uint32_t b = take_ticket(&ctl->small_);
+    const uint32_t tag = ctl->epoch * 16u + 3u;
+    const int lo = (int)((long long)b * d.n / d.n_sims);
+    const int hi = (int)((long long)(b + 1) * d.n / d.n_sims);
+    const int m = hi - lo;
+    const int t = threadIdx.x;
+    const uint32_t c = ctl->cur;
+    const bool ok = ctl->err_sticky == 0;
+    const bool peek = (d.flags & AM_PEEK) != 0;
+    if (t == 0) s_ncl = 0;
+    if (t < m) {
+        const int2 p = d.pos[c][lo + t];
+        sx[t] = p.x;
+        sy[t] = p.y;
+        ss[t] = d.step[c][lo + t];
+        sst[t] = d.status[c][lo + t];
+        sbad[t] = 0;
+        par[t] = (uint32_t)t;
+    }
+    __syncthreads();
+    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    bool blocked = false;
+    unsigned long long dig = 0;
+    if (t < m && sst[t] != ST_DONE) {
+        const int ax = sx[t], ay = sy[t], as = ss[t];
+        for (int j = 0; j < m; j++) {
+            if (j == t || sst[j] == ST_DONE) continue;
+            const int dx = sx[j] - ax, dy = sy[j] - ay, bs = ss[j];
+            if (bs == as) {
+                if (within(dx, dy, Rc, d.metric)) {
+                    if (t < j) suf_unite(par, (uint32_t)t, (uint32_t)j);
+                    if ((d.flags & AM_DIGEST) && within(dx, dy, (uint32_t)d.r_p, d.metric))
+                        dig += digest_term((uint32_t)(lo + j), dx, dy);
+                }
+            } else if (!blocked && bs < as) {
+                blocked = within(dx, dy, rb_radius((long long)as - bs, d.v, d.r_p), d.metric);
+            }
+        }
+    }
+    __syncthreads();
+    int lab = -1;
+    if (t < m && sst[t] != ST_DONE) {
+        lab = (int)suf_find(par, (uint32_t)t);
+        if (blocked || sst[t] == ST_RUNNING) sbad[lab] = 1;
+    }
+    __syncthreads();
+    bool rdy = false;
+    if (t < m) {
+        rdy = ok && sst[t] == ST_IDLE && !sbad[lab];
+        srdy[t] = rdy;
+        slab[t] = lab;
+        mask[lo + t] = rdy;
+        d.labels[lo + t] = lab < 0 ? -1 : lo + lab;
+        if (d.flags & AM_DIGEST) d.digest[lo + t] = dig;
+        if (rdy && !peek) d.status[c][lo + t] = ST_RUNNING;
+        if (rdy && lab == t) atomicAdd(&s_ncl, 1u);
+    }
+    const int cnt = __syncthreads_count(rdy);
+    // rank by (step, label, id) among this simulation's ready agents
+    int rank = 0;
+    if (rdy) {
+        const int as = ss[t];
+        for (int j = 0; j < m; j++) {
+            if (!srdy[j] || j == t) continue;
+            const int bs = ss[j];
+            if (bs < as || (bs == as && (slab[j] < lab || (slab[j] == lab && j < t)))) rank++;
+        }
+    }
+    if (t == 0) {
+        s_excl = chain_scan(d.tiles_s, b, tag, (uint32_t)cnt);
+        if (s_ncl) atomicAdd(&ctl->n_clusters, (int)s_ncl);
+        if (b == (uint32_t)d.n_sims - 1) ctl->n_ready = (int)(s_excl + cnt);
+    }
+    __syncthreads();
+    if (rdy) order[s_excl + rank] = lo + t;
+    finish_block(&ctl->small_, gridDim.x);
+}
+
+// reset the per-round counters that the host reads (before the round kernels)
+__global__ void k_round_begin(Ctl* ctl)
+{
+    ctl->epoch += 1;
+    ctl->n_ready = 0;
+    ctl->n_clusters = 0;
+}
+
+}  // namespace am

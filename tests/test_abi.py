@@ -1,0 +1,75 @@
+"""CPU-side checks of the boundary: libametro.so builds for sm_100a, loads, and exports
+every symbol include/*.h declares (no compute calls without a GPU)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2411_03519_b200 as pkg
+from paper_2411_03519_b200 import _build, _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    names = set()
+    for h in ("am.h", "am_driver.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^\s*(?:const\s+)?[\w\s\*]+?\b(am_\w+)\s*\(", src, flags=re.M):
+            names.add(m.group(1))
+    return names
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return _lib.load()
+
+
+def test_header_declares_the_north_star_calls():
+    names = _declared()
+    for n in ("am_init", "am_update", "am_ready", "am_clusters"):
+        assert n in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = _declared()
+    assert len(names) >= 20
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    # and the binding declares a signature for each of them
+    assert names <= set(_lib.SIGNATURES), names - set(_lib.SIGNATURES)
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _build.LIB],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_init_errors_without_gpu(lib):
+    assert lib.am_version().decode().startswith("ametro-b200")
+    h = C.c_void_p()
+    # argument errors are caught before any CUDA call
+    assert lib.am_init(C.byref(h), 0, 10, 4, 1, 10, None) == _lib.E_ARG
+    assert b"map dims" in lib.am_last_error(None)
+    assert lib.am_init(C.byref(h), 10, 10, -1, 1, 10, None) == _lib.E_ARG
+    cfg = _lib.Config(0, 3, 0, 0, 0, None)
+    assert lib.am_init(C.byref(h), 10, 10, 4, 1, 2, C.byref(cfg)) == _lib.E_ARG   # n_sims > n
+    cfg = _lib.Config(0, 1, 6, 0, 0, None)
+    assert lib.am_init(C.byref(h), 10, 10, 4, 1, 2, C.byref(cfg)) == _lib.E_ARG   # cell not pow2
+    assert lib.am_update(None, None, None) == _lib.E_ARG
+    assert lib.am_destroy(None) == _lib.OK
+
+
+def test_package_does_not_import_the_oracle():
+    src = ""
+    pdir = os.path.dirname(pkg.__file__)
+    for root, _, files in os.walk(pdir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src += open(os.path.join(root, f)).read()
+    assert "import oracle" not in src and "from oracle" not in src and "oracle.c" not in src

@@ -1,0 +1,111 @@
+"""GPU replay driver vs the oracle's OoO replay and lock-step simulator: per-round
+logs (order and labels of every dispatched agent), final positions, per-agent
+trajectory hashes, T_ooo and round counts -- all bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import amgen
+import oracle as O
+from paper_2411_03519_b200 import Replay
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle(w, lm, log=True, check=False):
+    sy = O.SynthTables.from_model(lm, wall=w.wall)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, n_sims=w.n_sims)
+    cap_r = 10**6 if log else 0
+    cap_e = len(w.x) * w.steps + 10 if log else 0
+    return O.replay(p, sy, w.x, w.y, Q=w.Q, log_rounds=cap_r, log_entries=cap_e, check=check), \
+        O.lockstep(p, sy, w.x, w.y, w.steps)
+
+
+def _gpu_logged(rep, n_sims, n):
+    """Step round by round; split the round's order per simulation (sim-major)."""
+    logs = [[] for _ in range(n_sims)]
+    for _ in range(10**7):
+        mask, order, labels = rep.step()
+        o = order.cpu().numpy()
+        lab = labels.cpu().numpy()
+        sims = (o.astype(np.int64) * n_sims + n_sims - 1) // n if n_sims > 1 else np.zeros(len(o), int)
+        for b in np.unique(sims):
+            sel = o[sims == b]
+            logs[b].append((sel.copy(), lab[sel].copy()))
+        if rep.tracker.stats()["n_active"] == 0 and len(o) == 0:
+            break
+    return logs
+
+
+def _split_oracle_log(r, n_sims):
+    logs = [[] for _ in range(n_sims)]
+    k = 0
+    for t, b, nr in zip(r["log_t"], r["log_sim"], r["log_nready"]):
+        if nr:
+            logs[b].append((r["log_id"][k:k + nr], r["log_label"][k:k + nr]))
+        k += nr
+    return logs
+
+
+@pytest.mark.parametrize("name,steps,n_sims,path", [
+    ("C1", 1000, 1, None),
+    ("C1", 300, 1, "binned"),
+    ("C3", 200, 16, None),
+])
+def test_replay_round_logs(name, steps, n_sims, path):
+    w = amgen.config(name, steps=steps, n=n_sims if name == "C3" else None)
+    lm = amgen.latency_model(w.profile)
+    r, ls = _oracle(w, lm)
+    assert r["log_complete"]
+    rep = Replay.from_workload(w, lm, force=path)
+    glogs = _gpu_logged(rep, w.n_sims, len(w.x))
+    ologs = _split_oracle_log(r, w.n_sims)
+    for b in range(w.n_sims):
+        assert len(glogs[b]) == len(ologs[b]), (b, len(glogs[b]), len(ologs[b]))
+        for (gi, gl), (oi, ol) in zip(glogs[b], ologs[b]):
+            np.testing.assert_array_equal(gi, oi)
+            np.testing.assert_array_equal(gl, ol)
+    res = rep.results()
+    np.testing.assert_array_equal(res["T_ooo"], r["T_ooo"])
+    np.testing.assert_array_equal(res["rounds"], r["rounds"])
+    np.testing.assert_array_equal(res["x"], r["x"])
+    np.testing.assert_array_equal(res["y"], r["y"])
+    np.testing.assert_array_equal(res["traj"], r["traj"])
+    # outcome preservation: the OoO replay ends where lock-step ends
+    np.testing.assert_array_equal(res["traj"], ls["traj"])
+    assert rep.dispatched() == len(w.x) * w.steps
+    rep.close()
+
+
+@pytest.mark.parametrize("name,steps,n,path", [
+    ("C1", 1000, None, None),
+    ("C2", 40, None, None),
+    ("C2", 40, None, "binned"),
+    ("C3", 300, 512, None),
+    ("C4", 20, 2000, "binned"),
+])
+def test_replay_final_state(name, steps, n, path):
+    w = amgen.config(name, steps=steps, n=n)
+    lm = amgen.latency_model(w.profile)
+    r, ls = _oracle(w, lm, log=False)
+    rep = Replay.from_workload(w, lm, force=path)
+    rep.run_to_end(chunk=512)
+    res = rep.results()
+    np.testing.assert_array_equal(res["T_ooo"], r["T_ooo"])
+    np.testing.assert_array_equal(res["rounds"], r["rounds"])
+    np.testing.assert_array_equal(res["traj"], r["traj"])
+    np.testing.assert_array_equal(res["traj"], ls["traj"])
+    assert np.all(res["steps"] == w.steps)
+    assert np.all(res["T_ooo"] <= ls["T_sync"]) if w.Q == 0 else True
+    rep.close()
+
+
+@pytest.mark.parametrize("x1,T,L0,L1,T_ooo", [
+    (7, 2, [10, 1], [1, 10], 11), (6, 2, [10, 1], [1, 10], 20),
+    (5, 2, [10, 1], [1, 10], 20), (7, 3, [1, 1, 1], [10, 10, 10], 30)])
+def test_replay_closed_forms(x1, T, L0, L1, T_ooo):
+    """D1/D2/D3/D5 on the GPU driver: stay policy, explicit durations."""
+    rep = Replay(64, 8, 4, 1, [0, x1], [0, 0], T, dur_table=[L0, L1], policy=1)
+    rep.run_to_end(chunk=8)
+    assert int(rep.results()["T_ooo"][0]) == T_ooo
+    rep.close()
