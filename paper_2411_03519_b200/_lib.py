@@ -67,6 +67,9 @@ SIGNATURES = {
     "am_destroy": (C.c_int, [_vp]),
     "am_last_error": (C.c_char_p, [_vp]),
     "am_version": (C.c_char_p, []),
+    "am_profile_enable": (C.c_int, [_vp, _i32]),
+    "am_profile_read": (C.c_int, [_vp, _vp, _vp, _i32]),
+    "am_profile_name": (C.c_char_p, [_i32]),
     "am_replay_create": (C.c_int, [C.POINTER(_vp), _vp, C.POINTER(Synth), _i64, _vp, _vp]),
     "am_replay_run": (C.c_int, [_vp, _i64, C.POINTER(_i64)]),
     "am_replay_step": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(_i32)]),

@@ -1,7 +1,7 @@
 // am_driver.cu -- GPU-resident trace-replay driver (include/am_driver.h).
 //
 // One replay round for every simulation at once (Alg. 3 with infinite LLM capacity,
-// replay mode P:228): k_commit -> am_update -> am_ready -> k_disp_a -> k_disp_b.
+// replay mode P:228): am_update -> am_ready -> k_disp_a -> k_disp_b -> k_commit.
 // The synthetic policy/latency model is the same definition the oracle implements
 // independently (am_driver.h); nothing here is shared with oracle/.
 #include <climits>
@@ -63,14 +63,16 @@ __device__ __forceinline__ long long duration(const am_synth& sy, int i, int s)
     return dsum;
 }
 
-// commit every RUNNING agent whose cluster completed (tcommit <= t_sim): the move
-// computed at dispatch is applied and the step advances (worker l.20-21).
+// commit every RUNNING agent whose cluster completed (tcommit <= t_sim, the clock
+// k_disp_b just advanced): the move computed at dispatch is applied and the step
+// advances (worker l.20-21).  Agents that stay RUNNING bound the next
+// event; any agent left active marks its simulation active for the next round.
 __global__ void __launch_bounds__(256) k_commit(RepDev r)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const Dev& d = r.d;
     if (i >= d.n) return;
-    const uint8_t st = d.status[d.ctl->cur][i];
+    const uint8_t st = d.status[d.ctl->cur][i];   // after this round's dispatch
     if (st == ST_DONE) return;
     const int b = sim_of(d, i);
     const long long t = r.t_sim[b];
@@ -183,19 +185,29 @@ static int rp_err(am_replay* rp, cudaError_t e, const char* where)
         if (e_ != cudaSuccess) return rp_err(rp, e_, #call); \
     } while (0)
 
+// One round: update (ingest the world state) -> ready -> dispatch -> next event ->
+// commit at the next event time.  Committing at the end of the round (instead of the
+// start of the next) leaves the state a host-side user would hold between rounds in
+// the world arrays; the sequence of rounds is unchanged.
 static int enqueue_round(am_replay* rp)
 {
     am_ctx* c = rp->ctx;
     const int n = c->d.n;
     const unsigned nb = (unsigned)((n + 255) / 256);
-    k_commit<<<nb, 256, 0, rp->stream>>>(rp->r);
     int rc = am_update(c, (const int32_t*)rp->r.pos, rp->r.steps);
     if (rc) return rc;
     rc = am_ready(c, rp->mask, rp->order, nullptr);
     if (rc) return rc;
     rp->r.d = c->d;
+    am_prof_begin(c, K_DISP_A);
     k_disp_a<<<nb, 256, 0, rp->stream>>>(rp->r);
+    am_prof_end(c, K_DISP_A);
+    am_prof_begin(c, K_DISP_B);
     k_disp_b<<<nb, 256, 0, rp->stream>>>(rp->r);
+    am_prof_end(c, K_DISP_B);
+    am_prof_begin(c, K_COMMIT);
+    k_commit<<<nb, 256, 0, rp->stream>>>(rp->r);
+    am_prof_end(c, K_COMMIT);
     RK(cudaGetLastError());
     return AM_OK;
 }
@@ -259,6 +271,9 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
         long long* h = (long long*)malloc(8 * S);
         for (long long k = 0; k < S; k++) h[k] = LLONG_MAX;
         RK(cudaMemcpy(r.tnext, h, 8 * S, cudaMemcpyHostToDevice));
+        int32_t* a = (int32_t*)h;
+        for (long long k = 0; k < S; k++) a[k] = 1;
+        RK(cudaMemcpy(r.active_flag, a, 4 * S, cudaMemcpyHostToDevice));
         free(h);
     }
     am_set_stream(ctx, rp->stream);

@@ -67,6 +67,65 @@ static int ilog2_ceil(long long x)
 
 static inline unsigned blocks(long long n, int t) { return (unsigned)std::max(1LL, (n + t - 1) / t); }
 
+static const char* kKernelNames[K_COUNT] = {
+    "k_ingest", "k_bin", "k_cells", "k_scatter", "k_scan", "k_finalize", "k_ready", "k_sort_hist",
+    "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b"};
+
+void am_prof_begin(am_ctx* c, int id)
+{
+    if (c->prof.on) cudaEventRecordWithFlags(c->prof.ev[id][0], c->stream, cudaEventRecordExternal);
+}
+void am_prof_end(am_ctx* c, int id)
+{
+    if (c->prof.on) {
+        cudaEventRecordWithFlags(c->prof.ev[id][1], c->stream, cudaEventRecordExternal);
+        c->prof.pending |= 1u << id;
+    }
+}
+// after a synchronisation: accumulate the recorded kernel times
+void am_prof_collect(am_ctx* c)
+{
+    if (!c->prof.on) return;
+    for (int k = 0; k < K_COUNT; k++) {
+        if (!(c->prof.pending & (1u << k))) continue;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c->prof.ev[k][0], c->prof.ev[k][1]) == cudaSuccess) {
+            c->prof.ms[k] += ms;
+            c->prof.cnt[k] += 1;
+        }
+    }
+    c->prof.pending = 0;
+    cudaGetLastError();
+}
+
+extern "C" int am_profile_enable(am_ctx* c, int32_t on)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (on && !c->prof.ev[0][0]) {
+        for (int k = 0; k < K_COUNT; k++)
+            for (int j = 0; j < 2; j++) CK(c, cudaEventCreate(&c->prof.ev[k][j]));
+    }
+    c->prof.on = on != 0;
+    c->prof.pending = 0;
+    for (int k = 0; k < K_COUNT; k++) { c->prof.ms[k] = 0; c->prof.cnt[k] = 0; }
+    return AM_OK;
+}
+
+extern "C" int am_profile_read(am_ctx* c, double* ms, int64_t* counts, int32_t max)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    for (int k = 0; k < K_COUNT && k < max; k++) {
+        if (ms) ms[k] = c->prof.ms[k];
+        if (counts) counts[k] = c->prof.cnt[k];
+    }
+    return K_COUNT;
+}
+
+extern "C" const char* am_profile_name(int32_t id)
+{
+    return (id >= 0 && id < K_COUNT) ? kKernelNames[id] : "";
+}
+
 extern "C" const char* am_version(void) { return "ametro-b200 0.1 (sm_100a)"; }
 
 extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max,
@@ -234,7 +293,9 @@ static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, co
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
     if (c->d.n == 0) return AM_OK;
     if (!pos || !steps || (mode == 2 && !st)) return set_err(c, AM_E_ARG, "NULL array");
+    am_prof_begin(c, K_INGEST);
     k_ingest<<<blocks(c->d.n, 256), 256, 0, c->stream>>>(c->d, (const int2*)pos, steps, st, mode);
+    am_prof_end(c, K_INGEST);
     CK(c, cudaGetLastError());
     return AM_OK;
 }
@@ -280,6 +341,7 @@ extern "C" int am_sync(am_ctx* c)
     CK(c, cudaMemcpyAsync(c->h_ctl, c->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
     fill_stats(c);
+    am_prof_collect(c);
     const int bits = c->h_ctl->err_sticky;
     if (bits) {
         CK(c, cudaMemsetAsync(&c->d.ctl->err_sticky, 0, sizeof(int32_t), c->stream));
@@ -305,21 +367,30 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
     if (!mask || !order) return set_err(c, AM_E_ARG, "NULL mask/order");
     const Dev& d = c->d;
     cudaStream_t s = c->stream;
+#define LAUNCH(id, ...)        \
+    do {                       \
+        am_prof_begin(c, id);  \
+        __VA_ARGS__;           \
+        am_prof_end(c, id);    \
+    } while (0)
     k_round_begin<<<1, 1, 0, s>>>(d.ctl);
     if (c->path == 0) {
-        k_small<<<d.n_sims, c->small_threads, 0, s>>>(d, mask, order);
+        LAUNCH(K_SMALL, (k_small<<<d.n_sims, c->small_threads, 0, s>>>(d, mask, order)));
     } else {
         const unsigned nb = blocks(d.n, 256);
-        k_bin<<<nb, 256, 0, s>>>(d);
-        k_cells<<<c->ntiles_cells, 256, 0, s>>>(d);
-        k_scatter<<<nb, 256, 0, s>>>(d);
-        k_scan<<<nb, 256, 0, s>>>(d);
-        k_finalize<<<nb, 256, 0, s>>>(d);
-        k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask);
-        k_sort_hist<<<c->ntiles_sort, 256, 0, s>>>(d, c->sort_passes_max);
+        LAUNCH(K_BIN, (k_bin<<<nb, 256, 0, s>>>(d)));
+        LAUNCH(K_CELLS, (k_cells<<<c->ntiles_cells, 256, 0, s>>>(d)));
+        LAUNCH(K_SCATTER, (k_scatter<<<nb, 256, 0, s>>>(d)));
+        LAUNCH(K_SCAN, (k_scan<<<nb, 256, 0, s>>>(d)));
+        LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));
+        LAUNCH(K_READY, (k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask)));
+        LAUNCH(K_SORT_HIST, (k_sort_hist<<<c->ntiles_sort, 256, 0, s>>>(d, c->sort_passes_max)));
+        am_prof_begin(c, K_SORT_PASS);
         for (int p = 0; p < c->sort_passes_max; p++)
             k_sort_pass<<<c->ntiles_sort, 256, 0, s>>>(d, p, order);
+        am_prof_end(c, K_SORT_PASS);
     }
+#undef LAUNCH
     CK(c, cudaGetLastError());
     c->have_round = true;
     if (async) return AM_OK;
@@ -385,6 +456,9 @@ extern "C" int am_destroy(am_ctx* c)
 {
     if (!c) return AM_OK;
     cudaStreamSynchronize(c->stream);
+    if (c->prof.ev[0][0])
+        for (int k = 0; k < K_COUNT; k++)
+            for (int j = 0; j < 2; j++) cudaEventDestroy(c->prof.ev[k][j]);
     cudaFree(c->ws);
     cudaFreeHost(c->h_ctl);
     delete c;

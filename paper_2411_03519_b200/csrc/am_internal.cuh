@@ -87,7 +87,29 @@ struct Dev {
 
 }  // namespace am
 
+// per-kernel device timing (am_profile_*): external event records around every
+// launch, so they also work inside captured CUDA graphs
+namespace am {
+enum KernelId : int {
+    K_INGEST = 0, K_BIN, K_CELLS, K_SCATTER, K_SCAN, K_FINALIZE, K_READY, K_SORT_HIST, K_SORT_PASS,
+    K_SMALL, K_COMMIT, K_DISP_A, K_DISP_B, K_COUNT
+};
+struct Prof {
+    bool on = false;
+    cudaEvent_t ev[K_COUNT][2] = {};
+    unsigned pending = 0;
+    double ms[K_COUNT] = {};
+    long long cnt[K_COUNT] = {};
+};
+}  // namespace am
+
+struct am_ctx;
+void am_prof_begin(am_ctx* c, int id);
+void am_prof_end(am_ctx* c, int id);
+void am_prof_collect(am_ctx* c);
+
 struct am_ctx {
+    am::Prof prof;
     am::Dev d;
     am::Ctl* h_ctl = nullptr;        // pinned host mirror
     cudaStream_t stream = nullptr;

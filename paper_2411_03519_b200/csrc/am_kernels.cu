@@ -441,15 +441,24 @@ __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
         }
     }
     if (finish_block(&ctl->hist, gridDim.x)) {
-        // thread 0 only: exclusive scans (np x 256)
+        // last block: thread t owns digit t; exclusive scan over the 256 digits per pass
+        __shared__ uint32_t wtot[8];
+        const int t = threadIdx.x, lane = t & 31, w = t >> 5;
         for (int p = 0; p < np; p++) {
-            uint32_t acc = 0;
-            for (int b = 0; b < 256; b++) {
-                const uint32_t v = *(volatile uint32_t*)(d.ghist + p * 256 + b);
-                d.gstart[p * 256 + b] = acc;
-                acc += v;
-                d.ghist[p * 256 + b] = 0;
+            const uint32_t v = __ldcg(d.ghist + p * 256 + t);
+            uint32_t incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += y;
             }
+            if (lane == 31) wtot[w] = incl;
+            __syncthreads();
+            uint32_t base = 0;
+            for (int q = 0; q < w; q++) base += wtot[q];
+            d.gstart[p * 256 + t] = base + incl - v;
+            d.ghist[p * 256 + t] = 0;
+            __syncthreads();
         }
         __threadfence();
     }
