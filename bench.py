@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py -- AI Metropolis dependency tracker on B200.
+
+A STEP is one scheduling round of the GPU-resident trace replay of BASELINE config 5
+(1M agents on a 16384x16384 map, hotspots, busy-hour latency profile, 50 ms quantum):
+am_update (ingest + commit validation, S1) -> am_ready (binning S2, cell table S3,
+time-dilated scan S4, cluster labelling S5, ready set + priority order S6) ->
+dispatch + commit (driver, S8).  The replay is pre-rolled to steady state (untimed),
+then W warm-up and K timed rounds; L2 is flushed (512 MB write) between timed rounds.
+
+metric: agent-steps resolved per second (= agents dispatched by the tracker per second
+of device time); rounds/s is reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 (torchrun): every rank runs its own replica of the workload (no data-path
+collective; "replicas" -- the spatial-slab exchange is not in this round).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "agent-steps resolved/sec and scheduling rounds/sec; % of HBM roofline"
+UNIT = "agent-steps/s"
+
+# Algorithmic bytes per launch of each kernel: the bytes the
+# kernel's definition must move at minimum, each input/output counted once.
+# n = agents, a = active (not DONE) agents, c = Morton cells, r = ready agents,
+# q = RUNNING agents, p = radix passes.
+def algorithmic_bytes(kernel: str, s: dict) -> float:
+    n, a, c, r, p = s["n"], s["n_active"], s["ncells"], s["n_ready"], s["passes"]
+    table = {
+        # read pos 8 + step 4 (new) + old step 4 + status 1 + old pos 8; write pos 8 + step 4 + status 1
+        "k_ingest": 38.0 * n,
+        # read status 1 + pos 8 + step 4; write key 4 + rank 4 + parent 4 + bad 1; cell count+min 8
+        "k_bin": 34.0 * n,
+        # read count 4 + min 4; write start/min 8 + reset 8 + pyramid 0.27
+        "k_cells": 24.27 * c,
+        # read key 4 + rank 4 + cell start 4 + pos 8 + step 4 + status 1; write record 16
+        "k_scatter": 41.0 * a,
+        # read own record 16 + own cell entry 8; write blocked bit 0.125 + digest 8
+        "k_scan": 32.125 * a,
+        # read record 16 + blocked bit 0.125 + parent 4; write label 4
+        "k_finalize": 24.125 * a,
+        # read status 1 + label 4 + bad 1; write mask 1 + status 1; ready: step 4 + key/id 12
+        "k_ready": 8.0 * n + 16.0 * r,
+        "k_sort_hist": 8.0 * r,
+        # per pass read+write key 8 + id 4; last pass writes 4-byte order
+        "k_sort_pass": 24.0 * r * p,
+        # ready: order 4 + step 4 + label 4 + latency tables ~0 + cluster time 8
+        "k_disp_a": 20.0 * r,
+        # ready: order 4 + label 4 + cluster time 8 + step 4 + pos 8 + digest 8; write tcommit 8 + newpos 8
+        "k_disp_b": 52.0 * r,
+        # read status 1 (+ tcommit 8 for RUNNING); commit: pos/step/traj r+w
+        "k_commit": 1.0 * n + 8.0 * s["n_running"],
+    }
+    return table.get(kernel, 0.0)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", pk
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu = gpu_id
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 5 + k and s[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ CPU oracle baseline
+def oracle_sample(w, seconds: float, seed: int = 0):
+    """The oracle as it stands (single-threaded C, brute force) on a bounded sample of
+    the workload: sampled agents of the workload's initial round state, each resolved
+    one by one (blocked test O(N), component walk O(N*|C|)).  Returns
+    (ready agent-steps resolved per second, agents sampled, seconds)."""
+    import numpy as np
+
+    import oracle as O
+    n = len(w.x)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, w.steps)
+    steps = np.zeros(n, np.int32)
+    status = np.zeros(n, np.uint8)
+    rng = np.random.default_rng(seed)
+    ready = sampled = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        smp = rng.integers(0, n, 4).astype(np.int32)
+        r = O.round_sampled(p, w.x, w.y, steps, status, smp)
+        ready += int(r["mask"].sum())
+        sampled += len(smp)
+    dt = time.perf_counter() - t0
+    return ready / dt, sampled, dt
+
+
+def run_reference(args, w):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle as O
+    O.build()
+    times, resolved, sampled = [], 0, 0
+    for k in range(args.warmup + args.steps):
+        v, sm, dt = oracle_sample(w, args.ref_step_seconds, seed=k)
+        if k >= args.warmup:
+            times.append(dt)
+            resolved += v * dt
+            sampled += sm
+    total = sum(times)
+    value = resolved / total if total else 0.0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": _config(w, ws),
+        "cpu_baseline": {"kind": "oracle", "value": value, "unit": UNIT, "cores": 1,
+                         "sample": f"{sampled} sampled agents of the {w.name} initial round "
+                                   f"({len(w.x)} agents), resolved one by one by oracle.c"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config(w, ws):
+    return {"workload": f"{w.name}: {len(w.x)} agents, {w.map_w}x{w.map_h} open map, hotspots, "
+                        f"busy-hour latencies, Q={w.Q // 1000} ms, T={w.steps}",
+            "agents": len(w.x), "map": [w.map_w, w.map_h], "r_p": w.r_p, "v_max": w.v,
+            "quantum_us": w.Q, "parallelism": "replicas" if ws > 1 else "single",
+            "l2": "flushed between timed rounds (512 MB write)"}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, w, lm):
+    import numpy as np
+    import torch
+
+    from paper_2411_03519_b200 import Replay
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    rep = Replay.from_workload(w, lm, device=dev)
+    stream = torch.cuda.ExternalStream(rep.stream_ptr(), device=dev)
+    names = ["k_ingest", "k_bin", "k_cells", "k_scatter", "k_scan", "k_finalize", "k_ready",
+             "k_sort_hist", "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b"]
+    ncells = None
+
+    # pre-roll to steady state (untimed)
+    rep.run(args.preroll)
+    # warm-up with every kernel timed -> per-kernel shares, the dominant kernel
+    rep.profile((1 << len(names)) - 1)
+    for _ in range(args.warmup):
+        rep.launch(1)
+        rep.sync()
+    prof_w = rep.profile_read()
+    dom = max((k for k in prof_w if prof_w[k][1] > 0), key=lambda k: prof_w[k][0])
+    shares = {k: v[0] / v[1] for k, v in prof_w.items() if v[1] > 0}
+    # timed region: only the dominant kernel bracketed by events
+    rep.profile(1 << names.index(dom))
+    rep.launch(1)
+    rep.sync()
+    rep.profile(1 << names.index(dom))
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    st_active, st_ready, st_running = [], [], []
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    d0 = rep.dispatched()
+    try:
+        gid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        gid = str(local)
+    with ClockSampler(gid) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xFF)
+                ev[k][0].record(stream)
+            rep.launch(1)
+            ev[k][1].record(stream)
+            act, nr = rep.sync()
+            s = rep.tracker.stats()
+            st_active.append(s["n_active"])
+            st_ready.append(nr)
+            st_running.append(s["n_running"])
+    torch.cuda.synchronize(dev)
+    if pg:
+        pg.barrier()
+    d1 = rep.dispatched()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    prof_t = rep.profile_read()
+    dom_ms, dom_cnt = prof_t[dom]
+    agent_steps = d1 - d0
+    # max over ranks of the timed device time; sum of work
+    if pg:
+        t = torch.tensor([total_ms, float(agent_steps)], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        pg.all_reduce(tmax[:1], op=pg.ReduceOp.MAX)
+        pg.all_reduce(t[1:], op=pg.ReduceOp.SUM)
+        total_ms, agent_steps = float(tmax[0]), int(t[1])
+    value = agent_steps / (total_ms / 1000.0) if total_ms > 0 else 0.0
+    rounds_per_s = args.steps / (total_ms / 1000.0) if total_ms > 0 else 0.0
+
+    # ---- end to end: world state in pinned host memory, copies inside the timed region
+    n = rep.n
+    h_pos = torch.empty((n, 2), dtype=torch.int32, pin_memory=True)
+    h_steps = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_mask = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h_order = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    rep.profile(0)
+    torch.cuda.synchronize(dev)
+    h_pos.copy_(rep.pos)
+    h_steps.copy_(rep.steps)
+    e_ms = []
+    e0 = rep.dispatched()
+    for k in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+            a.record(stream)
+        rep.io(h_pos, h_steps, h_mask, h_order)
+        b.record(stream)
+        rep.sync()
+        e_ms.append(a.elapsed_time(b))
+    e_steps = rep.dispatched() - e0
+    e_total = sum(e_ms)
+    e_value = e_steps / (e_total / 1000.0) if e_total > 0 else 0.0
+    if pg:
+        t = torch.tensor([e_total, float(e_steps)], dtype=torch.float64, device=dev)
+        tm = t.clone()
+        pg.all_reduce(tm[:1], op=pg.ReduceOp.MAX)
+        pg.all_reduce(t[1:], op=pg.ReduceOp.SUM)
+        e_value = float(t[1]) / (float(tm[0]) / 1000.0)
+
+    if rank != 0:
+        rep.close()
+        if pg:
+            pg.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel
+    L = rep.tracker.L
+    stats = {"n": n, "n_active": statistics.mean(st_active), "n_ready": statistics.mean(st_ready),
+             "n_running": statistics.mean(st_running), "passes": rep.tracker.L.am_launches_per_round(rep.tracker.ctx) - 9,
+             "ncells": 0}
+    # cell count of the binned path: (workspace layout) -- from the config the library chose
+    cell = rep.tracker.stats()["cell"]
+    g = 64
+    while g * cell < max(w.map_w, w.map_h):
+        g *= 2
+    stats["ncells"] = g * g
+    peak, peak_src, pk = _peaks()
+    avg_dom_s = dom_ms / max(1, dom_cnt) / 1000.0
+    alg = algorithmic_bytes(dom, stats)
+    achieved = alg / avg_dom_s / 1e9 if avg_dom_s > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(dom)
+            traffic = tr.get("dram_bytes_per_launch") if tr else None
+    except Exception:
+        pass
+    clocks = clk.summary()
+    # the oracle on the host cores, bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        v, sm, dt = oracle_sample(w, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{sm} sampled agents of the {w.name} initial round ({n} agents) resolved "
+                         f"one by one by oracle.c in {dt:.1f} s (single thread)",
+               "host_cores_available": os.cpu_count()}
+    launches = rep.launches_per_round() * args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": _config(w, ws),
+        "rounds_per_s": rounds_per_s,
+        "agent_steps_per_round": agent_steps / args.steps / ws,
+        "round_stats": {"active": stats["n_active"], "ready": stats["n_ready"],
+                        "running": stats["n_running"]},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg, "avg_launch_us": avg_dom_s * 1e6},
+        "kernel_share_warmup_us": {k: round(v * 1000.0, 2) for k, v in sorted(shares.items())},
+        "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": 12 * n,
+                "d2h_bytes_per_step": 12 * n + n + 4 * n, "ms_per_step": e_total / args.steps},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    rep.close()
+    if pg:
+        pg.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C5")
+    ap.add_argument("--agents", type=int, default=None, help="shrink the workload (same density)")
+    ap.add_argument("--preroll", type=int, default=400)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=2.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    import amgen
+    w = amgen.config(args.workload, n=args.agents)
+    lm = amgen.latency_model(w.profile)
+    if args.impl == "reference":
+        return run_reference(args, w)
+    return run_ours(args, w, lm)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -161,15 +161,19 @@ int am_destroy(am_ctx* ctx);
 /* Message of the last failing call on ctx ("" if none); ctx may be NULL (init errors). */
 const char* am_last_error(const am_ctx* ctx);
 
-/* Per-kernel device timing (tracing).  When enabled, every kernel launch of the
+/* Per-kernel device timing (tracing).  mask selects kernel ids (bit k = kernel k,
+ * names from am_profile_name; 0 disables).  Every selected kernel launch of the
  * context (tracker and replay driver) is bracketed by CUDA events recorded on the
  * context's stream (external event records, so they work inside CUDA graphs); each
  * synchronising call adds the elapsed times to per-kernel totals.  Enabling resets
  * the totals.  am_profile_read fills ms[k] / counts[k] for k < max (host arrays) and
  * returns the number of kernel ids; am_profile_name gives kernel k's name. */
-int am_profile_enable(am_ctx* ctx, int32_t on);
+int am_profile_enable(am_ctx* ctx, uint32_t mask);
 int am_profile_read(am_ctx* ctx, double* ms, int64_t* counts, int32_t max);
 const char* am_profile_name(int32_t id);
+
+/* Kernel launches of one am_update + am_ready on this context (host-side count). */
+int32_t am_launches_per_round(const am_ctx* ctx);
 
 /* Library version string. */
 const char* am_version(void);

@@ -84,6 +84,27 @@ int am_replay_results(am_replay* r, int64_t* T_ooo, int64_t* rounds, uint64_t* t
 /* Total agent-steps dispatched so far (host). */
 int am_replay_dispatched(am_replay* r, int64_t* agent_steps);
 
+/* One round with the world state in HOST memory (pinned for asynchronous copies):
+ * copies h_pos_in int32[n][2] / h_steps_in int32[n] to the replay's world arrays, runs
+ * the round, copies back the committed state (h_pos_out, h_steps_out; may alias the
+ * inputs), the ready mask uint8[n] and the order int32[n].  Output pointers may be
+ * NULL.  If n_ready is non-NULL the call synchronises and stores the round's ready
+ * count (first *n_ready order entries valid); otherwise call am_replay_sync.  This
+ * is the end-to-end user loop measured by bench.py. */
+int am_replay_io(am_replay* r, const int32_t* h_pos_in, const int32_t* h_steps_in,
+                 int32_t* h_pos_out, int32_t* h_steps_out, uint8_t* h_mask, int32_t* h_order,
+                 int32_t* n_ready);
+
+/* Enqueue `rounds` rounds (CUDA graphs) without synchronising. */
+int am_replay_launch(am_replay* r, int64_t rounds);
+
+/* Synchronise; *active = agents not DONE, *n_ready = last round's ready count
+ * (either may be NULL).  Reports validation / liveness errors. */
+int am_replay_sync(am_replay* r, int64_t* active, int32_t* n_ready);
+
+/* The cudaStream_t the replay launches on (for timing events). */
+void* am_replay_stream(am_replay* r);
+
 int am_replay_destroy(am_replay* r);
 
 #ifdef __cplusplus

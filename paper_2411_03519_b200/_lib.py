@@ -67,7 +67,8 @@ SIGNATURES = {
     "am_destroy": (C.c_int, [_vp]),
     "am_last_error": (C.c_char_p, [_vp]),
     "am_version": (C.c_char_p, []),
-    "am_profile_enable": (C.c_int, [_vp, _i32]),
+    "am_profile_enable": (C.c_int, [_vp, _u32]),
+    "am_launches_per_round": (_i32, [_vp]),
     "am_profile_read": (C.c_int, [_vp, _vp, _vp, _i32]),
     "am_profile_name": (C.c_char_p, [_i32]),
     "am_replay_create": (C.c_int, [C.POINTER(_vp), _vp, C.POINTER(Synth), _i64, _vp, _vp]),
@@ -76,6 +77,10 @@ SIGNATURES = {
     "am_replay_results": (C.c_int, [_vp, _vp, _vp, _vp]),
     "am_replay_dispatched": (C.c_int, [_vp, C.POINTER(_i64)]),
     "am_replay_destroy": (C.c_int, [_vp]),
+    "am_replay_stream": (_vp, [_vp]),
+    "am_replay_launch": (C.c_int, [_vp, _i64]),
+    "am_replay_sync": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i32)]),
+    "am_replay_io": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i32)]),
 }
 
 

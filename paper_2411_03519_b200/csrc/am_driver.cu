@@ -169,6 +169,7 @@ struct am_replay {
     cudaStream_t stream = nullptr;      // own stream (graph capture)
     cudaStream_t user_stream = nullptr;
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;
+    unsigned graph_prof = 0;            // profiling mask the graphs were captured with
     long long* h_buf = nullptr;         // pinned: dispatched, liveness
 };
 
@@ -318,12 +319,26 @@ static int finish_check(am_replay* rp, int64_t* active)
     return AM_OK;
 }
 
+static int ensure_graphs(am_replay* rp)
+{
+    const unsigned pm = rp->ctx->prof.on ? rp->ctx->prof.mask : 0u;
+    if (pm != rp->graph_prof) {  // events are baked into the graphs at capture
+        if (rp->g1) cudaGraphExecDestroy(rp->g1);
+        if (rp->g8) cudaGraphExecDestroy(rp->g8);
+        rp->g1 = rp->g8 = nullptr;
+        rp->graph_prof = pm;
+    }
+    int rc;
+    if (!rp->g8 && (rc = build_graph(rp, 8, &rp->g8))) return rc;
+    if (!rp->g1 && (rc = build_graph(rp, 1, &rp->g1))) return rc;
+    return AM_OK;
+}
+
 extern "C" int am_replay_run(am_replay* rp, int64_t max_rounds, int64_t* active)
 {
     if (!rp) return AM_E_ARG;
     int rc;
-    if (!rp->g8 && (rc = build_graph(rp, 8, &rp->g8))) return rc;
-    if (!rp->g1 && (rc = build_graph(rp, 1, &rp->g1))) return rc;
+    if ((rc = ensure_graphs(rp))) return rc;
     int64_t k = 0;
     for (; k + 8 <= max_rounds; k += 8) RK(cudaGraphLaunch(rp->g8, rp->stream));
     for (; k < max_rounds; k++) RK(cudaGraphLaunch(rp->g1, rp->stream));
@@ -344,6 +359,55 @@ extern "C" int am_replay_step(am_replay* rp, uint8_t* mask, int32_t* order, int3
     rc = finish_check(rp, &act);
     if (rc) return rc;
     if (n_ready) *n_ready = c->h_ctl->n_ready;
+    return AM_OK;
+}
+
+extern "C" void* am_replay_stream(am_replay* rp) { return rp ? (void*)rp->stream : nullptr; }
+
+// One round with the world state held in HOST memory (the end-to-end user loop):
+// H2D of positions/steps, the round (CUDA graph), D2H of the committed state, the
+// ready mask, the priority order (n entries) and the ready count, then synchronise.
+extern "C" int am_replay_io(am_replay* rp, const int32_t* h_pos_in, const int32_t* h_steps_in,
+                            int32_t* h_pos_out, int32_t* h_steps_out, uint8_t* h_mask, int32_t* h_order,
+                            int32_t* n_ready)
+{
+    if (!rp || !h_pos_in || !h_steps_in) return AM_E_ARG;
+    int rc;
+    if ((rc = ensure_graphs(rp))) return rc;
+    am_ctx* c = rp->ctx;
+    const size_t n = (size_t)c->d.n;
+    RK(cudaMemcpyAsync(rp->r.pos, h_pos_in, 8 * n, cudaMemcpyHostToDevice, rp->stream));
+    RK(cudaMemcpyAsync(rp->r.steps, h_steps_in, 4 * n, cudaMemcpyHostToDevice, rp->stream));
+    RK(cudaGraphLaunch(rp->g1, rp->stream));
+    if (h_pos_out) RK(cudaMemcpyAsync(h_pos_out, rp->r.pos, 8 * n, cudaMemcpyDeviceToHost, rp->stream));
+    if (h_steps_out) RK(cudaMemcpyAsync(h_steps_out, rp->r.steps, 4 * n, cudaMemcpyDeviceToHost, rp->stream));
+    if (h_mask) RK(cudaMemcpyAsync(h_mask, rp->mask, n, cudaMemcpyDeviceToHost, rp->stream));
+    if (h_order) RK(cudaMemcpyAsync(h_order, rp->order, 4 * n, cudaMemcpyDeviceToHost, rp->stream));
+    if (n_ready) {
+        rc = finish_check(rp, nullptr);
+        if (rc) return rc;
+        *n_ready = c->h_ctl->n_ready;
+    }
+    return AM_OK;
+}
+
+extern "C" int am_replay_launch(am_replay* rp, int64_t rounds)
+{
+    if (!rp || rounds < 0) return AM_E_ARG;
+    int rc;
+    if ((rc = ensure_graphs(rp))) return rc;
+    int64_t k = 0;
+    for (; k + 8 <= rounds; k += 8) RK(cudaGraphLaunch(rp->g8, rp->stream));
+    for (; k < rounds; k++) RK(cudaGraphLaunch(rp->g1, rp->stream));
+    return AM_OK;
+}
+
+extern "C" int am_replay_sync(am_replay* rp, int64_t* active, int32_t* n_ready)
+{
+    if (!rp) return AM_E_ARG;
+    int rc = finish_check(rp, active);
+    if (rc) return rc;
+    if (n_ready) *n_ready = rp->ctx->h_ctl->n_ready;
     return AM_OK;
 }
 

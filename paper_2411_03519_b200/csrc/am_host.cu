@@ -73,11 +73,11 @@ static const char* kKernelNames[K_COUNT] = {
 
 void am_prof_begin(am_ctx* c, int id)
 {
-    if (c->prof.on) cudaEventRecordWithFlags(c->prof.ev[id][0], c->stream, cudaEventRecordExternal);
+    if (c->prof.on && (c->prof.mask >> id & 1u)) cudaEventRecordWithFlags(c->prof.ev[id][0], c->stream, cudaEventRecordExternal);
 }
 void am_prof_end(am_ctx* c, int id)
 {
-    if (c->prof.on) {
+    if (c->prof.on && (c->prof.mask >> id & 1u)) {
         cudaEventRecordWithFlags(c->prof.ev[id][1], c->stream, cudaEventRecordExternal);
         c->prof.pending |= 1u << id;
     }
@@ -98,14 +98,15 @@ void am_prof_collect(am_ctx* c)
     cudaGetLastError();
 }
 
-extern "C" int am_profile_enable(am_ctx* c, int32_t on)
+extern "C" int am_profile_enable(am_ctx* c, uint32_t mask)
 {
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
-    if (on && !c->prof.ev[0][0]) {
+    if (mask && !c->prof.ev[0][0]) {
         for (int k = 0; k < K_COUNT; k++)
             for (int j = 0; j < 2; j++) CK(c, cudaEventCreate(&c->prof.ev[k][j]));
     }
-    c->prof.on = on != 0;
+    c->prof.on = mask != 0;
+    c->prof.mask = mask;
     c->prof.pending = 0;
     for (int k = 0; k < K_COUNT; k++) { c->prof.ms[k] = 0; c->prof.cnt[k] = 0; }
     return AM_OK;
@@ -119,6 +120,12 @@ extern "C" int am_profile_read(am_ctx* c, double* ms, int64_t* counts, int32_t m
         if (counts) counts[k] = c->prof.cnt[k];
     }
     return K_COUNT;
+}
+
+extern "C" int32_t am_launches_per_round(const am_ctx* c)
+{
+    if (!c) return 0;
+    return c->path == 0 ? 2 : 9 + c->sort_passes_max;   // incl. k_round_begin
 }
 
 extern "C" const char* am_profile_name(int32_t id)

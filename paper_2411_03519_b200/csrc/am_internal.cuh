@@ -96,6 +96,7 @@ enum KernelId : int {
 };
 struct Prof {
     bool on = false;
+    unsigned mask = 0;            // kernels timed (bit = KernelId)
     cudaEvent_t ev[K_COUNT][2] = {};
     unsigned pending = 0;
     double ms[K_COUNT] = {};

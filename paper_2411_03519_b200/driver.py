@@ -100,6 +100,41 @@ class Replay:
                     x=self.pos[:, 0].cpu().numpy(), y=self.pos[:, 1].cpu().numpy(),
                     steps=self.steps.cpu().numpy())
 
+    # ---------------------------------------------------------------- bench helpers
+    def stream_ptr(self) -> int:
+        return int(self.L.am_replay_stream(self.h) or 0)
+
+    def launch(self, rounds: int) -> None:
+        check(self.L.am_replay_launch(self.h, int(rounds)), self.tracker.ctx)
+
+    def sync(self):
+        act = C.c_int64(0)
+        nr = C.c_int32(0)
+        check(self.L.am_replay_sync(self.h, C.byref(act), C.byref(nr)), self.tracker.ctx)
+        return act.value, nr.value
+
+    def io(self, h_pos: torch.Tensor, h_steps: torch.Tensor, h_mask: torch.Tensor,
+           h_order: torch.Tensor) -> None:
+        """One round with the world state in pinned host tensors (updated in place);
+        enqueued only -- call sync()."""
+        for t in (h_pos, h_steps, h_mask, h_order):
+            assert not t.is_cuda and t.is_contiguous()
+        check(self.L.am_replay_io(self.h, h_pos.data_ptr(), h_steps.data_ptr(), h_pos.data_ptr(),
+                                  h_steps.data_ptr(), h_mask.data_ptr(), h_order.data_ptr(), None),
+              self.tracker.ctx)
+
+    def profile(self, mask: int) -> None:
+        check(self.L.am_profile_enable(self.tracker.ctx, int(mask)), self.tracker.ctx)
+
+    def profile_read(self) -> dict:
+        ms = (C.c_double * 32)()
+        cnt = (C.c_int64 * 32)()
+        k = self.L.am_profile_read(self.tracker.ctx, ms, cnt, 32)
+        return {self.L.am_profile_name(i).decode(): (ms[i], cnt[i]) for i in range(k)}
+
+    def launches_per_round(self) -> int:
+        return int(self.L.am_launches_per_round(self.tracker.ctx)) + 3
+
     def dispatched(self) -> int:
         v = C.c_int64(0)
         check(self.L.am_replay_dispatched(self.h, C.byref(v)), self.tracker.ctx)
