@@ -75,6 +75,7 @@ extern "C" {
 #define AM_ASYNC        0x8u /* am_ready does not synchronise; n_ready may be NULL        */
 #define AM_FORCE_BINNED 0x10u/* always use the cell-binned pipeline (tests)                */
 #define AM_FORCE_SMALL  0x20u/* always use the fused per-simulation kernel (<=1024/sim)    */
+#define AM_STATS        0x40u/* count scan work (cells, candidate pairs) for am_scan_stats  */
 
 typedef struct am_ctx am_ctx;                 /* opaque */
 
@@ -171,6 +172,12 @@ const char* am_last_error(const am_ctx* ctx);
 int am_profile_enable(am_ctx* ctx, uint32_t mask);
 int am_profile_read(am_ctx* ctx, double* ms, int64_t* counts, int32_t max);
 const char* am_profile_name(int32_t id);
+
+/* Work counters of the neighbour scan accumulated while AM_STATS is set (host
+ * array out[6]: cells visited, candidate pairs tested, agents entering the far
+ * (time-dilated) phase, 16x16-cell blocks tested, 4x4-cell blocks tested, blocked
+ * agents); resets them.  Synchronises. */
+int am_scan_stats(am_ctx* ctx, uint64_t* out);
 
 /* Kernel launches of one am_update + am_ready on this context (host-side count). */
 int32_t am_launches_per_round(const am_ctx* ctx);

@@ -17,7 +17,7 @@ E_ARG, E_BOUNDS, E_PROTOCOL, E_VELOCITY, E_CUDA, E_NCCL = -1, -2, -3, -4, -5, -6
 E_STATE, E_LIVENESS = -11, -12
 IDLE, RUNNING, DONE = 0, 1, 2
 METRIC_L2, METRIC_LINF = 0, 1
-VALIDATE, PEEK, DIGEST, ASYNC, FORCE_BINNED, FORCE_SMALL = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+VALIDATE, PEEK, DIGEST, ASYNC, FORCE_BINNED, FORCE_SMALL, STATS = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
 
 ERROR_NAMES = {E_ARG: "AM_E_ARG", E_BOUNDS: "AM_E_BOUNDS", E_PROTOCOL: "AM_E_PROTOCOL",
                E_VELOCITY: "AM_E_VELOCITY", E_CUDA: "AM_E_CUDA", E_NCCL: "AM_E_NCCL",
@@ -69,6 +69,7 @@ SIGNATURES = {
     "am_version": (C.c_char_p, []),
     "am_profile_enable": (C.c_int, [_vp, _u32]),
     "am_launches_per_round": (_i32, [_vp]),
+    "am_scan_stats": (C.c_int, [_vp, _vp]),
     "am_profile_read": (C.c_int, [_vp, _vp, _vp, _i32]),
     "am_profile_name": (C.c_char_p, [_i32]),
     "am_replay_create": (C.c_int, [C.POINTER(_vp), _vp, C.POINTER(Synth), _i64, _vp, _vp]),

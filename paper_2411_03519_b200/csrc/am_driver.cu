@@ -69,32 +69,58 @@ __device__ __forceinline__ long long duration(const am_synth& sy, int i, int s)
 // event; any agent left active marks its simulation active for the next round.
 __global__ void __launch_bounds__(256) k_commit(RepDev r)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const Dev& d = r.d;
-    if (i >= d.n) return;
-    const uint8_t st = d.status[d.ctl->cur][i];   // after this round's dispatch
-    if (st == ST_DONE) return;
-    const int b = sim_of(d, i);
-    const long long t = r.t_sim[b];
-    bool active = true;
-    if (st == ST_RUNNING) {
-        const long long tc = r.tcommit[i];
-        if (tc <= t) {
-            const int2 np = r.newpos[i];
-            const int s = r.steps[i] + 1;
-            r.pos[i] = np;
-            r.steps[i] = s;
-            r.traj[i] = traj_step(r.traj[i], s, np.x, np.y);
-            if (d.target > 0 && s == d.target) {
-                active = false;
-                atomicMax((unsigned long long*)(r.tdone + b), (unsigned long long)t);
+    const bool one = d.n_sims == 1;
+    const uint32_t c = d.ctl->cur;
+    unsigned long long tmin = ~0ull;  // pending completions (single-simulation case)
+    int any_active = 0;
+#pragma unroll
+    for (int k = 0; k < kIngestItems; k++) {
+        const int i = blockIdx.x * (256 * kIngestItems) + k * 256 + threadIdx.x;
+        if (i >= d.n) break;
+        const uint8_t st = d.status[c][i];  // after this round's dispatch
+        if (st == ST_DONE) continue;
+        const int b = sim_of(d, i);
+        const long long t = r.t_sim[b];
+        bool active = true;
+        if (st == ST_RUNNING) {
+            const long long tc = r.tcommit[i];
+            if (tc <= t) {
+                const int2 np = r.newpos[i];
+                const int s = r.steps[i] + 1;
+                r.pos[i] = np;
+                r.steps[i] = s;
+                r.traj[i] = traj_step(r.traj[i], s, np.x, np.y);
+                if (d.target > 0 && s == d.target) {
+                    active = false;
+                    atomicMax((unsigned long long*)(r.tdone + b), (unsigned long long)t);
+                }
+            } else if (one) {
+                tmin = min(tmin, (unsigned long long)tc);
+            } else {
+                // stays RUNNING through this round: bounds the next event
+                atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
             }
-        } else {
-            // stays RUNNING through this round: bounds the next event
-            atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
+        }
+        if (active) {
+            if (one) any_active = 1;
+            else r.active_flag[b] = 1;
         }
     }
-    if (active) r.active_flag[b] = 1;
+    if (one) {  // block reduction, one atomic per block
+        __shared__ unsigned long long s_min[8];
+        __shared__ int s_act[8];
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int o = 16; o > 0; o >>= 1) tmin = min(tmin, __shfl_xor_sync(0xFFFFFFFFu, tmin, o));
+        any_active = __reduce_or_sync(0xFFFFFFFFu, (unsigned)any_active);
+        if (lane == 0) { s_min[w] = tmin; s_act[w] = any_active; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 1; q < 8; q++) { tmin = min(tmin, s_min[q]); any_active |= s_act[q]; }
+            if (tmin != ~0ull) atomicMin((unsigned long long*)r.tnext, tmin);
+            if (any_active) r.active_flag[0] = 1;
+        }
+    }
 }
 
 // dispatch, part a: cluster completion time = t + max member duration (atomicMax at
@@ -119,6 +145,7 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
     const Dev& d = r.d;
     const int nr = d.ctl->n_ready;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long tmin = ~0ull;
     if (k < nr) {
         const int i = r.order[k];
         const int b = sim_of(d, i);
@@ -135,7 +162,19 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
         bool ok = qx >= 0 && qx < d.map_w && qy >= 0 && qy < d.map_h;
         if (ok && r.sy.wall && r.sy.wall[(long long)qy * d.map_w + qx]) ok = false;
         r.newpos[i] = ok ? make_int2(qx, qy) : p;
-        atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
+        if (d.n_sims > 1) atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
+        else tmin = (unsigned long long)tc;
+    }
+    if (d.n_sims == 1) {  // block reduction, one atomic per block
+        __shared__ unsigned long long s_min[8];
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int o = 16; o > 0; o >>= 1) tmin = min(tmin, __shfl_xor_sync(0xFFFFFFFFu, tmin, o));
+        if (lane == 0) s_min[w] = tmin;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 1; q < 8; q++) tmin = min(tmin, s_min[q]);
+            if (tmin != ~0ull) atomicMin((unsigned long long*)r.tnext, tmin);
+        }
     }
     // (agents still RUNNING from earlier rounds were folded into tnext by k_commit)
     if (finish_block(r.chain, gridDim.x)) {
@@ -207,7 +246,7 @@ static int enqueue_round(am_replay* rp)
     k_disp_b<<<nb, 256, 0, rp->stream>>>(rp->r);
     am_prof_end(c, K_DISP_B);
     am_prof_begin(c, K_COMMIT);
-    k_commit<<<nb, 256, 0, rp->stream>>>(rp->r);
+    k_commit<<<(unsigned)((n + 256 * kIngestItems - 1) / (256 * kIngestItems)), 256, 0, rp->stream>>>(rp->r);
     am_prof_end(c, K_COMMIT);
     RK(cudaGetLastError());
     return AM_OK;

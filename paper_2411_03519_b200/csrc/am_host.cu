@@ -122,6 +122,19 @@ extern "C" int am_profile_read(am_ctx* c, double* ms, int64_t* counts, int32_t m
     return K_COUNT;
 }
 
+extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
+{
+    if (!c || !out) return set_err(c, AM_E_ARG, "NULL argument");
+    CK(c, cudaMemcpyAsync(c->h_ctl, c->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    const Ctl& h = *c->h_ctl;
+    out[0] = h.st_cells; out[1] = h.st_cand; out[2] = h.st_p2; out[3] = h.st_b2; out[4] = h.st_b1;
+    out[5] = h.st_blocked;
+    CK(c, cudaMemsetAsync(&c->d.ctl->st_cells, 0, 6 * sizeof(unsigned long long), c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return AM_OK;
+}
+
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
@@ -301,7 +314,7 @@ static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, co
     if (c->d.n == 0) return AM_OK;
     if (!pos || !steps || (mode == 2 && !st)) return set_err(c, AM_E_ARG, "NULL array");
     am_prof_begin(c, K_INGEST);
-    k_ingest<<<blocks(c->d.n, 256), 256, 0, c->stream>>>(c->d, (const int2*)pos, steps, st, mode);
+    k_ingest<<<blocks(c->d.n, 256 * kIngestItems), 256, 0, c->stream>>>(c->d, (const int2*)pos, steps, st, mode);
     am_prof_end(c, K_INGEST);
     CK(c, cudaGetLastError());
     return AM_OK;

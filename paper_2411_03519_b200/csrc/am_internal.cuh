@@ -18,6 +18,7 @@ constexpr int kCellsPerTile = 4096;       // cell-table scan tile (256 threads x
 constexpr int kReadyTile = 2048;          // ready compaction tile (256 threads x 8 agents)
 constexpr int kSortTile = 2048;           // radix pass tile (256 threads x 8 keys)
 constexpr int kMaxSortPasses = 8;
+constexpr int kIngestItems = 4;          // agents per thread in k_ingest / k_commit
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
 constexpr uint32_t kRClamp = 46340u;      // >= every distance on a 32768^2 map; R^2 < 2^31
 
@@ -45,6 +46,9 @@ struct Ctl {
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
     unsigned long long sort_or;   // OR of all ready keys
+    // scan statistics (AM_STATS): cells visited, candidate pairs, phase-2 agents,
+    // pyramid blocks tested (16x16, 4x4)
+    unsigned long long st_cells, st_cand, st_p2, st_b2, st_b1, st_blocked;
     Chain ingest, bin, cells, ready, hist, small_, pass[kMaxSortPasses];
 };
 

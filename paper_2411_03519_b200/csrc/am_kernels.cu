@@ -27,12 +27,13 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
 {
     Ctl* ctl = d.ctl;
     const uint32_t c = ctl->cur;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int err = 0, act = 0, run = 0;
-    int s = 0;
-    if (i < d.n) {
-        int2 p = npos[i];
-        s = nstep[i];
+    int err = 0, act = 0, run = 0, smin = INT_MAX, smax = INT_MIN;
+#pragma unroll
+    for (int k = 0; k < kIngestItems; k++) {
+        const int i = blockIdx.x * (256 * kIngestItems) + k * 256 + threadIdx.x;
+        if (i >= d.n) break;
+        const int2 p = npos[i];
+        const int s = nstep[i];
         uint8_t st;
         if (p.x < 0 || p.x >= d.map_w || p.y < 0 || p.y >= d.map_h) err |= ERR_BOUNDS;
         if (mode == 0) {
@@ -42,7 +43,7 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
             st = ost;
             if (ds == 0) {
                 if (d.flags & AM_VALIDATE) {
-                    int2 op = d.pos[c][i];
+                    const int2 op = d.pos[c][i];
                     if (op.x != p.x || op.y != p.y) err |= ERR_PROTOCOL;
                 }
             } else if (ds == 1) {
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
                     err |= ERR_PROTOCOL;
                 } else {
                     if (d.flags & AM_VALIDATE) {
-                        int2 op = d.pos[c][i];
+                        const int2 op = d.pos[c][i];
                         if (!within(p.x - op.x, p.y - op.y, (uint32_t)d.v, d.metric)) err |= ERR_VELOCITY;
                     }
                     st = (d.target > 0 && s == d.target) ? ST_DONE : ST_IDLE;
@@ -68,24 +69,35 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
         d.pos[c ^ 1u][i] = p;
         d.step[c ^ 1u][i] = s;
         d.status[c ^ 1u][i] = st;
-        act = st != ST_DONE;
-        run = st == ST_RUNNING;
-    }
-    // block reductions
-    const int lane = threadIdx.x & 31;
-    int werr = __reduce_or_sync(0xFFFFFFFFu, (unsigned)err);
-    int wmin = __reduce_min_sync(0xFFFFFFFFu, act ? s : INT_MAX);
-    int wmax = __reduce_max_sync(0xFFFFFFFFu, act ? s : INT_MIN);
-    int wact = __reduce_add_sync(0xFFFFFFFFu, (unsigned)act);
-    int wrun = __reduce_add_sync(0xFFFFFFFFu, (unsigned)run);
-    if (lane == 0) {
-        if (werr) atomicOr(&ctl->err_new, werr);
-        if (wact) {
-            atomicMin(&ctl->acc_W, wmin);
-            atomicMax(&ctl->acc_S, wmax);
-            atomicAdd(&ctl->acc_active, wact);
+        if (st != ST_DONE) {
+            act++;
+            smin = min(smin, s);
+            smax = max(smax, s);
         }
-        if (wrun) atomicAdd(&ctl->acc_running, wrun);
+        run += st == ST_RUNNING;
+    }
+    // block reduction, then one atomic per quantity per block
+    __shared__ int r_err[8], r_min[8], r_max[8], r_act[8], r_run[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    err = (int)__reduce_or_sync(0xFFFFFFFFu, (unsigned)err);
+    smin = __reduce_min_sync(0xFFFFFFFFu, smin);
+    smax = __reduce_max_sync(0xFFFFFFFFu, smax);
+    act = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)act);
+    run = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)run);
+    if (lane == 0) { r_err[w] = err; r_min[w] = smin; r_max[w] = smax; r_act[w] = act; r_run[w] = run; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < 8; q++) {
+            err |= r_err[q]; smin = min(smin, r_min[q]); smax = max(smax, r_max[q]);
+            act += r_act[q]; run += r_run[q];
+        }
+        if (err) atomicOr(&ctl->err_new, err);
+        if (act) {
+            atomicMin(&ctl->acc_W, smin);
+            atomicMax(&ctl->acc_S, smax);
+            atomicAdd(&ctl->acc_active, act);
+        }
+        if (run) atomicAdd(&ctl->acc_running, run);
     }
     if (finish_block(&ctl->ingest, gridDim.x) && threadIdx.x == 0) {
         const int e = *(volatile int*)&ctl->err_new;
@@ -212,9 +224,10 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
 template <bool kCouple>
 __device__ __forceinline__ bool scan_cell(const Dev& d, uint32_t key, int ax, int ay, int as,
                                           uint32_t aid, bool blocked, uint32_t Rc,
-                                          unsigned long long& dig)
+                                          unsigned long long& dig, uint32_t& ncand)
 {
     const int beg = d.ctab[key].x, end = d.ctab[key + 1].x;
+    ncand += (uint32_t)(end - beg);
     for (int b = beg; b < end; b++) {
         const int4 B = d.rec[b];
         const uint32_t bid = (uint32_t)B.z;
@@ -248,6 +261,7 @@ __global__ void __launch_bounds__(256) k_scan(Dev d)
     const int nact = d.ctl->n_active;
     const int W = d.ctl->W;
     bool blocked = false;
+    uint32_t ncells = 0, ncand = 0, np2 = 0, nb2 = 0, nb1 = 0;
     if (r < nact) {
         const int4 A = d.rec[r];
         const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
@@ -265,13 +279,15 @@ __global__ void __launch_bounds__(256) k_scan(Dev d)
                                     ((cy + 1) << cl) - 1, Rc, d.metric))
                         continue;
                     const uint32_t key = morton(cx, cy);
+                    ncells++;
                     if (d.ctab[key].y > as) continue;
-                    blocked = scan_cell<true>(d, key, ax, ay, as, aid, blocked, Rc, dig);
+                    blocked = scan_cell<true>(d, key, ax, ay, as, aid, blocked, Rc, dig, ncand);
                 }
         }
         if (d.flags & AM_DIGEST) d.digest[aid] = dig;
         // ---- phase 2
         if (!blocked && as > W) {
+            np2 = 1;
             const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
             const int l2 = cl + 4;  // 16 cells per side
             const int G2 = G >> 4;
@@ -280,6 +296,7 @@ __global__ void __launch_bounds__(256) k_scan(Dev d)
             for (int by = by0; by <= by1 && !blocked; by++)
                 for (int bx = bx0; bx <= bx1 && !blocked; bx++) {
                     const int m2 = d.lmin2[morton(bx, by)];
+                    nb2++;
                     if (m2 >= as) continue;
                     if (!box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
                                     rb_radius((long long)as - m2, d.v, d.r_p), d.metric))
@@ -289,6 +306,7 @@ __global__ void __launch_bounds__(256) k_scan(Dev d)
                             const int qx = bx * 4 + sx, qy = by * 4 + sy;  // 4x4-cell block
                             const int l1 = cl + 2;
                             const int m1 = d.lmin1[morton(qx, qy)];
+                            nb1++;
                             if (m1 >= as) continue;
                             if (!box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
                                             ((qy + 1) << l1) - 1, rb_radius((long long)as - m1, d.v, d.r_p),
@@ -303,11 +321,12 @@ __global__ void __launch_bounds__(256) k_scan(Dev d)
                                     if (box_within(ax, ay, x0, y0, x1, y1, Rc, d.metric)) continue;
                                     const uint32_t key = morton(cx, cy);
                                     const int m0 = d.ctab[key].y;
+                                    ncells++;
                                     if (m0 >= as) continue;
                                     if (!box_within(ax, ay, x0, y0, x1, y1,
                                                     rb_radius((long long)as - m0, d.v, d.r_p), d.metric))
                                         continue;
-                                    blocked = scan_cell<false>(d, key, ax, ay, as, aid, false, Rc, dig);
+                                    blocked = scan_cell<false>(d, key, ax, ay, as, aid, false, Rc, dig, ncand);
                                 }
                         }
                 }
@@ -315,6 +334,19 @@ __global__ void __launch_bounds__(256) k_scan(Dev d)
     }
     const unsigned bits = __ballot_sync(0xFFFFFFFFu, blocked);
     if ((threadIdx.x & 31) == 0 && r < nact) d.blkbits[r >> 5] = bits;
+    if (d.flags & AM_STATS) {
+        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
+        const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, np2), c3 = __reduce_add_sync(0xFFFFFFFFu, nb2);
+        const unsigned c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
+            atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
+            atomicAdd(&d.ctl->st_p2, (unsigned long long)c2);
+            atomicAdd(&d.ctl->st_b2, (unsigned long long)c3);
+            atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
+            atomicAdd(&d.ctl->st_blocked, (unsigned long long)__popc(bits));
+        }
+    }
 }
 
 // k_finalize: label = root of the agent's tree (= min id of its cluster, Q10);
@@ -403,12 +435,18 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
             pos++;
         }
     }
-    // OR of all keys -> number of radix passes
+    // OR of all keys -> number of radix passes (one atomic per block)
+    __shared__ unsigned long long s_or[8];
     unsigned lo = __reduce_or_sync(0xFFFFFFFFu, (unsigned)kor);
     unsigned hi = __reduce_or_sync(0xFFFFFFFFu, (unsigned)(kor >> 32));
-    if (lane == 0 && (lo | hi)) atomicOr(&ctl->sort_or, ((unsigned long long)hi << 32) | lo);
+    if (lane == 0) s_or[w] = ((unsigned long long)hi << 32) | lo;
     __syncthreads();
-    if (t == 0 && ncl) atomicAdd(&ctl->n_clusters, (int)ncl);
+    if (t == 0) {
+        unsigned long long o = 0;
+        for (int q = 0; q < 8; q++) o |= s_or[q];
+        if (o) atomicOr(&ctl->sort_or, o);
+        if (ncl) atomicAdd(&ctl->n_clusters, (int)ncl);
+    }
     if (finish_block(&ctl->ready, gridDim.x) && t == 0) {
         unsigned long long o = *(volatile unsigned long long*)&ctl->sort_or;
         int bits = o ? 64 - __clzll((long long)o) : 0;

@@ -22,13 +22,13 @@ class Replay:
     def __init__(self, map_w, map_h, r_p, v, x0, y0, steps_target, *, n_sims=1, wall=None,
                  lat=None, cdf32=None, vals=None, base_us=5000, lat_seed=4, policy_seed=3,
                  dur_table=None, policy=0, quantum_us=0, cell=0, metric="l2", force=None,
-                 device="cuda"):
+                 stats=False, device="cuda"):
         self.device = torch.device(device)
         n = len(x0)
         self.n = n
         self.tracker = Tracker(map_w, map_h, r_p, v, n, target=steps_target, n_sims=n_sims,
                                cell=cell, metric=metric, validate=True, digest=True, force=force,
-                               device=self.device)
+                               stats=stats, device=self.device)
         dev = self.device
         self.pos = torch.tensor(np.stack([np.asarray(x0), np.asarray(y0)], 1), dtype=torch.int32,
                                 device=dev).contiguous()

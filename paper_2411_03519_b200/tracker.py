@@ -36,7 +36,7 @@ class Tracker:
     def __init__(self, map_w: int, map_h: int, r_p: int, v: int, n: int, *, target: int = 0,
                  n_sims: int = 1, cell: int = 0, metric: str = "l2", validate: bool = True,
                  peek: bool = False, digest: bool = False, force: str | None = None,
-                 device=None, stream: torch.cuda.Stream | None = None):
+                 stats: bool = False, device=None, stream: torch.cuda.Stream | None = None):
         self.L = _lib.load()
         self.device = torch.device(device if device is not None else "cuda")
         self.n = int(n)
@@ -48,6 +48,8 @@ class Tracker:
             flags |= _lib.PEEK
         if digest:
             flags |= _lib.DIGEST
+        if stats:
+            flags |= _lib.STATS
         if force == "binned":
             flags |= _lib.FORCE_BINNED
         elif force == "small":
@@ -124,6 +126,11 @@ class Tracker:
 
     def reset(self) -> None:
         check(self.L.am_reset(self.ctx), self.ctx)
+
+    def scan_stats(self) -> dict:
+        out = (C.c_uint64 * 6)()
+        check(self.L.am_scan_stats(self.ctx, out), self.ctx)
+        return dict(zip(("cells", "candidates", "far_agents", "blocks16", "blocks4", "blocked"), list(out)))
 
     def workspace_bytes(self) -> int:
         return int(self.L.am_workspace_bytes(self.ctx))
