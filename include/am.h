@@ -76,6 +76,7 @@ extern "C" {
 #define AM_FORCE_BINNED 0x10u/* always use the cell-binned pipeline (tests)                */
 #define AM_FORCE_SMALL  0x20u/* always use the fused per-simulation kernel (<=1024/sim)    */
 #define AM_STATS        0x40u/* count scan work (cells, candidate pairs) for am_scan_stats  */
+#define AM_SCAN_THREAD  0x80u/* one thread per agent neighbour scan (ablation baseline)    */
 
 typedef struct am_ctx am_ctx;                 /* opaque */
 

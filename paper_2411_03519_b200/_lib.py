@@ -17,7 +17,8 @@ E_ARG, E_BOUNDS, E_PROTOCOL, E_VELOCITY, E_CUDA, E_NCCL = -1, -2, -3, -4, -5, -6
 E_STATE, E_LIVENESS = -11, -12
 IDLE, RUNNING, DONE = 0, 1, 2
 METRIC_L2, METRIC_LINF = 0, 1
-VALIDATE, PEEK, DIGEST, ASYNC, FORCE_BINNED, FORCE_SMALL, STATS = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
+VALIDATE, PEEK, DIGEST, ASYNC, FORCE_BINNED, FORCE_SMALL, STATS, SCAN_THREAD = (
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80)
 
 ERROR_NAMES = {E_ARG: "AM_E_ARG", E_BOUNDS: "AM_E_BOUNDS", E_PROTOCOL: "AM_E_PROTOCOL",
                E_VELOCITY: "AM_E_VELOCITY", E_CUDA: "AM_E_CUDA", E_NCCL: "AM_E_NCCL",

@@ -13,6 +13,7 @@ __global__ void k_bin(Dev d);
 __global__ void k_cells(Dev d);
 __global__ void k_scatter(Dev d);
 __global__ void k_scan(Dev d);
+__global__ void k_scan_thread(Dev d);
 __global__ void k_finalize(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
@@ -255,7 +256,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_key = take(4 * N); o_rank = take(4 * N);
         o_cnt = take(4 * NC); o_cmin = take(4 * NC);
         o_ctab = take(8 * (NC + 1)); o_l1 = take(4 * (NC / 16)); o_l2 = take(4 * (NC / 256));
-        o_rec = take(16 * N); o_blk = take(4 * (N / 32 + 1));
+        o_rec = take(16 * N); o_blk = take(N);
         o_par = take(4 * N); o_bad = take(N);
         o_rk0 = take(8 * N); o_rk1 = take(8 * N); o_rv0 = take(4 * N); o_rv1 = take(4 * N);
         o_tc = take(8 * (size_t)x->ntiles_cells); o_tr = take(8 * (size_t)x->ntiles_ready);
@@ -279,7 +280,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.key = (uint32_t*)(b + o_key); d.rank = (uint32_t*)(b + o_rank);
         d.cnt = (uint32_t*)(b + o_cnt); d.cmin = (int32_t*)(b + o_cmin);
         d.ctab = (int2*)(b + o_ctab); d.lmin1 = (int32_t*)(b + o_l1); d.lmin2 = (int32_t*)(b + o_l2);
-        d.rec = (int4*)(b + o_rec); d.blkbits = (uint32_t*)(b + o_blk);
+        d.rec = (int4*)(b + o_rec); d.blk8 = (uint8_t*)(b + o_blk);
         d.parent = (uint32_t*)(b + o_par); d.bad = (uint8_t*)(b + o_bad);
         d.rkey[0] = (unsigned long long*)(b + o_rk0); d.rkey[1] = (unsigned long long*)(b + o_rk1);
         d.rval[0] = (uint32_t*)(b + o_rv0); d.rval[1] = (uint32_t*)(b + o_rv1);
@@ -401,7 +402,10 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         LAUNCH(K_BIN, (k_bin<<<nb, 256, 0, s>>>(d)));
         LAUNCH(K_CELLS, (k_cells<<<c->ntiles_cells, 256, 0, s>>>(d)));
         LAUNCH(K_SCATTER, (k_scatter<<<nb, 256, 0, s>>>(d)));
-        LAUNCH(K_SCAN, (k_scan<<<nb, 256, 0, s>>>(d)));
+        if (d.flags & AM_SCAN_THREAD)
+            LAUNCH(K_SCAN, (k_scan_thread<<<nb, 256, 0, s>>>(d)));
+        else
+            LAUNCH(K_SCAN, (k_scan<<<blocks(d.ncells / 16, 8), 256, 0, s>>>(d)));
         LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));
         LAUNCH(K_READY, (k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask)));
         LAUNCH(K_SORT_HIST, (k_sort_hist<<<c->ntiles_sort, 256, 0, s>>>(d, c->sort_passes_max)));

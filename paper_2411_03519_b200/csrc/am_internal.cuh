@@ -74,7 +74,7 @@ struct Dev {
     int32_t* lmin1;        // [ncells/16]  min step per 4x4-cell block
     int32_t* lmin2;        // [ncells/256] min step per 16x16-cell block
     int4* rec;             // [n] sorted records {x | y<<16, step, id, status}
-    uint32_t* blkbits;     // [n/32+1] blocked bit per sorted record
+    uint8_t* blk8;         // [n] blocked flag per sorted record
     uint32_t* parent;      // [n] union-find forest in id space (root = min id)
     uint8_t* bad;          // [n] cluster (root) has a blocked or RUNNING member
     int32_t* labels;       // [n]
@@ -170,12 +170,24 @@ __device__ __forceinline__ bool within(int dx, int dy, uint32_t R, int metric)
     return d2 <= R * R;
 }
 
+// distance between the tile boxes [ax0,ax1]x[ay0,ay1] and [bx0,bx1]x[by0,by1] within R
+__device__ __forceinline__ bool box_dist_within(int ax0, int ay0, int ax1, int ay1, int bx0, int by0,
+                                                int bx1, int by1, uint32_t R, int metric);
+
 // distance from point (x,y) to the tile box [x0,x1] x [y0,y1] within R
 __device__ __forceinline__ bool box_within(int x, int y, int x0, int y0, int x1, int y1,
                                            uint32_t R, int metric)
 {
     int dx = x < x0 ? x0 - x : (x > x1 ? x - x1 : 0);
     int dy = y < y0 ? y0 - y : (y > y1 ? y - y1 : 0);
+    return within(dx, dy, R, metric);
+}
+
+__device__ __forceinline__ bool box_dist_within(int ax0, int ay0, int ax1, int ay1, int bx0, int by0,
+                                                int bx1, int by1, uint32_t R, int metric)
+{
+    const int dx = bx0 > ax1 ? bx0 - ax1 : (ax0 > bx1 ? ax0 - bx1 : 0);
+    const int dy = by0 > ay1 ? by0 - ay1 : (ay0 > by1 ? ay0 - by1 : 0);
     return within(dx, dy, R, metric);
 }
 

@@ -255,7 +255,7 @@ __device__ __forceinline__ bool scan_cell(const Dev& d, uint32_t key, int ax, in
 //            over the disk of radius R_b(s_A - W), walking the min-step pyramid:
 //            a block with min step m is skipped if m >= s_A or its box distance
 //            exceeds R_b(s_A - m) (exact pruning: no agent inside can block A).
-__global__ void __launch_bounds__(256) k_scan(Dev d)
+__global__ void __launch_bounds__(256) k_scan_thread(Dev d)
 {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int nact = d.ctl->n_active;
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256) k_scan(Dev d)
         }
     }
     const unsigned bits = __ballot_sync(0xFFFFFFFFu, blocked);
-    if ((threadIdx.x & 31) == 0 && r < nact) d.blkbits[r >> 5] = bits;
+    if (r < nact) d.blk8[r] = blocked;
     if (d.flags & AM_STATS) {
         const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
         const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, np2), c3 = __reduce_add_sync(0xFFFFFFFFu, nb2);
@@ -349,6 +349,219 @@ __global__ void __launch_bounds__(256) k_scan(Dev d)
     }
 }
 
+// ---------------------------------------------------------------------------------
+// k_scan: warp-cooperative time-dilated neighbour scan.  One warp per 4x4-cell block
+// (Morton-contiguous records); the block's agents are taken 32 at a time ("chunk",
+// one agent per lane) and share ONE traversal, pruned against the chunk's bounding
+// box and maximum step, so every cell-table / pyramid / record load is a coalesced
+// or broadcast warp load and the per-lane work is a SIMD loop over candidates.
+//   near phase: cells within box distance R_c = r_p + v of the chunk box: coupling
+//               unions, digests, blocking tests;
+//   far phase:  only lanes not yet blocked; cells beyond R_c inside the disk of
+//               radius R_b(max_step - W), walked through the 16x16 and 4x4 min-step
+//               pyramid; a block with min step m is skipped if m >= max step or its
+//               box distance to the chunk box exceeds R_b(max step - m) (exact: no
+//               agent inside can block any agent of the chunk).
+struct Lane {
+    int ax, ay, as;
+    uint32_t aid;
+    bool valid, blocked;
+    unsigned long long dig;
+};
+
+// test the lane's agent against the records [beg, beg+cnt) of one cell
+template <bool kNear>
+__device__ __forceinline__ void scan_records(const Dev& d, Lane& L, int beg, int cnt, uint32_t Rc,
+                                             uint32_t& ncand)
+{
+    const int lane = threadIdx.x & 31;
+    ncand += (uint32_t)cnt;
+    for (int j0 = 0; j0 < cnt; j0 += 32) {
+        int4 mine = make_int4(0, 0, 0, 0);
+        if (j0 + lane < cnt) mine = d.rec[beg + j0 + lane];
+        const int m = min(32, cnt - j0);
+        for (int t = 0; t < m; t++) {
+            const int bxy = __shfl_sync(0xFFFFFFFFu, mine.x, t);
+            const int bs = __shfl_sync(0xFFFFFFFFu, mine.y, t);
+            const uint32_t bid = (uint32_t)__shfl_sync(0xFFFFFFFFu, mine.z, t);
+            if (!L.valid || bid == L.aid) continue;
+            const int dx = (bxy & 0xFFFF) - L.ax, dy = (bxy >> 16) - L.ay;
+            if (kNear && bs == L.as) {
+                if (within(dx, dy, Rc, d.metric)) {
+                    if (L.aid < bid) uf_unite(d.parent, L.aid, bid);
+                    if ((d.flags & AM_DIGEST) && within(dx, dy, (uint32_t)d.r_p, d.metric))
+                        L.dig += digest_term(bid, dx, dy);
+                }
+            } else if (!L.blocked && bs < L.as) {
+                if (within(dx, dy, rb_radius((long long)L.as - bs, d.v, d.r_p), d.metric)) L.blocked = true;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 1) k_scan(Dev d)
+{
+    const int lane = threadIdx.x & 31;
+    const int blk = blockIdx.x * 8 + (threadIdx.x >> 5);   // 4x4-cell block (key >> 4)
+    if (blk >= (d.ncells >> 4)) return;                     // warp-uniform
+    const int beg = d.ctab[blk * 16].x, end = d.ctab[blk * 16 + 16].x;
+    if (beg == end) return;
+    const int W = d.ctl->W;
+    const int cl = d.clog, G = 1 << d.glog;
+    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    uint32_t ncells = 0, ncand = 0, np2 = 0, nb2 = 0, nb1 = 0;
+    for (int base = beg; base < end; base += 32) {
+        Lane L;
+        const int r = base + lane;
+        L.valid = r < end;
+        const int4 A = L.valid ? d.rec[r] : make_int4(0, INT_MIN, -1, 0);
+        L.ax = A.x & 0xFFFF;
+        L.ay = A.x >> 16;
+        L.as = A.y;
+        L.aid = (uint32_t)A.z;
+        L.blocked = false;
+        L.dig = 0;
+        // chunk bounding box and max step
+        const int x0 = __reduce_min_sync(0xFFFFFFFFu, L.valid ? L.ax : INT_MAX);
+        const int x1 = __reduce_max_sync(0xFFFFFFFFu, L.valid ? L.ax : INT_MIN);
+        const int y0 = __reduce_min_sync(0xFFFFFFFFu, L.valid ? L.ay : INT_MAX);
+        const int y1 = __reduce_max_sync(0xFFFFFFFFu, L.valid ? L.ay : INT_MIN);
+        const int smax = __reduce_max_sync(0xFFFFFFFFu, L.valid ? L.as : INT_MIN);
+        // ---- near phase
+        {
+            const int cx0 = max(0, (x0 - (int)Rc) >> cl), cx1 = min(G - 1, (x1 + (int)Rc) >> cl);
+            const int cy0 = max(0, (y0 - (int)Rc) >> cl), cy1 = min(G - 1, (y1 + (int)Rc) >> cl);
+            const int nx = cx1 - cx0 + 1, ncell = nx * (cy1 - cy0 + 1);
+            for (int c0 = 0; c0 < ncell; c0 += 32) {
+                const int k = c0 + lane;
+                int cb = 0, cc = 0;
+                bool take = false;
+                if (k < ncell) {
+                    const int cx = cx0 + k % nx, cy = cy0 + k / nx;
+                    if (box_dist_within(x0, y0, x1, y1, cx << cl, cy << cl, ((cx + 1) << cl) - 1,
+                                        ((cy + 1) << cl) - 1, Rc, d.metric)) {
+                        const uint32_t key = morton(cx, cy);
+                        const int2 e = d.ctab[key];
+                        cb = e.x;
+                        cc = d.ctab[key + 1].x - e.x;
+                        take = cc > 0 && e.y <= smax;
+                    }
+                    ncells++;
+                }
+                unsigned todo = __ballot_sync(0xFFFFFFFFu, take);
+                while (todo) {
+                    const int src = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const int b0 = __shfl_sync(0xFFFFFFFFu, cb, src), n0 = __shfl_sync(0xFFFFFFFFu, cc, src);
+                    scan_records<true>(d, L, b0, n0, Rc, ncand);
+                }
+            }
+        }
+        // ---- far phase (lanes not blocked yet)
+        const bool open = L.valid && !L.blocked && L.as > W;
+        const int fmax = __reduce_max_sync(0xFFFFFFFFu, open ? L.as : INT_MIN);
+        if (fmax > W) {
+            np2 += open;
+            const int fx0 = __reduce_min_sync(0xFFFFFFFFu, open ? L.ax : INT_MAX);
+            const int fx1 = __reduce_max_sync(0xFFFFFFFFu, open ? L.ax : INT_MIN);
+            const int fy0 = __reduce_min_sync(0xFFFFFFFFu, open ? L.ay : INT_MAX);
+            const int fy1 = __reduce_max_sync(0xFFFFFFFFu, open ? L.ay : INT_MIN);
+            const int R = (int)rb_radius((long long)fmax - W, d.v, d.r_p);
+            const int l2 = cl + 4, G2 = G >> 4;
+            const int bx0 = max(0, (fx0 - R) >> l2), bx1 = min(G2 - 1, (fx1 + R) >> l2);
+            const int by0 = max(0, (fy0 - R) >> l2), by1 = min(G2 - 1, (fy1 + R) >> l2);
+            const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);
+            bool done = false;
+            for (int q0 = 0; q0 < nb && !done; q0 += 32) {
+                const int q = q0 + lane;
+                bool keep2 = false;
+                int bx = 0, by = 0;
+                if (q < nb) {
+                    bx = bx0 + q % nbx;
+                    by = by0 + q / nbx;
+                    const int m2 = d.lmin2[morton(bx, by)];
+                    keep2 = m2 < fmax &&
+                            box_dist_within(fx0, fy0, fx1, fy1, bx << l2, by << l2, ((bx + 1) << l2) - 1,
+                                            ((by + 1) << l2) - 1, rb_radius((long long)fmax - m2, d.v, d.r_p),
+                                            d.metric);
+                    nb2++;
+                }
+                unsigned todo2 = __ballot_sync(0xFFFFFFFFu, keep2);
+                while (todo2 && !done) {
+                    const int src2 = __ffs(todo2) - 1;
+                    todo2 &= todo2 - 1;
+                    const int BX = __shfl_sync(0xFFFFFFFFu, bx, src2), BY = __shfl_sync(0xFFFFFFFFu, by, src2);
+                    // 16 4x4-cell blocks of this 16x16 block: lanes 0..15
+                    const int l1 = cl + 2;
+                    const int qx = BX * 4 + (lane & 3), qy = BY * 4 + ((lane >> 2) & 3);
+                    bool keep1 = false;
+                    if (lane < 16) {
+                        const int m1 = d.lmin1[morton(qx, qy)];
+                        keep1 = m1 < fmax &&
+                                box_dist_within(fx0, fy0, fx1, fy1, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
+                                                ((qy + 1) << l1) - 1, rb_radius((long long)fmax - m1, d.v, d.r_p),
+                                                d.metric);
+                        nb1++;
+                    }
+                    unsigned todo1 = __ballot_sync(0xFFFFFFFFu, keep1);
+                    while (todo1 && !done) {
+                        const int src1 = __ffs(todo1) - 1;
+                        todo1 &= todo1 - 1;
+                        const int QX = __shfl_sync(0xFFFFFFFFu, qx, src1), QY = __shfl_sync(0xFFFFFFFFu, qy, src1);
+                        const int cx = QX * 4 + (lane & 3), cy = QY * 4 + ((lane >> 2) & 3);
+                        int cb = 0, cc = 0;
+                        bool take = false;
+                        if (lane < 16) {
+                            const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
+                            // near-phase cells were tested completely already
+                            if (!box_dist_within(x0, y0, x1, y1, X0, Y0, X1, Y1, Rc, d.metric)) {
+                                const uint32_t key = morton(cx, cy);
+                                const int2 e = d.ctab[key];
+                                if (e.y < fmax &&
+                                    box_dist_within(fx0, fy0, fx1, fy1, X0, Y0, X1, Y1,
+                                                    rb_radius((long long)fmax - e.y, d.v, d.r_p), d.metric)) {
+                                    cb = e.x;
+                                    cc = d.ctab[key + 1].x - e.x;
+                                    take = cc > 0;
+                                }
+                            }
+                            ncells++;
+                        }
+                        unsigned todo0 = __ballot_sync(0xFFFFFFFFu, take);
+                        while (todo0) {
+                            const int src0 = __ffs(todo0) - 1;
+                            todo0 &= todo0 - 1;
+                            const int b0 = __shfl_sync(0xFFFFFFFFu, cb, src0), n0 = __shfl_sync(0xFFFFFFFFu, cc, src0);
+                            scan_records<false>(d, L, b0, n0, Rc, ncand);
+                        }
+                        done = __all_sync(0xFFFFFFFFu, !open || L.blocked);
+                    }
+                }
+            }
+        }
+        if (L.valid) {
+            d.blk8[r] = L.blocked;
+            if (d.flags & AM_DIGEST) d.digest[L.aid] = L.dig;
+        }
+        if (d.flags & AM_STATS) {
+            const unsigned nbk = __popc(__ballot_sync(0xFFFFFFFFu, L.valid && L.blocked));
+            if (lane == 0) atomicAdd(&d.ctl->st_blocked, (unsigned long long)nbk);
+        }
+    }
+    if (d.flags & AM_STATS) {
+        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = ncand;  // ncand is warp-uniform
+        const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, np2), c3 = __reduce_add_sync(0xFFFFFFFFu, nb2);
+        const unsigned c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
+        if (lane == 0) {
+            atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
+            atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
+            atomicAdd(&d.ctl->st_p2, (unsigned long long)c2);
+            atomicAdd(&d.ctl->st_b2, (unsigned long long)c3);
+            atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
+        }
+    }
+}
+
 // k_finalize: label = root of the agent's tree (= min id of its cluster, Q10);
 // a blocked or RUNNING member makes its cluster not ready (Q7).
 __global__ void __launch_bounds__(256) k_finalize(Dev d)
@@ -359,7 +572,7 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
     const uint32_t aid = (uint32_t)A.z;
     const uint32_t root = uf_find(d.parent, aid);
     d.labels[aid] = (int32_t)root;
-    const bool blk = (d.blkbits[r >> 5] >> (r & 31)) & 1u;
+    const bool blk = d.blk8[r] != 0;
     if (blk || A.w == ST_RUNNING) d.bad[root] = 1;
 }
 

@@ -36,7 +36,8 @@ class Tracker:
     def __init__(self, map_w: int, map_h: int, r_p: int, v: int, n: int, *, target: int = 0,
                  n_sims: int = 1, cell: int = 0, metric: str = "l2", validate: bool = True,
                  peek: bool = False, digest: bool = False, force: str | None = None,
-                 stats: bool = False, device=None, stream: torch.cuda.Stream | None = None):
+                 stats: bool = False, scan_thread: bool = False, device=None,
+                 stream: torch.cuda.Stream | None = None):
         self.L = _lib.load()
         self.device = torch.device(device if device is not None else "cuda")
         self.n = int(n)
@@ -50,6 +51,8 @@ class Tracker:
             flags |= _lib.DIGEST
         if stats:
             flags |= _lib.STATS
+        if scan_thread:
+            flags |= _lib.SCAN_THREAD
         if force == "binned":
             flags |= _lib.FORCE_BINNED
         elif force == "small":

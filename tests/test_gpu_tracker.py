@@ -101,6 +101,19 @@ def test_random_states_vs_oracle(case):
         tr.close()
 
 
+@pytest.mark.parametrize("case", CASES[5:], ids=[f"n{c[0]}_spread{c[4]}" for c in CASES[5:]])
+def test_thread_scan_ablation_matches(case):
+    """The one-thread-per-agent scan (AM_SCAN_THREAD, ablation baseline) gives the same bits."""
+    n, m, r_p, v, ms, pr, pd, metric, seed = case
+    target = ms + 1
+    x, y, s, st = _random_case(n, m, r_p, v, ms, pr, pd, seed, target)
+    p = O.params(m, m, r_p, v, target, O.LINF if metric == "linf" else O.L2)
+    st_o = st.copy()
+    r = O.round_(p, x, y, s, st_o, peek=False)
+    tr = Tracker(m, m, r_p, v, n, target=target, metric=metric, force="binned", scan_thread=True)
+    _compare(_gpu_round(tr, x, y, s, st), r, st_o)
+
+
 @pytest.mark.parametrize("cell", [1, 4, 8, 32])
 def test_cell_size_does_not_change_results(cell):
     n, m = 3000, 256
