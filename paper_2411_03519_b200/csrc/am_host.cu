@@ -405,7 +405,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         if (d.flags & AM_SCAN_THREAD)
             LAUNCH(K_SCAN, (k_scan_thread<<<nb, 256, 0, s>>>(d)));
         else
-            LAUNCH(K_SCAN, (k_scan<<<blocks(d.ncells / 16, 8), 256, 0, s>>>(d)));
+            LAUNCH(K_SCAN, (k_scan<<<blocks(d.ncells / 16, 8), 256, 0, s>>>(d)));  // 8 warps, one 4x4 block each
         LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));
         LAUNCH(K_READY, (k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask)));
         LAUNCH(K_SORT_HIST, (k_sort_hist<<<c->ntiles_sort, 256, 0, s>>>(d, c->sort_passes_max)));

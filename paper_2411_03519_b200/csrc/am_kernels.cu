@@ -350,83 +350,177 @@ __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
 }
 
 // ---------------------------------------------------------------------------------
-// k_scan: warp-cooperative time-dilated neighbour scan.  One warp per 4x4-cell block
-// (Morton-contiguous records); the block's agents are taken 32 at a time ("chunk",
-// one agent per lane) and share ONE traversal, pruned against the chunk's bounding
-// box and maximum step, so every cell-table / pyramid / record load is a coalesced
-// or broadcast warp load and the per-lane work is a SIMD loop over candidates.
+// k_scan: warp-cooperative time-dilated neighbour scan.
+//
+// One warp per 4x4-cell block (its records are Morton-contiguous).  The block's agents
+// are taken 32 at a time (a "chunk") and share ONE traversal, pruned against the
+// chunk's bounding box and maximum step.  The traversal only collects candidate cells
+// (lane-parallel tests + ballot compaction into a per-warp shared-memory list); full
+// lists are flushed by loading the cells' records into shared memory and testing the
+// (agent x candidate) pairs with every lane busy -- lane l owns agent l % na and
+// candidate l / na of each group, so no per-pair shuffles are needed.
 //   near phase: cells within box distance R_c = r_p + v of the chunk box: coupling
-//               unions, digests, blocking tests;
-//   far phase:  only lanes not yet blocked; cells beyond R_c inside the disk of
-//               radius R_b(max_step - W), walked through the 16x16 and 4x4 min-step
-//               pyramid; a block with min step m is skipped if m >= max step or its
-//               box distance to the chunk box exceeds R_b(max step - m) (exact: no
+//               unions, perception digests, blocking tests;
+//   far phase:  agents not yet blocked and ahead of W; cells beyond R_c inside the disk
+//               of radius R_b(max step - W), walked through the 16x16 / 4x4 min-step
+//               pyramid; a block with min step m is skipped if m >= max step or its box
+//               distance to the chunk box exceeds R_b(max step - m) (exact pruning: no
 //               agent inside can block any agent of the chunk).
-struct Lane {
-    int ax, ay, as;
-    uint32_t aid;
-    bool valid, blocked;
-    unsigned long long dig;
+constexpr int kScanWarps = 8;
+constexpr int kCellList = 64;     // pending candidate cells per warp
+constexpr int kCandBuf = 128;     // candidate records staged per flush
+
+struct ScanSmem {
+    int4 arec[32];                // the phase's agents (records)
+    int4 crec[kCandBuf];          // candidate records
+    int cstart[kCellList];        // pending cells: first record, count, exclusive prefix
+    int ccount[kCellList];
+    int cpref[kCellList];
+    unsigned long long dig[32];
 };
 
-// test the lane's agent against the records [beg, beg+cnt) of one cell
-template <bool kNear>
-__device__ __forceinline__ void scan_records(const Dev& d, Lane& L, int beg, int cnt, uint32_t Rc,
-                                             uint32_t& ncand)
+// R_b(lag)^2 in 32-bit arithmetic: lag >= 1, clamped as rb_radius
+__device__ __forceinline__ uint32_t rb2(int lag, int v, int r_p, int lagcap)
 {
-    const int lane = threadIdx.x & 31;
-    ncand += (uint32_t)cnt;
-    for (int j0 = 0; j0 < cnt; j0 += 32) {
-        int4 mine = make_int4(0, 0, 0, 0);
-        if (j0 + lane < cnt) mine = d.rec[beg + j0 + lane];
-        const int m = min(32, cnt - j0);
-        for (int t = 0; t < m; t++) {
-            const int bxy = __shfl_sync(0xFFFFFFFFu, mine.x, t);
-            const int bs = __shfl_sync(0xFFFFFFFFu, mine.y, t);
-            const uint32_t bid = (uint32_t)__shfl_sync(0xFFFFFFFFu, mine.z, t);
-            if (!L.valid || bid == L.aid) continue;
-            const int dx = (bxy & 0xFFFF) - L.ax, dy = (bxy >> 16) - L.ay;
-            if (kNear && bs == L.as) {
-                if (within(dx, dy, Rc, d.metric)) {
-                    if (L.aid < bid) uf_unite(d.parent, L.aid, bid);
-                    if ((d.flags & AM_DIGEST) && within(dx, dy, (uint32_t)d.r_p, d.metric))
-                        L.dig += digest_term(bid, dx, dy);
-                }
-            } else if (!L.blocked && bs < L.as) {
-                if (within(dx, dy, rb_radius((long long)L.as - bs, d.v, d.r_p), d.metric)) L.blocked = true;
-            }
-        }
-    }
+    const uint32_t R = min((uint32_t)min(lag, lagcap) * (uint32_t)v + (uint32_t)(v + r_p), kRClamp);
+    return R * R;
 }
 
-__global__ void __launch_bounds__(256, 1) k_scan(Dev d)
+__device__ __forceinline__ bool within2(int dx, int dy, uint32_t R2, uint32_t R, int metric)
+{
+    if (metric == AM_METRIC_LINF) return (uint32_t)abs(dx) <= R && (uint32_t)abs(dy) <= R;
+    return (uint32_t)(dx * dx) + (uint32_t)(dy * dy) <= R2;
+}
+
+// Test the phase's na agents (sm.arec) against the pending cells' records.  Returns the
+// per-agent blocked mask (bit a).  kNear: also coupling unions and digests.
+template <bool kNear>
+__device__ __forceinline__ unsigned flush_cells(const Dev& d, ScanSmem& sm, int nc, int na, unsigned blocked,
+                                                unsigned long long& ncand)
 {
     const int lane = threadIdx.x & 31;
-    const int blk = blockIdx.x * 8 + (threadIdx.x >> 5);   // 4x4-cell block (key >> 4)
+    // exclusive prefix of the counts (nc <= kCellList = 64: two 32-lane scans)
+    int total = 0;
+    for (int c0 = 0; c0 < nc; c0 += 32) {
+        const int k = c0 + lane;
+        const int v = k < nc ? sm.ccount[k] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (k < nc) sm.cpref[k] = total + incl - v;
+        total += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+    __syncwarp();
+    ncand += (unsigned long long)total;
+    const int cpi = 32 / na;                       // candidates per iteration
+    const int my_a = lane % na, my_c = lane / na;  // this lane's agent / candidate slot
+    const int4 A = sm.arec[my_a];
+    const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+    const uint32_t aid = (uint32_t)A.z;
+    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const uint32_t Rc2 = Rc * Rc, Rp2 = (uint32_t)d.r_p * (uint32_t)d.r_p;
+    for (int f0 = 0; f0 < total; f0 += kCandBuf) {
+        const int nb = min(kCandBuf, total - f0);
+        // stage the records of flat candidates [f0, f0+nb)
+        for (int j = lane; j < nb; j += 32) {
+            const int f = f0 + j;
+            int lo = 0, hi = nc - 1;               // last cell with cpref <= f
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (sm.cpref[mid] <= f) lo = mid; else hi = mid - 1;
+            }
+            sm.crec[j] = d.rec[sm.cstart[lo] + (f - sm.cpref[lo])];
+        }
+        __syncwarp();
+        bool hit = false;
+        unsigned long long dig = 0;
+        if (my_c < cpi && my_a < na) {
+            const bool mine_blocked = (blocked >> my_a) & 1u;
+            for (int c = my_c; c < nb; c += cpi) {
+                const int4 B = sm.crec[c];
+                const uint32_t bid = (uint32_t)B.z;
+                if (bid == aid) continue;
+                const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                if (kNear && B.y == as) {
+                    if (within2(dx, dy, Rc2, Rc, d.metric)) {
+                        if (aid < bid) uf_unite(d.parent, aid, bid);
+                        if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
+                            dig += digest_term(bid, dx, dy);
+                    }
+                } else if (B.y < as && !mine_blocked && !hit) {
+                    const int lag = as - B.y;
+                    const uint32_t R2 = rb2(lag, d.v, d.r_p, lagcap);
+                    const uint32_t R = min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
+                    hit = within2(dx, dy, R2, R, d.metric);
+                }
+            }
+        }
+        // fold the lanes' hits onto their agents
+        const unsigned hm = __ballot_sync(0xFFFFFFFFu, hit);
+        for (int k = 0; k < cpi; k++) blocked |= (hm >> (k * na)) & ((na == 32) ? 0xFFFFFFFFu : ((1u << na) - 1u));
+        if (kNear && (d.flags & AM_DIGEST) && dig) atomicAdd(&sm.dig[my_a], dig);
+        __syncwarp();
+        if (!kNear && __popc(blocked) == na) break;    // every far agent blocked
+    }
+    return blocked;
+}
+
+// append a lane's candidate cell to the pending list; flush when full
+template <bool kNear>
+__device__ __forceinline__ void add_cells(const Dev& d, ScanSmem& sm, bool take, int cb, int cc, int& nc,
+                                          int na, unsigned& blocked, unsigned long long& ncand)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
+    if (!m) return;
+    const int cnt = __popc(m);
+    if (nc + cnt > kCellList) {
+        blocked = flush_cells<kNear>(d, sm, nc, na, blocked, ncand);
+        nc = 0;
+    }
+    if (take) {
+        const int pos = nc + __popc(m & ((1u << lane) - 1u));
+        sm.cstart[pos] = cb;
+        sm.ccount[pos] = cc;
+    }
+    __syncwarp();
+    nc += cnt;
+}
+
+__global__ void __launch_bounds__(256, 3) k_scan(Dev d)
+{
+    __shared__ ScanSmem s_all[kScanWarps];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    ScanSmem& sm = s_all[wq];
+    const int blk = blockIdx.x * kScanWarps + wq;          // 4x4-cell block (key >> 4)
     if (blk >= (d.ncells >> 4)) return;                     // warp-uniform
     const int beg = d.ctab[blk * 16].x, end = d.ctab[blk * 16 + 16].x;
     if (beg == end) return;
     const int W = d.ctl->W;
     const int cl = d.clog, G = 1 << d.glog;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-    uint32_t ncells = 0, ncand = 0, np2 = 0, nb2 = 0, nb1 = 0;
+    unsigned long long ncand = 0;
+    uint32_t ncells = 0, np2 = 0, nb2 = 0, nb1 = 0;
     for (int base = beg; base < end; base += 32) {
-        Lane L;
         const int r = base + lane;
-        L.valid = r < end;
-        const int4 A = L.valid ? d.rec[r] : make_int4(0, INT_MIN, -1, 0);
-        L.ax = A.x & 0xFFFF;
-        L.ay = A.x >> 16;
-        L.as = A.y;
-        L.aid = (uint32_t)A.z;
-        L.blocked = false;
-        L.dig = 0;
-        // chunk bounding box and max step
-        const int x0 = __reduce_min_sync(0xFFFFFFFFu, L.valid ? L.ax : INT_MAX);
-        const int x1 = __reduce_max_sync(0xFFFFFFFFu, L.valid ? L.ax : INT_MIN);
-        const int y0 = __reduce_min_sync(0xFFFFFFFFu, L.valid ? L.ay : INT_MAX);
-        const int y1 = __reduce_max_sync(0xFFFFFFFFu, L.valid ? L.ay : INT_MIN);
-        const int smax = __reduce_max_sync(0xFFFFFFFFu, L.valid ? L.as : INT_MIN);
+        const bool valid = r < end;
+        const int4 A = valid ? d.rec[r] : make_int4(0, INT_MIN, -1, 0);
+        const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+        const int na = min(32, end - base);
+        sm.arec[lane] = A;
+        sm.dig[lane] = 0;
+        __syncwarp();
+        const int x0 = __reduce_min_sync(0xFFFFFFFFu, valid ? ax : INT_MAX);
+        const int x1 = __reduce_max_sync(0xFFFFFFFFu, valid ? ax : INT_MIN);
+        const int y0 = __reduce_min_sync(0xFFFFFFFFu, valid ? ay : INT_MAX);
+        const int y1 = __reduce_max_sync(0xFFFFFFFFu, valid ? ay : INT_MIN);
+        const int smax = __reduce_max_sync(0xFFFFFFFFu, valid ? as : INT_MIN);
+        unsigned blocked = 0;     // bit a: chunk agent a is blocked
+        int nc = 0;
         // ---- near phase
         {
             const int cx0 = max(0, (x0 - (int)Rc) >> cl), cx1 = min(G - 1, (x1 + (int)Rc) >> cl);
@@ -448,37 +542,42 @@ __global__ void __launch_bounds__(256, 1) k_scan(Dev d)
                     }
                     ncells++;
                 }
-                unsigned todo = __ballot_sync(0xFFFFFFFFu, take);
-                while (todo) {
-                    const int src = __ffs(todo) - 1;
-                    todo &= todo - 1;
-                    const int b0 = __shfl_sync(0xFFFFFFFFu, cb, src), n0 = __shfl_sync(0xFFFFFFFFu, cc, src);
-                    scan_records<true>(d, L, b0, n0, Rc, ncand);
-                }
+                add_cells<true>(d, sm, take, cb, cc, nc, na, blocked, ncand);
             }
+            if (nc) blocked = flush_cells<true>(d, sm, nc, na, blocked, ncand);
+            nc = 0;
         }
-        // ---- far phase (lanes not blocked yet)
-        const bool open = L.valid && !L.blocked && L.as > W;
-        const int fmax = __reduce_max_sync(0xFFFFFFFFu, open ? L.as : INT_MIN);
-        if (fmax > W) {
+        const bool my_blocked = valid && ((blocked >> lane) & 1u);
+        // ---- far phase: agents not blocked yet and ahead of the watermark
+        const bool open = valid && !my_blocked && as > W;
+        const unsigned om = __ballot_sync(0xFFFFFFFFu, open);
+        bool far_blocked = false;
+        if (om) {
+            const int nf = __popc(om);
             np2 += open;
-            const int fx0 = __reduce_min_sync(0xFFFFFFFFu, open ? L.ax : INT_MAX);
-            const int fx1 = __reduce_max_sync(0xFFFFFFFFu, open ? L.ax : INT_MIN);
-            const int fy0 = __reduce_min_sync(0xFFFFFFFFu, open ? L.ay : INT_MAX);
-            const int fy1 = __reduce_max_sync(0xFFFFFFFFu, open ? L.ay : INT_MIN);
+            // compact the open agents into arec[0..nf)
+            const int4 Amine = A;
+            __syncwarp();
+            if (open) sm.arec[__popc(om & ((1u << lane) - 1u))] = Amine;
+            __syncwarp();
+            const int fmax = __reduce_max_sync(0xFFFFFFFFu, open ? as : INT_MIN);
+            const int fx0 = __reduce_min_sync(0xFFFFFFFFu, open ? ax : INT_MAX);
+            const int fx1 = __reduce_max_sync(0xFFFFFFFFu, open ? ax : INT_MIN);
+            const int fy0 = __reduce_min_sync(0xFFFFFFFFu, open ? ay : INT_MAX);
+            const int fy1 = __reduce_max_sync(0xFFFFFFFFu, open ? ay : INT_MIN);
             const int R = (int)rb_radius((long long)fmax - W, d.v, d.r_p);
-            const int l2 = cl + 4, G2 = G >> 4;
+            const int l2 = cl + 4, l1 = cl + 2, G2 = G >> 4;
             const int bx0 = max(0, (fx0 - R) >> l2), bx1 = min(G2 - 1, (fx1 + R) >> l2);
             const int by0 = max(0, (fy0 - R) >> l2), by1 = min(G2 - 1, (fy1 + R) >> l2);
             const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);
-            bool done = false;
-            for (int q0 = 0; q0 < nb && !done; q0 += 32) {
-                const int q = q0 + lane;
+            unsigned fb = 0;      // bit j: open agent j blocked
+            for (int q0 = 0; q0 < nb && __popc(fb) < nf; q0 += 32) {
+                const int qq = q0 + lane;
                 bool keep2 = false;
                 int bx = 0, by = 0;
-                if (q < nb) {
-                    bx = bx0 + q % nbx;
-                    by = by0 + q / nbx;
+                if (qq < nb) {
+                    bx = bx0 + qq % nbx;
+                    by = by0 + qq / nbx;
                     const int m2 = d.lmin2[morton(bx, by)];
                     keep2 = m2 < fmax &&
                             box_dist_within(fx0, fy0, fx1, fy1, bx << l2, by << l2, ((bx + 1) << l2) - 1,
@@ -487,14 +586,12 @@ __global__ void __launch_bounds__(256, 1) k_scan(Dev d)
                     nb2++;
                 }
                 unsigned todo2 = __ballot_sync(0xFFFFFFFFu, keep2);
-                while (todo2 && !done) {
+                while (todo2 && __popc(fb) < nf) {
                     const int src2 = __ffs(todo2) - 1;
                     todo2 &= todo2 - 1;
                     const int BX = __shfl_sync(0xFFFFFFFFu, bx, src2), BY = __shfl_sync(0xFFFFFFFFu, by, src2);
-                    // 16 4x4-cell blocks of this 16x16 block: lanes 0..15
-                    const int l1 = cl + 2;
-                    const int qx = BX * 4 + (lane & 3), qy = BY * 4 + ((lane >> 2) & 3);
                     bool keep1 = false;
+                    const int qx = BX * 4 + (lane & 3), qy = BY * 4 + ((lane >> 2) & 3);
                     if (lane < 16) {
                         const int m1 = d.lmin1[morton(qx, qy)];
                         keep1 = m1 < fmax &&
@@ -504,14 +601,21 @@ __global__ void __launch_bounds__(256, 1) k_scan(Dev d)
                         nb1++;
                     }
                     unsigned todo1 = __ballot_sync(0xFFFFFFFFu, keep1);
-                    while (todo1 && !done) {
-                        const int src1 = __ffs(todo1) - 1;
+                    while (todo1 && __popc(fb) < nf) {
+                        // two 4x4 blocks per iteration: lanes 0-15 the first, 16-31 the second
+                        const int s1a = __ffs(todo1) - 1;
                         todo1 &= todo1 - 1;
-                        const int QX = __shfl_sync(0xFFFFFFFFu, qx, src1), QY = __shfl_sync(0xFFFFFFFFu, qy, src1);
+                        int s1b = -1;
+                        if (todo1) {
+                            s1b = __ffs(todo1) - 1;
+                            todo1 &= todo1 - 1;
+                        }
+                        const int srcb = (lane < 16 || s1b < 0) ? s1a : s1b;
+                        const int QX = __shfl_sync(0xFFFFFFFFu, qx, srcb), QY = __shfl_sync(0xFFFFFFFFu, qy, srcb);
                         const int cx = QX * 4 + (lane & 3), cy = QY * 4 + ((lane >> 2) & 3);
                         int cb = 0, cc = 0;
                         bool take = false;
-                        if (lane < 16) {
+                        if (lane < 16 || s1b >= 0) {
                             const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
                             // near-phase cells were tested completely already
                             if (!box_dist_within(x0, y0, x1, y1, X0, Y0, X1, Y1, Rc, d.metric)) {
@@ -527,34 +631,32 @@ __global__ void __launch_bounds__(256, 1) k_scan(Dev d)
                             }
                             ncells++;
                         }
-                        unsigned todo0 = __ballot_sync(0xFFFFFFFFu, take);
-                        while (todo0) {
-                            const int src0 = __ffs(todo0) - 1;
-                            todo0 &= todo0 - 1;
-                            const int b0 = __shfl_sync(0xFFFFFFFFu, cb, src0), n0 = __shfl_sync(0xFFFFFFFFu, cc, src0);
-                            scan_records<false>(d, L, b0, n0, Rc, ncand);
-                        }
-                        done = __all_sync(0xFFFFFFFFu, !open || L.blocked);
+                        add_cells<false>(d, sm, take, cb, cc, nc, nf, fb, ncand);
                     }
                 }
             }
+            if (nc && __popc(fb) < nf) fb = flush_cells<false>(d, sm, nc, nf, fb, ncand);
+            nc = 0;
+            if (open) far_blocked = (fb >> __popc(om & ((1u << lane) - 1u))) & 1u;
         }
-        if (L.valid) {
-            d.blk8[r] = L.blocked;
-            if (d.flags & AM_DIGEST) d.digest[L.aid] = L.dig;
+        const bool blk = my_blocked || far_blocked;
+        if (valid) {
+            d.blk8[r] = blk;
+            if (d.flags & AM_DIGEST) d.digest[A.z] = sm.dig[lane];
         }
+        __syncwarp();
         if (d.flags & AM_STATS) {
-            const unsigned nbk = __popc(__ballot_sync(0xFFFFFFFFu, L.valid && L.blocked));
+            const unsigned nbk = __popc(__ballot_sync(0xFFFFFFFFu, valid && blk));
             if (lane == 0) atomicAdd(&d.ctl->st_blocked, (unsigned long long)nbk);
         }
     }
     if (d.flags & AM_STATS) {
-        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = ncand;  // ncand is warp-uniform
+        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells);
         const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, np2), c3 = __reduce_add_sync(0xFFFFFFFFu, nb2);
         const unsigned c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
         if (lane == 0) {
             atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
-            atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
+            atomicAdd(&d.ctl->st_cand, ncand);                 // warp-uniform
             atomicAdd(&d.ctl->st_p2, (unsigned long long)c2);
             atomicAdd(&d.ctl->st_b2, (unsigned long long)c3);
             atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
