@@ -63,6 +63,8 @@ def algorithmic_bytes(kernel: str, s: dict) -> float:
         "k_disp_b": 52.0 * r,
         # read status 1 (+ tcommit 8 for RUNNING); commit: pos/step/traj r+w
         "k_commit": 1.0 * n + 8.0 * s["n_running"],
+        # read edges 8 per coupled pair (~0.6 per agent) + parent words
+        "k_union": 12.0 * 0.6 * a,
     }
     return table.get(kernel, 0.0)
 
@@ -209,7 +211,7 @@ def run_ours(args, w, lm):
     rep = Replay.from_workload(w, lm, device=dev)
     stream = torch.cuda.ExternalStream(rep.stream_ptr(), device=dev)
     names = ["k_ingest", "k_bin", "k_cells", "k_scatter", "k_scan", "k_finalize", "k_ready",
-             "k_sort_hist", "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b"]
+             "k_sort_hist", "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b", "k_union"]
     ncells = None
 
     # pre-roll to steady state (untimed)
@@ -310,7 +312,7 @@ def run_ours(args, w, lm):
     # ---- roofline of the dominant kernel
     L = rep.tracker.L
     stats = {"n": n, "n_active": statistics.mean(st_active), "n_ready": statistics.mean(st_ready),
-             "n_running": statistics.mean(st_running), "passes": rep.tracker.L.am_launches_per_round(rep.tracker.ctx) - 9,
+             "n_running": statistics.mean(st_running), "passes": rep.tracker.L.am_launches_per_round(rep.tracker.ctx) - 10,
              "ncells": 0}
     # cell count of the binned path: (workspace layout) -- from the config the library chose
     cell = rep.tracker.stats()["cell"]

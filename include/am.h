@@ -77,6 +77,8 @@ extern "C" {
 #define AM_FORCE_SMALL  0x20u/* always use the fused per-simulation kernel (<=1024/sim)    */
 #define AM_STATS        0x40u/* count scan work (cells, candidate pairs) for am_scan_stats  */
 #define AM_SCAN_THREAD  0x80u/* one thread per agent neighbour scan (ablation baseline)    */
+#define AM_DBG_SKIP_NEAR 0x1000u /* PROFILING ONLY: skip the scan's near phase (wrong results) */
+#define AM_DBG_SKIP_FAR  0x2000u /* PROFILING ONLY: skip the scan's far phase (wrong results)  */
 
 typedef struct am_ctx am_ctx;                 /* opaque */
 

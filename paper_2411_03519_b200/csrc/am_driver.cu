@@ -209,6 +209,7 @@ struct am_replay {
     cudaStream_t user_stream = nullptr;
     cudaGraphExec_t g1 = nullptr, g8 = nullptr;
     unsigned graph_prof = 0;            // profiling mask the graphs were captured with
+    uint32_t graph_flags = 0;           // context flags the graphs were captured with
     long long* h_buf = nullptr;         // pinned: dispatched, liveness
 };
 
@@ -361,11 +362,12 @@ static int finish_check(am_replay* rp, int64_t* active)
 static int ensure_graphs(am_replay* rp)
 {
     const unsigned pm = rp->ctx->prof.on ? rp->ctx->prof.mask : 0u;
-    if (pm != rp->graph_prof) {  // events are baked into the graphs at capture
+    if (pm != rp->graph_prof || rp->ctx->d.flags != rp->graph_flags) {  // baked in at capture
         if (rp->g1) cudaGraphExecDestroy(rp->g1);
         if (rp->g8) cudaGraphExecDestroy(rp->g8);
         rp->g1 = rp->g8 = nullptr;
         rp->graph_prof = pm;
+        rp->graph_flags = rp->ctx->d.flags;
     }
     int rc;
     if (!rp->g8 && (rc = build_graph(rp, 8, &rp->g8))) return rc;

@@ -15,6 +15,7 @@ __global__ void k_scatter(Dev d);
 __global__ void k_scan(Dev d);
 __global__ void k_scan_thread(Dev d);
 __global__ void k_finalize(Dev d);
+__global__ void k_union(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
 __global__ void k_sort_pass(Dev d, int pass, int32_t* order);
@@ -70,7 +71,7 @@ static inline unsigned blocks(long long n, int t) { return (unsigned)std::max(1L
 
 static const char* kKernelNames[K_COUNT] = {
     "k_ingest", "k_bin", "k_cells", "k_scatter", "k_scan", "k_finalize", "k_ready", "k_sort_hist",
-    "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b"};
+    "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b", "k_union"};
 
 void am_prof_begin(am_ctx* c, int id)
 {
@@ -139,7 +140,7 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 2 : 9 + c->sort_passes_max;   // incl. k_round_begin
+    return c->path == 0 ? 2 : 10 + c->sort_passes_max;   // incl. k_round_begin, k_union
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -250,7 +251,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
     size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
-           o_tsort = 0, o_gh = 0, o_gs = 0;
+           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0;
     const size_t NC = (size_t)d.ncells;
     if (x->path == 1) {
         o_key = take(4 * N); o_rank = take(4 * N);
@@ -262,6 +263,8 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_tc = take(8 * (size_t)x->ntiles_cells); o_tr = take(8 * (size_t)x->ntiles_ready);
         o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * 256);
         o_gh = take(4 * kMaxSortPasses * 256); o_gs = take(4 * kMaxSortPasses * 256);
+        d.edge_cap = (int)std::max<size_t>(256, (2 * N + kEdgeStripes - 1) / kEdgeStripes);
+        o_edges = take(8 * (size_t)kEdgeStripes * d.edge_cap); o_ectr = take(4 * kEdgeStripes);
     }
     x->ws_bytes = off;
     cudaError_t e = cudaMalloc(&x->ws, off);
@@ -287,6 +290,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.tiles_c = (unsigned long long*)(b + o_tc); d.tiles_r = (unsigned long long*)(b + o_tr);
         d.tiles_sort = (unsigned long long*)(b + o_tsort);
         d.ghist = (uint32_t*)(b + o_gh); d.gstart = (uint32_t*)(b + o_gs);
+        d.edges = (uint2*)(b + o_edges); d.edge_ctr = (uint32_t*)(b + o_ectr);
     }
     // initial contents: everything zero except the min-step table
     e = cudaMemsetAsync(x->ws, 0, off, x->stream);
@@ -405,7 +409,10 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         if (d.flags & AM_SCAN_THREAD)
             LAUNCH(K_SCAN, (k_scan_thread<<<nb, 256, 0, s>>>(d)));
         else
+        {
             LAUNCH(K_SCAN, (k_scan<<<blocks(d.ncells / 16, 8), 256, 0, s>>>(d)));  // 8 warps, one 4x4 block each
+            LAUNCH(K_UNION, (k_union<<<blocks((long long)kEdgeStripes * d.edge_cap, 256), 256, 0, s>>>(d)));
+        }
         LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));
         LAUNCH(K_READY, (k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask)));
         LAUNCH(K_SORT_HIST, (k_sort_hist<<<c->ntiles_sort, 256, 0, s>>>(d, c->sort_passes_max)));

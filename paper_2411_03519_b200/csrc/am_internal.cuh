@@ -18,7 +18,8 @@ constexpr int kCellsPerTile = 4096;       // cell-table scan tile (256 threads x
 constexpr int kReadyTile = 2048;          // ready compaction tile (256 threads x 8 agents)
 constexpr int kSortTile = 2048;           // radix pass tile (256 threads x 8 keys)
 constexpr int kMaxSortPasses = 8;
-constexpr int kIngestItems = 4;          // agents per thread in k_ingest / k_commit
+constexpr int kIngestItems = 4;
+constexpr int kEdgeStripes = 64;          // global coupling-edge lists          // agents per thread in k_ingest / k_commit
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
 constexpr uint32_t kRClamp = 46340u;      // >= every distance on a 32768^2 map; R^2 < 2^31
 
@@ -75,6 +76,9 @@ struct Dev {
     int32_t* lmin2;        // [ncells/256] min step per 16x16-cell block
     int4* rec;             // [n] sorted records {x | y<<16, step, id, status}
     uint8_t* blk8;         // [n] blocked flag per sorted record
+    uint2* edges;          // [kEdgeStripes][edge_cap] coupling edges (a < b)
+    uint32_t* edge_ctr;    // [kEdgeStripes]
+    int32_t edge_cap;      // per stripe
     uint32_t* parent;      // [n] union-find forest in id space (root = min id)
     uint8_t* bad;          // [n] cluster (root) has a blocked or RUNNING member
     int32_t* labels;       // [n]
@@ -96,7 +100,7 @@ struct Dev {
 namespace am {
 enum KernelId : int {
     K_INGEST = 0, K_BIN, K_CELLS, K_SCATTER, K_SCAN, K_FINALIZE, K_READY, K_SORT_HIST, K_SORT_PASS,
-    K_SMALL, K_COMMIT, K_DISP_A, K_DISP_B, K_COUNT
+    K_SMALL, K_COMMIT, K_DISP_A, K_DISP_B, K_UNION, K_COUNT
 };
 struct Prof {
     bool on = false;

@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
     d.rank[i] = rank;
     d.parent[i] = (uint32_t)i;
     d.bad[i] = 0;
+    if (i < kEdgeStripes) d.edge_ctr[i] = 0;
 }
 
 // k_cells: exclusive scan of the cell counts in Morton order -> ctab{start, min};
@@ -369,6 +370,7 @@ __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
 constexpr int kScanWarps = 8;
 constexpr int kCellList = 64;     // pending candidate cells per warp
 constexpr int kCandBuf = 128;     // candidate records staged per flush
+constexpr int kEdgeStage = 128;   // coupling edges staged per warp
 
 struct ScanSmem {
     int4 arec[32];                // the phase's agents (records)
@@ -377,7 +379,40 @@ struct ScanSmem {
     int ccount[kCellList];
     int cpref[kCellList];
     unsigned long long dig[32];
+    uint2 edges[kEdgeStage];      // coupling edges staged for the edge list
+    int ne;
 };
+
+// Coupling edges found by the scan are not united in place (a union chases parent
+// pointers through L2 and would stall the 31 other lanes of the warp): they are
+// staged per warp and appended to one of kEdgeStripes global edge lists (one atomic
+// per staged batch); k_union unites them with one thread per edge.  An edge that does
+// not fit is united in place (correct, just slower).
+__device__ __forceinline__ void stage_edge(const Dev& d, ScanSmem& sm, uint32_t a, uint32_t b)
+{
+    const int pos = atomicAdd(&sm.ne, 1);
+    if (pos < kEdgeStage) sm.edges[pos] = make_uint2(a, b);
+    else uf_unite(d.parent, a, b);
+}
+__device__ __forceinline__ void flush_edges(const Dev& d, ScanSmem& sm)
+{
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    const int ne = min(sm.ne, kEdgeStage);
+    if (ne == 0) return;
+    const int stripe = (blockIdx.x * kScanWarps + (threadIdx.x >> 5)) & (kEdgeStripes - 1);
+    int base = 0;
+    if (lane == 0) base = (int)atomicAdd(d.edge_ctr + stripe, (unsigned)ne);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    for (int k = lane; k < ne; k += 32) {
+        const uint2 e = sm.edges[k];
+        if (base + k < d.edge_cap) d.edges[(size_t)stripe * d.edge_cap + base + k] = e;
+        else uf_unite(d.parent, e.x, e.y);
+    }
+    __syncwarp();
+    if (lane == 0) sm.ne = 0;
+    __syncwarp();
+}
 
 // R_b(lag)^2 in 32-bit arithmetic: lag >= 1, clamped as rb_radius
 __device__ __forceinline__ uint32_t rb2(int lag, int v, int r_p, int lagcap)
@@ -447,7 +482,7 @@ __device__ __forceinline__ unsigned flush_cells(const Dev& d, ScanSmem& sm, int 
                 const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
                 if (kNear && B.y == as) {
                     if (within2(dx, dy, Rc2, Rc, d.metric)) {
-                        if (aid < bid) uf_unite(d.parent, aid, bid);
+                        if (aid < bid) stage_edge(d, sm, aid, bid);
                         if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
                             dig += digest_term(bid, dx, dy);
                     }
@@ -458,6 +493,10 @@ __device__ __forceinline__ unsigned flush_cells(const Dev& d, ScanSmem& sm, int 
                     hit = within2(dx, dy, R2, R, d.metric);
                 }
             }
+        }
+        if (kNear) {
+            __syncwarp();
+            if (sm.ne >= kEdgeStage / 2) flush_edges(d, sm);
         }
         // fold the lanes' hits onto their agents
         const unsigned hm = __ballot_sync(0xFFFFFFFFu, hit);
@@ -513,43 +552,59 @@ __global__ void __launch_bounds__(256, 3) k_scan(Dev d)
         const int na = min(32, end - base);
         sm.arec[lane] = A;
         sm.dig[lane] = 0;
+        if (lane == 0) sm.ne = 0;
         __syncwarp();
         const int x0 = __reduce_min_sync(0xFFFFFFFFu, valid ? ax : INT_MAX);
         const int x1 = __reduce_max_sync(0xFFFFFFFFu, valid ? ax : INT_MIN);
         const int y0 = __reduce_min_sync(0xFFFFFFFFu, valid ? ay : INT_MAX);
         const int y1 = __reduce_max_sync(0xFFFFFFFFu, valid ? ay : INT_MIN);
-        const int smax = __reduce_max_sync(0xFFFFFFFFu, valid ? as : INT_MIN);
-        unsigned blocked = 0;     // bit a: chunk agent a is blocked
-        int nc = 0;
-        // ---- near phase
-        {
-            const int cx0 = max(0, (x0 - (int)Rc) >> cl), cx1 = min(G - 1, (x1 + (int)Rc) >> cl);
-            const int cy0 = max(0, (y0 - (int)Rc) >> cl), cy1 = min(G - 1, (y1 + (int)Rc) >> cl);
-            const int nx = cx1 - cx0 + 1, ncell = nx * (cy1 - cy0 + 1);
-            for (int c0 = 0; c0 < ncell; c0 += 32) {
-                const int k = c0 + lane;
-                int cb = 0, cc = 0;
-                bool take = false;
-                if (k < ncell) {
-                    const int cx = cx0 + k % nx, cy = cy0 + k / nx;
-                    if (box_dist_within(x0, y0, x1, y1, cx << cl, cy << cl, ((cx + 1) << cl) - 1,
-                                        ((cy + 1) << cl) - 1, Rc, d.metric)) {
-                        const uint32_t key = morton(cx, cy);
-                        const int2 e = d.ctab[key];
-                        cb = e.x;
-                        cc = d.ctab[key + 1].x - e.x;
-                        take = cc > 0 && e.y <= smax;
-                    }
+        // ---- near phase, one lane per agent: the (at most 2x2 when cell >= R_c) cells
+        // within box distance R_c of the agent; lanes of one cell read the same entries
+        bool nblk = false;
+        if (valid && !(d.flags & AM_DBG_SKIP_NEAR)) {
+            const uint32_t aid = (uint32_t)A.z;
+            const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+            const uint32_t Rc2 = Rc * Rc, Rp2 = (uint32_t)d.r_p * (uint32_t)d.r_p;
+            unsigned long long dig = 0;
+            const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
+            const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
+            for (int cy = cy0; cy <= cy1; cy++)
+                for (int cx = cx0; cx <= cx1; cx++) {
+                    if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1,
+                                    Rc, d.metric))
+                        continue;
+                    const uint32_t key = morton(cx, cy);
+                    const int2 e = d.ctab[key];
                     ncells++;
+                    if (e.y > as) continue;
+                    const int e1 = d.ctab[key + 1].x;
+                    ncand += (unsigned long long)(e1 - e.x);
+                    for (int b = e.x; b < e1; b++) {
+                        const int4 B = d.rec[b];
+                        const uint32_t bid = (uint32_t)B.z;
+                        if (bid == aid) continue;
+                        const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                        if (B.y == as) {
+                            if (within2(dx, dy, Rc2, Rc, d.metric)) {
+                                if (aid < bid) stage_edge(d, sm, aid, bid);
+                                if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
+                                    dig += digest_term(bid, dx, dy);
+                            }
+                        } else if (!nblk && B.y < as) {
+                            const int lag = as - B.y;
+                            const uint32_t R = min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
+                            nblk = within2(dx, dy, R * R, R, d.metric);
+                        }
+                    }
                 }
-                add_cells<true>(d, sm, take, cb, cc, nc, na, blocked, ncand);
-            }
-            if (nc) blocked = flush_cells<true>(d, sm, nc, na, blocked, ncand);
-            nc = 0;
+            sm.dig[lane] = dig;
         }
+        flush_edges(d, sm);
+        unsigned blocked = __ballot_sync(0xFFFFFFFFu, nblk);
+        int nc = 0;
         const bool my_blocked = valid && ((blocked >> lane) & 1u);
         // ---- far phase: agents not blocked yet and ahead of the watermark
-        const bool open = valid && !my_blocked && as > W;
+        const bool open = valid && !my_blocked && as > W && !(d.flags & AM_DBG_SKIP_FAR);
         const unsigned om = __ballot_sync(0xFFFFFFFFu, open);
         bool far_blocked = false;
         if (om) {
@@ -617,8 +672,9 @@ __global__ void __launch_bounds__(256, 3) k_scan(Dev d)
                         bool take = false;
                         if (lane < 16 || s1b >= 0) {
                             const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
-                            // near-phase cells were tested completely already
-                            if (!box_dist_within(x0, y0, x1, y1, X0, Y0, X1, Y1, Rc, d.metric)) {
+                            // (cells the near phase covered are re-tested for blocking only:
+                            // harmless, the per-agent near sets differ across the chunk)
+                            {
                                 const uint32_t key = morton(cx, cy);
                                 const int2 e = d.ctab[key];
                                 if (e.y < fmax &&
@@ -662,6 +718,19 @@ __global__ void __launch_bounds__(256, 3) k_scan(Dev d)
             atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
         }
     }
+}
+
+// k_union: unite the staged coupling edges, one thread per edge (ECL-CC style hooking
+// of the larger root under the smaller, so roots stay the minimum id).
+__global__ void __launch_bounds__(256) k_union(Dev d)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int stripe = (int)(t / d.edge_cap), k = (int)(t % d.edge_cap);
+    if (stripe >= kEdgeStripes) return;
+    const int ne = min((int)d.edge_ctr[stripe], d.edge_cap);
+    if (k >= ne) return;
+    const uint2 e = d.edges[(size_t)stripe * d.edge_cap + k];
+    uf_unite(d.parent, e.x, e.y);
 }
 
 // k_finalize: label = root of the agent's tree (= min id of its cluster, Q10);

@@ -26,18 +26,31 @@ def main():
     ap.add_argument("--stats", action="store_true")
     ap.add_argument("--prof", action="store_true")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--dbg", type=lambda v: int(v, 0), default=0, help="extra AM_* flag bits")
+    ap.add_argument("--scan-thread", action="store_true")
     a = ap.parse_args()
     w = amgen.config(a.workload, n=a.agents)
     lm = amgen.latency_model(w.profile)
     rep = Replay.from_workload(w, lm, stats=a.stats, cell=a.cell)
+    if a.dbg or a.scan_thread:
+        from paper_2411_03519_b200 import _lib
+        # applied after the pre-roll so the replay state stays valid
+        extra = a.dbg | (_lib.SCAN_THREAD if a.scan_thread else 0)
+    else:
+        extra = 0
     t0 = time.perf_counter()
     rep.run(a.preroll)
     t1 = time.perf_counter()
     print(f"preroll {a.preroll} rounds: {t1 - t0:.3f} s wall", flush=True)
     if a.stats:
         rep.tracker.scan_stats()
+    if extra:
+        L = rep.tracker.L
+        rep.tracker.flags |= extra
+        # graphs bake the flags: set them on the context and force a re-capture
+        L.am_set_flags(rep.tracker.ctx, rep.tracker.flags | 0x4 | 0x8)   # + DIGEST | ASYNC
     if a.prof:
-        rep.profile((1 << 13) - 1)
+        rep.profile((1 << 14) - 1)
     rows = []
     for k in range(a.rounds):
         rep.launch(1)
