@@ -48,8 +48,10 @@ def algorithmic_bytes(kernel: str, s: dict) -> float:
         "k_cells": 24.27 * c,
         # read key 4 + rank 4 + cell start 4 + pos 8 + step 4 + status 1; write record 16
         "k_scatter": 41.0 * a,
-        # read own record 16 + own cell entry 8; write blocked bit 0.125 + digest 8
-        "k_scan": 32.125 * a,
+        # near phase: read own record 16 + own cell entry 8; write blocked flag 1 + digest 8
+        "k_near": 33.0 * a,
+        # far phase: read own record 16 + blocked flag 1; write blocked flag 1
+        "k_scan": 18.0 * a,
         # read record 16 + blocked bit 0.125 + parent 4; write label 4
         "k_finalize": 24.125 * a,
         # read status 1 + label 4 + bad 1; write mask 1 + status 1; ready: step 4 + key/id 12
@@ -211,7 +213,7 @@ def run_ours(args, w, lm):
     rep = Replay.from_workload(w, lm, device=dev)
     stream = torch.cuda.ExternalStream(rep.stream_ptr(), device=dev)
     names = ["k_ingest", "k_bin", "k_cells", "k_scatter", "k_scan", "k_finalize", "k_ready",
-             "k_sort_hist", "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b", "k_union"]
+             "k_sort_hist", "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b", "k_union", "k_near"]
     ncells = None
 
     # pre-roll to steady state (untimed)
@@ -312,7 +314,7 @@ def run_ours(args, w, lm):
     # ---- roofline of the dominant kernel
     L = rep.tracker.L
     stats = {"n": n, "n_active": statistics.mean(st_active), "n_ready": statistics.mean(st_ready),
-             "n_running": statistics.mean(st_running), "passes": rep.tracker.L.am_launches_per_round(rep.tracker.ctx) - 10,
+             "n_running": statistics.mean(st_running), "passes": rep.tracker.L.am_launches_per_round(rep.tracker.ctx) - 11,
              "ncells": 0}
     # cell count of the binned path: (workspace layout) -- from the config the library chose
     cell = rep.tracker.stats()["cell"]

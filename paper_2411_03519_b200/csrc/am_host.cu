@@ -16,6 +16,8 @@ __global__ void k_scan(Dev d);
 __global__ void k_scan_thread(Dev d);
 __global__ void k_finalize(Dev d);
 __global__ void k_union(Dev d);
+__global__ void k_near(Dev d);
+__global__ void k_far(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
 __global__ void k_sort_pass(Dev d, int pass, int32_t* order);
@@ -71,7 +73,7 @@ static inline unsigned blocks(long long n, int t) { return (unsigned)std::max(1L
 
 static const char* kKernelNames[K_COUNT] = {
     "k_ingest", "k_bin", "k_cells", "k_scatter", "k_scan", "k_finalize", "k_ready", "k_sort_hist",
-    "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b", "k_union"};
+    "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b", "k_union", "k_near"};
 
 void am_prof_begin(am_ctx* c, int id)
 {
@@ -140,7 +142,7 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 2 : 10 + c->sort_passes_max;   // incl. k_round_begin, k_union
+    return c->path == 0 ? 2 : 11 + c->sort_passes_max;   // incl. k_round_begin, k_near, k_union
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -186,6 +188,11 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     d.metric = c.metric;
     d.flags = c.flags;
     x->stream = (cudaStream_t)c.stream;
+    {
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        x->num_sms = sms > 0 ? sms : 148;
+    }
 
     // path selection
     bool small = (c.n_sims > 1) || (n <= kSmallMax);
@@ -410,7 +417,8 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             LAUNCH(K_SCAN, (k_scan_thread<<<nb, 256, 0, s>>>(d)));
         else
         {
-            LAUNCH(K_SCAN, (k_scan<<<blocks(d.ncells / 16, 8), 256, 0, s>>>(d)));  // 8 warps, one 4x4 block each
+            LAUNCH(K_NEAR, (k_near<<<nb, 256, 0, s>>>(d)));
+            LAUNCH(K_SCAN, (k_far<<<nb, 256, 0, s>>>(d)));
             LAUNCH(K_UNION, (k_union<<<blocks((long long)kEdgeStripes * d.edge_cap, 256), 256, 0, s>>>(d)));
         }
         LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));

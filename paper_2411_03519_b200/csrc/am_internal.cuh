@@ -100,7 +100,7 @@ struct Dev {
 namespace am {
 enum KernelId : int {
     K_INGEST = 0, K_BIN, K_CELLS, K_SCATTER, K_SCAN, K_FINALIZE, K_READY, K_SORT_HIST, K_SORT_PASS,
-    K_SMALL, K_COMMIT, K_DISP_A, K_DISP_B, K_UNION, K_COUNT
+    K_SMALL, K_COMMIT, K_DISP_A, K_DISP_B, K_UNION, K_NEAR, K_COUNT
 };
 struct Prof {
     bool on = false;
@@ -125,6 +125,7 @@ struct am_ctx {
     int path = 0;                    // 0 = fused per-sim kernel, 1 = binned pipeline
     int cell = 0;
     int small_threads = 32;
+    int num_sms = 148;
     int sort_passes_max = 1;
     int ntiles_sort = 1;
     int ntiles_ready = 1;

@@ -530,20 +530,129 @@ __device__ __forceinline__ void add_cells(const Dev& d, ScanSmem& sm, bool take,
     nc += cnt;
 }
 
+// k_near: the near phase as its own kernel, one thread per sorted record: the (at
+// most 2x2 when cell >= R_c) cells within box distance R_c of the agent.  Coupling
+// unions are staged as edges, perception digests and blocking
+// tests against every agent in those cells.  Threads of one warp hold
+// Morton-consecutive agents, so they mostly read the same cell entries and records.
+struct NearSmem {
+    uint2 edges[kEdgeStage];
+    int ne;
+};
+__device__ __forceinline__ void stage_edge_n(const Dev& d, NearSmem& sm, uint32_t a, uint32_t b)
+{
+    const int pos = atomicAdd(&sm.ne, 1);
+    if (pos < kEdgeStage) sm.edges[pos] = make_uint2(a, b);
+    else uf_unite(d.parent, a, b);
+}
+
+__global__ void __launch_bounds__(256, 6) k_near(Dev d)
+{
+    __shared__ NearSmem s_all[8];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    NearSmem& sm = s_all[wq];
+    if (lane == 0) sm.ne = 0;
+    __syncwarp();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nact = d.ctl->n_active;
+    bool nblk = false;
+    if (r < nact) {
+        const int4 A = d.rec[r];
+        const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+        const uint32_t aid = (uint32_t)A.z;
+        const int cl = d.clog, G = 1 << d.glog;
+        const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+        const uint32_t Rc2 = Rc * Rc, Rp2 = (uint32_t)d.r_p * (uint32_t)d.r_p;
+        const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+        unsigned long long dig = 0;
+        const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
+        const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
+        for (int cy = cy0; cy <= cy1; cy++)
+            for (int cx = cx0; cx <= cx1; cx++) {
+                if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rc,
+                                d.metric))
+                    continue;
+                const uint32_t key = morton(cx, cy);
+                const int2 e = d.ctab[key];
+                if (e.y > as) continue;
+                const int e1 = d.ctab[key + 1].x;
+                for (int b = e.x; b < e1; b++) {
+                    const int4 B = d.rec[b];
+                    const uint32_t bid = (uint32_t)B.z;
+                    if (bid == aid) continue;
+                    const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                    if (B.y == as) {
+                        if (within2(dx, dy, Rc2, Rc, d.metric)) {
+                            if (aid < bid) stage_edge_n(d, sm, aid, bid);
+                            if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
+                                dig += digest_term(bid, dx, dy);
+                        }
+                    } else if (!nblk && B.y < as) {
+                        const int lag = as - B.y;
+                        const uint32_t R =
+                            min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
+                        nblk = within2(dx, dy, R * R, R, d.metric);
+                    }
+                }
+            }
+        d.blk8[r] = nblk;
+        if (d.flags & AM_DIGEST) d.digest[aid] = dig;
+    }
+    // append the warp's staged edges to a global stripe
+    __syncwarp();
+    const int ne = min(sm.ne, kEdgeStage);
+    if (ne) {
+        const int stripe = (blockIdx.x * 8 + wq) & (kEdgeStripes - 1);
+        int base = 0;
+        if (lane == 0) base = (int)atomicAdd(d.edge_ctr + stripe, (unsigned)ne);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        for (int k = lane; k < ne; k += 32) {
+            const uint2 e = sm.edges[k];
+            if (base + k < d.edge_cap) d.edges[(size_t)stripe * d.edge_cap + base + k] = e;
+            else uf_unite(d.parent, e.x, e.y);
+        }
+    }
+    if (d.flags & AM_STATS) {
+        const unsigned nbk = __popc(__ballot_sync(0xFFFFFFFFu, nblk));
+        if (lane == 0 && nbk) atomicAdd(&d.ctl->st_blocked, (unsigned long long)nbk);
+    }
+}
+
+// one near-phase pair (agent A in registers, candidate record B)
+__device__ __forceinline__ void near_pair(const Dev& d, ScanSmem& sm, const int4 B, int ax, int ay, int as,
+                                          uint32_t aid, int lagcap, uint32_t Rc, uint32_t Rc2, uint32_t Rp2,
+                                          bool& nblk, unsigned long long& dig)
+{
+    const uint32_t bid = (uint32_t)B.z;
+    if (bid == aid) return;
+    const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+    if (B.y == as) {
+        if (within2(dx, dy, Rc2, Rc, d.metric)) {
+            if (aid < bid) stage_edge(d, sm, aid, bid);
+            if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
+                dig += digest_term(bid, dx, dy);
+        }
+    } else if (!nblk && B.y < as) {
+        const int lag = as - B.y;
+        const uint32_t R = min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
+        nblk = within2(dx, dy, R * R, R, d.metric);
+    }
+}
+
 __global__ void __launch_bounds__(256, 3) k_scan(Dev d)
 {
     __shared__ ScanSmem s_all[kScanWarps];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     ScanSmem& sm = s_all[wq];
-    const int blk = blockIdx.x * kScanWarps + wq;          // 4x4-cell block (key >> 4)
-    if (blk >= (d.ncells >> 4)) return;                     // warp-uniform
-    const int beg = d.ctab[blk * 16].x, end = d.ctab[blk * 16 + 16].x;
-    if (beg == end) return;
     const int W = d.ctl->W;
     const int cl = d.clog, G = 1 << d.glog;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
     unsigned long long ncand = 0;
     uint32_t ncells = 0, np2 = 0, nb2 = 0, nb1 = 0;
+    // persistent warps: 4x4-cell blocks (key >> 4) strided over all warps of the grid
+    const int nblocks = d.ncells >> 4, nwarps = gridDim.x * kScanWarps;
+    for (int blk = blockIdx.x * kScanWarps + wq; blk < nblocks; blk += nwarps) {
+    const int beg = d.ctab[blk * 16].x, end = d.ctab[blk * 16 + 16].x;
     for (int base = beg; base < end; base += 32) {
         const int r = base + lane;
         const bool valid = r < end;
@@ -558,48 +667,8 @@ __global__ void __launch_bounds__(256, 3) k_scan(Dev d)
         const int x1 = __reduce_max_sync(0xFFFFFFFFu, valid ? ax : INT_MIN);
         const int y0 = __reduce_min_sync(0xFFFFFFFFu, valid ? ay : INT_MAX);
         const int y1 = __reduce_max_sync(0xFFFFFFFFu, valid ? ay : INT_MIN);
-        // ---- near phase, one lane per agent: the (at most 2x2 when cell >= R_c) cells
-        // within box distance R_c of the agent; lanes of one cell read the same entries
-        bool nblk = false;
-        if (valid && !(d.flags & AM_DBG_SKIP_NEAR)) {
-            const uint32_t aid = (uint32_t)A.z;
-            const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
-            const uint32_t Rc2 = Rc * Rc, Rp2 = (uint32_t)d.r_p * (uint32_t)d.r_p;
-            unsigned long long dig = 0;
-            const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
-            const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
-            for (int cy = cy0; cy <= cy1; cy++)
-                for (int cx = cx0; cx <= cx1; cx++) {
-                    if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1,
-                                    Rc, d.metric))
-                        continue;
-                    const uint32_t key = morton(cx, cy);
-                    const int2 e = d.ctab[key];
-                    ncells++;
-                    if (e.y > as) continue;
-                    const int e1 = d.ctab[key + 1].x;
-                    ncand += (unsigned long long)(e1 - e.x);
-                    for (int b = e.x; b < e1; b++) {
-                        const int4 B = d.rec[b];
-                        const uint32_t bid = (uint32_t)B.z;
-                        if (bid == aid) continue;
-                        const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-                        if (B.y == as) {
-                            if (within2(dx, dy, Rc2, Rc, d.metric)) {
-                                if (aid < bid) stage_edge(d, sm, aid, bid);
-                                if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
-                                    dig += digest_term(bid, dx, dy);
-                            }
-                        } else if (!nblk && B.y < as) {
-                            const int lag = as - B.y;
-                            const uint32_t R = min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
-                            nblk = within2(dx, dy, R * R, R, d.metric);
-                        }
-                    }
-                }
-            sm.dig[lane] = dig;
-        }
-        flush_edges(d, sm);
+        // near-phase verdicts from k_near
+        const bool nblk = valid && d.blk8[r] != 0;
         unsigned blocked = __ballot_sync(0xFFFFFFFFu, nblk);
         int nc = 0;
         const bool my_blocked = valid && ((blocked >> lane) & 1u);
@@ -695,16 +764,12 @@ __global__ void __launch_bounds__(256, 3) k_scan(Dev d)
             nc = 0;
             if (open) far_blocked = (fb >> __popc(om & ((1u << lane) - 1u))) & 1u;
         }
-        const bool blk = my_blocked || far_blocked;
-        if (valid) {
-            d.blk8[r] = blk;
-            if (d.flags & AM_DIGEST) d.digest[A.z] = sm.dig[lane];
-        }
-        __syncwarp();
+        if (far_blocked) d.blk8[r] = 1;
         if (d.flags & AM_STATS) {
-            const unsigned nbk = __popc(__ballot_sync(0xFFFFFFFFu, valid && blk));
-            if (lane == 0) atomicAdd(&d.ctl->st_blocked, (unsigned long long)nbk);
+            const unsigned nbk = __popc(__ballot_sync(0xFFFFFFFFu, far_blocked));
+            if (lane == 0 && nbk) atomicAdd(&d.ctl->st_blocked, (unsigned long long)nbk);
         }
+    }
     }
     if (d.flags & AM_STATS) {
         const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells);
@@ -716,6 +781,121 @@ __global__ void __launch_bounds__(256, 3) k_scan(Dev d)
             atomicAdd(&d.ctl->st_p2, (unsigned long long)c2);
             atomicAdd(&d.ctl->st_b2, (unsigned long long)c3);
             atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
+        }
+    }
+}
+
+// k_far: the far (time-dilated) phase, one thread per sorted record that k_near left
+// unblocked and that is ahead of the watermark W.  The thread walks the min-step
+// pyramid with ITS OWN point and step: a 16x16-cell block, 4x4-cell block or cell
+// with min step m is skipped if m >= s_A or its box distance exceeds R_b(s_A - m)
+// (exact pruning: nothing inside can block A).  The 16 children of a block are
+// Morton-contiguous, so each level is fetched with a few 16-byte vector loads (one
+// L2 round trip) instead of 16 dependent ones.  Cells within R_c of A were tested
+// completely by k_near and are skipped.
+__device__ __forceinline__ void morton_child(int k, int& dx, int& dy)
+{
+    dx = (k & 1) | ((k >> 1) & 2);
+    dy = ((k >> 1) & 1) | ((k >> 2) & 2);
+}
+
+__global__ void __launch_bounds__(256) k_far(Dev d)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nact = d.ctl->n_active;
+    const int W = d.ctl->W;
+    bool blocked = false;
+    uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, np2 = 0;
+    if (r < nact && !d.blk8[r]) {
+        const int4 A = d.rec[r];
+        const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+        if (as > W && !(d.flags & AM_DBG_SKIP_FAR)) {
+            np2 = 1;
+            const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
+            const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+            const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+            const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
+            const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
+            const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
+            for (int by = by0; by <= by1 && !blocked; by++)
+                for (int bx = bx0; bx <= bx1 && !blocked; bx++) {
+                    const uint32_t k2 = morton(bx, by);
+                    const int m2 = __ldg(d.lmin2 + k2);
+                    nb2++;
+                    if (m2 >= as || !box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1,
+                                                ((by + 1) << l2) - 1, rb_radius((long long)as - m2, d.v, d.r_p),
+                                                d.metric))
+                        continue;
+                    // the 16 4x4-cell children: 64 contiguous bytes
+                    const int4* c4 = reinterpret_cast<const int4*>(d.lmin1 + k2 * 16);
+                    int m1[16];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const int4 v = __ldg(c4 + q);
+                        m1[4 * q] = v.x; m1[4 * q + 1] = v.y; m1[4 * q + 2] = v.z; m1[4 * q + 3] = v.w;
+                    }
+#pragma unroll 1
+                    for (int k1 = 0; k1 < 16 && !blocked; k1++) {
+                        int ox, oy;
+                        morton_child(k1, ox, oy);
+                        const int qx = bx * 4 + ox, qy = by * 4 + oy;
+                        nb1++;
+                        if (m1[k1] >= as || !box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
+                                                        ((qy + 1) << l1) - 1,
+                                                        rb_radius((long long)as - m1[k1], d.v, d.r_p), d.metric))
+                            continue;
+                        // the 16 cells: 16 contiguous {start, min} entries + the next start
+                        const uint32_t k1g = k2 * 16 + k1;
+                        const int4* e4 = reinterpret_cast<const int4*>(d.ctab + k1g * 16);
+                        int st[17], mn[16];
+#pragma unroll
+                        for (int q = 0; q < 8; q++) {
+                            const int4 v = e4[q];
+                            st[2 * q] = v.x; mn[2 * q] = v.y; st[2 * q + 1] = v.z; mn[2 * q + 1] = v.w;
+                        }
+                        st[16] = d.ctab[k1g * 16 + 16].x;
+#pragma unroll
+                        for (int k0 = 0; k0 < 16; k0++) {
+                            if (blocked || st[k0 + 1] == st[k0] || mn[k0] >= as) continue;
+                            morton_child(k0, ox, oy);
+                            const int cx = qx * 4 + ox, cy = qy * 4 + oy;
+                            const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
+                            ncells++;
+                            if (box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric)) continue;   // k_near's
+                            if (!box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - mn[k0], d.v, d.r_p),
+                                            d.metric))
+                                continue;
+                            ncand += (uint32_t)(st[k0 + 1] - st[k0]);
+                            for (int b = st[k0]; b < st[k0 + 1]; b++) {
+                                const int4 B = d.rec[b];
+                                if (B.y >= as) continue;
+                                const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                                const int lag = as - B.y;
+                                const uint32_t Rb =
+                                    min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
+                                if (within2(dx, dy, Rb * Rb, Rb, d.metric)) {
+                                    blocked = true;
+                                    break;
+                                }
+                            }
+                        }
+                    }
+                }
+            if (blocked) d.blk8[r] = 1;
+        }
+    }
+    if (d.flags & AM_STATS) {
+        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
+        const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, np2), c3 = __reduce_add_sync(0xFFFFFFFFu, nb2);
+        const unsigned c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
+        const unsigned c5 = __popc(__ballot_sync(0xFFFFFFFFu, blocked));
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
+            atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
+            atomicAdd(&d.ctl->st_p2, (unsigned long long)c2);
+            atomicAdd(&d.ctl->st_b2, (unsigned long long)c3);
+            atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
+            if (c5) atomicAdd(&d.ctl->st_blocked, (unsigned long long)c5);
         }
     }
 }

@@ -50,7 +50,7 @@ def main():
         # graphs bake the flags: set them on the context and force a re-capture
         L.am_set_flags(rep.tracker.ctx, rep.tracker.flags | 0x4 | 0x8)   # + DIGEST | ASYNC
     if a.prof:
-        rep.profile((1 << 14) - 1)
+        rep.profile((1 << 15) - 1)
     rows = []
     for k in range(a.rounds):
         rep.launch(1)
