@@ -258,7 +258,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
     size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
-           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0;
+           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0;
     const size_t NC = (size_t)d.ncells;
     if (x->path == 1) {
         o_key = take(4 * N); o_rank = take(4 * N);
@@ -271,6 +271,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * 256);
         o_gh = take(4 * kMaxSortPasses * 256); o_gs = take(4 * kMaxSortPasses * 256);
         d.edge_cap = (int)std::max<size_t>(256, (2 * N + kEdgeStripes - 1) / kEdgeStripes);
+        o_wit = take(4 * N); o_lrs = take(4 * N); o_farq = take(4 * N);
         o_edges = take(8 * (size_t)kEdgeStripes * d.edge_cap); o_ectr = take(4 * kEdgeStripes);
     }
     x->ws_bytes = off;
@@ -298,15 +299,18 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.tiles_sort = (unsigned long long*)(b + o_tsort);
         d.ghist = (uint32_t*)(b + o_gh); d.gstart = (uint32_t*)(b + o_gs);
         d.edges = (uint2*)(b + o_edges); d.edge_ctr = (uint32_t*)(b + o_ectr);
+        d.witness = (uint32_t*)(b + o_wit); d.lrstep = (int32_t*)(b + o_lrs); d.farq = (uint32_t*)(b + o_farq);
     }
     // initial contents: everything zero except the min-step table
     e = cudaMemsetAsync(x->ws, 0, off, x->stream);
     if (e == cudaSuccess && x->path == 1) e = cudaMemsetAsync(d.cmin, 0x7F, 4 * NC, x->stream);  // ~INT_MAX
+    if (e == cudaSuccess && x->path == 1) e = cudaMemsetAsync(d.witness, 0xFF, 4 * N, x->stream);
     Ctl h{};
     h.acc_W = INT_MAX;
     h.acc_S = INT_MIN;
     h.W = INT_MAX;
     h.S = INT_MIN;
+    h.full = 1;
     if (e == cudaSuccess) e = cudaMemcpyAsync(d.ctl, &h, sizeof h, cudaMemcpyHostToDevice, x->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
     if (e != cudaSuccess) {
@@ -413,12 +417,13 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         LAUNCH(K_BIN, (k_bin<<<nb, 256, 0, s>>>(d)));
         LAUNCH(K_CELLS, (k_cells<<<c->ntiles_cells, 256, 0, s>>>(d)));
         LAUNCH(K_SCATTER, (k_scatter<<<nb, 256, 0, s>>>(d)));
-        if (d.flags & AM_SCAN_THREAD)
+        if (d.flags & AM_SCAN_THREAD)   // ablation: everything recomputed, no witnesses
             LAUNCH(K_SCAN, (k_scan_thread<<<nb, 256, 0, s>>>(d)));
         else
         {
             LAUNCH(K_NEAR, (k_near<<<nb, 256, 0, s>>>(d)));
-            LAUNCH(K_SCAN, (k_far<<<nb, 256, 0, s>>>(d)));
+            // far phase over the compacted queue, persistent grid-stride
+            LAUNCH(K_SCAN, (k_far<<<std::min<unsigned>(nb, (unsigned)c->num_sms * 8), 256, 0, s>>>(d)));
             LAUNCH(K_UNION, (k_union<<<blocks((long long)kEdgeStripes * d.edge_cap, 256), 256, 0, s>>>(d)));
         }
         LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));
@@ -468,6 +473,12 @@ extern "C" int am_stats(const am_ctx* c, am_round_stats* out)
 extern "C" int am_set_flags(am_ctx* c, uint32_t flags)
 {
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (c->path == 1 && ((flags ^ c->d.flags) & AM_SCAN_THREAD)) {
+        // the ablation scan keeps no blocking witnesses: recompute everything next round
+        const int32_t one = 1;
+        CK(c, cudaMemcpyAsync(&c->d.ctl->full, &one, sizeof one, cudaMemcpyHostToDevice, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+    }
     c->d.flags = flags;
     return AM_OK;
 }

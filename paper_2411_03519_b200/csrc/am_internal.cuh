@@ -43,7 +43,9 @@ struct Ctl {
     int32_t  n_active, n_running;
     int32_t  n_ready, n_clusters;
     int32_t  npasses;      // radix passes needed by this round's ready keys
-    int32_t  pad0;
+    int32_t  full;         // recompute every blocking verdict this round
+    int32_t  far_count;    // records queued for the far phase
+    int32_t  pad1;
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
     unsigned long long sort_or;   // OR of all ready keys
@@ -75,7 +77,10 @@ struct Dev {
     int32_t* lmin1;        // [ncells/16]  min step per 4x4-cell block
     int32_t* lmin2;        // [ncells/256] min step per 16x16-cell block
     int4* rec;             // [n] sorted records {x | y<<16, step, id, status}
-    uint8_t* blk8;         // [n] blocked flag per sorted record
+    uint8_t* blk8;         // [n] blocked verdict per sorted record (0 no, 1 yes, 2 far pending)
+    uint32_t* witness;     // [n] per id: the blocker found last time it was computed
+    int32_t* lrstep;       // [n] per id: step at the last round
+    uint32_t* farq;        // [n] records queued for the far phase
     uint2* edges;          // [kEdgeStripes][edge_cap] coupling edges (a < b)
     uint32_t* edge_ctr;    // [kEdgeStripes]
     int32_t edge_cap;      // per stripe

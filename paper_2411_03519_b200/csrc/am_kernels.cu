@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
     if (finish_block(&ctl->ingest, gridDim.x) && threadIdx.x == 0) {
         const int e = *(volatile int*)&ctl->err_new;
         if (e == 0) {
+            if (mode != 0) ctl->full = 1;
             ctl->cur = c ^ 1u;
             ctl->W = *(volatile int*)&ctl->acc_W;
             ctl->S = *(volatile int*)&ctl->acc_S;
@@ -555,15 +556,38 @@ __global__ void __launch_bounds__(256, 6) k_near(Dev d)
     __syncwarp();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int nact = d.ctl->n_active;
-    bool nblk = false;
+    const int W = d.ctl->W;
+    // without commit validation positions may change without a step change: no reuse
+    const bool full = d.ctl->full != 0 || !(d.flags & AM_VALIDATE);
+    bool nblk = false, farq = false;
     if (r < nact) {
         const int4 A = d.rec[r];
         const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
         const uint32_t aid = (uint32_t)A.z;
+        // Which blocking verdict must be recomputed (incremental
+        // blocking): only IDLE agents' verdicts matter (a RUNNING member makes its
+        // cluster not ready anyway).  A commit can only remove blocking relations of
+        // other agents, so an IDLE agent unchanged since the last round keeps its
+        // verdict unless its recorded blocker (witness) committed since.
+        const bool idle = A.w == ST_IDLE;
+        bool need = false, known = false;
+        if (idle) {
+            if (full || d.lrstep[aid] != as) {
+                need = true;
+            } else {
+                const uint32_t w = d.witness[aid];
+                if (w == kSentinel) known = false, need = false;
+                else if (d.lrstep[w] != d.step[d.ctl->cur][w]) need = true;
+                else known = true, need = false;
+            }
+        }
+        nblk = known;
+        uint32_t wit = kSentinel;
         const int cl = d.clog, G = 1 << d.glog;
         const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
         const uint32_t Rc2 = Rc * Rc, Rp2 = (uint32_t)d.r_p * (uint32_t)d.r_p;
         const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+        const bool test_blk = need;
         unsigned long long dig = 0;
         const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
         const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
@@ -587,16 +611,41 @@ __global__ void __launch_bounds__(256, 6) k_near(Dev d)
                             if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
                                 dig += digest_term(bid, dx, dy);
                         }
-                    } else if (!nblk && B.y < as) {
+                    } else if (test_blk && !nblk && B.y < as) {
                         const int lag = as - B.y;
                         const uint32_t R =
                             min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
-                        nblk = within2(dx, dy, R * R, R, d.metric);
+                        if (within2(dx, dy, R * R, R, d.metric)) {
+                            nblk = true;
+                            wit = bid;
+                        }
                     }
                 }
             }
-        d.blk8[r] = nblk;
+        // blk8: 0 = not blocked, 1 = blocked, 2 = not blocked so far, far phase needed
+        uint8_t code = nblk ? 1 : 0;
+        if (need) {
+            if (nblk) d.witness[aid] = wit;
+            else if (as > W && !(d.flags & AM_DBG_SKIP_FAR)) code = 2;
+            else d.witness[aid] = kSentinel;
+        }
+        d.blk8[r] = code;
         if (d.flags & AM_DIGEST) d.digest[aid] = dig;
+        farq = code == 2;
+    }
+    // compact the records that need the far phase (one atomic per block)
+    {
+        __shared__ uint32_t s_cnt, s_base;
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, farq);
+        uint32_t wbase = 0;
+        if (lane == 0 && m) wbase = atomicAdd(&s_cnt, (uint32_t)__popc(m));
+        wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_cnt) s_base = atomicAdd((uint32_t*)&d.ctl->far_count, s_cnt);
+        __syncthreads();
+        if (farq) d.farq[s_base + wbase + __popc(m & ((1u << lane) - 1u))] = (uint32_t)r;
     }
     // append the warp's staged edges to a global stripe
     __syncwarp();
@@ -801,15 +850,17 @@ __device__ __forceinline__ void morton_child(int k, int& dx, int& dy)
 
 __global__ void __launch_bounds__(256) k_far(Dev d)
 {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nact = d.ctl->n_active;
+    const int nq = d.ctl->far_count;
     const int W = d.ctl->W;
+    uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, np2 = 0, nblocked = 0;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
     bool blocked = false;
-    uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, np2 = 0;
-    if (r < nact && !d.blk8[r]) {
+    {
+        const int r = (int)d.farq[q];
         const int4 A = d.rec[r];
         const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
-        if (as > W && !(d.flags & AM_DBG_SKIP_FAR)) {
+        uint32_t wit = kSentinel;
+        {
             np2 = 1;
             const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
             const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
@@ -875,20 +926,24 @@ __global__ void __launch_bounds__(256) k_far(Dev d)
                                     min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
                                 if (within2(dx, dy, Rb * Rb, Rb, d.metric)) {
                                     blocked = true;
+                                    wit = (uint32_t)B.z;
                                     break;
                                 }
                             }
                         }
                     }
                 }
-            if (blocked) d.blk8[r] = 1;
+            d.blk8[r] = blocked ? 1 : 0;
+            d.witness[A.z] = wit;
         }
+    }
+    nblocked += blocked;
     }
     if (d.flags & AM_STATS) {
         const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
         const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, np2), c3 = __reduce_add_sync(0xFFFFFFFFu, nb2);
         const unsigned c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
-        const unsigned c5 = __popc(__ballot_sync(0xFFFFFFFFu, blocked));
+        const unsigned c5 = __reduce_add_sync(0xFFFFFFFFu, nblocked);
         if ((threadIdx.x & 31) == 0) {
             atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
             atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
@@ -923,7 +978,7 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
     const uint32_t aid = (uint32_t)A.z;
     const uint32_t root = uf_find(d.parent, aid);
     d.labels[aid] = (int32_t)root;
-    const bool blk = d.blk8[r] != 0;
+    const bool blk = d.blk8[r] == 1;
     if (blk || A.w == ST_RUNNING) d.bad[root] = 1;
 }
 
@@ -955,6 +1010,7 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
         lab[k] = -1;
         if (i < d.n) {
             const uint8_t st = d.status[c][i];
+            d.lrstep[i] = d.step[c][i];
             if (st == ST_DONE) {
                 d.labels[i] = -1;
             } else {
@@ -1017,6 +1073,7 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
         int np = (bits + 7) / 8;
         ctl->npasses = np < 1 ? 1 : np;
         ctl->sort_or = 0;
+        ctl->full = 0;
     }
 }
 
@@ -1266,6 +1323,7 @@ __global__ void k_round_begin(Ctl* ctl)
     ctl->epoch += 1;
     ctl->n_ready = 0;
     ctl->n_clusters = 0;
+    ctl->far_count = 0;
 }
 
 }  // namespace am
