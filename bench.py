@@ -314,7 +314,7 @@ def run_ours(args, w, lm):
     # ---- roofline of the dominant kernel
     L = rep.tracker.L
     stats = {"n": n, "n_active": statistics.mean(st_active), "n_ready": statistics.mean(st_ready),
-             "n_running": statistics.mean(st_running), "passes": rep.tracker.L.am_launches_per_round(rep.tracker.ctx) - 11,
+             "n_running": statistics.mean(st_running), "passes": rep.tracker.L.am_launches_per_round(rep.tracker.ctx) - 12,
              "ncells": 0}
     # cell count of the binned path: (workspace layout) -- from the config the library chose
     cell = rep.tracker.stats()["cell"]

@@ -17,7 +17,8 @@ __global__ void k_scan_thread(Dev d);
 __global__ void k_finalize(Dev d);
 __global__ void k_union(Dev d);
 __global__ void k_near(Dev d);
-__global__ void k_far(Dev d);
+__global__ void k_far1(Dev d);
+__global__ void k_far2(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
 __global__ void k_sort_pass(Dev d, int pass, int32_t* order);
@@ -142,7 +143,7 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 2 : 11 + c->sort_passes_max;   // incl. k_round_begin, k_near, k_union
+    return c->path == 0 ? 2 : 12 + c->sort_passes_max;   // incl. k_round_begin, k_near, k_far1/2, k_union
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -258,7 +259,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
     size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
-           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0;
+           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0;
     const size_t NC = (size_t)d.ncells;
     if (x->path == 1) {
         o_key = take(4 * N); o_rank = take(4 * N);
@@ -272,6 +273,8 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_gh = take(4 * kMaxSortPasses * 256); o_gs = take(4 * kMaxSortPasses * 256);
         d.edge_cap = (int)std::max<size_t>(256, (2 * N + kEdgeStripes - 1) / kEdgeStripes);
         o_wit = take(4 * N); o_lrs = take(4 * N); o_farq = take(4 * N);
+        d.item_cap = (int)std::max<size_t>(1024, (4 * N + kEdgeStripes - 1) / kEdgeStripes);
+        o_items = take(8 * (size_t)kEdgeStripes * d.item_cap); o_ictr = take(4 * kEdgeStripes);
         o_edges = take(8 * (size_t)kEdgeStripes * d.edge_cap); o_ectr = take(4 * kEdgeStripes);
     }
     x->ws_bytes = off;
@@ -300,6 +303,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.ghist = (uint32_t*)(b + o_gh); d.gstart = (uint32_t*)(b + o_gs);
         d.edges = (uint2*)(b + o_edges); d.edge_ctr = (uint32_t*)(b + o_ectr);
         d.witness = (uint32_t*)(b + o_wit); d.lrstep = (int32_t*)(b + o_lrs); d.farq = (uint32_t*)(b + o_farq);
+        d.items = (uint2*)(b + o_items); d.item_ctr = (uint32_t*)(b + o_ictr);
     }
     // initial contents: everything zero except the min-step table
     e = cudaMemsetAsync(x->ws, 0, off, x->stream);
@@ -422,8 +426,12 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         else
         {
             LAUNCH(K_NEAR, (k_near<<<nb, 256, 0, s>>>(d)));
-            // far phase over the compacted queue, persistent grid-stride
-            LAUNCH(K_SCAN, (k_far<<<std::min<unsigned>(nb, (unsigned)c->num_sms * 8), 256, 0, s>>>(d)));
+            // far phase over the compacted queue: pyramid levels, then one thread per
+            // surviving (agent, 4x4-cell block) item; persistent grid-stride
+            am_prof_begin(c, K_SCAN);
+            k_far1<<<std::min<unsigned>(nb, (unsigned)c->num_sms * 8), 256, 0, s>>>(d);
+            k_far2<<<std::min<unsigned>(nb, (unsigned)c->num_sms * 8), 256, 0, s>>>(d);
+            am_prof_end(c, K_SCAN);
             LAUNCH(K_UNION, (k_union<<<blocks((long long)kEdgeStripes * d.edge_cap, 256), 256, 0, s>>>(d)));
         }
         LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));

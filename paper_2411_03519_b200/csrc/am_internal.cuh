@@ -81,6 +81,9 @@ struct Dev {
     uint32_t* witness;     // [n] per id: the blocker found last time it was computed
     int32_t* lrstep;       // [n] per id: step at the last round
     uint32_t* farq;        // [n] records queued for the far phase
+    uint2* items;          // [kEdgeStripes][item_cap] far work items (record, 4x4-block key)
+    uint32_t* item_ctr;    // [kEdgeStripes]
+    int32_t item_cap;      // per stripe
     uint2* edges;          // [kEdgeStripes][edge_cap] coupling edges (a < b)
     uint32_t* edge_ctr;    // [kEdgeStripes]
     int32_t edge_cap;      // per stripe
@@ -153,6 +156,16 @@ __device__ __forceinline__ uint32_t part1by1(uint32_t x)
     x = (x | (x << 4)) & 0x0F0F0F0Fu;
     x = (x | (x << 2)) & 0x33333333u;
     x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+// inverse of part1by1: the even bits of x packed together
+__device__ __forceinline__ uint32_t part_compact(uint32_t x)
+{
+    x &= 0x55555555u;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+    x = (x | (x >> 4)) & 0x00FF00FFu;
+    x = (x | (x >> 8)) & 0x0000FFFFu;
     return x;
 }
 // Morton (Z-order) key of a cell: every aligned 2^k x 2^k block of cells is a

@@ -140,7 +140,10 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
     d.rank[i] = rank;
     d.parent[i] = (uint32_t)i;
     d.bad[i] = 0;
-    if (i < kEdgeStripes) d.edge_ctr[i] = 0;
+    if (i < kEdgeStripes) {
+        d.edge_ctr[i] = 0;
+        d.item_ctr[i] = 0;
+    }
 }
 
 // k_cells: exclusive scan of the cell counts in Morton order -> ctab{start, min};
@@ -848,109 +851,172 @@ __device__ __forceinline__ void morton_child(int k, int& dx, int& dy)
     dy = ((k >> 1) & 1) | ((k >> 2) & 2);
 }
 
-__global__ void __launch_bounds__(256) k_far(Dev d)
+// test agent A against the cells of one 4x4-cell block (Morton key k1g at block
+// coordinates qx, qy); returns the id of a blocker or kSentinel
+__device__ __forceinline__ uint32_t far_block(const Dev& d, uint32_t k1g, int qx, int qy, int ax, int ay, int as,
+                                              uint32_t Rc, int lagcap, uint32_t& ncells, uint32_t& ncand)
+{
+    const int cl = d.clog;
+    const int4* e4 = reinterpret_cast<const int4*>(d.ctab + (size_t)k1g * 16);
+    int st[17], mn[16];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        const int4 v = e4[q];
+        st[2 * q] = v.x; mn[2 * q] = v.y; st[2 * q + 1] = v.z; mn[2 * q + 1] = v.w;
+    }
+    st[16] = d.ctab[(size_t)k1g * 16 + 16].x;
+#pragma unroll
+    for (int k0 = 0; k0 < 16; k0++) {
+        if (st[k0 + 1] == st[k0] || mn[k0] >= as) continue;
+        int ox, oy;
+        morton_child(k0, ox, oy);
+        const int cx = qx * 4 + ox, cy = qy * 4 + oy;
+        const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
+        ncells++;
+        if (box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric)) continue;   // tested by k_near
+        if (!box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - mn[k0], d.v, d.r_p), d.metric)) continue;
+        ncand += (uint32_t)(st[k0 + 1] - st[k0]);
+        for (int b = st[k0]; b < st[k0 + 1]; b++) {
+            const int4 B = d.rec[b];
+            if (B.y >= as) continue;
+            const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+            const int lag = as - B.y;
+            const uint32_t Rb = min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
+            if (within2(dx, dy, Rb * Rb, Rb, d.metric)) return (uint32_t)B.z;
+        }
+    }
+    return kSentinel;
+}
+
+// k_far1: one thread per queued agent: the 16x16- and 4x4-cell levels of the pyramid
+// (vector loads of the 16 Morton-contiguous children), then one work item per
+// surviving 4x4-cell block appended to a striped item list for k_far2, so a leading
+// agent with many candidate blocks is spread over many threads.  If the item list is
+// full the thread tests the block itself.
+__global__ void __launch_bounds__(256, 2) k_far1(Dev d)
 {
     const int nq = d.ctl->far_count;
     const int W = d.ctl->W;
-    uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, np2 = 0, nblocked = 0;
+    uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
+    const int stripe = blockIdx.x & (kEdgeStripes - 1);
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
-    bool blocked = false;
-    {
         const int r = (int)d.farq[q];
         const int4 A = d.rec[r];
         const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+        const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
+        const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+        const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+        const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
+        const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
+        const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
         uint32_t wit = kSentinel;
-        {
-            np2 = 1;
-            const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
-            const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-            const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
-            const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
-            const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
-            const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
-            for (int by = by0; by <= by1 && !blocked; by++)
-                for (int bx = bx0; bx <= bx1 && !blocked; bx++) {
-                    const uint32_t k2 = morton(bx, by);
-                    const int m2 = __ldg(d.lmin2 + k2);
-                    nb2++;
-                    if (m2 >= as || !box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1,
-                                                ((by + 1) << l2) - 1, rb_radius((long long)as - m2, d.v, d.r_p),
-                                                d.metric))
-                        continue;
-                    // the 16 4x4-cell children: 64 contiguous bytes
-                    const int4* c4 = reinterpret_cast<const int4*>(d.lmin1 + k2 * 16);
-                    int m1[16];
+        d.blk8[r] = 0;
+        for (int by = by0; by <= by1 && wit == kSentinel; by++)
+            for (int bx = bx0; bx <= bx1 && wit == kSentinel; bx++) {
+                const uint32_t k2 = morton(bx, by);
+                const int m2 = __ldg(d.lmin2 + k2);
+                nb2++;
+                if (m2 >= as || !box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
+                                            rb_radius((long long)as - m2, d.v, d.r_p), d.metric))
+                    continue;
+                const int4* c4 = reinterpret_cast<const int4*>(d.lmin1 + k2 * 16);
+                unsigned keep = 0;
 #pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        const int4 v = __ldg(c4 + q);
-                        m1[4 * q] = v.x; m1[4 * q + 1] = v.y; m1[4 * q + 2] = v.z; m1[4 * q + 3] = v.w;
-                    }
-#pragma unroll 1
-                    for (int k1 = 0; k1 < 16 && !blocked; k1++) {
+                for (int qv = 0; qv < 4; qv++) {
+                    const int4 v = __ldg(c4 + qv);
+                    const int mm[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const int k1 = 4 * qv + j;
                         int ox, oy;
                         morton_child(k1, ox, oy);
                         const int qx = bx * 4 + ox, qy = by * 4 + oy;
-                        nb1++;
-                        if (m1[k1] >= as || !box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
-                                                        ((qy + 1) << l1) - 1,
-                                                        rb_radius((long long)as - m1[k1], d.v, d.r_p), d.metric))
-                            continue;
-                        // the 16 cells: 16 contiguous {start, min} entries + the next start
-                        const uint32_t k1g = k2 * 16 + k1;
-                        const int4* e4 = reinterpret_cast<const int4*>(d.ctab + k1g * 16);
-                        int st[17], mn[16];
-#pragma unroll
-                        for (int q = 0; q < 8; q++) {
-                            const int4 v = e4[q];
-                            st[2 * q] = v.x; mn[2 * q] = v.y; st[2 * q + 1] = v.z; mn[2 * q + 1] = v.w;
-                        }
-                        st[16] = d.ctab[k1g * 16 + 16].x;
-#pragma unroll
-                        for (int k0 = 0; k0 < 16; k0++) {
-                            if (blocked || st[k0 + 1] == st[k0] || mn[k0] >= as) continue;
-                            morton_child(k0, ox, oy);
-                            const int cx = qx * 4 + ox, cy = qy * 4 + oy;
-                            const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
-                            ncells++;
-                            if (box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric)) continue;   // k_near's
-                            if (!box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - mn[k0], d.v, d.r_p),
-                                            d.metric))
-                                continue;
-                            ncand += (uint32_t)(st[k0 + 1] - st[k0]);
-                            for (int b = st[k0]; b < st[k0 + 1]; b++) {
-                                const int4 B = d.rec[b];
-                                if (B.y >= as) continue;
-                                const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-                                const int lag = as - B.y;
-                                const uint32_t Rb =
-                                    min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
-                                if (within2(dx, dy, Rb * Rb, Rb, d.metric)) {
-                                    blocked = true;
-                                    wit = (uint32_t)B.z;
-                                    break;
-                                }
-                            }
-                        }
+                        if (mm[j] < as && box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
+                                                     ((qy + 1) << l1) - 1, rb_radius((long long)as - mm[j], d.v, d.r_p),
+                                                     d.metric))
+                            keep |= 1u << k1;
                     }
                 }
-            d.blk8[r] = blocked ? 1 : 0;
-            d.witness[A.z] = wit;
-        }
-    }
-    nblocked += blocked;
+                nb1 += 16;
+                if (!keep) continue;
+                const int cnt = __popc(keep);
+                const int base = (int)atomicAdd(d.item_ctr + stripe, (unsigned)cnt);
+                int k = 0;
+                while (keep && wit == kSentinel) {
+                    const int k1 = __ffs(keep) - 1;
+                    keep &= keep - 1;
+                    const uint32_t k1g = k2 * 16 + (uint32_t)k1;
+                    if (base + k < d.item_cap) {
+                        d.items[(size_t)stripe * d.item_cap + base + k] = make_uint2((uint32_t)r, k1g);
+                        nitems++;
+                    } else {
+                        int ox, oy;
+                        morton_child(k1, ox, oy);
+                        wit = far_block(d, k1g, bx * 4 + ox, by * 4 + oy, ax, ay, as, Rc, lagcap, ncells, ncand);
+                    }
+                    k++;
+                }
+            }
+        if (wit != kSentinel) d.blk8[r] = 1;
+        d.witness[A.z] = wit;
     }
     if (d.flags & AM_STATS) {
         const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
-        const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, np2), c3 = __reduce_add_sync(0xFFFFFFFFu, nb2);
-        const unsigned c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
-        const unsigned c5 = __reduce_add_sync(0xFFFFFFFFu, nblocked);
+        const unsigned c3 = __reduce_add_sync(0xFFFFFFFFu, nb2), c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
+        const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, nitems);
         if ((threadIdx.x & 31) == 0) {
             atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
             atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
-            atomicAdd(&d.ctl->st_p2, (unsigned long long)c2);
+            atomicAdd(&d.ctl->st_p2, (unsigned long long)c2);   // far work items
             atomicAdd(&d.ctl->st_b2, (unsigned long long)c3);
             atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
-            if (c5) atomicAdd(&d.ctl->st_blocked, (unsigned long long)c5);
+        }
+    }
+}
+
+// k_far2: one thread per (agent, 4x4-cell block) item: its 16 cells (one vector
+// fetch) and the records of the cells that survive the min-step test.
+__global__ void __launch_bounds__(256) k_far2(Dev d)
+{
+    __shared__ int s_pref[kEdgeStripes + 1];
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int k = 0; k < kEdgeStripes; k++) {
+            s_pref[k] = acc;
+            acc += min((int)d.item_ctr[k], d.item_cap);
+        }
+        s_pref[kEdgeStripes] = acc;
+    }
+    __syncthreads();
+    const int total = s_pref[kEdgeStripes];
+    uint32_t ncells = 0, ncand = 0, nblk = 0;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+        int lo = 0, hi = kEdgeStripes - 1;          // last stripe with s_pref <= g
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_pref[mid] <= g) lo = mid; else hi = mid - 1;
+        }
+        const uint2 it = d.items[(size_t)lo * d.item_cap + (g - s_pref[lo])];
+        const int r = (int)it.x;
+        if (*(volatile uint8_t*)(d.blk8 + r) == 1) continue;   // another block already blocked it
+        const int4 A = d.rec[r];
+        const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+        const uint32_t k1g = it.y;
+        const int ox = (int)part_compact(k1g), oy = (int)part_compact(k1g >> 1);
+        const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+        const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+        const uint32_t wit = far_block(d, k1g, ox, oy, ax, ay, as, Rc, lagcap, ncells, ncand);
+        if (wit != kSentinel) {
+            d.blk8[r] = 1;
+            d.witness[A.z] = wit;
+            nblk++;
+        }
+    }
+    if (d.flags & AM_STATS) {
+        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
+            atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
         }
     }
 }
