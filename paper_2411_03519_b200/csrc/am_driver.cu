@@ -383,6 +383,7 @@ extern "C" int am_replay_run(am_replay* rp, int64_t max_rounds, int64_t* active)
     int64_t k = 0;
     for (; k + 8 <= max_rounds; k += 8) RK(cudaGraphLaunch(rp->g8, rp->stream));
     for (; k < max_rounds; k++) RK(cudaGraphLaunch(rp->g1, rp->stream));
+    if (max_rounds > 0) am_prof_mark(rp->ctx, rp->graph_prof);
     return finish_check(rp, active);
 }
 
@@ -420,6 +421,7 @@ extern "C" int am_replay_io(am_replay* rp, const int32_t* h_pos_in, const int32_
     RK(cudaMemcpyAsync(rp->r.pos, h_pos_in, 8 * n, cudaMemcpyHostToDevice, rp->stream));
     RK(cudaMemcpyAsync(rp->r.steps, h_steps_in, 4 * n, cudaMemcpyHostToDevice, rp->stream));
     RK(cudaGraphLaunch(rp->g1, rp->stream));
+    am_prof_mark(c, rp->graph_prof);
     if (h_pos_out) RK(cudaMemcpyAsync(h_pos_out, rp->r.pos, 8 * n, cudaMemcpyDeviceToHost, rp->stream));
     if (h_steps_out) RK(cudaMemcpyAsync(h_steps_out, rp->r.steps, 4 * n, cudaMemcpyDeviceToHost, rp->stream));
     if (h_mask) RK(cudaMemcpyAsync(h_mask, rp->mask, n, cudaMemcpyDeviceToHost, rp->stream));
@@ -440,6 +442,7 @@ extern "C" int am_replay_launch(am_replay* rp, int64_t rounds)
     int64_t k = 0;
     for (; k + 8 <= rounds; k += 8) RK(cudaGraphLaunch(rp->g8, rp->stream));
     for (; k < rounds; k++) RK(cudaGraphLaunch(rp->g1, rp->stream));
+    if (rounds > 0) am_prof_mark(rp->ctx, rp->graph_prof);
     return AM_OK;
 }
 

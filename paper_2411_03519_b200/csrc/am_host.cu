@@ -87,6 +87,11 @@ void am_prof_end(am_ctx* c, int id)
         c->prof.pending |= 1u << id;
     }
 }
+// a graph captured with profiling mask `mask` was launched: its events are pending
+void am_prof_mark(am_ctx* c, unsigned mask)
+{
+    if (c->prof.on) c->prof.pending |= mask;
+}
 // after a synchronisation: accumulate the recorded kernel times
 void am_prof_collect(am_ctx* c)
 {
@@ -259,7 +264,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
     size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
-           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0;
+           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0, o_fctr = 0;
     const size_t NC = (size_t)d.ncells;
     if (x->path == 1) {
         o_key = take(4 * N); o_rank = take(4 * N);
@@ -272,7 +277,10 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * 256);
         o_gh = take(4 * kMaxSortPasses * 256); o_gs = take(4 * kMaxSortPasses * 256);
         d.edge_cap = (int)std::max<size_t>(256, (2 * N + kEdgeStripes - 1) / kEdgeStripes);
-        o_wit = take(4 * N); o_lrs = take(4 * N); o_farq = take(4 * N);
+        o_wit = take(4 * N); o_lrs = take(4 * N);
+        // a stripe receives the records of the blocks b with b % 64 == stripe
+        d.farq_cap = (int)(((blocks(n, 256) + kEdgeStripes - 1) / kEdgeStripes) * 256);
+        o_farq = take(4 * (size_t)kEdgeStripes * d.farq_cap); o_fctr = take(4 * kEdgeStripes);
         d.item_cap = (int)std::max<size_t>(1024, (4 * N + kEdgeStripes - 1) / kEdgeStripes);
         o_items = take(8 * (size_t)kEdgeStripes * d.item_cap); o_ictr = take(4 * kEdgeStripes);
         o_edges = take(8 * (size_t)kEdgeStripes * d.edge_cap); o_ectr = take(4 * kEdgeStripes);
@@ -302,7 +310,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.tiles_sort = (unsigned long long*)(b + o_tsort);
         d.ghist = (uint32_t*)(b + o_gh); d.gstart = (uint32_t*)(b + o_gs);
         d.edges = (uint2*)(b + o_edges); d.edge_ctr = (uint32_t*)(b + o_ectr);
-        d.witness = (uint32_t*)(b + o_wit); d.lrstep = (int32_t*)(b + o_lrs); d.farq = (uint32_t*)(b + o_farq);
+        d.witness = (uint32_t*)(b + o_wit); d.lrstep = (int32_t*)(b + o_lrs); d.farq = (uint32_t*)(b + o_farq); d.farq_ctr = (uint32_t*)(b + o_fctr);
         d.items = (uint2*)(b + o_items); d.item_ctr = (uint32_t*)(b + o_ictr);
     }
     // initial contents: everything zero except the min-step table

@@ -80,7 +80,9 @@ struct Dev {
     uint8_t* blk8;         // [n] blocked verdict per sorted record (0 no, 1 yes, 2 far pending)
     uint32_t* witness;     // [n] per id: the blocker found last time it was computed
     int32_t* lrstep;       // [n] per id: step at the last round
-    uint32_t* farq;        // [n] records queued for the far phase
+    uint32_t* farq;        // [kEdgeStripes][farq_cap] records queued for the far phase
+    uint32_t* farq_ctr;    // [kEdgeStripes]
+    int32_t farq_cap;      // per stripe (every block of 8 warps maps to one stripe)
     uint2* items;          // [kEdgeStripes][item_cap] far work items (record, 4x4-block key)
     uint32_t* item_ctr;    // [kEdgeStripes]
     int32_t item_cap;      // per stripe
@@ -124,6 +126,7 @@ struct am_ctx;
 void am_prof_begin(am_ctx* c, int id);
 void am_prof_end(am_ctx* c, int id);
 void am_prof_collect(am_ctx* c);
+void am_prof_mark(am_ctx* c, unsigned mask);
 
 struct am_ctx {
     am::Prof prof;

@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
     if (i < kEdgeStripes) {
         d.edge_ctr[i] = 0;
         d.item_ctr[i] = 0;
+        d.farq_ctr[i] = 0;
     }
 }
 
@@ -636,19 +637,17 @@ __global__ void __launch_bounds__(256, 6) k_near(Dev d)
         if (d.flags & AM_DIGEST) d.digest[aid] = dig;
         farq = code == 2;
     }
-    // compact the records that need the far phase (one atomic per block)
+    // queue the records that need the far phase: one atomic per warp on one of the
+    // striped queue counters (no block-wide barrier)
     {
-        __shared__ uint32_t s_cnt, s_base;
-        if (threadIdx.x == 0) s_cnt = 0;
-        __syncthreads();
         const unsigned m = __ballot_sync(0xFFFFFFFFu, farq);
-        uint32_t wbase = 0;
-        if (lane == 0 && m) wbase = atomicAdd(&s_cnt, (uint32_t)__popc(m));
-        wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
-        __syncthreads();
-        if (threadIdx.x == 0 && s_cnt) s_base = atomicAdd((uint32_t*)&d.ctl->far_count, s_cnt);
-        __syncthreads();
-        if (farq) d.farq[s_base + wbase + __popc(m & ((1u << lane) - 1u))] = (uint32_t)r;
+        if (m) {
+            const int stripe = (blockIdx.x * 8 + wq) & (kEdgeStripes - 1);
+            uint32_t wbase = 0;
+            if (lane == 0) wbase = atomicAdd(d.farq_ctr + stripe, (uint32_t)__popc(m));
+            wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
+            if (farq) d.farq[(size_t)stripe * d.farq_cap + wbase + __popc(m & ((1u << lane) - 1u))] = (uint32_t)r;
+        }
     }
     // append the warp's staged edges to a global stripe
     __syncwarp();
@@ -895,12 +894,27 @@ __device__ __forceinline__ uint32_t far_block(const Dev& d, uint32_t k1g, int qx
 // full the thread tests the block itself.
 __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
 {
-    const int nq = d.ctl->far_count;
+    __shared__ int s_pref[kEdgeStripes + 1];
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int k = 0; k < kEdgeStripes; k++) {
+            s_pref[k] = acc;
+            acc += (int)d.farq_ctr[k];
+        }
+        s_pref[kEdgeStripes] = acc;
+    }
+    __syncthreads();
+    const int nq = s_pref[kEdgeStripes];
     const int W = d.ctl->W;
     uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
     const int stripe = blockIdx.x & (kEdgeStripes - 1);
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
-        const int r = (int)d.farq[q];
+        int lo = 0, hi = kEdgeStripes - 1;          // last queue stripe with s_pref <= q
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
+        }
+        const int r = (int)d.farq[(size_t)lo * d.farq_cap + (q - s_pref[lo])];
         const int4 A = d.rec[r];
         const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
         const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
