@@ -447,7 +447,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         LAUNCH(K_SORT_HIST, (k_sort_hist<<<c->ntiles_sort, 256, 0, s>>>(d, c->sort_passes_max)));
         am_prof_begin(c, K_SORT_PASS);
         for (int p = 0; p < c->sort_passes_max; p++)
-            k_sort_pass<<<c->ntiles_sort, 256, 0, s>>>(d, p, order);
+            k_sort_pass<<<c->ntiles_sort, 1024, 0, s>>>(d, p, order);
         am_prof_end(c, K_SORT_PASS);
     }
 #undef LAUNCH

@@ -16,7 +16,7 @@ namespace am {
 constexpr int kSmallMax = 1024;           // agents per simulation for the fused kernel
 constexpr int kCellsPerTile = 4096;       // cell-table scan tile (256 threads x 16 cells)
 constexpr int kReadyTile = 2048;          // ready compaction tile (256 threads x 8 agents)
-constexpr int kSortTile = 2048;           // radix pass tile (256 threads x 8 keys)
+constexpr int kSortTile = 8192;           // radix pass tile (1024 threads x 8 keys)
 constexpr int kMaxSortPasses = 8;
 constexpr int kIngestItems = 4;
 constexpr int kEdgeStripes = 64;          // global coupling-edge lists          // agents per thread in k_ingest / k_commit

@@ -1204,13 +1204,15 @@ __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
 }
 
 // k_sort_pass: one stable LSD pass over 8 bits (onesweep: per-digit decoupled
-// look-back across tiles).  Warp w of a tile owns items [256w, 256w+256) and ranks them
+// look-back across tiles of 8192 keys, 32 warps x 8 keys per lane, so a typical
+// round's ready set spans a handful of tiles and the look-back chains stay short).
+// Warp w of a tile owns items [256w, 256w+256) and ranks them
 // in index order with __match_any_sync, so the pass is stable.  The last pass writes
 // the ids straight into `order`.
-__global__ void __launch_bounds__(256) k_sort_pass(Dev d, int pass, int32_t* __restrict__ order)
+__global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __restrict__ order)
 {
     Ctl* ctl = d.ctl;
-    __shared__ uint32_t wcnt[8][256];
+    __shared__ uint32_t wcnt[32][256];
     __shared__ uint32_t goff[256];
     const int n = ctl->n_ready;
     const int np = ctl->npasses;
@@ -1226,7 +1228,7 @@ __global__ void __launch_bounds__(256) k_sort_pass(Dev d, int pass, int32_t* __r
     unsigned long long* kout = d.rkey[(pass + 1) & 1];
     uint32_t* vout = d.rval[(pass + 1) & 1];
     const bool last = pass == np - 1;
-    for (int k = t; k < 8 * 256; k += 256) (&wcnt[0][0])[k] = 0;
+    for (int k = t; k < 32 * 256; k += 1024) (&wcnt[0][0])[k] = 0;
     __syncthreads();
     const int shift = 8 * pass;
     unsigned long long key[8];
@@ -1249,10 +1251,10 @@ __global__ void __launch_bounds__(256) k_sort_pass(Dev d, int pass, int32_t* __r
     }
     __syncthreads();
     // per digit (thread t = digit): exclusive prefix over warps, tile total, look-back
-    {
+    if (t < 256) {
         uint32_t acc = 0;
-#pragma unroll
-        for (int q = 0; q < 8; q++) { uint32_t v = wcnt[q][t]; wcnt[q][t] = acc; acc += v; }
+#pragma unroll 8
+        for (int q = 0; q < 32; q++) { uint32_t v = wcnt[q][t]; wcnt[q][t] = acc; acc += v; }
         unsigned long long* tw = d.tiles_sort + ((size_t)pass * gridDim.x) * 256;
         uint32_t excl;
         // column-major tile words: word of (tile, digit) at tw[digit * ntiles + tile]
