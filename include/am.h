@@ -138,6 +138,12 @@ int am_ready(am_ctx* ctx, uint8_t* mask, int32_t* order, int32_t* n_ready);
  * id of the agent's cluster, -1 for DONE agents.  Stream-ordered copy. */
 int am_clusters(am_ctx* ctx, int32_t* labels);
 
+/* Blocking verdicts of the most recent round: uint8 [n_agents] (device), 1 iff the
+ * agent is IDLE and blocked by some agent behind it in time; 0 for
+ * RUNNING and DONE agents (their clusters are never ready anyway).  Used by the
+ * spatial-slab merge (am_slab.h).  Stream-ordered copy. */
+int am_blocked(am_ctx* ctx, uint8_t* blocked);
+
 /* Current statuses (uint8 [n_agents], device), stream-ordered copy. */
 int am_status(am_ctx* ctx, uint8_t* status);
 

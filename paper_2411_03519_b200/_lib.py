@@ -42,6 +42,12 @@ class RoundStats(C.Structure):
                 ("path", C.c_int32), ("cell", C.c_int32)]
 
 
+class SlabGeom(C.Structure):
+    _fields_ = [("map_w", C.c_int32), ("map_h", C.c_int32), ("r_p", C.c_int32), ("v_max", C.c_int32),
+                ("metric", C.c_int32), ("n_slabs", C.c_int32), ("my_slab", C.c_int32),
+                ("n_total", C.c_int32)]
+
+
 class Synth(C.Structure):
     _fields_ = [("lat", C.c_void_p), ("cdf32", C.c_void_p), ("vals", C.c_void_p),
                 ("n_vals", C.c_int32), ("base_us", C.c_int32), ("lat_seed", C.c_uint64),
@@ -58,6 +64,7 @@ SIGNATURES = {
     "am_ready": (C.c_int, [_vp, _vp, _vp, C.POINTER(_i32)]),
     "am_clusters": (C.c_int, [_vp, _vp]),
     "am_status": (C.c_int, [_vp, _vp]),
+    "am_blocked": (C.c_int, [_vp, _vp]),
     "am_stats": (C.c_int, [_vp, C.POINTER(RoundStats)]),
     "am_sync": (C.c_int, [_vp]),
     "am_set_flags": (C.c_int, [_vp, _u32]),
@@ -80,6 +87,11 @@ SIGNATURES = {
     "am_replay_dispatched": (C.c_int, [_vp, C.POINTER(_i64)]),
     "am_replay_destroy": (C.c_int, [_vp]),
     "am_replay_stream": (_vp, [_vp]),
+    "am_slab_watermark": (C.c_int, [_i32, _vp, _vp, _vp, _vp]),
+    "am_slab_halo": (C.c_int, [C.POINTER(SlabGeom), _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp]),
+    "am_slab_links": (C.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "am_slab_merge": (C.c_int, [C.POINTER(SlabGeom), _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32,
+                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "am_replay_launch": (C.c_int, [_vp, _i64]),
     "am_replay_sync": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i32)]),
     "am_replay_io": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i32)]),

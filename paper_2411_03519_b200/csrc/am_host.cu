@@ -260,7 +260,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_pos0 = take(8 * N), o_pos1 = take(8 * N);
     size_t o_st0 = take(4 * N), o_st1 = take(4 * N);
     size_t o_ss0 = take(N), o_ss1 = take(N);
-    size_t o_labels = take(4 * N), o_digest = take(8 * N);
+    size_t o_labels = take(4 * N), o_digest = take(8 * N), o_blkid = take(N);
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
     size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
@@ -296,6 +296,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     d.step[0] = (int32_t*)(b + o_st0); d.step[1] = (int32_t*)(b + o_st1);
     d.status[0] = (uint8_t*)(b + o_ss0); d.status[1] = (uint8_t*)(b + o_ss1);
     d.labels = (int32_t*)(b + o_labels);
+    d.blkid = (uint8_t*)(b + o_blkid);
     d.digest = (unsigned long long*)(b + o_digest);
     d.tiles_s = (unsigned long long*)(b + o_tiles_s);
     if (x->path == 1) {
@@ -466,6 +467,16 @@ extern "C" int am_clusters(am_ctx* c, int32_t* labels)
     if (!c->have_round) return set_err(c, AM_E_STATE, "am_clusters before any am_ready");
     if (c->d.n == 0) return AM_OK;
     CK(c, cudaMemcpyAsync(labels, c->d.labels, 4 * (size_t)c->d.n, cudaMemcpyDeviceToDevice, c->stream));
+    return AM_OK;
+}
+
+extern "C" int am_blocked(am_ctx* c, uint8_t* blocked)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (!blocked) return set_err(c, AM_E_ARG, "NULL blocked");
+    if (!c->have_round) return set_err(c, AM_E_STATE, "am_blocked before any am_ready");
+    if (c->d.n == 0) return AM_OK;
+    CK(c, cudaMemcpyAsync(blocked, c->d.blkid, (size_t)c->d.n, cudaMemcpyDeviceToDevice, c->stream));
     return AM_OK;
 }
 

@@ -92,6 +92,7 @@ struct Dev {
     uint32_t* parent;      // [n] union-find forest in id space (root = min id)
     uint8_t* bad;          // [n] cluster (root) has a blocked or RUNNING member
     int32_t* labels;       // [n]
+    uint8_t* blkid;        // [n] blocked verdict per id (IDLE agents; 0 otherwise)
     unsigned long long* digest;   // [n] perception digests (AM_DIGEST)
     unsigned long long* rkey[2];  // [n] ready keys (ping-pong)
     uint32_t* rval[2];            // [n] ready ids (ping-pong)

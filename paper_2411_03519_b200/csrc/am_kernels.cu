@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
     d.rank[i] = rank;
     d.parent[i] = (uint32_t)i;
     d.bad[i] = 0;
+    d.blkid[i] = 0;
     if (i < kEdgeStripes) {
         d.edge_ctr[i] = 0;
         d.item_ctr[i] = 0;
@@ -1059,6 +1060,7 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
     const uint32_t root = uf_find(d.parent, aid);
     d.labels[aid] = (int32_t)root;
     const bool blk = d.blk8[r] == 1;
+    d.blkid[aid] = blk && A.w == ST_IDLE;
     if (blk || A.w == ST_RUNNING) d.bad[root] = 1;
 }
 
@@ -1374,6 +1376,7 @@ __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mas
         slab[t] = lab;
         mask[lo + t] = rdy;
         d.labels[lo + t] = lab < 0 ? -1 : lo + lab;
+        d.blkid[lo + t] = blocked && sst[t] == ST_IDLE;
         if (d.flags & AM_DIGEST) d.digest[lo + t] = dig;
         if (rdy && !peek) d.status[c][lo + t] = ST_RUNNING;
         if (rdy && lab == t) atomicAdd(&s_ncl, 1u);

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     names = set()
-    for h in ("am.h", "am_driver.h"):
+    for h in ("am.h", "am_driver.h", "am_slab.h"):
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         for m in re.finditer(r"^\s*(?:const\s+)?[\w\s\*]+?\b(am_\w+)\s*\(", src, flags=re.M):
