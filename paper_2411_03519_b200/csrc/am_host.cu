@@ -23,7 +23,9 @@ __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
 __global__ void k_sort_pass(Dev d, int pass, int32_t* order);
 __global__ void k_small(Dev d, uint8_t* mask, int32_t* order);
-__global__ void k_round_begin(Ctl* ctl);
+__global__ void k_round_begin(Dev d);
+__global__ void k_efilter(Dev d);
+__global__ void k_digest(Dev d, const int32_t* order);
 
 __global__ void k_copy_status(Dev d, uint8_t* out)
 {
@@ -148,7 +150,7 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 2 : 12 + c->sort_passes_max;   // incl. k_round_begin, k_near, k_far1/2, k_union
+    return c->path == 0 ? 2 : 13 + c->sort_passes_max + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -264,7 +266,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
     size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
-           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0, o_fctr = 0;
+           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0, o_fctr = 0, o_wq = 0;
     const size_t NC = (size_t)d.ncells;
     if (x->path == 1) {
         o_key = take(4 * N); o_rank = take(4 * N);
@@ -276,14 +278,16 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_tc = take(8 * (size_t)x->ntiles_cells); o_tr = take(8 * (size_t)x->ntiles_ready);
         o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * 256);
         o_gh = take(4 * kMaxSortPasses * 256); o_gs = take(4 * kMaxSortPasses * 256);
-        d.edge_cap = (int)std::max<size_t>(256, (2 * N + kEdgeStripes - 1) / kEdgeStripes);
+        d.ecap = (int)(3 * N + 4096);
+        d.wq_cap = (int)((((N + 31) / 32 + kEdgeStripes - 1) / kEdgeStripes) * 32 + 32);
         o_wit = take(4 * N); o_lrs = take(4 * N);
         // a stripe receives the records of the blocks b with b % 64 == stripe
         d.farq_cap = (int)(((blocks(n, 256) + kEdgeStripes - 1) / kEdgeStripes) * 256);
         o_farq = take(4 * (size_t)kEdgeStripes * d.farq_cap); o_fctr = take(4 * kEdgeStripes);
         d.item_cap = (int)std::max<size_t>(1024, (4 * N + kEdgeStripes - 1) / kEdgeStripes);
         o_items = take(8 * (size_t)kEdgeStripes * d.item_cap); o_ictr = take(4 * kEdgeStripes);
-        o_edges = take(8 * (size_t)kEdgeStripes * d.edge_cap); o_ectr = take(4 * kEdgeStripes);
+        o_edges = take(8 * 2 * (size_t)d.ecap); o_ectr = take(4 * kEdgeStripes);
+        o_wq = take(4 * (size_t)kEdgeStripes * d.wq_cap);
     }
     x->ws_bytes = off;
     cudaError_t e = cudaMalloc(&x->ws, off);
@@ -303,14 +307,14 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.key = (uint32_t*)(b + o_key); d.rank = (uint32_t*)(b + o_rank);
         d.cnt = (uint32_t*)(b + o_cnt); d.cmin = (int32_t*)(b + o_cmin);
         d.ctab = (int2*)(b + o_ctab); d.lmin1 = (int32_t*)(b + o_l1); d.lmin2 = (int32_t*)(b + o_l2);
-        d.rec = (int4*)(b + o_rec); d.blk8 = (uint8_t*)(b + o_blk);
+        d.rec = (int4*)(b + o_rec); d.v8 = (uint8_t*)(b + o_blk);
         d.parent = (uint32_t*)(b + o_par); d.bad = (uint8_t*)(b + o_bad);
         d.rkey[0] = (unsigned long long*)(b + o_rk0); d.rkey[1] = (unsigned long long*)(b + o_rk1);
         d.rval[0] = (uint32_t*)(b + o_rv0); d.rval[1] = (uint32_t*)(b + o_rv1);
         d.tiles_c = (unsigned long long*)(b + o_tc); d.tiles_r = (unsigned long long*)(b + o_tr);
         d.tiles_sort = (unsigned long long*)(b + o_tsort);
         d.ghist = (uint32_t*)(b + o_gh); d.gstart = (uint32_t*)(b + o_gs);
-        d.edges = (uint2*)(b + o_edges); d.edge_ctr = (uint32_t*)(b + o_ectr);
+        d.edges = (uint2*)(b + o_edges); d.wq_ctr = (uint32_t*)(b + o_ectr); d.wq = (uint32_t*)(b + o_wq);
         d.witness = (uint32_t*)(b + o_wit); d.lrstep = (int32_t*)(b + o_lrs); d.farq = (uint32_t*)(b + o_farq); d.farq_ctr = (uint32_t*)(b + o_fctr);
         d.items = (uint2*)(b + o_items); d.item_ctr = (uint32_t*)(b + o_ictr);
     }
@@ -422,7 +426,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         __VA_ARGS__;           \
         am_prof_end(c, id);    \
     } while (0)
-    k_round_begin<<<1, 1, 0, s>>>(d.ctl);
+    k_round_begin<<<1, 1, 0, s>>>(d);
     if (c->path == 0) {
         LAUNCH(K_SMALL, (k_small<<<d.n_sims, c->small_threads, 0, s>>>(d, mask, order)));
     } else {
@@ -434,14 +438,17 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             LAUNCH(K_SCAN, (k_scan_thread<<<nb, 256, 0, s>>>(d)));
         else
         {
-            LAUNCH(K_NEAR, (k_near<<<nb, 256, 0, s>>>(d)));
+            const unsigned pers = (unsigned)c->num_sms * 8;   // persistent grid-stride kernels
+            // coupling edges of unchanged pairs carried over; scan of the work queue
+            LAUNCH(K_NEAR, (k_efilter<<<std::min(blocks(d.ecap, 256), pers), 256, 0, s>>>(d),
+                            k_near<<<std::min(nb, pers), 256, 0, s>>>(d)));
             // far phase over the compacted queue: pyramid levels, then one thread per
-            // surviving (agent, 4x4-cell block) item; persistent grid-stride
+            // surviving (agent, 4x4-cell block) item
             am_prof_begin(c, K_SCAN);
-            k_far1<<<std::min<unsigned>(nb, (unsigned)c->num_sms * 8), 256, 0, s>>>(d);
-            k_far2<<<std::min<unsigned>(nb, (unsigned)c->num_sms * 8), 256, 0, s>>>(d);
+            k_far1<<<std::min(nb, pers), 256, 0, s>>>(d);
+            k_far2<<<std::min(nb, pers), 256, 0, s>>>(d);
             am_prof_end(c, K_SCAN);
-            LAUNCH(K_UNION, (k_union<<<blocks((long long)kEdgeStripes * d.edge_cap, 256), 256, 0, s>>>(d)));
+            LAUNCH(K_UNION, (k_union<<<std::min(blocks(d.ecap, 256), pers), 256, 0, s>>>(d)));
         }
         LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));
         LAUNCH(K_READY, (k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask)));
@@ -450,6 +457,8 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         for (int p = 0; p < c->sort_passes_max; p++)
             k_sort_pass<<<c->ntiles_sort, 1024, 0, s>>>(d, p, order);
         am_prof_end(c, K_SORT_PASS);
+        // perception digests of the dispatched agents (replay driver)
+        if (d.flags & AM_DIGEST) k_digest<<<nb, 256, 0, s>>>(d, order);
     }
 #undef LAUNCH
     CK(c, cudaGetLastError());

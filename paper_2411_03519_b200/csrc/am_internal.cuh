@@ -18,9 +18,11 @@ constexpr int kCellsPerTile = 4096;       // cell-table scan tile (256 threads x
 constexpr int kReadyTile = 2048;          // ready compaction tile (256 threads x 8 agents)
 constexpr int kSortTile = 8192;           // radix pass tile (1024 threads x 8 keys)
 constexpr int kMaxSortPasses = 8;
-constexpr int kIngestItems = 4;
-constexpr int kEdgeStripes = 64;          // global coupling-edge lists          // agents per thread in k_ingest / k_commit
+constexpr int kIngestItems = 4;           // agents per thread in k_ingest / k_commit
+constexpr int kEdgeStripes = 64;          // striped queues (one atomic counter per stripe)
+constexpr int kEdgeStage = 128;           // coupling edges staged per warp before appending
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+constexpr int kRecChanged = 0x10;         // record status byte: agent's step changed since last round
 constexpr uint32_t kRClamp = 46340u;      // >= every distance on a 32768^2 map; R^2 < 2^31
 
 enum : int32_t { ERR_BOUNDS = 1, ERR_PROTOCOL = 2, ERR_VELOCITY = 4 };
@@ -43,16 +45,17 @@ struct Ctl {
     int32_t  n_active, n_running;
     int32_t  n_ready, n_clusters;
     int32_t  npasses;      // radix passes needed by this round's ready keys
-    int32_t  full;         // recompute every blocking verdict this round
-    int32_t  far_count;    // records queued for the far phase
-    int32_t  pad1;
+    int32_t  full;         // recompute every verdict / coupling edge this round
+    int32_t  full_next;    // force a full round next time (edge list overflowed, ablation scan)
+    uint32_t ecur;         // which coupling-edge list is current
+    uint32_t ecnt[2];      // edges in each list
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
     unsigned long long sort_or;   // OR of all ready keys
     // scan statistics (AM_STATS): cells visited, candidate pairs, phase-2 agents,
     // pyramid blocks tested (16x16, 4x4)
     unsigned long long st_cells, st_cand, st_p2, st_b2, st_b1, st_blocked;
-    Chain ingest, bin, cells, ready, hist, small_, pass[kMaxSortPasses];
+    Chain ingest, bin, cells, ready, hist, small_, uni, pass[kMaxSortPasses];
 };
 
 // all device pointers of a context, passed by value to kernels
@@ -77,18 +80,20 @@ struct Dev {
     int32_t* lmin1;        // [ncells/16]  min step per 4x4-cell block
     int32_t* lmin2;        // [ncells/256] min step per 16x16-cell block
     int4* rec;             // [n] sorted records {x | y<<16, step, id, status}
-    uint8_t* blk8;         // [n] blocked verdict per sorted record (0 no, 1 yes, 2 far pending)
+    uint8_t* v8;           // [n] per id: blocking verdict (0 no, 1 yes, 2 far phase pending)
     uint32_t* witness;     // [n] per id: the blocker found last time it was computed
     int32_t* lrstep;       // [n] per id: step at the last round
-    uint32_t* farq;        // [kEdgeStripes][farq_cap] records queued for the far phase
+    uint32_t* farq;        // [kEdgeStripes][farq_cap] agents queued for the far phase
     uint32_t* farq_ctr;    // [kEdgeStripes]
     int32_t farq_cap;      // per stripe (every block of 8 warps maps to one stripe)
-    uint2* items;          // [kEdgeStripes][item_cap] far work items (record, 4x4-block key)
+    uint2* items;          // [kEdgeStripes][item_cap] far work items (agent, 4x4-block key)
     uint32_t* item_ctr;    // [kEdgeStripes]
     int32_t item_cap;      // per stripe
-    uint2* edges;          // [kEdgeStripes][edge_cap] coupling edges (a < b)
-    uint32_t* edge_ctr;    // [kEdgeStripes]
-    int32_t edge_cap;      // per stripe
+    uint2* edges;          // [2][ecap] coupling edge lists (a < b), current and next
+    int32_t ecap;
+    uint32_t* wq;          // [kEdgeStripes][wq_cap] work queue of the scan (id | changed<<31)
+    uint32_t* wq_ctr;      // [kEdgeStripes]
+    int32_t wq_cap;
     uint32_t* parent;      // [n] union-find forest in id space (root = min id)
     uint8_t* bad;          // [n] cluster (root) has a blocked or RUNNING member
     int32_t* labels;       // [n]

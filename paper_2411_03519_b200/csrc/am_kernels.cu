@@ -17,6 +17,9 @@
 
 namespace am {
 
+__device__ __forceinline__ bool round_full(const Dev& d);
+__device__ __forceinline__ bool agent_changed(const Dev& d, uint32_t c, uint32_t i);
+
 // ============================================================== am_update: ingest
 // mode 0 = commit (update_agents, Alg. 3 l.11), 1 = initial state,
 // 2 = full state with statuses (snapshot).  Reads state[cur], writes state[1-cur];
@@ -123,28 +126,46 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
 // ============================================================== binned round
 // k_bin: Morton cell key, slot inside the cell (atomic histogram), per-cell min step;
 // also resets the union-find forest and the per-root bad flags for this round.
+// It also builds the scan's work queue (see the incremental scan below): changed agents
+// (step differs from the last round, or a full round) and IDLE agents whose witness
+// changed.
 __global__ void __launch_bounds__(256) k_bin(Dev d)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= d.n) return;
+    const int lane = threadIdx.x & 31;
     const uint32_t c = d.ctl->cur;
-    const uint8_t st = d.status[c][i];
-    uint32_t key = kSentinel, rank = 0;
-    if (st != ST_DONE) {
-        const int2 p = d.pos[c][i];
-        key = morton((uint32_t)p.x >> d.clog, (uint32_t)p.y >> d.clog);
-        rank = atomicAdd(d.cnt + key, 1u);
-        atomicMin(d.cmin + key, d.step[c][i]);
+    bool work = false, chg = false;
+    if (i < d.n) {
+        const uint8_t st = d.status[c][i];
+        uint32_t key = kSentinel, rank = 0;
+        if (st != ST_DONE) {
+            const int2 p = d.pos[c][i];
+            const int s = d.step[c][i];
+            key = morton((uint32_t)p.x >> d.clog, (uint32_t)p.y >> d.clog);
+            rank = atomicAdd(d.cnt + key, 1u);
+            atomicMin(d.cmin + key, s);
+            chg = round_full(d) || d.lrstep[i] != s;
+            work = chg;
+            if (!work && st == ST_IDLE) {
+                const uint32_t w = d.witness[i];
+                work = w != kSentinel && agent_changed(d, c, w);
+            }
+        }
+        d.key[i] = key;
+        d.rank[i] = rank;
+        d.parent[i] = (uint32_t)i;
+        d.bad[i] = 0;
+        d.blkid[i] = 0;
     }
-    d.key[i] = key;
-    d.rank[i] = rank;
-    d.parent[i] = (uint32_t)i;
-    d.bad[i] = 0;
-    d.blkid[i] = 0;
-    if (i < kEdgeStripes) {
-        d.edge_ctr[i] = 0;
-        d.item_ctr[i] = 0;
-        d.farq_ctr[i] = 0;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, work);
+    if (m) {
+        const int stripe = (int)((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kEdgeStripes - 1));
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(d.wq_ctr + stripe, (uint32_t)__popc(m));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (work)
+            d.wq[(size_t)stripe * d.wq_cap + base + __popc(m & ((1u << lane) - 1u))] =
+                (uint32_t)i | (chg ? 0x80000000u : 0u);
     }
 }
 
@@ -223,8 +244,10 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
     if (key == kSentinel) return;
     const uint32_t c = d.ctl->cur;
     const int2 p = d.pos[c][i];
+    const int s = d.step[c][i];
     const uint32_t r = (uint32_t)d.ctab[key].x + d.rank[i];
-    d.rec[r] = make_int4(p.x | (p.y << 16), d.step[c][i], i, d.status[c][i]);
+    const int chg = (round_full(d) || d.lrstep[i] != s) ? kRecChanged : 0;
+    d.rec[r] = make_int4(p.x | (p.y << 16), s, i, d.status[c][i] | chg);
 }
 
 // test every record of cell `key` against agent A; returns true if A got blocked.
@@ -340,7 +363,8 @@ __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
         }
     }
     const unsigned bits = __ballot_sync(0xFFFFFFFFu, blocked);
-    if (r < nact) d.blk8[r] = blocked;
+    if (r < nact) d.v8[(uint32_t)d.rec[r].z] = blocked;
+    if (r == 0) d.ctl->full_next = 1;   // keeps no edge list / witnesses
     if (d.flags & AM_STATS) {
         const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
         const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, np2), c3 = __reduce_add_sync(0xFFFFFFFFu, nb2);
@@ -357,70 +381,17 @@ __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
 }
 
 // ---------------------------------------------------------------------------------
-// k_scan: warp-cooperative time-dilated neighbour scan.
-//
-// One warp per 4x4-cell block (its records are Morton-contiguous).  The block's agents
-// are taken 32 at a time (a "chunk") and share ONE traversal, pruned against the
-// chunk's bounding box and maximum step.  The traversal only collects candidate cells
-// (lane-parallel tests + ballot compaction into a per-warp shared-memory list); full
-// lists are flushed by loading the cells' records into shared memory and testing the
-// (agent x candidate) pairs with every lane busy -- lane l owns agent l % na and
-// candidate l / na of each group, so no per-pair shuffles are needed.
-//   near phase: cells within box distance R_c = r_p + v of the chunk box: coupling
-//               unions, perception digests, blocking tests;
-//   far phase:  agents not yet blocked and ahead of W; cells beyond R_c inside the disk
-//               of radius R_b(max step - W), walked through the 16x16 / 4x4 min-step
-//               pyramid; a block with min step m is skipped if m >= max step or its box
-//               distance to the chunk box exceeds R_b(max step - m) (exact pruning: no
-//               agent inside can block any agent of the chunk).
-constexpr int kScanWarps = 8;
-constexpr int kCellList = 64;     // pending candidate cells per warp
-constexpr int kCandBuf = 128;     // candidate records staged per flush
-constexpr int kEdgeStage = 128;   // coupling edges staged per warp
-
-struct ScanSmem {
-    int4 arec[32];                // the phase's agents (records)
-    int4 crec[kCandBuf];          // candidate records
-    int cstart[kCellList];        // pending cells: first record, count, exclusive prefix
-    int ccount[kCellList];
-    int cpref[kCellList];
-    unsigned long long dig[32];
-    uint2 edges[kEdgeStage];      // coupling edges staged for the edge list
-    int ne;
-};
-
-// Coupling edges found by the scan are not united in place (a union chases parent
-// pointers through L2 and would stall the 31 other lanes of the warp): they are
-// staged per warp and appended to one of kEdgeStripes global edge lists (one atomic
-// per staged batch); k_union unites them with one thread per edge.  An edge that does
-// not fit is united in place (correct, just slower).
-__device__ __forceinline__ void stage_edge(const Dev& d, ScanSmem& sm, uint32_t a, uint32_t b)
-{
-    const int pos = atomicAdd(&sm.ne, 1);
-    if (pos < kEdgeStage) sm.edges[pos] = make_uint2(a, b);
-    else uf_unite(d.parent, a, b);
-}
-__device__ __forceinline__ void flush_edges(const Dev& d, ScanSmem& sm)
-{
-    const int lane = threadIdx.x & 31;
-    __syncwarp();
-    const int ne = min(sm.ne, kEdgeStage);
-    if (ne == 0) return;
-    const int stripe = (blockIdx.x * kScanWarps + (threadIdx.x >> 5)) & (kEdgeStripes - 1);
-    int base = 0;
-    if (lane == 0) base = (int)atomicAdd(d.edge_ctr + stripe, (unsigned)ne);
-    base = __shfl_sync(0xFFFFFFFFu, base, 0);
-    for (int k = lane; k < ne; k += 32) {
-        const uint2 e = sm.edges[k];
-        if (base + k < d.edge_cap) d.edges[(size_t)stripe * d.edge_cap + base + k] = e;
-        else uf_unite(d.parent, e.x, e.y);
-    }
-    __syncwarp();
-    if (lane == 0) sm.ne = 0;
-    __syncwarp();
-}
-
-// R_b(lag)^2 in 32-bit arithmetic: lag >= 1, clamped as rb_radius
+// Incremental scan.  Per round only the agents in the WORK QUEUE
+// built by k_bin are scanned:
+//   * "changed" agents (their step changed since the last round: they committed, or
+//     every agent in a full round): new coupling edges and a fresh
+//     blocking verdict;
+//   * IDLE agents whose recorded blocker (witness) changed: a fresh blocking verdict.
+// Coupling edges between two unchanged agents are carried over from the last round's
+// edge list by k_efilter (an edge depends only on its two endpoints' states).  An
+// IDLE agent whose step did not change keeps "not blocked" (a commit can only remove
+// blocking relations of others, App. A) and keeps "blocked" while its
+// witness is unchanged.  RUNNING agents need no verdict (their cluster is not ready).
 __device__ __forceinline__ uint32_t rb2(int lag, int v, int r_p, int lagcap)
 {
     const uint32_t R = min((uint32_t)min(lag, lagcap) * (uint32_t)v + (uint32_t)(v + r_p), kRClamp);
@@ -433,426 +404,207 @@ __device__ __forceinline__ bool within2(int dx, int dy, uint32_t R2, uint32_t R,
     return (uint32_t)(dx * dx) + (uint32_t)(dy * dy) <= R2;
 }
 
-// Test the phase's na agents (sm.arec) against the pending cells' records.  Returns the
-// per-agent blocked mask (bit a).  kNear: also coupling unions and digests.
-template <bool kNear>
-__device__ __forceinline__ unsigned flush_cells(const Dev& d, ScanSmem& sm, int nc, int na, unsigned blocked,
-                                                unsigned long long& ncand)
+__device__ __forceinline__ bool round_full(const Dev& d)
 {
-    const int lane = threadIdx.x & 31;
-    // exclusive prefix of the counts (nc <= kCellList = 64: two 32-lane scans)
-    int total = 0;
-    for (int c0 = 0; c0 < nc; c0 += 32) {
-        const int k = c0 + lane;
-        const int v = k < nc ? sm.ccount[k] : 0;
-        int incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (k < nc) sm.cpref[k] = total + incl - v;
-        total += __shfl_sync(0xFFFFFFFFu, incl, 31);
-    }
-    __syncwarp();
-    ncand += (unsigned long long)total;
-    const int cpi = 32 / na;                       // candidates per iteration
-    const int my_a = lane % na, my_c = lane / na;  // this lane's agent / candidate slot
-    const int4 A = sm.arec[my_a];
-    const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
-    const uint32_t aid = (uint32_t)A.z;
-    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
-    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-    const uint32_t Rc2 = Rc * Rc, Rp2 = (uint32_t)d.r_p * (uint32_t)d.r_p;
-    for (int f0 = 0; f0 < total; f0 += kCandBuf) {
-        const int nb = min(kCandBuf, total - f0);
-        // stage the records of flat candidates [f0, f0+nb)
-        for (int j = lane; j < nb; j += 32) {
-            const int f = f0 + j;
-            int lo = 0, hi = nc - 1;               // last cell with cpref <= f
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (sm.cpref[mid] <= f) lo = mid; else hi = mid - 1;
-            }
-            sm.crec[j] = d.rec[sm.cstart[lo] + (f - sm.cpref[lo])];
-        }
-        __syncwarp();
-        bool hit = false;
-        unsigned long long dig = 0;
-        if (my_c < cpi && my_a < na) {
-            const bool mine_blocked = (blocked >> my_a) & 1u;
-            for (int c = my_c; c < nb; c += cpi) {
-                const int4 B = sm.crec[c];
-                const uint32_t bid = (uint32_t)B.z;
-                if (bid == aid) continue;
-                const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-                if (kNear && B.y == as) {
-                    if (within2(dx, dy, Rc2, Rc, d.metric)) {
-                        if (aid < bid) stage_edge(d, sm, aid, bid);
-                        if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
-                            dig += digest_term(bid, dx, dy);
-                    }
-                } else if (B.y < as && !mine_blocked && !hit) {
-                    const int lag = as - B.y;
-                    const uint32_t R2 = rb2(lag, d.v, d.r_p, lagcap);
-                    const uint32_t R = min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
-                    hit = within2(dx, dy, R2, R, d.metric);
-                }
-            }
-        }
-        if (kNear) {
-            __syncwarp();
-            if (sm.ne >= kEdgeStage / 2) flush_edges(d, sm);
-        }
-        // fold the lanes' hits onto their agents
-        const unsigned hm = __ballot_sync(0xFFFFFFFFu, hit);
-        for (int k = 0; k < cpi; k++) blocked |= (hm >> (k * na)) & ((na == 32) ? 0xFFFFFFFFu : ((1u << na) - 1u));
-        if (kNear && (d.flags & AM_DIGEST) && dig) atomicAdd(&sm.dig[my_a], dig);
-        __syncwarp();
-        if (!kNear && __popc(blocked) == na) break;    // every far agent blocked
-    }
-    return blocked;
+    // without commit validation positions may change without a step change: no reuse
+    return d.ctl->full != 0 || !(d.flags & AM_VALIDATE);
 }
 
-// append a lane's candidate cell to the pending list; flush when full
-template <bool kNear>
-__device__ __forceinline__ void add_cells(const Dev& d, ScanSmem& sm, bool take, int cb, int cc, int& nc,
-                                          int na, unsigned& blocked, unsigned long long& ncand)
+__device__ __forceinline__ bool agent_changed(const Dev& d, uint32_t c, uint32_t i)
 {
-    const int lane = threadIdx.x & 31;
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
-    if (!m) return;
-    const int cnt = __popc(m);
-    if (nc + cnt > kCellList) {
-        blocked = flush_cells<kNear>(d, sm, nc, na, blocked, ncand);
-        nc = 0;
-    }
-    if (take) {
-        const int pos = nc + __popc(m & ((1u << lane) - 1u));
-        sm.cstart[pos] = cb;
-        sm.ccount[pos] = cc;
-    }
-    __syncwarp();
-    nc += cnt;
+    return d.lrstep[i] != d.step[c][i];
 }
 
-// k_near: the near phase as its own kernel, one thread per sorted record: the (at
-// most 2x2 when cell >= R_c) cells within box distance R_c of the agent.  Coupling
-// unions are staged as edges, perception digests and blocking
-// tests against every agent in those cells.  Threads of one warp hold
-// Morton-consecutive agents, so they mostly read the same cell entries and records.
-struct NearSmem {
-    uint2 edges[kEdgeStage];
+// append one coupling edge (a < b) to the next edge list; a warp stages its edges in
+// shared memory and reserves space with one atomic per batch
+struct EdgeStage {
+    uint2 e[kEdgeStage];
     int ne;
 };
-__device__ __forceinline__ void stage_edge_n(const Dev& d, NearSmem& sm, uint32_t a, uint32_t b)
+__device__ __forceinline__ void stage_edge(const Dev& d, EdgeStage& sm, uint32_t a, uint32_t b)
 {
     const int pos = atomicAdd(&sm.ne, 1);
-    if (pos < kEdgeStage) sm.edges[pos] = make_uint2(a, b);
-    else uf_unite(d.parent, a, b);
+    if (pos < kEdgeStage) sm.e[pos] = make_uint2(a, b);
+    else uf_unite(d.parent, a, b);                 // staging full: unite in place
 }
-
-__global__ void __launch_bounds__(256, 6) k_near(Dev d)
+__device__ __forceinline__ void flush_stage(const Dev& d, EdgeStage& sm, int lane)
 {
-    __shared__ NearSmem s_all[8];
-    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    NearSmem& sm = s_all[wq];
-    if (lane == 0) sm.ne = 0;
     __syncwarp();
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nact = d.ctl->n_active;
-    const int W = d.ctl->W;
-    // without commit validation positions may change without a step change: no reuse
-    const bool full = d.ctl->full != 0 || !(d.flags & AM_VALIDATE);
-    bool nblk = false, farq = false;
-    if (r < nact) {
-        const int4 A = d.rec[r];
-        const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
-        const uint32_t aid = (uint32_t)A.z;
-        // Which blocking verdict must be recomputed (incremental
-        // blocking): only IDLE agents' verdicts matter (a RUNNING member makes its
-        // cluster not ready anyway).  A commit can only remove blocking relations of
-        // other agents, so an IDLE agent unchanged since the last round keeps its
-        // verdict unless its recorded blocker (witness) committed since.
-        const bool idle = A.w == ST_IDLE;
-        bool need = false, known = false;
-        if (idle) {
-            if (full || d.lrstep[aid] != as) {
-                need = true;
+    const int ne = min(sm.ne, kEdgeStage);
+    if (ne) {
+        const uint32_t nxt = d.ctl->ecur ^ 1u;
+        int base = 0;
+        if (lane == 0) base = (int)atomicAdd((uint32_t*)&d.ctl->ecnt[nxt], (uint32_t)ne);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        for (int k = lane; k < ne; k += 32) {
+            const uint2 e = sm.e[k];
+            if (base + k < d.ecap) {
+                d.edges[(size_t)nxt * d.ecap + base + k] = e;
             } else {
-                const uint32_t w = d.witness[aid];
-                if (w == kSentinel) known = false, need = false;
-                else if (d.lrstep[w] != d.step[d.ctl->cur][w]) need = true;
-                else known = true, need = false;
+                uf_unite(d.parent, e.x, e.y);      // list full: unite now, rebuild next round
+                d.ctl->full_next = 1;
             }
         }
-        nblk = known;
-        uint32_t wit = kSentinel;
-        const int cl = d.clog, G = 1 << d.glog;
-        const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-        const uint32_t Rc2 = Rc * Rc, Rp2 = (uint32_t)d.r_p * (uint32_t)d.r_p;
-        const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
-        const bool test_blk = need;
-        unsigned long long dig = 0;
-        const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
-        const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
-        for (int cy = cy0; cy <= cy1; cy++)
-            for (int cx = cx0; cx <= cx1; cx++) {
-                if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rc,
-                                d.metric))
-                    continue;
-                const uint32_t key = morton(cx, cy);
-                const int2 e = d.ctab[key];
-                if (e.y > as) continue;
-                const int e1 = d.ctab[key + 1].x;
-                for (int b = e.x; b < e1; b++) {
-                    const int4 B = d.rec[b];
-                    const uint32_t bid = (uint32_t)B.z;
-                    if (bid == aid) continue;
-                    const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-                    if (B.y == as) {
-                        if (within2(dx, dy, Rc2, Rc, d.metric)) {
-                            if (aid < bid) stage_edge_n(d, sm, aid, bid);
-                            if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
-                                dig += digest_term(bid, dx, dy);
-                        }
-                    } else if (test_blk && !nblk && B.y < as) {
-                        const int lag = as - B.y;
-                        const uint32_t R =
-                            min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
-                        if (within2(dx, dy, R * R, R, d.metric)) {
-                            nblk = true;
-                            wit = bid;
+    }
+    __syncwarp();
+    if (lane == 0) sm.ne = 0;
+    __syncwarp();
+}
+
+// k_efilter: carry over last round's coupling edges whose endpoints both kept their
+// state (nothing in a full round).  One atomic per block.
+__global__ void __launch_bounds__(256) k_efilter(Dev d)
+{
+    const uint32_t cur = d.ctl->ecur, c = d.ctl->cur;
+    const int ne = min((int)d.ctl->ecnt[cur], d.ecap);
+    const bool full = round_full(d);
+    __shared__ uint32_t s_cnt, s_base;
+    const int lane = threadIdx.x & 31;
+    for (int base = blockIdx.x * 256; base < ne; base += gridDim.x * 256) {
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        const int k = base + threadIdx.x;
+        bool keep = false;
+        uint2 e = make_uint2(0, 0);
+        if (k < ne && !full) {
+            e = d.edges[(size_t)cur * d.ecap + k];
+            keep = !agent_changed(d, c, e.x) && !agent_changed(d, c, e.y);
+        }
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
+        uint32_t wb = 0;
+        if (lane == 0 && m) wb = atomicAdd(&s_cnt, (uint32_t)__popc(m));
+        wb = __shfl_sync(0xFFFFFFFFu, wb, 0);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_cnt) s_base = atomicAdd((uint32_t*)&d.ctl->ecnt[cur ^ 1u], s_cnt);
+        __syncthreads();
+        if (keep) {
+            const uint32_t pos = s_base + wb + __popc(m & ((1u << lane) - 1u));
+            d.edges[(size_t)(cur ^ 1u) * d.ecap + pos] = e;   // kept <= previous count <= ecap
+        }
+        __syncthreads();
+    }
+}
+
+// k_near: one thread per queued agent A (id, bit 31 = changed): the (at most 2x2 when
+// cell >= R_c) cells within box distance R_c: coupling edges for changed agents
+// (once per pair: from the smaller id when both changed), near blocking test for
+// IDLE agents with the blocker recorded as witness; agents still
+// unblocked and ahead of W go to the far queue.
+__global__ void __launch_bounds__(256, 6) k_near(Dev d)
+{
+    __shared__ EdgeStage s_all[8];
+    __shared__ int s_pref[kEdgeStripes + 1];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    EdgeStage& sm = s_all[wq];
+    if (lane == 0) sm.ne = 0;
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int k = 0; k < kEdgeStripes; k++) {
+            s_pref[k] = acc;
+            acc += (int)d.wq_ctr[k];
+        }
+        s_pref[kEdgeStripes] = acc;
+    }
+    __syncthreads();
+    const int nq = s_pref[kEdgeStripes];
+    const uint32_t c = d.ctl->cur;
+    const int W = d.ctl->W;
+    const bool full = round_full(d);
+    const int cl = d.clog, G = 1 << d.glog;
+    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const uint32_t Rc2 = Rc * Rc;
+    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+    // grid-stride over the queue; every warp iteration is warp-uniform in trip count
+    for (int q0 = blockIdx.x * blockDim.x; q0 < nq; q0 += gridDim.x * blockDim.x) {
+        const int q = q0 + threadIdx.x;
+        bool farq = false;
+        uint32_t aid = 0;
+        if (q < nq) {
+            int lo = 0, hi = kEdgeStripes - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t w = d.wq[(size_t)lo * d.wq_cap + (q - s_pref[lo])];
+            aid = w & 0x7FFFFFFFu;
+            const bool chg = (w >> 31) != 0;
+            const int2 P = d.pos[c][aid];
+            const int ax = P.x, ay = P.y, as = d.step[c][aid];
+            const bool idle = d.status[c][aid] == ST_IDLE;
+            bool nblk = false;
+            uint32_t wit = kSentinel;
+            const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
+            const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
+            for (int cy = cy0; cy <= cy1; cy++)
+                for (int cx = cx0; cx <= cx1; cx++) {
+                    if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rc,
+                                    d.metric))
+                        continue;
+                    const uint32_t key = morton(cx, cy);
+                    const int2 e = d.ctab[key];
+                    if (e.y > as) continue;
+                    const int e1 = d.ctab[key + 1].x;
+                    for (int b = e.x; b < e1; b++) {
+                        const int4 B = d.rec[b];
+                        const uint32_t bid = (uint32_t)B.z;
+                        if (bid == aid) continue;
+                        const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                        if (B.y == as) {
+                            // B's record carries its changed bit (k_scatter)
+                            if (chg && within2(dx, dy, Rc2, Rc, d.metric) &&
+                                (full || !(B.w & kRecChanged) || aid < bid))
+                                stage_edge(d, sm, min(aid, bid), max(aid, bid));
+                        } else if (idle && !nblk && B.y < as) {
+                            const int lag = as - B.y;
+                            const uint32_t R =
+                                min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
+                            if (within2(dx, dy, R * R, R, d.metric)) {
+                                nblk = true;
+                                wit = bid;
+                            }
                         }
                     }
                 }
+            if (idle) {
+                if (nblk) {
+                    d.v8[aid] = 1;
+                    d.witness[aid] = wit;
+                } else if (as > W && !(d.flags & AM_DBG_SKIP_FAR)) {
+                    d.v8[aid] = 2;          // far phase decides
+                    farq = true;
+                } else {
+                    d.v8[aid] = 0;
+                    d.witness[aid] = kSentinel;
+                }
             }
-        // blk8: 0 = not blocked, 1 = blocked, 2 = not blocked so far, far phase needed
-        uint8_t code = nblk ? 1 : 0;
-        if (need) {
-            if (nblk) d.witness[aid] = wit;
-            else if (as > W && !(d.flags & AM_DBG_SKIP_FAR)) code = 2;
-            else d.witness[aid] = kSentinel;
         }
-        d.blk8[r] = code;
-        if (d.flags & AM_DIGEST) d.digest[aid] = dig;
-        farq = code == 2;
-    }
-    // queue the records that need the far phase: one atomic per warp on one of the
-    // striped queue counters (no block-wide barrier)
-    {
+        flush_stage(d, sm, lane);
+        // far queue: one atomic per warp on a striped counter
         const unsigned m = __ballot_sync(0xFFFFFFFFu, farq);
         if (m) {
             const int stripe = (blockIdx.x * 8 + wq) & (kEdgeStripes - 1);
             uint32_t wbase = 0;
             if (lane == 0) wbase = atomicAdd(d.farq_ctr + stripe, (uint32_t)__popc(m));
             wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
-            if (farq) d.farq[(size_t)stripe * d.farq_cap + wbase + __popc(m & ((1u << lane) - 1u))] = (uint32_t)r;
-        }
-    }
-    // append the warp's staged edges to a global stripe
-    __syncwarp();
-    const int ne = min(sm.ne, kEdgeStage);
-    if (ne) {
-        const int stripe = (blockIdx.x * 8 + wq) & (kEdgeStripes - 1);
-        int base = 0;
-        if (lane == 0) base = (int)atomicAdd(d.edge_ctr + stripe, (unsigned)ne);
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
-        for (int k = lane; k < ne; k += 32) {
-            const uint2 e = sm.edges[k];
-            if (base + k < d.edge_cap) d.edges[(size_t)stripe * d.edge_cap + base + k] = e;
-            else uf_unite(d.parent, e.x, e.y);
-        }
-    }
-    if (d.flags & AM_STATS) {
-        const unsigned nbk = __popc(__ballot_sync(0xFFFFFFFFu, nblk));
-        if (lane == 0 && nbk) atomicAdd(&d.ctl->st_blocked, (unsigned long long)nbk);
-    }
-}
-
-// one near-phase pair (agent A in registers, candidate record B)
-__device__ __forceinline__ void near_pair(const Dev& d, ScanSmem& sm, const int4 B, int ax, int ay, int as,
-                                          uint32_t aid, int lagcap, uint32_t Rc, uint32_t Rc2, uint32_t Rp2,
-                                          bool& nblk, unsigned long long& dig)
-{
-    const uint32_t bid = (uint32_t)B.z;
-    if (bid == aid) return;
-    const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-    if (B.y == as) {
-        if (within2(dx, dy, Rc2, Rc, d.metric)) {
-            if (aid < bid) stage_edge(d, sm, aid, bid);
-            if ((d.flags & AM_DIGEST) && within2(dx, dy, Rp2, (uint32_t)d.r_p, d.metric))
-                dig += digest_term(bid, dx, dy);
-        }
-    } else if (!nblk && B.y < as) {
-        const int lag = as - B.y;
-        const uint32_t R = min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
-        nblk = within2(dx, dy, R * R, R, d.metric);
-    }
-}
-
-__global__ void __launch_bounds__(256, 3) k_scan(Dev d)
-{
-    __shared__ ScanSmem s_all[kScanWarps];
-    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    ScanSmem& sm = s_all[wq];
-    const int W = d.ctl->W;
-    const int cl = d.clog, G = 1 << d.glog;
-    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-    unsigned long long ncand = 0;
-    uint32_t ncells = 0, np2 = 0, nb2 = 0, nb1 = 0;
-    // persistent warps: 4x4-cell blocks (key >> 4) strided over all warps of the grid
-    const int nblocks = d.ncells >> 4, nwarps = gridDim.x * kScanWarps;
-    for (int blk = blockIdx.x * kScanWarps + wq; blk < nblocks; blk += nwarps) {
-    const int beg = d.ctab[blk * 16].x, end = d.ctab[blk * 16 + 16].x;
-    for (int base = beg; base < end; base += 32) {
-        const int r = base + lane;
-        const bool valid = r < end;
-        const int4 A = valid ? d.rec[r] : make_int4(0, INT_MIN, -1, 0);
-        const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
-        const int na = min(32, end - base);
-        sm.arec[lane] = A;
-        sm.dig[lane] = 0;
-        if (lane == 0) sm.ne = 0;
-        __syncwarp();
-        const int x0 = __reduce_min_sync(0xFFFFFFFFu, valid ? ax : INT_MAX);
-        const int x1 = __reduce_max_sync(0xFFFFFFFFu, valid ? ax : INT_MIN);
-        const int y0 = __reduce_min_sync(0xFFFFFFFFu, valid ? ay : INT_MAX);
-        const int y1 = __reduce_max_sync(0xFFFFFFFFu, valid ? ay : INT_MIN);
-        // near-phase verdicts from k_near
-        const bool nblk = valid && d.blk8[r] != 0;
-        unsigned blocked = __ballot_sync(0xFFFFFFFFu, nblk);
-        int nc = 0;
-        const bool my_blocked = valid && ((blocked >> lane) & 1u);
-        // ---- far phase: agents not blocked yet and ahead of the watermark
-        const bool open = valid && !my_blocked && as > W && !(d.flags & AM_DBG_SKIP_FAR);
-        const unsigned om = __ballot_sync(0xFFFFFFFFu, open);
-        bool far_blocked = false;
-        if (om) {
-            const int nf = __popc(om);
-            np2 += open;
-            // compact the open agents into arec[0..nf)
-            const int4 Amine = A;
-            __syncwarp();
-            if (open) sm.arec[__popc(om & ((1u << lane) - 1u))] = Amine;
-            __syncwarp();
-            const int fmax = __reduce_max_sync(0xFFFFFFFFu, open ? as : INT_MIN);
-            const int fx0 = __reduce_min_sync(0xFFFFFFFFu, open ? ax : INT_MAX);
-            const int fx1 = __reduce_max_sync(0xFFFFFFFFu, open ? ax : INT_MIN);
-            const int fy0 = __reduce_min_sync(0xFFFFFFFFu, open ? ay : INT_MAX);
-            const int fy1 = __reduce_max_sync(0xFFFFFFFFu, open ? ay : INT_MIN);
-            const int R = (int)rb_radius((long long)fmax - W, d.v, d.r_p);
-            const int l2 = cl + 4, l1 = cl + 2, G2 = G >> 4;
-            const int bx0 = max(0, (fx0 - R) >> l2), bx1 = min(G2 - 1, (fx1 + R) >> l2);
-            const int by0 = max(0, (fy0 - R) >> l2), by1 = min(G2 - 1, (fy1 + R) >> l2);
-            const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);
-            unsigned fb = 0;      // bit j: open agent j blocked
-            for (int q0 = 0; q0 < nb && __popc(fb) < nf; q0 += 32) {
-                const int qq = q0 + lane;
-                bool keep2 = false;
-                int bx = 0, by = 0;
-                if (qq < nb) {
-                    bx = bx0 + qq % nbx;
-                    by = by0 + qq / nbx;
-                    const int m2 = d.lmin2[morton(bx, by)];
-                    keep2 = m2 < fmax &&
-                            box_dist_within(fx0, fy0, fx1, fy1, bx << l2, by << l2, ((bx + 1) << l2) - 1,
-                                            ((by + 1) << l2) - 1, rb_radius((long long)fmax - m2, d.v, d.r_p),
-                                            d.metric);
-                    nb2++;
-                }
-                unsigned todo2 = __ballot_sync(0xFFFFFFFFu, keep2);
-                while (todo2 && __popc(fb) < nf) {
-                    const int src2 = __ffs(todo2) - 1;
-                    todo2 &= todo2 - 1;
-                    const int BX = __shfl_sync(0xFFFFFFFFu, bx, src2), BY = __shfl_sync(0xFFFFFFFFu, by, src2);
-                    bool keep1 = false;
-                    const int qx = BX * 4 + (lane & 3), qy = BY * 4 + ((lane >> 2) & 3);
-                    if (lane < 16) {
-                        const int m1 = d.lmin1[morton(qx, qy)];
-                        keep1 = m1 < fmax &&
-                                box_dist_within(fx0, fy0, fx1, fy1, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
-                                                ((qy + 1) << l1) - 1, rb_radius((long long)fmax - m1, d.v, d.r_p),
-                                                d.metric);
-                        nb1++;
-                    }
-                    unsigned todo1 = __ballot_sync(0xFFFFFFFFu, keep1);
-                    while (todo1 && __popc(fb) < nf) {
-                        // two 4x4 blocks per iteration: lanes 0-15 the first, 16-31 the second
-                        const int s1a = __ffs(todo1) - 1;
-                        todo1 &= todo1 - 1;
-                        int s1b = -1;
-                        if (todo1) {
-                            s1b = __ffs(todo1) - 1;
-                            todo1 &= todo1 - 1;
-                        }
-                        const int srcb = (lane < 16 || s1b < 0) ? s1a : s1b;
-                        const int QX = __shfl_sync(0xFFFFFFFFu, qx, srcb), QY = __shfl_sync(0xFFFFFFFFu, qy, srcb);
-                        const int cx = QX * 4 + (lane & 3), cy = QY * 4 + ((lane >> 2) & 3);
-                        int cb = 0, cc = 0;
-                        bool take = false;
-                        if (lane < 16 || s1b >= 0) {
-                            const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
-                            // (cells the near phase covered are re-tested for blocking only:
-                            // harmless, the per-agent near sets differ across the chunk)
-                            {
-                                const uint32_t key = morton(cx, cy);
-                                const int2 e = d.ctab[key];
-                                if (e.y < fmax &&
-                                    box_dist_within(fx0, fy0, fx1, fy1, X0, Y0, X1, Y1,
-                                                    rb_radius((long long)fmax - e.y, d.v, d.r_p), d.metric)) {
-                                    cb = e.x;
-                                    cc = d.ctab[key + 1].x - e.x;
-                                    take = cc > 0;
-                                }
-                            }
-                            ncells++;
-                        }
-                        add_cells<false>(d, sm, take, cb, cc, nc, nf, fb, ncand);
-                    }
-                }
-            }
-            if (nc && __popc(fb) < nf) fb = flush_cells<false>(d, sm, nc, nf, fb, ncand);
-            nc = 0;
-            if (open) far_blocked = (fb >> __popc(om & ((1u << lane) - 1u))) & 1u;
-        }
-        if (far_blocked) d.blk8[r] = 1;
-        if (d.flags & AM_STATS) {
-            const unsigned nbk = __popc(__ballot_sync(0xFFFFFFFFu, far_blocked));
-            if (lane == 0 && nbk) atomicAdd(&d.ctl->st_blocked, (unsigned long long)nbk);
-        }
-    }
-    }
-    if (d.flags & AM_STATS) {
-        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells);
-        const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, np2), c3 = __reduce_add_sync(0xFFFFFFFFu, nb2);
-        const unsigned c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
-        if (lane == 0) {
-            atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
-            atomicAdd(&d.ctl->st_cand, ncand);                 // warp-uniform
-            atomicAdd(&d.ctl->st_p2, (unsigned long long)c2);
-            atomicAdd(&d.ctl->st_b2, (unsigned long long)c3);
-            atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
+            if (farq) d.farq[(size_t)stripe * d.farq_cap + wbase + __popc(m & ((1u << lane) - 1u))] = aid;
         }
     }
 }
 
-// k_far: the far (time-dilated) phase, one thread per sorted record that k_near left
-// unblocked and that is ahead of the watermark W.  The thread walks the min-step
-// pyramid with ITS OWN point and step: a 16x16-cell block, 4x4-cell block or cell
-// with min step m is skipped if m >= s_A or its box distance exceeds R_b(s_A - m)
-// (exact pruning: nothing inside can block A).  The 16 children of a block are
-// Morton-contiguous, so each level is fetched with a few 16-byte vector loads (one
-// L2 round trip) instead of 16 dependent ones.  Cells within R_c of A were tested
-// completely by k_near and are skipped.
+// k_far: the far (time-dilated) phase for the queued agents.  A walks the min-step
+// pyramid with ITS OWN point and step: a 16x16-cell block, 4x4-cell block or cell with
+// min step m is skipped if m >= s_A or its box distance exceeds R_b(s_A - m) (exact
+// pruning: nothing inside can block A).  The 16 children of a block are
+// Morton-contiguous, so each level is fetched with a few 16-byte vector loads.  Cells
+// within R_c of A were tested completely by k_near and are skipped.
 __device__ __forceinline__ void morton_child(int k, int& dx, int& dy)
 {
     dx = (k & 1) | ((k >> 1) & 2);
     dy = ((k >> 1) & 1) | ((k >> 2) & 2);
 }
 
-// test agent A against the cells of one 4x4-cell block (Morton key k1g at block
-// coordinates qx, qy); returns the id of a blocker or kSentinel
+// test A against the cells of one 4x4-cell block (Morton key k1g at block coordinates
+// qx, qy); returns the id of a blocker or kSentinel
 __device__ __forceinline__ uint32_t far_block(const Dev& d, uint32_t k1g, int qx, int qy, int ax, int ay, int as,
                                               uint32_t Rc, int lagcap, uint32_t& ncells, uint32_t& ncand)
 {
@@ -888,11 +640,10 @@ __device__ __forceinline__ uint32_t far_block(const Dev& d, uint32_t k1g, int qx
     return kSentinel;
 }
 
-// k_far1: one thread per queued agent: the 16x16- and 4x4-cell levels of the pyramid
-// (vector loads of the 16 Morton-contiguous children), then one work item per
-// surviving 4x4-cell block appended to a striped item list for k_far2, so a leading
-// agent with many candidate blocks is spread over many threads.  If the item list is
-// full the thread tests the block itself.
+// k_far1: one thread per queued agent: the 16x16- and 4x4-cell levels of the pyramid,
+// then one work item per surviving 4x4-cell block appended to a striped item list for
+// k_far2, so a leading agent with many candidate blocks is spread over many threads.
+// If the item list is full the thread tests the block itself.
 __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
 {
     __shared__ int s_pref[kEdgeStripes + 1];
@@ -907,6 +658,7 @@ __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
     __syncthreads();
     const int nq = s_pref[kEdgeStripes];
     const int W = d.ctl->W;
+    const uint32_t c = d.ctl->cur;
     uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
     const int stripe = blockIdx.x & (kEdgeStripes - 1);
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
@@ -915,9 +667,9 @@ __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
             const int mid = (lo + hi + 1) >> 1;
             if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
         }
-        const int r = (int)d.farq[(size_t)lo * d.farq_cap + (q - s_pref[lo])];
-        const int4 A = d.rec[r];
-        const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+        const uint32_t aid = d.farq[(size_t)lo * d.farq_cap + (q - s_pref[lo])];
+        const int2 P = d.pos[c][aid];
+        const int ax = P.x, ay = P.y, as = d.step[c][aid];
         const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
         const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
         const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
@@ -925,7 +677,6 @@ __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
         const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
         const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
         uint32_t wit = kSentinel;
-        d.blk8[r] = 0;
         for (int by = by0; by <= by1 && wit == kSentinel; by++)
             for (int bx = bx0; bx <= bx1 && wit == kSentinel; bx++) {
                 const uint32_t k2 = morton(bx, by);
@@ -962,7 +713,7 @@ __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
                     keep &= keep - 1;
                     const uint32_t k1g = k2 * 16 + (uint32_t)k1;
                     if (base + k < d.item_cap) {
-                        d.items[(size_t)stripe * d.item_cap + base + k] = make_uint2((uint32_t)r, k1g);
+                        d.items[(size_t)stripe * d.item_cap + base + k] = make_uint2(aid, k1g);
                         nitems++;
                     } else {
                         int ox, oy;
@@ -972,8 +723,8 @@ __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
                     k++;
                 }
             }
-        if (wit != kSentinel) d.blk8[r] = 1;
-        d.witness[A.z] = wit;
+        d.v8[aid] = wit != kSentinel ? 1 : 0;
+        d.witness[aid] = wit;
     }
     if (d.flags & AM_STATS) {
         const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
@@ -989,8 +740,8 @@ __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
     }
 }
 
-// k_far2: one thread per (agent, 4x4-cell block) item: its 16 cells (one vector
-// fetch) and the records of the cells that survive the min-step test.
+// k_far2: one thread per (agent, 4x4-cell block) item: its 16 cells (one vector fetch)
+// and the records of the cells that survive the min-step test.
 __global__ void __launch_bounds__(256) k_far2(Dev d)
 {
     __shared__ int s_pref[kEdgeStripes + 1];
@@ -1004,7 +755,8 @@ __global__ void __launch_bounds__(256) k_far2(Dev d)
     }
     __syncthreads();
     const int total = s_pref[kEdgeStripes];
-    uint32_t ncells = 0, ncand = 0, nblk = 0;
+    const uint32_t c = d.ctl->cur;
+    uint32_t ncells = 0, ncand = 0;
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
         int lo = 0, hi = kEdgeStripes - 1;          // last stripe with s_pref <= g
         while (lo < hi) {
@@ -1012,19 +764,18 @@ __global__ void __launch_bounds__(256) k_far2(Dev d)
             if (s_pref[mid] <= g) lo = mid; else hi = mid - 1;
         }
         const uint2 it = d.items[(size_t)lo * d.item_cap + (g - s_pref[lo])];
-        const int r = (int)it.x;
-        if (*(volatile uint8_t*)(d.blk8 + r) == 1) continue;   // another block already blocked it
-        const int4 A = d.rec[r];
-        const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+        const uint32_t aid = it.x;
+        if (*(volatile uint8_t*)(d.v8 + aid) == 1) continue;   // another block already blocked it
+        const int2 P = d.pos[c][aid];
+        const int ax = P.x, ay = P.y, as = d.step[c][aid];
         const uint32_t k1g = it.y;
         const int ox = (int)part_compact(k1g), oy = (int)part_compact(k1g >> 1);
         const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
         const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
         const uint32_t wit = far_block(d, k1g, ox, oy, ax, ay, as, Rc, lagcap, ncells, ncand);
         if (wit != kSentinel) {
-            d.blk8[r] = 1;
-            d.witness[A.z] = wit;
-            nblk++;
+            d.v8[aid] = 1;
+            d.witness[aid] = wit;
         }
     }
     if (d.flags & AM_STATS) {
@@ -1036,17 +787,21 @@ __global__ void __launch_bounds__(256) k_far2(Dev d)
     }
 }
 
-// k_union: unite the staged coupling edges, one thread per edge (ECL-CC style hooking
-// of the larger root under the smaller, so roots stay the minimum id).
+// k_union: unite this round's coupling edges (carried-over + new), one thread per edge
+// (ECL-CC style hooking of the larger root under the smaller, so roots stay the
+// minimum id); the last block makes the list current for the next round.
 __global__ void __launch_bounds__(256) k_union(Dev d)
 {
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int stripe = (int)(t / d.edge_cap), k = (int)(t % d.edge_cap);
-    if (stripe >= kEdgeStripes) return;
-    const int ne = min((int)d.edge_ctr[stripe], d.edge_cap);
-    if (k >= ne) return;
-    const uint2 e = d.edges[(size_t)stripe * d.edge_cap + k];
-    uf_unite(d.parent, e.x, e.y);
+    const uint32_t nxt = d.ctl->ecur ^ 1u;
+    const int ne = min((int)d.ctl->ecnt[nxt], d.ecap);
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ne; k += gridDim.x * blockDim.x) {
+        const uint2 e = d.edges[(size_t)nxt * d.ecap + k];
+        uf_unite(d.parent, e.x, e.y);
+    }
+    if (finish_block(&d.ctl->uni, gridDim.x) && threadIdx.x == 0) {
+        d.ctl->ecur = nxt;
+        __threadfence();
+    }
 }
 
 // k_finalize: label = root of the agent's tree (= min id of its cluster, Q10);
@@ -1059,9 +814,44 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
     const uint32_t aid = (uint32_t)A.z;
     const uint32_t root = uf_find(d.parent, aid);
     d.labels[aid] = (int32_t)root;
-    const bool blk = d.blk8[r] == 1;
-    d.blkid[aid] = blk && A.w == ST_IDLE;
-    if (blk || A.w == ST_RUNNING) d.bad[root] = 1;
+    const uint8_t st = (uint8_t)(A.w & 3);
+    const bool blk = st == ST_IDLE && d.v8[aid] == 1;
+    d.blkid[aid] = blk;
+    if (blk || st == ST_RUNNING) d.bad[root] = 1;
+}
+
+// k_digest: perception digests ("perceives an area within a radius") of the
+// agents dispatched this round, for the replay driver: sum over same-step non-DONE
+// agents within r_p of mix64(id<<32 ^ (u16)dx<<16 ^ (u16)dy).
+__global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict__ order)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= d.ctl->n_ready) return;
+    const uint32_t c = d.ctl->cur;
+    const uint32_t aid = (uint32_t)order[k];
+    const int2 P = d.pos[c][aid];
+    const int ax = P.x, ay = P.y, as = d.step[c][aid];
+    const int cl = d.clog, G = 1 << d.glog;
+    const uint32_t Rp = (uint32_t)d.r_p, Rp2 = Rp * Rp;
+    unsigned long long dig = 0;
+    const int cx0 = max(0, (ax - (int)Rp) >> cl), cx1 = min(G - 1, (ax + (int)Rp) >> cl);
+    const int cy0 = max(0, (ay - (int)Rp) >> cl), cy1 = min(G - 1, (ay + (int)Rp) >> cl);
+    for (int cy = cy0; cy <= cy1; cy++)
+        for (int cx = cx0; cx <= cx1; cx++) {
+            if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rp, d.metric))
+                continue;
+            const uint32_t key = morton(cx, cy);
+            const int2 e = d.ctab[key];
+            if (e.y > as) continue;
+            const int e1 = d.ctab[key + 1].x;
+            for (int b = e.x; b < e1; b++) {
+                const int4 B = d.rec[b];
+                if (B.y != as || (uint32_t)B.z == aid) continue;
+                const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                if (within2(dx, dy, Rp2, Rp, d.metric)) dig += digest_term((uint32_t)B.z, dx, dy);
+            }
+        }
+    d.digest[aid] = dig;
 }
 
 // k_ready: mask, DONE labels, dispatch (IDLE -> RUNNING), and the
@@ -1403,12 +1193,21 @@ __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mas
 }
 
 // reset the per-round counters that the host reads (before the round kernels)
-__global__ void k_round_begin(Ctl* ctl)
+__global__ void k_round_begin(Dev d)
 {
+    Ctl* ctl = d.ctl;
     ctl->epoch += 1;
     ctl->n_ready = 0;
     ctl->n_clusters = 0;
-    ctl->far_count = 0;
+    ctl->full |= ctl->full_next;
+    ctl->full_next = 0;
+    ctl->ecnt[ctl->ecur ^ 1u] = 0;
+    if (d.wq_ctr)
+        for (int k = 0; k < kEdgeStripes; k++) {
+            d.wq_ctr[k] = 0;
+            d.farq_ctr[k] = 0;
+            d.item_ctr[k] = 0;
+        }
 }
 
 }  // namespace am
