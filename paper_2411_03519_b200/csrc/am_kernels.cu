@@ -424,8 +424,19 @@ struct EdgeStage {
 __device__ __forceinline__ void stage_edge(const Dev& d, EdgeStage& sm, uint32_t a, uint32_t b)
 {
     const int pos = atomicAdd(&sm.ne, 1);
-    if (pos < kEdgeStage) sm.e[pos] = make_uint2(a, b);
-    else uf_unite(d.parent, a, b);                 // staging full: unite in place
+    if (pos < kEdgeStage) {
+        sm.e[pos] = make_uint2(a, b);
+        return;
+    }
+    // staging full (dense neighbourhood): append this edge directly
+    const uint32_t nxt = d.ctl->ecur ^ 1u;
+    const uint32_t k = atomicAdd((uint32_t*)&d.ctl->ecnt[nxt], 1u);
+    if ((int)k < d.ecap) {
+        d.edges[(size_t)nxt * d.ecap + k] = make_uint2(a, b);
+    } else {
+        uf_unite(d.parent, a, b);                  // list full: unite now, rebuild next round
+        d.ctl->full_next = 1;
+    }
 }
 __device__ __forceinline__ void flush_stage(const Dev& d, EdgeStage& sm, int lane)
 {
@@ -552,7 +563,7 @@ __global__ void __launch_bounds__(256, 6) k_near(Dev d)
                         if (B.y == as) {
                             // B's record carries its changed bit (k_scatter)
                             if (chg && within2(dx, dy, Rc2, Rc, d.metric) &&
-                                (full || !(B.w & kRecChanged) || aid < bid))
+                                (!(B.w & kRecChanged) || aid < bid))
                                 stage_edge(d, sm, min(aid, bid), max(aid, bid));
                         } else if (idle && !nblk && B.y < as) {
                             const int lag = as - B.y;

@@ -241,8 +241,8 @@ def test_protocol_sequence_matches_oracle_state_machine():
         for rnd in range(12):
             ro = so.round()
             mask, order = tr.ready()
-            np.testing.assert_array_equal(order.cpu().numpy(), ro["order"])
-            np.testing.assert_array_equal(tr.clusters().cpu().numpy(), ro["label"])
+            np.testing.assert_array_equal(order.cpu().numpy(), ro["order"], err_msg=f"{path} round {rnd}")
+            np.testing.assert_array_equal(tr.clusters().cpu().numpy(), ro["label"], err_msg=f"{path} round {rnd}")
             # commit half of the RUNNING agents, moving them by one tile
             run = np.nonzero(so.status == O.RUNNING)[0]
             pick = run[rng.random(len(run)) < 0.5]
