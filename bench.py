@@ -48,10 +48,12 @@ def algorithmic_bytes(kernel: str, s: dict) -> float:
         "k_cells": 24.27 * c,
         # read key 4 + rank 4 + cell start 4 + pos 8 + step 4 + status 1; write record 16
         "k_scatter": 41.0 * a,
-        # near phase: read own record 16 + own cell entry 8; write blocked flag 1 + digest 8
-        "k_near": 33.0 * a,
-        # far phase: read own record 16 + blocked flag 1; write blocked flag 1
-        "k_scan": 18.0 * a,
+        # incremental near phase, per re-scanned agent w: read pos 8 + step 4 + status 1 +
+        # own cell entry 8; write verdict 1 + witness 4 + a new edge 8; carried edges 8 each
+        "k_near": 34.0 * s["n_work"] + 8.0 * s["n_edges"],
+        # far phase, per far-queued agent f: read pos 8 + step 4 + 16x16 / 4x4 level words
+        # 4 + 64; write verdict 1 + witness 4; per work item: 16-cell entry block 136
+        "k_scan": 85.0 * s["n_far"] + 136.0 * s["n_items"],
         # read record 16 + blocked bit 0.125 + parent 4; write label 4
         "k_finalize": 24.125 * a,
         # read status 1 + label 4 + bad 1; write mask 1 + status 1; ready: step 4 + key/id 12
@@ -65,8 +67,8 @@ def algorithmic_bytes(kernel: str, s: dict) -> float:
         "k_disp_b": 52.0 * r,
         # read status 1 (+ tcommit 8 for RUNNING); commit: pos/step/traj r+w
         "k_commit": 1.0 * n + 8.0 * s["n_running"],
-        # read edges 8 per coupled pair (~0.6 per agent) + parent words
-        "k_union": 12.0 * 0.6 * a,
+        # read edge 8 + two parent words per edge
+        "k_union": 16.0 * s["n_edges"],
     }
     return table.get(kernel, 0.0)
 
@@ -234,7 +236,7 @@ def run_ours(args, w, lm):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    st_active, st_ready, st_running = [], [], []
+    st_active, st_ready, st_running, st_work, st_far, st_items, st_edges, st_np = [], [], [], [], [], [], [], []
     if pg:
         pg.barrier()
     torch.cuda.synchronize(dev)
@@ -255,6 +257,11 @@ def run_ours(args, w, lm):
             st_active.append(s["n_active"])
             st_ready.append(nr)
             st_running.append(s["n_running"])
+            st_work.append(s["n_work"])
+            st_far.append(s["n_far"])
+            st_items.append(s["n_items"])
+            st_edges.append(s["n_edges"])
+            st_np.append(s["n_passes"])
     torch.cuda.synchronize(dev)
     if pg:
         pg.barrier()
@@ -314,7 +321,9 @@ def run_ours(args, w, lm):
     # ---- roofline of the dominant kernel
     L = rep.tracker.L
     stats = {"n": n, "n_active": statistics.mean(st_active), "n_ready": statistics.mean(st_ready),
-             "n_running": statistics.mean(st_running), "passes": rep.tracker.L.am_launches_per_round(rep.tracker.ctx) - 12,
+             "n_running": statistics.mean(st_running), "n_work": statistics.mean(st_work),
+             "n_far": statistics.mean(st_far), "n_items": statistics.mean(st_items),
+             "n_edges": statistics.mean(st_edges), "passes": statistics.mean(st_np),
              "ncells": 0}
     # cell count of the binned path: (workspace layout) -- from the config the library chose
     cell = rep.tracker.stats()["cell"]
@@ -351,7 +360,8 @@ def run_ours(args, w, lm):
         "rounds_per_s": rounds_per_s,
         "agent_steps_per_round": agent_steps / args.steps / ws,
         "round_stats": {"active": stats["n_active"], "ready": stats["n_ready"],
-                        "running": stats["n_running"]},
+                        "running": stats["n_running"], "rescanned": stats["n_work"],
+                        "far": stats["n_far"], "far_items": stats["n_items"], "edges": stats["n_edges"]},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg, "avg_launch_us": avg_dom_s * 1e6},

@@ -102,6 +102,11 @@ typedef struct {
     int32_t n_clusters;    /* ready clusters                                              */
     int32_t path;          /* 0 = fused per-simulation kernel, 1 = cell-binned pipeline   */
     int32_t cell;          /* cell edge used by the binned pipeline                       */
+    int32_t n_work;        /* binned: agents re-scanned this round (incremental work queue) */
+    int32_t n_far;         /* binned: agents that needed the far (time-dilated) phase     */
+    int32_t n_items;       /* binned: (agent, 4x4-cell block) far work items              */
+    int32_t n_edges;       /* binned: coupling edges united this round                    */
+    int32_t n_passes;      /* binned: radix passes the priority order needed              */
 } am_round_stats;
 
 /* Create a tracker for n_agents agents on a map_w x map_h tile map (1..32768 each),

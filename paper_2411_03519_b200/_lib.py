@@ -39,7 +39,9 @@ class Config(C.Structure):
 class RoundStats(C.Structure):
     _fields_ = [("n_ready", C.c_int32), ("n_active", C.c_int32), ("n_running", C.c_int32),
                 ("watermark", C.c_int32), ("max_step", C.c_int32), ("n_clusters", C.c_int32),
-                ("path", C.c_int32), ("cell", C.c_int32)]
+                ("path", C.c_int32), ("cell", C.c_int32), ("n_work", C.c_int32),
+                ("n_far", C.c_int32), ("n_items", C.c_int32), ("n_edges", C.c_int32),
+                ("n_passes", C.c_int32)]
 
 
 class SlabGeom(C.Structure):

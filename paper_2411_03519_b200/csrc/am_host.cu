@@ -280,7 +280,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_gh = take(4 * kMaxSortPasses * 256); o_gs = take(4 * kMaxSortPasses * 256);
         d.ecap = (int)(3 * N + 4096);
         d.wq_cap = (int)((((N + 31) / 32 + kEdgeStripes - 1) / kEdgeStripes) * 32 + 32);
-        o_wit = take(4 * N); o_lrs = take(4 * N);
+        o_wit = take(4 * N); o_lrs = take(N);
         // a stripe receives the records of the blocks b with b % 64 == stripe
         d.farq_cap = (int)(((blocks(n, 256) + kEdgeStripes - 1) / kEdgeStripes) * 256);
         o_farq = take(4 * (size_t)kEdgeStripes * d.farq_cap); o_fctr = take(4 * kEdgeStripes);
@@ -315,7 +315,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.tiles_sort = (unsigned long long*)(b + o_tsort);
         d.ghist = (uint32_t*)(b + o_gh); d.gstart = (uint32_t*)(b + o_gs);
         d.edges = (uint2*)(b + o_edges); d.wq_ctr = (uint32_t*)(b + o_ectr); d.wq = (uint32_t*)(b + o_wq);
-        d.witness = (uint32_t*)(b + o_wit); d.lrstep = (int32_t*)(b + o_lrs); d.farq = (uint32_t*)(b + o_farq); d.farq_ctr = (uint32_t*)(b + o_fctr);
+        d.witness = (uint32_t*)(b + o_wit); d.chg8 = (uint8_t*)(b + o_lrs); d.farq = (uint32_t*)(b + o_farq); d.farq_ctr = (uint32_t*)(b + o_fctr);
         d.items = (uint2*)(b + o_items); d.item_ctr = (uint32_t*)(b + o_ictr);
     }
     // initial contents: everything zero except the min-step table
@@ -386,6 +386,11 @@ static void fill_stats(am_ctx* c)
     c->stats.watermark = h.W;
     c->stats.max_step = h.S;
     c->stats.n_clusters = h.n_clusters;
+    c->stats.n_work = h.n_work;
+    c->stats.n_far = h.n_far;
+    c->stats.n_items = h.n_items;
+    c->stats.n_edges = h.n_edges;
+    c->stats.n_passes = h.npasses;
 }
 
 extern "C" int am_sync(am_ctx* c)

@@ -49,6 +49,7 @@ struct Ctl {
     int32_t  full_next;    // force a full round next time (edge list overflowed, ablation scan)
     uint32_t ecur;         // which coupling-edge list is current
     uint32_t ecnt[2];      // edges in each list
+    int32_t  n_work, n_far, n_items, n_edges;   // this round's scan work (stats)
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
     unsigned long long sort_or;   // OR of all ready keys
@@ -82,7 +83,7 @@ struct Dev {
     int4* rec;             // [n] sorted records {x | y<<16, step, id, status}
     uint8_t* v8;           // [n] per id: blocking verdict (0 no, 1 yes, 2 far phase pending)
     uint32_t* witness;     // [n] per id: the blocker found last time it was computed
-    int32_t* lrstep;       // [n] per id: step at the last round
+    uint8_t* chg8;         // [n] per id: step changed since the last round (set by am_update)
     uint32_t* farq;        // [kEdgeStripes][farq_cap] agents queued for the far phase
     uint32_t* farq_ctr;    // [kEdgeStripes]
     int32_t farq_cap;      // per stripe (every block of 8 warps maps to one stripe)
@@ -315,6 +316,47 @@ __device__ __forceinline__ uint32_t chain_scan(unsigned long long* tiles, uint32
         --j;
     }
     st_relaxed(tiles + tile, tile_word(tag, 2, excl + agg));
+    return excl;
+}
+
+// Warp-parallel decoupled look-back: called by ALL 32 lanes of one warp; lane k reads
+// predecessor (j - k), so 32 predecessors are inspected per L2 round trip.  Returns
+// the exclusive prefix in every lane.
+__device__ __forceinline__ uint32_t chain_scan_warp(unsigned long long* tiles, uint32_t tile, uint32_t tag,
+                                                    uint32_t agg)
+{
+    const int lane = threadIdx.x & 31;
+    tag &= 0x3FFFFFFFu;
+    if (tile == 0) {
+        if (lane == 0) st_relaxed(tiles, tile_word(tag, 2, agg));
+        return 0;
+    }
+    if (lane == 0) st_relaxed(tiles + tile, tile_word(tag, 1, agg));
+    uint32_t excl = 0;
+    int j = (int)tile - 1;
+    for (;;) {
+        const int idx = j - lane;
+        uint32_t fl = 2, val = 0;
+        bool ok = true;
+        if (idx >= 0) {
+            const unsigned long long w = ld_relaxed(tiles + idx);
+            ok = (uint32_t)(w >> 34) == tag && ((uint32_t)(w >> 32) & 3u) != 0;
+            fl = (uint32_t)(w >> 32) & 3u;
+            val = (uint32_t)w;
+        }
+        const unsigned incl = __ballot_sync(0xFFFFFFFFu, ok && fl == 2);
+        const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
+        if (incl) {
+            const int f = __ffs(incl) - 1;                 // nearest inclusive predecessor
+            if (bad & ((2u << f) - 1u)) continue;          // someone before it not published yet
+            excl += __reduce_add_sync(0xFFFFFFFFu, lane <= f ? val : 0u);
+            break;
+        }
+        if (bad) continue;
+        excl += __reduce_add_sync(0xFFFFFFFFu, val);
+        j -= 32;
+    }
+    if (lane == 0) st_relaxed(tiles + tile, tile_word(tag, 2, excl + agg));
     return excl;
 }
 

@@ -50,6 +50,9 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
                     if (op.x != p.x || op.y != p.y) err |= ERR_PROTOCOL;
                 }
             } else if (ds == 1) {
+                // step changed since the last round (kept even if this update is rejected:
+                // that only makes the next round re-scan the agent)
+                if (d.chg8) d.chg8[i] = 1;
                 if (ost != ST_RUNNING) {
                     err |= ERR_PROTOCOL;
                 } else {
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
             key = morton((uint32_t)p.x >> d.clog, (uint32_t)p.y >> d.clog);
             rank = atomicAdd(d.cnt + key, 1u);
             atomicMin(d.cmin + key, s);
-            chg = round_full(d) || d.lrstep[i] != s;
+            chg = round_full(d) || d.chg8[i];
             work = chg;
             if (!work && st == ST_IDLE) {
                 const uint32_t w = d.witness[i];
@@ -213,12 +216,15 @@ __global__ void __launch_bounds__(256) k_cells(Dev d)
     }
     if (lane == 31) wsum[w] = incl;
     __syncthreads();
-    if (t == 0) {
+    if (w == 0) {
         uint32_t acc = 0;
-        for (int k = 0; k < 8; k++) { uint32_t v = wsum[k]; wsum[k] = acc; acc += v; }
-        tile_excl = chain_scan(d.tiles_c, tile, tag, acc);
-        if (tile == gridDim.x - 1) {
-            d.ctab[d.ncells] = make_int2((int)(tile_excl + acc), INT_MAX);
+        for (int k = 0; k < 8; k++) acc += wsum[k];
+        const uint32_t ex = chain_scan_warp(d.tiles_c, tile, tag, acc);
+        if (t == 0) {
+            tile_excl = ex;
+            uint32_t a2 = 0;
+            for (int k = 0; k < 8; k++) { uint32_t v = wsum[k]; wsum[k] = a2; a2 += v; }
+            if (tile == gridDim.x - 1) d.ctab[d.ncells] = make_int2((int)(ex + acc), INT_MAX);
         }
     }
     __syncthreads();
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
     const int2 p = d.pos[c][i];
     const int s = d.step[c][i];
     const uint32_t r = (uint32_t)d.ctab[key].x + d.rank[i];
-    const int chg = (round_full(d) || d.lrstep[i] != s) ? kRecChanged : 0;
+    const int chg = (round_full(d) || d.chg8[i]) ? kRecChanged : 0;
     d.rec[r] = make_int4(p.x | (p.y << 16), s, i, d.status[c][i] | chg);
 }
 
@@ -412,7 +418,8 @@ __device__ __forceinline__ bool round_full(const Dev& d)
 
 __device__ __forceinline__ bool agent_changed(const Dev& d, uint32_t c, uint32_t i)
 {
-    return d.lrstep[i] != d.step[c][i];
+    (void)c;
+    return d.chg8[i] != 0;
 }
 
 // append one coupling edge (a < b) to the next edge list; a warp stages its edges in
@@ -518,9 +525,9 @@ __global__ void __launch_bounds__(256, 6) k_near(Dev d)
     }
     __syncthreads();
     const int nq = s_pref[kEdgeStripes];
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_work = nq;
     const uint32_t c = d.ctl->cur;
     const int W = d.ctl->W;
-    const bool full = round_full(d);
     const int cl = d.clog, G = 1 << d.glog;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
     const uint32_t Rc2 = Rc * Rc;
@@ -668,6 +675,7 @@ __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
     }
     __syncthreads();
     const int nq = s_pref[kEdgeStripes];
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_far = nq;
     const int W = d.ctl->W;
     const uint32_t c = d.ctl->cur;
     uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
@@ -766,6 +774,7 @@ __global__ void __launch_bounds__(256) k_far2(Dev d)
     }
     __syncthreads();
     const int total = s_pref[kEdgeStripes];
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_items = total;
     const uint32_t c = d.ctl->cur;
     uint32_t ncells = 0, ncand = 0;
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
@@ -805,6 +814,7 @@ __global__ void __launch_bounds__(256) k_union(Dev d)
 {
     const uint32_t nxt = d.ctl->ecur ^ 1u;
     const int ne = min((int)d.ctl->ecnt[nxt], d.ecap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_edges = ne;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ne; k += gridDim.x * blockDim.x) {
         const uint2 e = d.edges[(size_t)nxt * d.ecap + k];
         uf_unite(d.parent, e.x, e.y);
@@ -893,7 +903,7 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
         lab[k] = -1;
         if (i < d.n) {
             const uint8_t st = d.status[c][i];
-            d.lrstep[i] = d.step[c][i];
+            if (d.chg8) d.chg8[i] = 0;     // the round consumed this agent's change
             if (st == ST_DONE) {
                 d.labels[i] = -1;
             } else {
@@ -917,11 +927,16 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
     if (lane == 31) wsum[w] = incl;
     __syncthreads();
     if (mycl) atomicAdd(&ncl, mycl);
-    if (t == 0) {
+    if (w == 0) {
         uint32_t acc = 0;
-        for (int k = 0; k < 8; k++) { uint32_t v = wsum[k]; wsum[k] = acc; acc += v; }
-        tile_excl = chain_scan(d.tiles_r, tile, tag, acc);
-        if (tile == gridDim.x - 1) ctl->n_ready = (int)(tile_excl + acc);
+        for (int k = 0; k < 8; k++) acc += wsum[k];
+        const uint32_t ex = chain_scan_warp(d.tiles_r, tile, tag, acc);
+        if (t == 0) {
+            tile_excl = ex;
+            uint32_t a2 = 0;
+            for (int k = 0; k < 8; k++) { uint32_t v = wsum[k]; wsum[k] = a2; a2 += v; }
+            if (tile == gridDim.x - 1) ctl->n_ready = (int)(ex + acc);
+        }
     }
     __syncthreads();
     uint32_t pos = tile_excl + wsum[w] + incl - cnt;
@@ -972,9 +987,17 @@ __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
     __syncthreads();
     const int i0 = blockIdx.x * kSortTile;
     if (i0 < n) {
-        for (int k = threadIdx.x; k < kSortTile && i0 + k < n; k += blockDim.x) {
-            const unsigned long long key = d.rkey[0][i0 + k];
-            for (int p = 0; p < np; p++) atomicAdd(&h[p][(key >> (8 * p)) & 255u], 1u);
+        const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+        for (int k0 = 0; k0 < kSortTile; k0 += blockDim.x) {
+            const int k = k0 + threadIdx.x;
+            const bool valid = k < kSortTile && i0 + k < n;
+            const unsigned long long key = valid ? d.rkey[0][i0 + k] : 0ull;
+            for (int p = 0; p < np; p++) {
+                // one shared-memory atomic per distinct digit per warp (skewed high digits)
+                const int dg = valid ? (int)((key >> (8 * p)) & 255u) : 256;
+                const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg);
+                if (valid && (peers & lt) == 0) atomicAdd(&h[p][dg], (uint32_t)__popc(peers));
+            }
         }
         __syncthreads();
         for (int k = threadIdx.x; k < np * 256; k += blockDim.x) {
