@@ -129,13 +129,13 @@ __global__ void __launch_bounds__(256) k_disp_a(RepDev r)
 {
     const Dev& d = r.d;
     const int nr = d.ctl->n_ready;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k == 0) *r.dispatched += nr;
-    if (k >= nr) return;
-    const int i = r.order[k];
-    const int b = sim_of(d, i);
-    const long long tc = r.t_sim[b] + duration(r.sy, i, r.steps[i]);
-    atomicMax((unsigned long long*)(r.tcl + d.labels[i]), (unsigned long long)tc);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *r.dispatched += nr;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x) {
+        const int i = r.order[k];
+        const int b = sim_of(d, i);
+        const long long tc = r.t_sim[b] + duration(r.sy, i, r.steps[i]);
+        atomicMax((unsigned long long*)(r.tcl + d.labels[i]), (unsigned long long)tc);
+    }
 }
 
 // dispatch, part b: member completion times and moves (random-walk policy on the
@@ -144,9 +144,8 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
 {
     const Dev& d = r.d;
     const int nr = d.ctl->n_ready;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long tmin = ~0ull;
-    if (k < nr) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x) {
         const int i = r.order[k];
         const int b = sim_of(d, i);
         const long long tc = r.tcl[d.labels[i]];
@@ -163,7 +162,7 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
         if (ok && r.sy.wall && r.sy.wall[(long long)qy * d.map_w + qx]) ok = false;
         r.newpos[i] = ok ? make_int2(qx, qy) : p;
         if (d.n_sims > 1) atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
-        else tmin = (unsigned long long)tc;
+        else tmin = min(tmin, (unsigned long long)tc);
     }
     if (d.n_sims == 1) {  // block reduction, one atomic per block
         __shared__ unsigned long long s_min[8];
@@ -241,10 +240,11 @@ static int enqueue_round(am_replay* rp)
     if (rc) return rc;
     rp->r.d = c->d;
     am_prof_begin(c, K_DISP_A);
-    k_disp_a<<<nb, 256, 0, rp->stream>>>(rp->r);
+    const unsigned nbd = std::min(nb, (unsigned)c->num_sms * 4);   // grid-stride over the ready list
+    k_disp_a<<<nbd, 256, 0, rp->stream>>>(rp->r);
     am_prof_end(c, K_DISP_A);
     am_prof_begin(c, K_DISP_B);
-    k_disp_b<<<nb, 256, 0, rp->stream>>>(rp->r);
+    k_disp_b<<<nbd, 256, 0, rp->stream>>>(rp->r);
     am_prof_end(c, K_DISP_B);
     am_prof_begin(c, K_COMMIT);
     k_commit<<<(unsigned)((n + 256 * kIngestItems - 1) / (256 * kIngestItems)), 256, 0, rp->stream>>>(rp->r);

@@ -457,13 +457,13 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         }
         LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));
         LAUNCH(K_READY, (k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask)));
-        LAUNCH(K_SORT_HIST, (k_sort_hist<<<c->ntiles_sort, 256, 0, s>>>(d, c->sort_passes_max)));
+        LAUNCH(K_SORT_HIST, (k_sort_hist<<<std::min(c->ntiles_sort, 32), 256, 0, s>>>(d, c->sort_passes_max)));
         am_prof_begin(c, K_SORT_PASS);
-        for (int p = 0; p < c->sort_passes_max; p++)
-            k_sort_pass<<<c->ntiles_sort, 1024, 0, s>>>(d, p, order);
+        for (int p = 0; p < c->sort_passes_max; p++)   // persistent: <= 16 CTAs take tiles
+            k_sort_pass<<<std::min(c->ntiles_sort, 16), 1024, 0, s>>>(d, p, order);
         am_prof_end(c, K_SORT_PASS);
         // perception digests of the dispatched agents (replay driver)
-        if (d.flags & AM_DIGEST) k_digest<<<nb, 256, 0, s>>>(d, order);
+        if (d.flags & AM_DIGEST) k_digest<<<std::min(nb, (unsigned)c->num_sms * 2), 256, 0, s>>>(d, order);
     }
 #undef LAUNCH
     CK(c, cudaGetLastError());

@@ -469,6 +469,27 @@ __device__ __forceinline__ void flush_stage(const Dev& d, EdgeStage& sm, int lan
     __syncwarp();
 }
 
+// exclusive prefix of the kEdgeStripes (= 64) stripe counters into s_pref[0..64],
+// computed by warp 0 with two parallel loads per lane (one L2 round trip)
+__device__ __forceinline__ void stripe_prefix(const uint32_t* ctr, int cap, int* s_pref)
+{
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int a = min((int)__ldcg(ctr + lane), cap), b = min((int)__ldcg(ctr + 32 + lane), cap);
+        int ia = a, ib = b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int ya = __shfl_up_sync(0xFFFFFFFFu, ia, o), yb = __shfl_up_sync(0xFFFFFFFFu, ib, o);
+            if (lane >= o) { ia += ya; ib += yb; }
+        }
+        const int ta = __shfl_sync(0xFFFFFFFFu, ia, 31);
+        s_pref[lane] = ia - a;
+        s_pref[32 + lane] = ta + ib - b;
+        if (lane == 31) s_pref[64] = ta + ib;
+    }
+    __syncthreads();
+}
+
 // k_efilter: carry over last round's coupling edges whose endpoints both kept their
 // state (nothing in a full round).  One atomic per block.
 __global__ void __launch_bounds__(256) k_efilter(Dev d)
@@ -515,15 +536,7 @@ __global__ void __launch_bounds__(256, 6) k_near(Dev d)
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     EdgeStage& sm = s_all[wq];
     if (lane == 0) sm.ne = 0;
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int k = 0; k < kEdgeStripes; k++) {
-            s_pref[k] = acc;
-            acc += (int)d.wq_ctr[k];
-        }
-        s_pref[kEdgeStripes] = acc;
-    }
-    __syncthreads();
+    stripe_prefix(d.wq_ctr, 1 << 30, s_pref);
     const int nq = s_pref[kEdgeStripes];
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_work = nq;
     const uint32_t c = d.ctl->cur;
@@ -665,15 +678,7 @@ __device__ __forceinline__ uint32_t far_block(const Dev& d, uint32_t k1g, int qx
 __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
 {
     __shared__ int s_pref[kEdgeStripes + 1];
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int k = 0; k < kEdgeStripes; k++) {
-            s_pref[k] = acc;
-            acc += (int)d.farq_ctr[k];
-        }
-        s_pref[kEdgeStripes] = acc;
-    }
-    __syncthreads();
+    stripe_prefix(d.farq_ctr, 1 << 30, s_pref);
     const int nq = s_pref[kEdgeStripes];
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_far = nq;
     const int W = d.ctl->W;
@@ -764,15 +769,7 @@ __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
 __global__ void __launch_bounds__(256) k_far2(Dev d)
 {
     __shared__ int s_pref[kEdgeStripes + 1];
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int k = 0; k < kEdgeStripes; k++) {
-            s_pref[k] = acc;
-            acc += min((int)d.item_ctr[k], d.item_cap);
-        }
-        s_pref[kEdgeStripes] = acc;
-    }
-    __syncthreads();
+    stripe_prefix(d.item_ctr, d.item_cap, s_pref);
     const int total = s_pref[kEdgeStripes];
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_items = total;
     const uint32_t c = d.ctl->cur;
@@ -841,15 +838,20 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
     if (blk || st == ST_RUNNING) d.bad[root] = 1;
 }
 
+__device__ void digest_one(const Dev& d, uint32_t aid);
+
 // k_digest: perception digests ("perceives an area within a radius") of the
 // agents dispatched this round, for the replay driver: sum over same-step non-DONE
 // agents within r_p of mix64(id<<32 ^ (u16)dx<<16 ^ (u16)dy).
 __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict__ order)
 {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= d.ctl->n_ready) return;
+    const int nr = d.ctl->n_ready;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x)
+        digest_one(d, (uint32_t)order[k]);
+}
+__device__ void digest_one(const Dev& d, uint32_t aid)
+{
     const uint32_t c = d.ctl->cur;
-    const uint32_t aid = (uint32_t)order[k];
     const int2 P = d.pos[c][aid];
     const int ax = P.x, ay = P.y, as = d.step[c][aid];
     const int cl = d.clog, G = 1 << d.glog;
@@ -985,13 +987,13 @@ __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
     const int np = min(ctl->npasses, max_passes);
     for (int k = threadIdx.x; k < kMaxSortPasses * 256; k += blockDim.x) (&h[0][0])[k] = 0;
     __syncthreads();
-    const int i0 = blockIdx.x * kSortTile;
-    if (i0 < n) {
+    {
         const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
-        for (int k0 = 0; k0 < kSortTile; k0 += blockDim.x) {
+        // persistent grid-stride over the keys (the grid is sized for a typical round)
+        for (int k0 = blockIdx.x * blockDim.x; k0 < n; k0 += gridDim.x * blockDim.x) {
             const int k = k0 + threadIdx.x;
-            const bool valid = k < kSortTile && i0 + k < n;
-            const unsigned long long key = valid ? d.rkey[0][i0 + k] : 0ull;
+            const bool valid = k < n;
+            const unsigned long long key = valid ? d.rkey[0][k] : 0ull;
             for (int p = 0; p < np; p++) {
                 // one shared-memory atomic per distinct digit per warp (skewed high digits)
                 const int dg = valid ? (int)((key >> (8 * p)) & 255u) : 256;
@@ -1042,11 +1044,11 @@ __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __
     __shared__ uint32_t goff[256];
     const int n = ctl->n_ready;
     const int np = ctl->npasses;
+    // persistent: a few CTAs take tiles in ticket order (the look-back only waits on
+    // tiles that are being processed, so any grid size is deadlock-free)
+    for (;;) {
     const uint32_t tile = take_ticket(&ctl->pass[pass]);
-    if (pass >= np || (int)tile * kSortTile >= n) {
-        finish_block(&ctl->pass[pass], gridDim.x);
-        return;
-    }
+    if (pass >= np || (int)tile * kSortTile >= n) break;
     const uint32_t tag = ctl->epoch * 16u + 4u + (uint32_t)pass;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const unsigned long long* kin = d.rkey[pass & 1];
@@ -1100,6 +1102,8 @@ __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __
                 vout[dst] = val[k];
             }
         }
+    }
+    __syncthreads();   // wcnt / goff are reused by the next tile
     }
     finish_block(&ctl->pass[pass], gridDim.x);
 }
