@@ -21,7 +21,7 @@ __global__ void k_far1(Dev d);
 __global__ void k_far2(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
-__global__ void k_sort_pass(Dev d, int pass, int32_t* order);
+__global__ void k_sort_pass(Dev d, int pass, int32_t* order, int ntiles);
 __global__ void k_small(Dev d, uint8_t* mask, int32_t* order);
 __global__ void k_round_begin(Dev d);
 __global__ void k_efilter(Dev d);
@@ -460,7 +460,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         LAUNCH(K_SORT_HIST, (k_sort_hist<<<std::min(c->ntiles_sort, 32), 256, 0, s>>>(d, c->sort_passes_max)));
         am_prof_begin(c, K_SORT_PASS);
         for (int p = 0; p < c->sort_passes_max; p++)   // persistent: <= 16 CTAs take tiles
-            k_sort_pass<<<std::min(c->ntiles_sort, 16), 1024, 0, s>>>(d, p, order);
+            k_sort_pass<<<std::min(c->ntiles_sort, 16), 1024, 0, s>>>(d, p, order, c->ntiles_sort);
         am_prof_end(c, K_SORT_PASS);
         // perception digests of the dispatched agents (replay driver)
         if (d.flags & AM_DIGEST) k_digest<<<std::min(nb, (unsigned)c->num_sms * 2), 256, 0, s>>>(d, order);

@@ -1037,7 +1037,7 @@ __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
 // Warp w of a tile owns items [256w, 256w+256) and ranks them
 // in index order with __match_any_sync, so the pass is stable.  The last pass writes
 // the ids straight into `order`.
-__global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __restrict__ order)
+__global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __restrict__ order, int ntiles)
 {
     Ctl* ctl = d.ctl;
     __shared__ uint32_t wcnt[32][256];
@@ -1083,10 +1083,10 @@ __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __
         uint32_t acc = 0;
 #pragma unroll 8
         for (int q = 0; q < 32; q++) { uint32_t v = wcnt[q][t]; wcnt[q][t] = acc; acc += v; }
-        unsigned long long* tw = d.tiles_sort + ((size_t)pass * gridDim.x) * 256;
+        unsigned long long* tw = d.tiles_sort + ((size_t)pass * ntiles) * 256;
         uint32_t excl;
         // column-major tile words: word of (tile, digit) at tw[digit * ntiles + tile]
-        unsigned long long* col = tw + (size_t)t * gridDim.x;
+        unsigned long long* col = tw + (size_t)t * ntiles;
         excl = chain_scan(col, tile, tag, acc);
         goff[t] = d.gstart[pass * 256 + t] + excl;
     }

@@ -264,3 +264,25 @@ def test_empty_and_all_done():
     mask, order = tr.ready()
     assert len(order) == 0 and int(mask.sum()) == 0
     assert (tr.clusters() == -1).all()
+
+
+@pytest.mark.parametrize("path", ["binned"])
+def test_large_ready_set_closed_form(path):
+    """300k isolated agents (spacing 20 > R_b(6) = 11), steps 0..6: every agent is its own
+    ready cluster, so order = agents sorted by (step, id) -- a closed form at a size whose
+    ready set spans many radix tiles (the first replay round has this shape)."""
+    side = 548
+    n = side * side
+    ids = np.arange(n)
+    x = ((ids % side) * 20).astype(np.int32)
+    y = ((ids // side) * 20).astype(np.int32)
+    s = (ids * 7919 % 7).astype(np.int32)
+    st = np.zeros(n, np.uint8)
+    tr = Tracker(side * 20, side * 20, 4, 1, n, force=path)
+    g = _gpu_round(tr, x, y, s, st)
+    assert g["mask"].all()
+    np.testing.assert_array_equal(g["label"], ids)
+    np.testing.assert_array_equal(g["order"], np.lexsort((ids, s)))
+    # a second round on the dispatched state: nothing is ready
+    mask, order = tr.ready()
+    assert len(order) == 0
