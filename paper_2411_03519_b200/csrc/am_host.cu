@@ -37,6 +37,7 @@ __global__ void k_copy_status(Dev d, uint8_t* out)
 using namespace am;
 
 static thread_local std::string g_init_err;
+static constexpr int kSortSmem = (32 + 1) * kRadix * 4;   // k_sort_pass dynamic shared memory
 
 static int set_err(am_ctx* c, int code, const char* msg)
 {
@@ -196,6 +197,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     d.metric = c.metric;
     d.flags = c.flags;
     x->stream = (cudaStream_t)c.stream;
+    cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
     {
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -248,7 +250,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     {
         int lagbits = c.target_step > 0 ? ilog2_ceil((long long)c.target_step + 1) : 31;
         int bits = lagbits + d.idbits;
-        x->sort_passes_max = std::min(kMaxSortPasses, std::max(1, (bits + 7) / 8));
+        x->sort_passes_max = std::min(kMaxSortPasses, std::max(1, (bits + kRadixBits - 1) / kRadixBits));
     }
     x->ntiles_sort = (int)blocks(n, kSortTile);
     x->ntiles_ready = (int)blocks(n, kReadyTile);
@@ -276,8 +278,8 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_par = take(4 * N); o_bad = take(N);
         o_rk0 = take(8 * N); o_rk1 = take(8 * N); o_rv0 = take(4 * N); o_rv1 = take(4 * N);
         o_tc = take(8 * (size_t)x->ntiles_cells); o_tr = take(8 * (size_t)x->ntiles_ready);
-        o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * 256);
-        o_gh = take(4 * kMaxSortPasses * 256); o_gs = take(4 * kMaxSortPasses * 256);
+        o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * kRadix);
+        o_gh = take(4 * kMaxSortPasses * kRadix); o_gs = take(4 * kMaxSortPasses * kRadix);
         d.ecap = (int)(3 * N + 4096);
         d.wq_cap = (int)((((N + 31) / 32 + kEdgeStripes - 1) / kEdgeStripes) * 32 + 32);
         o_wit = take(4 * N); o_lrs = take(N);
@@ -460,7 +462,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         LAUNCH(K_SORT_HIST, (k_sort_hist<<<std::min(c->ntiles_sort, 32), 256, 0, s>>>(d, c->sort_passes_max)));
         am_prof_begin(c, K_SORT_PASS);
         for (int p = 0; p < c->sort_passes_max; p++)   // persistent: <= 16 CTAs take tiles
-            k_sort_pass<<<std::min(c->ntiles_sort, 16), 1024, 0, s>>>(d, p, order, c->ntiles_sort);
+            k_sort_pass<<<std::min(c->ntiles_sort, 16), 1024, kSortSmem, s>>>(d, p, order, c->ntiles_sort);
         am_prof_end(c, K_SORT_PASS);
         // perception digests of the dispatched agents (replay driver)
         if (d.flags & AM_DIGEST) k_digest<<<std::min(nb, (unsigned)c->num_sms * 2), 256, 0, s>>>(d, order);

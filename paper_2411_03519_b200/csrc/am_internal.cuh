@@ -18,6 +18,8 @@ constexpr int kCellsPerTile = 4096;       // cell-table scan tile (256 threads x
 constexpr int kReadyTile = 2048;          // ready compaction tile (256 threads x 8 agents)
 constexpr int kSortTile = 8192;           // radix pass tile (1024 threads x 8 keys)
 constexpr int kMaxSortPasses = 8;
+constexpr int kRadixBits = 9;            // radix digit width of the priority sort
+constexpr int kRadix = 1 << kRadixBits;
 constexpr int kIngestItems = 4;           // agents per thread in k_ingest / k_commit
 constexpr int kEdgeStripes = 64;          // striped queues (one atomic counter per stripe)
 constexpr int kEdgeStage = 128;           // coupling edges staged per warp before appending

@@ -970,49 +970,50 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
     if (finish_block(&ctl->ready, gridDim.x) && t == 0) {
         unsigned long long o = *(volatile unsigned long long*)&ctl->sort_or;
         int bits = o ? 64 - __clzll((long long)o) : 0;
-        int np = (bits + 7) / 8;
+        int np = (bits + kRadixBits - 1) / kRadixBits;
         ctl->npasses = np < 1 ? 1 : np;
         ctl->sort_or = 0;
         ctl->full = 0;
     }
 }
 
-// k_sort_hist: global 8-bit digit histograms of the ready keys for every pass; the
-// last block turns them into exclusive digit offsets.
+// k_sort_hist: global kRadixBits-bit digit histograms of the ready keys for every pass
+// (persistent grid-stride); the last block turns them into exclusive digit offsets.
 __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
 {
     Ctl* ctl = d.ctl;
-    __shared__ uint32_t h[kMaxSortPasses][256];
+    __shared__ uint32_t h[kMaxSortPasses][kRadix];
     const int n = ctl->n_ready;
     const int np = min(ctl->npasses, max_passes);
-    for (int k = threadIdx.x; k < kMaxSortPasses * 256; k += blockDim.x) (&h[0][0])[k] = 0;
+    for (int k = threadIdx.x; k < kMaxSortPasses * kRadix; k += blockDim.x) (&h[0][0])[k] = 0;
     __syncthreads();
     {
         const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
-        // persistent grid-stride over the keys (the grid is sized for a typical round)
         for (int k0 = blockIdx.x * blockDim.x; k0 < n; k0 += gridDim.x * blockDim.x) {
             const int k = k0 + threadIdx.x;
             const bool valid = k < n;
             const unsigned long long key = valid ? d.rkey[0][k] : 0ull;
             for (int p = 0; p < np; p++) {
                 // one shared-memory atomic per distinct digit per warp (skewed high digits)
-                const int dg = valid ? (int)((key >> (8 * p)) & 255u) : 256;
+                const int dg = valid ? (int)((key >> (kRadixBits * p)) & (kRadix - 1)) : kRadix;
                 const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg);
                 if (valid && (peers & lt) == 0) atomicAdd(&h[p][dg], (uint32_t)__popc(peers));
             }
         }
         __syncthreads();
-        for (int k = threadIdx.x; k < np * 256; k += blockDim.x) {
+        for (int k = threadIdx.x; k < np * kRadix; k += blockDim.x) {
             const uint32_t v = (&h[0][0])[k];
             if (v) atomicAdd(d.ghist + k, v);
         }
     }
     if (finish_block(&ctl->hist, gridDim.x)) {
-        // last block: thread t owns digit t; exclusive scan over the 256 digits per pass
+        // last block: thread t owns digits 2t and 2t+1; exclusive scan per pass
         __shared__ uint32_t wtot[8];
         const int t = threadIdx.x, lane = t & 31, w = t >> 5;
         for (int p = 0; p < np; p++) {
-            const uint32_t v = __ldcg(d.ghist + p * 256 + t);
+            const uint32_t v0 = __ldcg(d.ghist + p * kRadix + 2 * t);
+            const uint32_t v1 = __ldcg(d.ghist + p * kRadix + 2 * t + 1);
+            const uint32_t v = v0 + v1;
             uint32_t incl = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1023,25 +1024,28 @@ __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
             __syncthreads();
             uint32_t base = 0;
             for (int q = 0; q < w; q++) base += wtot[q];
-            d.gstart[p * 256 + t] = base + incl - v;
-            d.ghist[p * 256 + t] = 0;
+            const uint32_t ex = base + incl - v;
+            d.gstart[p * kRadix + 2 * t] = ex;
+            d.gstart[p * kRadix + 2 * t + 1] = ex + v0;
+            d.ghist[p * kRadix + 2 * t] = 0;
+            d.ghist[p * kRadix + 2 * t + 1] = 0;
             __syncthreads();
         }
         __threadfence();
     }
 }
 
-// k_sort_pass: one stable LSD pass over 8 bits (onesweep: per-digit decoupled
-// look-back across tiles of 8192 keys, 32 warps x 8 keys per lane, so a typical
-// round's ready set spans a handful of tiles and the look-back chains stay short).
-// Warp w of a tile owns items [256w, 256w+256) and ranks them
-// in index order with __match_any_sync, so the pass is stable.  The last pass writes
-// the ids straight into `order`.
+// k_sort_pass: one stable LSD pass over kRadixBits bits (onesweep: per-digit decoupled
+// look-back across tiles of 8192 keys, 32 warps x 8 keys per lane).  Warp w of a tile
+// owns items [256w, 256w+256) and ranks them in index order with __match_any_sync, so
+// the pass is stable.  The last pass writes the ids straight into `order`.
+// Dynamic shared memory: wcnt[32][kRadix] + goff[kRadix].
 __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __restrict__ order, int ntiles)
 {
     Ctl* ctl = d.ctl;
-    __shared__ uint32_t wcnt[32][256];
-    __shared__ uint32_t goff[256];
+    extern __shared__ uint32_t sort_smem[];
+    uint32_t (*wcnt)[kRadix] = reinterpret_cast<uint32_t (*)[kRadix]>(sort_smem);
+    uint32_t* goff = sort_smem + 32 * kRadix;
     const int n = ctl->n_ready;
     const int np = ctl->npasses;
     // persistent: a few CTAs take tiles in ticket order (the look-back only waits on
@@ -1056,9 +1060,9 @@ __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __
     unsigned long long* kout = d.rkey[(pass + 1) & 1];
     uint32_t* vout = d.rval[(pass + 1) & 1];
     const bool last = pass == np - 1;
-    for (int k = t; k < 32 * 256; k += 1024) (&wcnt[0][0])[k] = 0;
+    for (int k = t; k < 32 * kRadix; k += 1024) (&wcnt[0][0])[k] = 0;
     __syncthreads();
-    const int shift = 8 * pass;
+    const int shift = kRadixBits * pass;
     unsigned long long key[8];
     uint32_t val[8], rnk[8];
     int dig[8];
@@ -1069,7 +1073,7 @@ __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __
         const bool valid = i < n;
         key[k] = valid ? kin[i] : 0ull;
         val[k] = valid ? vin[i] : 0u;
-        dig[k] = valid ? (int)((key[k] >> shift) & 255u) : 256;
+        dig[k] = valid ? (int)((key[k] >> shift) & (kRadix - 1)) : kRadix;
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, dig[k]);
         const uint32_t base = valid ? wcnt[w][dig[k]] : 0u;
         rnk[k] = base + __popc(peers & lt);
@@ -1079,21 +1083,20 @@ __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __
     }
     __syncthreads();
     // per digit (thread t = digit): exclusive prefix over warps, tile total, look-back
-    if (t < 256) {
+    if (t < kRadix) {
         uint32_t acc = 0;
 #pragma unroll 8
         for (int q = 0; q < 32; q++) { uint32_t v = wcnt[q][t]; wcnt[q][t] = acc; acc += v; }
-        unsigned long long* tw = d.tiles_sort + ((size_t)pass * ntiles) * 256;
-        uint32_t excl;
+        unsigned long long* tw = d.tiles_sort + ((size_t)pass * ntiles) * kRadix;
         // column-major tile words: word of (tile, digit) at tw[digit * ntiles + tile]
         unsigned long long* col = tw + (size_t)t * ntiles;
-        excl = chain_scan(col, tile, tag, acc);
-        goff[t] = d.gstart[pass * 256 + t] + excl;
+        const uint32_t excl = chain_scan(col, tile, tag, acc);
+        goff[t] = d.gstart[pass * kRadix + t] + excl;
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-        if (dig[k] < 256) {
+        if (dig[k] < kRadix) {
             const uint32_t dst = goff[dig[k]] + wcnt[w][dig[k]] + rnk[k];
             if (last) {
                 order[dst] = (int32_t)val[k];
