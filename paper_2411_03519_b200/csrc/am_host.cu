@@ -3,6 +3,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 
 #include "am_internal.cuh"
@@ -198,6 +199,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     d.flags = c.flags;
     x->stream = (cudaStream_t)c.stream;
     cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
+    if (const char* e = getenv("AM_SORT_CTAS")) x->sort_ctas = std::max(1, atoi(e));   // tuning knob
     {
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -462,7 +464,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         LAUNCH(K_SORT_HIST, (k_sort_hist<<<std::min(c->ntiles_sort, 32), 256, 0, s>>>(d, c->sort_passes_max)));
         am_prof_begin(c, K_SORT_PASS);
         for (int p = 0; p < c->sort_passes_max; p++)   // persistent: <= 16 CTAs take tiles
-            k_sort_pass<<<std::min(c->ntiles_sort, 16), 1024, kSortSmem, s>>>(d, p, order, c->ntiles_sort);
+            k_sort_pass<<<std::min(c->ntiles_sort, c->sort_ctas), 1024, kSortSmem, s>>>(d, p, order, c->ntiles_sort);
         am_prof_end(c, K_SORT_PASS);
         // perception digests of the dispatched agents (replay driver)
         if (d.flags & AM_DIGEST) k_digest<<<std::min(nb, (unsigned)c->num_sms * 2), 256, 0, s>>>(d, order);

@@ -146,6 +146,7 @@ struct am_ctx {
     int cell = 0;
     int small_threads = 32;
     int num_sms = 148;
+    int sort_ctas = 16;              // persistent CTAs of each radix pass
     int sort_passes_max = 1;
     int ntiles_sort = 1;
     int ntiles_ready = 1;

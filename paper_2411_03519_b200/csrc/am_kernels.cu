@@ -977,6 +977,20 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
     }
 }
 
+// lanes of the warp holding the same digit (and validity), from kRadixBits + 1 ballots
+__device__ __forceinline__ unsigned warp_match_digit(int dg, bool valid)
+{
+    const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
+    unsigned peers = valid ? vm : ~vm;
+#pragma unroll
+    for (int b = 0; b < kRadixBits; b++) {
+        const bool bit = (dg >> b) & 1;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, bit);
+        peers &= bit ? m : ~m;
+    }
+    return peers;
+}
+
 // k_sort_hist: global kRadixBits-bit digit histograms of the ready keys for every pass
 // (persistent grid-stride); the last block turns them into exclusive digit offsets.
 __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
@@ -996,7 +1010,7 @@ __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
             for (int p = 0; p < np; p++) {
                 // one shared-memory atomic per distinct digit per warp (skewed high digits)
                 const int dg = valid ? (int)((key >> (kRadixBits * p)) & (kRadix - 1)) : kRadix;
-                const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg);
+                const unsigned peers = warp_match_digit(dg, valid);
                 if (valid && (peers & lt) == 0) atomicAdd(&h[p][dg], (uint32_t)__popc(peers));
             }
         }
@@ -1074,7 +1088,7 @@ __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __
         key[k] = valid ? kin[i] : 0ull;
         val[k] = valid ? vin[i] : 0u;
         dig[k] = valid ? (int)((key[k] >> shift) & (kRadix - 1)) : kRadix;
-        const unsigned peers = __match_any_sync(0xFFFFFFFFu, dig[k]);
+        const unsigned peers = warp_match_digit(dig[k], valid);
         const uint32_t base = valid ? wcnt[w][dig[k]] : 0u;
         rnk[k] = base + __popc(peers & lt);
         __syncwarp();
