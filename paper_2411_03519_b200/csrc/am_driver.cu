@@ -74,18 +74,29 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r)
     const uint32_t c = d.ctl->cur;
     unsigned long long tmin = ~0ull;  // pending completions (single-simulation case)
     int any_active = 0;
+    // loads of all items first (independent chains in flight), then the commits
+    uint8_t st[kIngestItems];
+    long long tc[kIngestItems];
 #pragma unroll
     for (int k = 0; k < kIngestItems; k++) {
         const int i = blockIdx.x * (256 * kIngestItems) + k * 256 + threadIdx.x;
-        if (i >= d.n) break;
-        const uint8_t st = d.status[c][i];  // after this round's dispatch
-        if (st == ST_DONE) continue;
+        st[k] = ST_DONE;
+        tc[k] = 0;
+        if (i < d.n) {
+            st[k] = d.status[c][i];  // after this round's dispatch
+            tc[k] = r.tcommit[i];
+        }
+    }
+    const long long t1 = one ? r.t_sim[0] : 0;
+#pragma unroll
+    for (int k = 0; k < kIngestItems; k++) {
+        const int i = blockIdx.x * (256 * kIngestItems) + k * 256 + threadIdx.x;
+        if (st[k] == ST_DONE) continue;
         const int b = sim_of(d, i);
-        const long long t = r.t_sim[b];
+        const long long t = one ? t1 : r.t_sim[b];
         bool active = true;
-        if (st == ST_RUNNING) {
-            const long long tc = r.tcommit[i];
-            if (tc <= t) {
+        if (st[k] == ST_RUNNING) {
+            if (tc[k] <= t) {
                 const int2 np = r.newpos[i];
                 const int s = r.steps[i] + 1;
                 r.pos[i] = np;
@@ -96,10 +107,10 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r)
                     atomicMax((unsigned long long*)(r.tdone + b), (unsigned long long)t);
                 }
             } else if (one) {
-                tmin = min(tmin, (unsigned long long)tc);
+                tmin = min(tmin, (unsigned long long)tc[k]);
             } else {
                 // stays RUNNING through this round: bounds the next event
-                atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
+                atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc[k]);
             }
         }
         if (active) {

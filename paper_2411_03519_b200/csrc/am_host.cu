@@ -20,6 +20,7 @@ __global__ void k_union(Dev d);
 __global__ void k_near(Dev d);
 __global__ void k_far1(Dev d);
 __global__ void k_far2(Dev d);
+__global__ void k_far(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
 __global__ void k_sort_pass(Dev d, int pass, int32_t* order, int ntiles);
@@ -27,6 +28,8 @@ __global__ void k_small(Dev d, uint8_t* mask, int32_t* order);
 __global__ void k_round_begin(Dev d);
 __global__ void k_efilter(Dev d);
 __global__ void k_digest(Dev d, const int32_t* order);
+__global__ void k_csort(Dev d, int32_t* order, int smem_bytes);
+size_t csort_smem_fixed();
 
 __global__ void k_copy_status(Dev d, uint8_t* out)
 {
@@ -80,14 +83,22 @@ static const char* kKernelNames[K_COUNT] = {
     "k_ingest", "k_bin", "k_cells", "k_scatter", "k_scan", "k_finalize", "k_ready", "k_sort_hist",
     "k_sort_pass", "k_small", "k_commit", "k_disp_a", "k_disp_b", "k_union", "k_near"};
 
+// inside a stream capture the records become external event nodes of the graph
+static void prof_record(am_ctx* c, cudaEvent_t ev)
+{
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, c->stream, cudaEventRecordExternal);
+    else cudaEventRecord(ev, c->stream);
+}
 void am_prof_begin(am_ctx* c, int id)
 {
-    if (c->prof.on && (c->prof.mask >> id & 1u)) cudaEventRecordWithFlags(c->prof.ev[id][0], c->stream, cudaEventRecordExternal);
+    if (c->prof.on && (c->prof.mask >> id & 1u)) prof_record(c, c->prof.ev[id][0]);
 }
 void am_prof_end(am_ctx* c, int id)
 {
     if (c->prof.on && (c->prof.mask >> id & 1u)) {
-        cudaEventRecordWithFlags(c->prof.ev[id][1], c->stream, cudaEventRecordExternal);
+        prof_record(c, c->prof.ev[id][1]);
         c->prof.pending |= 1u << id;
     }
 }
@@ -152,7 +163,7 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 2 : 13 + c->sort_passes_max + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
+    return c->path == 0 ? 2 : 12 + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -200,6 +211,43 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     x->stream = (cudaStream_t)c.stream;
     cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
     if (const char* e = getenv("AM_SORT_CTAS")) x->sort_ctas = std::max(1, atoi(e));   // tuning knob
+    if (const char* e = getenv("AM_FAR")) x->far_items = !strcmp(e, "items");          // ablation
+    // the one-kernel cluster sort: the largest cluster (16, else 8) that can be resident
+    {
+        const char* e = getenv("AM_SORT");   // "onesweep" = multi-kernel ablation
+        if (!(e && !strcmp(e, "onesweep"))) {
+            int dev = 0, maxsm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            // pairs per CTA: 3 buffers of 16-byte elements at worst (64-bit keys)
+            const size_t fixed = csort_smem_fixed();
+            const int cap = (size_t)maxsm > fixed ? (int)(((size_t)maxsm - fixed) / 48) : 0;
+            if (cap >= 1024 &&
+                cudaFuncSetAttribute(k_csort, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess) {
+                cudaFuncSetAttribute(k_csort, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                int want = 0;
+                if (const char* q = getenv("AM_CSORT_CTAS")) want = atoi(q);   // tuning knob
+                for (int cs : {16, 8, 4, 2, 1}) {
+                    if (want && cs != want) continue;
+                    cudaLaunchConfig_t lc{};
+                    lc.gridDim = dim3(cs);
+                    lc.blockDim = dim3(1024);
+                    lc.dynamicSmemBytes = (size_t)maxsm;
+                    cudaLaunchAttribute at{};
+                    at.id = cudaLaunchAttributeClusterDimension;
+                    at.val.clusterDim.x = cs; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+                    lc.attrs = &at; lc.numAttrs = 1;
+                    int ncl = 0;
+                    if (cudaOccupancyMaxActiveClusters(&ncl, k_csort, &lc) == cudaSuccess && ncl >= 1) {
+                        x->csort_ctas = cs;
+                        x->csort_cap = maxsm;   // dynamic shared memory bytes per CTA
+                        break;
+                    }
+                }
+            }
+            cudaGetLastError();
+        }
+    }
     {
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -270,23 +318,26 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
     size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
-           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0, o_fctr = 0, o_wq = 0;
+           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0, o_fctr = 0, o_wq = 0, o_dirty = 0;
     const size_t NC = (size_t)d.ncells;
     if (x->path == 1) {
         o_key = take(4 * N); o_rank = take(4 * N);
         o_cnt = take(4 * NC); o_cmin = take(4 * NC);
         o_ctab = take(8 * (NC + 1)); o_l1 = take(4 * (NC / 16)); o_l2 = take(4 * (NC / 256));
         o_rec = take(16 * N); o_blk = take(N);
-        o_par = take(4 * N); o_bad = take(N);
+        o_par = take(4 * N); o_bad = take(N); o_dirty = take(4 * N);
         o_rk0 = take(8 * N); o_rk1 = take(8 * N); o_rv0 = take(4 * N); o_rv1 = take(4 * N);
         o_tc = take(8 * (size_t)x->ntiles_cells); o_tr = take(8 * (size_t)x->ntiles_ready);
         o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * kRadix);
         o_gh = take(4 * kMaxSortPasses * kRadix); o_gs = take(4 * kMaxSortPasses * kRadix);
         d.ecap = (int)(3 * N + 4096);
-        d.wq_cap = (int)((((N + 31) / 32 + kEdgeStripes - 1) / kEdgeStripes) * 32 + 32);
+        // striped queues, stripe = block index mod 64: k_bin has one thread per agent;
+        // k_near is a grid-stride loop over <= n queued agents on min(blocks, 8 x SMs) blocks
+        const long long nbl = blocks(n, 256), gnear = std::min<long long>(nbl, 8LL * x->num_sms);
+        d.wq_cap = (int)(((nbl + kEdgeStripes - 1) / kEdgeStripes) * 256);
         o_wit = take(4 * N); o_lrs = take(N);
         // a stripe receives the records of the blocks b with b % 64 == stripe
-        d.farq_cap = (int)(((blocks(n, 256) + kEdgeStripes - 1) / kEdgeStripes) * 256);
+        d.farq_cap = (int)(((gnear + kEdgeStripes - 1) / kEdgeStripes) * ((n + gnear * 256 - 1) / (gnear * 256)) * 256);
         o_farq = take(4 * (size_t)kEdgeStripes * d.farq_cap); o_fctr = take(4 * kEdgeStripes);
         d.item_cap = (int)std::max<size_t>(1024, (4 * N + kEdgeStripes - 1) / kEdgeStripes);
         o_items = take(8 * (size_t)kEdgeStripes * d.item_cap); o_ictr = take(4 * kEdgeStripes);
@@ -312,7 +363,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.cnt = (uint32_t*)(b + o_cnt); d.cmin = (int32_t*)(b + o_cmin);
         d.ctab = (int2*)(b + o_ctab); d.lmin1 = (int32_t*)(b + o_l1); d.lmin2 = (int32_t*)(b + o_l2);
         d.rec = (int4*)(b + o_rec); d.v8 = (uint8_t*)(b + o_blk);
-        d.parent = (uint32_t*)(b + o_par); d.bad = (uint8_t*)(b + o_bad);
+        d.parent = (uint32_t*)(b + o_par); d.bad = (uint8_t*)(b + o_bad); d.dirty = (uint32_t*)(b + o_dirty);
         d.rkey[0] = (unsigned long long*)(b + o_rk0); d.rkey[1] = (unsigned long long*)(b + o_rk1);
         d.rval[0] = (uint32_t*)(b + o_rv0); d.rval[1] = (uint32_t*)(b + o_rv1);
         d.tiles_c = (unsigned long long*)(b + o_tc); d.tiles_r = (unsigned long long*)(b + o_tr);
@@ -454,18 +505,36 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             // far phase over the compacted queue: pyramid levels, then one thread per
             // surviving (agent, 4x4-cell block) item
             am_prof_begin(c, K_SCAN);
-            k_far1<<<std::min(nb, pers), 256, 0, s>>>(d);
-            k_far2<<<std::min(nb, pers), 256, 0, s>>>(d);
+            if (c->far_items) {   // ablation: per-agent pyramid pass + per-(agent, 4x4 block) items
+                k_far1<<<std::min(nb, pers), 256, 0, s>>>(d);
+                k_far2<<<std::min(nb, pers), 256, 0, s>>>(d);
+            } else {              // one half-warp per far-queued agent
+                k_far<<<std::min(nb, pers), 256, 0, s>>>(d);
+            }
             am_prof_end(c, K_SCAN);
             LAUNCH(K_UNION, (k_union<<<std::min(blocks(d.ecap, 256), pers), 256, 0, s>>>(d)));
         }
         LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));
         LAUNCH(K_READY, (k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask)));
-        LAUNCH(K_SORT_HIST, (k_sort_hist<<<std::min(c->ntiles_sort, 32), 256, 0, s>>>(d, c->sort_passes_max)));
-        am_prof_begin(c, K_SORT_PASS);
-        for (int p = 0; p < c->sort_passes_max; p++)   // persistent: <= 16 CTAs take tiles
-            k_sort_pass<<<std::min(c->ntiles_sort, c->sort_ctas), 1024, kSortSmem, s>>>(d, p, order, c->ntiles_sort);
-        am_prof_end(c, K_SORT_PASS);
+        if (c->csort_ctas) {
+            // one cluster of csort_ctas CTAs sorts the whole ready set (am_sort.cu)
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(c->csort_ctas);
+            lc.blockDim = dim3(1024);
+            lc.dynamicSmemBytes = (size_t)c->csort_cap;
+            lc.stream = s;
+            cudaLaunchAttribute at{};
+            at.id = cudaLaunchAttributeClusterDimension;
+            at.val.clusterDim.x = c->csort_ctas; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+            lc.attrs = &at; lc.numAttrs = 1;
+            LAUNCH(K_SORT_PASS, CK(c, cudaLaunchKernelEx(&lc, k_csort, d, order, c->csort_cap)));
+        } else {
+            LAUNCH(K_SORT_HIST, (k_sort_hist<<<std::min(c->ntiles_sort, 32), 256, 0, s>>>(d, c->sort_passes_max)));
+            am_prof_begin(c, K_SORT_PASS);
+            for (int p = 0; p < c->sort_passes_max; p++)   // persistent: <= 16 CTAs take tiles
+                k_sort_pass<<<std::min(c->ntiles_sort, c->sort_ctas), 1024, kSortSmem, s>>>(d, p, order, c->ntiles_sort);
+            am_prof_end(c, K_SORT_PASS);
+        }
         // perception digests of the dispatched agents (replay driver)
         if (d.flags & AM_DIGEST) k_digest<<<std::min(nb, (unsigned)c->num_sms * 2), 256, 0, s>>>(d, order);
     }

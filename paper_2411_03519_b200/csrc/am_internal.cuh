@@ -46,11 +46,13 @@ struct Ctl {
     int32_t  W, S;         // watermark (min step of non-DONE) and max step
     int32_t  n_active, n_running;
     int32_t  n_ready, n_clusters;
-    int32_t  npasses;      // radix passes needed by this round's ready keys
+    int32_t  npasses;      // radix passes needed by this round's ready keys (onesweep digits)
+    int32_t  sort_bits;    // significant bits of this round's ready keys
     int32_t  full;         // recompute every verdict / coupling edge this round
     int32_t  full_next;    // force a full round next time (edge list overflowed, ablation scan)
     uint32_t ecur;         // which coupling-edge list is current
     uint32_t ecnt[2];      // edges in each list
+    int32_t  ecarried;     // edges carried over into this round's list (the new ones follow)
     int32_t  n_work, n_far, n_items, n_edges;   // this round's scan work (stats)
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
@@ -58,7 +60,7 @@ struct Ctl {
     // scan statistics (AM_STATS): cells visited, candidate pairs, phase-2 agents,
     // pyramid blocks tested (16x16, 4x4)
     unsigned long long st_cells, st_cand, st_p2, st_b2, st_b1, st_blocked;
-    Chain ingest, bin, cells, ready, hist, small_, uni, pass[kMaxSortPasses];
+    Chain ingest, bin, cells, ready, hist, small_, uni, efil, pass[kMaxSortPasses];
 };
 
 // all device pointers of a context, passed by value to kernels
@@ -98,6 +100,7 @@ struct Dev {
     uint32_t* wq_ctr;      // [kEdgeStripes]
     int32_t wq_cap;
     uint32_t* parent;      // [n] union-find forest in id space (root = min id)
+    uint32_t* dirty;       // [n] per last-round label: epoch of the round its cluster must be rebuilt in
     uint8_t* bad;          // [n] cluster (root) has a blocked or RUNNING member
     int32_t* labels;       // [n]
     uint8_t* blkid;        // [n] blocked verdict per id (IDLE agents; 0 otherwise)
@@ -148,6 +151,9 @@ struct am_ctx {
     int num_sms = 148;
     int sort_ctas = 16;              // persistent CTAs of each radix pass
     int sort_passes_max = 1;
+    int far_items = 0;               // far phase as k_far1 + k_far2 (ablation)
+    int csort_ctas = 0;              // cluster size of the one-kernel priority sort (0 = onesweep)
+    int csort_cap = 0;               // dynamic shared memory bytes per CTA of k_csort
     int ntiles_sort = 1;
     int ntiles_ready = 1;
     int ntiles_cells = 1;

@@ -31,54 +31,73 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
     Ctl* ctl = d.ctl;
     const uint32_t c = ctl->cur;
     int err = 0, act = 0, run = 0, smin = INT_MAX, smax = INT_MIN;
+    const bool validate = (d.flags & AM_VALIDATE) != 0;
+    // every load of the thread's items is issued before any compute or store, so the
+    // thread keeps kIngestItems independent load chains in flight (memory-level
+    // parallelism; the state buffers and the caller's arrays may not alias)
+    int2 p[kIngestItems], op[kIngestItems];
+    int s[kIngestItems], os[kIngestItems];
+    uint8_t ost[kIngestItems];
+#pragma unroll
+    for (int k = 0; k < kIngestItems; k++) {
+        const int i = blockIdx.x * (256 * kIngestItems) + k * 256 + threadIdx.x;
+        p[k] = make_int2(0, 0); op[k] = make_int2(0, 0); s[k] = 0; os[k] = 0; ost[k] = 0;
+        if (i < d.n) {
+            p[k] = __ldcs(npos + i);
+            s[k] = __ldcs(nstep + i);
+            if (mode == 0) {
+                os[k] = d.step[c][i];
+                ost[k] = d.status[c][i];
+                if (validate) op[k] = d.pos[c][i];
+            } else if (mode == 2) {
+                ost[k] = nstat[i];
+            }
+        }
+    }
 #pragma unroll
     for (int k = 0; k < kIngestItems; k++) {
         const int i = blockIdx.x * (256 * kIngestItems) + k * 256 + threadIdx.x;
         if (i >= d.n) break;
-        const int2 p = npos[i];
-        const int s = nstep[i];
         uint8_t st;
-        if (p.x < 0 || p.x >= d.map_w || p.y < 0 || p.y >= d.map_h) err |= ERR_BOUNDS;
+        if (p[k].x < 0 || p[k].x >= d.map_w || p[k].y < 0 || p[k].y >= d.map_h) err |= ERR_BOUNDS;
         if (mode == 0) {
-            const int os = d.step[c][i];
-            const uint8_t ost = d.status[c][i];
-            const long long ds = (long long)s - os;
-            st = ost;
+            const long long ds = (long long)s[k] - os[k];
+            st = ost[k];
             if (ds == 0) {
-                if (d.flags & AM_VALIDATE) {
-                    const int2 op = d.pos[c][i];
-                    if (op.x != p.x || op.y != p.y) err |= ERR_PROTOCOL;
-                }
+                if (validate && (op[k].x != p[k].x || op[k].y != p[k].y)) err |= ERR_PROTOCOL;
             } else if (ds == 1) {
                 // step changed since the last round (kept even if this update is rejected:
                 // that only makes the next round re-scan the agent)
                 if (d.chg8) d.chg8[i] = 1;
-                if (ost != ST_RUNNING) {
+                // its last-round cluster must be rebuilt by the next round's union-find
+                if (d.dirty) {
+                    const int lab = d.labels[i];
+                    if (lab >= 0) d.dirty[lab] = ctl->epoch + 1u;
+                }
+                if (ost[k] != ST_RUNNING) {
                     err |= ERR_PROTOCOL;
                 } else {
-                    if (d.flags & AM_VALIDATE) {
-                        const int2 op = d.pos[c][i];
-                        if (!within(p.x - op.x, p.y - op.y, (uint32_t)d.v, d.metric)) err |= ERR_VELOCITY;
-                    }
-                    st = (d.target > 0 && s == d.target) ? ST_DONE : ST_IDLE;
+                    if (validate && !within(p[k].x - op[k].x, p[k].y - op[k].y, (uint32_t)d.v, d.metric))
+                        err |= ERR_VELOCITY;
+                    st = (d.target > 0 && s[k] == d.target) ? ST_DONE : ST_IDLE;
                 }
             } else {
                 err |= ERR_PROTOCOL;
             }
         } else if (mode == 1) {
-            if (s < 0 || (d.target > 0 && s > d.target)) err |= ERR_PROTOCOL;
-            st = (d.target > 0 && s == d.target) ? ST_DONE : ST_IDLE;
+            if (s[k] < 0 || (d.target > 0 && s[k] > d.target)) err |= ERR_PROTOCOL;
+            st = (d.target > 0 && s[k] == d.target) ? ST_DONE : ST_IDLE;
         } else {
-            st = nstat[i];
-            if (st > ST_DONE || s < 0) err |= ERR_PROTOCOL;
+            st = ost[k];
+            if (st > ST_DONE || s[k] < 0) err |= ERR_PROTOCOL;
         }
-        d.pos[c ^ 1u][i] = p;
-        d.step[c ^ 1u][i] = s;
+        d.pos[c ^ 1u][i] = p[k];
+        d.step[c ^ 1u][i] = s[k];
         d.status[c ^ 1u][i] = st;
         if (st != ST_DONE) {
             act++;
-            smin = min(smin, s);
-            smax = max(smax, s);
+            smin = min(smin, s[k]);
+            smax = max(smax, s[k]);
         }
         run += st == ST_RUNNING;
     }
@@ -127,6 +146,25 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
 }
 
 // ============================================================== binned round
+// block-aggregated append of the flagged threads' values to queue stripe `stripe` (one
+// global atomic per block, in thread order); every thread of the 256-thread block calls it
+__device__ __forceinline__ void block_append(uint32_t* q, int cap, uint32_t* ctr, int stripe, bool flag,
+                                             uint32_t val, uint32_t* s_w /*[9]*/)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, flag);
+    if (lane == 0) s_w[w] = (uint32_t)__popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int k = 0; k < 8; k++) { const uint32_t v = s_w[k]; s_w[k] = acc; acc += v; }
+        s_w[8] = acc ? atomicAdd(ctr + stripe, acc) : 0u;
+    }
+    __syncthreads();
+    if (flag) q[(size_t)stripe * cap + s_w[8] + s_w[w] + (uint32_t)__popc(m & ((1u << lane) - 1u))] = val;
+    __syncthreads();   // s_w is reused
+}
+
 // k_bin: Morton cell key, slot inside the cell (atomic histogram), per-cell min step;
 // also resets the union-find forest and the per-root bad flags for this round.
 // It also builds the scan's work queue (see the incremental scan below): changed agents
@@ -135,41 +173,33 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
 __global__ void __launch_bounds__(256) k_bin(Dev d)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
     const uint32_t c = d.ctl->cur;
     bool work = false, chg = false;
     if (i < d.n) {
+        // independent loads first (one round trip), then the atomics and the witness's
+        // change flag (a second one)
         const uint8_t st = d.status[c][i];
+        const int2 p = d.pos[c][i];
+        const int s = d.step[c][i];
+        const bool ch = d.chg8[i] != 0;
+        const uint32_t w = d.witness[i];
         uint32_t key = kSentinel, rank = 0;
         if (st != ST_DONE) {
-            const int2 p = d.pos[c][i];
-            const int s = d.step[c][i];
             key = morton((uint32_t)p.x >> d.clog, (uint32_t)p.y >> d.clog);
             rank = atomicAdd(d.cnt + key, 1u);
             atomicMin(d.cmin + key, s);
-            chg = round_full(d) || d.chg8[i];
-            work = chg;
-            if (!work && st == ST_IDLE) {
-                const uint32_t w = d.witness[i];
-                work = w != kSentinel && agent_changed(d, c, w);
-            }
+            chg = round_full(d) || ch;
+            work = chg || (st == ST_IDLE && w != kSentinel && agent_changed(d, c, w));
         }
         d.key[i] = key;
         d.rank[i] = rank;
-        d.parent[i] = (uint32_t)i;
         d.bad[i] = 0;
         d.blkid[i] = 0;
     }
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, work);
-    if (m) {
-        const int stripe = (int)((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kEdgeStripes - 1));
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(d.wq_ctr + stripe, (uint32_t)__popc(m));
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
-        if (work)
-            d.wq[(size_t)stripe * d.wq_cap + base + __popc(m & ((1u << lane) - 1u))] =
-                (uint32_t)i | (chg ? 0x80000000u : 0u);
-    }
+    // work queue: stripe = block index mod 64, one atomic per block
+    __shared__ uint32_t s_w[9];
+    block_append(d.wq, d.wq_cap, d.wq_ctr, (int)(blockIdx.x & (kEdgeStripes - 1)), work,
+                 (uint32_t)i | (chg ? 0x80000000u : 0u), s_w);
 }
 
 // k_cells: exclusive scan of the cell counts in Morton order -> ctab{start, min};
@@ -246,14 +276,25 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n) return;
-    const uint32_t key = d.key[i];
-    if (key == kSentinel) return;
     const uint32_t c = d.ctl->cur;
+    const uint32_t key = d.key[i];
+    const uint32_t rk = d.rank[i];
     const int2 p = d.pos[c][i];
     const int s = d.step[c][i];
-    const uint32_t r = (uint32_t)d.ctab[key].x + d.rank[i];
-    const int chg = (round_full(d) || d.chg8[i]) ? kRecChanged : 0;
-    d.rec[r] = make_int4(p.x | (p.y << 16), s, i, d.status[c][i] | chg);
+    const uint8_t st = d.status[c][i];
+    const bool ch = d.chg8[i] != 0;
+    const int lab = d.labels[i];
+    if (key == kSentinel) return;
+    const uint32_t r = (uint32_t)d.ctab[key].x + rk;
+    const bool full = round_full(d);
+    const int chg = (full || ch) ? kRecChanged : 0;
+    d.rec[r] = make_int4(p.x | (p.y << 16), s, i, st | chg);
+    // union-find forest of this round: an agent whose last-round cluster has no changed
+    // member keeps that cluster (all its coupling edges are unchanged: it is still
+    // connected, and it can only grow through an edge of a changed agent), so it hangs
+    // under the old root (= min id = its label); members of dirty clusters start alone
+    const bool dirty = full || lab < 0 || d.dirty[lab] == d.ctl->epoch;
+    d.parent[i] = dirty ? (uint32_t)i : (uint32_t)lab;
 }
 
 // test every record of cell `key` against agent A; returns true if A got blocked.
@@ -519,8 +560,16 @@ __global__ void __launch_bounds__(256) k_efilter(Dev d)
         if (keep) {
             const uint32_t pos = s_base + wb + __popc(m & ((1u << lane) - 1u));
             d.edges[(size_t)(cur ^ 1u) * d.ecap + pos] = e;   // kept <= previous count <= ecap
+            // both endpoints were in one cluster last round; if that cluster is dirty its
+            // forest is rebuilt from its edges (a clean cluster's edges are implied by
+            // the members hanging under its root, k_scatter)
+            if (d.dirty[d.labels[e.x]] == d.ctl->epoch) uf_unite(d.parent, e.x, e.y);
         }
         __syncthreads();
+    }
+    if (finish_block(&d.ctl->efil, gridDim.x) && threadIdx.x == 0) {
+        d.ctl->ecarried = (int32_t)*(volatile uint32_t*)&d.ctl->ecnt[cur ^ 1u];
+        __threadfence();
     }
 }
 
@@ -533,6 +582,7 @@ __global__ void __launch_bounds__(256, 6) k_near(Dev d)
 {
     __shared__ EdgeStage s_all[8];
     __shared__ int s_pref[kEdgeStripes + 1];
+    __shared__ uint32_t s_w[9];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     EdgeStage& sm = s_all[wq];
     if (lane == 0) sm.ne = 0;
@@ -610,15 +660,8 @@ __global__ void __launch_bounds__(256, 6) k_near(Dev d)
             }
         }
         flush_stage(d, sm, lane);
-        // far queue: one atomic per warp on a striped counter
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, farq);
-        if (m) {
-            const int stripe = (blockIdx.x * 8 + wq) & (kEdgeStripes - 1);
-            uint32_t wbase = 0;
-            if (lane == 0) wbase = atomicAdd(d.farq_ctr + stripe, (uint32_t)__popc(m));
-            wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
-            if (farq) d.farq[(size_t)stripe * d.farq_cap + wbase + __popc(m & ((1u << lane) - 1u))] = aid;
-        }
+        // far queue: stripe = block index mod 64, one atomic per block iteration
+        block_append(d.farq, d.farq_cap, d.farq_ctr, (int)(blockIdx.x & (kEdgeStripes - 1)), farq, aid, s_w);
     }
 }
 
@@ -804,6 +847,152 @@ __global__ void __launch_bounds__(256) k_far2(Dev d)
     }
 }
 
+// k_far: the far phase with one HALF-WARP per far-queued agent A.  The Morton pyramid
+// has a fan-out of 16 at every level, so the 16 lanes test the 16 children of a block
+// at once: (level 2) the 16x16-cell blocks of A's R_b(s_A - W) box, 16 per step; (level
+// 1) the 4x4-cell children of each surviving block; (level 0) the cells of each
+// surviving 4x4 block (one 8-byte table entry per lane, next start by shuffle); the
+// records of the surviving cells are flattened over the lanes (prefix sum of the cell
+// counts, a 4-step shuffle search per lane) and tested 16 at a time.  Pruning is the
+// exact test of k_far1/k_far2 (min step m of a block: skip if m >= s_A or its box
+// distance exceeds R_b(s_A - m)); cells within R_c of A were tested by k_near.  The
+// first blocker found becomes A's witness.
+__global__ void __launch_bounds__(256) k_far(Dev d)
+{
+    __shared__ int s_pref[kEdgeStripes + 1];
+    __shared__ uint32_t s_items;
+    if (threadIdx.x == 0) s_items = 0;
+    stripe_prefix(d.farq_ctr, 1 << 30, s_pref);
+    const int nq = s_pref[kEdgeStripes];
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_far = nq;
+    const int W = d.ctl->W;
+    const uint32_t c = d.ctl->cur;
+    const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4, hw = threadIdx.x >> 4;
+    const unsigned hm = 0xFFFFu << (16 * h);
+    const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
+    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+    int ox_l, oy_l;
+    morton_child(l, ox_l, oy_l);
+    uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
+    for (int q0 = blockIdx.x * 16; q0 < nq; q0 += gridDim.x * 16) {
+        const int q = q0 + hw;
+        if (q >= nq) continue;   // half-warp uniform
+        int lo = 0, hi = kEdgeStripes - 1;          // last queue stripe with s_pref <= q
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
+        }
+        const uint32_t aid = d.farq[(size_t)lo * d.farq_cap + (q - s_pref[lo])];
+        const int2 P = d.pos[c][aid];
+        const int ax = P.x, ay = P.y, as = d.step[c][aid];
+        const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
+        const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
+        const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
+        const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);
+        uint32_t wit = kSentinel;
+        nb2 += l == 0 ? (uint32_t)nb : 0u;
+        for (int j0 = 0; j0 < nb && wit == kSentinel; j0 += 16) {
+            // level 2: 16 blocks of 16x16 cells per step
+            const int j = j0 + l;
+            const int bx = bx0 + j % nbx, by = by0 + j / nbx;
+            bool ok2 = false;
+            if (j < nb) {
+                const int m2 = __ldg(d.lmin2 + morton(bx, by));
+                ok2 = m2 < as && box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
+                                            rb_radius((long long)as - m2, d.v, d.r_p), d.metric);
+            }
+            unsigned mask2 = (__ballot_sync(hm, ok2) >> (16 * h)) & 0xFFFFu;
+            while (mask2 && wit == kSentinel) {
+                const int jj = __ffs(mask2) - 1;
+                mask2 &= mask2 - 1;
+                const int bxj = __shfl_sync(hm, bx, jj, 16), byj = __shfl_sync(hm, by, jj, 16);
+                const uint32_t k2 = morton(bxj, byj);
+                nb1 += l == 0 ? 16u : 0u;
+                // level 1: lane l tests child l (4x4 cells)
+                const int qx = bxj * 4 + ox_l, qy = byj * 4 + oy_l;
+                const int m1 = __ldg(d.lmin1 + k2 * 16 + l);
+                const bool ok1 = m1 < as && box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
+                                                       ((qy + 1) << l1) - 1, rb_radius((long long)as - m1, d.v, d.r_p),
+                                                       d.metric);
+                unsigned mask1 = (__ballot_sync(hm, ok1) >> (16 * h)) & 0xFFFFu;
+                while (mask1 && wit == kSentinel) {
+                    const int ii = __ffs(mask1) - 1;
+                    mask1 &= mask1 - 1;
+                    nitems += l == 0 ? 1u : 0u;
+                    const uint32_t k1g = k2 * 16 + (uint32_t)ii;
+                    const int qxi = __shfl_sync(hm, qx, ii, 16), qyi = __shfl_sync(hm, qy, ii, 16);
+                    // level 0: lane l tests cell l of the 4x4 block
+                    const int2 e = d.ctab[(size_t)k1g * 16 + l];
+                    int nx = __shfl_down_sync(hm, e.x, 1, 16);
+                    if (l == 15) nx = d.ctab[(size_t)k1g * 16 + 16].x;
+                    const int cx = qxi * 4 + ox_l, cy = qyi * 4 + oy_l;
+                    const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
+                    const bool okc = nx > e.x && e.y < as && !box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric) &&
+                                     box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - e.y, d.v, d.r_p),
+                                                d.metric);
+                    const int cnt = okc ? nx - e.x : 0;
+                    ncells += nx > e.x ? 1u : 0u;
+                    // flatten the candidate records over the 16 lanes
+                    int incl = cnt;
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) {
+                        const int y = __shfl_up_sync(hm, incl, o, 16);
+                        if (l >= o) incl += y;
+                    }
+                    const int excl = incl - cnt;
+                    const int total = __shfl_sync(hm, incl, 15, 16);
+                    ncand += l == 0 ? (uint32_t)total : 0u;
+                    for (int b0 = 0; b0 < total && wit == kSentinel; b0 += 16) {
+                        const int tq = b0 + l;
+                        // lane holding candidate tq: the last lane with excl <= tq
+                        int sl = 0;
+#pragma unroll
+                        for (int st = 8; st > 0; st >>= 1) {
+                            const int ex = __shfl_sync(hm, excl, sl + st, 16);
+                            if (ex <= tq) sl += st;
+                        }
+                        const int rs = __shfl_sync(hm, e.x, sl, 16), rx = __shfl_sync(hm, excl, sl, 16);
+                        bool found = false;
+                        uint32_t bid = 0;
+                        if (tq < total) {
+                            const int4 B = d.rec[rs + (tq - rx)];
+                            bid = (uint32_t)B.z;
+                            if (B.y < as) {
+                                const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                                const uint32_t Rb = min((uint32_t)min(as - B.y, lagcap) * (uint32_t)d.v +
+                                                            (uint32_t)(d.v + d.r_p), kRClamp);
+                                found = within2(dx, dy, Rb * Rb, Rb, d.metric);
+                            }
+                        }
+                        const unsigned fm = (__ballot_sync(hm, found) >> (16 * h)) & 0xFFFFu;
+                        if (fm) wit = __shfl_sync(hm, bid, __ffs(fm) - 1, 16);
+                    }
+                }
+            }
+        }
+        if (l == 0) {
+            d.v8[aid] = wit != kSentinel ? 1 : 0;
+            d.witness[aid] = wit;
+        }
+    }
+    const unsigned it = __reduce_add_sync(0xFFFFFFFFu, nitems);
+    if (lane == 0 && it) atomicAdd(&s_items, it);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_items) atomicAdd(&d.ctl->n_items, (int)s_items);
+    if (d.flags & AM_STATS) {
+        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
+        const unsigned c3 = __reduce_add_sync(0xFFFFFFFFu, nb2), c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
+        if (lane == 0) {
+            atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
+            atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
+            atomicAdd(&d.ctl->st_p2, (unsigned long long)it);   // far work items (4x4 blocks)
+            atomicAdd(&d.ctl->st_b2, (unsigned long long)c3);
+            atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
+        }
+    }
+}
+
 // k_union: unite this round's coupling edges (carried-over + new), one thread per edge
 // (ECL-CC style hooking of the larger root under the smaller, so roots stay the
 // minimum id); the last block makes the list current for the next round.
@@ -812,7 +1001,8 @@ __global__ void __launch_bounds__(256) k_union(Dev d)
     const uint32_t nxt = d.ctl->ecur ^ 1u;
     const int ne = min((int)d.ctl->ecnt[nxt], d.ecap);
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_edges = ne;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ne; k += gridDim.x * blockDim.x) {
+    // the carried edges were united by k_efilter where their cluster was dirty
+    for (int k = d.ctl->ecarried + blockIdx.x * blockDim.x + threadIdx.x; k < ne; k += gridDim.x * blockDim.x) {
         const uint2 e = d.edges[(size_t)nxt * d.ecap + k];
         uf_unite(d.parent, e.x, e.y);
     }
@@ -824,17 +1014,18 @@ __global__ void __launch_bounds__(256) k_union(Dev d)
 
 // k_finalize: label = root of the agent's tree (= min id of its cluster, Q10);
 // a blocked or RUNNING member makes its cluster not ready (Q7).
+// Id order: status / parent / verdict / label accesses are coalesced; only agents
+// whose parent is not themselves chase pointers (singletons are one load).
 __global__ void __launch_bounds__(256) k_finalize(Dev d)
 {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= d.ctl->n_active) return;
-    const int4 A = d.rec[r];
-    const uint32_t aid = (uint32_t)A.z;
-    const uint32_t root = uf_find(d.parent, aid);
-    d.labels[aid] = (int32_t)root;
-    const uint8_t st = (uint8_t)(A.w & 3);
-    const bool blk = st == ST_IDLE && d.v8[aid] == 1;
-    d.blkid[aid] = blk;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.n) return;
+    const uint8_t st = d.status[d.ctl->cur][i];
+    if (st == ST_DONE) return;
+    const uint32_t root = uf_find(d.parent, (uint32_t)i);
+    d.labels[i] = (int32_t)root;
+    const bool blk = st == ST_IDLE && d.v8[i] == 1;
+    d.blkid[i] = blk;
     if (blk || st == ST_RUNNING) d.bad[root] = 1;
 }
 
@@ -895,27 +1086,38 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) ncl = 0;
     const int i0 = tile * kReadyTile + t * 8;
-    uint8_t ready[8];
+    uint8_t ready[8], st[8];
     int lab[8];
     uint32_t cnt = 0, mycl = 0;
+    // loads in two independent rounds (status + label, then the roots' bad flags),
+    // stores after
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         const int i = i0 + k;
-        ready[k] = 0;
+        st[k] = ST_DONE;
         lab[k] = -1;
         if (i < d.n) {
-            const uint8_t st = d.status[c][i];
+            st[k] = d.status[c][i];
+            lab[k] = d.labels[i];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        ready[k] = 0;
+        if (st[k] != ST_DONE && ok && st[k] == ST_IDLE) ready[k] = !d.bad[lab[k]];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int i = i0 + k;
+        if (i < d.n) {
             if (d.chg8) d.chg8[i] = 0;     // the round consumed this agent's change
-            if (st == ST_DONE) {
+            if (st[k] == ST_DONE) {
                 d.labels[i] = -1;
-            } else {
-                lab[k] = d.labels[i];
-                ready[k] = ok && st == ST_IDLE && !d.bad[lab[k]];
-                if (ready[k]) {
-                    if (!peek) d.status[c][i] = ST_RUNNING;
-                    cnt++;
-                    mycl += (lab[k] == i);
-                }
+                lab[k] = -1;
+            } else if (ready[k]) {
+                if (!peek) d.status[c][i] = ST_RUNNING;
+                cnt++;
+                mycl += (lab[k] == i);
             }
             mask[i] = ready[k];
         }
@@ -972,6 +1174,7 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
         int bits = o ? 64 - __clzll((long long)o) : 0;
         int np = (bits + kRadixBits - 1) / kRadixBits;
         ctl->npasses = np < 1 ? 1 : np;
+        ctl->sort_bits = bits;
         ctl->sort_or = 0;
         ctl->full = 0;
     }
@@ -1254,6 +1457,7 @@ __global__ void k_round_begin(Dev d)
     ctl->epoch += 1;
     ctl->n_ready = 0;
     ctl->n_clusters = 0;
+    ctl->n_items = 0;
     ctl->full |= ctl->full_next;
     ctl->full_next = 0;
     ctl->ecnt[ctl->ecur ^ 1u] = 0;

@@ -286,3 +286,36 @@ def test_large_ready_set_closed_form(path):
     # a second round on the dispatched state: nothing is ready
     mask, order = tr.ready()
     assert len(order) == 0
+
+
+@pytest.mark.parametrize("wide", [False, True], ids=["keys32", "keys64"])
+@pytest.mark.parametrize("sort", ["cluster", "onesweep"])
+@pytest.mark.parametrize("pairs", [1, 700, 21000, 150000])
+def test_interleaved_pair_clusters_closed_form(pairs, sort, wide, monkeypatch):
+    """Coupled pairs whose members are n/2 ids apart (clusters interleave in id space),
+    isolated from each other (spacing 20 > R_b(4) = 9): label = min id of the pair, and
+    order = ready agents sorted by (step, label, id) -- the priority rule P:143 / Q9 /
+    Q10 as a closed form.  Sizes span the cluster sort's shared-memory-resident mode
+    (<= 16 x ~8k ready agents) and its streaming mode, and the onesweep ablation.
+    `wide`: v = 0 (R_b = r_p at any lag) with step gaps up to ~2^27, so the priority keys
+    need more than 32 bits (the 16-byte element path of the cluster sort)."""
+    if sort == "onesweep":
+        monkeypatch.setenv("AM_SORT", "onesweep")
+    n = 2 * pairs
+    side = int(np.ceil(np.sqrt(pairs)))
+    k = np.arange(pairs)
+    px = ((k % side) * 20).astype(np.int32)
+    py = ((k // side) * 20).astype(np.int32)
+    x = np.concatenate([px, px + 1]).astype(np.int32)       # partner one tile east
+    y = np.concatenate([py, py]).astype(np.int32)
+    step = (k * 7919 % 5).astype(np.int32) * (33554467 if wide else 1)
+    s = np.concatenate([step, step]).astype(np.int32)
+    st = np.zeros(n, np.uint8)
+    ids = np.arange(n)
+    label = np.concatenate([k, k]).astype(np.int32)
+    tr = Tracker(side * 20 + 2, side * 20 + 2, 4, 0 if wide else 1, n, force="binned")
+    g = _gpu_round(tr, x, y, s, st)
+    assert g["mask"].all()
+    np.testing.assert_array_equal(g["label"], label)
+    np.testing.assert_array_equal(g["order"], np.lexsort((ids, label, s)))
+    tr.close()
