@@ -48,12 +48,14 @@ def algorithmic_bytes(kernel: str, s: dict) -> float:
         "k_cells": 24.27 * c,
         # read key 4 + rank 4 + cell start 4 + pos 8 + step 4 + status 1; write record 16
         "k_scatter": 41.0 * a,
-        # incremental near phase, per re-scanned agent w: read pos 8 + step 4 + status 1 +
-        # own cell entry 8; write verdict 1 + witness 4 + a new edge 8; carried edges 8 each
-        "k_near": 34.0 * s["n_work"] + 8.0 * s["n_edges"],
-        # far phase, per far-queued agent f: read pos 8 + step 4 + 16x16 / 4x4 level words
-        # 4 + 64; write verdict 1 + witness 4; per work item: 16-cell entry block 136
-        "k_scan": 85.0 * s["n_far"] + 136.0 * s["n_items"],
+        # k_efilter (timed as "k_near"): read last round's edge list 8 per edge, write the
+        # kept ones 8 per edge (upper bound on the kept share: all)
+        "k_near": 16.0 * s["n_edges"],
+        # k_scan_hw, per re-scanned agent w: read queue entry 4 + pos 8 + step 4 + status 1
+        # + own cell entry 8; write verdict 1 + witness 4 + a new edge 8; per far agent f:
+        # 16x16 / 4x4 level words 4 + 64; per far item (surviving 4x4-cell block): its
+        # 16 cell entries 136
+        "k_scan": 38.0 * s["n_work"] + 68.0 * s["n_far"] + 136.0 * s["n_items"],
         # read record 16 + blocked bit 0.125 + parent 4; write label 4
         "k_finalize": 24.125 * a,
         # read status 1 + label 4 + bad 1; write mask 1 + status 1; ready: step 4 + key/id 12

@@ -28,7 +28,8 @@ struct RepDev {
     long long* tdone;           // [S] time of the last commit that finished an agent
     long long* rounds;          // [S]
     int32_t* active_flag;       // [S]
-    const int32_t* order;       // this round's order (replay-owned)
+    const int32_t* order;       // this round's ready agents (any order: the ready list of the
+                                // binned path, the priority order of the fused path)
     long long* dispatched;      // [1]
     int32_t* liveness;          // [1]
     Chain* chain;               // last-block counter of k_disp_b
@@ -69,6 +70,7 @@ __device__ __forceinline__ long long duration(const am_synth& sy, int i, int s)
 // event; any agent left active marks its simulation active for the next round.
 __global__ void __launch_bounds__(256) k_commit(RepDev r)
 {
+    pdl_begin();
     const Dev& d = r.d;
     const bool one = d.n_sims == 1;
     const uint32_t c = d.ctl->cur;
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r)
 // the cluster's root label; a stale value is <= t).
 __global__ void __launch_bounds__(256) k_disp_a(RepDev r)
 {
+    pdl_begin();
     const Dev& d = r.d;
     const int nr = d.ctl->n_ready;
     if (blockIdx.x == 0 && threadIdx.x == 0) *r.dispatched += nr;
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(256) k_disp_a(RepDev r)
 // perception digest), next event per simulation (last block).
 __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
 {
+    pdl_begin();
     const Dev& d = r.d;
     const int nr = d.ctl->n_ready;
     unsigned long long tmin = ~0ull;
@@ -252,13 +256,14 @@ static int enqueue_round(am_replay* rp)
     rp->r.d = c->d;
     am_prof_begin(c, K_DISP_A);
     const unsigned nbd = std::min(nb, (unsigned)c->num_sms * 4);   // grid-stride over the ready list
-    k_disp_a<<<nbd, 256, 0, rp->stream>>>(rp->r);
+    RK(launch_k(c->pdl, rp->stream, k_disp_a, nbd, 256, 0, rp->r));
     am_prof_end(c, K_DISP_A);
     am_prof_begin(c, K_DISP_B);
-    k_disp_b<<<nbd, 256, 0, rp->stream>>>(rp->r);
+    RK(launch_k(c->pdl, rp->stream, k_disp_b, nbd, 256, 0, rp->r));
     am_prof_end(c, K_DISP_B);
     am_prof_begin(c, K_COMMIT);
-    k_commit<<<(unsigned)((n + 256 * kIngestItems - 1) / (256 * kIngestItems)), 256, 0, rp->stream>>>(rp->r);
+    RK(launch_k(c->pdl, rp->stream, k_commit, (unsigned)((n + 256 * kIngestItems - 1) / (256 * kIngestItems)), 256, 0, rp->r));
+    am_join_side(c);   // the priority sort ran beside dispatch and commit
     am_prof_end(c, K_COMMIT);
     RK(cudaGetLastError());
     return AM_OK;
@@ -311,7 +316,7 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
     r.chain = (Chain*)(b + o_chain);
     rp->mask = (uint8_t*)(b + o_mask);
     rp->order = (int32_t*)(b + o_order);
-    r.order = rp->order;
+    r.order = ctx->path == 1 ? ctx->d.rid : rp->order;
     RK(cudaStreamCreateWithFlags(&rp->stream, cudaStreamNonBlocking));
     RK(cudaMallocHost((void**)&rp->h_buf, 64));
     RK(cudaStreamSynchronize(rp->user_stream));

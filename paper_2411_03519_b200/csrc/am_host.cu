@@ -21,6 +21,7 @@ __global__ void k_near(Dev d);
 __global__ void k_far1(Dev d);
 __global__ void k_far2(Dev d);
 __global__ void k_far(Dev d);
+__global__ void k_scan_hw(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
 __global__ void k_sort_pass(Dev d, int pass, int32_t* order, int ntiles);
@@ -163,7 +164,7 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 2 : 12 + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
+    return c->path == 0 ? 2 : 10 + (c->scan_split ? (c->far_items ? 3 : 2) : 1) + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -212,6 +213,8 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
     if (const char* e = getenv("AM_SORT_CTAS")) x->sort_ctas = std::max(1, atoi(e));   // tuning knob
     if (const char* e = getenv("AM_FAR")) x->far_items = !strcmp(e, "items");          // ablation
+    if (const char* e = getenv("AM_SCAN")) x->scan_split = !strcmp(e, "split");        // ablation
+    if (const char* e = getenv("AM_PDL")) x->pdl = atoi(e) != 0;                      // ablation
     // the one-kernel cluster sort: the largest cluster (16, else 8) that can be resident
     {
         const char* e = getenv("AM_SORT");   // "onesweep" = multi-kernel ablation
@@ -219,11 +222,11 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
             int dev = 0, maxsm = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-            // pairs per CTA: 3 buffers of 16-byte elements at worst (64-bit keys)
-            const size_t fixed = csort_smem_fixed();
-            const int cap = (size_t)maxsm > fixed ? (int)(((size_t)maxsm - fixed) / 48) : 0;
+            // shared memory: the fixed part + two tile buffers (8192 x 8 or 4096 x 16 bytes)
+            const size_t need = csort_smem_fixed() + 2 * 8192 * 8;
+            const int cap = (size_t)maxsm >= need ? 1024 : 0;
             if (cap >= 1024 &&
-                cudaFuncSetAttribute(k_csort, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) == cudaSuccess) {
+                cudaFuncSetAttribute(k_csort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need) == cudaSuccess) {
                 cudaFuncSetAttribute(k_csort, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
                 int want = 0;
                 if (const char* q = getenv("AM_CSORT_CTAS")) want = atoi(q);   // tuning knob
@@ -232,7 +235,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
                     cudaLaunchConfig_t lc{};
                     lc.gridDim = dim3(cs);
                     lc.blockDim = dim3(1024);
-                    lc.dynamicSmemBytes = (size_t)maxsm;
+                    lc.dynamicSmemBytes = need;
                     cudaLaunchAttribute at{};
                     at.id = cudaLaunchAttributeClusterDimension;
                     at.val.clusterDim.x = cs; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
@@ -240,7 +243,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
                     int ncl = 0;
                     if (cudaOccupancyMaxActiveClusters(&ncl, k_csort, &lc) == cudaSuccess && ncl >= 1) {
                         x->csort_ctas = cs;
-                        x->csort_cap = maxsm;   // dynamic shared memory bytes per CTA
+                        x->csort_cap = (int)need;   // dynamic shared memory bytes per CTA
                         break;
                     }
                 }
@@ -318,15 +321,15 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
     size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
-           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0, o_fctr = 0, o_wq = 0, o_dirty = 0;
+           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0, o_fctr = 0, o_wq = 0, o_dirty = 0, o_agf = 0, o_rid = 0;
     const size_t NC = (size_t)d.ncells;
     if (x->path == 1) {
         o_key = take(4 * N); o_rank = take(4 * N);
         o_cnt = take(4 * NC); o_cmin = take(4 * NC);
         o_ctab = take(8 * (NC + 1)); o_l1 = take(4 * (NC / 16)); o_l2 = take(4 * (NC / 256));
         o_rec = take(16 * N); o_blk = take(N);
-        o_par = take(4 * N); o_bad = take(N); o_dirty = take(4 * N);
-        o_rk0 = take(8 * N); o_rk1 = take(8 * N); o_rv0 = take(4 * N); o_rv1 = take(4 * N);
+        o_par = take(4 * N); o_bad = take(N); o_dirty = take(4 * N); o_agf = take(N);
+        o_rk0 = take(8 * N); o_rk1 = take(8 * N); o_rid = take(4 * N); o_rv0 = take(4 * N); o_rv1 = take(4 * N);
         o_tc = take(8 * (size_t)x->ntiles_cells); o_tr = take(8 * (size_t)x->ntiles_ready);
         o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * kRadix);
         o_gh = take(4 * kMaxSortPasses * kRadix); o_gs = take(4 * kMaxSortPasses * kRadix);
@@ -347,6 +350,12 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     x->ws_bytes = off;
     cudaError_t e = cudaMalloc(&x->ws, off);
     if (e != cudaSuccess) { delete x; return cuda_err(nullptr, e, "am_init: cudaMalloc"); }
+    if (x->path == 1 && x->csort_ctas) {
+        e = cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming);
+        if (e != cudaSuccess) { cudaFree(x->ws); delete x; return cuda_err(nullptr, e, "am_init: side stream"); }
+    }
     e = cudaMallocHost((void**)&x->h_ctl, sizeof(Ctl));
     if (e != cudaSuccess) { cudaFree(x->ws); delete x; return cuda_err(nullptr, e, "am_init: cudaMallocHost"); }
     char* b = (char*)x->ws;
@@ -363,8 +372,8 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.cnt = (uint32_t*)(b + o_cnt); d.cmin = (int32_t*)(b + o_cmin);
         d.ctab = (int2*)(b + o_ctab); d.lmin1 = (int32_t*)(b + o_l1); d.lmin2 = (int32_t*)(b + o_l2);
         d.rec = (int4*)(b + o_rec); d.v8 = (uint8_t*)(b + o_blk);
-        d.parent = (uint32_t*)(b + o_par); d.bad = (uint8_t*)(b + o_bad); d.dirty = (uint32_t*)(b + o_dirty);
-        d.rkey[0] = (unsigned long long*)(b + o_rk0); d.rkey[1] = (unsigned long long*)(b + o_rk1);
+        d.parent = (uint32_t*)(b + o_par); d.bad = (uint8_t*)(b + o_bad); d.dirty = (uint32_t*)(b + o_dirty); d.agflag = (uint8_t*)(b + o_agf);
+        d.rid = (int32_t*)(b + o_rid); d.rkey[0] = (unsigned long long*)(b + o_rk0); d.rkey[1] = (unsigned long long*)(b + o_rk1);
         d.rval[0] = (uint32_t*)(b + o_rv0); d.rval[1] = (uint32_t*)(b + o_rv1);
         d.tiles_c = (unsigned long long*)(b + o_tc); d.tiles_r = (unsigned long long*)(b + o_tr);
         d.tiles_sort = (unsigned long long*)(b + o_tsort);
@@ -401,8 +410,9 @@ static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, co
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
     if (c->d.n == 0) return AM_OK;
     if (!pos || !steps || (mode == 2 && !st)) return set_err(c, AM_E_ARG, "NULL array");
+    am_join_side(c);
     am_prof_begin(c, K_INGEST);
-    k_ingest<<<blocks(c->d.n, 256 * kIngestItems), 256, 0, c->stream>>>(c->d, (const int2*)pos, steps, st, mode);
+    CK(c, launch_k(c->pdl, c->stream, k_ingest, blocks(c->d.n, 256 * kIngestItems), 256, 0, c->d, (const int2*)pos, steps, st, mode));
     am_prof_end(c, K_INGEST);
     CK(c, cudaGetLastError());
     return AM_OK;
@@ -448,9 +458,19 @@ static void fill_stats(am_ctx* c)
     c->stats.n_passes = h.npasses;
 }
 
+// the main stream waits for the side-stream sort of the last round
+void am_join_side(am_ctx* c)
+{
+    if (c->join_pending) {
+        cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+        c->join_pending = false;
+    }
+}
+
 extern "C" int am_sync(am_ctx* c)
 {
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    am_join_side(c);
     CK(c, cudaMemcpyAsync(c->h_ctl, c->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
     fill_stats(c);
@@ -478,6 +498,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         return AM_OK;
     }
     if (!mask || !order) return set_err(c, AM_E_ARG, "NULL mask/order");
+    am_join_side(c);   // the previous round's sort reads the buffers this round rewrites
     const Dev& d = c->d;
     cudaStream_t s = c->stream;
 #define LAUNCH(id, ...)        \
@@ -486,62 +507,83 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         __VA_ARGS__;           \
         am_prof_end(c, id);    \
     } while (0)
-    k_round_begin<<<1, 1, 0, s>>>(d);
+    CK(c, launch_k(c->pdl, s, k_round_begin, 1, 1, 0, d));
     if (c->path == 0) {
-        LAUNCH(K_SMALL, (k_small<<<d.n_sims, c->small_threads, 0, s>>>(d, mask, order)));
+        LAUNCH(K_SMALL, CK(c, launch_k(c->pdl, s, k_small, d.n_sims, c->small_threads, 0, d, mask, order)));
     } else {
         const unsigned nb = blocks(d.n, 256);
-        LAUNCH(K_BIN, (k_bin<<<nb, 256, 0, s>>>(d)));
-        LAUNCH(K_CELLS, (k_cells<<<c->ntiles_cells, 256, 0, s>>>(d)));
-        LAUNCH(K_SCATTER, (k_scatter<<<nb, 256, 0, s>>>(d)));
+        LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, nb, 256, 0, d)));
+        LAUNCH(K_CELLS, CK(c, launch_k(c->pdl, s, k_cells, c->ntiles_cells, 256, 0, d)));
+        LAUNCH(K_SCATTER, CK(c, launch_k(c->pdl, s, k_scatter, nb, 256, 0, d)));
         if (d.flags & AM_SCAN_THREAD)   // ablation: everything recomputed, no witnesses
-            LAUNCH(K_SCAN, (k_scan_thread<<<nb, 256, 0, s>>>(d)));
+            LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_thread, nb, 256, 0, d)));
         else
         {
             const unsigned pers = (unsigned)c->num_sms * 8;   // persistent grid-stride kernels
             // coupling edges of unchanged pairs carried over; scan of the work queue
-            LAUNCH(K_NEAR, (k_efilter<<<std::min(blocks(d.ecap, 256), pers), 256, 0, s>>>(d),
-                            k_near<<<std::min(nb, pers), 256, 0, s>>>(d)));
-            // far phase over the compacted queue: pyramid levels, then one thread per
-            // surviving (agent, 4x4-cell block) item
-            am_prof_begin(c, K_SCAN);
-            if (c->far_items) {   // ablation: per-agent pyramid pass + per-(agent, 4x4 block) items
-                k_far1<<<std::min(nb, pers), 256, 0, s>>>(d);
-                k_far2<<<std::min(nb, pers), 256, 0, s>>>(d);
-            } else {              // one half-warp per far-queued agent
-                k_far<<<std::min(nb, pers), 256, 0, s>>>(d);
+            if (c->scan_split) {
+                // ablation: k_near (thread per agent) + far queue + far kernel(s)
+                am_prof_begin(c, K_NEAR);
+                CK(c, launch_k(c->pdl, s, k_efilter, std::min(blocks(d.ecap, 256), pers), 256, 0, d));
+                CK(c, launch_k(c->pdl, s, k_near, std::min(nb, pers), 256, 0, d));
+                am_prof_end(c, K_NEAR);
+                am_prof_begin(c, K_SCAN);
+                if (c->far_items) {   // per-agent pyramid pass + per-(agent, 4x4 block) items
+                    CK(c, launch_k(c->pdl, s, k_far1, std::min(nb, pers), 256, 0, d));
+                    CK(c, launch_k(c->pdl, s, k_far2, std::min(nb, pers), 256, 0, d));
+                } else {              // one half-warp per far-queued agent
+                    CK(c, launch_k(c->pdl, s, k_far, std::min(nb, pers), 256, 0, d));
+                }
+                am_prof_end(c, K_SCAN);
+            } else {
+                LAUNCH(K_NEAR, CK(c, launch_k(c->pdl, s, k_efilter, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
+                // one half-warp per queued agent: near phase, then far phase
+                LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw, std::min(blocks(d.n, 16), pers), 256, 0, d)));
             }
-            am_prof_end(c, K_SCAN);
-            LAUNCH(K_UNION, (k_union<<<std::min(blocks(d.ecap, 256), pers), 256, 0, s>>>(d)));
+            LAUNCH(K_UNION, CK(c, launch_k(c->pdl, s, k_union, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
         }
-        LAUNCH(K_FINALIZE, (k_finalize<<<nb, 256, 0, s>>>(d)));
-        LAUNCH(K_READY, (k_ready<<<c->ntiles_ready, 256, 0, s>>>(d, mask)));
+        LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, nb, 256, 0, d)));
+        LAUNCH(K_READY, CK(c, launch_k(c->pdl, s, k_ready, c->ntiles_ready, 256, 0, d, mask)));
         if (c->csort_ctas) {
-            // one cluster of csort_ctas CTAs sorts the whole ready set (am_sort.cu)
+            // one cluster of csort_ctas CTAs sorts the whole ready set (am_sort.cu), on the
+            // side stream: nothing else in the round reads `order` (digests and dispatch
+            // take the id-ordered ready list), so it overlaps the rest of the round and
+            // joins the main stream at am_join_side (end of a replay round, am_sync)
+            CK(c, cudaEventRecord(c->ev_fork, s));
+            CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
             cudaLaunchConfig_t lc{};
             lc.gridDim = dim3(c->csort_ctas);
             lc.blockDim = dim3(1024);
             lc.dynamicSmemBytes = (size_t)c->csort_cap;
-            lc.stream = s;
+            lc.stream = c->side;
             cudaLaunchAttribute at{};
             at.id = cudaLaunchAttributeClusterDimension;
             at.val.clusterDim.x = c->csort_ctas; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
             lc.attrs = &at; lc.numAttrs = 1;
-            LAUNCH(K_SORT_PASS, CK(c, cudaLaunchKernelEx(&lc, k_csort, d, order, c->csort_cap)));
+            cudaStream_t ms = c->stream;
+            c->stream = c->side;   // profiling events of the sort on its stream
+            am_prof_begin(c, K_SORT_PASS);
+            const cudaError_t le = cudaLaunchKernelEx(&lc, k_csort, d, order, c->csort_cap);
+            am_prof_end(c, K_SORT_PASS);
+            c->stream = ms;
+            if (le != cudaSuccess) return cuda_err(c, le, "k_csort launch");
+            CK(c, cudaEventRecord(c->ev_join, c->side));
+            c->join_pending = true;
         } else {
-            LAUNCH(K_SORT_HIST, (k_sort_hist<<<std::min(c->ntiles_sort, 32), 256, 0, s>>>(d, c->sort_passes_max)));
+            LAUNCH(K_SORT_HIST, CK(c, launch_k(c->pdl, s, k_sort_hist, std::min(c->ntiles_sort, 32), 256, 0, d, c->sort_passes_max)));
             am_prof_begin(c, K_SORT_PASS);
             for (int p = 0; p < c->sort_passes_max; p++)   // persistent: <= 16 CTAs take tiles
-                k_sort_pass<<<std::min(c->ntiles_sort, c->sort_ctas), 1024, kSortSmem, s>>>(d, p, order, c->ntiles_sort);
+                CK(c, launch_k(c->pdl, s, k_sort_pass, std::min(c->ntiles_sort, c->sort_ctas), 1024, kSortSmem, d, p, order, c->ntiles_sort));
             am_prof_end(c, K_SORT_PASS);
         }
         // perception digests of the dispatched agents (replay driver)
-        if (d.flags & AM_DIGEST) k_digest<<<std::min(nb, (unsigned)c->num_sms * 2), 256, 0, s>>>(d, order);
+        if (d.flags & AM_DIGEST) CK(c, launch_k(c->pdl, s, k_digest, std::min(nb, (unsigned)c->num_sms * 2), 256, 0, d, (const int32_t*)d.rid));
     }
 #undef LAUNCH
     CK(c, cudaGetLastError());
     c->have_round = true;
     if (async) return AM_OK;
+    am_join_side(c);
     int rc = am_sync(c);
     *n_ready = rc == AM_OK ? c->h_ctl->n_ready : 0;
     return rc;
@@ -623,6 +665,12 @@ extern "C" int am_destroy(am_ctx* c)
     if (c->prof.ev[0][0])
         for (int k = 0; k < K_COUNT; k++)
             for (int j = 0; j < 2; j++) cudaEventDestroy(c->prof.ev[k][j]);
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaStreamDestroy(c->side);
+        cudaEventDestroy(c->ev_fork);
+        cudaEventDestroy(c->ev_join);
+    }
     cudaFree(c->ws);
     cudaFreeHost(c->h_ctl);
     delete c;

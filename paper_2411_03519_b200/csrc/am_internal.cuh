@@ -101,11 +101,13 @@ struct Dev {
     int32_t wq_cap;
     uint32_t* parent;      // [n] union-find forest in id space (root = min id)
     uint32_t* dirty;       // [n] per last-round label: epoch of the round its cluster must be rebuilt in
+    uint8_t* agflag;       // [n] per agent, this round (k_scatter): bit 0 changed, bit 1 cluster dirty
     uint8_t* bad;          // [n] cluster (root) has a blocked or RUNNING member
     int32_t* labels;       // [n]
     uint8_t* blkid;        // [n] blocked verdict per id (IDLE agents; 0 otherwise)
     unsigned long long* digest;   // [n] perception digests (AM_DIGEST)
     unsigned long long* rkey[2];  // [n] ready keys (ping-pong)
+    int32_t* rid;                 // [n] ready ids in id order (k_ready; dispatch and digests read it)
     uint32_t* rval[2];            // [n] ready ids (ping-pong)
     unsigned long long* tiles_c;  // chained-scan tile words: cell table scan
     unsigned long long* tiles_r;  //   ready compaction
@@ -134,11 +136,31 @@ struct Prof {
 };
 }  // namespace am
 
+// launch with the programmatic-stream-serialization attribute (pdl) -- the kernel must
+// begin with pdl_begin()
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(bool pdl, cudaStream_t s, void (*k)(KArgs...), dim3 g, dim3 b, size_t smem,
+                            Args... args)
+{
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = g;
+    lc.blockDim = b;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at.val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = &at;
+    lc.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&lc, k, static_cast<KArgs>(args)...);
+}
+
 struct am_ctx;
 void am_prof_begin(am_ctx* c, int id);
 void am_prof_end(am_ctx* c, int id);
 void am_prof_collect(am_ctx* c);
 void am_prof_mark(am_ctx* c, unsigned mask);
+void am_join_side(am_ctx* c);
 
 struct am_ctx {
     am::Prof prof;
@@ -151,6 +173,11 @@ struct am_ctx {
     int num_sms = 148;
     int sort_ctas = 16;              // persistent CTAs of each radix pass
     int sort_passes_max = 1;
+    cudaStream_t side = nullptr;     // the priority sort runs here, beside digest/dispatch
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool join_pending = false;
+    bool pdl = true;                 // programmatic dependent launch between round kernels
+    int scan_split = 0;              // scan as k_near + far kernel(s) (ablation)
     int far_items = 0;               // far phase as k_far1 + k_far2 (ablation)
     int csort_ctas = 0;              // cluster size of the one-kernel priority sort (0 = onesweep)
     int csort_cap = 0;               // dynamic shared memory bytes per CTA of k_csort
@@ -167,6 +194,16 @@ struct am_ctx {
 
 // ---------------------------------------------------------------- device helpers
 namespace am {
+
+// Programmatic dependent launch: every kernel of the round starts with this.  It waits
+// until the preceding kernel of the stream has completed and its memory is visible (a
+// no-op without the launch attribute), then lets the next kernel's CTAs be launched, so
+// grid launch and CTA rasterisation overlap the tail of the kernel before.
+__device__ __forceinline__ void pdl_begin()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ uint32_t part1by1(uint32_t x)
 {

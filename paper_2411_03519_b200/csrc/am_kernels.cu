@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
                                                 const int32_t* __restrict__ nstep,
                                                 const uint8_t* __restrict__ nstat, int mode)
 {
+    pdl_begin();
     Ctl* ctl = d.ctl;
     const uint32_t c = ctl->cur;
     int err = 0, act = 0, run = 0, smin = INT_MAX, smax = INT_MIN;
@@ -172,6 +173,7 @@ __device__ __forceinline__ void block_append(uint32_t* q, int cap, uint32_t* ctr
 // changed.
 __global__ void __launch_bounds__(256) k_bin(Dev d)
 {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t c = d.ctl->cur;
     bool work = false, chg = false;
@@ -207,6 +209,7 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
 // resets cnt/cmin for the next round.  256 threads x 16 cells per tile.
 __global__ void __launch_bounds__(256) k_cells(Dev d)
 {
+    pdl_begin();
     Ctl* ctl = d.ctl;
     __shared__ uint32_t wsum[8];
     __shared__ uint32_t tile_excl;
@@ -274,6 +277,7 @@ __global__ void __launch_bounds__(256) k_cells(Dev d)
 // no output depends on it).
 __global__ void __launch_bounds__(256) k_scatter(Dev d)
 {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n) return;
     const uint32_t c = d.ctl->cur;
@@ -284,9 +288,12 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
     const uint8_t st = d.status[c][i];
     const bool ch = d.chg8[i] != 0;
     const int lab = d.labels[i];
-    if (key == kSentinel) return;
-    const uint32_t r = (uint32_t)d.ctab[key].x + rk;
     const bool full = round_full(d);
+    if (key == kSentinel) {   // DONE: counts as changed for the carried edges (k_efilter)
+        d.agflag[i] = 1;
+        return;
+    }
+    const uint32_t r = (uint32_t)d.ctab[key].x + rk;
     const int chg = (full || ch) ? kRecChanged : 0;
     d.rec[r] = make_int4(p.x | (p.y << 16), s, i, st | chg);
     // union-find forest of this round: an agent whose last-round cluster has no changed
@@ -295,6 +302,7 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
     // under the old root (= min id = its label); members of dirty clusters start alone
     const bool dirty = full || lab < 0 || d.dirty[lab] == d.ctl->epoch;
     d.parent[i] = dirty ? (uint32_t)i : (uint32_t)lab;
+    d.agflag[i] = (uint8_t)((chg ? 1 : 0) | (dirty ? 2 : 0));
 }
 
 // test every record of cell `key` against agent A; returns true if A got blocked.
@@ -334,6 +342,7 @@ __device__ __forceinline__ bool scan_cell(const Dev& d, uint32_t key, int ax, in
 //            exceeds R_b(s_A - m) (exact pruning: no agent inside can block A).
 __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
 {
+    pdl_begin();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int nact = d.ctl->n_active;
     const int W = d.ctl->W;
@@ -535,35 +544,40 @@ __device__ __forceinline__ void stripe_prefix(const uint32_t* ctr, int cap, int*
 // state (nothing in a full round).  One atomic per block.
 __global__ void __launch_bounds__(256) k_efilter(Dev d)
 {
-    const uint32_t cur = d.ctl->ecur, c = d.ctl->cur;
+    pdl_begin();
+    const uint32_t cur = d.ctl->ecur;
     const int ne = min((int)d.ctl->ecnt[cur], d.ecap);
     const bool full = round_full(d);
-    __shared__ uint32_t s_cnt, s_base;
-    const int lane = threadIdx.x & 31;
-    for (int base = blockIdx.x * 256; base < ne; base += gridDim.x * 256) {
-        if (threadIdx.x == 0) s_cnt = 0;
-        __syncthreads();
+    __shared__ uint32_t s_w[9];
+    for (int base = blockIdx.x * 256; base < ne; base += gridDim.x * 256) {   // block uniform
         const int k = base + threadIdx.x;
-        bool keep = false;
+        bool keep = false, dirty = false;
         uint2 e = make_uint2(0, 0);
         if (k < ne && !full) {
             e = d.edges[(size_t)cur * d.ecap + k];
-            keep = !agent_changed(d, c, e.x) && !agent_changed(d, c, e.y);
+            // per-endpoint flags of this round (k_scatter): bit 0 changed, bit 1 the
+            // endpoint's last-round cluster is dirty (both endpoints share that cluster)
+            const uint8_t fx = d.agflag[e.x], fy = d.agflag[e.y];
+            keep = !((fx | fy) & 1);
+            dirty = (fx & 2) != 0;
         }
+        // kept edges are appended in order with one atomic per block
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
-        uint32_t wb = 0;
-        if (lane == 0 && m) wb = atomicAdd(&s_cnt, (uint32_t)__popc(m));
-        wb = __shfl_sync(0xFFFFFFFFu, wb, 0);
+        if (lane == 0) s_w[w] = (uint32_t)__popc(m);
         __syncthreads();
-        if (threadIdx.x == 0 && s_cnt) s_base = atomicAdd((uint32_t*)&d.ctl->ecnt[cur ^ 1u], s_cnt);
+        if (threadIdx.x == 0) {
+            uint32_t acc = 0;
+            for (int q = 0; q < 8; q++) { const uint32_t v = s_w[q]; s_w[q] = acc; acc += v; }
+            s_w[8] = acc ? atomicAdd((uint32_t*)&d.ctl->ecnt[cur ^ 1u], acc) : 0u;
+        }
         __syncthreads();
         if (keep) {
-            const uint32_t pos = s_base + wb + __popc(m & ((1u << lane) - 1u));
+            const uint32_t pos = s_w[8] + s_w[w] + (uint32_t)__popc(m & ((1u << lane) - 1u));
             d.edges[(size_t)(cur ^ 1u) * d.ecap + pos] = e;   // kept <= previous count <= ecap
-            // both endpoints were in one cluster last round; if that cluster is dirty its
-            // forest is rebuilt from its edges (a clean cluster's edges are implied by
-            // the members hanging under its root, k_scatter)
-            if (d.dirty[d.labels[e.x]] == d.ctl->epoch) uf_unite(d.parent, e.x, e.y);
+            // a dirty cluster's forest is rebuilt from its edges (a clean cluster's edges
+            // are implied by its members hanging under its root, k_scatter)
+            if (dirty) uf_unite(d.parent, e.x, e.y);
         }
         __syncthreads();
     }
@@ -580,6 +594,7 @@ __global__ void __launch_bounds__(256) k_efilter(Dev d)
 // unblocked and ahead of W go to the far queue.
 __global__ void __launch_bounds__(256, 6) k_near(Dev d)
 {
+    pdl_begin();
     __shared__ EdgeStage s_all[8];
     __shared__ int s_pref[kEdgeStripes + 1];
     __shared__ uint32_t s_w[9];
@@ -720,6 +735,7 @@ __device__ __forceinline__ uint32_t far_block(const Dev& d, uint32_t k1g, int qx
 // If the item list is full the thread tests the block itself.
 __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
 {
+    pdl_begin();
     __shared__ int s_pref[kEdgeStripes + 1];
     stripe_prefix(d.farq_ctr, 1 << 30, s_pref);
     const int nq = s_pref[kEdgeStripes];
@@ -811,6 +827,7 @@ __global__ void __launch_bounds__(256, 2) k_far1(Dev d)
 // and the records of the cells that survive the min-step test.
 __global__ void __launch_bounds__(256) k_far2(Dev d)
 {
+    pdl_begin();
     __shared__ int s_pref[kEdgeStripes + 1];
     stripe_prefix(d.item_ctr, d.item_cap, s_pref);
     const int total = s_pref[kEdgeStripes];
@@ -857,132 +874,21 @@ __global__ void __launch_bounds__(256) k_far2(Dev d)
 // exact test of k_far1/k_far2 (min step m of a block: skip if m >= s_A or its box
 // distance exceeds R_b(s_A - m)); cells within R_c of A were tested by k_near.  The
 // first blocker found becomes A's witness.
-__global__ void __launch_bounds__(256) k_far(Dev d)
-{
-    __shared__ int s_pref[kEdgeStripes + 1];
-    __shared__ uint32_t s_items;
-    if (threadIdx.x == 0) s_items = 0;
-    stripe_prefix(d.farq_ctr, 1 << 30, s_pref);
-    const int nq = s_pref[kEdgeStripes];
-    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_far = nq;
-    const int W = d.ctl->W;
-    const uint32_t c = d.ctl->cur;
-    const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4, hw = threadIdx.x >> 4;
-    const unsigned hm = 0xFFFFu << (16 * h);
-    const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
-    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
-    int ox_l, oy_l;
-    morton_child(l, ox_l, oy_l);
+// Work counters of the half-warp scan (AM_STATS and the far-item count).
+struct HwStats {
     uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
-    for (int q0 = blockIdx.x * 16; q0 < nq; q0 += gridDim.x * 16) {
-        const int q = q0 + hw;
-        if (q >= nq) continue;   // half-warp uniform
-        int lo = 0, hi = kEdgeStripes - 1;          // last queue stripe with s_pref <= q
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
-        }
-        const uint32_t aid = d.farq[(size_t)lo * d.farq_cap + (q - s_pref[lo])];
-        const int2 P = d.pos[c][aid];
-        const int ax = P.x, ay = P.y, as = d.step[c][aid];
-        const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
-        const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
-        const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
-        const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);
-        uint32_t wit = kSentinel;
-        nb2 += l == 0 ? (uint32_t)nb : 0u;
-        for (int j0 = 0; j0 < nb && wit == kSentinel; j0 += 16) {
-            // level 2: 16 blocks of 16x16 cells per step
-            const int j = j0 + l;
-            const int bx = bx0 + j % nbx, by = by0 + j / nbx;
-            bool ok2 = false;
-            if (j < nb) {
-                const int m2 = __ldg(d.lmin2 + morton(bx, by));
-                ok2 = m2 < as && box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
-                                            rb_radius((long long)as - m2, d.v, d.r_p), d.metric);
-            }
-            unsigned mask2 = (__ballot_sync(hm, ok2) >> (16 * h)) & 0xFFFFu;
-            while (mask2 && wit == kSentinel) {
-                const int jj = __ffs(mask2) - 1;
-                mask2 &= mask2 - 1;
-                const int bxj = __shfl_sync(hm, bx, jj, 16), byj = __shfl_sync(hm, by, jj, 16);
-                const uint32_t k2 = morton(bxj, byj);
-                nb1 += l == 0 ? 16u : 0u;
-                // level 1: lane l tests child l (4x4 cells)
-                const int qx = bxj * 4 + ox_l, qy = byj * 4 + oy_l;
-                const int m1 = __ldg(d.lmin1 + k2 * 16 + l);
-                const bool ok1 = m1 < as && box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
-                                                       ((qy + 1) << l1) - 1, rb_radius((long long)as - m1, d.v, d.r_p),
-                                                       d.metric);
-                unsigned mask1 = (__ballot_sync(hm, ok1) >> (16 * h)) & 0xFFFFu;
-                while (mask1 && wit == kSentinel) {
-                    const int ii = __ffs(mask1) - 1;
-                    mask1 &= mask1 - 1;
-                    nitems += l == 0 ? 1u : 0u;
-                    const uint32_t k1g = k2 * 16 + (uint32_t)ii;
-                    const int qxi = __shfl_sync(hm, qx, ii, 16), qyi = __shfl_sync(hm, qy, ii, 16);
-                    // level 0: lane l tests cell l of the 4x4 block
-                    const int2 e = d.ctab[(size_t)k1g * 16 + l];
-                    int nx = __shfl_down_sync(hm, e.x, 1, 16);
-                    if (l == 15) nx = d.ctab[(size_t)k1g * 16 + 16].x;
-                    const int cx = qxi * 4 + ox_l, cy = qyi * 4 + oy_l;
-                    const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
-                    const bool okc = nx > e.x && e.y < as && !box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric) &&
-                                     box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - e.y, d.v, d.r_p),
-                                                d.metric);
-                    const int cnt = okc ? nx - e.x : 0;
-                    ncells += nx > e.x ? 1u : 0u;
-                    // flatten the candidate records over the 16 lanes
-                    int incl = cnt;
-#pragma unroll
-                    for (int o = 1; o < 16; o <<= 1) {
-                        const int y = __shfl_up_sync(hm, incl, o, 16);
-                        if (l >= o) incl += y;
-                    }
-                    const int excl = incl - cnt;
-                    const int total = __shfl_sync(hm, incl, 15, 16);
-                    ncand += l == 0 ? (uint32_t)total : 0u;
-                    for (int b0 = 0; b0 < total && wit == kSentinel; b0 += 16) {
-                        const int tq = b0 + l;
-                        // lane holding candidate tq: the last lane with excl <= tq
-                        int sl = 0;
-#pragma unroll
-                        for (int st = 8; st > 0; st >>= 1) {
-                            const int ex = __shfl_sync(hm, excl, sl + st, 16);
-                            if (ex <= tq) sl += st;
-                        }
-                        const int rs = __shfl_sync(hm, e.x, sl, 16), rx = __shfl_sync(hm, excl, sl, 16);
-                        bool found = false;
-                        uint32_t bid = 0;
-                        if (tq < total) {
-                            const int4 B = d.rec[rs + (tq - rx)];
-                            bid = (uint32_t)B.z;
-                            if (B.y < as) {
-                                const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-                                const uint32_t Rb = min((uint32_t)min(as - B.y, lagcap) * (uint32_t)d.v +
-                                                            (uint32_t)(d.v + d.r_p), kRClamp);
-                                found = within2(dx, dy, Rb * Rb, Rb, d.metric);
-                            }
-                        }
-                        const unsigned fm = (__ballot_sync(hm, found) >> (16 * h)) & 0xFFFFu;
-                        if (fm) wit = __shfl_sync(hm, bid, __ffs(fm) - 1, 16);
-                    }
-                }
-            }
-        }
-        if (l == 0) {
-            d.v8[aid] = wit != kSentinel ? 1 : 0;
-            d.witness[aid] = wit;
-        }
-    }
-    const unsigned it = __reduce_add_sync(0xFFFFFFFFu, nitems);
+};
+
+// per-warp reduction of the half-warp scan counters, one atomic per block for the items
+__device__ __forceinline__ void hw_flush_stats(const Dev& d, const HwStats& hs, int lane, uint32_t& s_items)
+{
+    const unsigned it = __reduce_add_sync(0xFFFFFFFFu, hs.nitems);
     if (lane == 0 && it) atomicAdd(&s_items, it);
     __syncthreads();
     if (threadIdx.x == 0 && s_items) atomicAdd(&d.ctl->n_items, (int)s_items);
     if (d.flags & AM_STATS) {
-        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
-        const unsigned c3 = __reduce_add_sync(0xFFFFFFFFu, nb2), c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
+        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, hs.ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, hs.ncand);
+        const unsigned c3 = __reduce_add_sync(0xFFFFFFFFu, hs.nb2), c4 = __reduce_add_sync(0xFFFFFFFFu, hs.nb1);
         if (lane == 0) {
             atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
             atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
@@ -993,11 +899,278 @@ __global__ void __launch_bounds__(256) k_far(Dev d)
     }
 }
 
+// The far-phase traversal of one agent A = (ax, ay, as) by the 16 lanes of a half-warp
+// (lane l, half h, lane mask hm); returns a blocker's id or kSentinel.  Level by level
+// the 16 lanes test the 16 Morton children of a block; see k_far.
+__device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as, int W, int l, int h, unsigned hm,
+                                           int ox_l, int oy_l, HwStats& hs)
+{
+    const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
+    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+    uint32_t& ncells = hs.ncells;
+    uint32_t& ncand = hs.ncand;
+    uint32_t& nb2 = hs.nb2;
+    uint32_t& nb1 = hs.nb1;
+    uint32_t& nitems = hs.nitems;
+    const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
+    const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
+    const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
+    const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);
+    uint32_t wit = kSentinel;
+    nb2 += l == 0 ? (uint32_t)nb : 0u;
+    for (int j0 = 0; j0 < nb && wit == kSentinel; j0 += 16) {
+        // level 2: 16 blocks of 16x16 cells per step
+        const int j = j0 + l;
+        const int bx = bx0 + j % nbx, by = by0 + j / nbx;
+        bool ok2 = false;
+        if (j < nb) {
+            const int m2 = __ldg(d.lmin2 + morton(bx, by));
+            ok2 = m2 < as && box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
+                                        rb_radius((long long)as - m2, d.v, d.r_p), d.metric);
+        }
+        unsigned mask2 = (__ballot_sync(hm, ok2) >> (16 * h)) & 0xFFFFu;
+        while (mask2 && wit == kSentinel) {
+            const int jj = __ffs(mask2) - 1;
+            mask2 &= mask2 - 1;
+            const int bxj = __shfl_sync(hm, bx, jj, 16), byj = __shfl_sync(hm, by, jj, 16);
+            const uint32_t k2 = morton(bxj, byj);
+            nb1 += l == 0 ? 16u : 0u;
+            // level 1: lane l tests child l (4x4 cells)
+            const int qx = bxj * 4 + ox_l, qy = byj * 4 + oy_l;
+            const int m1 = __ldg(d.lmin1 + k2 * 16 + l);
+            const bool ok1 = m1 < as && box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
+                                                   ((qy + 1) << l1) - 1, rb_radius((long long)as - m1, d.v, d.r_p),
+                                                   d.metric);
+            unsigned mask1 = (__ballot_sync(hm, ok1) >> (16 * h)) & 0xFFFFu;
+            while (mask1 && wit == kSentinel) {
+                const int ii = __ffs(mask1) - 1;
+                mask1 &= mask1 - 1;
+                nitems += l == 0 ? 1u : 0u;
+                const uint32_t k1g = k2 * 16 + (uint32_t)ii;
+                const int qxi = __shfl_sync(hm, qx, ii, 16), qyi = __shfl_sync(hm, qy, ii, 16);
+                // level 0: lane l tests cell l of the 4x4 block
+                const int2 e = d.ctab[(size_t)k1g * 16 + l];
+                int nx = __shfl_down_sync(hm, e.x, 1, 16);
+                if (l == 15) nx = d.ctab[(size_t)k1g * 16 + 16].x;
+                const int cx = qxi * 4 + ox_l, cy = qyi * 4 + oy_l;
+                const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
+                const bool okc = nx > e.x && e.y < as && !box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric) &&
+                                 box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - e.y, d.v, d.r_p),
+                                            d.metric);
+                const int cnt = okc ? nx - e.x : 0;
+                ncells += nx > e.x ? 1u : 0u;
+                // flatten the candidate records over the 16 lanes
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    const int y = __shfl_up_sync(hm, incl, o, 16);
+                    if (l >= o) incl += y;
+                }
+                const int excl = incl - cnt;
+                const int total = __shfl_sync(hm, incl, 15, 16);
+                ncand += l == 0 ? (uint32_t)total : 0u;
+                for (int b0 = 0; b0 < total && wit == kSentinel; b0 += 16) {
+                    const int tq = b0 + l;
+                    // lane holding candidate tq: the last lane with excl <= tq
+                    int sl = 0;
+#pragma unroll
+                    for (int st = 8; st > 0; st >>= 1) {
+                        const int ex = __shfl_sync(hm, excl, sl + st, 16);
+                        if (ex <= tq) sl += st;
+                    }
+                    const int rs = __shfl_sync(hm, e.x, sl, 16), rx = __shfl_sync(hm, excl, sl, 16);
+                    bool found = false;
+                    uint32_t bid = 0;
+                    if (tq < total) {
+                        const int4 B = d.rec[rs + (tq - rx)];
+                        bid = (uint32_t)B.z;
+                        if (B.y < as) {
+                            const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                            const uint32_t Rb = min((uint32_t)min(as - B.y, lagcap) * (uint32_t)d.v +
+                                                        (uint32_t)(d.v + d.r_p), kRClamp);
+                            found = within2(dx, dy, Rb * Rb, Rb, d.metric);
+                        }
+                    }
+                    const unsigned fm = (__ballot_sync(hm, found) >> (16 * h)) & 0xFFFFu;
+                    if (fm) wit = __shfl_sync(hm, bid, __ffs(fm) - 1, 16);
+                }
+            }
+        }
+    }
+    return wit;
+}
+
+__global__ void __launch_bounds__(256) k_far(Dev d)
+{
+    pdl_begin();
+    __shared__ int s_pref[kEdgeStripes + 1];
+    __shared__ uint32_t s_items;
+    if (threadIdx.x == 0) s_items = 0;
+    stripe_prefix(d.farq_ctr, 1 << 30, s_pref);
+    const int nq = s_pref[kEdgeStripes];
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_far = nq;
+    const int W = d.ctl->W;
+    const uint32_t c = d.ctl->cur;
+    const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4, hw = threadIdx.x >> 4;
+    const unsigned hm = 0xFFFFu << (16 * h);
+    int ox_l, oy_l;
+    morton_child(l, ox_l, oy_l);
+    HwStats hs;
+    for (int q0 = blockIdx.x * 16; q0 < nq; q0 += gridDim.x * 16) {
+        const int q = q0 + hw;
+        if (q >= nq) continue;   // half-warp uniform
+        int lo = 0, hi = kEdgeStripes - 1;          // last queue stripe with s_pref <= q
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
+        }
+        const uint32_t aid = d.farq[(size_t)lo * d.farq_cap + (q - s_pref[lo])];
+        const int2 P = d.pos[c][aid];
+        const uint32_t wit = hw_far(d, P.x, P.y, d.step[c][aid], W, l, h, hm, ox_l, oy_l, hs);
+        if (l == 0) {
+            d.v8[aid] = wit != kSentinel ? 1 : 0;
+            d.witness[aid] = wit;
+        }
+    }
+    hw_flush_stats(d, hs, lane, s_items);
+}
+
+// k_scan_hw: the whole incremental scan with one HALF-WARP per queued agent A (work
+// queue of k_bin: id, bit 31 = changed).  Near phase: the cells within box distance R_c
+// of A (<= 2x2 when cell >= R_c), one lane per cell, their records flattened over the 16
+// lanes: coupling edges for a changed A (once per pair: from the smaller
+// id when both changed) and, for an IDLE A, the blocking test with the
+// blocker kept as witness.  An IDLE A still unblocked and ahead of W continues with the
+// far phase (hw_far) in the same half-warp -- no far queue, no second launch.
+__global__ void __launch_bounds__(256) k_scan_hw(Dev d)
+{
+    pdl_begin();
+    __shared__ EdgeStage s_all[8];
+    __shared__ int s_pref[kEdgeStripes + 1];
+    __shared__ uint32_t s_items;
+    const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4, hw = threadIdx.x >> 4;
+    const unsigned hm = 0xFFFFu << (16 * h);
+    EdgeStage& sm = s_all[threadIdx.x >> 5];
+    if (lane == 0) sm.ne = 0;
+    if (threadIdx.x == 0) s_items = 0;
+    stripe_prefix(d.wq_ctr, 1 << 30, s_pref);
+    const int nq = s_pref[kEdgeStripes];
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_work = nq;
+    const uint32_t c = d.ctl->cur;
+    const int W = d.ctl->W;
+    const int cl = d.clog, G = 1 << d.glog;
+    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const uint32_t Rc2 = Rc * Rc;
+    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+    int ox_l, oy_l;
+    morton_child(l, ox_l, oy_l);
+    HwStats hs;
+    uint32_t nfar = 0;
+    for (int q0 = blockIdx.x * 16; q0 < nq; q0 += gridDim.x * 16) {   // block uniform
+        const int q = q0 + hw;
+        if (q < nq) {                                                  // half-warp uniform
+            int lo = 0, hi = kEdgeStripes - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t wv = d.wq[(size_t)lo * d.wq_cap + (q - s_pref[lo])];
+            const uint32_t aid = wv & 0x7FFFFFFFu;
+            const bool chg = (wv >> 31) != 0;
+            const int2 P = d.pos[c][aid];
+            const int ax = P.x, ay = P.y, as = d.step[c][aid];
+            const bool idle = d.status[c][aid] == ST_IDLE;
+            // ---- near phase
+            const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
+            const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
+            const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
+            bool nblk = false;
+            uint32_t wit = kSentinel;
+            for (int c0 = 0; c0 < ncell; c0 += 16) {
+                const int k = c0 + l;
+                int st0 = 0, cnt = 0;
+                if (k < ncell) {
+                    const int cx = cx0 + k % ncx, cy = cy0 + k / ncx;
+                    if (box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rc,
+                                   d.metric)) {
+                        const uint32_t key = morton(cx, cy);
+                        const int2 e = d.ctab[key];
+                        const int e1 = d.ctab[key + 1].x;
+                        if (e.y <= as) { st0 = e.x; cnt = e1 - e.x; }
+                    }
+                }
+                hs.ncells += cnt > 0 ? 1u : 0u;
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    const int y = __shfl_up_sync(hm, incl, o, 16);
+                    if (l >= o) incl += y;
+                }
+                const int excl = incl - cnt;
+                const int total = __shfl_sync(hm, incl, 15, 16);
+                hs.ncand += l == 0 ? (uint32_t)total : 0u;
+                for (int b0 = 0; b0 < total; b0 += 16) {
+                    if (!chg && (nblk || !idle)) break;   // nothing left to decide (uniform)
+                    const int tq = b0 + l;
+                    int sl = 0;
+#pragma unroll
+                    for (int stp = 8; stp > 0; stp >>= 1) {
+                        const int ex = __shfl_sync(hm, excl, sl + stp, 16);
+                        if (ex <= tq) sl += stp;
+                    }
+                    const int rs = __shfl_sync(hm, st0, sl, 16), rx = __shfl_sync(hm, excl, sl, 16);
+                    bool found = false;
+                    uint32_t bid = 0;
+                    if (tq < total) {
+                        const int4 B = d.rec[rs + (tq - rx)];
+                        bid = (uint32_t)B.z;
+                        if (bid != aid) {
+                            const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                            if (B.y == as) {
+                                // B's record carries its changed bit (k_scatter)
+                                if (chg && within2(dx, dy, Rc2, Rc, d.metric) && (!(B.w & kRecChanged) || aid < bid))
+                                    stage_edge(d, sm, min(aid, bid), max(aid, bid));
+                            } else if (idle && !nblk && B.y < as) {
+                                const uint32_t R = min((uint32_t)min(as - B.y, lagcap) * (uint32_t)d.v +
+                                                           (uint32_t)(d.v + d.r_p), kRClamp);
+                                found = within2(dx, dy, R * R, R, d.metric);
+                            }
+                        }
+                    }
+                    const unsigned fm = (__ballot_sync(hm, found) >> (16 * h)) & 0xFFFFu;
+                    if (fm && !nblk) {
+                        nblk = true;
+                        wit = __shfl_sync(hm, bid, __ffs(fm) - 1, 16);
+                    }
+                }
+            }
+            // ---- far phase (IDLE, not blocked nearby, ahead of the watermark)
+            if (idle) {
+                if (!nblk && as > W && !(d.flags & AM_DBG_SKIP_FAR)) {
+                    nfar += l == 0 ? 1u : 0u;
+                    wit = hw_far(d, ax, ay, as, W, l, h, hm, ox_l, oy_l, hs);
+                    nblk = wit != kSentinel;
+                }
+                if (l == 0) {
+                    d.v8[aid] = nblk ? 1 : 0;
+                    d.witness[aid] = nblk ? wit : kSentinel;
+                }
+            }
+        }
+        flush_stage(d, sm, lane);   // warp collective: both half-warps
+    }
+    const unsigned nf = __reduce_add_sync(0xFFFFFFFFu, nfar);
+    if (lane == 0 && nf) atomicAdd((unsigned*)&d.ctl->n_far, nf);
+    hw_flush_stats(d, hs, lane, s_items);
+}
+
 // k_union: unite this round's coupling edges (carried-over + new), one thread per edge
 // (ECL-CC style hooking of the larger root under the smaller, so roots stay the
 // minimum id); the last block makes the list current for the next round.
 __global__ void __launch_bounds__(256) k_union(Dev d)
 {
+    pdl_begin();
     const uint32_t nxt = d.ctl->ecur ^ 1u;
     const int ne = min((int)d.ctl->ecnt[nxt], d.ecap);
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_edges = ne;
@@ -1018,6 +1191,7 @@ __global__ void __launch_bounds__(256) k_union(Dev d)
 // whose parent is not themselves chase pointers (singletons are one load).
 __global__ void __launch_bounds__(256) k_finalize(Dev d)
 {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n) return;
     const uint8_t st = d.status[d.ctl->cur][i];
@@ -1036,6 +1210,7 @@ __device__ void digest_one(const Dev& d, uint32_t aid);
 // agents within r_p of mix64(id<<32 ^ (u16)dx<<16 ^ (u16)dy).
 __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict__ order)
 {
+    pdl_begin();
     const int nr = d.ctl->n_ready;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x)
         digest_one(d, (uint32_t)order[k]);
@@ -1073,6 +1248,7 @@ __device__ void digest_one(const Dev& d, uint32_t aid)
 // 256 threads x 8 consecutive agents per tile; chained scan keeps id order.
 __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask)
 {
+    pdl_begin();
     Ctl* ctl = d.ctl;
     __shared__ uint32_t wsum[8];
     __shared__ uint32_t tile_excl;
@@ -1153,6 +1329,7 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
                 ((unsigned long long)(uint32_t)(d.step[c][i] - W) << d.idbits) | (uint32_t)lab[k];
             d.rkey[0][pos] = key;
             d.rval[0][pos] = (uint32_t)i;
+            d.rid[pos] = i;
             kor |= key;
             pos++;
         }
@@ -1198,6 +1375,7 @@ __device__ __forceinline__ unsigned warp_match_digit(int dg, bool valid)
 // (persistent grid-stride); the last block turns them into exclusive digit offsets.
 __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
 {
+    pdl_begin();
     Ctl* ctl = d.ctl;
     __shared__ uint32_t h[kMaxSortPasses][kRadix];
     const int n = ctl->n_ready;
@@ -1259,6 +1437,7 @@ __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
 // Dynamic shared memory: wcnt[32][kRadix] + goff[kRadix].
 __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __restrict__ order, int ntiles)
 {
+    pdl_begin();
     Ctl* ctl = d.ctl;
     extern __shared__ uint32_t sort_smem[];
     uint32_t (*wcnt)[kRadix] = reinterpret_cast<uint32_t (*)[kRadix]>(sort_smem);
@@ -1365,6 +1544,7 @@ __device__ __forceinline__ void suf_unite(uint32_t* parent, uint32_t a, uint32_t
 __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mask,
                                                  int32_t* __restrict__ order)
 {
+    pdl_begin();
     Ctl* ctl = d.ctl;
     __shared__ int sx[kSmallMax], sy[kSmallMax], ss[kSmallMax];
     __shared__ uint8_t sst[kSmallMax], sbad[kSmallMax], srdy[kSmallMax];
@@ -1453,11 +1633,13 @@ __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mas
 // reset the per-round counters that the host reads (before the round kernels)
 __global__ void k_round_begin(Dev d)
 {
+    pdl_begin();
     Ctl* ctl = d.ctl;
     ctl->epoch += 1;
     ctl->n_ready = 0;
     ctl->n_clusters = 0;
     ctl->n_items = 0;
+    ctl->n_far = 0;
     ctl->full |= ctl->full_next;
     ctl->full_next = 0;
     ctl->ecnt[ctl->ecur ^ 1u] = 0;

@@ -7,22 +7,21 @@
 // passes are separated by cluster barriers instead of kernel launches, and the per-CTA
 // digit histograms are exchanged through distributed shared memory (DSMEM).
 //
-// CTA r owns the contiguous chunk [r*chunk, (r+1)*chunk) of the sequence.  A pass:
-//   (1) digit histogram of the chunk (warp-aggregated shared-memory atomics);
+// CTA r owns the contiguous chunk [r*chunk, (r+1)*chunk) of the sequence.  A pass over
+// one 8-bit digit:
+//   (1) digit histogram of the chunk (shared-memory atomics: counts need no order);
 //   (2) cluster barrier; every CTA reads the C histograms over DSMEM -> for each digit
 //       the global start of this CTA's run (digit start + the CTAs before it);
-//   (3) stable ranking of a tile (per-warp digit counters, each warp owns a consecutive
-//       index range, ballot-based peer matching) into a LOCAL staging buffer sorted by
-//       digit -- random stores stay in the CTA's own shared memory;
-//   (4) copy-out: consecutive staged elements of one digit go to consecutive
-//       destinations, so the scatter to the owning CTA's buffer (DSMEM) or to global
-//       memory is coalesced;
-//   (5) cluster barrier.
+//   (3) per tile of the chunk: a stable local sort by the digit in shared memory, as
+//       two stable 4-bit rank-and-scatter steps.  Ranking uses per-thread counters
+//       (thread t owns K consecutive elements and a private column of 16 counters; one
+//       block-wide scan over the 16 x 1024 counters in (digit, thread) order gives every
+//       element its rank) -- no atomics, no warp matching;
+//   (4) copy-out: consecutive sorted elements of one digit go to consecutive global
+//       destinations (coalesced; the ping-pong buffers stay L2-resident);
+//   (5) global fence + cluster barrier.
 // Elements are (key, id) pairs, packed in 8 bytes when the keys have <= 32 significant
-// bits (C5: 7 lag bits + 20 id bits), else 16 bytes.  When the ready set fits in the
-// cluster's shared memory the pairs stay resident between passes (touching global
-// memory once in and once out); larger sets (e.g. the first replay rounds, every agent
-// at step 0) stream through the global rkey/rval buffers with the same passes.
+// bits (C5: 7 lag bits + 20 id bits), else 16 bytes.
 #include <cooperative_groups.h>
 
 #include "am_internal.cuh"
@@ -31,12 +30,28 @@ namespace cg = cooperative_groups;
 
 namespace am {
 
-constexpr int kCsBits = 8;
+#ifdef CS_TIMING   // tools/micro/csort_bench.cu: globaltimer stamps of CTA 0
+__device__ unsigned long long g_cs_t[128];
+__device__ __forceinline__ unsigned long long cs_now()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define CS_STAMP(k) \
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_cs_t[(k)] = cs_now();
+#else
+#define CS_STAMP(k)
+#endif
+
+constexpr int kCsBits = 8;                   // digit of one global pass
 constexpr int kCsRadix = 1 << kCsBits;
+constexpr int kCsSub = 4;                    // bits of one local rank step
+constexpr int kCsSubR = 1 << kCsSub;
 constexpr int kCsThreads = 1024;
-constexpr int kCsItems = 8;                               // per lane per ranking tile (8-byte pairs)
-// fixed shared memory: wcnt[32][R] + hist, base, run, tstart, ttot [R] + scan[32]
-constexpr size_t kCsFixed = (size_t)(32 * kCsRadix + 5 * kCsRadix + 32) * 4;
+constexpr int kCsK = 8;                      // max elements per thread per tile
+// fixed shared memory: cnt[16][1024] (padded) + hist, base, run, tstart, ttot [256] + wsum[32]
+constexpr size_t kCsFixed = (size_t)(kCsSubR * kCsThreads * 33 / 32 + 5 * kCsRadix + 32) * 4;
 
 struct E32 {
     uint32_t k, v;
@@ -50,187 +65,227 @@ __device__ __forceinline__ unsigned long long ekey(const E64& e) { return e.k; }
 __device__ __forceinline__ void eset(E32& e, unsigned long long k, uint32_t v) { e.k = (uint32_t)k; e.v = v; }
 __device__ __forceinline__ void eset(E64& e, unsigned long long k, uint32_t v) { e.k = k; e.v = v; e.pad = 0; }
 
-// lanes of the warp holding the same digit (and validity), from kCsBits + 1 ballots
-__device__ __forceinline__ unsigned cs_match(int dg, bool valid)
+// the ping-pong buffers of the intermediate passes: packed pairs in rkey[b] (E32), or
+// keys in rkey[b] and ids in rval[b] (E64)
+__device__ __forceinline__ void gload(const Dev& d, int b, int i, E32& e)
 {
-    const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
-    unsigned peers = valid ? vm : ~vm;
-#pragma unroll
-    for (int b = 0; b < kCsBits; b++) {
-        const bool bit = (dg >> b) & 1;
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, bit);
-        peers &= bit ? m : ~m;
-    }
-    return peers;
+    e = reinterpret_cast<const E32*>(d.rkey[b])[i];
+}
+__device__ __forceinline__ void gload(const Dev& d, int b, int i, E64& e)
+{
+    eset(e, d.rkey[b][i], d.rval[b][i]);
+}
+__device__ __forceinline__ void gstore(const Dev& d, int b, int i, const E32& e)
+{
+    reinterpret_cast<E32*>(d.rkey[b])[i] = e;
+}
+__device__ __forceinline__ void gstore(const Dev& d, int b, int i, const E64& e)
+{
+    d.rkey[b][i] = e.k;
+    d.rval[b][i] = e.v;
 }
 
 size_t csort_smem_fixed() { return kCsFixed; }
 
-// exclusive scan of v over the kCsRadix digits held by threads 0..kCsRadix-1 (all
-// threads of the block call it); returns the exclusive prefix in those threads
-__device__ __forceinline__ uint32_t digit_scan(uint32_t v, uint32_t* scan)
+// block-wide exclusive scan (1024 threads); wsum: 32 words of shared memory
+__device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* wsum)
 {
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (lane >= o) incl += y;
     }
-    if (t < kCsRadix && lane == 31) scan[w] = incl;
+    if (lane == 31) wsum[w] = incl;
     __syncthreads();
-    uint32_t off = 0;
-    if (t < kCsRadix)
-        for (int q = 0; q < w; q++) off += scan[q];
+    if (w == 0) {
+        const uint32_t x = wsum[lane];
+        uint32_t s = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
+            if (lane >= o) s += y;
+        }
+        wsum[lane] = s - x;
+    }
     __syncthreads();
-    return off + incl - v;
+    const uint32_t r = wsum[w] + incl - v;
+    __syncthreads();
+    return r;
 }
 
-template <class E>
-__device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned char* smem, size_t smem_bytes,
-                          int n, int np)
+// Stable local sort step: the tile's elements src[0..tm) by the sub-digit
+// (key >> shift) & 15 into dst.  Thread t owns elements [t*K, t*K+K) and counter column
+// t of a [16][1024] counter array, stored with one pad word per 32 (cpad) so that both
+// the per-thread column updates and the scan (thread u owns the 16 consecutive counters
+// [16u, 16u+16) of the (digit, thread) order) are bank-conflict free.
+__device__ __forceinline__ int cpad(int i) { return i + (i >> 5); }
+
+template <class E, int K>
+__device__ __forceinline__ void rank_step(const E* src, E* dst, int tm, int shift, uint32_t* cnt,
+                                          uint32_t* wsum)
+{
+    const int t = threadIdx.x;
+    uint32_t lp[K];   // rank among this thread's earlier elements of the same sub-digit
+#pragma unroll
+    for (int q = 0; q < kCsSubR; q++) cnt[cpad(q * kCsThreads + t)] = 0;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int i = t * K + k;
+        lp[k] = 0;
+        if (i < tm) {
+            const int sd = (int)((ekey(src[i]) >> shift) & (kCsSubR - 1));
+            uint32_t* c = cnt + cpad(sd * kCsThreads + t);
+            lp[k] = *c;
+            *c = lp[k] + 1;
+        }
+    }
+    __syncthreads();
+    // exclusive scan of the counters in (digit, thread) order: serial over the thread's
+    // 16, block-wide over the 1024 per-thread sums
+    uint32_t v[16], acc = 0;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        v[j] = cnt[cpad(16 * t + j)];
+        const uint32_t x = v[j];
+        v[j] = acc;
+        acc += x;
+    }
+    const uint32_t off = block_scan(acc, wsum);
+#pragma unroll
+    for (int j = 0; j < 16; j++) cnt[cpad(16 * t + j)] = off + v[j];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const int i = t * K + k;
+        if (i < tm) {
+            const E e = src[i];
+            dst[cnt[cpad((int)((ekey(e) >> shift) & (kCsSubR - 1)) * kCsThreads + t)] + lp[k]] = e;
+        }
+    }
+    __syncthreads();
+}
+
+template <class E, int K>
+__device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned char* smem, int n, int np)
 {
     cg::cluster_group cl = cg::this_cluster();
     const int C = (int)cl.num_blocks();
     const int me = (int)cl.block_rank();
-    uint32_t (*wcnt)[kCsRadix] = reinterpret_cast<uint32_t (*)[kCsRadix]>(smem);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem) + 32 * kCsRadix;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* hist = cnt + kCsSubR * kCsThreads * 33 / 32;
     uint32_t* base = hist + kCsRadix;     // global start of this CTA's run of each digit
     uint32_t* run = base + kCsRadix;      // elements of each digit in earlier tiles
-    uint32_t* tstart = run + kCsRadix;    // start of each digit in the staged tile
+    uint32_t* tstart = run + kCsRadix;    // start of each digit in the sorted tile
     uint32_t* ttot = tstart + kCsRadix;   // elements of each digit in the tile
-    uint32_t* scan = ttot + kCsRadix;
-    const int cap = (int)((smem_bytes - kCsFixed) / (3 * sizeof(E)));
-    E* const buf0 = reinterpret_cast<E*>(smem + kCsFixed);   // ping-pong buffers 0 and 1
-    E* const stage = buf0 + 2 * cap;
+    uint32_t* wsum = ttot + kCsRadix;
+    constexpr int tile = kCsThreads * K;
+    E* const sa = reinterpret_cast<E*>(smem + kCsFixed);
+    E* const sb = sa + tile;
 
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const unsigned lt = (1u << lane) - 1u;
+    const int t = threadIdx.x;
     const int chunk = (n + C - 1) / C;
     const int lo = min(n, me * chunk), m = min(n, lo + chunk) - lo;
-    const bool resident = chunk <= cap;
-    constexpr int kItems = sizeof(E) == 8 ? kCsItems : kCsItems / 2;   // register budget
-    const int tile = min(cap, kCsThreads * kItems);
 
     for (int p = 0; p < np; p++) {
+        CS_STAMP(1 + 8 * p);
         const int shift = kCsBits * p;
         const bool last = p == np - 1;
-        // source of this pass: the global compaction (pass 0 or streaming), or this CTA's
-        // resident buffer
-        const bool gsrc = p == 0 || !resident;
-        const unsigned long long* gk = d.rkey[p & 1] + lo;
-        const uint32_t* gv = d.rval[p & 1] + lo;
-        const E* ssrc = buf0 + (p & 1) * cap;
+        // pass 0 reads the compaction (rkey[0] keys, rval[0] ids); pass p >= 1 reads
+        // ping-pong buffer p & 1 and writes buffer (p + 1) & 1
         auto load = [&](int i) {
             E e;
-            if (gsrc) eset(e, gk[i], gv[i]); else e = ssrc[i];
+            if (p == 0) eset(e, d.rkey[0][lo + i], d.rval[0][lo + i]);
+            else gload(d, p & 1, lo + i, e);
             return e;
         };
         // ---- (1) histogram of this CTA's chunk
         for (int k = t; k < kCsRadix; k += kCsThreads) { hist[k] = 0; run[k] = 0; }
         __syncthreads();
-        for (int k0 = 0; k0 < m; k0 += kCsThreads) {
-            const int k = k0 + t;
-            const bool valid = k < m;
-            const int dg = valid ? (int)((ekey(load(k)) >> shift) & (kCsRadix - 1)) : 0;
-            const unsigned peers = cs_match(dg, valid);
-            if (valid && (peers & lt) == 0) atomicAdd(&hist[dg], (uint32_t)__popc(peers));
-        }
+        for (int k = t; k < m; k += kCsThreads)
+            atomicAdd(&hist[(int)((ekey(load(k)) >> shift) & (kCsRadix - 1))], 1u);
         // ---- (2) histograms over DSMEM -> base[digit]
+        CS_STAMP(2 + 8 * p);
         cl.sync();
+        CS_STAMP(3 + 8 * p);
         {
             uint32_t tot = 0, before = 0;
             if (t < kCsRadix) {
-                uint32_t v[16];
-#pragma unroll
-                for (int r = 0; r < 16; r++) v[r] = r < C ? *cl.map_shared_rank(hist + t, r) : 0u;
-#pragma unroll
-                for (int r = 0; r < 16; r++) {
-                    tot += v[r];
-                    before += r < me ? v[r] : 0u;
+                for (int r = 0; r < C; r++) {
+                    const uint32_t x = *cl.map_shared_rank(hist + t, r);
+                    tot += x;
+                    before += r < me ? x : 0u;
                 }
             }
-            const uint32_t ex = digit_scan(tot, scan);
+            const uint32_t ex = block_scan(tot, wsum);
             if (t < kCsRadix) base[t] = ex + before;
         }
-        // ---- (3) + (4) tiles: stable ranking into the staging buffer, coalesced copy-out
+        CS_STAMP(4 + 8 * p);
+        // ---- (3) + (4) tiles: stable local sort, coalesced copy-out
         for (int tb = 0; tb < m; tb += tile) {
             const int tm = min(tile, m - tb);
-            for (int k = t; k < 32 * kCsRadix; k += kCsThreads) (&wcnt[0][0])[k] = 0;
+            if (t < kCsRadix) ttot[t] = 0;
             __syncthreads();
-            E el[kItems];
-            uint32_t rnk[kItems];
-            int dig[kItems];
-#pragma unroll
-            for (int k = 0; k < kItems; k++) {
-                const int i = w * (32 * kItems) + k * 32 + lane;
-                const bool valid = i < tm;
-                if (valid) el[k] = load(tb + i); else eset(el[k], 0ull, 0u);
-                dig[k] = valid ? (int)((ekey(el[k]) >> shift) & (kCsRadix - 1)) : kCsRadix;
-                const unsigned peers = cs_match(dig[k] & (kCsRadix - 1), valid);
-                const uint32_t b0 = valid ? wcnt[w][dig[k]] : 0u;
-                rnk[k] = b0 + __popc(peers & lt);
-                __syncwarp();
-                if (valid && (peers & lt) == 0) wcnt[w][dig[k]] = b0 + __popc(peers);
-                __syncwarp();
+            for (int k = t; k < tm; k += kCsThreads) {
+                const E e = load(tb + k);
+                sa[k] = e;
+                atomicAdd(&ttot[(int)((ekey(e) >> shift) & (kCsRadix - 1))], 1u);
             }
             __syncthreads();
-            // per digit: exclusive prefix over the warps -> tile totals -> tile starts
-            uint32_t acc = 0;
-            if (t < kCsRadix) {
-#pragma unroll 8
-                for (int q = 0; q < 32; q++) { const uint32_t v = wcnt[q][t]; wcnt[q][t] = acc; acc += v; }
-                ttot[t] = acc;
+            rank_step<E, K>(sa, sb, tm, shift, cnt, wsum);
+            rank_step<E, K>(sb, sa, tm, shift + kCsSub, cnt, wsum);
+            CS_STAMP(5 + 8 * p);
+            {
+                const uint32_t ts = block_scan(t < kCsRadix ? ttot[t] : 0u, wsum);
+                if (t < kCsRadix) tstart[t] = ts;
             }
-            const uint32_t ts = digit_scan(acc, scan);
-            if (t < kCsRadix) tstart[t] = ts;
             __syncthreads();
-#pragma unroll
-            for (int k = 0; k < kItems; k++)
-                if (dig[k] < kCsRadix) stage[tstart[dig[k]] + wcnt[w][dig[k]] + rnk[k]] = el[k];
-            __syncthreads();
-            // copy-out in staged order: destination = run start of the digit + offset
             for (int j = t; j < tm; j += kCsThreads) {
-                const E e = stage[j];
+                const E e = sa[j];
                 const int dg = (int)((ekey(e) >> shift) & (kCsRadix - 1));
                 const uint32_t dst = base[dg] + run[dg] + (uint32_t)j - tstart[dg];
-                if (last) {
-                    order[dst] = (int32_t)e.v;
-                } else if (resident) {
-                    const int r = (int)(dst / (uint32_t)chunk);
-                    *cl.map_shared_rank(buf0 + ((p + 1) & 1) * cap + (dst - (uint32_t)r * chunk), r) = e;
-                } else {
-                    d.rkey[(p + 1) & 1][dst] = ekey(e);
-                    d.rval[(p + 1) & 1][dst] = e.v;
-                }
+                if (last) order[dst] = (int32_t)e.v;
+                else gstore(d, (p + 1) & 1, (int)dst, e);
             }
             __syncthreads();
             if (t < kCsRadix) run[t] += ttot[t];
             __syncthreads();
         }
         // ---- (5) every element of this pass has landed before the next pass reads it
-        if (!resident) __threadfence();
+        CS_STAMP(6 + 8 * p);
+        __threadfence();
         cl.sync();
+        CS_STAMP(7 + 8 * p);
     }
 }
 
 __global__ void __launch_bounds__(kCsThreads, 1) k_csort(Dev d, int32_t* __restrict__ order, int smem_bytes)
 {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char cs_smem[];
+    (void)smem_bytes;
+    CS_STAMP(0);
     const int n = d.ctl->n_ready;
     const int bits = d.ctl->sort_bits;
     const int np = (bits + kCsBits - 1) / kCsBits;
+    const int C = (int)cg::this_cluster().num_blocks();
     if (n == 0) return;
     if (np == 0) {   // every key equal: the compaction order (id) is the order
-        cg::cluster_group cl = cg::this_cluster();
-        const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
+        const int me = (int)cg::this_cluster().block_rank();
         for (int k = me * kCsThreads + threadIdx.x; k < n; k += C * kCsThreads) order[k] = (int32_t)d.rval[0][k];
         return;
     }
-    if (bits <= 32)
-        csort_run<E32>(d, order, cs_smem, (size_t)smem_bytes, n, np);
-    else
-        csort_run<E64>(d, order, cs_smem, (size_t)smem_bytes, n, np);
+    // elements per thread per tile: as few as the chunk needs (shorter serial work)
+    const int chunk = (n + C - 1) / C;
+    if (bits <= 32) {
+        if (chunk <= 2 * kCsThreads) csort_run<E32, 2>(d, order, cs_smem, n, np);
+        else if (chunk <= 4 * kCsThreads) csort_run<E32, 4>(d, order, cs_smem, n, np);
+        else csort_run<E32, kCsK>(d, order, cs_smem, n, np);
+    } else {
+        if (chunk <= 2 * kCsThreads) csort_run<E64, 2>(d, order, cs_smem, n, np);
+        else csort_run<E64, 4>(d, order, cs_smem, n, np);
+    }
 }
 
 }  // namespace am

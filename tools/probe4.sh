@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+./tools/micro/csort_bench
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+python tools/kernel_times.py --label hw
+python tools/sort_probe.py
