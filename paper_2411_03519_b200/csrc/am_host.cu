@@ -17,10 +17,6 @@ __global__ void k_scan(Dev d);
 __global__ void k_scan_thread(Dev d);
 __global__ void k_finalize(Dev d);
 __global__ void k_union(Dev d);
-__global__ void k_near(Dev d);
-__global__ void k_far1(Dev d);
-__global__ void k_far2(Dev d);
-__global__ void k_far(Dev d);
 __global__ void k_scan_hw(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
@@ -164,7 +160,7 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 2 : 10 + (c->scan_split ? (c->far_items ? 3 : 2) : 1) + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
+    return c->path == 0 ? 2 : 11 + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -212,8 +208,6 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     x->stream = (cudaStream_t)c.stream;
     cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
     if (const char* e = getenv("AM_SORT_CTAS")) x->sort_ctas = std::max(1, atoi(e));   // tuning knob
-    if (const char* e = getenv("AM_FAR")) x->far_items = !strcmp(e, "items");          // ablation
-    if (const char* e = getenv("AM_SCAN")) x->scan_split = !strcmp(e, "split");        // ablation
     if (const char* e = getenv("AM_PDL")) x->pdl = atoi(e) != 0;                      // ablation
     // the one-kernel cluster sort: the largest cluster (16, else 8) that can be resident
     {
@@ -321,7 +315,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
     size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
-           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_farq = 0, o_items = 0, o_ictr = 0, o_fctr = 0, o_wq = 0, o_dirty = 0, o_agf = 0, o_rid = 0;
+           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_wq = 0, o_dirty = 0, o_agf = 0, o_rid = 0;
     const size_t NC = (size_t)d.ncells;
     if (x->path == 1) {
         o_key = take(4 * N); o_rank = take(4 * N);
@@ -334,26 +328,22 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * kRadix);
         o_gh = take(4 * kMaxSortPasses * kRadix); o_gs = take(4 * kMaxSortPasses * kRadix);
         d.ecap = (int)(3 * N + 4096);
-        // striped queues, stripe = block index mod 64: k_bin has one thread per agent;
-        // k_near is a grid-stride loop over <= n queued agents on min(blocks, 8 x SMs) blocks
-        const long long nbl = blocks(n, 256), gnear = std::min<long long>(nbl, 8LL * x->num_sms);
+        // the scan's work queue: stripes = block index mod 64 of k_scatter (one thread per
+        // agent), so a stripe holds at most ceil(blocks / 64) x 256 records
+        const long long nbl = blocks(n, 256);
         d.wq_cap = (int)(((nbl + kEdgeStripes - 1) / kEdgeStripes) * 256);
         o_wit = take(4 * N); o_lrs = take(N);
-        // a stripe receives the records of the blocks b with b % 64 == stripe
-        d.farq_cap = (int)(((gnear + kEdgeStripes - 1) / kEdgeStripes) * ((n + gnear * 256 - 1) / (gnear * 256)) * 256);
-        o_farq = take(4 * (size_t)kEdgeStripes * d.farq_cap); o_fctr = take(4 * kEdgeStripes);
-        d.item_cap = (int)std::max<size_t>(1024, (4 * N + kEdgeStripes - 1) / kEdgeStripes);
-        o_items = take(8 * (size_t)kEdgeStripes * d.item_cap); o_ictr = take(4 * kEdgeStripes);
-        o_edges = take(8 * 2 * (size_t)d.ecap); o_ectr = take(4 * kEdgeStripes);
-        o_wq = take(4 * (size_t)kEdgeStripes * d.wq_cap);
+        o_edges = take(8 * 4 * (size_t)d.ecap); o_ectr = take(4 * kEdgeStripes);
+        o_wq = take(16 * (size_t)kEdgeStripes * d.wq_cap);
     }
     x->ws_bytes = off;
     cudaError_t e = cudaMalloc(&x->ws, off);
     if (e != cudaSuccess) { delete x; return cuda_err(nullptr, e, "am_init: cudaMalloc"); }
-    if (x->path == 1 && x->csort_ctas) {
+    if (x->path == 1) {
         e = cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_efil, cudaEventDisableTiming);
         if (e != cudaSuccess) { cudaFree(x->ws); delete x; return cuda_err(nullptr, e, "am_init: side stream"); }
     }
     e = cudaMallocHost((void**)&x->h_ctl, sizeof(Ctl));
@@ -378,9 +368,8 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.tiles_c = (unsigned long long*)(b + o_tc); d.tiles_r = (unsigned long long*)(b + o_tr);
         d.tiles_sort = (unsigned long long*)(b + o_tsort);
         d.ghist = (uint32_t*)(b + o_gh); d.gstart = (uint32_t*)(b + o_gs);
-        d.edges = (uint2*)(b + o_edges); d.wq_ctr = (uint32_t*)(b + o_ectr); d.wq = (uint32_t*)(b + o_wq);
-        d.witness = (uint32_t*)(b + o_wit); d.chg8 = (uint8_t*)(b + o_lrs); d.farq = (uint32_t*)(b + o_farq); d.farq_ctr = (uint32_t*)(b + o_fctr);
-        d.items = (uint2*)(b + o_items); d.item_ctr = (uint32_t*)(b + o_ictr);
+        d.cedges = (uint2*)(b + o_edges); d.nedges = d.cedges + 2 * (size_t)d.ecap; d.wq_ctr = (uint32_t*)(b + o_ectr); d.wq = (int4*)(b + o_wq);
+        d.witness = (uint32_t*)(b + o_wit); d.chg8 = (uint8_t*)(b + o_lrs);
     }
     // initial contents: everything zero except the min-step table
     e = cudaMemsetAsync(x->ws, 0, off, x->stream);
@@ -521,25 +510,19 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         {
             const unsigned pers = (unsigned)c->num_sms * 8;   // persistent grid-stride kernels
             // coupling edges of unchanged pairs carried over; scan of the work queue
-            if (c->scan_split) {
-                // ablation: k_near (thread per agent) + far queue + far kernel(s)
-                am_prof_begin(c, K_NEAR);
-                CK(c, launch_k(c->pdl, s, k_efilter, std::min(blocks(d.ecap, 256), pers), 256, 0, d));
-                CK(c, launch_k(c->pdl, s, k_near, std::min(nb, pers), 256, 0, d));
-                am_prof_end(c, K_NEAR);
-                am_prof_begin(c, K_SCAN);
-                if (c->far_items) {   // per-agent pyramid pass + per-(agent, 4x4 block) items
-                    CK(c, launch_k(c->pdl, s, k_far1, std::min(nb, pers), 256, 0, d));
-                    CK(c, launch_k(c->pdl, s, k_far2, std::min(nb, pers), 256, 0, d));
-                } else {              // one half-warp per far-queued agent
-                    CK(c, launch_k(c->pdl, s, k_far, std::min(nb, pers), 256, 0, d));
-                }
-                am_prof_end(c, K_SCAN);
-            } else {
-                LAUNCH(K_NEAR, CK(c, launch_k(c->pdl, s, k_efilter, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
-                // one half-warp per queued agent: near phase, then far phase
-                LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw, std::min(blocks(d.n, 16), pers), 256, 0, d)));
+            // the carried edges (k_efilter, side stream) beside the scan of the work queue
+            // (one half-warp per queued agent: near phase, then far phase; main stream)
+            CK(c, cudaEventRecord(c->ev_fork, s));
+            CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+            {
+                cudaStream_t ms = c->stream;
+                c->stream = c->side;
+                LAUNCH(K_NEAR, CK(c, launch_k(false, c->side, k_efilter, std::min(blocks(2LL * d.ecap, 256), pers), 256, 0, d)));
+                c->stream = ms;
             }
+            CK(c, cudaEventRecord(c->ev_efil, c->side));
+            LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw, std::min(blocks(d.n, 16), pers), 256, 0, d)));
+            CK(c, cudaStreamWaitEvent(s, c->ev_efil, 0));
             LAUNCH(K_UNION, CK(c, launch_k(c->pdl, s, k_union, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
         }
         LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, nb, 256, 0, d)));
@@ -670,6 +653,7 @@ extern "C" int am_destroy(am_ctx* c)
         cudaStreamDestroy(c->side);
         cudaEventDestroy(c->ev_fork);
         cudaEventDestroy(c->ev_join);
+        cudaEventDestroy(c->ev_efil);
     }
     cudaFree(c->ws);
     cudaFreeHost(c->h_ctl);

@@ -50,9 +50,9 @@ struct Ctl {
     int32_t  sort_bits;    // significant bits of this round's ready keys
     int32_t  full;         // recompute every verdict / coupling edge this round
     int32_t  full_next;    // force a full round next time (edge list overflowed, ablation scan)
-    uint32_t ecur;         // which coupling-edge list is current
-    uint32_t ecnt[2];      // edges in each list
-    int32_t  ecarried;     // edges carried over into this round's list (the new ones follow)
+    uint32_t ecur;         // which pair of coupling-edge lists is current (ping-pong)
+    uint32_t ccnt[2];      // edges in each carried list (k_efilter output)
+    uint32_t ncnt[2];      // edges in each new list (k_scan_hw output)
     int32_t  n_work, n_far, n_items, n_edges;   // this round's scan work (stats)
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
@@ -88,15 +88,11 @@ struct Dev {
     uint8_t* v8;           // [n] per id: blocking verdict (0 no, 1 yes, 2 far phase pending)
     uint32_t* witness;     // [n] per id: the blocker found last time it was computed
     uint8_t* chg8;         // [n] per id: step changed since the last round (set by am_update)
-    uint32_t* farq;        // [kEdgeStripes][farq_cap] agents queued for the far phase
-    uint32_t* farq_ctr;    // [kEdgeStripes]
-    int32_t farq_cap;      // per stripe (every block of 8 warps maps to one stripe)
-    uint2* items;          // [kEdgeStripes][item_cap] far work items (agent, 4x4-block key)
-    uint32_t* item_ctr;    // [kEdgeStripes]
-    int32_t item_cap;      // per stripe
-    uint2* edges;          // [2][ecap] coupling edge lists (a < b), current and next
+    uint2* cedges;         // [2][ecap] carried coupling edges (a < b), ping-pong
+    uint2* nedges;         // [2][ecap] new coupling edges (a < b), ping-pong
     int32_t ecap;
-    uint32_t* wq;          // [kEdgeStripes][wq_cap] work queue of the scan (id | changed<<31)
+    int4* wq;              // [kEdgeStripes][wq_cap] work queue of the scan: the agent's record
+                           // {x | y<<16, step, id | changed<<31, status}
     uint32_t* wq_ctr;      // [kEdgeStripes]
     int32_t wq_cap;
     uint32_t* parent;      // [n] union-find forest in id space (root = min id)
@@ -173,12 +169,11 @@ struct am_ctx {
     int num_sms = 148;
     int sort_ctas = 16;              // persistent CTAs of each radix pass
     int sort_passes_max = 1;
-    cudaStream_t side = nullptr;     // the priority sort runs here, beside digest/dispatch
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t side = nullptr;     // edge filter (beside the scan) and priority sort (beside
+                                     // digest/dispatch) run here
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_efil = nullptr;
     bool join_pending = false;
     bool pdl = true;                 // programmatic dependent launch between round kernels
-    int scan_split = 0;              // scan as k_near + far kernel(s) (ablation)
-    int far_items = 0;               // far phase as k_far1 + k_far2 (ablation)
     int csort_ctas = 0;              // cluster size of the one-kernel priority sort (0 = onesweep)
     int csort_cap = 0;               // dynamic shared memory bytes per CTA of k_csort
     int ntiles_sort = 1;

@@ -149,8 +149,9 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
 // ============================================================== binned round
 // block-aggregated append of the flagged threads' values to queue stripe `stripe` (one
 // global atomic per block, in thread order); every thread of the 256-thread block calls it
-__device__ __forceinline__ void block_append(uint32_t* q, int cap, uint32_t* ctr, int stripe, bool flag,
-                                             uint32_t val, uint32_t* s_w /*[9]*/)
+template <class T>
+__device__ __forceinline__ void block_append(T* q, int cap, uint32_t* ctr, int stripe, bool flag, const T& val,
+                                             uint32_t* s_w /*[9]*/)
 {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned m = __ballot_sync(0xFFFFFFFFu, flag);
@@ -167,41 +168,28 @@ __device__ __forceinline__ void block_append(uint32_t* q, int cap, uint32_t* ctr
 }
 
 // k_bin: Morton cell key, slot inside the cell (atomic histogram), per-cell min step;
-// also resets the union-find forest and the per-root bad flags for this round.
-// It also builds the scan's work queue (see the incremental scan below): changed agents
-// (step differs from the last round, or a full round) and IDLE agents whose witness
-// changed.
+// also resets the per-root bad flags for this round.
 __global__ void __launch_bounds__(256) k_bin(Dev d)
 {
     pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t c = d.ctl->cur;
-    bool work = false, chg = false;
     if (i < d.n) {
-        // independent loads first (one round trip), then the atomics and the witness's
-        // change flag (a second one)
+        // independent loads first (one round trip), then the atomics
         const uint8_t st = d.status[c][i];
         const int2 p = d.pos[c][i];
         const int s = d.step[c][i];
-        const bool ch = d.chg8[i] != 0;
-        const uint32_t w = d.witness[i];
         uint32_t key = kSentinel, rank = 0;
         if (st != ST_DONE) {
             key = morton((uint32_t)p.x >> d.clog, (uint32_t)p.y >> d.clog);
             rank = atomicAdd(d.cnt + key, 1u);
             atomicMin(d.cmin + key, s);
-            chg = round_full(d) || ch;
-            work = chg || (st == ST_IDLE && w != kSentinel && agent_changed(d, c, w));
         }
         d.key[i] = key;
         d.rank[i] = rank;
         d.bad[i] = 0;
         d.blkid[i] = 0;
     }
-    // work queue: stripe = block index mod 64, one atomic per block
-    __shared__ uint32_t s_w[9];
-    block_append(d.wq, d.wq_cap, d.wq_ctr, (int)(blockIdx.x & (kEdgeStripes - 1)), work,
-                 (uint32_t)i | (chg ? 0x80000000u : 0u), s_w);
 }
 
 // k_cells: exclusive scan of the cell counts in Morton order -> ctab{start, min};
@@ -274,35 +262,48 @@ __global__ void __launch_bounds__(256) k_cells(Dev d)
 }
 
 // k_scatter: agents -> records sorted by cell (the order inside a cell is arbitrary;
-// no output depends on it).
+// no output depends on it); the union-find reset, per-agent flags and the scan's work
+// queue of this round.
 __global__ void __launch_bounds__(256) k_scatter(Dev d)
 {
     pdl_begin();
+    __shared__ uint32_t s_w[9];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= d.n) return;
     const uint32_t c = d.ctl->cur;
-    const uint32_t key = d.key[i];
-    const uint32_t rk = d.rank[i];
-    const int2 p = d.pos[c][i];
-    const int s = d.step[c][i];
-    const uint8_t st = d.status[c][i];
-    const bool ch = d.chg8[i] != 0;
-    const int lab = d.labels[i];
-    const bool full = round_full(d);
-    if (key == kSentinel) {   // DONE: counts as changed for the carried edges (k_efilter)
-        d.agflag[i] = 1;
-        return;
+    bool work = false;
+    int4 q = make_int4(0, 0, 0, 0);
+    if (i < d.n) {
+        const uint32_t key = d.key[i];
+        const uint32_t rk = d.rank[i];
+        const int2 p = d.pos[c][i];
+        const int s = d.step[c][i];
+        const uint8_t st = d.status[c][i];
+        const bool ch = d.chg8[i] != 0;
+        const int lab = d.labels[i];
+        const uint32_t w = d.witness[i];
+        const bool full = round_full(d);
+        if (key == kSentinel) {   // DONE: counts as changed for the carried edges (k_efilter)
+            d.agflag[i] = 1;
+        } else {
+            const bool chg = full || ch;
+            const uint32_t r = (uint32_t)d.ctab[key].x + rk;
+            d.rec[r] = make_int4(p.x | (p.y << 16), s, i, st | (chg ? kRecChanged : 0));
+            // union-find forest of this round: an agent whose last-round cluster has no
+            // changed member keeps that cluster (all its coupling edges are unchanged: it
+            // is still connected, and it can only grow through an edge of a changed
+            // agent), so it hangs under the old root (= min id = its label); members of
+            // dirty clusters start alone
+            const bool dirty = full || lab < 0 || d.dirty[lab] == d.ctl->epoch;
+            d.parent[i] = dirty ? (uint32_t)i : (uint32_t)lab;
+            d.agflag[i] = (uint8_t)((chg ? 1 : 0) | (dirty ? 2 : 0));
+            // the scan's work queue (incremental scan): changed
+            // agents, and IDLE agents whose recorded blocker (witness) changed
+            work = chg || (st == ST_IDLE && w != kSentinel && agent_changed(d, c, w));
+            q = make_int4(p.x | (p.y << 16), s, (int)((uint32_t)i | (chg ? 0x80000000u : 0u)), st);
+        }
     }
-    const uint32_t r = (uint32_t)d.ctab[key].x + rk;
-    const int chg = (full || ch) ? kRecChanged : 0;
-    d.rec[r] = make_int4(p.x | (p.y << 16), s, i, st | chg);
-    // union-find forest of this round: an agent whose last-round cluster has no changed
-    // member keeps that cluster (all its coupling edges are unchanged: it is still
-    // connected, and it can only grow through an edge of a changed agent), so it hangs
-    // under the old root (= min id = its label); members of dirty clusters start alone
-    const bool dirty = full || lab < 0 || d.dirty[lab] == d.ctl->epoch;
-    d.parent[i] = dirty ? (uint32_t)i : (uint32_t)lab;
-    d.agflag[i] = (uint8_t)((chg ? 1 : 0) | (dirty ? 2 : 0));
+    // stripe = block index mod 64, one atomic per block
+    block_append(d.wq, d.wq_cap, d.wq_ctr, (int)(blockIdx.x & (kEdgeStripes - 1)), work, q, s_w);
 }
 
 // test every record of cell `key` against agent A; returns true if A got blocked.
@@ -487,9 +488,9 @@ __device__ __forceinline__ void stage_edge(const Dev& d, EdgeStage& sm, uint32_t
     }
     // staging full (dense neighbourhood): append this edge directly
     const uint32_t nxt = d.ctl->ecur ^ 1u;
-    const uint32_t k = atomicAdd((uint32_t*)&d.ctl->ecnt[nxt], 1u);
+    const uint32_t k = atomicAdd((uint32_t*)&d.ctl->ncnt[nxt], 1u);
     if ((int)k < d.ecap) {
-        d.edges[(size_t)nxt * d.ecap + k] = make_uint2(a, b);
+        d.nedges[(size_t)nxt * d.ecap + k] = make_uint2(a, b);
     } else {
         uf_unite(d.parent, a, b);                  // list full: unite now, rebuild next round
         d.ctl->full_next = 1;
@@ -502,12 +503,12 @@ __device__ __forceinline__ void flush_stage(const Dev& d, EdgeStage& sm, int lan
     if (ne) {
         const uint32_t nxt = d.ctl->ecur ^ 1u;
         int base = 0;
-        if (lane == 0) base = (int)atomicAdd((uint32_t*)&d.ctl->ecnt[nxt], (uint32_t)ne);
+        if (lane == 0) base = (int)atomicAdd((uint32_t*)&d.ctl->ncnt[nxt], (uint32_t)ne);
         base = __shfl_sync(0xFFFFFFFFu, base, 0);
         for (int k = lane; k < ne; k += 32) {
             const uint2 e = sm.e[k];
             if (base + k < d.ecap) {
-                d.edges[(size_t)nxt * d.ecap + base + k] = e;
+                d.nedges[(size_t)nxt * d.ecap + base + k] = e;
             } else {
                 uf_unite(d.parent, e.x, e.y);      // list full: unite now, rebuild next round
                 d.ctl->full_next = 1;
@@ -540,13 +541,15 @@ __device__ __forceinline__ void stripe_prefix(const uint32_t* ctr, int cap, int*
     __syncthreads();
 }
 
-// k_efilter: carry over last round's coupling edges whose endpoints both kept their
-// state (nothing in a full round).  One atomic per block.
+// k_efilter: carry over last round's coupling edges (its carried and new lists) whose
+// endpoints both kept their state (nothing in a full round) into this round's carried
+// list, and unite those of dirty clusters.  Runs on the side stream beside k_scan_hw,
+// which writes this round's new list.  One atomic per block.
 __global__ void __launch_bounds__(256) k_efilter(Dev d)
 {
     pdl_begin();
-    const uint32_t cur = d.ctl->ecur;
-    const int ne = min((int)d.ctl->ecnt[cur], d.ecap);
+    const uint32_t cur = d.ctl->ecur, nxt = cur ^ 1u;
+    const int nc = min((int)d.ctl->ccnt[cur], d.ecap), ne = nc + min((int)d.ctl->ncnt[cur], d.ecap);
     const bool full = round_full(d);
     __shared__ uint32_t s_w[9];
     for (int base = blockIdx.x * 256; base < ne; base += gridDim.x * 256) {   // block uniform
@@ -554,7 +557,7 @@ __global__ void __launch_bounds__(256) k_efilter(Dev d)
         bool keep = false, dirty = false;
         uint2 e = make_uint2(0, 0);
         if (k < ne && !full) {
-            e = d.edges[(size_t)cur * d.ecap + k];
+            e = k < nc ? d.cedges[(size_t)cur * d.ecap + k] : d.nedges[(size_t)cur * d.ecap + (k - nc)];
             // per-endpoint flags of this round (k_scatter): bit 0 changed, bit 1 the
             // endpoint's last-round cluster is dirty (both endpoints share that cluster)
             const uint8_t fx = d.agflag[e.x], fy = d.agflag[e.y];
@@ -569,311 +572,32 @@ __global__ void __launch_bounds__(256) k_efilter(Dev d)
         if (threadIdx.x == 0) {
             uint32_t acc = 0;
             for (int q = 0; q < 8; q++) { const uint32_t v = s_w[q]; s_w[q] = acc; acc += v; }
-            s_w[8] = acc ? atomicAdd((uint32_t*)&d.ctl->ecnt[cur ^ 1u], acc) : 0u;
+            s_w[8] = acc ? atomicAdd((uint32_t*)&d.ctl->ccnt[nxt], acc) : 0u;
         }
         __syncthreads();
         if (keep) {
             const uint32_t pos = s_w[8] + s_w[w] + (uint32_t)__popc(m & ((1u << lane) - 1u));
-            d.edges[(size_t)(cur ^ 1u) * d.ecap + pos] = e;   // kept <= previous count <= ecap
-            // a dirty cluster's forest is rebuilt from its edges (a clean cluster's edges
-            // are implied by its members hanging under its root, k_scatter)
-            if (dirty) uf_unite(d.parent, e.x, e.y);
+            if ((int)pos < d.ecap) {
+                d.cedges[(size_t)nxt * d.ecap + pos] = e;
+                // a dirty cluster's forest is rebuilt from its edges (a clean cluster's
+                // edges are implied by its members hanging under its root, k_scatter)
+                if (dirty) uf_unite(d.parent, e.x, e.y);
+            } else {
+                uf_unite(d.parent, e.x, e.y);   // list full: unite now, rebuild next round
+                d.ctl->full_next = 1;
+            }
         }
         __syncthreads();
     }
-    if (finish_block(&d.ctl->efil, gridDim.x) && threadIdx.x == 0) {
-        d.ctl->ecarried = (int32_t)*(volatile uint32_t*)&d.ctl->ecnt[cur ^ 1u];
-        __threadfence();
-    }
 }
 
-// k_near: one thread per queued agent A (id, bit 31 = changed): the (at most 2x2 when
-// cell >= R_c) cells within box distance R_c: coupling edges for changed agents
-// (once per pair: from the smaller id when both changed), near blocking test for
-// IDLE agents with the blocker recorded as witness; agents still
-// unblocked and ahead of W go to the far queue.
-__global__ void __launch_bounds__(256, 6) k_near(Dev d)
-{
-    pdl_begin();
-    __shared__ EdgeStage s_all[8];
-    __shared__ int s_pref[kEdgeStripes + 1];
-    __shared__ uint32_t s_w[9];
-    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    EdgeStage& sm = s_all[wq];
-    if (lane == 0) sm.ne = 0;
-    stripe_prefix(d.wq_ctr, 1 << 30, s_pref);
-    const int nq = s_pref[kEdgeStripes];
-    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_work = nq;
-    const uint32_t c = d.ctl->cur;
-    const int W = d.ctl->W;
-    const int cl = d.clog, G = 1 << d.glog;
-    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-    const uint32_t Rc2 = Rc * Rc;
-    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
-    // grid-stride over the queue; every warp iteration is warp-uniform in trip count
-    for (int q0 = blockIdx.x * blockDim.x; q0 < nq; q0 += gridDim.x * blockDim.x) {
-        const int q = q0 + threadIdx.x;
-        bool farq = false;
-        uint32_t aid = 0;
-        if (q < nq) {
-            int lo = 0, hi = kEdgeStripes - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
-            }
-            const uint32_t w = d.wq[(size_t)lo * d.wq_cap + (q - s_pref[lo])];
-            aid = w & 0x7FFFFFFFu;
-            const bool chg = (w >> 31) != 0;
-            const int2 P = d.pos[c][aid];
-            const int ax = P.x, ay = P.y, as = d.step[c][aid];
-            const bool idle = d.status[c][aid] == ST_IDLE;
-            bool nblk = false;
-            uint32_t wit = kSentinel;
-            const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
-            const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
-            for (int cy = cy0; cy <= cy1; cy++)
-                for (int cx = cx0; cx <= cx1; cx++) {
-                    if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rc,
-                                    d.metric))
-                        continue;
-                    const uint32_t key = morton(cx, cy);
-                    const int2 e = d.ctab[key];
-                    if (e.y > as) continue;
-                    const int e1 = d.ctab[key + 1].x;
-                    for (int b = e.x; b < e1; b++) {
-                        const int4 B = d.rec[b];
-                        const uint32_t bid = (uint32_t)B.z;
-                        if (bid == aid) continue;
-                        const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-                        if (B.y == as) {
-                            // B's record carries its changed bit (k_scatter)
-                            if (chg && within2(dx, dy, Rc2, Rc, d.metric) &&
-                                (!(B.w & kRecChanged) || aid < bid))
-                                stage_edge(d, sm, min(aid, bid), max(aid, bid));
-                        } else if (idle && !nblk && B.y < as) {
-                            const int lag = as - B.y;
-                            const uint32_t R =
-                                min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
-                            if (within2(dx, dy, R * R, R, d.metric)) {
-                                nblk = true;
-                                wit = bid;
-                            }
-                        }
-                    }
-                }
-            if (idle) {
-                if (nblk) {
-                    d.v8[aid] = 1;
-                    d.witness[aid] = wit;
-                } else if (as > W && !(d.flags & AM_DBG_SKIP_FAR)) {
-                    d.v8[aid] = 2;          // far phase decides
-                    farq = true;
-                } else {
-                    d.v8[aid] = 0;
-                    d.witness[aid] = kSentinel;
-                }
-            }
-        }
-        flush_stage(d, sm, lane);
-        // far queue: stripe = block index mod 64, one atomic per block iteration
-        block_append(d.farq, d.farq_cap, d.farq_ctr, (int)(blockIdx.x & (kEdgeStripes - 1)), farq, aid, s_w);
-    }
-}
-
-// k_far: the far (time-dilated) phase for the queued agents.  A walks the min-step
-// pyramid with ITS OWN point and step: a 16x16-cell block, 4x4-cell block or cell with
-// min step m is skipped if m >= s_A or its box distance exceeds R_b(s_A - m) (exact
-// pruning: nothing inside can block A).  The 16 children of a block are
-// Morton-contiguous, so each level is fetched with a few 16-byte vector loads.  Cells
-// within R_c of A were tested completely by k_near and are skipped.
+// Morton child k (0..15) of a 4x4 block: offsets (dx, dy) in 0..3
 __device__ __forceinline__ void morton_child(int k, int& dx, int& dy)
 {
     dx = (k & 1) | ((k >> 1) & 2);
     dy = ((k >> 1) & 1) | ((k >> 2) & 2);
 }
 
-// test A against the cells of one 4x4-cell block (Morton key k1g at block coordinates
-// qx, qy); returns the id of a blocker or kSentinel
-__device__ __forceinline__ uint32_t far_block(const Dev& d, uint32_t k1g, int qx, int qy, int ax, int ay, int as,
-                                              uint32_t Rc, int lagcap, uint32_t& ncells, uint32_t& ncand)
-{
-    const int cl = d.clog;
-    const int4* e4 = reinterpret_cast<const int4*>(d.ctab + (size_t)k1g * 16);
-    int st[17], mn[16];
-#pragma unroll
-    for (int q = 0; q < 8; q++) {
-        const int4 v = e4[q];
-        st[2 * q] = v.x; mn[2 * q] = v.y; st[2 * q + 1] = v.z; mn[2 * q + 1] = v.w;
-    }
-    st[16] = d.ctab[(size_t)k1g * 16 + 16].x;
-#pragma unroll
-    for (int k0 = 0; k0 < 16; k0++) {
-        if (st[k0 + 1] == st[k0] || mn[k0] >= as) continue;
-        int ox, oy;
-        morton_child(k0, ox, oy);
-        const int cx = qx * 4 + ox, cy = qy * 4 + oy;
-        const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
-        ncells++;
-        if (box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric)) continue;   // tested by k_near
-        if (!box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - mn[k0], d.v, d.r_p), d.metric)) continue;
-        ncand += (uint32_t)(st[k0 + 1] - st[k0]);
-        for (int b = st[k0]; b < st[k0 + 1]; b++) {
-            const int4 B = d.rec[b];
-            if (B.y >= as) continue;
-            const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-            const int lag = as - B.y;
-            const uint32_t Rb = min((uint32_t)min(lag, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
-            if (within2(dx, dy, Rb * Rb, Rb, d.metric)) return (uint32_t)B.z;
-        }
-    }
-    return kSentinel;
-}
-
-// k_far1: one thread per queued agent: the 16x16- and 4x4-cell levels of the pyramid,
-// then one work item per surviving 4x4-cell block appended to a striped item list for
-// k_far2, so a leading agent with many candidate blocks is spread over many threads.
-// If the item list is full the thread tests the block itself.
-__global__ void __launch_bounds__(256, 2) k_far1(Dev d)
-{
-    pdl_begin();
-    __shared__ int s_pref[kEdgeStripes + 1];
-    stripe_prefix(d.farq_ctr, 1 << 30, s_pref);
-    const int nq = s_pref[kEdgeStripes];
-    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_far = nq;
-    const int W = d.ctl->W;
-    const uint32_t c = d.ctl->cur;
-    uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
-    const int stripe = blockIdx.x & (kEdgeStripes - 1);
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
-        int lo = 0, hi = kEdgeStripes - 1;          // last queue stripe with s_pref <= q
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
-        }
-        const uint32_t aid = d.farq[(size_t)lo * d.farq_cap + (q - s_pref[lo])];
-        const int2 P = d.pos[c][aid];
-        const int ax = P.x, ay = P.y, as = d.step[c][aid];
-        const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
-        const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-        const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
-        const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
-        const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
-        const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
-        uint32_t wit = kSentinel;
-        for (int by = by0; by <= by1 && wit == kSentinel; by++)
-            for (int bx = bx0; bx <= bx1 && wit == kSentinel; bx++) {
-                const uint32_t k2 = morton(bx, by);
-                const int m2 = __ldg(d.lmin2 + k2);
-                nb2++;
-                if (m2 >= as || !box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
-                                            rb_radius((long long)as - m2, d.v, d.r_p), d.metric))
-                    continue;
-                const int4* c4 = reinterpret_cast<const int4*>(d.lmin1 + k2 * 16);
-                unsigned keep = 0;
-#pragma unroll
-                for (int qv = 0; qv < 4; qv++) {
-                    const int4 v = __ldg(c4 + qv);
-                    const int mm[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        const int k1 = 4 * qv + j;
-                        int ox, oy;
-                        morton_child(k1, ox, oy);
-                        const int qx = bx * 4 + ox, qy = by * 4 + oy;
-                        if (mm[j] < as && box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
-                                                     ((qy + 1) << l1) - 1, rb_radius((long long)as - mm[j], d.v, d.r_p),
-                                                     d.metric))
-                            keep |= 1u << k1;
-                    }
-                }
-                nb1 += 16;
-                if (!keep) continue;
-                const int cnt = __popc(keep);
-                const int base = (int)atomicAdd(d.item_ctr + stripe, (unsigned)cnt);
-                int k = 0;
-                while (keep && wit == kSentinel) {
-                    const int k1 = __ffs(keep) - 1;
-                    keep &= keep - 1;
-                    const uint32_t k1g = k2 * 16 + (uint32_t)k1;
-                    if (base + k < d.item_cap) {
-                        d.items[(size_t)stripe * d.item_cap + base + k] = make_uint2(aid, k1g);
-                        nitems++;
-                    } else {
-                        int ox, oy;
-                        morton_child(k1, ox, oy);
-                        wit = far_block(d, k1g, bx * 4 + ox, by * 4 + oy, ax, ay, as, Rc, lagcap, ncells, ncand);
-                    }
-                    k++;
-                }
-            }
-        d.v8[aid] = wit != kSentinel ? 1 : 0;
-        d.witness[aid] = wit;
-    }
-    if (d.flags & AM_STATS) {
-        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
-        const unsigned c3 = __reduce_add_sync(0xFFFFFFFFu, nb2), c4 = __reduce_add_sync(0xFFFFFFFFu, nb1);
-        const unsigned c2 = __reduce_add_sync(0xFFFFFFFFu, nitems);
-        if ((threadIdx.x & 31) == 0) {
-            atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
-            atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
-            atomicAdd(&d.ctl->st_p2, (unsigned long long)c2);   // far work items
-            atomicAdd(&d.ctl->st_b2, (unsigned long long)c3);
-            atomicAdd(&d.ctl->st_b1, (unsigned long long)c4);
-        }
-    }
-}
-
-// k_far2: one thread per (agent, 4x4-cell block) item: its 16 cells (one vector fetch)
-// and the records of the cells that survive the min-step test.
-__global__ void __launch_bounds__(256) k_far2(Dev d)
-{
-    pdl_begin();
-    __shared__ int s_pref[kEdgeStripes + 1];
-    stripe_prefix(d.item_ctr, d.item_cap, s_pref);
-    const int total = s_pref[kEdgeStripes];
-    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_items = total;
-    const uint32_t c = d.ctl->cur;
-    uint32_t ncells = 0, ncand = 0;
-    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
-        int lo = 0, hi = kEdgeStripes - 1;          // last stripe with s_pref <= g
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_pref[mid] <= g) lo = mid; else hi = mid - 1;
-        }
-        const uint2 it = d.items[(size_t)lo * d.item_cap + (g - s_pref[lo])];
-        const uint32_t aid = it.x;
-        if (*(volatile uint8_t*)(d.v8 + aid) == 1) continue;   // another block already blocked it
-        const int2 P = d.pos[c][aid];
-        const int ax = P.x, ay = P.y, as = d.step[c][aid];
-        const uint32_t k1g = it.y;
-        const int ox = (int)part_compact(k1g), oy = (int)part_compact(k1g >> 1);
-        const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-        const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
-        const uint32_t wit = far_block(d, k1g, ox, oy, ax, ay, as, Rc, lagcap, ncells, ncand);
-        if (wit != kSentinel) {
-            d.v8[aid] = 1;
-            d.witness[aid] = wit;
-        }
-    }
-    if (d.flags & AM_STATS) {
-        const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, ncand);
-        if ((threadIdx.x & 31) == 0) {
-            atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
-            atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
-        }
-    }
-}
-
-// k_far: the far phase with one HALF-WARP per far-queued agent A.  The Morton pyramid
-// has a fan-out of 16 at every level, so the 16 lanes test the 16 children of a block
-// at once: (level 2) the 16x16-cell blocks of A's R_b(s_A - W) box, 16 per step; (level
-// 1) the 4x4-cell children of each surviving block; (level 0) the cells of each
-// surviving 4x4 block (one 8-byte table entry per lane, next start by shuffle); the
-// records of the surviving cells are flattened over the lanes (prefix sum of the cell
-// counts, a 4-step shuffle search per lane) and tested 16 at a time.  Pruning is the
-// exact test of k_far1/k_far2 (min step m of a block: skip if m >= s_A or its box
-// distance exceeds R_b(s_A - m)); cells within R_c of A were tested by k_near.  The
-// first blocker found becomes A's witness.
 // Work counters of the half-warp scan (AM_STATS and the far-item count).
 struct HwStats {
     uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
@@ -899,9 +623,17 @@ __device__ __forceinline__ void hw_flush_stats(const Dev& d, const HwStats& hs, 
     }
 }
 
-// The far-phase traversal of one agent A = (ax, ay, as) by the 16 lanes of a half-warp
-// (lane l, half h, lane mask hm); returns a blocker's id or kSentinel.  Level by level
-// the 16 lanes test the 16 Morton children of a block; see k_far.
+// The far phase (time-dilated blocking beyond R_c) of one agent A = (ax, ay, as) by the
+// 16 lanes of a half-warp (lane l, half h, lane mask hm), walking the Morton min-step
+// pyramid with A's own point and step.  The pyramid has a fan-out of 16 at every level,
+// so the 16 lanes test the 16 children of a block at once: (level 2) the 16x16-cell
+// blocks of A's R_b(s_A - W) box, 16 per step; (level 1) the 4x4-cell children of each
+// surviving block; (level 0) the cells of each surviving 4x4 block (one 8-byte table
+// entry per lane, next start by shuffle).  A block, 4x4 block or cell with min step m
+// is skipped if m >= s_A or its box distance exceeds R_b(s_A - m) (exact pruning:
+// nothing inside can block A); cells within R_c of A are tested by the near phase.  The
+// records of the surviving cells are flattened over the lanes and tested 16 at a time.
+// Returns a blocker's id or kSentinel.
 __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as, int W, int l, int h, unsigned hm,
                                            int ox_l, int oy_l, HwStats& hs)
 {
@@ -1001,68 +733,110 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
     return wit;
 }
 
-__global__ void __launch_bounds__(256) k_far(Dev d)
+// k_scan_hw: the whole incremental scan with one HALF-WARP per queued agent A.  The work
+// queue (k_scatter) holds A's 16-byte record {x | y<<16, step, id | changed<<31, status}.
+//   * the cells of A's query box -- R_c = r_p + v for coupling, plus R_b(s_A - W) when A
+//     is IDLE and ahead of the watermark (the far blocking test) -- when the box holds at
+//     most kDirect cells: one round trip loads every cell entry {start, min step} (<= 4
+//     per lane), and the cells that can matter are compacted into a per-half-warp list,
+//     near cells (box distance <= R_c) first.  Near cells: coupling edges for a changed
+//     A (once per pair: from the smaller id when both changed) and the
+//     blocking test for an IDLE A.  Far cells: blocking only, kept if
+//     their min step m < s_A and their box distance <= R_b(s_A - m) (exact pruning);
+//   * larger boxes: the near cells the same way, then the Morton min-step pyramid
+//     (hw_far) for the far test.
+// The records of the listed cells are flattened over the 16 lanes (prefix sum of the
+// cell counts, 4-step shuffle search per lane) and tested 16 at a time; the first
+// blocker becomes A's witness.
+constexpr int kDirect = 64;    // cells of the query box resolved with one table fetch
+
+// test the records of the cells in `list[0..nl)` (near cells first: nn of them) against
+// A; returns (in nblk/wit) the first blocker; stages coupling edges for a changed A
+__device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const int2* list, int nl, int nn, int ax,
+                                           int ay, int as, uint32_t aid, bool chg, bool idle, int l, int h,
+                                           unsigned hm, bool& nblk, uint32_t& wit, HwStats& hs)
 {
-    pdl_begin();
-    __shared__ int s_pref[kEdgeStripes + 1];
-    __shared__ uint32_t s_items;
-    if (threadIdx.x == 0) s_items = 0;
-    stripe_prefix(d.farq_ctr, 1 << 30, s_pref);
-    const int nq = s_pref[kEdgeStripes];
-    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_far = nq;
-    const int W = d.ctl->W;
-    const uint32_t c = d.ctl->cur;
-    const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4, hw = threadIdx.x >> 4;
-    const unsigned hm = 0xFFFFu << (16 * h);
-    int ox_l, oy_l;
-    morton_child(l, ox_l, oy_l);
-    HwStats hs;
-    for (int q0 = blockIdx.x * 16; q0 < nq; q0 += gridDim.x * 16) {
-        const int q = q0 + hw;
-        if (q >= nq) continue;   // half-warp uniform
-        int lo = 0, hi = kEdgeStripes - 1;          // last queue stripe with s_pref <= q
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
+    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const uint32_t Rc2 = Rc * Rc;
+    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+    for (int c0 = 0; c0 < nl; c0 += 16) {
+        // nothing left to decide: blocked (or not IDLE) and no coupling in the rest
+        if ((nblk || !idle) && (!chg || c0 >= nn)) break;
+        const int k = c0 + l;
+        int st0 = 0, cnt = 0;
+        if (k < nl) {
+            const int2 e = list[k];
+            st0 = e.x;
+            cnt = e.y;
         }
-        const uint32_t aid = d.farq[(size_t)lo * d.farq_cap + (q - s_pref[lo])];
-        const int2 P = d.pos[c][aid];
-        const uint32_t wit = hw_far(d, P.x, P.y, d.step[c][aid], W, l, h, hm, ox_l, oy_l, hs);
-        if (l == 0) {
-            d.v8[aid] = wit != kSentinel ? 1 : 0;
-            d.witness[aid] = wit;
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const int y = __shfl_up_sync(hm, incl, o, 16);
+            if (l >= o) incl += y;
+        }
+        const int excl = incl - cnt;
+        const int total = __shfl_sync(hm, incl, 15, 16);
+        // the near cells' records form a prefix [0, near_end) of the flattened range
+        const int near_end = nn > c0 ? __shfl_sync(hm, incl, min(nn - c0, 16) - 1, 16) : 0;
+        hs.ncand += l == 0 ? (uint32_t)total : 0u;
+        for (int b0 = 0; b0 < total; b0 += 16) {
+            if ((nblk || !idle) && !(chg && b0 < near_end)) break;   // half-warp uniform
+            const int tq = b0 + l;
+            int sl = 0;
+#pragma unroll
+            for (int stp = 8; stp > 0; stp >>= 1) {
+                const int ex = __shfl_sync(hm, excl, sl + stp, 16);
+                if (ex <= tq) sl += stp;
+            }
+            const int rs = __shfl_sync(hm, st0, sl, 16), rx = __shfl_sync(hm, excl, sl, 16);
+            const bool bnear = tq < near_end;
+            bool found = false;
+            uint32_t bid = 0;
+            if (tq < total) {
+                const int4 B = d.rec[rs + (tq - rx)];
+                bid = (uint32_t)B.z;
+                if (bid != aid) {
+                    const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                    if (B.y == as) {
+                        // B's record carries its changed bit (k_scatter)
+                        if (chg && bnear && within2(dx, dy, Rc2, Rc, d.metric) && (!(B.w & kRecChanged) || aid < bid))
+                            stage_edge(d, sm, min(aid, bid), max(aid, bid));
+                    } else if (idle && !nblk && B.y < as) {
+                        const uint32_t R =
+                            min((uint32_t)min(as - B.y, lagcap) * (uint32_t)d.v + (uint32_t)(d.v + d.r_p), kRClamp);
+                        found = within2(dx, dy, R * R, R, d.metric);
+                    }
+                }
+            }
+            const unsigned fm = (__ballot_sync(hm, found) >> (16 * h)) & 0xFFFFu;
+            if (fm && !nblk) {
+                nblk = true;
+                wit = __shfl_sync(hm, bid, __ffs(fm) - 1, 16);
+            }
         }
     }
-    hw_flush_stats(d, hs, lane, s_items);
 }
 
-// k_scan_hw: the whole incremental scan with one HALF-WARP per queued agent A (work
-// queue of k_bin: id, bit 31 = changed).  Near phase: the cells within box distance R_c
-// of A (<= 2x2 when cell >= R_c), one lane per cell, their records flattened over the 16
-// lanes: coupling edges for a changed A (once per pair: from the smaller
-// id when both changed) and, for an IDLE A, the blocking test with the
-// blocker kept as witness.  An IDLE A still unblocked and ahead of W continues with the
-// far phase (hw_far) in the same half-warp -- no far queue, no second launch.
 __global__ void __launch_bounds__(256) k_scan_hw(Dev d)
 {
     pdl_begin();
     __shared__ EdgeStage s_all[8];
+    __shared__ int2 s_list[16][kDirect];
     __shared__ int s_pref[kEdgeStripes + 1];
     __shared__ uint32_t s_items;
     const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4, hw = threadIdx.x >> 4;
     const unsigned hm = 0xFFFFu << (16 * h);
     EdgeStage& sm = s_all[threadIdx.x >> 5];
+    int2* list = s_list[hw];
     if (lane == 0) sm.ne = 0;
     if (threadIdx.x == 0) s_items = 0;
     stripe_prefix(d.wq_ctr, 1 << 30, s_pref);
     const int nq = s_pref[kEdgeStripes];
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_work = nq;
-    const uint32_t c = d.ctl->cur;
     const int W = d.ctl->W;
     const int cl = d.clog, G = 1 << d.glog;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-    const uint32_t Rc2 = Rc * Rc;
-    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
     int ox_l, oy_l;
     morton_child(l, ox_l, oy_l);
     HwStats hs;
@@ -1075,80 +849,74 @@ __global__ void __launch_bounds__(256) k_scan_hw(Dev d)
                 const int mid = (lo + hi + 1) >> 1;
                 if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
             }
-            const uint32_t wv = d.wq[(size_t)lo * d.wq_cap + (q - s_pref[lo])];
-            const uint32_t aid = wv & 0x7FFFFFFFu;
-            const bool chg = (wv >> 31) != 0;
-            const int2 P = d.pos[c][aid];
-            const int ax = P.x, ay = P.y, as = d.step[c][aid];
-            const bool idle = d.status[c][aid] == ST_IDLE;
-            // ---- near phase
-            const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
-            const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
+            const int4 A = d.wq[(size_t)lo * d.wq_cap + (q - s_pref[lo])];
+            const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
+            const uint32_t aid = (uint32_t)A.z & 0x7FFFFFFFu;
+            const bool chg = ((uint32_t)A.z >> 31) != 0;
+            const bool idle = (A.w & 3) == ST_IDLE;
+            const bool far = idle && as > W && !(d.flags & AM_DBG_SKIP_FAR);
+            nfar += (far && l == 0) ? 1u : 0u;
+            // query box: far radius when the far test is due and the box is small enough
+            const int Rf = far ? (int)rb_radius((long long)as - W, d.v, d.r_p) : (int)Rc;
+            int cx0 = max(0, (ax - Rf) >> cl), cx1 = min(G - 1, (ax + Rf) >> cl);
+            int cy0 = max(0, (ay - Rf) >> cl), cy1 = min(G - 1, (ay + Rf) >> cl);
+            const bool direct = (cx1 - cx0 + 1) * (cy1 - cy0 + 1) <= kDirect;
+            if (!direct) {   // near cells only; the far test walks the pyramid below
+                cx0 = max(0, (ax - (int)Rc) >> cl); cx1 = min(G - 1, (ax + (int)Rc) >> cl);
+                cy0 = max(0, (ay - (int)Rc) >> cl); cy1 = min(G - 1, (ay + (int)Rc) >> cl);
+            }
             const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
             bool nblk = false;
             uint32_t wit = kSentinel;
-            for (int c0 = 0; c0 < ncell; c0 += 16) {
-                const int k = c0 + l;
-                int st0 = 0, cnt = 0;
-                if (k < ncell) {
-                    const int cx = cx0 + k % ncx, cy = cy0 + k / ncx;
-                    if (box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rc,
-                                   d.metric)) {
-                        const uint32_t key = morton(cx, cy);
-                        const int2 e = d.ctab[key];
-                        const int e1 = d.ctab[key + 1].x;
-                        if (e.y <= as) { st0 = e.x; cnt = e1 - e.x; }
+            for (int cb = 0; cb < ncell; cb += kDirect) {   // one chunk unless cells are tiny
+                if ((nblk || !idle) && !chg) break;
+                // one round trip: the entries of the chunk's cells (<= 4 per lane)
+                int2 ent[kDirect / 16];
+                int nxt[kDirect / 16];
+#pragma unroll
+                for (int j = 0; j < kDirect / 16; j++) {
+                    const int k = cb + j * 16 + l;
+                    ent[j] = make_int2(0, INT_MAX);
+                    nxt[j] = 0;
+                    if (k < ncell) {
+                        const uint32_t key = morton(cx0 + k % ncx, cy0 + k / ncx);
+                        ent[j] = d.ctab[key];
+                        nxt[j] = d.ctab[key + 1].x;
                     }
                 }
-                hs.ncells += cnt > 0 ? 1u : 0u;
-                int incl = cnt;
+                // classify, compact into the list: near cells first, then far cells
+                int nn = 0, nl = 0;
 #pragma unroll
-                for (int o = 1; o < 16; o <<= 1) {
-                    const int y = __shfl_up_sync(hm, incl, o, 16);
-                    if (l >= o) incl += y;
-                }
-                const int excl = incl - cnt;
-                const int total = __shfl_sync(hm, incl, 15, 16);
-                hs.ncand += l == 0 ? (uint32_t)total : 0u;
-                for (int b0 = 0; b0 < total; b0 += 16) {
-                    if (!chg && (nblk || !idle)) break;   // nothing left to decide (uniform)
-                    const int tq = b0 + l;
-                    int sl = 0;
+                for (int pass = 0; pass < 2; pass++) {
 #pragma unroll
-                    for (int stp = 8; stp > 0; stp >>= 1) {
-                        const int ex = __shfl_sync(hm, excl, sl + stp, 16);
-                        if (ex <= tq) sl += stp;
-                    }
-                    const int rs = __shfl_sync(hm, st0, sl, 16), rx = __shfl_sync(hm, excl, sl, 16);
-                    bool found = false;
-                    uint32_t bid = 0;
-                    if (tq < total) {
-                        const int4 B = d.rec[rs + (tq - rx)];
-                        bid = (uint32_t)B.z;
-                        if (bid != aid) {
-                            const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-                            if (B.y == as) {
-                                // B's record carries its changed bit (k_scatter)
-                                if (chg && within2(dx, dy, Rc2, Rc, d.metric) && (!(B.w & kRecChanged) || aid < bid))
-                                    stage_edge(d, sm, min(aid, bid), max(aid, bid));
-                            } else if (idle && !nblk && B.y < as) {
-                                const uint32_t R = min((uint32_t)min(as - B.y, lagcap) * (uint32_t)d.v +
-                                                           (uint32_t)(d.v + d.r_p), kRClamp);
-                                found = within2(dx, dy, R * R, R, d.metric);
-                            }
+                    for (int j = 0; j < kDirect / 16; j++) {
+                        const int k = cb + j * 16 + l;
+                        bool ok = false;
+                        if (k < ncell && nxt[j] > ent[j].x) {
+                            const int cx = cx0 + k % ncx, cy = cy0 + k / ncx;
+                            const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
+                            const bool isnear = box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric);
+                            const int mn = ent[j].y;
+                            if (pass == 0)
+                                ok = isnear && (chg ? mn <= as : (idle && mn < as));
+                            else
+                                ok = !isnear && far && direct && mn < as &&
+                                     box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - mn, d.v, d.r_p),
+                                                d.metric);
                         }
+                        const unsigned bm = (__ballot_sync(hm, ok) >> (16 * h)) & 0xFFFFu;
+                        if (ok) list[nl + __popc(bm & ((1u << l) - 1u))] = make_int2(ent[j].x, nxt[j] - ent[j].x);
+                        nl += __popc(bm);
                     }
-                    const unsigned fm = (__ballot_sync(hm, found) >> (16 * h)) & 0xFFFFu;
-                    if (fm && !nblk) {
-                        nblk = true;
-                        wit = __shfl_sync(hm, bid, __ffs(fm) - 1, 16);
-                    }
+                    if (pass == 0) nn = nl;
                 }
+                hs.ncells += l == 0 ? (uint32_t)nl : 0u;
+                __syncwarp(hm);
+                hw_records(d, sm, list, nl, nn, ax, ay, as, aid, chg, idle, l, h, hm, nblk, wit, hs);
+                __syncwarp(hm);   // the list is rewritten by the next chunk / agent
             }
-            // ---- far phase (IDLE, not blocked nearby, ahead of the watermark)
             if (idle) {
-                if (!nblk && as > W && !(d.flags & AM_DBG_SKIP_FAR)) {
-                    nfar += l == 0 ? 1u : 0u;
+                if (far && !direct && !nblk) {
                     wit = hw_far(d, ax, ay, as, W, l, h, hm, ox_l, oy_l, hs);
                     nblk = wit != kSentinel;
                 }
@@ -1172,11 +940,11 @@ __global__ void __launch_bounds__(256) k_union(Dev d)
 {
     pdl_begin();
     const uint32_t nxt = d.ctl->ecur ^ 1u;
-    const int ne = min((int)d.ctl->ecnt[nxt], d.ecap);
-    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_edges = ne;
+    const int ne = min((int)d.ctl->ncnt[nxt], d.ecap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_edges = ne + min((int)d.ctl->ccnt[nxt], d.ecap);
     // the carried edges were united by k_efilter where their cluster was dirty
-    for (int k = d.ctl->ecarried + blockIdx.x * blockDim.x + threadIdx.x; k < ne; k += gridDim.x * blockDim.x) {
-        const uint2 e = d.edges[(size_t)nxt * d.ecap + k];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ne; k += gridDim.x * blockDim.x) {
+        const uint2 e = d.nedges[(size_t)nxt * d.ecap + k];
         uf_unite(d.parent, e.x, e.y);
     }
     if (finish_block(&d.ctl->uni, gridDim.x) && threadIdx.x == 0) {
@@ -1642,13 +1410,10 @@ __global__ void k_round_begin(Dev d)
     ctl->n_far = 0;
     ctl->full |= ctl->full_next;
     ctl->full_next = 0;
-    ctl->ecnt[ctl->ecur ^ 1u] = 0;
+    ctl->ccnt[ctl->ecur ^ 1u] = 0;
+    ctl->ncnt[ctl->ecur ^ 1u] = 0;
     if (d.wq_ctr)
-        for (int k = 0; k < kEdgeStripes; k++) {
-            d.wq_ctr[k] = 0;
-            d.farq_ctr[k] = 0;
-            d.item_ctr[k] = 0;
-        }
+        for (int k = 0; k < kEdgeStripes; k++) d.wq_ctr[k] = 0;
 }
 
 }  // namespace am
