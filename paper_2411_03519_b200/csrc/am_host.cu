@@ -10,6 +10,7 @@
 
 namespace am {
 __global__ void k_ingest(Dev d, const int2* npos, const int32_t* nstep, const uint8_t* nstat, int mode);
+__global__ void k_ingest_done(Dev d, int mode);
 __global__ void k_bin(Dev d);
 __global__ void k_cells(Dev d);
 __global__ void k_scatter(Dev d);
@@ -160,7 +161,7 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 2 : 11 + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
+    return c->path == 0 ? 3 : 12 + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -249,6 +250,12 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         x->num_sms = sms > 0 ? sms : 148;
+    }
+    {   // the scan's persistent grid: exactly the resident blocks (no block waits for a slot)
+        int per = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan_hw, 256, 0) == cudaSuccess && per > 0)
+            x->scan_blocks = per * x->num_sms;
+        cudaGetLastError();
     }
 
     // path selection
@@ -402,6 +409,7 @@ static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, co
     am_join_side(c);
     am_prof_begin(c, K_INGEST);
     CK(c, launch_k(c->pdl, c->stream, k_ingest, blocks(c->d.n, 256 * kIngestItems), 256, 0, c->d, (const int2*)pos, steps, st, mode));
+    CK(c, launch_k(c->pdl, c->stream, k_ingest_done, 1, 1, 0, c->d, mode));
     am_prof_end(c, K_INGEST);
     CK(c, cudaGetLastError());
     return AM_OK;
@@ -502,7 +510,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
     } else {
         const unsigned nb = blocks(d.n, 256);
         LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, nb, 256, 0, d)));
-        LAUNCH(K_CELLS, CK(c, launch_k(c->pdl, s, k_cells, c->ntiles_cells, 256, 0, d)));
+        LAUNCH(K_CELLS, CK(c, launch_k(c->pdl, s, k_cells, c->ntiles_cells, kCellsThreads, 0, d)));
         LAUNCH(K_SCATTER, CK(c, launch_k(c->pdl, s, k_scatter, nb, 256, 0, d)));
         if (d.flags & AM_SCAN_THREAD)   // ablation: everything recomputed, no witnesses
             LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_thread, nb, 256, 0, d)));
@@ -521,7 +529,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
                 c->stream = ms;
             }
             CK(c, cudaEventRecord(c->ev_efil, c->side));
-            LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw, std::min(blocks(d.n, 16), pers), 256, 0, d)));
+            LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw, std::min(blocks(d.n, 16), (unsigned)c->scan_blocks), 256, 0, d)));
             CK(c, cudaStreamWaitEvent(s, c->ev_efil, 0));
             LAUNCH(K_UNION, CK(c, launch_k(c->pdl, s, k_union, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
         }

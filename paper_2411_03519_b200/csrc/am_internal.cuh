@@ -14,7 +14,8 @@
 namespace am {
 
 constexpr int kSmallMax = 1024;           // agents per simulation for the fused kernel
-constexpr int kCellsPerTile = 4096;       // cell-table scan tile (256 threads x 16 cells)
+constexpr int kCellsThreads = 256;        // cell-table scan: threads per tile
+constexpr int kCellsPerTile = kCellsThreads * 16;   // 16 cells (one 4x4 Morton block) per thread
 constexpr int kReadyTile = 2048;          // ready compaction tile (256 threads x 8 agents)
 constexpr int kSortTile = 8192;           // radix pass tile (1024 threads x 8 keys)
 constexpr int kMaxSortPasses = 8;
@@ -167,6 +168,7 @@ struct am_ctx {
     int cell = 0;
     int small_threads = 32;
     int num_sms = 148;
+    int scan_blocks = 148 * 4;       // resident blocks of k_scan_hw (occupancy x SMs)
     int sort_ctas = 16;              // persistent CTAs of each radix pass
     int sort_passes_max = 1;
     cudaStream_t side = nullptr;     // edge filter (beside the scan) and priority sort (beside

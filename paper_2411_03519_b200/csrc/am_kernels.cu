@@ -125,25 +125,32 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
         }
         if (run) atomicAdd(&ctl->acc_running, run);
     }
-    if (finish_block(&ctl->ingest, gridDim.x) && threadIdx.x == 0) {
-        const int e = *(volatile int*)&ctl->err_new;
-        if (e == 0) {
-            if (mode != 0) ctl->full = 1;
-            ctl->cur = c ^ 1u;
-            ctl->W = *(volatile int*)&ctl->acc_W;
-            ctl->S = *(volatile int*)&ctl->acc_S;
-            ctl->n_active = *(volatile int*)&ctl->acc_active;
-            ctl->n_running = *(volatile int*)&ctl->acc_running;
-        } else {
-            ctl->err_sticky |= e;
-        }
-        ctl->err_new = 0;
-        ctl->acc_W = INT_MAX;
-        ctl->acc_S = INT_MIN;
-        ctl->acc_active = 0;
-        ctl->acc_running = 0;
-        __threadfence();
+}
+
+// k_ingest_done: one thread after k_ingest: flips to the new state buffer iff no agent
+// raised an error (all-or-nothing update), publishes W / S / counts, resets the
+// accumulators.  (A separate launch instead of a last-block ticket: no per-block fence.)
+__global__ void k_ingest_done(Dev d, int mode)
+{
+    pdl_begin();
+    if (threadIdx.x != 0) return;
+    Ctl* ctl = d.ctl;
+    const int e = ctl->err_new;
+    if (e == 0) {
+        if (mode != 0) ctl->full = 1;
+        ctl->cur ^= 1u;
+        ctl->W = ctl->acc_W;
+        ctl->S = ctl->acc_S;
+        ctl->n_active = ctl->acc_active;
+        ctl->n_running = ctl->acc_running;
+    } else {
+        ctl->err_sticky |= e;
     }
+    ctl->err_new = 0;
+    ctl->acc_W = INT_MAX;
+    ctl->acc_S = INT_MIN;
+    ctl->acc_active = 0;
+    ctl->acc_running = 0;
 }
 
 // ============================================================== binned round
@@ -194,12 +201,14 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
 
 // k_cells: exclusive scan of the cell counts in Morton order -> ctab{start, min};
 // lmin1 = min over each 16-cell (4x4) block, lmin2 over each 256-cell (16x16) block;
-// resets cnt/cmin for the next round.  256 threads x 16 cells per tile.
-__global__ void __launch_bounds__(256) k_cells(Dev d)
+// resets cnt/cmin for the next round.  kCellsThreads threads x 16 cells per tile (small
+// tiles: many short look-back chains in parallel).
+__global__ void __launch_bounds__(kCellsThreads) k_cells(Dev d)
 {
     pdl_begin();
     Ctl* ctl = d.ctl;
-    __shared__ uint32_t wsum[8];
+    constexpr int kW = kCellsThreads / 32;
+    __shared__ uint32_t wsum[kW];
     __shared__ uint32_t tile_excl;
     const uint32_t tile = take_ticket(&ctl->cells);
     const uint32_t tag = ctl->epoch * 16u + 1u;
@@ -239,12 +248,12 @@ __global__ void __launch_bounds__(256) k_cells(Dev d)
     __syncthreads();
     if (w == 0) {
         uint32_t acc = 0;
-        for (int k = 0; k < 8; k++) acc += wsum[k];
+        for (int k = 0; k < kW; k++) acc += wsum[k];
         const uint32_t ex = chain_scan_warp(d.tiles_c, tile, tag, acc);
         if (t == 0) {
             tile_excl = ex;
             uint32_t a2 = 0;
-            for (int k = 0; k < 8; k++) { uint32_t v = wsum[k]; wsum[k] = a2; a2 += v; }
+            for (int k = 0; k < kW; k++) { uint32_t v = wsum[k]; wsum[k] = a2; a2 += v; }
             if (tile == gridDim.x - 1) d.ctab[d.ncells] = make_int2((int)(ex + acc), INT_MAX);
         }
     }
@@ -603,13 +612,12 @@ struct HwStats {
     uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
 };
 
-// per-warp reduction of the half-warp scan counters, one atomic per block for the items
-__device__ __forceinline__ void hw_flush_stats(const Dev& d, const HwStats& hs, int lane, uint32_t& s_items)
+// per-warp reduction of the half-warp scan counters, one atomic per warp (no block
+// barrier: a warp that is done leaves at once)
+__device__ __forceinline__ void hw_flush_stats(const Dev& d, const HwStats& hs, int lane)
 {
     const unsigned it = __reduce_add_sync(0xFFFFFFFFu, hs.nitems);
-    if (lane == 0 && it) atomicAdd(&s_items, it);
-    __syncthreads();
-    if (threadIdx.x == 0 && s_items) atomicAdd(&d.ctl->n_items, (int)s_items);
+    if (lane == 0 && it) atomicAdd(&d.ctl->n_items, (int)it);
     if (d.flags & AM_STATS) {
         const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, hs.ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, hs.ncand);
         const unsigned c3 = __reduce_add_sync(0xFFFFFFFFu, hs.nb2), c4 = __reduce_add_sync(0xFFFFFFFFu, hs.nb1);
@@ -824,13 +832,11 @@ __global__ void __launch_bounds__(256) k_scan_hw(Dev d)
     __shared__ EdgeStage s_all[8];
     __shared__ int2 s_list[16][kDirect];
     __shared__ int s_pref[kEdgeStripes + 1];
-    __shared__ uint32_t s_items;
     const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4, hw = threadIdx.x >> 4;
     const unsigned hm = 0xFFFFu << (16 * h);
     EdgeStage& sm = s_all[threadIdx.x >> 5];
     int2* list = s_list[hw];
     if (lane == 0) sm.ne = 0;
-    if (threadIdx.x == 0) s_items = 0;
     stripe_prefix(d.wq_ctr, 1 << 30, s_pref);
     const int nq = s_pref[kEdgeStripes];
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_work = nq;
@@ -866,6 +872,11 @@ __global__ void __launch_bounds__(256) k_scan_hw(Dev d)
                 cy0 = max(0, (ay - (int)Rc) >> cl); cy1 = min(G - 1, (ay + (int)Rc) >> cl);
             }
             const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
+            // row k / ncx of cell k of the box: a multiply-high by ceil(2^32 / ncx), exact
+            // for k, ncx < 2^16 (a plain division for the rare larger boxes)
+            const uint32_t rcx = ncx > 1 ? 0xFFFFFFFFu / (uint32_t)ncx + 1u : 0u;
+            const bool mulhi = ncx > 1 && ncell < 65536;
+            auto krow = [&](int k) { return ncx == 1 ? k : (mulhi ? (int)__umulhi((uint32_t)k, rcx) : k / ncx); };
             bool nblk = false;
             uint32_t wit = kSentinel;
             for (int cb = 0; cb < ncell; cb += kDirect) {   // one chunk unless cells are tiny
@@ -879,7 +890,8 @@ __global__ void __launch_bounds__(256) k_scan_hw(Dev d)
                     ent[j] = make_int2(0, INT_MAX);
                     nxt[j] = 0;
                     if (k < ncell) {
-                        const uint32_t key = morton(cx0 + k % ncx, cy0 + k / ncx);
+                        const int ky = krow(k), kx = k - ky * ncx;
+                        const uint32_t key = morton(cx0 + kx, cy0 + ky);
                         ent[j] = d.ctab[key];
                         nxt[j] = d.ctab[key + 1].x;
                     }
@@ -893,7 +905,8 @@ __global__ void __launch_bounds__(256) k_scan_hw(Dev d)
                         const int k = cb + j * 16 + l;
                         bool ok = false;
                         if (k < ncell && nxt[j] > ent[j].x) {
-                            const int cx = cx0 + k % ncx, cy = cy0 + k / ncx;
+                            const int ky = krow(k);
+                            const int cx = cx0 + (k - ky * ncx), cy = cy0 + ky;
                             const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
                             const bool isnear = box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric);
                             const int mn = ent[j].y;
@@ -930,7 +943,7 @@ __global__ void __launch_bounds__(256) k_scan_hw(Dev d)
     }
     const unsigned nf = __reduce_add_sync(0xFFFFFFFFu, nfar);
     if (lane == 0 && nf) atomicAdd((unsigned*)&d.ctl->n_far, nf);
-    hw_flush_stats(d, hs, lane, s_items);
+    hw_flush_stats(d, hs, lane);
 }
 
 // k_union: unite this round's coupling edges (carried-over + new), one thread per edge
