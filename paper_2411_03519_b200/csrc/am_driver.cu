@@ -249,7 +249,7 @@ static int enqueue_round(am_replay* rp)
     am_ctx* c = rp->ctx;
     const int n = c->d.n;
     const unsigned nb = (unsigned)((n + 255) / 256);
-    int rc = am_update(c, (const int32_t*)rp->r.pos, rp->r.steps);
+    int rc = am_update_binned(c, (const int32_t*)rp->r.pos, rp->r.steps);
     if (rc) return rc;
     rc = am_ready(c, rp->mask, rp->order, nullptr);
     if (rc) return rc;

@@ -9,8 +9,8 @@
 #include "am_internal.cuh"
 
 namespace am {
-__global__ void k_ingest(Dev d, const int2* npos, const int32_t* nstep, const uint8_t* nstat, int mode);
-__global__ void k_ingest_done(Dev d, int mode);
+__global__ void k_ingest(Dev d, const int2* npos, const int32_t* nstep, const uint8_t* nstat, int mode, int bin);
+__global__ void k_ingest_done(Dev d, int mode, int bin);
 __global__ void k_bin(Dev d);
 __global__ void k_cells(Dev d);
 __global__ void k_scatter(Dev d);
@@ -401,15 +401,17 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
 }
 
 
-static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, const uint8_t* st, int mode)
+static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, const uint8_t* st, int mode,
+                         bool bin = false)
 {
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
     if (c->d.n == 0) return AM_OK;
     if (!pos || !steps || (mode == 2 && !st)) return set_err(c, AM_E_ARG, "NULL array");
+    if (c->bin_pending) return set_err(c, AM_E_STATE, "update after a binned update without a round");
     am_join_side(c);
     am_prof_begin(c, K_INGEST);
-    CK(c, launch_k(c->pdl, c->stream, k_ingest, blocks(c->d.n, 256 * kIngestItems), 256, 0, c->d, (const int2*)pos, steps, st, mode));
-    CK(c, launch_k(c->pdl, c->stream, k_ingest_done, 1, 1, 0, c->d, mode));
+    CK(c, launch_k(c->pdl, c->stream, k_ingest, blocks(c->d.n, 256 * kIngestItems), 256, 0, c->d, (const int2*)pos, steps, st, mode, bin ? 1 : 0));
+    CK(c, launch_k(c->pdl, c->stream, k_ingest_done, 1, 1, 0, c->d, mode, bin ? 1 : 0));
     am_prof_end(c, K_INGEST);
     CK(c, cudaGetLastError());
     return AM_OK;
@@ -425,6 +427,17 @@ extern "C" int am_update(am_ctx* c, const int32_t* positions, const int32_t* sim
         rc = am_sync(c);  // the initial state is checked synchronously
         if (rc == AM_OK) c->first = false;
     }
+    return rc;
+}
+
+// Replay rounds (am_driver.cu): the commit update with the cell binning of the round
+// fused in (k_bin is skipped by the am_ready that must follow immediately).
+int am_update_binned(am_ctx* c, const int32_t* positions, const int32_t* sim_steps)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (c->first || c->path != 1) return am_update(c, positions, sim_steps);
+    const int rc = launch_ingest(c, positions, sim_steps, nullptr, 0, true);
+    if (rc == AM_OK) c->bin_pending = true;
     return rc;
 }
 
@@ -509,7 +522,8 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         LAUNCH(K_SMALL, CK(c, launch_k(c->pdl, s, k_small, d.n_sims, c->small_threads, 0, d, mask, order)));
     } else {
         const unsigned nb = blocks(d.n, 256);
-        LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, nb, 256, 0, d)));
+        if (!c->bin_pending) LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, nb, 256, 0, d)));
+        c->bin_pending = false;
         LAUNCH(K_CELLS, CK(c, launch_k(c->pdl, s, k_cells, c->ntiles_cells, kCellsThreads, 0, d)));
         LAUNCH(K_SCATTER, CK(c, launch_k(c->pdl, s, k_scatter, nb, 256, 0, d)));
         if (d.flags & AM_SCAN_THREAD)   // ablation: everything recomputed, no witnesses

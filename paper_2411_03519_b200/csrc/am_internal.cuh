@@ -158,6 +158,7 @@ void am_prof_end(am_ctx* c, int id);
 void am_prof_collect(am_ctx* c);
 void am_prof_mark(am_ctx* c, unsigned mask);
 void am_join_side(am_ctx* c);
+int am_update_binned(am_ctx* c, const int32_t* positions, const int32_t* sim_steps);
 
 struct am_ctx {
     am::Prof prof;
@@ -175,6 +176,7 @@ struct am_ctx {
                                      // digest/dispatch) run here
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_efil = nullptr;
     bool join_pending = false;
+    bool bin_pending = false;        // am_update_binned ran the round's k_bin already
     bool pdl = true;                 // programmatic dependent launch between round kernels
     int csort_ctas = 0;              // cluster size of the one-kernel priority sort (0 = onesweep)
     int csort_cap = 0;               // dynamic shared memory bytes per CTA of k_csort

@@ -26,7 +26,7 @@ __device__ __forceinline__ bool agent_changed(const Dev& d, uint32_t c, uint32_t
 // the last block flips cur iff no error was raised (all-or-nothing update).
 __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ npos,
                                                 const int32_t* __restrict__ nstep,
-                                                const uint8_t* __restrict__ nstat, int mode)
+                                                const uint8_t* __restrict__ nstat, int mode, int bin)
 {
     pdl_begin();
     Ctl* ctl = d.ctl;
@@ -101,6 +101,21 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
             smax = max(smax, s[k]);
         }
         run += st == ST_RUNNING;
+        if (bin) {
+            // fused k_bin (replay rounds): cell key, slot, cell min step of the new state.
+            // A rejected update leaves the round's ready set empty and forces a full
+            // recompute next round (k_ingest_done), so bins of a rejected state are harmless.
+            uint32_t key = kSentinel, rank = 0;
+            if (st != ST_DONE) {
+                key = morton((uint32_t)p[k].x >> d.clog, (uint32_t)p[k].y >> d.clog);
+                rank = atomicAdd(d.cnt + key, 1u);
+                atomicMin(d.cmin + key, s[k]);
+            }
+            d.key[i] = key;
+            d.rank[i] = rank;
+            d.bad[i] = 0;
+            d.blkid[i] = 0;
+        }
     }
     // block reduction, then one atomic per quantity per block
     __shared__ int r_err[8], r_min[8], r_max[8], r_act[8], r_run[8];
@@ -130,12 +145,13 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
 // k_ingest_done: one thread after k_ingest: flips to the new state buffer iff no agent
 // raised an error (all-or-nothing update), publishes W / S / counts, resets the
 // accumulators.  (A separate launch instead of a last-block ticket: no per-block fence.)
-__global__ void k_ingest_done(Dev d, int mode)
+__global__ void k_ingest_done(Dev d, int mode, int bin)
 {
     pdl_begin();
     if (threadIdx.x != 0) return;
     Ctl* ctl = d.ctl;
     const int e = ctl->err_new;
+    if (e != 0 && bin) ctl->full_next = 1;   // the fused bins and incremental state saw a rejected update
     if (e == 0) {
         if (mode != 0) ctl->full = 1;
         ctl->cur ^= 1u;
@@ -267,7 +283,6 @@ __global__ void __launch_bounds__(kCellsThreads) k_cells(Dev d)
         v.z = (int)run; v.w = mn[2 * k + 1]; run += cnt[2 * k + 1];
         out[k] = v;
     }
-    finish_block(&ctl->cells, gridDim.x);
 }
 
 // k_scatter: agents -> records sorted by cell (the order inside a cell is arbitrary;
@@ -960,10 +975,7 @@ __global__ void __launch_bounds__(256) k_union(Dev d)
         const uint2 e = d.nedges[(size_t)nxt * d.ecap + k];
         uf_unite(d.parent, e.x, e.y);
     }
-    if (finish_block(&d.ctl->uni, gridDim.x) && threadIdx.x == 0) {
-        d.ctl->ecur = nxt;
-        __threadfence();
-    }
+    // the lists of this round become current at the next k_round_begin
 }
 
 // k_finalize: label = root of the agent's tree (= min id of its cluster, Q10);
@@ -974,6 +986,7 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
 {
     pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) d.ctl->full = 0;   // every kernel that reads the full-round flag has run
     if (i >= d.n) return;
     const uint8_t st = d.status[d.ctl->cur][i];
     if (st == ST_DONE) return;
@@ -1127,15 +1140,20 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
         if (o) atomicOr(&ctl->sort_or, o);
         if (ncl) atomicAdd(&ctl->n_clusters, (int)ncl);
     }
-    if (finish_block(&ctl->ready, gridDim.x) && t == 0) {
-        unsigned long long o = *(volatile unsigned long long*)&ctl->sort_or;
-        int bits = o ? 64 - __clzll((long long)o) : 0;
-        int np = (bits + kRadixBits - 1) / kRadixBits;
-        ctl->npasses = np < 1 ? 1 : np;
-        ctl->sort_bits = bits;
-        ctl->sort_or = 0;
-        ctl->full = 0;
-    }
+    // no last-block epilogue: the sort derives its bit count from sort_or, k_round_begin
+    // resets the tile ticket and sort_or, k_finalize consumed the full-round flag
+}
+
+// significant bits of this round's ready keys (OR of all keys, k_ready)
+__device__ __forceinline__ int ready_key_bits(const Ctl* ctl)
+{
+    const unsigned long long o = *(volatile const unsigned long long*)&ctl->sort_or;
+    return o ? 64 - __clzll((long long)o) : 0;
+}
+__device__ __forceinline__ int onesweep_passes(const Ctl* ctl)
+{
+    const int np = (ready_key_bits(ctl) + kRadixBits - 1) / kRadixBits;
+    return np < 1 ? 1 : np;
 }
 
 // lanes of the warp holding the same digit (and validity), from kRadixBits + 1 ballots
@@ -1160,7 +1178,8 @@ __global__ void __launch_bounds__(256) k_sort_hist(Dev d, int max_passes)
     Ctl* ctl = d.ctl;
     __shared__ uint32_t h[kMaxSortPasses][kRadix];
     const int n = ctl->n_ready;
-    const int np = min(ctl->npasses, max_passes);
+    const int np = min(onesweep_passes(ctl), max_passes);
+    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->npasses = np; ctl->sort_bits = ready_key_bits(ctl); }
     for (int k = threadIdx.x; k < kMaxSortPasses * kRadix; k += blockDim.x) (&h[0][0])[k] = 0;
     __syncthreads();
     {
@@ -1224,7 +1243,7 @@ __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __
     uint32_t (*wcnt)[kRadix] = reinterpret_cast<uint32_t (*)[kRadix]>(sort_smem);
     uint32_t* goff = sort_smem + 32 * kRadix;
     const int n = ctl->n_ready;
-    const int np = ctl->npasses;
+    const int np = onesweep_passes(ctl);
     // persistent: a few CTAs take tiles in ticket order (the look-back only waits on
     // tiles that are being processed, so any grid size is deadlock-free)
     for (;;) {
@@ -1421,8 +1440,12 @@ __global__ void k_round_begin(Dev d)
     ctl->n_clusters = 0;
     ctl->n_items = 0;
     ctl->n_far = 0;
+    ctl->sort_or = 0;
+    ctl->ready.ticket = 0;   // k_ready and k_cells take tile tickets and keep no epilogue
+    ctl->cells.ticket = 0;
     ctl->full |= ctl->full_next;
     ctl->full_next = 0;
+    if (ctl->epoch > 1) ctl->ecur ^= 1u;   // last round's edge lists become current
     ctl->ccnt[ctl->ecur ^ 1u] = 0;
     ctl->ncnt[ctl->ecur ^ 1u] = 0;
     if (d.wq_ctr)

@@ -267,7 +267,9 @@ __global__ void __launch_bounds__(kCsThreads, 1) k_csort(Dev d, int32_t* __restr
     (void)smem_bytes;
     CS_STAMP(0);
     const int n = d.ctl->n_ready;
-    const int bits = d.ctl->sort_bits;
+    const unsigned long long kor = *(volatile const unsigned long long*)&d.ctl->sort_or;
+    const int bits = kor ? 64 - __clzll((long long)kor) : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { d.ctl->sort_bits = bits; d.ctl->npasses = (bits + kCsBits - 1) / kCsBits; }
     const int np = (bits + kCsBits - 1) / kCsBits;
     const int C = (int)cg::this_cluster().num_blocks();
     if (n == 0) return;
