@@ -14,6 +14,7 @@
 namespace am {
 
 constexpr int kSmallMax = 1024;           // agents per simulation for the fused kernel
+constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors up to this many tiles
 constexpr int kCellsThreads = 256;        // cell-table scan: threads per tile
 constexpr int kCellsPerTile = kCellsThreads * 16;   // 16 cells (one 4x4 Morton block) per thread
 constexpr int kReadyTile = 2048;          // ready compaction tile (256 threads x 8 agents)
@@ -403,6 +404,28 @@ __device__ __forceinline__ uint32_t chain_scan_warp(unsigned long long* tiles, u
     }
     if (lane == 0) st_relaxed(tiles + tile, tile_word(tag, 2, excl + agg));
     return excl;
+}
+
+// Reduce-all variant for grids whose tiles are all resident at once: warp 0 publishes
+// this tile's aggregate, then sums the aggregates of ALL predecessors in parallel (lane
+// k reads tiles k, k+32, ...; one round trip once they are published) instead of
+// walking a look-back chain.  Returns the exclusive prefix in every lane.  Only valid
+// when every predecessor tile is being processed concurrently (grid <= resident CTAs).
+__device__ __forceinline__ uint32_t chain_scan_all(unsigned long long* tiles, uint32_t tile, uint32_t tag,
+                                                   uint32_t agg)
+{
+    const int lane = threadIdx.x & 31;
+    tag &= 0x3FFFFFFFu;
+    if (lane == 0) st_relaxed(tiles + tile, tile_word(tag, 1, agg));
+    uint32_t sum = 0;
+    for (int j = lane; j < (int)tile; j += 32) {
+        unsigned long long w;
+        do {
+            w = ld_relaxed(tiles + j);
+        } while ((uint32_t)(w >> 34) != tag || ((uint32_t)(w >> 32) & 3u) == 0);
+        sum += (uint32_t)w;
+    }
+    return __reduce_add_sync(0xFFFFFFFFu, sum);
 }
 
 __device__ __forceinline__ uint32_t take_ticket(Chain* c)

@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(kCellsThreads) k_cells(Dev d)
     if (w == 0) {
         uint32_t acc = 0;
         for (int k = 0; k < kW; k++) acc += wsum[k];
-        const uint32_t ex = chain_scan_warp(d.tiles_c, tile, tag, acc);
+        const uint32_t ex = gridDim.x <= kScanAllTiles ? chain_scan_all(d.tiles_c, tile, tag, acc)
+                                                         : chain_scan_warp(d.tiles_c, tile, tag, acc);
         if (t == 0) {
             tile_excl = ex;
             uint32_t a2 = 0;
@@ -1104,7 +1105,8 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
     if (w == 0) {
         uint32_t acc = 0;
         for (int k = 0; k < 8; k++) acc += wsum[k];
-        const uint32_t ex = chain_scan_warp(d.tiles_r, tile, tag, acc);
+        const uint32_t ex = gridDim.x <= kScanAllTiles ? chain_scan_all(d.tiles_r, tile, tag, acc)
+                                                         : chain_scan_warp(d.tiles_r, tile, tag, acc);
         if (t == 0) {
             tile_excl = ex;
             uint32_t a2 = 0;
