@@ -103,9 +103,9 @@ typedef struct {
     int32_t path;          /* 0 = fused per-simulation kernel, 1 = cell-binned pipeline   */
     int32_t cell;          /* cell edge used by the binned pipeline                       */
     int32_t n_work;        /* binned: agents re-scanned this round (incremental work queue) */
-    int32_t n_far;         /* binned: agents that needed the far (time-dilated) phase     */
-    int32_t n_items;       /* binned: (agent, 4x4-cell block) far work items              */
-    int32_t n_edges;       /* binned: coupling edges united this round                    */
+    int32_t n_far;         /* binned: queued IDLE agents ahead of W (far blocking test due)  */
+    int32_t n_items;       /* binned: 4x4-cell blocks the far test walked in the pyramid   */
+    int32_t n_edges;       /* binned: coupling edges of this round (carried + new)        */
     int32_t n_passes;      /* binned: radix passes the priority order needed              */
 } am_round_stats;
 
@@ -193,7 +193,8 @@ const char* am_profile_name(int32_t id);
  * agents); resets them.  Synchronises. */
 int am_scan_stats(am_ctx* ctx, uint64_t* out);
 
-/* Kernel launches of one am_update + am_ready on this context (host-side count). */
+/* Kernel launches of one am_update + am_ready on this context (host-side count; a
+ * replay round on the binned path fuses two of them, see am_driver.h). */
 int32_t am_launches_per_round(const am_ctx* ctx);
 
 /* Library version string. */

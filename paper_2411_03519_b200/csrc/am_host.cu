@@ -161,7 +161,7 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 3 : 12 + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
+    return c->path == 0 ? 3 : 11 + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -517,7 +517,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         __VA_ARGS__;           \
         am_prof_end(c, id);    \
     } while (0)
-    CK(c, launch_k(c->pdl, s, k_round_begin, 1, 1, 0, d));
+    if (!c->bin_pending) CK(c, launch_k(c->pdl, s, k_round_begin, 1, 1, 0, d));   // else done by k_ingest_done
     if (c->path == 0) {
         LAUNCH(K_SMALL, CK(c, launch_k(c->pdl, s, k_small, d.n_sims, c->small_threads, 0, d, mask, order)));
     } else {
@@ -582,7 +582,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             am_prof_end(c, K_SORT_PASS);
         }
         // perception digests of the dispatched agents (replay driver)
-        if (d.flags & AM_DIGEST) CK(c, launch_k(c->pdl, s, k_digest, std::min(nb, (unsigned)c->num_sms * 2), 256, 0, d, (const int32_t*)d.rid));
+        if (d.flags & AM_DIGEST) CK(c, launch_k(c->pdl, s, k_digest, std::min(blocks(d.n, 16), (unsigned)c->num_sms * 8), 256, 0, d, (const int32_t*)d.rid));
     }
 #undef LAUNCH
     CK(c, cudaGetLastError());

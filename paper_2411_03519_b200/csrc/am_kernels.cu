@@ -142,6 +142,8 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
     }
 }
 
+__device__ void round_begin(const Dev& d);
+
 // k_ingest_done: one thread after k_ingest: flips to the new state buffer iff no agent
 // raised an error (all-or-nothing update), publishes W / S / counts, resets the
 // accumulators.  (A separate launch instead of a last-block ticket: no per-block fence.)
@@ -167,6 +169,7 @@ __global__ void k_ingest_done(Dev d, int mode, int bin)
     ctl->acc_S = INT_MIN;
     ctl->acc_active = 0;
     ctl->acc_running = 0;
+    if (bin) round_begin(d);   // replay rounds: the am_ready that follows skips k_round_begin
 }
 
 // ============================================================== binned round
@@ -998,44 +1001,73 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
     if (blk || st == ST_RUNNING) d.bad[root] = 1;
 }
 
-__device__ void digest_one(const Dev& d, uint32_t aid);
-
 // k_digest: perception digests ("perceives an area within a radius") of the
 // agents dispatched this round, for the replay driver: sum over same-step non-DONE
-// agents within r_p of mix64(id<<32 ^ (u16)dx<<16 ^ (u16)dy).
-__global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict__ order)
+// agents within r_p of mix64(id<<32 ^ (u16)dx<<16 ^ (u16)dy) (order-independent).
+// One HALF-WARP per dispatched agent: lanes take the cells within r_p (one table fetch),
+// the records of the cells are flattened over the 16 lanes, partial sums are reduced.
+__global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict__ ids)
 {
     pdl_begin();
     const int nr = d.ctl->n_ready;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x)
-        digest_one(d, (uint32_t)order[k]);
-}
-__device__ void digest_one(const Dev& d, uint32_t aid)
-{
     const uint32_t c = d.ctl->cur;
-    const int2 P = d.pos[c][aid];
-    const int ax = P.x, ay = P.y, as = d.step[c][aid];
+    const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4;
+    const unsigned hm = 0xFFFFu << (16 * h);
     const int cl = d.clog, G = 1 << d.glog;
     const uint32_t Rp = (uint32_t)d.r_p, Rp2 = Rp * Rp;
-    unsigned long long dig = 0;
-    const int cx0 = max(0, (ax - (int)Rp) >> cl), cx1 = min(G - 1, (ax + (int)Rp) >> cl);
-    const int cy0 = max(0, (ay - (int)Rp) >> cl), cy1 = min(G - 1, (ay + (int)Rp) >> cl);
-    for (int cy = cy0; cy <= cy1; cy++)
-        for (int cx = cx0; cx <= cx1; cx++) {
-            if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rp, d.metric))
-                continue;
-            const uint32_t key = morton(cx, cy);
-            const int2 e = d.ctab[key];
-            if (e.y > as) continue;
-            const int e1 = d.ctab[key + 1].x;
-            for (int b = e.x; b < e1; b++) {
-                const int4 B = d.rec[b];
-                if (B.y != as || (uint32_t)B.z == aid) continue;
-                const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-                if (within2(dx, dy, Rp2, Rp, d.metric)) dig += digest_term((uint32_t)B.z, dx, dy);
+    const int hw0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 4, nhw = (gridDim.x * blockDim.x) >> 4;
+    for (int k = hw0; k < nr; k += nhw) {   // half-warp uniform
+        const uint32_t aid = (uint32_t)ids[k];
+        const int2 P = d.pos[c][aid];
+        const int ax = P.x, ay = P.y, as = d.step[c][aid];
+        const int cx0 = max(0, (ax - (int)Rp) >> cl), cx1 = min(G - 1, (ax + (int)Rp) >> cl);
+        const int cy0 = max(0, (ay - (int)Rp) >> cl), cy1 = min(G - 1, (ay + (int)Rp) >> cl);
+        const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
+        unsigned long long dig = 0;
+        for (int cb = 0; cb < ncell; cb += 16) {
+            const int q = cb + l;
+            int st0 = 0, cnt = 0;
+            if (q < ncell) {
+                const int cx = cx0 + q % ncx, cy = cy0 + q / ncx;
+                if (box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rp, d.metric)) {
+                    const uint32_t key = morton(cx, cy);
+                    const int2 e = d.ctab[key];
+                    if (e.y <= as) {
+                        st0 = e.x;
+                        cnt = d.ctab[key + 1].x - e.x;
+                    }
+                }
+            }
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+                const int y = __shfl_up_sync(hm, incl, o, 16);
+                if (l >= o) incl += y;
+            }
+            const int excl = incl - cnt;
+            const int total = __shfl_sync(hm, incl, 15, 16);
+            for (int b0 = 0; b0 < total; b0 += 16) {
+                const int tq = b0 + l;
+                int sl = 0;
+#pragma unroll
+                for (int stp = 8; stp > 0; stp >>= 1) {
+                    const int ex = __shfl_sync(hm, excl, sl + stp, 16);
+                    if (ex <= tq) sl += stp;
+                }
+                const int rs = __shfl_sync(hm, st0, sl, 16), rx = __shfl_sync(hm, excl, sl, 16);
+                if (tq < total) {
+                    const int4 B = d.rec[rs + (tq - rx)];
+                    if (B.y == as && (uint32_t)B.z != aid) {
+                        const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
+                        if (within2(dx, dy, Rp2, Rp, d.metric)) dig += digest_term((uint32_t)B.z, dx, dy);
+                    }
+                }
             }
         }
-    d.digest[aid] = dig;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) dig += __shfl_xor_sync(hm, dig, o, 16);
+        if (l == 0) d.digest[aid] = dig;
+    }
 }
 
 // k_ready: mask, DONE labels, dispatch (IDLE -> RUNNING), and the
@@ -1433,9 +1465,8 @@ __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mas
 }
 
 // reset the per-round counters that the host reads (before the round kernels)
-__global__ void k_round_begin(Dev d)
+__device__ void round_begin(const Dev& d)
 {
-    pdl_begin();
     Ctl* ctl = d.ctl;
     ctl->epoch += 1;
     ctl->n_ready = 0;
@@ -1452,6 +1483,12 @@ __global__ void k_round_begin(Dev d)
     ctl->ncnt[ctl->ecur ^ 1u] = 0;
     if (d.wq_ctr)
         for (int k = 0; k < kEdgeStripes; k++) d.wq_ctr[k] = 0;
+}
+
+__global__ void k_round_begin(Dev d)
+{
+    pdl_begin();
+    round_begin(d);
 }
 
 }  // namespace am

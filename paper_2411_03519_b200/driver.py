@@ -133,7 +133,10 @@ class Replay:
         return {self.L.am_profile_name(i).decode(): (ms[i], cnt[i]) for i in range(k)}
 
     def launches_per_round(self) -> int:
-        return int(self.L.am_launches_per_round(self.tracker.ctx)) + 3
+        # + k_disp_a, k_disp_b, k_commit; on the binned path a replay round fuses k_bin
+        # into the update and k_round_begin into k_ingest_done (am_update_binned)
+        fused = 2 if self.tracker.stats()["path"] == 1 else 0
+        return int(self.L.am_launches_per_round(self.tracker.ctx)) + 3 - fused
 
     def dispatched(self) -> int:
         v = C.c_int64(0)
