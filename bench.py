@@ -198,6 +198,62 @@ def _config(w, ws):
             "l2": "flushed between timed rounds (512 MB write)"}
 
 
+# ------------------------------------------------------------------ the other configs
+def other_configs(dev, budget_s: float = 2.0):
+    """BASELINE configs 1-4 beside the headline (C5): the GPU-resident replay of each
+    (C1/C2/C3 on the fused per-simulation kernel, C4 on the binned pipeline), timed on
+    the device with CUDA events over whole launches of rounds (no L2 flush: these are
+    latency-bound small rounds).  C1 and C3 run to completion (every agent at T=1000);
+    C2 and C4 run a bounded number of rounds after a pre-roll."""
+    import torch
+
+    import amgen
+    from paper_2411_03519_b200 import Replay
+    out = {}
+    plan = [("C1", 0, None), ("C3", 0, None), ("C2", 400, 4000), ("C4", 400, 2000)]
+    for name, preroll, rounds in plan:
+        w = amgen.config(name)
+        lm = amgen.latency_model(w.profile)
+        rep = Replay.from_workload(w, lm, device=dev)
+        st = torch.cuda.ExternalStream(rep.stream_ptr(), device=dev)
+        if preroll:
+            rep.run(preroll)
+        rep.run(8)
+        d0 = rep.dispatched()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record(st)
+        done = 0
+        if rounds is None:   # to completion
+            while True:
+                rep.launch(512)
+                done += 512
+                act, _ = rep.sync()
+                if act == 0 or time.perf_counter() - t0 > 10 * budget_s:
+                    break
+        else:
+            while done < rounds and time.perf_counter() - t0 < budget_s:
+                rep.launch(256)
+                done += 256
+            rep.sync()
+        b.record(st)
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b)
+        steps = rep.dispatched() - d0
+        res = {"agents": len(w.x), "n_sims": w.n_sims, "rounds": done,
+               "agent_steps_per_s": steps / (ms / 1e3), "rounds_per_s": done / (ms / 1e3),
+               "path": "fused per-simulation kernel" if rep.tracker.stats()["path"] == 0 else "binned"}
+        if rounds is None:
+            r = rep.results()
+            res["completed"] = bool(act == 0)
+            res["sim_rounds_per_s"] = done * w.n_sims / (ms / 1e3)
+            if act == 0:
+                res["T_ooo_s_mean"] = float(r["T_ooo"].mean()) / 1e6
+        out[name] = res
+        rep.close()
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, w, lm):
     import numpy as np
@@ -345,6 +401,24 @@ def run_ours(args, w, lm):
     except Exception:
         pass
     clocks = clk.summary()
+    # round-level HBM traffic: ncu cold-cache DRAM bytes of every kernel of a round
+    # (profiles/ncu_traffic.json) over the measured round time
+    round_hbm = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tj = json.load(f)
+        tot = sum(v["dram_bytes_per_launch"] * v.get("launches", 1) for k, v in tj.items()
+                  if isinstance(v, dict) and "dram_bytes_per_launch" in v and k not in ("k_scan", "k_near"))
+        gbs = tot / (total_ms / args.steps / 1e3) / 1e9
+        round_hbm = {"dram_bytes_per_round": tot, "achieved_gbs": gbs, "frac": gbs / peak,
+                     "compulsory_bytes_per_round": 18.0 * n,
+                     "compulsory_frac": 18.0 * n / (total_ms / args.steps / 1e3) / 1e9 / peak,
+                     "source": "ncu launch list (cold-cache DRAM bytes per kernel) / event-timed round"}
+    except Exception:
+        pass
+    others = None
+    if ws == 1 and not args.no_other_configs:
+        others = other_configs(dev)
     # the oracle on the host cores, bounded sample (rank 0, N = 1 only)
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
@@ -367,12 +441,14 @@ def run_ours(args, w, lm):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg, "avg_launch_us": avg_dom_s * 1e6},
+        "round_hbm": round_hbm,
         "kernel_share_warmup_us": {k: round(v * 1000.0, 2) for k, v in sorted(shares.items())},
         "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": 12 * n,
                 "d2h_bytes_per_step": 12 * n + n + 4 * n, "ms_per_step": e_total / args.steps},
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,
+        "other_configs": others,
     }
     print(json.dumps(line), flush=True)
     rep.close()
@@ -393,6 +469,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     import amgen
