@@ -7,5 +7,5 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_$TAG.log 2>&
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()"; echo "smoke rc=$?"
 timeout 600 python bench.py --steps 30 --warmup 5 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"; cat gpurun_out/bench_$TAG.json; tail -3 gpurun_out/bench_$TAG.err
 if [ "$2" = "ncu" ]; then
-  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 9000 -c 60 --csv --log-file gpurun_out/launches_$TAG.csv python tools/profile_round.py --preroll 400 --rounds 3 > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu rc=$?"
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_$TAG.csv python tools/profile_round.py --preroll 400 --rounds 3 --range > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu rc=$?"
 fi

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--dbg", type=lambda v: int(v, 0), default=0, help="extra AM_* flag bits")
     ap.add_argument("--scan-thread", action="store_true")
+    ap.add_argument("--range", action="store_true",
+                    help="cudaProfilerStart/Stop around the measured rounds (ncu --profile-from-start off)")
     a = ap.parse_args()
     w = amgen.config(a.workload, n=a.agents)
     lm = amgen.latency_model(w.profile)
@@ -52,6 +54,9 @@ def main():
     if a.prof:
         rep.profile((1 << 15) - 1)
     rows = []
+    if a.range:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
     for k in range(a.rounds):
         rep.launch(1)
         act, nr = rep.sync()
@@ -63,6 +68,9 @@ def main():
             row.update({k2: v / max(1, st["n_active"]) for k2, v in sc.items()})
         rows.append(row)
         print(json.dumps(row), flush=True)
+    if a.range:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
     if a.prof:
         pr = rep.profile_read()
         print(json.dumps({k: round(v[0] / v[1] * 1000, 2) for k, v in pr.items() if v[1]}), flush=True)
