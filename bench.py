@@ -254,6 +254,47 @@ def other_configs(dev, budget_s: float = 2.0):
     return out
 
 
+def snapshot_rounds(rep, w, dev, flush, reps: int = 20):
+    """SURVEY 8(d.1) C5 "snapshot rounds/s": the state the replay pre-roll reached is
+    loaded into a fresh tracker with am_set_state (which forces every verdict, coupling
+    edge and cluster to be recomputed: no incremental reuse) and one full am_ready
+    round (AM_PEEK, nothing dispatched) is timed with CUDA events, L2 flushed before
+    each.  Returns rounds/s, the full-round time and its per-round statistics."""
+    import torch
+
+    from paper_2411_03519_b200 import Tracker
+    pos, steps = rep.pos.clone(), rep.steps.clone()
+    status = rep.tracker.status().clone()
+    n = pos.shape[0]
+    tr = Tracker(w.map_w, w.map_h, 4, 1, n, target=w.steps, peek=True, validate=False,
+                 force="binned", device=dev)
+    s = torch.cuda.current_stream(dev)
+    mask = torch.empty(n, dtype=torch.uint8, device=dev)
+    order = torch.empty(n, dtype=torch.int32, device=dev)
+    for _ in range(3):
+        tr.set_state(pos, steps, status)
+        tr.ready(mask, order)
+    ts = []
+    for k in range(reps):
+        tr.set_state(pos, steps, status)
+        flush.fill_(k & 0xFF)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        tr.ready_async(mask, order)
+        e1.record(s)
+        tr.sync()
+        ts.append(e0.elapsed_time(e1))
+    st = tr.stats()
+    tr.close()
+    ts.sort()
+    med = ts[len(ts) // 2]
+    return {"rounds_per_s": 1e3 / med, "ms_per_round_median": med, "ms_per_round_min": ts[0],
+            "rounds": reps, "agents": n, "ready": st["n_ready"], "scanned": st["n_work"],
+            "far": st["n_far"], "edges": st["n_edges"],
+            "what": "full (non-incremental) am_ready round on the pre-rolled C5 state, AM_PEEK, "
+                    "L2 flushed before each round"}
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, w, lm):
     import numpy as np
@@ -370,6 +411,8 @@ def run_ours(args, w, lm):
         pg.all_reduce(t[1:], op=pg.ReduceOp.SUM)
         e_value = float(t[1]) / (float(tm[0]) / 1000.0)
 
+    snap = snapshot_rounds(rep, w, dev, flush) if not args.no_snapshot else None
+
     if rank != 0:
         rep.close()
         if pg:
@@ -442,6 +485,7 @@ def run_ours(args, w, lm):
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg, "avg_launch_us": avg_dom_s * 1e6},
         "round_hbm": round_hbm,
+        "snapshot": snap,
         "kernel_share_warmup_us": {k: round(v * 1000.0, 2) for k, v in sorted(shares.items())},
         "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": 12 * n,
                 "d2h_bytes_per_step": 12 * n + n + 4 * n, "ms_per_step": e_total / args.steps},
@@ -470,6 +514,7 @@ def main():
     ap.add_argument("--ref-step-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
+    ap.add_argument("--no-snapshot", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     import amgen

@@ -101,7 +101,8 @@ SIGNATURES = {
 
 
 def lib_path() -> str:
-    return _build.LIB
+    v = os.environ.get("AM_LIB_VARIANT")   # experiment builds only (tools/ab_round.py)
+    return os.path.join(_build.PKG, f"libametro_{v}.so") if v else _build.LIB
 
 
 def load(build_if_stale: bool = False):

@@ -258,6 +258,7 @@ static int enqueue_round(am_replay* rp)
     const unsigned nbd = std::min(nb, (unsigned)c->num_sms * 4);   // grid-stride over the ready list
     RK(launch_k(c->pdl, rp->stream, k_disp_a, nbd, 256, 0, rp->r));
     am_prof_end(c, K_DISP_A);
+    am_join_digest(c);   // part b reads the digests (computed beside part a)
     am_prof_begin(c, K_DISP_B);
     RK(launch_k(c->pdl, rp->stream, k_disp_b, nbd, 256, 0, rp->r));
     am_prof_end(c, K_DISP_B);

@@ -308,7 +308,8 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     }
     x->ntiles_sort = (int)blocks(n, kSortTile);
     x->ntiles_ready = (int)blocks(n, kReadyTile);
-    x->ntiles_cells = d.ncells / kCellsPerTile;
+    x->cells_threads = (int)std::min<long long>(kCellsThreads, d.ncells / 16);
+    x->ntiles_cells = (int)(d.ncells / (16LL * x->cells_threads));
 
     // workspace layout
     size_t off = 0;
@@ -351,6 +352,8 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_efil, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&x->side2, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_dig, cudaEventDisableTiming);
         if (e != cudaSuccess) { cudaFree(x->ws); delete x; return cuda_err(nullptr, e, "am_init: side stream"); }
     }
     e = cudaMallocHost((void**)&x->h_ctl, sizeof(Ctl));
@@ -468,9 +471,19 @@ static void fill_stats(am_ctx* c)
     c->stats.n_passes = h.npasses;
 }
 
+// the main stream waits for the perception digests of the last round (side2)
+void am_join_digest(am_ctx* c)
+{
+    if (c->dig_pending) {
+        cudaStreamWaitEvent(c->stream, c->ev_dig, 0);
+        c->dig_pending = false;
+    }
+}
+
 // the main stream waits for the side-stream sort of the last round
 void am_join_side(am_ctx* c)
 {
+    am_join_digest(c);
     if (c->join_pending) {
         cudaStreamWaitEvent(c->stream, c->ev_join, 0);
         c->join_pending = false;
@@ -524,7 +537,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         const unsigned nb = blocks(d.n, 256);
         if (!c->bin_pending) LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, nb, 256, 0, d)));
         c->bin_pending = false;
-        LAUNCH(K_CELLS, CK(c, launch_k(c->pdl, s, k_cells, c->ntiles_cells, kCellsThreads, 0, d)));
+        LAUNCH(K_CELLS, CK(c, launch_k(c->pdl, s, k_cells, c->ntiles_cells, c->cells_threads, 0, d)));
         LAUNCH(K_SCATTER, CK(c, launch_k(c->pdl, s, k_scatter, nb, 256, 0, d)));
         if (d.flags & AM_SCAN_THREAD)   // ablation: everything recomputed, no witnesses
             LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_thread, nb, 256, 0, d)));
@@ -547,8 +560,8 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             CK(c, cudaStreamWaitEvent(s, c->ev_efil, 0));
             LAUNCH(K_UNION, CK(c, launch_k(c->pdl, s, k_union, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
         }
-        LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, nb, 256, 0, d)));
-        LAUNCH(K_READY, CK(c, launch_k(c->pdl, s, k_ready, c->ntiles_ready, 256, 0, d, mask)));
+        LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, blocks(d.n, 256 * kFinItems), 256, 0, d)));
+        LAUNCH(K_READY, CK(c, launch_k(c->pdl, s, k_ready, c->ntiles_ready, kReadyThreads, 0, d, mask)));
         if (c->csort_ctas) {
             // one cluster of csort_ctas CTAs sorts the whole ready set (am_sort.cu), on the
             // side stream: nothing else in the round reads `order` (digests and dispatch
@@ -581,8 +594,17 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
                 CK(c, launch_k(c->pdl, s, k_sort_pass, std::min(c->ntiles_sort, c->sort_ctas), 1024, kSortSmem, d, p, order, c->ntiles_sort));
             am_prof_end(c, K_SORT_PASS);
         }
-        // perception digests of the dispatched agents (replay driver)
-        if (d.flags & AM_DIGEST) CK(c, launch_k(c->pdl, s, k_digest, std::min(blocks(d.n, 16), (unsigned)c->num_sms * 8), 256, 0, d, (const int32_t*)d.rid));
+        // perception digests of the dispatched agents (replay driver), on a second side
+        // stream forked after k_ready: they overlap the driver's dispatch part a, which
+        // does not read them; the driver joins them (am_join_digest) before part b
+        if (d.flags & AM_DIGEST) {
+            CK(c, cudaEventRecord(c->ev_fork, s));
+            CK(c, cudaStreamWaitEvent(c->side2, c->ev_fork, 0));
+            CK(c, launch_k(false, c->side2, k_digest, std::min(blocks(d.n, 16), (unsigned)c->num_sms * 8), 256, 0, d,
+                           (const int32_t*)d.rid));
+            CK(c, cudaEventRecord(c->ev_dig, c->side2));
+            c->dig_pending = true;
+        }
     }
 #undef LAUNCH
     CK(c, cudaGetLastError());
@@ -676,6 +698,9 @@ extern "C" int am_destroy(am_ctx* c)
         cudaEventDestroy(c->ev_fork);
         cudaEventDestroy(c->ev_join);
         cudaEventDestroy(c->ev_efil);
+        cudaStreamSynchronize(c->side2);
+        cudaStreamDestroy(c->side2);
+        cudaEventDestroy(c->ev_dig);
     }
     cudaFree(c->ws);
     cudaFreeHost(c->h_ctl);

@@ -15,14 +15,31 @@ namespace am {
 
 constexpr int kSmallMax = 1024;           // agents per simulation for the fused kernel
 constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors up to this many tiles
-constexpr int kCellsThreads = 256;        // cell-table scan: threads per tile
-constexpr int kCellsPerTile = kCellsThreads * 16;   // 16 cells (one 4x4 Morton block) per thread
-constexpr int kReadyTile = 2048;          // ready compaction tile (256 threads x 8 agents)
+#ifndef AM_CELLS_THREADS
+#define AM_CELLS_THREADS 512
+#endif
+#ifndef AM_READY_ITEMS
+#define AM_READY_ITEMS 8
+#endif
+#ifndef AM_READY_THREADS
+#define AM_READY_THREADS 1024
+#endif
+#ifndef AM_FIN_ITEMS
+#define AM_FIN_ITEMS 4
+#endif
+#ifndef AM_INGEST_ITEMS
+#define AM_INGEST_ITEMS 4
+#endif
+constexpr int kCellsThreads = AM_CELLS_THREADS;   // cell-table scan: threads per tile
+constexpr int kReadyItems = AM_READY_ITEMS;   // agents per thread of the ready compaction
+constexpr int kReadyThreads = AM_READY_THREADS;   // threads per ready compaction tile
+constexpr int kReadyTile = kReadyThreads * kReadyItems;
 constexpr int kSortTile = 8192;           // radix pass tile (1024 threads x 8 keys)
 constexpr int kMaxSortPasses = 8;
 constexpr int kRadixBits = 9;            // radix digit width of the priority sort
 constexpr int kRadix = 1 << kRadixBits;
-constexpr int kIngestItems = 4;           // agents per thread in k_ingest / k_commit
+constexpr int kFinItems = AM_FIN_ITEMS;         // agents per thread in k_finalize
+constexpr int kIngestItems = AM_INGEST_ITEMS;   // agents per thread in k_ingest / k_commit
 constexpr int kEdgeStripes = 64;          // striped queues (one atomic counter per stripe)
 constexpr int kEdgeStage = 128;           // coupling edges staged per warp before appending
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
@@ -159,6 +176,7 @@ void am_prof_end(am_ctx* c, int id);
 void am_prof_collect(am_ctx* c);
 void am_prof_mark(am_ctx* c, unsigned mask);
 void am_join_side(am_ctx* c);
+void am_join_digest(am_ctx* c);
 int am_update_binned(am_ctx* c, const int32_t* positions, const int32_t* sim_steps);
 
 struct am_ctx {
@@ -177,6 +195,9 @@ struct am_ctx {
                                      // digest/dispatch) run here
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_efil = nullptr;
     bool join_pending = false;
+    cudaStream_t side2 = nullptr;    // perception digests (beside the driver's dispatch part a)
+    cudaEvent_t ev_dig = nullptr;
+    bool dig_pending = false;
     bool bin_pending = false;        // am_update_binned ran the round's k_bin already
     bool pdl = true;                 // programmatic dependent launch between round kernels
     int csort_ctas = 0;              // cluster size of the one-kernel priority sort (0 = onesweep)
@@ -184,6 +205,7 @@ struct am_ctx {
     int ntiles_sort = 1;
     int ntiles_ready = 1;
     int ntiles_cells = 1;
+    int cells_threads = 256;   // k_cells block size (16 cells per thread)
     bool first = true;
     bool have_round = false;
     void* ws = nullptr;

@@ -226,13 +226,13 @@ __global__ void __launch_bounds__(kCellsThreads) k_cells(Dev d)
 {
     pdl_begin();
     Ctl* ctl = d.ctl;
-    constexpr int kW = kCellsThreads / 32;
-    __shared__ uint32_t wsum[kW];
+    const int kW = blockDim.x >> 5;   // tile = blockDim.x threads x 16 cells (host: <= kCellsThreads)
+    __shared__ uint32_t wsum[kCellsThreads / 32];
     __shared__ uint32_t tile_excl;
     const uint32_t tile = take_ticket(&ctl->cells);
     const uint32_t tag = ctl->epoch * 16u + 1u;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const long long base = (long long)tile * kCellsPerTile + t * 16;
+    const long long base = (long long)tile * (blockDim.x * 16) + t * 16;
     uint4* cnt4 = reinterpret_cast<uint4*>(d.cnt + base);
     int4* min4 = reinterpret_cast<int4*>(d.cmin + base);
     uint32_t cnt[16];
@@ -989,16 +989,36 @@ __global__ void __launch_bounds__(256) k_union(Dev d)
 __global__ void __launch_bounds__(256) k_finalize(Dev d)
 {
     pdl_begin();
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) d.ctl->full = 0;   // every kernel that reads the full-round flag has run
-    if (i >= d.n) return;
-    const uint8_t st = d.status[d.ctl->cur][i];
-    if (st == ST_DONE) return;
-    const uint32_t root = uf_find(d.parent, (uint32_t)i);
-    d.labels[i] = (int32_t)root;
-    const bool blk = st == ST_IDLE && d.v8[i] == 1;
-    d.blkid[i] = blk;
-    if (blk || st == ST_RUNNING) d.bad[root] = 1;
+    const int i0 = blockIdx.x * (256 * kFinItems) + threadIdx.x;
+    if (i0 == 0) d.ctl->full = 0;   // every kernel that reads the full-round flag has run
+    const uint32_t c = d.ctl->cur;
+    // every item's status / verdict / parent load is issued before any pointer chase
+    // (independent chains in flight; one wave of threads covers the agents)
+    uint8_t st[kFinItems], vb[kFinItems];
+    uint32_t par[kFinItems];
+#pragma unroll
+    for (int k = 0; k < kFinItems; k++) {
+        const int i = i0 + k * 256;
+        st[k] = ST_DONE;
+        vb[k] = 0;
+        par[k] = 0;
+        if (i < d.n) {
+            st[k] = d.status[c][i];
+            vb[k] = d.v8[i];
+            par[k] = ld_cg(d.parent + i);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kFinItems; k++) {
+        const int i = i0 + k * 256;
+        if (st[k] == ST_DONE) continue;
+        uint32_t root = par[k];
+        if (root != (uint32_t)i) root = uf_find(d.parent, (uint32_t)i);
+        d.labels[i] = (int32_t)root;
+        const bool blk = st[k] == ST_IDLE && vb[k] == 1;
+        d.blkid[i] = blk;
+        if (blk || st[k] == ST_RUNNING) d.bad[root] = 1;
+    }
 }
 
 // k_digest: perception digests ("perceives an area within a radius") of the
@@ -1073,11 +1093,12 @@ __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict
 // k_ready: mask, DONE labels, dispatch (IDLE -> RUNNING), and the
 // ordered compaction of the ready set: keys ((step - W) << idbits) | label, values id.
 // 256 threads x 8 consecutive agents per tile; chained scan keeps id order.
-__global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask)
+__global__ void __launch_bounds__(kReadyThreads) k_ready(Dev d, uint8_t* __restrict__ mask)
 {
     pdl_begin();
     Ctl* ctl = d.ctl;
-    __shared__ uint32_t wsum[8];
+    constexpr int kW = kReadyThreads / 32;
+    __shared__ uint32_t wsum[kW];
     __shared__ uint32_t tile_excl;
     __shared__ uint32_t ncl;
     const uint32_t tile = take_ticket(&ctl->ready);
@@ -1088,14 +1109,14 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
     const bool peek = (d.flags & AM_PEEK) != 0;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) ncl = 0;
-    const int i0 = tile * kReadyTile + t * 8;
-    uint8_t ready[8], st[8];
-    int lab[8];
+    const int i0 = tile * kReadyTile + t * kReadyItems;
+    uint8_t ready[kReadyItems], st[kReadyItems];
+    int lab[kReadyItems];
     uint32_t cnt = 0, mycl = 0;
     // loads in two independent rounds (status + label, then the roots' bad flags),
     // stores after
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
+    for (int k = 0; k < kReadyItems; k++) {
         const int i = i0 + k;
         st[k] = ST_DONE;
         lab[k] = -1;
@@ -1105,12 +1126,12 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
         }
     }
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
+    for (int k = 0; k < kReadyItems; k++) {
         ready[k] = 0;
         if (st[k] != ST_DONE && ok && st[k] == ST_IDLE) ready[k] = !d.bad[lab[k]];
     }
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
+    for (int k = 0; k < kReadyItems; k++) {
         const int i = i0 + k;
         if (i < d.n) {
             if (d.chg8) d.chg8[i] = 0;     // the round consumed this agent's change
@@ -1136,13 +1157,13 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
     if (mycl) atomicAdd(&ncl, mycl);
     if (w == 0) {
         uint32_t acc = 0;
-        for (int k = 0; k < 8; k++) acc += wsum[k];
+        for (int k = 0; k < kW; k++) acc += wsum[k];
         const uint32_t ex = gridDim.x <= kScanAllTiles ? chain_scan_all(d.tiles_r, tile, tag, acc)
                                                          : chain_scan_warp(d.tiles_r, tile, tag, acc);
         if (t == 0) {
             tile_excl = ex;
             uint32_t a2 = 0;
-            for (int k = 0; k < 8; k++) { uint32_t v = wsum[k]; wsum[k] = a2; a2 += v; }
+            for (int k = 0; k < kW; k++) { uint32_t v = wsum[k]; wsum[k] = a2; a2 += v; }
             if (tile == gridDim.x - 1) ctl->n_ready = (int)(ex + acc);
         }
     }
@@ -1150,7 +1171,7 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
     uint32_t pos = tile_excl + wsum[w] + incl - cnt;
     unsigned long long kor = 0;
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
+    for (int k = 0; k < kReadyItems; k++) {
         if (ready[k]) {
             const int i = i0 + k;
             const unsigned long long key =
@@ -1163,14 +1184,14 @@ __global__ void __launch_bounds__(256) k_ready(Dev d, uint8_t* __restrict__ mask
         }
     }
     // OR of all keys -> number of radix passes (one atomic per block)
-    __shared__ unsigned long long s_or[8];
+    __shared__ unsigned long long s_or[kW];
     unsigned lo = __reduce_or_sync(0xFFFFFFFFu, (unsigned)kor);
     unsigned hi = __reduce_or_sync(0xFFFFFFFFu, (unsigned)(kor >> 32));
     if (lane == 0) s_or[w] = ((unsigned long long)hi << 32) | lo;
     __syncthreads();
     if (t == 0) {
         unsigned long long o = 0;
-        for (int q = 0; q < 8; q++) o |= s_or[q];
+        for (int q = 0; q < kW; q++) o |= s_or[q];
         if (o) atomicOr(&ctl->sort_or, o);
         if (ncl) atomicAdd(&ctl->n_clusters, (int)ncl);
     }
