@@ -775,7 +775,13 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
 // The records of the listed cells are flattened over the 16 lanes (prefix sum of the
 // cell counts, 4-step shuffle search per lane) and tested 16 at a time; the first
 // blocker becomes A's witness.
-constexpr int kDirect = 64;    // cells of the query box resolved with one table fetch
+#ifndef AM_DIRECT
+#define AM_DIRECT 64
+#endif
+#ifndef AM_SCAN_MINB
+#define AM_SCAN_MINB 5   // 5 resident CTAs per SM (<= 51 registers; A/B: -6% round time)
+#endif
+constexpr int kDirect = AM_DIRECT;   // cells of the query box resolved with one table fetch
 
 // test the records of the cells in `list[0..nl)` (near cells first: nn of them) against
 // A; returns (in nblk/wit) the first blocker; stages coupling edges for a changed A
@@ -845,7 +851,7 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
     }
 }
 
-__global__ void __launch_bounds__(256) k_scan_hw(Dev d)
+__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
 {
     pdl_begin();
     __shared__ EdgeStage s_all[8];
