@@ -274,31 +274,31 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     x->small_threads = std::max(32, ((per_sim_max + 31) / 32) * 32);
 
     // cell size: >= R_c = r_p + v (coupling needs <= 2x2 cells), grown until the Morton
-    // grid has at most max(4N, 4096) cells and at most 4096 cells per side.
+    // grid has at most max(4N, 4096) cells and at most 4096 cells per side.  The grid is
+    // rectangular (2^gxlog x 2^gylog cells, each side >= 64 cells, mkey): a long thin map
+    // -- e.g. one spatial slab of a wide map -- gets a long thin cell table.
     long long Rc = (long long)radius_p + v_max;
+    auto gl = [&](long long extent, int cl) {
+        return ilog2_ceil(std::max(64LL, (extent + (1LL << cl) - 1) >> cl));
+    };
     int clog;
     if (c.cell) {
         clog = ilog2_ceil(c.cell);
     } else {
         clog = ilog2_ceil(std::max(1LL, Rc));
         for (;;) {
-            long long side = std::max((map_w + (1LL << clog) - 1) >> clog, (map_h + (1LL << clog) - 1) >> clog);
-            long long g = 1LL << ilog2_ceil(std::max(64LL, side));
-            if (g * g <= std::max(4 * n, 4096LL) || clog >= 15) break;
+            const long long g = 1LL << (gl(map_w, clog) + gl(map_h, clog));
+            if (g <= std::max(4 * n, 4096LL) || clog >= 15) break;
             clog++;
         }
     }
-    for (;;) {  // hard cap on the grid side
-        long long side = std::max((map_w + (1LL << clog) - 1) >> clog, (map_h + (1LL << clog) - 1) >> clog);
-        if (side <= 4096 || clog >= 15) break;
-        clog++;
-    }
-    {
-        long long side = std::max((map_w + (1LL << clog) - 1) >> clog, (map_h + (1LL << clog) - 1) >> clog);
-        d.glog = ilog2_ceil(std::max(64LL, side));
-    }
+    while (std::max(gl(map_w, clog), gl(map_h, clog)) > 12 && clog < 15) clog++;   // <= 4096 cells per side
+    d.gxlog = gl(map_w, clog);
+    d.gylog = gl(map_h, clog);
+    d.mbits = std::min(d.gxlog, d.gylog);
+    d.mxhi = d.gxlog > d.gylog ? 1 : 0;
     d.clog = clog;
-    d.ncells = 1 << (2 * d.glog);
+    d.ncells = 1 << (d.gxlog + d.gylog);
     x->cell = 1 << clog;
     d.idbits = std::max(1, ilog2_ceil(std::max(2LL, n)));
     {

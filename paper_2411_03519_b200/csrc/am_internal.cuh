@@ -88,8 +88,10 @@ struct Dev {
     int32_t n, n_sims, map_w, map_h, r_p, v, target, metric;
     uint32_t flags;
     int32_t clog;          // log2 cell edge
-    int32_t glog;          // log2 cells per side of the Morton grid
-    int32_t ncells;        // (1 << glog)^2
+    int32_t gxlog, gylog;  // log2 cells along x / y of the Morton grid (each >= 6)
+    int32_t mbits;         // min(gxlog, gylog): interleaved bits per coordinate
+    int32_t mxhi;          // 1 if x is the longer side (its extra high bits sit above)
+    int32_t ncells;        // 1 << (gxlog + gylog)
     int32_t idbits;        // bits to hold an agent id
     // double-buffered state
     int2* pos[2];
@@ -251,6 +253,19 @@ __device__ __forceinline__ uint32_t part_compact(uint32_t x)
 __device__ __forceinline__ uint32_t morton(uint32_t cx, uint32_t cy)
 {
     return part1by1(cx) | (part1by1(cy) << 1);
+}
+// Key of cell (cx, cy) of a rectangular 2^gxlog x 2^gylog grid at pyramid level lv
+// (0 = cells, 2 = 4x4-cell blocks, 4 = 16x16-cell blocks; coordinates in units of that
+// level): the low mbits - lv bits of both coordinates are interleaved (Z-order inside
+// square tiles), the longer side's remaining high bits sit above them.  Aligned 4x4 /
+// 16x16 blocks are therefore contiguous key ranges, and key_lv(c) >> 4 = key_{lv+2}(c >> 2)
+// (mbits >= 6).  A square grid gives the plain Morton key.
+__device__ __forceinline__ uint32_t mkey(const Dev& d, uint32_t cx, uint32_t cy, int lv)
+{
+    const int m = d.mbits - lv;
+    const uint32_t lo = (1u << m) - 1u;
+    const uint32_t hi = (d.mxhi ? cx : cy) >> m;
+    return part1by1(cx & lo) | (part1by1(cy & lo) << 1) | (hi << (2 * m));
 }
 
 // blocking radius clamped so that R^2 fits in 31 bits; exact because the

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
             // recompute next round (k_ingest_done), so bins of a rejected state are harmless.
             uint32_t key = kSentinel, rank = 0;
             if (st != ST_DONE) {
-                key = morton((uint32_t)p[k].x >> d.clog, (uint32_t)p[k].y >> d.clog);
+                key = mkey(d, (uint32_t)p[k].x >> d.clog, (uint32_t)p[k].y >> d.clog, 0);
                 rank = atomicAdd(d.cnt + key, 1u);
                 atomicMin(d.cmin + key, s[k]);
             }
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
         const int s = d.step[c][i];
         uint32_t key = kSentinel, rank = 0;
         if (st != ST_DONE) {
-            key = morton((uint32_t)p.x >> d.clog, (uint32_t)p.y >> d.clog);
+            key = mkey(d, (uint32_t)p.x >> d.clog, (uint32_t)p.y >> d.clog, 0);
             rank = atomicAdd(d.cnt + key, 1u);
             atomicMin(d.cmin + key, s);
         }
@@ -381,19 +381,19 @@ __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
         const int4 A = d.rec[r];
         const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
         const uint32_t aid = (uint32_t)A.z;
-        const int cl = d.clog, G = 1 << d.glog;
+        const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
         const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
         unsigned long long dig = 0;
         // ---- phase 1
         {
-            const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(G - 1, (ax + (int)Rc) >> cl);
-            const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(G - 1, (ay + (int)Rc) >> cl);
+            const int cx0 = max(0, (ax - (int)Rc) >> cl), cx1 = min(Gx - 1, (ax + (int)Rc) >> cl);
+            const int cy0 = max(0, (ay - (int)Rc) >> cl), cy1 = min(Gy - 1, (ay + (int)Rc) >> cl);
             for (int cy = cy0; cy <= cy1; cy++)
                 for (int cx = cx0; cx <= cx1; cx++) {
                     if (!box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1,
                                     ((cy + 1) << cl) - 1, Rc, d.metric))
                         continue;
-                    const uint32_t key = morton(cx, cy);
+                    const uint32_t key = mkey(d, cx, cy, 0);
                     ncells++;
                     if (d.ctab[key].y > as) continue;
                     blocked = scan_cell<true>(d, key, ax, ay, as, aid, blocked, Rc, dig, ncand);
@@ -405,12 +405,12 @@ __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
             np2 = 1;
             const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
             const int l2 = cl + 4;  // 16 cells per side
-            const int G2 = G >> 4;
-            const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
-            const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
+            const int G2x = Gx >> 4, G2y = Gy >> 4;
+            const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2x - 1, (ax + R) >> l2);
+            const int by0 = max(0, (ay - R) >> l2), by1 = min(G2y - 1, (ay + R) >> l2);
             for (int by = by0; by <= by1 && !blocked; by++)
                 for (int bx = bx0; bx <= bx1 && !blocked; bx++) {
-                    const int m2 = d.lmin2[morton(bx, by)];
+                    const int m2 = d.lmin2[mkey(d, bx, by, 4)];
                     nb2++;
                     if (m2 >= as) continue;
                     if (!box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
                         for (int sx = 0; sx < 4 && !blocked; sx++) {
                             const int qx = bx * 4 + sx, qy = by * 4 + sy;  // 4x4-cell block
                             const int l1 = cl + 2;
-                            const int m1 = d.lmin1[morton(qx, qy)];
+                            const int m1 = d.lmin1[mkey(d, qx, qy, 2)];
                             nb1++;
                             if (m1 >= as) continue;
                             if (!box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
                                     const int x1 = ((cx + 1) << cl) - 1, y1 = ((cy + 1) << cl) - 1;
                                     // phase-1 cells were tested completely already
                                     if (box_within(ax, ay, x0, y0, x1, y1, Rc, d.metric)) continue;
-                                    const uint32_t key = morton(cx, cy);
+                                    const uint32_t key = mkey(d, cx, cy, 0);
                                     const int m0 = d.ctab[key].y;
                                     ncells++;
                                     if (m0 >= as) continue;
@@ -664,7 +664,7 @@ __device__ __forceinline__ void hw_flush_stats(const Dev& d, const HwStats& hs, 
 __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as, int W, int l, int h, unsigned hm,
                                            int ox_l, int oy_l, HwStats& hs)
 {
-    const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2 = (1 << d.glog) >> 4;
+    const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2x = (1 << d.gxlog) >> 4, G2y = (1 << d.gylog) >> 4;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
     const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
     uint32_t& ncells = hs.ncells;
@@ -673,8 +673,8 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
     uint32_t& nb1 = hs.nb1;
     uint32_t& nitems = hs.nitems;
     const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
-    const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2 - 1, (ax + R) >> l2);
-    const int by0 = max(0, (ay - R) >> l2), by1 = min(G2 - 1, (ay + R) >> l2);
+    const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2x - 1, (ax + R) >> l2);
+    const int by0 = max(0, (ay - R) >> l2), by1 = min(G2y - 1, (ay + R) >> l2);
     const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);
     uint32_t wit = kSentinel;
     nb2 += l == 0 ? (uint32_t)nb : 0u;
@@ -684,7 +684,7 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
         const int bx = bx0 + j % nbx, by = by0 + j / nbx;
         bool ok2 = false;
         if (j < nb) {
-            const int m2 = __ldg(d.lmin2 + morton(bx, by));
+            const int m2 = __ldg(d.lmin2 + mkey(d, bx, by, 4));
             ok2 = m2 < as && box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
                                         rb_radius((long long)as - m2, d.v, d.r_p), d.metric);
         }
@@ -693,7 +693,7 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
             const int jj = __ffs(mask2) - 1;
             mask2 &= mask2 - 1;
             const int bxj = __shfl_sync(hm, bx, jj, 16), byj = __shfl_sync(hm, by, jj, 16);
-            const uint32_t k2 = morton(bxj, byj);
+            const uint32_t k2 = mkey(d, bxj, byj, 4);
             nb1 += l == 0 ? 16u : 0u;
             // level 1: lane l tests child l (4x4 cells)
             const int qx = bxj * 4 + ox_l, qy = byj * 4 + oy_l;
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
     const int nq = s_pref[kEdgeStripes];
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_work = nq;
     const int W = d.ctl->W;
-    const int cl = d.clog, G = 1 << d.glog;
+    const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
     int ox_l, oy_l;
     morton_child(l, ox_l, oy_l);
@@ -889,12 +889,12 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
             nfar += (far && l == 0) ? 1u : 0u;
             // query box: far radius when the far test is due and the box is small enough
             const int Rf = far ? (int)rb_radius((long long)as - W, d.v, d.r_p) : (int)Rc;
-            int cx0 = max(0, (ax - Rf) >> cl), cx1 = min(G - 1, (ax + Rf) >> cl);
-            int cy0 = max(0, (ay - Rf) >> cl), cy1 = min(G - 1, (ay + Rf) >> cl);
+            int cx0 = max(0, (ax - Rf) >> cl), cx1 = min(Gx - 1, (ax + Rf) >> cl);
+            int cy0 = max(0, (ay - Rf) >> cl), cy1 = min(Gy - 1, (ay + Rf) >> cl);
             const bool direct = (cx1 - cx0 + 1) * (cy1 - cy0 + 1) <= kDirect;
             if (!direct) {   // near cells only; the far test walks the pyramid below
-                cx0 = max(0, (ax - (int)Rc) >> cl); cx1 = min(G - 1, (ax + (int)Rc) >> cl);
-                cy0 = max(0, (ay - (int)Rc) >> cl); cy1 = min(G - 1, (ay + (int)Rc) >> cl);
+                cx0 = max(0, (ax - (int)Rc) >> cl); cx1 = min(Gx - 1, (ax + (int)Rc) >> cl);
+                cy0 = max(0, (ay - (int)Rc) >> cl); cy1 = min(Gy - 1, (ay + (int)Rc) >> cl);
             }
             const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
             // row k / ncx of cell k of the box: a multiply-high by ceil(2^32 / ncx), exact
@@ -916,7 +916,7 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
                     nxt[j] = 0;
                     if (k < ncell) {
                         const int ky = krow(k), kx = k - ky * ncx;
-                        const uint32_t key = morton(cx0 + kx, cy0 + ky);
+                        const uint32_t key = mkey(d, cx0 + kx, cy0 + ky, 0);
                         ent[j] = d.ctab[key];
                         nxt[j] = d.ctab[key + 1].x;
                     }
@@ -1039,15 +1039,15 @@ __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict
     const uint32_t c = d.ctl->cur;
     const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4;
     const unsigned hm = 0xFFFFu << (16 * h);
-    const int cl = d.clog, G = 1 << d.glog;
+    const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
     const uint32_t Rp = (uint32_t)d.r_p, Rp2 = Rp * Rp;
     const int hw0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 4, nhw = (gridDim.x * blockDim.x) >> 4;
     for (int k = hw0; k < nr; k += nhw) {   // half-warp uniform
         const uint32_t aid = (uint32_t)ids[k];
         const int2 P = d.pos[c][aid];
         const int ax = P.x, ay = P.y, as = d.step[c][aid];
-        const int cx0 = max(0, (ax - (int)Rp) >> cl), cx1 = min(G - 1, (ax + (int)Rp) >> cl);
-        const int cy0 = max(0, (ay - (int)Rp) >> cl), cy1 = min(G - 1, (ay + (int)Rp) >> cl);
+        const int cx0 = max(0, (ax - (int)Rp) >> cl), cx1 = min(Gx - 1, (ax + (int)Rp) >> cl);
+        const int cy0 = max(0, (ay - (int)Rp) >> cl), cy1 = min(Gy - 1, (ay + (int)Rp) >> cl);
         const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
         unsigned long long dig = 0;
         for (int cb = 0; cb < ncell; cb += 16) {
@@ -1056,7 +1056,7 @@ __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict
             if (q < ncell) {
                 const int cx = cx0 + q % ncx, cy = cy0 + q / ncx;
                 if (box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rp, d.metric)) {
-                    const uint32_t key = morton(cx, cy);
+                    const uint32_t key = mkey(d, cx, cy, 0);
                     const int2 e = d.ctab[key];
                     if (e.y <= as) {
                         st0 = e.x;

@@ -60,14 +60,18 @@ class SlabRank:
         self.n = int(self.gid.numel())
         self.ghost_cap = int(ghost_cap or max(4096, self.n // 2))
         self.halo_cap = max(1024, self.n)
+        # the local tracker spans only this slab's rows plus a halo window of H rows on
+        # each side (slab-local cell table); H grows when the round's halo radius does
+        self.lo, self.hi = slab_of_rows(map_h, n_slabs)[my_slab]
+        self.H = 0
+        self.tracker = None
         self._alloc()
         self.stream = torch.cuda.current_stream(self.dev).cuda_stream
 
     def _alloc(self):
         d, G = self.dev, self.G
         self.n_cap = self.n + self.ghost_cap
-        self.tracker = Tracker(self.map_w, self.map_h, self.r_p, self.v, self.n_cap, cell=self.cell,
-                               metric=self.metric, validate=False, peek=True, force="binned", device=d)
+        self._make_tracker()
         self.ws = torch.empty(2, dtype=torch.int32, device=d)
         self.send = torch.empty((G, self.halo_cap, 4), dtype=torch.int32, device=d)
         self.counts = torch.zeros(G, dtype=torch.int32, device=d)
@@ -89,6 +93,28 @@ class SlabRank:
         self.out_label = torch.empty(max(self.n, 1), dtype=torch.int32, device=d)
         self.out_mask = torch.empty(max(self.n, 1), dtype=torch.uint8, device=d)
         self.out_key = torch.empty(max(self.n, 1), dtype=torch.int64, device=d)
+
+    def _make_tracker(self):
+        """Local tracker over rows [y0, y1) = this slab +- H halo rows (translated to
+        y - y0: distances, hence every result, are translation invariant)."""
+        if self.tracker is not None:
+            self.tracker.close()
+        self.y0 = max(0, self.lo - self.H)
+        self.y1 = min(self.map_h, self.hi + self.H)
+        self.tracker = Tracker(self.map_w, max(1, self.y1 - self.y0), self.r_p, self.v, self.n_cap, cell=self.cell,
+                               metric=self.metric, validate=False, peek=True, force="binned", device=self.dev)
+
+    def _window(self, ws_global: torch.Tensor):
+        """Grow the halo window to the round's halo radius R_b(S - W) (every ghost lies
+        within it of this slab, am_slab.h) with 2x slack."""
+        W, negS = ws_global.tolist()
+        if W == INT32_MAX:
+            return
+        lag = max(0, -negS - W)
+        rh = min(self.map_h, (lag + 1) * self.v + self.r_p + 1)
+        if rh > self.H and (self.lo - self.H > 0 or self.hi + self.H < self.map_h):
+            self.H = min(self.map_h, 2 * rh)
+            self._make_tracker()
 
     # ------------------------------------------------------------------ phases
     def p1_watermark(self) -> torch.Tensor:
@@ -115,6 +141,7 @@ class SlabRank:
             self.ghost_cap = 2 * (self.n + m)
             self._alloc()
         n, nl = self.n, self.n + m
+        self._window(self.ws)
         self.lpos[:n] = self.pos
         self.lsteps[:n] = self.steps
         self.lstatus[:n] = self.status
@@ -129,6 +156,8 @@ class SlabRank:
         self.lstatus[nl:] = DONE
         self.lsteps[nl:] = 0
         self.lpos[nl:] = 0
+        if self.y0:
+            self.lpos[:nl, 1] -= self.y0
         tr = self.tracker
         tr.set_state(self.lpos, self.lsteps, self.lstatus)
         tr.ready()
@@ -166,8 +195,10 @@ class SlabRank:
 
 
 # ---------------------------------------------------------------------- drivers
-def round_loopback(ranks: list[SlabRank]):
-    """Virtual slabs in one process: the exchanges are in-device copies."""
+def round_loopback(ranks: list[SlabRank], timings: list | None = None):
+    """Virtual slabs in one process: the exchanges are in-device copies.  With
+    `timings` (a list), the device time of every slab's local round (phase 3) is
+    appended to it in ms (CUDA events; what one GPU would spend on its slab)."""
     ws = torch.stack([r.p1_watermark() for r in ranks]).min(0).values
     outgoing = [r.p2_halo(ws) for r in ranks]
     recs = []
@@ -175,7 +206,17 @@ def round_loopback(ranks: list[SlabRank]):
         k = r.g.my_slab
         parts = [outgoing[j][k] for j in range(len(ranks)) if j != k]
         recs.append(torch.cat(parts) if parts else torch.empty((0, 4), dtype=torch.int32, device=r.dev))
-    lb = [r.p3_local(g) for r, g in zip(ranks, recs)]
+    lb = []
+    for r, g in zip(ranks, recs):
+        if timings is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            lb.append(r.p3_local(g))
+            e1.record()
+            e1.synchronize()
+            timings.append(e0.elapsed_time(e1))
+        else:
+            lb.append(r.p3_local(g))
     links = torch.cat([x[0] for x in lb])
     bads = torch.cat([x[1] for x in lb])
     return [r.p4_merge(links, bads, ws) for r in ranks]

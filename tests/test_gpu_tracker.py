@@ -126,6 +126,45 @@ def test_cell_size_does_not_change_results(cell):
     _compare(g, r, st)
 
 
+RECT = [
+    # n, map_w, map_h, r_p, v, max_step, seed: rectangular Morton grids (mkey), both orientations
+    (3000, 2000, 64, 4, 1, 5, 21),
+    (3000, 64, 2500, 4, 1, 5, 22),
+    (8000, 5000, 300, 4, 1, 30, 23),
+    (4000, 1000, 130, 12, 3, 8, 24),
+]
+
+
+@pytest.mark.parametrize("case", RECT, ids=[f"{c[1]}x{c[2]}" for c in RECT])
+@pytest.mark.parametrize("cell", [0, 2, 16])
+def test_rectangular_maps_vs_oracle(case, cell):
+    n, w, h, r_p, v, ms, seed = case
+    target = ms + 1
+    x, y, s, st = amgen.random_state(n, w, h, seed, max_step=ms, p_running=0.2)
+    p = O.params(w, h, r_p, v, target)
+    st_o = st.copy()
+    r = O.round_(p, x, y, s, st_o, peek=False)
+    tr = Tracker(w, h, r_p, v, n, target=target, cell=cell, force="binned")
+    _compare(_gpu_round(tr, x, y, s, st), r, st_o)
+    tr.close()
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_banded_wide_thin_map(seed):
+    """A valid large-spread state on a 6000 x 96 map: the far phase walks the pyramid
+    of a 1-block-high rectangular grid."""
+    n, w, h = 12000, 6000, 96
+    x, y, s, st = amgen.banded_state(n, w, h, seed, p_running=0.3)
+    p = O.params(w, h, 4, 1, 0)
+    st_o = st.copy()
+    r = O.round_(p, x, y, s, st_o)
+    assert s.max() - s.min() > 50
+    for cell in (0, 1):
+        tr = Tracker(w, h, 4, 1, n, cell=cell, force="binned")
+        _compare(_gpu_round(tr, x, y, s, st), r, st_o)
+        tr.close()
+
+
 @pytest.mark.parametrize("seed", [0, 1])
 def test_banded_valid_state_large_spread(seed):
     """Valid states with a step spread of ~100: exercises the time-dilated

@@ -86,6 +86,12 @@ def main():
         dist.all_reduce(tm[:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
         ms, n_ready = float(tm[0]), int(t[1])
+    per_slab = None
+    if a.virtual:   # every slab's local round (phase 3) alone: the per-GPU share of a round
+        tl = []
+        for _ in range(3):
+            slabs.round_loopback(ranks, tl)
+        per_slab = [round(min(tl[k::G]), 4) for k in range(G)]
     if rank == 0:
         # single-GPU reference round on the same snapshot
         tr = Tracker(w.map_w, w.map_h, w.r_p, w.v, n, peek=True, force="binned", device=dev)
@@ -96,7 +102,10 @@ def main():
                           "virtual": bool(a.virtual), "n_gpus": ws, "agents": n,
                           "ms_per_round": ms, "ready": n_ready, "ready_single_gpu": ref_ready,
                           "agent_steps_resolved_per_s": n_ready / (ms / 1000.0),
-                          "match": n_ready == ref_ready}), flush=True)
+                          "match": n_ready == ref_ready,
+                          "local_round_ms_per_slab": per_slab,
+                          "local_rows_per_slab": [r.y1 - r.y0 for r in ranks] if a.virtual else None}),
+              flush=True)
     if dist:
         dist.destroy_process_group()
 
