@@ -168,7 +168,7 @@ __device__ __forceinline__ void rank_step(const E* src, E* dst, int tm, int shif
 }
 
 template <class E, int K>
-__device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned char* smem, int n, int np)
+__device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned char* smem, int n, int np, int bits)
 {
     cg::cluster_group cl = cg::this_cluster();
     const int C = (int)cl.num_blocks();
@@ -234,7 +234,13 @@ __device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned ch
             }
             __syncthreads();
             rank_step<E, K>(sa, sb, tm, shift, cnt, wsum);
-            rank_step<E, K>(sb, sa, tm, shift + kCsSub, cnt, wsum);
+            // the high sub-digit of the last pass may hold no key bit (C5: 27 bits ->
+            // the 4th pass sorts 3): all zero, so its stable step is the identity
+            const E* res = sb;
+            if (shift + kCsSub < bits) {
+                rank_step<E, K>(sb, sa, tm, shift + kCsSub, cnt, wsum);
+                res = sa;
+            }
             CS_STAMP(5 + 8 * p);
             {
                 const uint32_t ts = block_scan(t < kCsRadix ? ttot[t] : 0u, wsum);
@@ -242,7 +248,7 @@ __device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned ch
             }
             __syncthreads();
             for (int j = t; j < tm; j += kCsThreads) {
-                const E e = sa[j];
+                const E e = res[j];
                 const int dg = (int)((ekey(e) >> shift) & (kCsRadix - 1));
                 const uint32_t dst = base[dg] + run[dg] + (uint32_t)j - tstart[dg];
                 if (last) order[dst] = (int32_t)e.v;
@@ -281,12 +287,12 @@ __global__ void __launch_bounds__(kCsThreads, 1) k_csort(Dev d, int32_t* __restr
     // elements per thread per tile: as few as the chunk needs (shorter serial work)
     const int chunk = (n + C - 1) / C;
     if (bits <= 32) {
-        if (chunk <= 2 * kCsThreads) csort_run<E32, 2>(d, order, cs_smem, n, np);
-        else if (chunk <= 4 * kCsThreads) csort_run<E32, 4>(d, order, cs_smem, n, np);
-        else csort_run<E32, kCsK>(d, order, cs_smem, n, np);
+        if (chunk <= 2 * kCsThreads) csort_run<E32, 2>(d, order, cs_smem, n, np, bits);
+        else if (chunk <= 4 * kCsThreads) csort_run<E32, 4>(d, order, cs_smem, n, np, bits);
+        else csort_run<E32, kCsK>(d, order, cs_smem, n, np, bits);
     } else {
-        if (chunk <= 2 * kCsThreads) csort_run<E64, 2>(d, order, cs_smem, n, np);
-        else csort_run<E64, 4>(d, order, cs_smem, n, np);
+        if (chunk <= 2 * kCsThreads) csort_run<E64, 2>(d, order, cs_smem, n, np, bits);
+        else csort_run<E64, 4>(d, order, cs_smem, n, np, bits);
     }
 }
 
