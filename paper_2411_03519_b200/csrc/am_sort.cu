@@ -187,6 +187,7 @@ __device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned ch
     const int t = threadIdx.x;
     const int chunk = (n + C - 1) / C;
     const int lo = min(n, me * chunk), m = min(n, lo + chunk) - lo;
+    const bool one = m <= tile;
 
     for (int p = 0; p < np; p++) {
         CS_STAMP(1 + 8 * p);
@@ -200,11 +201,30 @@ __device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned ch
             else gload(d, p & 1, lo + i, e);
             return e;
         };
-        // ---- (1) histogram of this CTA's chunk
+        // ---- (1) histogram of this CTA's chunk.  A chunk that fits one tile (C5: ~2.6k
+        // elements per CTA) is loaded once, all of a thread's loads in flight together,
+        // straight into the tile buffer: phase (3) sorts it without reloading it
         for (int k = t; k < kCsRadix; k += kCsThreads) { hist[k] = 0; run[k] = 0; }
         __syncthreads();
-        for (int k = t; k < m; k += kCsThreads)
-            atomicAdd(&hist[(int)((ekey(load(k)) >> shift) & (kCsRadix - 1))], 1u);
+        if (one) {
+            E ev[K];
+#pragma unroll
+            for (int q = 0; q < K; q++) {
+                const int k = t + q * kCsThreads;
+                if (k < m) ev[q] = load(k);
+            }
+#pragma unroll
+            for (int q = 0; q < K; q++) {
+                const int k = t + q * kCsThreads;
+                if (k < m) {
+                    sa[k] = ev[q];
+                    atomicAdd(&hist[(int)((ekey(ev[q]) >> shift) & (kCsRadix - 1))], 1u);
+                }
+            }
+        } else {
+            for (int k = t; k < m; k += kCsThreads)
+                atomicAdd(&hist[(int)((ekey(load(k)) >> shift) & (kCsRadix - 1))], 1u);
+        }
         // ---- (2) histograms over DSMEM -> base[digit]
         CS_STAMP(2 + 8 * p);
         cl.sync();
@@ -212,10 +232,13 @@ __device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned ch
         {
             uint32_t tot = 0, before = 0;
             if (t < kCsRadix) {
-                for (int r = 0; r < C; r++) {
-                    const uint32_t x = *cl.map_shared_rank(hist + t, r);
-                    tot += x;
-                    before += r < me ? x : 0u;
+                uint32_t xs[16];   // all remote reads in flight together (C <= 16)
+#pragma unroll
+                for (int r = 0; r < 16; r++) xs[r] = r < C ? *cl.map_shared_rank(hist + t, r) : 0u;
+#pragma unroll
+                for (int r = 0; r < 16; r++) {
+                    tot += xs[r];
+                    before += r < me ? xs[r] : 0u;
                 }
             }
             const uint32_t ex = block_scan(tot, wsum);
@@ -225,12 +248,16 @@ __device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned ch
         // ---- (3) + (4) tiles: stable local sort, coalesced copy-out
         for (int tb = 0; tb < m; tb += tile) {
             const int tm = min(tile, m - tb);
-            if (t < kCsRadix) ttot[t] = 0;
-            __syncthreads();
-            for (int k = t; k < tm; k += kCsThreads) {
-                const E e = load(tb + k);
-                sa[k] = e;
-                atomicAdd(&ttot[(int)((ekey(e) >> shift) & (kCsRadix - 1))], 1u);
+            if (one) {   // loaded in phase (1); the tile's digit counts are the histogram
+                if (t < kCsRadix) ttot[t] = hist[t];
+            } else {
+                if (t < kCsRadix) ttot[t] = 0;
+                __syncthreads();
+                for (int k = t; k < tm; k += kCsThreads) {
+                    const E e = load(tb + k);
+                    sa[k] = e;
+                    atomicAdd(&ttot[(int)((ekey(e) >> shift) & (kCsRadix - 1))], 1u);
+                }
             }
             __syncthreads();
             rank_step<E, K>(sa, sb, tm, shift, cnt, wsum);
