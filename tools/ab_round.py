@@ -2,7 +2,7 @@
 flags (here, on CPU), then on the GPU time each variant in its own process.
 
   python tools/ab_round.py build  name1=DEF1,DEF2 name2= ...     (CPU: compile)
-  python tools/ab_round.py run    name1 name2 ... [--rounds 40]  (GPU: time)
+  python tools/ab_round.py run    name1 name2:ENV=VAL ... [--rounds 40]  (GPU: time)
 
 Per variant: pre-roll 400 rounds, then `rounds` replay rounds timed with CUDA events
 on the replay stream (round time, no L2 flush) and a second pass with every kernel
@@ -72,7 +72,11 @@ def main():
     for rep in range(2):
         for name in names:
             env = dict(os.environ)
-            env["AM_LIB_VARIANT"] = name
+            lib, _, extra = name.partition(":")   # "variant:ENV=VAL,ENV2=VAL2" sets env knobs
+            env["AM_LIB_VARIANT"] = lib
+            for kv in filter(None, extra.split(",")):
+                k, _, v = kv.partition("=")
+                env[k] = v
             r = subprocess.run([sys.executable, __file__, "child", str(rounds), workload], env=env,
                                capture_output=True, text=True, timeout=600)
             line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]

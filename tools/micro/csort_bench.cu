@@ -27,6 +27,10 @@ int main(int argc, char** argv)
         for (int j = 0; j < 2; j++) {
             cudaMalloc(&d.rkey[j], 8 * (size_t)n); cudaMalloc(&d.rval[j], 4 * (size_t)n);
         }
+        unsigned long long kor = 0;
+        for (int i = 0; i < n; i++) kor |= k[i];
+        h.sort_or = kor;   // k_csort derives the pass count from the OR of the keys
+        cudaMemcpy(ctl, &h, sizeof h, cudaMemcpyHostToDevice);
         cudaMemcpy(d.rkey[0], k.data(), 8 * (size_t)n, cudaMemcpyHostToDevice);
         cudaMemcpy(d.rval[0], v.data(), 4 * (size_t)n, cudaMemcpyHostToDevice);
         int32_t* order;
