@@ -87,8 +87,11 @@ int am_replay_dispatched(am_replay* r, int64_t* agent_steps);
 /* One round with the world state in HOST memory (pinned for asynchronous copies):
  * copies h_pos_in int32[n][2] / h_steps_in int32[n] to the replay's world arrays, runs
  * the round, copies back the committed state (h_pos_out, h_steps_out; may alias the
- * inputs), the ready mask uint8[n] and the order int32[n].  Output pointers may be
- * NULL.  If n_ready is non-NULL the call synchronises and stores the round's ready
+ * inputs), the ready mask uint8[n] and the order int32[n] (capacity n; only the first
+ * n_ready entries are written when h_order is page-locked, the whole capacity
+ * otherwise).  When the state outputs alias the inputs and are page-locked, only the
+ * agents committed by the round are written back (the arrays already hold the rest).
+ * Output pointers may be NULL.  If n_ready is non-NULL the call synchronises and stores the round's ready
  * count (first *n_ready order entries valid); otherwise call am_replay_sync.  This
  * is the end-to-end user loop measured by bench.py. */
 int am_replay_io(am_replay* r, const int32_t* h_pos_in, const int32_t* h_steps_in,

@@ -209,6 +209,33 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
     }
 }
 
+// the round's priority order straight into page-locked host memory (mapped, UVA):
+// only the n_ready valid entries cross the link, not the n-entry capacity
+__global__ void __launch_bounds__(256) k_order_out(const int32_t* __restrict__ order, const Ctl* ctl,
+                                                   int32_t* __restrict__ h_order)
+{
+    const int nr = ctl->n_ready;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x)
+        h_order[k] = order[k];
+}
+
+// delta write-back of the committed world state into page-locked host arrays that
+// already hold the round's input (am_replay_io with aliased in/out arrays): an agent's
+// position changes only with its step (commit validation), so exactly the agents whose
+// step differs from the copied-in value are written
+__global__ void __launch_bounds__(256) k_delta_out(int n, const int32_t* __restrict__ shadow,
+                                                   const int2* __restrict__ pos, const int32_t* __restrict__ steps,
+                                                   int2* __restrict__ h_pos, int32_t* __restrict__ h_steps)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int s = steps[i];
+        if (s != shadow[i]) {
+            h_steps[i] = s;
+            h_pos[i] = pos[i];
+        }
+    }
+}
+
 }  // namespace am
 
 using namespace am;
@@ -225,6 +252,7 @@ struct am_replay {
     unsigned graph_prof = 0;            // profiling mask the graphs were captured with
     uint32_t graph_flags = 0;           // context flags the graphs were captured with
     long long* h_buf = nullptr;         // pinned: dispatched, liveness
+    int32_t* shadow = nullptr;          // am_replay_io: the steps as copied in (delta write-back)
 };
 
 static int rp_err(am_replay* rp, cudaError_t e, const char* where)
@@ -435,14 +463,43 @@ extern "C" int am_replay_io(am_replay* rp, const int32_t* h_pos_in, const int32_
     if ((rc = ensure_graphs(rp))) return rc;
     am_ctx* c = rp->ctx;
     const size_t n = (size_t)c->d.n;
+    // delta write-back when the outputs alias the inputs and are page-locked: the host
+    // arrays already hold the copied-in state, only committed agents change
+    auto mapped = [](const void* p, void** dp) {
+        cudaPointerAttributes pa{};
+        const bool ok = p && cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                        pa.devicePointer != nullptr;
+        cudaGetLastError();
+        if (ok) *dp = pa.devicePointer;
+        return ok;
+    };
+    void *dpos = nullptr, *dsteps = nullptr;
+    const bool delta = h_pos_out == h_pos_in && h_steps_out == h_steps_in && mapped(h_pos_out, &dpos) &&
+                       mapped(h_steps_out, &dsteps);
+    if (delta && !rp->shadow) RK(cudaMalloc(&rp->shadow, 4 * std::max<size_t>(n, 1)));
     RK(cudaMemcpyAsync(rp->r.pos, h_pos_in, 8 * n, cudaMemcpyHostToDevice, rp->stream));
     RK(cudaMemcpyAsync(rp->r.steps, h_steps_in, 4 * n, cudaMemcpyHostToDevice, rp->stream));
+    if (delta) RK(cudaMemcpyAsync(rp->shadow, rp->r.steps, 4 * n, cudaMemcpyDeviceToDevice, rp->stream));
     RK(cudaGraphLaunch(rp->g1, rp->stream));
     am_prof_mark(c, rp->graph_prof);
-    if (h_pos_out) RK(cudaMemcpyAsync(h_pos_out, rp->r.pos, 8 * n, cudaMemcpyDeviceToHost, rp->stream));
-    if (h_steps_out) RK(cudaMemcpyAsync(h_steps_out, rp->r.steps, 4 * n, cudaMemcpyDeviceToHost, rp->stream));
+    if (delta) {
+        RK(launch_k(false, rp->stream, k_delta_out, (unsigned)c->num_sms * 4, 256, 0, (int)n, (const int32_t*)rp->shadow,
+                    (const int2*)rp->r.pos, (const int32_t*)rp->r.steps, (int2*)dpos, (int32_t*)dsteps));
+    } else {
+        if (h_pos_out) RK(cudaMemcpyAsync(h_pos_out, rp->r.pos, 8 * n, cudaMemcpyDeviceToHost, rp->stream));
+        if (h_steps_out) RK(cudaMemcpyAsync(h_steps_out, rp->r.steps, 4 * n, cudaMemcpyDeviceToHost, rp->stream));
+    }
     if (h_mask) RK(cudaMemcpyAsync(h_mask, rp->mask, n, cudaMemcpyDeviceToHost, rp->stream));
-    if (h_order) RK(cudaMemcpyAsync(h_order, rp->order, 4 * n, cudaMemcpyDeviceToHost, rp->stream));
+    if (h_order) {
+        // page-locked (device-accessible) host order array: a kernel writes the n_ready
+        // valid entries; pageable memory: a copy of the whole capacity
+        void* dorder = nullptr;
+        if (mapped(h_order, &dorder))
+            RK(launch_k(false, rp->stream, k_order_out, (unsigned)c->num_sms, 256, 0, (const int32_t*)rp->order,
+                        (const Ctl*)c->d.ctl, (int32_t*)dorder));
+        else
+            RK(cudaMemcpyAsync(h_order, rp->order, 4 * n, cudaMemcpyDeviceToHost, rp->stream));
+    }
     if (n_ready) {
         rc = finish_check(rp, nullptr);
         if (rc) return rc;
@@ -504,6 +561,7 @@ extern "C" int am_replay_destroy(am_replay* rp)
     }
     if (rp->stream) cudaStreamDestroy(rp->stream);
     if (rp->h_buf) cudaFreeHost(rp->h_buf);
+    if (rp->shadow) cudaFree(rp->shadow);
     cudaFree(rp->mem);
     delete rp;
     return AM_OK;

@@ -109,3 +109,38 @@ def test_replay_closed_forms(x1, T, L0, L1, T_ooo):
     rep.run_to_end(chunk=8)
     assert int(rep.results()["T_ooo"][0]) == T_ooo
     rep.close()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_io_round_equals_device_round(pinned):
+    """am_replay_io (world state in host memory, the end-to-end user loop bench.py
+    times) gives the same rounds as the device-resident replay: mask, the n_ready
+    order entries and the committed state, round after round.  Page-locked host arrays
+    take the kernel writes (n_ready order entries, delta write-back of the committed
+    agents into the aliased state arrays), pageable ones the full copies."""
+    w = amgen.config("C4", n=3000)
+    lm = amgen.latency_model(w.profile)
+    a = Replay.from_workload(w, lm)
+    b = Replay.from_workload(w, lm)
+    a.run(30)
+    b.run(30)
+    n = a.n
+    h_pos = torch.empty((n, 2), dtype=torch.int32, pin_memory=pinned)
+    h_steps = torch.empty(n, dtype=torch.int32, pin_memory=pinned)
+    h_mask = torch.empty(n, dtype=torch.uint8, pin_memory=pinned)
+    h_order = torch.full((n,), -7, dtype=torch.int32, pin_memory=pinned)
+    torch.cuda.synchronize()
+    h_pos.copy_(b.pos)
+    h_steps.copy_(b.steps)
+    for _ in range(25):
+        mask, order, _ = a.step()
+        b.io(h_pos, h_steps, h_mask, h_order)
+        _, nr = b.sync()
+        torch.cuda.synchronize()
+        assert nr == order.numel()
+        np.testing.assert_array_equal(h_mask.numpy(), mask.cpu().numpy())
+        np.testing.assert_array_equal(h_order[:nr].numpy(), order.cpu().numpy())
+        np.testing.assert_array_equal(h_pos.numpy(), a.pos.cpu().numpy())
+        np.testing.assert_array_equal(h_steps.numpy(), a.steps.cpu().numpy())
+    a.close()
+    b.close()
