@@ -875,11 +875,10 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
     for (int q0 = blockIdx.x * 16; q0 < nq; q0 += gridDim.x * 16) {   // block uniform
         const int q = q0 + hw;
         if (q < nq) {                                                  // half-warp uniform
-            int lo = 0, hi = kEdgeStripes - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_pref[mid] <= q) lo = mid; else hi = mid - 1;
-            }
+            // stripe of queue entry q: the number of stripe starts <= q among stripes
+            // 1..63 (prefixes are non-decreasing), counted by the 16 lanes at once
+            const int lo = (int)__reduce_add_sync(hm, (unsigned)((s_pref[1 + l] <= q) + (s_pref[17 + l] <= q) +
+                                                                 (s_pref[33 + l] <= q) + (s_pref[49 + l] <= q)));
             const int4 A = d.wq[(size_t)lo * d.wq_cap + (q - s_pref[lo])];
             const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
             const uint32_t aid = (uint32_t)A.z & 0x7FFFFFFFu;
@@ -922,7 +921,9 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
                     }
                 }
                 // classify, compact into the list: near cells first, then far cells
+                // (pass 0 records which cells are near; pass 1 tests only the others)
                 int nn = 0, nl = 0;
+                unsigned nearbits = 0;
 #pragma unroll
                 for (int pass = 0; pass < 2; pass++) {
 #pragma unroll
@@ -930,17 +931,20 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
                         const int k = cb + j * 16 + l;
                         bool ok = false;
                         if (k < ncell && nxt[j] > ent[j].x) {
-                            const int ky = krow(k);
-                            const int cx = cx0 + (k - ky * ncx), cy = cy0 + ky;
-                            const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
-                            const bool isnear = box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric);
                             const int mn = ent[j].y;
-                            if (pass == 0)
+                            if (pass == 0) {
+                                const int ky = krow(k);
+                                const int cx = cx0 + (k - ky * ncx), cy = cy0 + ky;
+                                const bool isnear = box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1,
+                                                               ((cy + 1) << cl) - 1, Rc, d.metric);
+                                nearbits |= isnear ? 1u << j : 0u;
                                 ok = isnear && (chg ? mn <= as : (idle && mn < as));
-                            else
-                                ok = !isnear && far && direct && mn < as &&
-                                     box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - mn, d.v, d.r_p),
-                                                d.metric);
+                            } else if (!((nearbits >> j) & 1u) && far && direct && mn < as) {
+                                const int ky = krow(k);
+                                const int cx = cx0 + (k - ky * ncx), cy = cy0 + ky;
+                                ok = box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1,
+                                                rb_radius((long long)as - mn, d.v, d.r_p), d.metric);
+                            }
                         }
                         const unsigned bm = (__ballot_sync(hm, ok) >> (16 * h)) & 0xFFFFu;
                         if (ok) list[nl + __popc(bm & ((1u << l) - 1u))] = make_int2(ent[j].x, nxt[j] - ent[j].x);
