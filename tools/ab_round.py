@@ -17,12 +17,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def child(rounds: int, workload: str):
+def child(rounds: int, workload: str, agents: int = 0):
     import torch
 
     import amgen
     from paper_2411_03519_b200 import Replay
-    w = amgen.config(workload)
+    w = amgen.config(workload, n=agents or None)
     lm = amgen.latency_model(w.profile)
     rep = Replay.from_workload(w, lm)
     stream = torch.cuda.ExternalStream(rep.stream_ptr())
@@ -57,9 +57,9 @@ def main():
             print("built", name)
         return
     if mode == "child":
-        child(int(sys.argv[2]), sys.argv[3])
+        child(int(sys.argv[2]), sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else 0)
         return
-    rounds, workload, names = 40, "C5", []
+    rounds, workload, agents, names = 40, "C5", 0, []
     args = sys.argv[2:]
     k = 0
     while k < len(args):
@@ -67,6 +67,8 @@ def main():
             rounds = int(args[k + 1]); k += 2
         elif args[k] == "--workload":
             workload = args[k + 1]; k += 2
+        elif args[k] == "--agents":
+            agents = int(args[k + 1]); k += 2
         else:
             names.append(args[k]); k += 1
     for rep in range(2):
@@ -77,7 +79,7 @@ def main():
             for kv in filter(None, extra.split(",")):
                 k, _, v = kv.partition("=")
                 env[k] = v
-            r = subprocess.run([sys.executable, __file__, "child", str(rounds), workload], env=env,
+            r = subprocess.run([sys.executable, __file__, "child", str(rounds), workload, str(agents)], env=env,
                                capture_output=True, text=True, timeout=600)
             line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
             if not line:
