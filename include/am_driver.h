@@ -66,8 +66,11 @@ typedef struct am_replay am_replay;
 int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* synth,
                      int64_t quantum_us, int32_t* positions, int32_t* steps);
 
-/* Run up to max_rounds rounds without host synchronisation (CUDA graph of one round
- * replayed), then synchronise.  *active (host) receives the number of agents not yet
+/* Run up to max_rounds rounds without host synchronisation, then synchronise.  On the
+ * cell-binned path the rounds are a CUDA graph of one round replayed; when every
+ * simulation has <= 1024 agents (the fused per-simulation path) and tracing is off, one
+ * persistent kernel runs all the rounds with one CTA per simulation (identical rounds;
+ * am_replay_launch likewise).  *active (host) receives the number of agents not yet
  * DONE (0 = every simulation finished).  Rounds after a simulation finished are no-ops. */
 int am_replay_run(am_replay* r, int64_t max_rounds, int64_t* active);
 

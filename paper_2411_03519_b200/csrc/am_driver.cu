@@ -5,6 +5,7 @@
 // The synthetic policy/latency model is the same definition the oracle implements
 // independently (am_driver.h); nothing here is shared with oracle/.
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 #include <new>
 
@@ -62,6 +63,21 @@ __device__ __forceinline__ long long duration(const am_synth& sy, int i, int s)
         dsum += sy.lat[h >> 54];
     }
     return dsum;
+}
+
+// the synthetic policy (am_driver.h): random walk on the perception digest; a move into
+// a wall or off the map is cancelled
+__device__ __forceinline__ int2 policy_move(const RepDev& r, int i, int s, int2 p, unsigned long long dig)
+{
+    int mv = 0;
+    if (r.sy.policy == 0) {
+        const unsigned long long h = mix64(key3(r.sy.policy_seed, (uint32_t)i, (uint32_t)s) + dig);
+        mv = (int)(h % 5ull);
+    }
+    const int qx = p.x + (mv == 1) - (mv == 2), qy = p.y + (mv == 3) - (mv == 4);
+    bool ok = qx >= 0 && qx < r.d.map_w && qy >= 0 && qy < r.d.map_h;
+    if (ok && r.sy.wall && r.sy.wall[(long long)qy * r.d.map_w + qx]) ok = false;
+    return ok ? make_int2(qx, qy) : p;
 }
 
 // commit every RUNNING agent whose cluster completed (tcommit <= t_sim, the clock
@@ -165,17 +181,7 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
         const int b = sim_of(d, i);
         const long long tc = r.tcl[d.labels[i]];
         r.tcommit[i] = tc;
-        const int s = r.steps[i];
-        const int2 p = r.pos[i];
-        int mv = 0;
-        if (r.sy.policy == 0) {
-            const unsigned long long h = mix64(key3(r.sy.policy_seed, (uint32_t)i, (uint32_t)s) + d.digest[i]);
-            mv = (int)(h % 5ull);
-        }
-        const int qx = p.x + (mv == 1) - (mv == 2), qy = p.y + (mv == 3) - (mv == 4);
-        bool ok = qx >= 0 && qx < d.map_w && qy >= 0 && qy < d.map_h;
-        if (ok && r.sy.wall && r.sy.wall[(long long)qy * d.map_w + qx]) ok = false;
-        r.newpos[i] = ok ? make_int2(qx, qy) : p;
+        r.newpos[i] = policy_move(r, i, r.steps[i], r.pos[i], d.digest[i]);
         if (d.n_sims > 1) atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
         else tmin = min(tmin, (unsigned long long)tc);
     }
@@ -206,6 +212,153 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
             r.tnext[b] = LLONG_MAX;
             r.active_flag[b] = 0;
         }
+    }
+}
+
+// ============================================================== persistent small replay
+// The whole replay of one simulation (<= 1024 agents) in one CTA, up to max_rounds
+// rounds without leaving the kernel: the fused round of k_small (pairwise blocking and
+// coupling tests, shared-memory union-find, ready filter, perception digests), the
+// dispatch of k_disp_a / k_disp_b (cluster completion time = t + max member duration,
+// moves computed at dispatch), the event clock of k_disp_b's last block and the commits
+// of k_commit -- each step in the same order and with the same arithmetic as the
+// multi-kernel round, so every round's outcome is identical.  Entry and exit state is
+// the multi-kernel round's (world arrays, context state, tcommit / newpos / traj,
+// per-simulation clock and counters), so the two paths can alternate.  Grid = one CTA
+// per simulation; dynamic shared memory sized by the largest simulation (M agents).
+__global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_rounds, int M)
+{
+    const Dev& d = r.d;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    long long* stc = reinterpret_cast<long long*>(sm_raw);                       // [M] tcommit
+    unsigned long long* stcl = reinterpret_cast<unsigned long long*>(stc + M);   // [M] cluster time by label
+    int2* snp = reinterpret_cast<int2*>(stcl + M);                               // [M] move computed at dispatch
+    int* sx = reinterpret_cast<int*>(snp + M);
+    int* sy = sx + M;
+    int* ss = sy + M;
+    uint32_t* par = reinterpret_cast<uint32_t*>(ss + M);
+    uint8_t* sst = reinterpret_cast<uint8_t*>(par + M);
+    uint8_t* sbad = sst + M;
+    __shared__ unsigned long long s_tmin;
+    __shared__ int s_any, s_fin, s_nr;
+    const int b = blockIdx.x, t = threadIdx.x;
+    const int lo = (int)((long long)b * d.n / d.n_sims);
+    const int m = (int)((long long)(b + 1) * d.n / d.n_sims) - lo;
+    const uint32_t c = d.ctl->cur;
+    const int i = lo + t;
+    const bool mine = t < m;
+    unsigned long long traj = 0;
+    // entry: the world arrays (after the last commits) and the context's statuses; an
+    // agent the last commit advanced is IDLE (or DONE) again, as the next ingest makes it
+    if (mine) {
+        const int2 p = r.pos[i];
+        const int s = r.steps[i];
+        uint8_t st = d.status[c][i];
+        if (st == ST_RUNNING && s == d.step[c][i] + 1) st = (d.target > 0 && s == d.target) ? ST_DONE : ST_IDLE;
+        sx[t] = p.x; sy[t] = p.y; ss[t] = s; sst[t] = st;
+        stc[t] = r.tcommit[i];
+        snp[t] = r.newpos[i];
+        traj = r.traj[i];
+    }
+    long long tsim = r.t_sim[b], tdone = r.tdone[b], nrounds = r.rounds[b], disp = 0;
+    int act = r.active_flag[b], live_err = 0, lab = -1;
+    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    __syncthreads();
+    for (long long k = 0; k < max_rounds && act; k++) {
+        // ---- the tracker round (k_small)
+        if (mine) { par[t] = (uint32_t)t; sbad[t] = 0; stcl[t] = 0; }
+        if (t == 0) { s_tmin = ~0ull; s_any = 0; s_fin = 0; s_nr = 0; }
+        __syncthreads();
+        bool blocked = false;
+        unsigned long long dig = 0;
+        const uint8_t st = mine ? sst[t] : (uint8_t)ST_DONE;
+        if (st != ST_DONE) {
+            const int ax = sx[t], ay = sy[t], as = ss[t];
+            for (int j = 0; j < m; j++) {
+                if (j == t || sst[j] == ST_DONE) continue;
+                const int dx = sx[j] - ax, dy = sy[j] - ay, bs = ss[j];
+                if (bs == as) {
+                    if (within(dx, dy, Rc, d.metric)) {
+                        if (t < j) suf_unite(par, (uint32_t)t, (uint32_t)j);
+                        if (within(dx, dy, (uint32_t)d.r_p, d.metric)) dig += digest_term((uint32_t)(lo + j), dx, dy);
+                    }
+                } else if (!blocked && bs < as) {
+                    blocked = within(dx, dy, rb_radius((long long)as - bs, d.v, d.r_p), d.metric);
+                }
+            }
+        }
+        __syncthreads();
+        lab = -1;
+        if (st != ST_DONE) {
+            lab = (int)suf_find(par, (uint32_t)t);
+            if (blocked || st == ST_RUNNING) sbad[lab] = 1;
+        }
+        __syncthreads();
+        const bool rdy = st == ST_IDLE && !sbad[lab];
+        // ---- dispatch part a (k_disp_a): cluster completion time
+        if (rdy) atomicMax(stcl + lab, (unsigned long long)(tsim + duration(r.sy, i, ss[t])));
+        __syncthreads();
+        // ---- dispatch part b (k_disp_b): member completion times and moves
+        if (rdy) {
+            sst[t] = ST_RUNNING;
+            stc[t] = (long long)stcl[lab];
+            snp[t] = policy_move(r, i, ss[t], make_int2(sx[t], sy[t]), dig);
+            atomicAdd(&s_nr, 1);
+        }
+        if (mine && (rdy || st == ST_RUNNING)) atomicMin(&s_tmin, (unsigned long long)stc[t]);
+        __syncthreads();
+        // ---- next event (k_disp_b's last block); this round counts (an agent was active)
+        const unsigned long long tn = s_tmin;
+        disp += s_nr;
+        nrounds += 1;
+        if (tn == ~0ull) {   // agents left, nothing running: liveness violation
+            live_err = 1;
+            break;
+        }
+        tsim = r.Q > 0 ? (((long long)tn + r.Q - 1) / r.Q) * r.Q : (long long)tn;
+        // ---- commits at the new event time (k_commit)
+        if (mine && sst[t] == ST_RUNNING && stc[t] <= tsim) {
+            const int2 np = snp[t];
+            const int s = ss[t] + 1;
+            sx[t] = np.x; sy[t] = np.y; ss[t] = s;
+            traj = traj_step(traj, s, np.x, np.y);
+            const bool done = d.target > 0 && s == d.target;
+            sst[t] = done ? ST_DONE : ST_IDLE;
+            if (done) s_fin = 1;
+        }
+        if (mine && sst[t] != ST_DONE) s_any = 1;
+        __syncthreads();
+        if (s_fin) tdone = max(tdone, tsim);
+        act = s_any;
+        __syncthreads();   // s_* are reset at the top of the next round
+    }
+    // ---- exit: the multi-kernel round's state
+    if (mine) {
+        const int2 p = make_int2(sx[t], sy[t]);
+        r.pos[i] = p;
+        r.steps[i] = ss[t];
+        d.pos[c][i] = p;
+        d.step[c][i] = ss[t];
+        d.status[c][i] = sst[t];
+        r.tcommit[i] = stc[t];
+        r.newpos[i] = snp[t];
+        r.traj[i] = traj;
+        if (lab >= 0 || sst[t] == ST_DONE) d.labels[i] = sst[t] == ST_DONE ? -1 : lo + lab;
+    }
+    if (t == 0) { s_tmin = ~0ull; s_any = 0; }
+    __syncthreads();
+    if (mine && sst[t] == ST_RUNNING) atomicMin(&s_tmin, (unsigned long long)stc[t]);
+    if (mine && sst[t] != ST_DONE) atomicAdd(&s_any, 1);
+    __syncthreads();
+    if (t == 0) {
+        r.t_sim[b] = tsim;
+        r.tdone[b] = tdone;
+        r.rounds[b] = nrounds;
+        r.active_flag[b] = act && !live_err;
+        r.tnext[b] = s_tmin == ~0ull ? LLONG_MAX : (long long)s_tmin;
+        if (disp) atomicAdd((unsigned long long*)r.dispatched, (unsigned long long)disp);
+        if (live_err) *r.liveness = 1;
+        if (s_any) atomicAdd(&d.ctl->n_active, s_any);
     }
 }
 
@@ -420,10 +573,35 @@ static int ensure_graphs(am_replay* rp)
     return AM_OK;
 }
 
+// Fused per-simulation path (every simulation <= 1024 agents), no profiling: rounds
+// run inside one persistent kernel (k_small_replay), one CTA per simulation.
+static bool small_persistent(am_replay* rp)
+{
+    am_ctx* c = rp->ctx;
+    if (c->path != 0 || c->prof.on) return false;
+    static const int off = [] { const char* e = getenv("AM_SMALL_PERSIST"); return e && atoi(e) == 0; }();
+    return !off;   // AM_SMALL_PERSIST=0: the multi-kernel rounds (ablation)
+}
+static int launch_small_replay(am_replay* rp, int64_t rounds)
+{
+    am_ctx* c = rp->ctx;
+    const int M = c->small_threads;   // >= agents of the largest simulation, multiple of 32
+    const size_t smem = (size_t)M * (8 + 8 + 8 + 4 + 4 + 4 + 4 + 1 + 1);
+    RK(cudaMemsetAsync(&c->d.ctl->n_active, 0, sizeof(int32_t), rp->stream));
+    rp->r.d = c->d;
+    RK(launch_k(false, rp->stream, k_small_replay, (unsigned)c->d.n_sims, (unsigned)M, smem, rp->r,
+                (long long)rounds, M));
+    return AM_OK;
+}
+
 extern "C" int am_replay_run(am_replay* rp, int64_t max_rounds, int64_t* active)
 {
     if (!rp) return AM_E_ARG;
     int rc;
+    if (small_persistent(rp)) {
+        if (max_rounds > 0 && (rc = launch_small_replay(rp, max_rounds))) return rc;
+        return finish_check(rp, active);
+    }
     if ((rc = ensure_graphs(rp))) return rc;
     int64_t k = 0;
     for (; k + 8 <= max_rounds; k += 8) RK(cudaGraphLaunch(rp->g8, rp->stream));
@@ -512,6 +690,7 @@ extern "C" int am_replay_launch(am_replay* rp, int64_t rounds)
 {
     if (!rp || rounds < 0) return AM_E_ARG;
     int rc;
+    if (small_persistent(rp)) return rounds > 0 ? launch_small_replay(rp, rounds) : AM_OK;
     if ((rc = ensure_graphs(rp))) return rc;
     int64_t k = 0;
     for (; k + 8 <= rounds; k += 8) RK(cudaGraphLaunch(rp->g8, rp->stream));

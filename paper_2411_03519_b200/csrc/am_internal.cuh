@@ -344,6 +344,37 @@ __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x)
     }
     return cur;
 }
+// shared-memory union-find of the fused per-simulation kernels (same hooking rule)
+__device__ __forceinline__ uint32_t suf_find(volatile uint32_t* parent, uint32_t x)
+{
+    uint32_t cur = parent[x];
+    if (cur != x) {
+        uint32_t prev = x, next;
+        while (cur > (next = parent[cur])) {
+            parent[prev] = next;
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+__device__ __forceinline__ void suf_unite(uint32_t* parent, uint32_t a, uint32_t b)
+{
+    volatile uint32_t* vp = parent;
+    uint32_t ra = suf_find(vp, a), rb = suf_find(vp, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            uint32_t old = atomicCAS(parent + rb, rb, ra);
+            if (old == rb) break;
+            rb = old;
+        } else {
+            uint32_t old = atomicCAS(parent + ra, ra, rb);
+            if (old == ra) break;
+            ra = old;
+        }
+    }
+}
+
 __device__ __forceinline__ void uf_unite(uint32_t* parent, uint32_t a, uint32_t b)
 {
     uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);

@@ -1376,36 +1376,6 @@ __global__ void __launch_bounds__(1024) k_sort_pass(Dev d, int pass, int32_t* __
 // One CTA per simulation (<= 1024 agents): the whole round in shared memory.
 // Simulations take tickets in index order; a chained scan over simulations places
 // each one's ready agents in `order` (sim-major: order = (sim, step, label, id)).
-__device__ __forceinline__ uint32_t suf_find(volatile uint32_t* parent, uint32_t x)
-{
-    uint32_t cur = parent[x];
-    if (cur != x) {
-        uint32_t prev = x, next;
-        while (cur > (next = parent[cur])) {
-            parent[prev] = next;
-            prev = cur;
-            cur = next;
-        }
-    }
-    return cur;
-}
-__device__ __forceinline__ void suf_unite(uint32_t* parent, uint32_t a, uint32_t b)
-{
-    volatile uint32_t* vp = parent;
-    uint32_t ra = suf_find(vp, a), rb = suf_find(vp, b);
-    while (ra != rb) {
-        if (ra < rb) {
-            uint32_t old = atomicCAS(parent + rb, rb, ra);
-            if (old == rb) break;
-            rb = old;
-        } else {
-            uint32_t old = atomicCAS(parent + ra, ra, rb);
-            if (old == ra) break;
-            ra = old;
-        }
-    }
-}
-
 __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mask,
                                                  int32_t* __restrict__ order)
 {

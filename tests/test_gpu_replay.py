@@ -144,3 +144,38 @@ def test_host_io_round_equals_device_round(pinned):
         np.testing.assert_array_equal(h_steps.numpy(), a.steps.cpu().numpy())
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("name,n_sims", [("C1", None), ("C3", 64), ("C2", None)])
+def test_persistent_small_replay_equals_round_kernels(name, n_sims):
+    """The persistent per-simulation replay kernel (am_replay_run / _launch on the fused
+    path) and the multi-kernel rounds (am_replay_step) give identical states round for
+    round, and the two can alternate: A runs 40 rounds persistently, B steps 40 rounds;
+    then A steps 10 and B runs 10; then both run to the end."""
+    w = amgen.config(name, steps=120, n=n_sims)
+    lm = amgen.latency_model(w.profile)
+    a = Replay.from_workload(w, lm)
+    b = Replay.from_workload(w, lm)
+
+    def same():
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(a.pos.cpu().numpy(), b.pos.cpu().numpy())
+        np.testing.assert_array_equal(a.steps.cpu().numpy(), b.steps.cpu().numpy())
+        ra, rb = a.results(), b.results()
+        for k in ("T_ooo", "rounds", "traj"):
+            np.testing.assert_array_equal(ra[k], rb[k], err_msg=k)
+        assert a.dispatched() == b.dispatched()
+
+    a.run(40)
+    for _ in range(40):
+        b.step()
+    same()
+    for _ in range(10):
+        a.step()
+    b.run(10)
+    same()
+    a.run_to_end()
+    b.run_to_end()
+    same()
+    a.close()
+    b.close()
