@@ -225,23 +225,25 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
 // multi-kernel round, so every round's outcome is identical.  Entry and exit state is
 // the multi-kernel round's (world arrays, context state, tcommit / newpos / traj,
 // per-simulation clock and counters), so the two paths can alternate.  Grid = one CTA
-// per simulation; dynamic shared memory sized by the largest simulation (M agents).
-__global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_rounds, int M)
+// per simulation of M x G threads: G lanes (a power of two <= 32, one warp) share an
+// agent's pair tests (lane q takes partners j = q, q + G, ...; verdicts and digests are
+// combined by shuffles), lane 0 of the group does the agent's serial work.  Dynamic
+// shared memory is sized by the largest simulation (M agents).
+__global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_rounds, int M, int G)
 {
     const Dev& d = r.d;
     extern __shared__ __align__(16) unsigned char sm_raw[];
     long long* stc = reinterpret_cast<long long*>(sm_raw);                       // [M] tcommit
     unsigned long long* stcl = reinterpret_cast<unsigned long long*>(stc + M);   // [M] cluster time by label
     int2* snp = reinterpret_cast<int2*>(stcl + M);                               // [M] move computed at dispatch
-    int* sx = reinterpret_cast<int*>(snp + M);
-    int* sy = sx + M;
-    int* ss = sy + M;
-    uint32_t* par = reinterpret_cast<uint32_t*>(ss + M);
-    uint8_t* sst = reinterpret_cast<uint8_t*>(par + M);
-    uint8_t* sbad = sst + M;
+    int4* sa = reinterpret_cast<int4*>(snp + M);                                 // [M] {x, y, step, status}
+    uint32_t* par = reinterpret_cast<uint32_t*>(sa + M);
+    uint8_t* sbad = reinterpret_cast<uint8_t*>(par + M);
     __shared__ unsigned long long s_tmin;
     __shared__ int s_any, s_fin, s_nr;
-    const int b = blockIdx.x, t = threadIdx.x;
+    const int b = blockIdx.x;
+    const int t = threadIdx.x / G, q = threadIdx.x % G;   // agent slot, lane within its group
+    const bool lead = q == 0;
     const int lo = (int)((long long)b * d.n / d.n_sims);
     const int m = (int)((long long)(b + 1) * d.n / d.n_sims) - lo;
     const uint32_t c = d.ctl->cur;
@@ -250,12 +252,12 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
     unsigned long long traj = 0;
     // entry: the world arrays (after the last commits) and the context's statuses; an
     // agent the last commit advanced is IDLE (or DONE) again, as the next ingest makes it
-    if (mine) {
+    if (mine && lead) {
         const int2 p = r.pos[i];
         const int s = r.steps[i];
         uint8_t st = d.status[c][i];
         if (st == ST_RUNNING && s == d.step[c][i] + 1) st = (d.target > 0 && s == d.target) ? ST_DONE : ST_IDLE;
-        sx[t] = p.x; sy[t] = p.y; ss[t] = s; sst[t] = st;
+        sa[t] = make_int4(p.x, p.y, s, st);
         stc[t] = r.tcommit[i];
         snp[t] = r.newpos[i];
         traj = r.traj[i];
@@ -266,46 +268,51 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
     __syncthreads();
     for (long long k = 0; k < max_rounds && act; k++) {
         // ---- the tracker round (k_small)
-        if (mine) { par[t] = (uint32_t)t; sbad[t] = 0; stcl[t] = 0; }
-        if (t == 0) { s_tmin = ~0ull; s_any = 0; s_fin = 0; s_nr = 0; }
+        if (mine && lead) { par[t] = (uint32_t)t; sbad[t] = 0; stcl[t] = 0; }
+        if (threadIdx.x == 0) { s_tmin = ~0ull; s_any = 0; s_fin = 0; s_nr = 0; }
         __syncthreads();
         bool blocked = false;
         unsigned long long dig = 0;
-        const uint8_t st = mine ? sst[t] : (uint8_t)ST_DONE;
+        const int4 A = mine ? sa[t] : make_int4(0, 0, 0, ST_DONE);
+        const int st = A.w;
         if (st != ST_DONE) {
-            const int ax = sx[t], ay = sy[t], as = ss[t];
-            for (int j = 0; j < m; j++) {
-                if (j == t || sst[j] == ST_DONE) continue;
-                const int dx = sx[j] - ax, dy = sy[j] - ay, bs = ss[j];
-                if (bs == as) {
+            for (int j = q; j < m; j += G) {
+                const int4 B = sa[j];
+                if (j == t || B.w == ST_DONE) continue;
+                const int dx = B.x - A.x, dy = B.y - A.y;
+                if (B.z == A.z) {
                     if (within(dx, dy, Rc, d.metric)) {
                         if (t < j) suf_unite(par, (uint32_t)t, (uint32_t)j);
                         if (within(dx, dy, (uint32_t)d.r_p, d.metric)) dig += digest_term((uint32_t)(lo + j), dx, dy);
                     }
-                } else if (!blocked && bs < as) {
-                    blocked = within(dx, dy, rb_radius((long long)as - bs, d.v, d.r_p), d.metric);
+                } else if (!blocked && B.z < A.z) {
+                    blocked = within(dx, dy, rb_radius((long long)A.z - B.z, d.v, d.r_p), d.metric);
                 }
             }
+        }
+        for (int o = 1; o < G; o <<= 1) {   // combine the group's lanes (one warp)
+            blocked |= __shfl_xor_sync(0xFFFFFFFFu, blocked, o) != 0;
+            dig += __shfl_xor_sync(0xFFFFFFFFu, dig, o);
         }
         __syncthreads();
         lab = -1;
         if (st != ST_DONE) {
             lab = (int)suf_find(par, (uint32_t)t);
-            if (blocked || st == ST_RUNNING) sbad[lab] = 1;
+            if (lead && (blocked || st == ST_RUNNING)) sbad[lab] = 1;
         }
         __syncthreads();
-        const bool rdy = st == ST_IDLE && !sbad[lab];
+        const bool rdy = lead && st == ST_IDLE && !sbad[lab];
         // ---- dispatch part a (k_disp_a): cluster completion time
-        if (rdy) atomicMax(stcl + lab, (unsigned long long)(tsim + duration(r.sy, i, ss[t])));
+        if (rdy) atomicMax(stcl + lab, (unsigned long long)(tsim + duration(r.sy, i, A.z)));
         __syncthreads();
         // ---- dispatch part b (k_disp_b): member completion times and moves
         if (rdy) {
-            sst[t] = ST_RUNNING;
+            sa[t].w = ST_RUNNING;
             stc[t] = (long long)stcl[lab];
-            snp[t] = policy_move(r, i, ss[t], make_int2(sx[t], sy[t]), dig);
+            snp[t] = policy_move(r, i, A.z, make_int2(A.x, A.y), dig);
             atomicAdd(&s_nr, 1);
         }
-        if (mine && (rdy || st == ST_RUNNING)) atomicMin(&s_tmin, (unsigned long long)stc[t]);
+        if (mine && lead && (rdy || st == ST_RUNNING)) atomicMin(&s_tmin, (unsigned long long)stc[t]);
         __syncthreads();
         // ---- next event (k_disp_b's last block); this round counts (an agent was active)
         const unsigned long long tn = s_tmin;
@@ -317,40 +324,44 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
         }
         tsim = r.Q > 0 ? (((long long)tn + r.Q - 1) / r.Q) * r.Q : (long long)tn;
         // ---- commits at the new event time (k_commit)
-        if (mine && sst[t] == ST_RUNNING && stc[t] <= tsim) {
-            const int2 np = snp[t];
-            const int s = ss[t] + 1;
-            sx[t] = np.x; sy[t] = np.y; ss[t] = s;
-            traj = traj_step(traj, s, np.x, np.y);
-            const bool done = d.target > 0 && s == d.target;
-            sst[t] = done ? ST_DONE : ST_IDLE;
-            if (done) s_fin = 1;
+        if (mine && lead) {
+            int4 S = sa[t];
+            if (S.w == ST_RUNNING && stc[t] <= tsim) {
+                const int2 np = snp[t];
+                S.x = np.x; S.y = np.y; S.z += 1;
+                traj = traj_step(traj, S.z, np.x, np.y);
+                const bool done = d.target > 0 && S.z == d.target;
+                S.w = done ? ST_DONE : ST_IDLE;
+                sa[t] = S;
+                if (done) s_fin = 1;
+            }
+            if (S.w != ST_DONE) s_any = 1;
         }
-        if (mine && sst[t] != ST_DONE) s_any = 1;
         __syncthreads();
         if (s_fin) tdone = max(tdone, tsim);
         act = s_any;
         __syncthreads();   // s_* are reset at the top of the next round
     }
     // ---- exit: the multi-kernel round's state
-    if (mine) {
-        const int2 p = make_int2(sx[t], sy[t]);
+    const int4 S = mine ? sa[t] : make_int4(0, 0, 0, ST_DONE);
+    if (mine && lead) {
+        const int2 p = make_int2(S.x, S.y);
         r.pos[i] = p;
-        r.steps[i] = ss[t];
+        r.steps[i] = S.z;
         d.pos[c][i] = p;
-        d.step[c][i] = ss[t];
-        d.status[c][i] = sst[t];
+        d.step[c][i] = S.z;
+        d.status[c][i] = (uint8_t)S.w;
         r.tcommit[i] = stc[t];
         r.newpos[i] = snp[t];
         r.traj[i] = traj;
-        if (lab >= 0 || sst[t] == ST_DONE) d.labels[i] = sst[t] == ST_DONE ? -1 : lo + lab;
+        if (lab >= 0 || S.w == ST_DONE) d.labels[i] = S.w == ST_DONE ? -1 : lo + lab;
     }
-    if (t == 0) { s_tmin = ~0ull; s_any = 0; }
+    if (threadIdx.x == 0) { s_tmin = ~0ull; s_any = 0; }
     __syncthreads();
-    if (mine && sst[t] == ST_RUNNING) atomicMin(&s_tmin, (unsigned long long)stc[t]);
-    if (mine && sst[t] != ST_DONE) atomicAdd(&s_any, 1);
+    if (mine && lead && S.w == ST_RUNNING) atomicMin(&s_tmin, (unsigned long long)stc[t]);
+    if (mine && lead && S.w != ST_DONE) atomicAdd(&s_any, 1);
     __syncthreads();
-    if (t == 0) {
+    if (threadIdx.x == 0) {
         r.t_sim[b] = tsim;
         r.tdone[b] = tdone;
         r.rounds[b] = nrounds;
@@ -586,11 +597,22 @@ static int launch_small_replay(am_replay* rp, int64_t rounds)
 {
     am_ctx* c = rp->ctx;
     const int M = c->small_threads;   // >= agents of the largest simulation, multiple of 32
-    const size_t smem = (size_t)M * (8 + 8 + 8 + 4 + 4 + 4 + 4 + 1 + 1);
+    const size_t smem = (size_t)M * (8 + 8 + 8 + 16 + 4 + 1);
+    // lanes per agent: as many as one CTA of <= 1024 threads holds while all the
+    // simulations' CTAs fit in half the GPU's thread slots (measured: C1 G = 32 3.0x
+    // over G = 1; C3's 4096 simulations are best at G = 1)
+    int G = 1;
+    while (G < 32 && M * G * 2 <= 1024 && (long long)c->d.n_sims * M * G * 2 <= 1024LL * c->num_sms) G *= 2;
+    if (const char* e = getenv("AM_SMALL_LANES")) {   // tuning knob (rounded down to a power of two)
+        const int want = std::max(1, std::min(32, atoi(e)));
+        G = 1;
+        while (G * 2 <= want) G *= 2;
+    }
+    while (M * G > 1024) G /= 2;
     RK(cudaMemsetAsync(&c->d.ctl->n_active, 0, sizeof(int32_t), rp->stream));
     rp->r.d = c->d;
-    RK(launch_k(false, rp->stream, k_small_replay, (unsigned)c->d.n_sims, (unsigned)M, smem, rp->r,
-                (long long)rounds, M));
+    RK(launch_k(false, rp->stream, k_small_replay, (unsigned)c->d.n_sims, (unsigned)(M * G), smem, rp->r,
+                (long long)rounds, M, G));
     return AM_OK;
 }
 
