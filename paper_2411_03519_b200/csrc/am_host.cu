@@ -161,7 +161,8 @@ extern "C" int am_scan_stats(am_ctx* c, uint64_t* out)
 extern "C" int32_t am_launches_per_round(const am_ctx* c)
 {
     if (!c) return 0;
-    return c->path == 0 ? 3 : 11 + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) + ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
+    return c->path == 0 ? 3 : 11 - (AM_SCAN_UNITE ? 1 : 0) + (c->csort_ctas ? 1 : 1 + c->sort_passes_max) +
+                                  ((c->d.flags & AM_DIGEST) ? 1 : 0);  // all launches of a round
 }
 
 extern "C" const char* am_profile_name(int32_t id)
@@ -558,7 +559,8 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             CK(c, cudaEventRecord(c->ev_efil, c->side));
             LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw, std::min(blocks(d.n, 16), (unsigned)c->scan_blocks), 256, 0, d)));
             CK(c, cudaStreamWaitEvent(s, c->ev_efil, 0));
-            LAUNCH(K_UNION, CK(c, launch_k(c->pdl, s, k_union, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
+            if (!AM_SCAN_UNITE)   // else the scan united its new edges as it flushed them
+                LAUNCH(K_UNION, CK(c, launch_k(c->pdl, s, k_union, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
         }
         LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, blocks(d.n, 256 * kFinItems), 256, 0, d)));
         LAUNCH(K_READY, CK(c, launch_k(c->pdl, s, k_ready, c->ntiles_ready, kReadyThreads, 0, d, mask)));

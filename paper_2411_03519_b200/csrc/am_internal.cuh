@@ -27,6 +27,9 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #ifndef AM_FIN_ITEMS
 #define AM_FIN_ITEMS 4
 #endif
+#ifndef AM_SCAN_UNITE
+#define AM_SCAN_UNITE 0   // 1: the scan unites its new edges as it flushes them, no k_union (A/B: +13 us, rejected)
+#endif
 #ifndef AM_INGEST_ITEMS
 #define AM_INGEST_ITEMS 4
 #endif

@@ -519,6 +519,7 @@ __device__ __forceinline__ void stage_edge(const Dev& d, EdgeStage& sm, uint32_t
     const uint32_t k = atomicAdd((uint32_t*)&d.ctl->ncnt[nxt], 1u);
     if ((int)k < d.ecap) {
         d.nedges[(size_t)nxt * d.ecap + k] = make_uint2(a, b);
+        if (AM_SCAN_UNITE) uf_unite(d.parent, a, b);
     } else {
         uf_unite(d.parent, a, b);                  // list full: unite now, rebuild next round
         d.ctl->full_next = 1;
@@ -537,6 +538,9 @@ __device__ __forceinline__ void flush_stage(const Dev& d, EdgeStage& sm, int lan
             const uint2 e = sm.e[k];
             if (base + k < d.ecap) {
                 d.nedges[(size_t)nxt * d.ecap + base + k] = e;
+                // the union right here (the scan never reads the forest; k_efilter's
+                // concurrent unions of carried edges are lock-free hooks too)
+                if (AM_SCAN_UNITE) uf_unite(d.parent, e.x, e.y);
             } else {
                 uf_unite(d.parent, e.x, e.y);      // list full: unite now, rebuild next round
                 d.ctl->full_next = 1;
@@ -1000,7 +1004,13 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
 {
     pdl_begin();
     const int i0 = blockIdx.x * (256 * kFinItems) + threadIdx.x;
-    if (i0 == 0) d.ctl->full = 0;   // every kernel that reads the full-round flag has run
+    if (i0 == 0) {
+        d.ctl->full = 0;   // every kernel that reads the full-round flag has run
+        if (AM_SCAN_UNITE) {   // (k_union's statistic)
+            const uint32_t nxt = d.ctl->ecur ^ 1u;
+            d.ctl->n_edges = min((int)d.ctl->ncnt[nxt], d.ecap) + min((int)d.ctl->ccnt[nxt], d.ecap);
+        }
+    }
     const uint32_t c = d.ctl->cur;
     // every item's status / verdict / parent load is issued before any pointer chase
     // (independent chains in flight; one wave of threads covers the agents)
