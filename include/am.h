@@ -126,7 +126,9 @@ int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radius_p, int32_
 int am_update(am_ctx* ctx, const int32_t* positions, const int32_t* sim_steps);
 
 /* Set the full state, including statuses (uint8 [n_agents], AM_IDLE/RUNNING/DONE),
- * without commit validation (snapshots).  Bounds and status values are checked. */
+ * without commit validation (snapshots).  Bounds and status values are checked; the call
+ * synchronises and reports them, unless AM_ASYNC is set (then it is stream-ordered and a
+ * rejected state is reported by the next synchronising call). */
 int am_set_state(am_ctx* ctx, const int32_t* positions, const int32_t* sim_steps,
                  const uint8_t* status);
 

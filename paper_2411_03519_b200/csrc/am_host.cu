@@ -451,6 +451,10 @@ extern "C" int am_set_state(am_ctx* c, const int32_t* positions, const int32_t* 
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
     int rc = launch_ingest(c, positions, sim_steps, status, 2);
     if (rc) return rc;
+    if (c->d.flags & AM_ASYNC) {   // stream-ordered; a rejected state surfaces at the next sync
+        c->first = false;
+        return AM_OK;
+    }
     rc = am_sync(c);
     if (rc == AM_OK) c->first = false;
     return rc;

@@ -159,8 +159,14 @@ class SlabRank:
         if self.y0:
             self.lpos[:nl, 1] -= self.y0
         tr = self.tracker
-        tr.set_state(self.lpos, self.lsteps, self.lstatus)
-        tr.ready()
+        # stream-ordered local round (AM_ASYNC): no host synchronisation until the link
+        # counts; a rejected state would surface at the next synchronising call
+        self.L.am_set_flags(tr.ctx, tr.flags | _lib.ASYNC)
+        try:
+            tr.set_state(self.lpos, self.lsteps, self.lstatus)
+        finally:
+            self.L.am_set_flags(tr.ctx, tr.flags)
+        tr.ready_async()
         labels = tr.clusters()
         check(self.L.am_blocked(tr.ctx, self.lblocked.data_ptr()), tr.ctx)
         check(self.L.am_slab_links(nl, n, self.lgid.data_ptr(), labels.data_ptr(), self.lstatus.data_ptr(),
@@ -169,6 +175,7 @@ class SlabRank:
                                    self.nl.data_ptr() + 4, self.badlocal.data_ptr(), self.bnd.data_ptr(),
                                    self.stream))
         k, b = self.nl.tolist()
+        tr.sync()   # reports a rejected local state (bounds, statuses)
         if k > self.lcap or b > self.lcap:
             raise RuntimeError("link buffer overflow")   # <= one record per local agent
         self.labels_local = labels
