@@ -385,15 +385,26 @@ __global__ void __launch_bounds__(256) k_order_out(const int32_t* __restrict__ o
 
 // delta write-back of the committed world state into page-locked host arrays that
 // already hold the round's input (am_replay_io with aliased in/out arrays): an agent's
-// position changes only with its step (commit validation), so exactly the agents whose
-// step differs from the copied-in value are written
+// position changes only with its step (commit validation), so only agents whose step
+// differs from the copied-in value need writing.  They are sparse and scattered, and
+// single 4-8 byte writes over PCIe cost a transaction each, so every aligned group of 8
+// agents with a change is written whole (64 B of positions + 32 B of steps, coalesced;
+// the unchanged members rewrite the value the host already holds).
 __global__ void __launch_bounds__(256) k_delta_out(int n, const int32_t* __restrict__ shadow,
                                                    const int2* __restrict__ pos, const int32_t* __restrict__ steps,
                                                    int2* __restrict__ h_pos, int32_t* __restrict__ h_steps)
 {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int s = steps[i];
-        if (s != shadow[i]) {
+    const int lane = threadIdx.x & 31;
+    for (int base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; base < n; base += gridDim.x * blockDim.x) {
+        const int i = base + lane;   // warp-uniform loop: every lane takes part in the ballot
+        int s = 0;
+        bool ch = false;
+        if (i < n) {
+            s = steps[i];
+            ch = s != shadow[i];
+        }
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, ch);
+        if (i < n && ((m >> (lane & 24)) & 0xFFu)) {
             h_steps[i] = s;
             h_pos[i] = pos[i];
         }

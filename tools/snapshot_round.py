@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--workload", default="C5")
     ap.add_argument("--preroll", type=int, default=400)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--scan-thread", action="store_true", help="AM_SCAN_THREAD ablation scan")
     a = ap.parse_args()
     w = amgen.config(a.workload)
     lm = amgen.latency_model(w.profile)
@@ -31,7 +32,8 @@ def main():
     status = rep.tracker.status().clone()
     rep.close()
     n = pos.shape[0]
-    tr = Tracker(w.map_w, w.map_h, 4, 1, n, target=w.steps, peek=True, validate=False, force="binned")
+    tr = Tracker(w.map_w, w.map_h, 4, 1, n, target=w.steps, peek=True, validate=False, force="binned",
+                 scan_thread=a.scan_thread)
     s = torch.cuda.current_stream()
     mask = torch.empty(n, dtype=torch.uint8, device="cuda")
     order = torch.empty(n, dtype=torch.int32, device="cuda")
