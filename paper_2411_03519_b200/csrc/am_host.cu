@@ -28,6 +28,8 @@ __global__ void k_efilter(Dev d);
 __global__ void k_digest(Dev d, const int32_t* order);
 __global__ void k_csort(Dev d, int32_t* order, int smem_bytes);
 size_t csort_smem_fixed();
+size_t csort_smem_need();
+int csort_threads();
 
 __global__ void k_copy_status(Dev d, uint8_t* out)
 {
@@ -219,7 +221,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
             // shared memory: the fixed part + two tile buffers (8192 x 8 or 4096 x 16 bytes)
-            const size_t need = csort_smem_fixed() + 2 * 8192 * 8;
+            const size_t need = csort_smem_need();
             const int cap = (size_t)maxsm >= need ? 1024 : 0;
             if (cap >= 1024 &&
                 cudaFuncSetAttribute(k_csort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need) == cudaSuccess) {
@@ -230,7 +232,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
                     if (want && cs != want) continue;
                     cudaLaunchConfig_t lc{};
                     lc.gridDim = dim3(cs);
-                    lc.blockDim = dim3(1024);
+                    lc.blockDim = dim3(csort_threads());
                     lc.dynamicSmemBytes = need;
                     cudaLaunchAttribute at{};
                     at.id = cudaLaunchAttributeClusterDimension;
@@ -568,7 +570,10 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         }
         LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, blocks(d.n, 256 * kFinItems), 256, 0, d)));
         LAUNCH(K_READY, CK(c, launch_k(c->pdl, s, k_ready, c->ntiles_ready, kReadyThreads, 0, d, mask)));
-        if (c->csort_ctas) {
+        static const bool dbg_nosort = [] { const char* e = getenv("AM_DBG_NOSORT"); return e && atoi(e); }();
+        if (dbg_nosort) {
+            // PROFILING ONLY (wrong `order`): measures how much of the round the sort holds up
+        } else if (c->csort_ctas) {
             // one cluster of csort_ctas CTAs sorts the whole ready set (am_sort.cu), on the
             // side stream: nothing else in the round reads `order` (digests and dispatch
             // take the id-ordered ready list), so it overlaps the rest of the round and
@@ -577,7 +582,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
             cudaLaunchConfig_t lc{};
             lc.gridDim = dim3(c->csort_ctas);
-            lc.blockDim = dim3(1024);
+            lc.blockDim = dim3(csort_threads());
             lc.dynamicSmemBytes = (size_t)c->csort_cap;
             lc.stream = c->side;
             cudaLaunchAttribute at{};

@@ -48,7 +48,10 @@ constexpr int kCsBits = 8;                   // digit of one global pass
 constexpr int kCsRadix = 1 << kCsBits;
 constexpr int kCsSub = 4;                    // bits of one local rank step
 constexpr int kCsSubR = 1 << kCsSub;
-constexpr int kCsThreads = 1024;
+#ifndef AM_CS_THREADS
+#define AM_CS_THREADS 1024
+#endif
+constexpr int kCsThreads = AM_CS_THREADS;    // threads per CTA (power of two, 256..1024)
 constexpr int kCsK = 8;                      // max elements per thread per tile
 // fixed shared memory: cnt[16][1024] (padded) + hist, base, run, tstart, ttot [256] + wsum[32]
 constexpr size_t kCsFixed = (size_t)(kCsSubR * kCsThreads * 33 / 32 + 5 * kCsRadix + 32) * 4;
@@ -86,6 +89,10 @@ __device__ __forceinline__ void gstore(const Dev& d, int b, int i, const E64& e)
 }
 
 size_t csort_smem_fixed() { return kCsFixed; }
+// dynamic shared memory of k_csort: the fixed part + two tile buffers of 8-byte pairs
+// (or half as many 16-byte ones), and its block size
+size_t csort_smem_need() { return kCsFixed + 2 * (size_t)kCsThreads * kCsK * 8; }
+int csort_threads() { return kCsThreads; }
 
 // block-wide exclusive scan (1024 threads); wsum: 32 words of shared memory
 __device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* wsum)
@@ -100,7 +107,7 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* wsum)
     if (lane == 31) wsum[w] = incl;
     __syncthreads();
     if (w == 0) {
-        const uint32_t x = wsum[lane];
+        const uint32_t x = lane < (kCsThreads >> 5) ? wsum[lane] : 0u;
         uint32_t s = x;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
