@@ -448,6 +448,21 @@ def run_ours(args, w, lm):
             traffic = tr.get("dram_bytes_per_launch") if tr else None
     except Exception:
         pass
+    # the dominant kernel against the SM issue rate (it is latency/issue-bound, not HBM
+    # bound): warp instructions per launch from the committed ncu --set full capture
+    # (profiles/ncu_instr.json) over the live average launch time
+    issue = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_instr.json")) as f:
+            ij = json.load(f)
+        wi = ij[dom]["warp_instructions_per_launch"]
+        pk_i = ij["issue_peak_warp_instr_per_s"]["value"]
+        ach_i = wi / avg_dom_s if avg_dom_s > 0 else 0.0
+        issue = {"kernel": dom, "achieved": ach_i, "peak": pk_i, "unit": "warp-instr/s", "frac": ach_i / pk_i,
+                 "warp_instructions_per_launch": wi,
+                 "peak_source": ij["issue_peak_warp_instr_per_s"]["derivation"]}
+    except Exception:
+        pass
     clocks = clk.summary()
     # round-level HBM traffic: ncu cold-cache DRAM bytes of every kernel of a round
     # (profiles/ncu_traffic.json) over the measured round time
@@ -490,6 +505,7 @@ def run_ours(args, w, lm):
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg, "avg_launch_us": avg_dom_s * 1e6},
         "round_hbm": round_hbm,
+        "issue_roofline": issue,
         "snapshot": snap,
         "kernel_share_warmup_us": {k: round(v * 1000.0, 2) for k, v in sorted(shares.items())},
         # D2H (am_replay_io, page-locked host arrays, state outputs aliasing the inputs):
