@@ -65,6 +65,13 @@ __device__ __forceinline__ long long duration(const am_synth& sy, int i, int s)
     return dsum;
 }
 
+// within R (R2 = R * R) for the compile-time metric
+__device__ __forceinline__ bool within2(int dx, int dy, uint32_t R2, uint32_t R, int metric)
+{
+    if (metric == AM_METRIC_LINF) return (uint32_t)abs(dx) <= R && (uint32_t)abs(dy) <= R;
+    return (uint32_t)(dx * dx) + (uint32_t)(dy * dy) <= R2;
+}
+
 // the synthetic policy (am_driver.h): random walk on the perception digest; a move into
 // a wall or off the map is cancelled
 __device__ __forceinline__ int2 policy_move(const RepDev& r, int i, int s, int2 p, unsigned long long dig)
@@ -229,6 +236,7 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
 // agent's pair tests (lane q takes partners j = q, q + G, ...; verdicts and digests are
 // combined by shuffles), lane 0 of the group does the agent's serial work.  Dynamic
 // shared memory is sized by the largest simulation (M agents).
+template <int kMetric>
 __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_rounds, int M, int G)
 {
     const Dev& d = r.d;
@@ -265,6 +273,10 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
     long long tsim = r.t_sim[b], tdone = r.tdone[b], nrounds = r.rounds[b], disp = 0;
     int act = r.active_flag[b], live_err = 0, lab = -1;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const uint32_t Rc2 = Rc * Rc, Rp = (uint32_t)d.r_p, Rp2 = Rp * Rp;
+    // R_b(lag) = (lag + 1) v + r_p in 32 bits: lags beyond lagcap give >= kRClamp anyway
+    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+    const uint32_t vv = (uint32_t)d.v, vr = (uint32_t)(d.v + d.r_p);
     __syncthreads();
     for (long long k = 0; k < max_rounds && act; k++) {
         // ---- the tracker round (k_small)
@@ -281,12 +293,13 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
                 if (j == t || B.w == ST_DONE) continue;
                 const int dx = B.x - A.x, dy = B.y - A.y;
                 if (B.z == A.z) {
-                    if (within(dx, dy, Rc, d.metric)) {
+                    if (within2(dx, dy, Rc2, Rc, kMetric)) {
                         if (t < j) suf_unite(par, (uint32_t)t, (uint32_t)j);
-                        if (within(dx, dy, (uint32_t)d.r_p, d.metric)) dig += digest_term((uint32_t)(lo + j), dx, dy);
+                        if (within2(dx, dy, Rp2, Rp, kMetric)) dig += digest_term((uint32_t)(lo + j), dx, dy);
                     }
                 } else if (!blocked && B.z < A.z) {
-                    blocked = within(dx, dy, rb_radius((long long)A.z - B.z, d.v, d.r_p), d.metric);
+                    const uint32_t R = min((uint32_t)min(A.z - B.z, lagcap) * vv + vr, kRClamp);
+                    blocked = within2(dx, dy, R * R, R, kMetric);
                 }
             }
         }
@@ -622,8 +635,12 @@ static int launch_small_replay(am_replay* rp, int64_t rounds)
     while (M * G > 1024) G /= 2;
     RK(cudaMemsetAsync(&c->d.ctl->n_active, 0, sizeof(int32_t), rp->stream));
     rp->r.d = c->d;
-    RK(launch_k(false, rp->stream, k_small_replay, (unsigned)c->d.n_sims, (unsigned)(M * G), smem, rp->r,
-                (long long)rounds, M, G));
+    if (c->d.metric == AM_METRIC_LINF)
+        RK(launch_k(false, rp->stream, k_small_replay<AM_METRIC_LINF>, (unsigned)c->d.n_sims, (unsigned)(M * G), smem,
+                    rp->r, (long long)rounds, M, G));
+    else
+        RK(launch_k(false, rp->stream, k_small_replay<AM_METRIC_L2>, (unsigned)c->d.n_sims, (unsigned)(M * G), smem,
+                    rp->r, (long long)rounds, M, G));
     return AM_OK;
 }
 
