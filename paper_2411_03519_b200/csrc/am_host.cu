@@ -304,6 +304,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     d.ncells = 1 << (d.gxlog + d.gylog);
     x->cell = 1 << clog;
     d.idbits = std::max(1, ilog2_ceil(std::max(2LL, n)));
+    d.lagcap = (int32_t)(kRClamp / (uint32_t)std::max(1, v_max)) + 1;
     {
         int lagbits = c.target_step > 0 ? ilog2_ceil((long long)c.target_step + 1) : 31;
         int bits = lagbits + d.idbits;

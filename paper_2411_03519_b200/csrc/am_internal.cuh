@@ -96,6 +96,7 @@ struct Dev {
     int32_t mxhi;          // 1 if x is the longer side (its extra high bits sit above)
     int32_t ncells;        // 1 << (gxlog + gylog)
     int32_t idbits;        // bits to hold an agent id
+    int32_t lagcap;        // step lag beyond which R_b = (lag + 1) v + r_p reaches kRClamp
     // double-buffered state
     int2* pos[2];
     int32_t* step[2];
@@ -277,6 +278,12 @@ __device__ __forceinline__ uint32_t rb_radius(long long lag, int v, int r_p)
 {
     long long R = (lag + 1) * (long long)v + r_p;
     return R > (long long)kRClamp ? kRClamp : (uint32_t)R;
+}
+
+// the same radius for a non-negative int lag in 32-bit arithmetic (d.lagcap host-computed)
+__device__ __forceinline__ uint32_t rb32(int lag, int lagcap, int v, int r_p)
+{
+    return min((uint32_t)min(lag, lagcap) * (uint32_t)v + (uint32_t)(v + r_p), kRClamp);
 }
 
 __device__ __forceinline__ bool within(int dx, int dy, uint32_t R, int metric)

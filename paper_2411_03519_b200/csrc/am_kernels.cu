@@ -676,7 +676,7 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
     uint32_t& nb2 = hs.nb2;
     uint32_t& nb1 = hs.nb1;
     uint32_t& nitems = hs.nitems;
-    const int R = (int)rb_radius((long long)as - W, d.v, d.r_p);
+    const int R = (int)rb32(as - W, d.lagcap, d.v, d.r_p);
     const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2x - 1, (ax + R) >> l2);
     const int by0 = max(0, (ay - R) >> l2), by1 = min(G2y - 1, (ay + R) >> l2);
     const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);
@@ -690,7 +690,7 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
         if (j < nb) {
             const int m2 = __ldg(d.lmin2 + mkey(d, bx, by, 4));
             ok2 = m2 < as && box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
-                                        rb_radius((long long)as - m2, d.v, d.r_p), d.metric);
+                                        rb32(as - m2, d.lagcap, d.v, d.r_p), d.metric);
         }
         unsigned mask2 = (__ballot_sync(hm, ok2) >> (16 * h)) & 0xFFFFu;
         while (mask2 && wit == kSentinel) {
@@ -703,7 +703,7 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
             const int qx = bxj * 4 + ox_l, qy = byj * 4 + oy_l;
             const int m1 = __ldg(d.lmin1 + k2 * 16 + l);
             const bool ok1 = m1 < as && box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
-                                                   ((qy + 1) << l1) - 1, rb_radius((long long)as - m1, d.v, d.r_p),
+                                                   ((qy + 1) << l1) - 1, rb32(as - m1, d.lagcap, d.v, d.r_p),
                                                    d.metric);
             unsigned mask1 = (__ballot_sync(hm, ok1) >> (16 * h)) & 0xFFFFu;
             while (mask1 && wit == kSentinel) {
@@ -719,7 +719,7 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
                 const int cx = qxi * 4 + ox_l, cy = qyi * 4 + oy_l;
                 const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
                 const bool okc = nx > e.x && e.y < as && !box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric) &&
-                                 box_within(ax, ay, X0, Y0, X1, Y1, rb_radius((long long)as - e.y, d.v, d.r_p),
+                                 box_within(ax, ay, X0, Y0, X1, Y1, rb32(as - e.y, d.lagcap, d.v, d.r_p),
                                             d.metric);
                 const int cnt = okc ? nx - e.x : 0;
                 ncells += nx > e.x ? 1u : 0u;
@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
             const bool far = idle && as > W && !(d.flags & AM_DBG_SKIP_FAR);
             nfar += (far && l == 0) ? 1u : 0u;
             // query box: far radius when the far test is due and the box is small enough
-            const int Rf = far ? (int)rb_radius((long long)as - W, d.v, d.r_p) : (int)Rc;
+            const int Rf = far ? (int)rb32(as - W, d.lagcap, d.v, d.r_p) : (int)Rc;
             int cx0 = max(0, (ax - Rf) >> cl), cx1 = min(Gx - 1, (ax + Rf) >> cl);
             int cy0 = max(0, (ay - Rf) >> cl), cy1 = min(Gy - 1, (ay + Rf) >> cl);
             const bool direct = (cx1 - cx0 + 1) * (cy1 - cy0 + 1) <= kDirect;
@@ -947,7 +947,7 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
                                 const int ky = krow(k);
                                 const int cx = cx0 + (k - ky * ncx), cy = cy0 + ky;
                                 ok = box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1,
-                                                rb_radius((long long)as - mn, d.v, d.r_p), d.metric);
+                                                rb32(as - mn, d.lagcap, d.v, d.r_p), d.metric);
                             }
                         }
                         const unsigned bm = (__ballot_sync(hm, ok) >> (16 * h)) & 0xFFFFu;
