@@ -62,6 +62,15 @@ int am_slab_halo(const am_slab_geom* g, int32_t n, const int32_t* gid, const int
                  const int32_t* steps, const uint8_t* status, const int32_t* ws, int32_t cap,
                  int32_t* send, int32_t* counts, uint8_t* sent, void* stream);
 
+/* The local tracker's input arrays (capacity cap >= n + m): slots [0, n) the owned
+ * agents (gid/pos int32[n][2]/steps/status), slots [n, n + m) the received halo
+ * records ghosts int32 [m][4] {gid, x | y<<16, step, status}, the rest DONE padding;
+ * every y translated by -y0 (the slab's window).  Outputs lpos int32 [cap][2], lsteps
+ * int32 [cap], lstatus uint8 [cap], lgid int32 [cap]. */
+int am_slab_assemble(int32_t n, const int32_t* gid, const int32_t* pos, const int32_t* steps,
+                     const uint8_t* status, int32_t m, const int32_t* ghosts, int32_t cap, int32_t y0,
+                     int32_t* lpos, int32_t* lsteps, uint8_t* lstatus, int32_t* lgid, void* stream);
+
 /* Merge records of the local round over n_local agents (owned first, then ghosts).
  * labels/blocked: am_clusters / am_blocked output (local indices); sent: from
  * am_slab_halo (owned part).  links: int32 [cap][2]; bads: int32 [cap];

@@ -27,6 +27,38 @@ __global__ void k_slab_watermark(int n, const int32_t* __restrict__ steps, const
     }
 }
 
+// the local tracker's input: owned agents (slots [0, n)), received ghosts ([n, n + m)),
+// DONE padding up to cap; y translated by -y0 (the slab's halo window)
+__global__ void k_slab_assemble(int n, const int32_t* __restrict__ gid, const int2* __restrict__ pos,
+                                const int32_t* __restrict__ steps, const uint8_t* __restrict__ status, int m,
+                                const int4* __restrict__ ghosts, int cap, int y0, int2* __restrict__ lpos,
+                                int32_t* __restrict__ lsteps, uint8_t* __restrict__ lstatus,
+                                int32_t* __restrict__ lgid)
+{
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < cap; k += gridDim.x * blockDim.x) {
+        int2 p = make_int2(0, 0);
+        int s = 0, g = 0;
+        uint8_t st = ST_DONE;
+        if (k < n) {
+            p = pos[k];
+            p.y -= y0;
+            s = steps[k];
+            st = status[k];
+            g = gid[k];
+        } else if (k < n + m) {
+            const int4 r = ghosts[k - n];
+            p = make_int2(r.y & 0xFFFF, (r.y >> 16) - y0);
+            s = r.z;
+            st = (uint8_t)r.w;
+            g = r.x;
+        }
+        lpos[k] = p;
+        lsteps[k] = s;
+        lstatus[k] = st;
+        lgid[k] = g;
+    }
+}
+
 __global__ void k_slab_init2(int32_t* out)
 {
     out[0] = INT_MAX;
@@ -188,6 +220,19 @@ extern "C" int am_slab_watermark(int32_t n, const int32_t* steps, const uint8_t*
     k_slab_init2<<<1, 1, 0, s>>>(out);
     if (n > 0) k_slab_watermark<<<std::min(nblk(n), 1184u), 256, 0, s>>>(n, steps, status, out);
     return ck(cudaGetLastError());
+}
+
+extern "C" int am_slab_assemble(int32_t n, const int32_t* gid, const int32_t* pos, const int32_t* steps,
+                                const uint8_t* status, int32_t m, const int32_t* ghosts, int32_t cap, int32_t y0,
+                                int32_t* lpos, int32_t* lsteps, uint8_t* lstatus, int32_t* lgid, void* stream)
+{
+    if (n < 0 || m < 0 || cap < n + m || (n && (!gid || !pos || !steps || !status)) || (m && !ghosts) ||
+        (cap && (!lpos || !lsteps || !lstatus || !lgid)))
+        return AM_E_ARG;
+    if (cap == 0) return AM_OK;
+    k_slab_assemble<<<std::min((cap + 255) / 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
+        n, gid, (const int2*)pos, steps, status, m, (const int4*)ghosts, cap, y0, (int2*)lpos, lsteps, lstatus, lgid);
+    return cudaGetLastError() == cudaSuccess ? AM_OK : AM_E_CUDA;
 }
 
 extern "C" int am_slab_halo(const am_slab_geom* g, int32_t n, const int32_t* gid, const int32_t* pos,

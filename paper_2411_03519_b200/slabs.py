@@ -142,22 +142,11 @@ class SlabRank:
             self._alloc()
         n, nl = self.n, self.n + m
         self._window(self.ws)
-        self.lpos[:n] = self.pos
-        self.lsteps[:n] = self.steps
-        self.lstatus[:n] = self.status
-        self.lgid[:n] = self.gid
-        if m:
-            xy = ghosts[:, 1]
-            self.lpos[n:nl, 0] = xy & 0xFFFF
-            self.lpos[n:nl, 1] = xy >> 16
-            self.lsteps[n:nl] = ghosts[:, 2]
-            self.lstatus[n:nl] = ghosts[:, 3].to(torch.uint8)
-            self.lgid[n:nl] = ghosts[:, 0]
-        self.lstatus[nl:] = DONE
-        self.lsteps[nl:] = 0
-        self.lpos[nl:] = 0
-        if self.y0:
-            self.lpos[:nl, 1] -= self.y0
+        ghosts = ghosts.contiguous()
+        check(self.L.am_slab_assemble(n, self.gid.data_ptr(), self.pos.data_ptr(), self.steps.data_ptr(),
+                                      self.status.data_ptr(), m, ghosts.data_ptr() if m else None, self.n_cap,
+                                      self.y0, self.lpos.data_ptr(), self.lsteps.data_ptr(),
+                                      self.lstatus.data_ptr(), self.lgid.data_ptr(), self.stream))
         tr = self.tracker
         # stream-ordered local round (AM_ASYNC): no host synchronisation until the link
         # counts; a rejected state would surface at the next synchronising call
