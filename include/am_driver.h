@@ -84,6 +84,18 @@ int am_replay_step(am_replay* r, uint8_t* mask, int32_t* order, int32_t* labels,
  * per-agent trajectory hash chained at every commit). */
 int am_replay_results(am_replay* r, int64_t* T_ooo, int64_t* rounds, uint64_t* traj);
 
+/* Finite LLM capacity (call before the first round): at most
+ * `capacity` agent-steps in service at once (0 = infinite, the default).  Ready clusters
+ * are queued (members RUNNING, moves computed at queueing) and started -- completion =
+ * start + max member duration -- in the order of the key (step << 32 | label) when
+ * priority != 0 (the paper's step-priority ready_queue, section 3.5),
+ * else (round << 32 | label) (FIFO); strict order, a cluster larger than the capacity
+ * starts only when nothing is in service.  Only the fused per-simulation path
+ * (<= 1024 agents per simulation) supports it, through am_replay_run / am_replay_launch
+ * (am_replay_step / am_replay_io return AM_E_ARG).  Errors: AM_E_ARG, AM_E_STATE (rounds
+ * already ran). */
+int am_replay_set_capacity(am_replay* r, int64_t capacity, int32_t priority);
+
 /* Total agent-steps dispatched so far (host). */
 int am_replay_dispatched(am_replay* r, int64_t* agent_steps);
 

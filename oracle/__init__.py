@@ -94,6 +94,8 @@ def lib():
         L.orc_lockstep.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int32, vp, vp, vp, vp]
         L.orc_replay.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int64, vp, vp, vp, vp, vp,
                                  C.POINTER(Log)]
+        L.orc_replay_cap.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int64, C.c_int64, C.c_int32,
+                                     vp, vp, vp, vp, vp, C.POINTER(Log)]
         _lib = L
     return _lib
 
@@ -242,8 +244,10 @@ def lockstep(p: Params, sy: SynthTables, x0, y0, T: int):
 
 
 def replay(p: Params, sy: SynthTables, x0, y0, Q: int = 0, log_rounds: int = 0,
-           log_entries: int = 0, check: bool = False):
-    """Out-of-order replay (orc_replay).  p.target is the number of steps."""
+           log_entries: int = 0, check: bool = False, capacity: int = 0, priority: bool = True):
+    """Out-of-order replay (orc_replay; orc_replay_cap with a finite capacity of
+    `capacity` agent-steps in service, clusters started in step-priority or FIFO order).
+    p.target is the number of steps."""
     x, y = _i32(x0).copy(), _i32(y0).copy()
     n = len(x)
     traj = np.zeros(n, np.uint64)
@@ -256,8 +260,8 @@ def replay(p: Params, sy: SynthTables, x0, y0, Q: int = 0, log_rounds: int = 0,
     elab = np.zeros(max(log_entries, 1), np.int32)
     lg = Log(log_rounds, log_entries, _p(rt).value, _p(rs).value, _p(rn).value, _p(eid).value,
              _p(elab).value, 0, 0, int(check), 0, 0)
-    rc = lib().orc_replay(C.byref(p), C.byref(sy.s), n, int(Q), _p(x), _p(y), _p(traj), _p(tooo),
-                          _p(rounds), C.byref(lg))
+    rc = lib().orc_replay_cap(C.byref(p), C.byref(sy.s), n, int(Q), int(capacity), int(bool(priority)), _p(x),
+                              _p(y), _p(traj), _p(tooo), _p(rounds), C.byref(lg))
     if rc != OK:
         raise RuntimeError(f"orc_replay rc={rc}")
     nr = min(lg.n_rounds, log_rounds)

@@ -442,11 +442,34 @@ typedef struct {
  * }
  * x,y in place (start at step 0, all IDLE).  traj[i] as in orc_lockstep.
  */
+/*
+ * Finite LLM capacity (our model, the paper serves clusters from a
+ * priority ready_queue, section 3.5, "no preemption"):
+ * capacity K > 0 agent-steps may be in service at once.  A ready cluster is queued
+ * (its members become RUNNING, moves computed then) with the key
+ *   priority = 1: (step << 32) | label      (earlier steps first)
+ *   priority = 0: (round  << 32) | label    (FIFO by the round that queued it)
+ * with label the cluster's global min id and round the simulation's round index.
+ * After each round's enqueueing, clusters start in key order while they fit
+ * (strict order, no bypass; a cluster larger than K starts only when nothing is in
+ * service): completion = t + max member duration.  K = 0: infinite capacity, every
+ * ready cluster starts at once (orc_replay).
+ */
+int orc_replay_cap(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q, int64_t K, int32_t priority,
+                   int32_t* x, int32_t* y, uint64_t* traj, int64_t* T_ooo, int64_t* rounds, orc_log* log);
+
 int orc_replay(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q,
                int32_t* x, int32_t* y, uint64_t* traj, int64_t* T_ooo, int64_t* rounds,
                orc_log* log)
 {
-    if (p->target <= 0) return ORC_E_ARG;
+    return orc_replay_cap(p, sy, n, Q, 0, 1, x, y, traj, T_ooo, rounds, log);
+}
+
+int orc_replay_cap(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q, int64_t K, int32_t priority,
+                   int32_t* x, int32_t* y, uint64_t* traj, int64_t* T_ooo, int64_t* rounds, orc_log* log)
+{
+    if (p->target <= 0 || K < 0) return ORC_E_ARG;
+    uint64_t* qkey = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));   /* queued members' keys */
     int32_t* step = (int32_t*)calloc(n ? n : 1, sizeof(int32_t));
     uint8_t* status = (uint8_t*)calloc(n ? n : 1, 1);
     int64_t* tc = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
@@ -527,9 +550,37 @@ int orc_replay(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q,
             for (int32_t k = 0; k < nr; k++) {
                 int32_t a = ord[k];
                 tc[lo + a] = t + cmax[lo + lab[a]];
+                if (K > 0) {   /* finite capacity: queued, started below */
+                    tc[lo + a] = INT64_MAX;
+                    qkey[lo + a] = ((uint64_t)(priority ? (uint64_t)ss[a] : (uint64_t)(nr_b - 1)) << 32) |
+                                   (uint64_t)(uint32_t)(lo + lab[a]);
+                }
                 /* digest over the sim, in global ids (perceived agents are cluster-mates) */
                 uint64_t dg = orc_digest(p, lo, hi, x, y, step, status, lo + a);
                 orc_policy_move(p, sy, lo + a, ss[a], sx[a], sy_[a], dg, &mvx[lo + a], &mvy[lo + a]);
+            }
+            if (K > 0) {
+                /* in service: started members not yet committed */
+                int64_t busy = 0;
+                for (int32_t i = 0; i < m; i++)
+                    if (sst[i] == ORC_RUNNING && tc[lo + i] != INT64_MAX) busy++;
+                for (;;) {   /* start queued clusters in key order while they fit */
+                    uint64_t best = UINT64_MAX;
+                    for (int32_t i = 0; i < m; i++)
+                        if (sst[i] == ORC_RUNNING && tc[lo + i] == INT64_MAX && qkey[lo + i] < best) best = qkey[lo + i];
+                    if (best == UINT64_MAX) break;
+                    int64_t size = 0, dmax = 0;
+                    for (int32_t i = 0; i < m; i++)
+                        if (sst[i] == ORC_RUNNING && tc[lo + i] == INT64_MAX && qkey[lo + i] == best) {
+                            size++;
+                            int64_t d = orc_duration(sy, lo + i, ss[i]);
+                            if (d > dmax) dmax = d;
+                        }
+                    if (busy > 0 && busy + size > K) break;
+                    for (int32_t i = 0; i < m; i++)
+                        if (sst[i] == ORC_RUNNING && tc[lo + i] == INT64_MAX && qkey[lo + i] == best) tc[lo + i] = t + dmax;
+                    busy += size;
+                }
             }
             /* next event */
             int64_t tn = INT64_MAX;
@@ -544,7 +595,7 @@ int orc_replay(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q,
         rounds[b] = nr_b;
         free(lab); free(msk); free(ord); free(blk);
     }
-    free(step); free(status); free(tc); free(mvx); free(mvy); free(cmax);
+    free(step); free(status); free(tc); free(mvx); free(mvy); free(cmax); free(qkey);
     if (rc == ORC_OK && log && log->n_rounds >= log->cap_rounds && log->cap_rounds > 0) {
         /* log truncated is not an error; callers compare n_rounds with cap */
     }

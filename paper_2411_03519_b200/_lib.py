@@ -91,6 +91,7 @@ SIGNATURES = {
     "am_replay_stream": (_vp, [_vp]),
     "am_slab_watermark": (C.c_int, [_i32, _vp, _vp, _vp, _vp]),
     "am_slab_halo": (C.c_int, [C.POINTER(SlabGeom), _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp]),
+    "am_replay_set_capacity": (C.c_int, [_vp, C.c_int64, _i32]),
     "am_slab_assemble": (C.c_int, [_i32, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "am_slab_links": (C.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "am_slab_merge": (C.c_int, [C.POINTER(SlabGeom), _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32,

@@ -34,6 +34,9 @@ struct RepDev {
     long long* dispatched;      // [1]
     int32_t* liveness;          // [1]
     Chain* chain;               // last-block counter of k_disp_b
+    unsigned long long* qkey;   // [n] queue key of a queued (RUNNING, not started) agent (finite capacity)
+    long long K;                // agent-steps in service at once; 0 = infinite capacity
+    int32_t prio;               // 1: queue by (step, label); 0: by (round, label)
 };
 
 __device__ __forceinline__ int sim_of(const Dev& d, int i)
@@ -245,9 +248,11 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
     unsigned long long* stcl = reinterpret_cast<unsigned long long*>(stc + M);   // [M] cluster time by label
     int2* snp = reinterpret_cast<int2*>(stcl + M);                               // [M] move computed at dispatch
     int4* sa = reinterpret_cast<int4*>(snp + M);                                 // [M] {x, y, step, status}
-    uint32_t* par = reinterpret_cast<uint32_t*>(sa + M);
+    unsigned long long* sq = reinterpret_cast<unsigned long long*>(sa + M);   // [M] queue keys (finite capacity)
+    uint32_t* par = reinterpret_cast<uint32_t*>(sq + M);
     uint8_t* sbad = reinterpret_cast<uint8_t*>(par + M);
-    __shared__ unsigned long long s_tmin;
+    __shared__ unsigned long long s_tmin, s_best;
+    __shared__ long long s_busy, s_size, s_dmax;
     __shared__ int s_any, s_fin, s_nr;
     const int b = blockIdx.x;
     const int t = threadIdx.x / G, q = threadIdx.x % G;   // agent slot, lane within its group
@@ -268,6 +273,7 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
         sa[t] = make_int4(p.x, p.y, s, st);
         stc[t] = r.tcommit[i];
         snp[t] = r.newpos[i];
+        sq[t] = r.qkey[i];
         traj = r.traj[i];
     }
     long long tsim = r.t_sim[b], tdone = r.tdone[b], nrounds = r.rounds[b], disp = 0;
@@ -324,6 +330,37 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
             stc[t] = (long long)stcl[lab];
             snp[t] = policy_move(r, i, A.z, make_int2(A.x, A.y), dig);
             atomicAdd(&s_nr, 1);
+            if (r.K > 0) {   // finite capacity: queued now, started below in key order
+                stc[t] = LLONG_MAX;
+                sq[t] = ((unsigned long long)(r.prio ? (uint32_t)A.z : (uint32_t)nrounds) << 32) | (uint32_t)(lo + lab);
+            }
+        }
+        if (r.K > 0) {
+            // start queued clusters in key order while they fit (strict order; a cluster
+            // larger than K starts only when nothing is in service) -- orc_replay_cap
+            if (threadIdx.x == 0) s_busy = 0;
+            __syncthreads();
+            if (mine && lead && sa[t].w == ST_RUNNING && stc[t] != LLONG_MAX) atomicAdd((unsigned long long*)&s_busy, 1ull);
+            for (;;) {
+                if (threadIdx.x == 0) { s_best = ~0ull; s_size = 0; s_dmax = 0; }
+                __syncthreads();
+                const bool queued = mine && lead && sa[t].w == ST_RUNNING && stc[t] == LLONG_MAX;
+                if (queued) atomicMin(&s_best, sq[t]);
+                __syncthreads();
+                const unsigned long long best = s_best;
+                if (best == ~0ull) break;
+                const bool head = queued && sq[t] == best;
+                if (head) {
+                    atomicAdd((unsigned long long*)&s_size, 1ull);
+                    atomicMax((unsigned long long*)&s_dmax, (unsigned long long)duration(r.sy, i, sa[t].z));
+                }
+                __syncthreads();
+                if (s_busy > 0 && s_busy + s_size > r.K) break;
+                if (head) stc[t] = tsim + s_dmax;
+                __syncthreads();
+                if (threadIdx.x == 0) s_busy += s_size;
+            }
+            __syncthreads();
         }
         if (mine && lead && (rdy || st == ST_RUNNING)) atomicMin(&s_tmin, (unsigned long long)stc[t]);
         __syncthreads();
@@ -331,7 +368,7 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
         const unsigned long long tn = s_tmin;
         disp += s_nr;
         nrounds += 1;
-        if (tn == ~0ull) {   // agents left, nothing running: liveness violation
+        if (tn >= (unsigned long long)LLONG_MAX) {   // agents left, nothing in service: liveness violation
             live_err = 1;
             break;
         }
@@ -366,12 +403,13 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
         d.status[c][i] = (uint8_t)S.w;
         r.tcommit[i] = stc[t];
         r.newpos[i] = snp[t];
+        r.qkey[i] = sq[t];
         r.traj[i] = traj;
         if (lab >= 0 || S.w == ST_DONE) d.labels[i] = S.w == ST_DONE ? -1 : lo + lab;
     }
     if (threadIdx.x == 0) { s_tmin = ~0ull; s_any = 0; }
     __syncthreads();
-    if (mine && lead && S.w == ST_RUNNING) atomicMin(&s_tmin, (unsigned long long)stc[t]);
+    if (mine && lead && S.w == ST_RUNNING && stc[t] != LLONG_MAX) atomicMin(&s_tmin, (unsigned long long)stc[t]);
     if (mine && lead && S.w != ST_DONE) atomicAdd(&s_any, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -509,7 +547,7 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
     auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~size_t(255); return o; };
     size_t o_tc = take(8 * n), o_np = take(8 * n), o_tr = take(8 * n), o_tcl = take(8 * n);
     size_t o_ts = take(8 * S), o_tn = take(8 * S), o_td = take(8 * S), o_rd = take(8 * S), o_af = take(4 * S);
-    size_t o_disp = take(8), o_live = take(4), o_chain = take(sizeof(Chain));
+    size_t o_disp = take(8), o_live = take(4), o_chain = take(sizeof(Chain)), o_qk = take(8 * n);
     size_t o_mask = take(n), o_order = take(4 * n);
     cudaError_t e = cudaMalloc(&rp->mem, off);
     if (e != cudaSuccess) { delete rp; return rp_err(nullptr, e, "cudaMalloc"); }
@@ -531,6 +569,9 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
     r.dispatched = (long long*)(b + o_disp);
     r.liveness = (int32_t*)(b + o_live);
     r.chain = (Chain*)(b + o_chain);
+    r.qkey = (unsigned long long*)(b + o_qk);
+    r.K = 0;
+    r.prio = 1;
     rp->mask = (uint8_t*)(b + o_mask);
     rp->order = (int32_t*)(b + o_order);
     r.order = ctx->path == 1 ? ctx->d.rid : rp->order;
@@ -594,6 +635,11 @@ static int finish_check(am_replay* rp, int64_t* active)
 
 static int ensure_graphs(am_replay* rp)
 {
+    if (rp->r.K > 0) {   // finite capacity exists only in the persistent per-simulation kernel
+        rp->ctx->err = "finite LLM capacity runs through am_replay_run / am_replay_launch on the fused "
+                       "per-simulation path (<= 1024 agents per simulation, tracing off)";
+        return AM_E_ARG;
+    }
     const unsigned pm = rp->ctx->prof.on ? rp->ctx->prof.mask : 0u;
     if (pm != rp->graph_prof || rp->ctx->d.flags != rp->graph_flags) {  // baked in at capture
         if (rp->g1) cudaGraphExecDestroy(rp->g1);
@@ -613,6 +659,7 @@ static int ensure_graphs(am_replay* rp)
 static bool small_persistent(am_replay* rp)
 {
     am_ctx* c = rp->ctx;
+    if (rp->r.K > 0) return c->path == 0;   // finite capacity: only the persistent kernel has it
     if (c->path != 0 || c->prof.on) return false;
     static const int off = [] { const char* e = getenv("AM_SMALL_PERSIST"); return e && atoi(e) == 0; }();
     return !off;   // AM_SMALL_PERSIST=0: the multi-kernel rounds (ablation)
@@ -621,7 +668,7 @@ static int launch_small_replay(am_replay* rp, int64_t rounds)
 {
     am_ctx* c = rp->ctx;
     const int M = c->small_threads;   // >= agents of the largest simulation, multiple of 32
-    const size_t smem = (size_t)M * (8 + 8 + 8 + 16 + 4 + 1);
+    const size_t smem = (size_t)M * (8 + 8 + 8 + 16 + 8 + 4 + 1);
     // lanes per agent: as many as one CTA of <= 1024 threads holds while all the
     // simulations' CTAs fit in half the GPU's thread slots (measured: C1 G = 32 3.0x
     // over G = 1; C3's 4096 simulations are best at G = 1)
@@ -633,6 +680,13 @@ static int launch_small_replay(am_replay* rp, int64_t rounds)
         while (G * 2 <= want) G *= 2;
     }
     while (M * G > 1024) G /= 2;
+    static bool attr = [] {   // > 48 KB of dynamic shared memory for 1024-agent simulations
+        cudaFuncSetAttribute(k_small_replay<AM_METRIC_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(k_small_replay<AM_METRIC_LINF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaGetLastError();
+        return true;
+    }();
+    (void)attr;
     RK(cudaMemsetAsync(&c->d.ctl->n_active, 0, sizeof(int32_t), rp->stream));
     rp->r.d = c->d;
     if (c->d.metric == AM_METRIC_LINF)
@@ -660,9 +714,31 @@ extern "C" int am_replay_run(am_replay* rp, int64_t max_rounds, int64_t* active)
     return finish_check(rp, active);
 }
 
+extern "C" int am_replay_set_capacity(am_replay* rp, int64_t capacity, int32_t priority)
+{
+    if (!rp || capacity < 0) return AM_E_ARG;
+    long long rounds = 0;
+    RK(cudaMemcpy(&rounds, rp->r.rounds, sizeof rounds, cudaMemcpyDeviceToHost));   // sim 0's round count
+    if (rounds != 0) {
+        rp->ctx->err = "am_replay_set_capacity: only before the first round";
+        return AM_E_STATE;
+    }
+    if (capacity > 0 && !(rp->ctx->path == 0)) {
+        rp->ctx->err = "am_replay_set_capacity: finite capacity needs the fused per-simulation path";
+        return AM_E_ARG;
+    }
+    rp->r.K = capacity;
+    rp->r.prio = priority ? 1 : 0;
+    return AM_OK;
+}
+
 extern "C" int am_replay_step(am_replay* rp, uint8_t* mask, int32_t* order, int32_t* labels, int32_t* n_ready)
 {
     if (!rp) return AM_E_ARG;
+    if (rp->r.K > 0) {
+        rp->ctx->err = "am_replay_step: not available with a finite capacity (use am_replay_run)";
+        return AM_E_ARG;
+    }
     int rc = enqueue_round(rp);
     if (rc) return rc;
     am_ctx* c = rp->ctx;

@@ -22,7 +22,7 @@ class Replay:
     def __init__(self, map_w, map_h, r_p, v, x0, y0, steps_target, *, n_sims=1, wall=None,
                  lat=None, cdf32=None, vals=None, base_us=5000, lat_seed=4, policy_seed=3,
                  dur_table=None, policy=0, quantum_us=0, cell=0, metric="l2", force=None,
-                 stats=False, device="cuda"):
+                 stats=False, capacity=0, priority=True, device="cuda"):
         self.device = torch.device(device)
         n = len(x0)
         self.n = n
@@ -56,6 +56,8 @@ class Replay:
         self.h = h
         self.L = L
         self.n_sims = n_sims
+        if capacity:
+            check(L.am_replay_set_capacity(h, int(capacity), 1 if priority else 0), self.tracker.ctx)
 
     @classmethod
     def from_workload(cls, w, lm, **kw):

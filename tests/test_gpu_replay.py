@@ -179,3 +179,33 @@ def test_persistent_small_replay_equals_round_kernels(name, n_sims):
     same()
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("name,steps,n_sims,K,prio", [
+    ("C1", 300, None, 1, True),
+    ("C1", 300, None, 4, False),
+    ("C1", 300, None, 8, True),
+    ("C2", 60, None, 32, True),
+    ("C2", 60, None, 32, False),
+    ("C3", 120, 16, 3, True),
+])
+def test_capacity_replay_vs_oracle(name, steps, n_sims, K, prio):
+    """Finite LLM capacity (am_replay_set_capacity, persistent per-simulation kernel) vs
+    orc_replay_cap: T_ooo, round counts, final positions and trajectory hashes, bit for
+    bit; the outcome equals lock-step's."""
+    w = amgen.config(name, steps=steps, n=n_sims)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, n_sims=w.n_sims)
+    r = O.replay(p, sy, w.x, w.y, Q=w.Q, capacity=K, priority=prio)
+    rep = Replay.from_workload(w, lm, capacity=K, priority=prio)
+    rep.run_to_end()
+    res = rep.results()
+    for k in ("T_ooo", "rounds", "x", "y", "traj"):
+        np.testing.assert_array_equal(res[k], r[k], err_msg=k)
+    ls = O.lockstep(p, sy, w.x, w.y, w.steps)
+    np.testing.assert_array_equal(res["traj"], ls["traj"])
+    assert rep.dispatched() == len(w.x) * w.steps
+    with pytest.raises(Exception):
+        rep.step()   # finite capacity exists only in the persistent kernel
+    rep.close()

@@ -276,3 +276,58 @@ def test_duration_table_statistics():
     d = np.array([O.duration(sy, i, s) for i in range(40) for s in range(100)])
     k_mean = ((d - amgen.BASE_US) > 0).mean()
     assert 0.07 < k_mean < 0.17         # P(K>0) = 0.12 for the full-day profile
+
+
+# ------------------------------------------------------------------ finite capacity (NEXT #2)
+def test_capacity_one_is_sequential():
+    """K = 1 with pairwise far-apart (never coupled, never blocked) agents, exact events:
+    one agent-step in service at a time, back to back -> T_ooo = sum of all durations."""
+    rng = np.random.default_rng(11)
+    n, T = 5, 4
+    L = rng.integers(1, 50, size=(n, T))
+    p = O.params(400, 4, 4, 1, target=T)
+    sy = _stay_synth(L)
+    for prio in (True, False):
+        r = O.replay(p, sy, np.arange(n) * 40, np.zeros(n), capacity=1, priority=prio, check=True)
+        assert int(r["T_ooo"][0]) == int(L.sum())
+        assert r["violations"] == 0
+
+
+def test_capacity_by_hand():
+    """Worked by hand (exact events, far-apart agents, keys (step << 32) | label).
+    K = 1, A0 = [3, 3], A1 = [1, 2]: t=0 A0 runs [0,3); t=3 A1 (step 0) before A0
+    (step 1) [3,4); A0 [4,7); A1 [7,9) -> T = 9.
+    K = 2, A0 = [1, 1], A1 = [10, 1], A2 = [1, 1]: t=0 A0 [0,1) and A1 [0,10), A2 waits;
+    t=1 A2 (step 0) before A0 (step 1) [1,2); t=2 A0 [2,3); t=3 A2 [3,4); t=10 A1 [10,11)
+    -> T = 11.  FIFO keys (round << 32) | label give the same orders here."""
+    p = O.params(400, 4, 4, 1, target=2)
+    for prio in (True, False):
+        r = O.replay(p, _stay_synth([[3, 3], [1, 2]]), [0, 40], [0, 0], capacity=1, priority=prio)
+        assert int(r["T_ooo"][0]) == 9
+        r = O.replay(p, _stay_synth([[1, 1], [10, 1], [1, 1]]), [0, 40, 80], [0, 0, 0], capacity=2, priority=prio)
+        assert int(r["T_ooo"][0]) == 11
+
+
+@pytest.mark.parametrize("K", [1, 4, 16])
+def test_capacity_keeps_the_outcome(K):
+    """I4 with finite capacity: the schedule changes, the outcome does not; every
+    agent's steps are sequential (T_ooo >= max_i sum_s L_is); with every cluster within
+    the capacity (C1 clusters have <= 3 members) work conservation gives
+    T_ooo >= sum of durations / K; K >= n equals infinite capacity bit for bit."""
+    w = amgen.config("C1", steps=60)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps)
+    ls = O.lockstep(p, sy, w.x, w.y, w.steps)
+    durs = np.array([[O.duration(sy, i, s) for s in range(w.steps)] for i in range(len(w.x))])
+    for prio in (True, False):
+        r = O.replay(p, sy, w.x, w.y, capacity=K, priority=prio, check=True)
+        assert r["violations"] == 0
+        np.testing.assert_array_equal(r["traj"], ls["traj"])
+        assert r["T_ooo"][0] >= durs.sum(1).max()
+        if K >= 3:
+            assert r["T_ooo"][0] * K >= durs.sum()
+    inf = O.replay(p, sy, w.x, w.y)
+    big = O.replay(p, sy, w.x, w.y, capacity=len(w.x))
+    for k in ("T_ooo", "rounds", "traj"):
+        np.testing.assert_array_equal(inf[k], big[k])
