@@ -24,7 +24,9 @@
  *   mix64 = splitmix64 finaliser; key3(s,a,b) = mix64(mix64(mix64(s+a)+b))
  *   digest_i = sum_{j perceived} mix64((j<<32) ^ ((u16)dx<<16) ^ (u16)dy),
  *              perceived = same-step non-DONE j != i with dist <= radius_p
- *   h = mix64(key3(policy_seed, i, s) + digest_i); move = {0,+x,-x,+y,-y}[h % 5],
+ *   h = mix64(key3(policy_seed, i, s) + digest_i); move = {0,+x,-x,+y,-y}[h % 5]
+ *       (policy 2, the 8-connected walk for the L-infinity metric: those five then
+ *       (+1,+1), (-1,+1), (+1,-1), (-1,-1), [h % 9]),
  *       cancelled if the target tile is a wall or off the map
  *   K = vals[min{m : (key3(lat_seed,i,s) >> 32) < cdf32[m]}]
  *   dur(i,s) = base_us + sum_{k<K} lat[key3(lat_seed ^ 0xC0FFEE, (i<<20) ^ s, k) >> 54]
@@ -54,7 +56,7 @@ typedef struct {
     const uint8_t* wall;        /* [map_h*map_w] row-major, 1 = wall; NULL = open map      */
     const int64_t* dur_table;   /* optional explicit durations [n_agents][dur_T]; NULL     */
     int32_t  dur_T;
-    int32_t  policy;            /* 0 = random walk, 1 = always stay                         */
+    int32_t  policy;            /* 0 = random walk, 1 = always stay, 2 = 8-connected walk   */
 } am_synth;
 
 typedef struct am_replay am_replay;

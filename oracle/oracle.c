@@ -359,10 +359,13 @@ uint64_t orc_digest(const orc_params* p, int32_t lo, int32_t hi, const int32_t* 
 void orc_policy_move(const orc_params* p, const orc_synth* sy, int32_t i, int32_t s,
                      int32_t px, int32_t py, uint64_t digest, int32_t* nx, int32_t* ny)
 {
-    static const int32_t MX[5] = {0, 1, -1, 0, 0};
-    static const int32_t MY[5] = {0, 0, 0, 1, -1};
+    /* policy 0: 4-connected random walk {stay,+x,-x,+y,-y}[h % 5]; 1: stay;
+     * 2: 8-connected random walk (with the L-infinity metric a
+     *    diagonal move is within v = 1): {the 5 above, (+1,+1), (-1,+1), (+1,-1), (-1,-1)}[h % 9] */
+    static const int32_t MX[9] = {0, 1, -1, 0, 0, 1, -1, 1, -1};
+    static const int32_t MY[9] = {0, 0, 0, 1, -1, 1, 1, -1, -1};
     uint64_t h = orc_mix64(orc_key3(sy->policy_seed, (uint64_t)(uint32_t)i, (uint64_t)(uint32_t)s) + digest);
-    int32_t m = sy->policy == 1 ? 0 : (int32_t)(h % 5);
+    int32_t m = sy->policy == 1 ? 0 : sy->policy == 2 ? (int32_t)(h % 9) : (int32_t)(h % 5);
     int32_t qx = px + MX[m], qy = py + MY[m];
     int ok = qx >= 0 && qx < p->map_w && qy >= 0 && qy < p->map_h;
     if (ok && sy->wall && sy->wall[(int64_t)qy * p->map_w + qx]) ok = 0;

@@ -79,12 +79,15 @@ __device__ __forceinline__ bool within2(int dx, int dy, uint32_t R2, uint32_t R,
 // a wall or off the map is cancelled
 __device__ __forceinline__ int2 policy_move(const RepDev& r, int i, int s, int2 p, unsigned long long dig)
 {
+    // policy 0: {stay, +x, -x, +y, -y}[h % 5]; 1: stay; 2: the 8-connected walk (for the
+    // L-infinity metric): the five above, then (+1,+1), (-1,+1), (+1,-1), (-1,-1) [h % 9]
     int mv = 0;
-    if (r.sy.policy == 0) {
+    if (r.sy.policy == 0 || r.sy.policy == 2) {
         const unsigned long long h = mix64(key3(r.sy.policy_seed, (uint32_t)i, (uint32_t)s) + dig);
-        mv = (int)(h % 5ull);
+        mv = (int)(h % (r.sy.policy == 2 ? 9ull : 5ull));
     }
-    const int qx = p.x + (mv == 1) - (mv == 2), qy = p.y + (mv == 3) - (mv == 4);
+    const int qx = p.x + (mv == 1 || mv == 5 || mv == 7) - (mv == 2 || mv == 6 || mv == 8);
+    const int qy = p.y + (mv == 3 || mv == 5 || mv == 6) - (mv == 4 || mv == 7 || mv == 8);
     bool ok = qx >= 0 && qx < r.d.map_w && qy >= 0 && qy < r.d.map_h;
     if (ok && r.sy.wall && r.sy.wall[(long long)qy * r.d.map_w + qx]) ok = false;
     return ok ? make_int2(qx, qy) : p;

@@ -209,3 +209,22 @@ def test_capacity_replay_vs_oracle(name, steps, n_sims, K, prio):
     with pytest.raises(Exception):
         rep.step()   # finite capacity exists only in the persistent kernel
     rep.close()
+
+
+@pytest.mark.parametrize("path", [None, "binned"])
+def test_linf_eight_connected_replay_vs_oracle(path):
+    """NEXT #4 variant (L-infinity metric, 8-connected walk) on both GPU paths vs the
+    oracle: T_ooo, rounds, final positions, trajectories; outcome == lock-step."""
+    w = amgen.config("C1", steps=200)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall, policy=2)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, metric=O.LINF)
+    r = O.replay(p, sy, w.x, w.y, Q=w.Q)
+    rep = Replay.from_workload(w, lm, policy=2, metric="linf", force=path)
+    rep.run_to_end()
+    res = rep.results()
+    for k in ("T_ooo", "rounds", "x", "y", "traj"):
+        np.testing.assert_array_equal(res[k], r[k], err_msg=k)
+    ls = O.lockstep(p, sy, w.x, w.y, w.steps)
+    np.testing.assert_array_equal(res["traj"], ls["traj"])
+    rep.close()

@@ -331,3 +331,21 @@ def test_capacity_keeps_the_outcome(K):
     big = O.replay(p, sy, w.x, w.y, capacity=len(w.x))
     for k in ("T_ooo", "rounds", "traj"):
         np.testing.assert_array_equal(inf[k], big[k])
+
+
+def test_linf_eight_connected_walk_keeps_the_outcome():
+    """NEXT #4 variant: L-infinity metric with the 8-connected walk (policy 2; a diagonal
+    move is within v = 1 under L-infinity).  Diagonal moves happen, the OoO replay keeps
+    the validity condition and ends exactly where lock-step ends."""
+    w = amgen.config("C1", steps=120)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall, policy=2)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, metric=O.LINF)
+    one = O.lockstep(O.params(w.map_w, w.map_h, w.r_p, w.v, target=1, metric=O.LINF), sy, w.x, w.y, 1)
+    dx, dy = one["x"] - w.x, one["y"] - w.y
+    assert np.any((dx != 0) & (dy != 0)), "some first move is diagonal"
+    assert np.all(np.maximum(np.abs(dx), np.abs(dy)) <= 1)
+    r = O.replay(p, sy, w.x, w.y, check=True)
+    ls = O.lockstep(p, sy, w.x, w.y, w.steps)
+    assert r["violations"] == 0
+    np.testing.assert_array_equal(r["traj"], ls["traj"])
