@@ -1431,7 +1431,7 @@ __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mas
                         dig += digest_term((uint32_t)(lo + j), dx, dy);
                 }
             } else if (!blocked && bs < as) {
-                blocked = within(dx, dy, rb_radius((long long)as - bs, d.v, d.r_p), d.metric);
+                blocked = within(dx, dy, rb32(as - bs, d.lagcap, d.v, d.r_p), d.metric);
             }
         }
     }
