@@ -325,12 +325,12 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     size_t o_ss0 = take(N), o_ss1 = take(N);
     size_t o_labels = take(4 * N), o_digest = take(8 * N), o_blkid = take(N);
     size_t o_tiles_s = take(8 * (size_t)c.n_sims);
-    size_t o_key = 0, o_rank = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
+    size_t o_key = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
            o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
            o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_wq = 0, o_dirty = 0, o_agf = 0, o_rid = 0;
     const size_t NC = (size_t)d.ncells;
     if (x->path == 1) {
-        o_key = take(4 * N); o_rank = take(4 * N);
+        o_key = take(4 * N);
         o_cnt = take(4 * NC); o_cmin = take(4 * NC);
         o_ctab = take(8 * (NC + 1)); o_l1 = take(4 * (NC / 16)); o_l2 = take(4 * (NC / 256));
         o_rec = take(16 * N); o_blk = take(N);
@@ -372,7 +372,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     d.digest = (unsigned long long*)(b + o_digest);
     d.tiles_s = (unsigned long long*)(b + o_tiles_s);
     if (x->path == 1) {
-        d.key = (uint32_t*)(b + o_key); d.rank = (uint32_t*)(b + o_rank);
+        d.key = (uint32_t*)(b + o_key);
         d.cnt = (uint32_t*)(b + o_cnt); d.cmin = (int32_t*)(b + o_cmin);
         d.ctab = (int2*)(b + o_ctab); d.lmin1 = (int32_t*)(b + o_l1); d.lmin2 = (int32_t*)(b + o_l2);
         d.rec = (int4*)(b + o_rec); d.v8 = (uint8_t*)(b + o_blk);

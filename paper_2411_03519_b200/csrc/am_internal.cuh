@@ -103,7 +103,6 @@ struct Dev {
     uint8_t* status[2];
     // binned round
     uint32_t* key;         // Morton cell key per agent (kSentinel = DONE)
-    uint32_t* rank;        // slot of the agent inside its cell
     uint32_t* cnt;         // [ncells] agents per cell (zero between rounds)
     int32_t* cmin;         // [ncells] min step per cell (INT_MAX between rounds)
     int2* ctab;            // [ncells+1] {start, min step}

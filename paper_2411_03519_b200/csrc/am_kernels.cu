@@ -105,14 +105,15 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
             // fused k_bin (replay rounds): cell key, slot, cell min step of the new state.
             // A rejected update leaves the round's ready set empty and forces a full
             // recompute next round (k_ingest_done), so bins of a rejected state are harmless.
-            uint32_t key = kSentinel, rank = 0;
+            // (no returning atomic: k_scatter takes each record's slot by counting the
+            // cell back down, which also leaves the counts zero for the next round)
+            uint32_t key = kSentinel;
             if (st != ST_DONE) {
                 key = mkey(d, (uint32_t)p[k].x >> d.clog, (uint32_t)p[k].y >> d.clog, 0);
-                rank = atomicAdd(d.cnt + key, 1u);
+                atomicAdd(d.cnt + key, 1u);
                 atomicMin(d.cmin + key, s[k]);
             }
             d.key[i] = key;
-            d.rank[i] = rank;
             d.bad[i] = 0;
             d.blkid[i] = 0;
         }
@@ -205,14 +206,13 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
         const uint8_t st = d.status[c][i];
         const int2 p = d.pos[c][i];
         const int s = d.step[c][i];
-        uint32_t key = kSentinel, rank = 0;
+        uint32_t key = kSentinel;
         if (st != ST_DONE) {
             key = mkey(d, (uint32_t)p.x >> d.clog, (uint32_t)p.y >> d.clog, 0);
-            rank = atomicAdd(d.cnt + key, 1u);
+            atomicAdd(d.cnt + key, 1u);
             atomicMin(d.cmin + key, s);
         }
         d.key[i] = key;
-        d.rank[i] = rank;
         d.bad[i] = 0;
         d.blkid[i] = 0;
     }
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
 
 // k_cells: exclusive scan of the cell counts in Morton order -> ctab{start, min};
 // lmin1 = min over each 16-cell (4x4) block, lmin2 over each 256-cell (16x16) block;
-// resets cnt/cmin for the next round.  kCellsThreads threads x 16 cells per tile (small
+// resets cmin for the next round (k_scatter counts cnt back to zero).  kCellsThreads threads x 16 cells per tile (small
 // tiles: many short look-back chains in parallel).
 __global__ void __launch_bounds__(kCellsThreads) k_cells(Dev d)
 {
@@ -243,8 +243,7 @@ __global__ void __launch_bounds__(kCellsThreads) k_cells(Dev d)
         int4 b = min4[k];
         cnt[4 * k] = a.x; cnt[4 * k + 1] = a.y; cnt[4 * k + 2] = a.z; cnt[4 * k + 3] = a.w;
         mn[4 * k] = b.x; mn[4 * k + 1] = b.y; mn[4 * k + 2] = b.z; mn[4 * k + 3] = b.w;
-        cnt4[k] = make_uint4(0, 0, 0, 0);
-        min4[k] = make_int4(INT_MAX, INT_MAX, INT_MAX, INT_MAX);
+        min4[k] = make_int4(INT_MAX, INT_MAX, INT_MAX, INT_MAX);   // (counts: k_scatter counts them back to 0)
     }
     uint32_t sum = 0;
     int m1 = INT_MAX;
@@ -302,7 +301,6 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
     int4 q = make_int4(0, 0, 0, 0);
     if (i < d.n) {
         const uint32_t key = d.key[i];
-        const uint32_t rk = d.rank[i];
         const int2 p = d.pos[c][i];
         const int s = d.step[c][i];
         const uint8_t st = d.status[c][i];
@@ -314,7 +312,8 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
             d.agflag[i] = 1;
         } else {
             const bool chg = full || ch;
-            const uint32_t r = (uint32_t)d.ctab[key].x + rk;
+            // slot: the cell's start + its count taken back down (returns the counts to 0)
+            const uint32_t r = (uint32_t)d.ctab[key].x + (atomicSub(d.cnt + key, 1u) - 1u);
             d.rec[r] = make_int4(p.x | (p.y << 16), s, i, st | (chg ? kRecChanged : 0));
             // union-find forest of this round: an agent whose last-round cluster has no
             // changed member keeps that cluster (all its coupling edges are unchanged: it
