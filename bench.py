@@ -313,6 +313,43 @@ def snapshot_rounds(rep, w, dev, flush, reps: int = 20):
                     "L2 flushed before each round"}
 
 
+def virtual_slabs(rep, w, dev, slab_counts=(2, 8)):
+    """S7 on one GPU: the pre-rolled C5 state split into G horizontal
+    slabs, one distributed round (watermark all-reduce, halo all-to-all, slab-local
+    round, link all-gather, merge) with an in-process loopback exchange; the device time
+    of every slab's local round is what one GPU of a G-GPU run spends on it.  The merged
+    ready set must equal the single-GPU round's (checked)."""
+    import torch
+
+    from paper_2411_03519_b200 import Tracker, slabs
+    pos, steps = rep.pos.clone(), rep.steps.clone()
+    status = rep.tracker.status().clone()
+    n = pos.shape[0]
+    gid = torch.arange(n, dtype=torch.int32, device=dev)
+    tr = Tracker(w.map_w, w.map_h, w.r_p, w.v, n, peek=True, force="binned", device=dev)
+    tr.set_state(pos, steps, status)
+    _, order = tr.ready()
+    ref = int(order.numel())
+    tr.close()
+    out = {}
+    for G in slab_counts:
+        part = slabs.partition(pos[:, 1], w.map_h, G)
+        ranks = []
+        for k in range(G):
+            sel = torch.nonzero(part == k).flatten()
+            ranks.append(slabs.SlabRank(w.map_w, w.map_h, w.r_p, w.v, n, G, k, gid[sel], pos[sel], steps[sel],
+                                        status[sel], device=dev))
+        outs = slabs.round_loopback(ranks)   # warm-up (grows the halo windows)
+        tl = []
+        for _ in range(3):
+            outs = slabs.round_loopback(ranks, tl)
+        per = [min(tl[k::G]) for k in range(G)]
+        out[f"G={G}"] = {"local_round_ms_max_over_slabs": max(per), "local_round_ms_mean": sum(per) / G,
+                         "ready": sum(o["n_ready"] for o in outs), "equals_single_gpu": sum(o["n_ready"] for o in outs) == ref}
+        del ranks
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, w, lm):
     import numpy as np
@@ -442,6 +479,7 @@ def run_ours(args, w, lm):
         e_value = float(t[1]) / (float(tm[0]) / 1000.0)
 
     snap = snapshot_rounds(rep, w, dev, flush) if not args.no_snapshot else None
+    vslab = virtual_slabs(rep, w, dev) if (not args.no_snapshot and ws == 1) else None
 
     if rank != 0:
         rep.close()
@@ -532,6 +570,7 @@ def run_ours(args, w, lm):
         "round_hbm": round_hbm,
         "issue_roofline": issue,
         "snapshot": snap,
+        "virtual_slabs": vslab,
         "kernel_share_warmup_us": {k: round(v * 1000.0, 2) for k, v in sorted(shares.items())},
         # D2H (am_replay_io, page-locked host arrays, state outputs aliasing the inputs):
         # position + step of every aligned 8-agent group holding a committed agent (96 B
