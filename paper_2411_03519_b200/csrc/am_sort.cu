@@ -44,16 +44,26 @@ __device__ __forceinline__ unsigned long long cs_now()
 #define CS_STAMP(k)
 #endif
 
-constexpr int kCsBits = 8;                   // digit of one global pass
+#ifndef AM_CS_BITS
+#define AM_CS_BITS 9
+#endif
+#ifndef AM_CS_SUB
+#define AM_CS_SUB 3
+#endif
+constexpr int kCsBits = AM_CS_BITS;          // digit of one global pass
 constexpr int kCsRadix = 1 << kCsBits;
-constexpr int kCsSub = 4;                    // bits of one local rank step
+constexpr int kCsSub = AM_CS_SUB;            // bits of one local rank step (divides kCsBits)
+static_assert(kCsBits % kCsSub == 0, "rank steps must tile the digit");
 constexpr int kCsSubR = 1 << kCsSub;
 #ifndef AM_CS_THREADS
 #define AM_CS_THREADS 1024
 #endif
 constexpr int kCsThreads = AM_CS_THREADS;    // threads per CTA (power of two, 256..1024)
 constexpr int kCsK = 8;                      // max elements per thread per tile
-// fixed shared memory: cnt[16][1024] (padded) + hist, base, run, tstart, ttot [256] + wsum[32]
+// fixed shared memory: cnt[kCsSubR][kCsThreads] (padded) + hist, base, run, tstart, ttot
+// [kCsRadix] + wsum[32].  9-bit digits of three 3-bit rank steps (A/B on the C5 round:
+// 197.6 -> 189.4 us against 8-bit digits of two 4-bit steps: C5's 27-bit keys take
+// 3 passes instead of 4)
 constexpr size_t kCsFixed = (size_t)(kCsSubR * kCsThreads * 33 / 32 + 5 * kCsRadix + 32) * 4;
 
 struct E32 {
@@ -123,10 +133,11 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* wsum)
 }
 
 // Stable local sort step: the tile's elements src[0..tm) by the sub-digit
-// (key >> shift) & 15 into dst.  Thread t owns elements [t*K, t*K+K) and counter column
-// t of a [16][1024] counter array, stored with one pad word per 32 (cpad) so that both
-// the per-thread column updates and the scan (thread u owns the 16 consecutive counters
-// [16u, 16u+16) of the (digit, thread) order) are bank-conflict free.
+// (key >> shift) & (kCsSubR - 1) into dst.  Thread t owns elements [t*K, t*K+K) and
+// counter column t of a [kCsSubR][kCsThreads] counter array, stored with one pad word
+// per 32 (cpad) so that both the per-thread column updates and the scan (thread u owns
+// the kCsSubR consecutive counters [kCsSubR u, kCsSubR u + kCsSubR) of the (digit,
+// thread) order) are bank-conflict free.
 __device__ __forceinline__ int cpad(int i) { return i + (i >> 5); }
 
 template <class E, int K>
@@ -151,17 +162,17 @@ __device__ __forceinline__ void rank_step(const E* src, E* dst, int tm, int shif
     __syncthreads();
     // exclusive scan of the counters in (digit, thread) order: serial over the thread's
     // 16, block-wide over the 1024 per-thread sums
-    uint32_t v[16], acc = 0;
+    uint32_t v[kCsSubR], acc = 0;
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-        v[j] = cnt[cpad(16 * t + j)];
+    for (int j = 0; j < kCsSubR; j++) {
+        v[j] = cnt[cpad(kCsSubR * t + j)];
         const uint32_t x = v[j];
         v[j] = acc;
         acc += x;
     }
     const uint32_t off = block_scan(acc, wsum);
 #pragma unroll
-    for (int j = 0; j < 16; j++) cnt[cpad(16 * t + j)] = off + v[j];
+    for (int j = 0; j < kCsSubR; j++) cnt[cpad(kCsSubR * t + j)] = off + v[j];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; k++) {
@@ -267,13 +278,15 @@ __device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned ch
                 }
             }
             __syncthreads();
-            rank_step<E, K>(sa, sb, tm, shift, cnt, wsum);
-            // the high sub-digit of the last pass may hold no key bit (C5: 27 bits ->
-            // the 4th pass sorts 3): all zero, so its stable step is the identity
-            const E* res = sb;
-            if (shift + kCsSub < bits) {
-                rank_step<E, K>(sb, sa, tm, shift + kCsSub, cnt, wsum);
-                res = sa;
+            // the digit's sub-digits, low first; a sub-digit of the last pass above the
+            // keys' significant bits is all zero, so its stable step is the identity
+            E* res = sa;
+            E* oth = sb;
+#pragma unroll
+            for (int ss = 0; ss < kCsBits / kCsSub; ss++) {
+                if (shift + ss * kCsSub >= bits) break;
+                rank_step<E, K>(res, oth, tm, shift + ss * kCsSub, cnt, wsum);
+                E* x = res; res = oth; oth = x;
             }
             CS_STAMP(5 + 8 * p);
             {
