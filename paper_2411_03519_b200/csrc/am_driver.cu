@@ -106,11 +106,11 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r)
     unsigned long long tmin = ~0ull;  // pending completions (single-simulation case)
     int any_active = 0;
     // loads of all items first (independent chains in flight), then the commits
-    uint8_t st[kIngestItems];
-    long long tc[kIngestItems];
+    uint8_t st[kCommitItems];
+    long long tc[kCommitItems];
 #pragma unroll
-    for (int k = 0; k < kIngestItems; k++) {
-        const int i = blockIdx.x * (256 * kIngestItems) + k * 256 + threadIdx.x;
+    for (int k = 0; k < kCommitItems; k++) {
+        const int i = blockIdx.x * (256 * kCommitItems) + k * 256 + threadIdx.x;
         st[k] = ST_DONE;
         tc[k] = 0;
         if (i < d.n) {
@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r)
     }
     const long long t1 = one ? r.t_sim[0] : 0;
 #pragma unroll
-    for (int k = 0; k < kIngestItems; k++) {
-        const int i = blockIdx.x * (256 * kIngestItems) + k * 256 + threadIdx.x;
+    for (int k = 0; k < kCommitItems; k++) {
+        const int i = blockIdx.x * (256 * kCommitItems) + k * 256 + threadIdx.x;
         if (st[k] == ST_DONE) continue;
         const int b = sim_of(d, i);
         const long long t = one ? t1 : r.t_sim[b];
@@ -520,7 +520,7 @@ static int enqueue_round(am_replay* rp)
     RK(launch_k(c->pdl, rp->stream, k_disp_b, nbd, 256, 0, rp->r));
     am_prof_end(c, K_DISP_B);
     am_prof_begin(c, K_COMMIT);
-    RK(launch_k(c->pdl, rp->stream, k_commit, (unsigned)((n + 256 * kIngestItems - 1) / (256 * kIngestItems)), 256, 0, rp->r));
+    RK(launch_k(c->pdl, rp->stream, k_commit, (unsigned)((n + 256 * kCommitItems - 1) / (256 * kCommitItems)), 256, 0, rp->r));
     am_join_side(c);   // the priority sort ran beside dispatch and commit
     am_prof_end(c, K_COMMIT);
     RK(cudaGetLastError());

@@ -19,16 +19,19 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #define AM_CELLS_THREADS 512
 #endif
 #ifndef AM_READY_ITEMS
-#define AM_READY_ITEMS 8
+#define AM_READY_ITEMS 4
 #endif
 #ifndef AM_READY_THREADS
 #define AM_READY_THREADS 1024
 #endif
 #ifndef AM_FIN_ITEMS
-#define AM_FIN_ITEMS 4
+#define AM_FIN_ITEMS 2
 #endif
 #ifndef AM_SCAN_UNITE
 #define AM_SCAN_UNITE 0   // 1: the scan unites its new edges as it flushes them, no k_union (A/B: +13 us, rejected)
+#endif
+#ifndef AM_COMMIT_ITEMS
+#define AM_COMMIT_ITEMS 1
 #endif
 #ifndef AM_INGEST_ITEMS
 #define AM_INGEST_ITEMS 4
@@ -41,7 +44,8 @@ constexpr int kSortTile = 8192;           // radix pass tile (1024 threads x 8 k
 constexpr int kMaxSortPasses = 8;
 constexpr int kRadixBits = 9;            // radix digit width of the priority sort
 constexpr int kRadix = 1 << kRadixBits;
-constexpr int kFinItems = AM_FIN_ITEMS;         // agents per thread in k_finalize
+constexpr int kFinItems = AM_FIN_ITEMS;
+constexpr int kCommitItems = AM_COMMIT_ITEMS;   // agents per thread in the driver's k_commit         // agents per thread in k_finalize
 constexpr int kIngestItems = AM_INGEST_ITEMS;   // agents per thread in k_ingest / k_commit
 constexpr int kEdgeStripes = 64;          // striped queues (one atomic counter per stripe)
 constexpr int kEdgeStage = 128;           // coupling edges staged per warp before appending
