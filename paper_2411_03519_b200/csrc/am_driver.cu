@@ -482,6 +482,10 @@ struct am_replay {
     uint32_t graph_flags = 0;           // context flags the graphs were captured with
     long long* h_buf = nullptr;         // pinned: dispatched, liveness
     int32_t* shadow = nullptr;          // am_replay_io: the steps as copied in (delta write-back)
+    cudaStream_t copy = nullptr;        // am_replay_io: the mask's device->host copy beside the round
+    cudaEvent_t ev_copy = nullptr;
+    cudaGraphExec_t g_io = nullptr;     // one round + that copy, captured for the host mask g_io_mask
+    const void* g_io_mask = nullptr;
 };
 
 static int rp_err(am_replay* rp, cudaError_t e, const char* where)
@@ -607,6 +611,41 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
     return AM_OK;
 }
 
+// One round whose ready mask is copied to the page-locked host array h_mask on a
+// forked stream as soon as k_ready has written it (beside dispatch, commit and the
+// priority sort), captured as a graph for that host array.
+static int build_io_graph(am_replay* rp, uint8_t* h_mask)
+{
+    am_ctx* c = rp->ctx;
+    if (!rp->copy) {
+        RK(cudaStreamCreateWithFlags(&rp->copy, cudaStreamNonBlocking));
+        RK(cudaEventCreateWithFlags(&rp->ev_copy, cudaEventDisableTiming));
+    }
+    if (rp->g_io) cudaGraphExecDestroy(rp->g_io);
+    rp->g_io = nullptr;
+    cudaGraph_t g;
+    RK(cudaStreamBeginCapture(rp->stream, cudaStreamCaptureModeThreadLocal));
+    c->mask_event = true;
+    int rc = enqueue_round(rp);
+    c->mask_event = false;
+    cudaError_t e = cudaSuccess;
+    if (rc == AM_OK) {
+        e = cudaStreamWaitEvent(rp->copy, c->ev_mask, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h_mask, rp->mask, (size_t)c->d.n, cudaMemcpyDeviceToHost, rp->copy);
+        if (e == cudaSuccess) e = cudaEventRecord(rp->ev_copy, rp->copy);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(rp->stream, rp->ev_copy, 0);
+    }
+    cudaError_t e2 = cudaStreamEndCapture(rp->stream, &g);
+    if (rc) return rc;
+    if (e != cudaSuccess) return rp_err(rp, e, "io graph capture");
+    if (e2 != cudaSuccess) return rp_err(rp, e2, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&rp->g_io, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return rp_err(rp, e, "cudaGraphInstantiate");
+    rp->g_io_mask = h_mask;
+    return AM_OK;
+}
+
 static int build_graph(am_replay* rp, int rounds, cudaGraphExec_t* exec)
 {
     cudaGraph_t g;
@@ -647,7 +686,9 @@ static int ensure_graphs(am_replay* rp)
     if (pm != rp->graph_prof || rp->ctx->d.flags != rp->graph_flags) {  // baked in at capture
         if (rp->g1) cudaGraphExecDestroy(rp->g1);
         if (rp->g8) cudaGraphExecDestroy(rp->g8);
-        rp->g1 = rp->g8 = nullptr;
+        if (rp->g_io) cudaGraphExecDestroy(rp->g_io);
+        rp->g1 = rp->g8 = rp->g_io = nullptr;
+        rp->g_io_mask = nullptr;
         rp->graph_prof = pm;
         rp->graph_flags = rp->ctx->d.flags;
     }
@@ -787,8 +828,17 @@ extern "C" int am_replay_io(am_replay* rp, const int32_t* h_pos_in, const int32_
     RK(cudaMemcpyAsync(rp->r.pos, h_pos_in, 8 * n, cudaMemcpyHostToDevice, rp->stream));
     RK(cudaMemcpyAsync(rp->r.steps, h_steps_in, 4 * n, cudaMemcpyHostToDevice, rp->stream));
     if (delta) RK(cudaMemcpyAsync(rp->shadow, rp->r.steps, 4 * n, cudaMemcpyDeviceToDevice, rp->stream));
-    RK(cudaGraphLaunch(rp->g1, rp->stream));
-    am_prof_mark(c, rp->graph_prof);
+    // page-locked host mask on the binned path: a graph whose mask copy starts right after
+    // k_ready, beside dispatch, commit and the priority sort (captured per host array)
+    void* dmask = nullptr;
+    const bool split = c->path == 1 && h_mask && !c->prof.on && mapped(h_mask, &dmask);
+    if (split) {
+        if (rp->g_io_mask != (const void*)h_mask && (rc = build_io_graph(rp, h_mask))) return rc;
+        RK(cudaGraphLaunch(rp->g_io, rp->stream));
+    } else {
+        RK(cudaGraphLaunch(rp->g1, rp->stream));
+        am_prof_mark(c, rp->graph_prof);
+    }
     if (delta) {
         RK(launch_k(false, rp->stream, k_delta_out, (unsigned)c->num_sms * 4, 256, 0, (int)n, (const int32_t*)rp->shadow,
                     (const int2*)rp->r.pos, (const int32_t*)rp->r.steps, (int2*)dpos, (int32_t*)dsteps));
@@ -796,7 +846,7 @@ extern "C" int am_replay_io(am_replay* rp, const int32_t* h_pos_in, const int32_
         if (h_pos_out) RK(cudaMemcpyAsync(h_pos_out, rp->r.pos, 8 * n, cudaMemcpyDeviceToHost, rp->stream));
         if (h_steps_out) RK(cudaMemcpyAsync(h_steps_out, rp->r.steps, 4 * n, cudaMemcpyDeviceToHost, rp->stream));
     }
-    if (h_mask) RK(cudaMemcpyAsync(h_mask, rp->mask, n, cudaMemcpyDeviceToHost, rp->stream));
+    if (!split && h_mask) RK(cudaMemcpyAsync(h_mask, rp->mask, n, cudaMemcpyDeviceToHost, rp->stream));
     if (h_order) {
         // page-locked (device-accessible) host order array: a kernel writes the n_ready
         // valid entries; pageable memory: a copy of the whole capacity
@@ -863,6 +913,7 @@ extern "C" int am_replay_destroy(am_replay* rp)
     if (rp->stream) cudaStreamSynchronize(rp->stream);
     if (rp->g1) cudaGraphExecDestroy(rp->g1);
     if (rp->g8) cudaGraphExecDestroy(rp->g8);
+    if (rp->g_io) cudaGraphExecDestroy(rp->g_io);
     if (rp->ctx) {
         am_set_stream(rp->ctx, rp->user_stream);
         rp->ctx->d.flags &= ~AM_ASYNC;
@@ -870,6 +921,11 @@ extern "C" int am_replay_destroy(am_replay* rp)
     if (rp->stream) cudaStreamDestroy(rp->stream);
     if (rp->h_buf) cudaFreeHost(rp->h_buf);
     if (rp->shadow) cudaFree(rp->shadow);
+    if (rp->copy) {
+        cudaStreamSynchronize(rp->copy);
+        cudaStreamDestroy(rp->copy);
+        cudaEventDestroy(rp->ev_copy);
+    }
     cudaFree(rp->mem);
     delete rp;
     return AM_OK;

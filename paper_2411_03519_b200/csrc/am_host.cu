@@ -358,6 +358,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_efil, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&x->side2, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_dig, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_mask, cudaEventDisableTiming);
         if (e != cudaSuccess) { cudaFree(x->ws); delete x; return cuda_err(nullptr, e, "am_init: side stream"); }
     }
     e = cudaMallocHost((void**)&x->h_ctl, sizeof(Ctl));
@@ -571,6 +572,8 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         }
         LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, blocks(d.n, 256 * kFinItems), 256, 0, d)));
         LAUNCH(K_READY, CK(c, launch_k(c->pdl, s, k_ready, c->ntiles_ready, kReadyThreads, 0, d, mask)));
+        // the mask is final here: a caller may copy it out beside the rest of the round
+        if (c->mask_event && c->ev_mask) CK(c, cudaEventRecord(c->ev_mask, s));
         static const bool dbg_nosort = [] { const char* e = getenv("AM_DBG_NOSORT"); return e && atoi(e); }();
         if (dbg_nosort) {
             // PROFILING ONLY (wrong `order`): measures how much of the round the sort holds up
@@ -713,6 +716,7 @@ extern "C" int am_destroy(am_ctx* c)
         cudaStreamSynchronize(c->side2);
         cudaStreamDestroy(c->side2);
         cudaEventDestroy(c->ev_dig);
+        cudaEventDestroy(c->ev_mask);
     }
     cudaFree(c->ws);
     cudaFreeHost(c->h_ctl);

@@ -206,6 +206,8 @@ struct am_ctx {
     bool join_pending = false;
     cudaStream_t side2 = nullptr;    // perception digests (beside the driver's dispatch part a)
     cudaEvent_t ev_dig = nullptr;
+    cudaEvent_t ev_mask = nullptr;   // recorded after k_ready when mask_event is set (am_replay_io)
+    bool mask_event = false;
     bool dig_pending = false;
     bool bin_pending = false;        // am_update_binned ran the round's k_bin already
     bool pdl = true;                 // programmatic dependent launch between round kernels

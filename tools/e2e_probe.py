@@ -31,10 +31,14 @@ variants = {
     "+order": (None, None, h_mask, h_order),
     "+state(delta)": (h_pos, h_steps, h_mask, h_order),
 }
+flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda") if "--flush" in sys.argv else None
 for name, (po, so, mo, oo) in variants.items():
     ts = []
     for k in range(12):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if flush is not None:
+            with torch.cuda.stream(st):
+                flush.fill_(k & 0xFF)
         a.record(st)
         L.am_replay_io(rep.h, P(h_pos), P(h_steps), P(po), P(so), P(mo), P(oo), None)
         b.record(st)
