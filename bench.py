@@ -42,11 +42,11 @@ def algorithmic_bytes(kernel: str, s: dict) -> float:
     table = {
         # read pos 8 + step 4 (new) + old step 4 + status 1 + old pos 8; write pos 8 + step 4 + status 1
         "k_ingest": 38.0 * n,
-        # read status 1 + pos 8 + step 4; write key 4 + rank 4 + parent 4 + bad 1; cell count+min 8
-        "k_bin": 34.0 * n,
-        # read count 4 + min 4; write start/min 8 + reset 8 + pyramid 0.27
-        "k_cells": 24.27 * c,
-        # read key 4 + rank 4 + cell start 4 + pos 8 + step 4 + status 1; write record 16
+        # read status 1 + pos 8 + step 4; write key 4 + bad 1 + blkid 1; cell count + min 8
+        "k_bin": 27.0 * n,
+        # read count 4 + min 4; write start/min 8 + min reset 4 + pyramid 0.27
+        "k_cells": 20.27 * c,
+        # read key 4 + cell start 4 + count 4 + pos 8 + step 4 + status 1; write record 16
         "k_scatter": 41.0 * a,
         # k_efilter (timed as "k_near"): read last round's edge list 8 per edge, write the
         # kept ones 8 per edge (upper bound on the kept share: all)

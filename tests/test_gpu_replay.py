@@ -228,3 +228,23 @@ def test_linf_eight_connected_replay_vs_oracle(path):
     ls = O.lockstep(p, sy, w.x, w.y, w.steps)
     np.testing.assert_array_equal(res["traj"], ls["traj"])
     rep.close()
+
+
+def test_capacity_api_errors():
+    """am_replay_set_capacity: only before the first round (AM_E_STATE), only on the fused
+    per-simulation path (AM_E_ARG); the multi-kernel entry points refuse a finite
+    capacity."""
+    from paper_2411_03519_b200 import AmError, _lib
+    w = amgen.config("C1", steps=20)
+    lm = amgen.latency_model(w.profile)
+    rep = Replay.from_workload(w, lm)
+    rep.run(3)
+    with pytest.raises(AmError) as e:
+        _lib.check(rep.L.am_replay_set_capacity(rep.h, 4, 1), rep.tracker.ctx)
+    assert e.value.code == _lib.E_STATE
+    rep.close()
+    rep = Replay.from_workload(w, lm, force="binned")
+    with pytest.raises(AmError) as e:
+        _lib.check(rep.L.am_replay_set_capacity(rep.h, 4, 1), rep.tracker.ctx)
+    assert e.value.code == _lib.E_ARG
+    rep.close()
