@@ -33,6 +33,9 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #ifndef AM_COMMIT_ITEMS
 #define AM_COMMIT_ITEMS 1
 #endif
+#ifndef AM_SCAN_DYN
+#define AM_SCAN_DYN 0
+#endif
 #ifndef AM_INGEST_ITEMS
 #define AM_INGEST_ITEMS 4
 #endif
@@ -80,6 +83,7 @@ struct Ctl {
     uint32_t ccnt[2];      // edges in each carried list (k_efilter output)
     uint32_t ncnt[2];      // edges in each new list (k_scan_hw output)
     int32_t  n_work, n_far, n_items, n_edges;   // this round's scan work (stats)
+    uint32_t scan_next;    // dynamic work distribution of k_scan_hw (AM_SCAN_DYN)
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
     unsigned long long sort_or;   // OR of all ready keys

@@ -875,8 +875,18 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
     morton_child(l, ox_l, oy_l);
     HwStats hs;
     uint32_t nfar = 0;
+#if AM_SCAN_DYN
+    // dynamic distribution: each warp takes the next two queue entries (one per half-warp)
+    for (;;) {   // warp uniform
+        int q0 = 0;
+        if (lane == 0) q0 = (int)atomicAdd(&d.ctl->scan_next, 2u);
+        q0 = __shfl_sync(0xFFFFFFFFu, q0, 0);
+        if (q0 >= nq) break;
+        const int q = q0 + h;
+#else
     for (int q0 = blockIdx.x * 16; q0 < nq; q0 += gridDim.x * 16) {   // block uniform
         const int q = q0 + hw;
+#endif
         if (q < nq) {                                                  // half-warp uniform
             // stripe of queue entry q: the number of stripe starts <= q among stripes
             // 1..63 (prefixes are non-decreasing), counted by the 16 lanes at once
@@ -1483,6 +1493,7 @@ __device__ void round_begin(const Dev& d)
     ctl->n_clusters = 0;
     ctl->n_items = 0;
     ctl->n_far = 0;
+    ctl->scan_next = 0;
     ctl->sort_or = 0;
     ctl->ready.ticket = 0;   // k_ready and k_cells take tile tickets and keep no epilogue
     ctl->cells.ticket = 0;
