@@ -57,6 +57,11 @@ typedef struct {
     const int64_t* dur_table;   /* optional explicit durations [n_agents][dur_T]; NULL     */
     int32_t  dur_T;
     int32_t  policy;            /* 0 = random walk, 1 = always stay, 2 = 8-connected walk   */
+    int32_t  conflict;          /* 0 = co-occupancy allowed; 1 = exclusive tiles: a move is
+                                   cancelled if its target is occupied by a cluster-mate or
+                                   a lower-id cluster-mate proposes it (Alg. 3 l.20;
+                                   needs r_p >= 2 v; fused per-simulation path only,
+                                   through am_replay_run / am_replay_launch)              */
 } am_synth;
 
 typedef struct am_replay am_replay;

@@ -55,7 +55,8 @@ class Synth(C.Structure):
     _fields_ = [("lat", C.c_void_p), ("cdf32", C.c_void_p), ("vals", C.c_void_p),
                 ("n_vals", C.c_int32), ("base_us", C.c_int32), ("lat_seed", C.c_uint64),
                 ("policy_seed", C.c_uint64), ("wall", C.c_void_p),
-                ("dur_table", C.c_void_p), ("dur_T", C.c_int32), ("policy", C.c_int32)]
+                ("dur_table", C.c_void_p), ("dur_T", C.c_int32), ("policy", C.c_int32),
+                ("conflict", C.c_int32)]
 
 
 class Log(C.Structure):
@@ -195,7 +196,7 @@ class SynthTables:
     """Keeps the numpy arrays alive while the C struct points into them."""
 
     def __init__(self, lat, cdf32, vals, base_us, lat_seed, policy_seed, wall=None,
-                 dur_table=None, policy=0):
+                 dur_table=None, policy=0, conflict=0):
         self.lat = np.ascontiguousarray(lat, np.uint32)
         self.cdf32 = np.ascontiguousarray(cdf32, np.uint64)
         self.vals = np.ascontiguousarray(vals, np.int32)
@@ -205,12 +206,12 @@ class SynthTables:
                        len(self.vals), int(base_us), int(lat_seed), int(policy_seed),
                        None if self.wall is None else _p(self.wall).value,
                        None if self.dur is None else _p(self.dur).value,
-                       0 if self.dur is None else self.dur.shape[1], int(policy))
+                       0 if self.dur is None else self.dur.shape[1], int(policy), int(conflict))
 
     @classmethod
-    def from_model(cls, lm, wall=None, dur_table=None, policy=0):
+    def from_model(cls, lm, wall=None, dur_table=None, policy=0, conflict=0):
         return cls(lm.lat, lm.cdf32, lm.vals, lm.base_us, lm.lat_seed, lm.policy_seed, wall,
-                   dur_table, policy)
+                   dur_table, policy, conflict)
 
 
 def duration(sy: SynthTables, i: int, s: int) -> int:

@@ -316,8 +316,42 @@ typedef struct {
     const uint8_t* wall;      /* [map_h*map_w] row-major, 1 = wall; NULL = open map   */
     const int64_t* dur_table; /* optional explicit durations [n][dur_T] (closed forms)  */
     int32_t dur_T;
-    int32_t policy;           /* 0 = random walk, 1 = always stay                      */
+    int32_t policy;           /* 0 = random walk, 1 = always stay, 2 = 8-connected     */
+    int32_t conflict;         /* 0 = co-occupancy allowed; 1 = exclusive tiles (below)  */
 } orc_synth;
+
+/*
+ * Exclusive tiles ("write conflicts that must be resolved by
+ * developer-specified rules ... two agents might both want to use the bathroom, but
+ * only one can step in"; world.resolve_conflict_and_commit, Alg. 3 l.20 P:124):
+ * among a group of agents moving together, a proposed move is cancelled if its target
+ * tile is occupied now by another agent of the group, or if a lower-id agent of the
+ * group proposes the same tile (the lowest id among the proposers gets it).  The group
+ * is the whole simulation in lock-step and the cluster in the out-of-order replay:
+ * same-step agents that could contest a tile are within 2 v <= r_p + v (coupled), and
+ * validity keeps agents at other steps farther than r_p >= 2 v (required).
+ * idx[0..k) lists the group; x,y are current positions, px,py the proposals (updated
+ * in place: cancelled proposals become the current position).
+ */
+static void resolve_exclusive(int32_t k, const int32_t* idx, const int32_t* x, const int32_t* y,
+                              int32_t* px, int32_t* py)
+{
+    uint8_t* ok = (uint8_t*)malloc(k ? k : 1);
+    for (int32_t a = 0; a < k; a++) {
+        int32_t i = idx[a];
+        ok[a] = 1;
+        if (px[i] == x[i] && py[i] == y[i]) continue;   /* staying never conflicts */
+        for (int32_t b = 0; b < k && ok[a]; b++) {
+            int32_t j = idx[b];
+            if (j == i) continue;
+            if (x[j] == px[i] && y[j] == py[i]) ok[a] = 0;               /* occupied now */
+            if (j < i && px[j] == px[i] && py[j] == py[i]) ok[a] = 0;    /* lower id wants it */
+        }
+    }
+    for (int32_t a = 0; a < k; a++)
+        if (!ok[a]) { px[idx[a]] = x[idx[a]]; py[idx[a]] = y[idx[a]]; }
+    free(ok);
+}
 
 /* duration of agent i's step s in integer microseconds. */
 int64_t orc_duration(const orc_synth* sy, int32_t i, int32_t s)
@@ -404,6 +438,12 @@ int orc_lockstep(const orc_params* p, const orc_synth* sy, int32_t n, int32_t T,
                 orc_policy_move(p, sy, i, s, x[i], y[i], dg, &nx[i], &ny[i]);
                 int64_t d = orc_duration(sy, i, s);
                 if (d > mx) mx = d;
+            }
+            if (sy->conflict) {   /* the whole simulation moves together */
+                int32_t* idx = (int32_t*)malloc(sizeof(int32_t) * (hi - lo ? hi - lo : 1));
+                for (int32_t i = lo; i < hi; i++) idx[i - lo] = i;
+                resolve_exclusive(hi - lo, idx, x, y, nx, ny);
+                free(idx);
             }
             T_sync[b] += mx;
         }
@@ -561,6 +601,18 @@ int orc_replay_cap(const orc_params* p, const orc_synth* sy, int32_t n, int64_t 
                 /* digest over the sim, in global ids (perceived agents are cluster-mates) */
                 uint64_t dg = orc_digest(p, lo, hi, x, y, step, status, lo + a);
                 orc_policy_move(p, sy, lo + a, ss[a], sx[a], sy_[a], dg, &mvx[lo + a], &mvy[lo + a]);
+            }
+            if (sy->conflict && nr > 0) {   /* per ready cluster (members share a label) */
+                int32_t* idx = (int32_t*)malloc(sizeof(int32_t) * nr);
+                for (int32_t k = 0; k < nr; k++) {
+                    int32_t a = ord[k];
+                    int32_t ng = 0;
+                    for (int32_t q = 0; q < nr; q++)
+                        if (lab[ord[q]] == lab[a]) idx[ng++] = lo + ord[q];
+                    if (idx[0] != lo + a) continue;   /* each cluster once: from its lowest member */
+                    resolve_exclusive(ng, idx, x, y, mvx, mvy);
+                }
+                free(idx);
             }
             if (K > 0) {
                 /* in service: started members not yet committed */

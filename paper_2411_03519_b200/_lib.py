@@ -54,7 +54,7 @@ class Synth(C.Structure):
     _fields_ = [("lat", C.c_void_p), ("cdf32", C.c_void_p), ("vals", C.c_void_p),
                 ("n_vals", C.c_int32), ("base_us", C.c_int32), ("lat_seed", C.c_uint64),
                 ("policy_seed", C.c_uint64), ("wall", C.c_void_p), ("dur_table", C.c_void_p),
-                ("dur_T", C.c_int32), ("policy", C.c_int32)]
+                ("dur_T", C.c_int32), ("policy", C.c_int32), ("conflict", C.c_int32)]
 
 
 # name -> (restype, argtypes); every symbol include/*.h declares

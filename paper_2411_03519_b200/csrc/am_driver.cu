@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
     int2* snp = reinterpret_cast<int2*>(stcl + M);                               // [M] move computed at dispatch
     int4* sa = reinterpret_cast<int4*>(snp + M);                                 // [M] {x, y, step, status}
     unsigned long long* sq = reinterpret_cast<unsigned long long*>(sa + M);   // [M] queue keys (finite capacity)
-    uint32_t* par = reinterpret_cast<uint32_t*>(sq + M);
+    int* slab = reinterpret_cast<int*>(sq + M);                                  // [M] this round's labels
+    uint32_t* par = reinterpret_cast<uint32_t*>(slab + M);
     uint8_t* sbad = reinterpret_cast<uint8_t*>(par + M);
     __shared__ unsigned long long s_tmin, s_best;
     __shared__ long long s_busy, s_size, s_dmax;
@@ -324,14 +325,35 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
         }
         __syncthreads();
         const bool rdy = lead && st == ST_IDLE && !sbad[lab];
+        if (mine && lead) slab[t] = rdy ? lab : -1;   // ready clusters' members (exclusive tiles)
         // ---- dispatch part a (k_disp_a): cluster completion time
         if (rdy) atomicMax(stcl + lab, (unsigned long long)(tsim + duration(r.sy, i, A.z)));
         __syncthreads();
         // ---- dispatch part b (k_disp_b): member completion times and moves
+        if (rdy) snp[t] = policy_move(r, i, A.z, make_int2(A.x, A.y), dig);
+        if (r.sy.conflict) {
+            // exclusive tiles, per ready cluster (resolve_exclusive in the oracle): a
+            // move is cancelled if its target is a cluster-mate's current tile or a
+            // lower-id cluster-mate proposes the same tile
+            __syncthreads();
+            bool keep = true;
+            if (rdy) {
+                const int2 q = snp[t];
+                if (q.x != A.x || q.y != A.y) {
+                    for (int j = 0; j < m && keep; j++) {
+                        if (j == t || slab[j] != lab) continue;
+                        const int4 B = sa[j];
+                        const int2 qj = snp[j];
+                        if ((B.x == q.x && B.y == q.y) || (j < t && qj.x == q.x && qj.y == q.y)) keep = false;
+                    }
+                }
+            }
+            __syncthreads();
+            if (rdy && !keep) snp[t] = make_int2(A.x, A.y);
+        }
         if (rdy) {
             sa[t].w = ST_RUNNING;
             stc[t] = (long long)stcl[lab];
-            snp[t] = policy_move(r, i, A.z, make_int2(A.x, A.y), dig);
             atomicAdd(&s_nr, 1);
             if (r.K > 0) {   // finite capacity: queued now, started below in key order
                 stc[t] = LLONG_MAX;
@@ -545,6 +567,10 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
             return AM_E_ARG;
         }
     }
+    if (synth->conflict && (ctx->path != 0 || ctx->d.r_p < 2 * ctx->d.v)) {
+        ctx->err = "am_replay_create: exclusive tiles need the fused per-simulation path and r_p >= 2 v";
+        return AM_E_ARG;
+    }
     am_replay* rp = new (std::nothrow) am_replay();
     if (!rp) return AM_E_ARG;
     rp->ctx = ctx;
@@ -677,9 +703,9 @@ static int finish_check(am_replay* rp, int64_t* active)
 
 static int ensure_graphs(am_replay* rp)
 {
-    if (rp->r.K > 0) {   // finite capacity exists only in the persistent per-simulation kernel
-        rp->ctx->err = "finite LLM capacity runs through am_replay_run / am_replay_launch on the fused "
-                       "per-simulation path (<= 1024 agents per simulation, tracing off)";
+    if (rp->r.K > 0 || rp->r.sy.conflict) {   // only the persistent per-simulation kernel has these
+        rp->ctx->err = "finite LLM capacity and exclusive tiles run through am_replay_run / am_replay_launch "
+                       "on the fused per-simulation path (<= 1024 agents per simulation, tracing off)";
         return AM_E_ARG;
     }
     const unsigned pm = rp->ctx->prof.on ? rp->ctx->prof.mask : 0u;
@@ -703,7 +729,7 @@ static int ensure_graphs(am_replay* rp)
 static bool small_persistent(am_replay* rp)
 {
     am_ctx* c = rp->ctx;
-    if (rp->r.K > 0) return c->path == 0;   // finite capacity: only the persistent kernel has it
+    if (rp->r.K > 0 || rp->r.sy.conflict) return c->path == 0;   // only the persistent kernel has them
     if (c->path != 0 || c->prof.on) return false;
     static const int off = [] { const char* e = getenv("AM_SMALL_PERSIST"); return e && atoi(e) == 0; }();
     return !off;   // AM_SMALL_PERSIST=0: the multi-kernel rounds (ablation)
@@ -712,7 +738,7 @@ static int launch_small_replay(am_replay* rp, int64_t rounds)
 {
     am_ctx* c = rp->ctx;
     const int M = c->small_threads;   // >= agents of the largest simulation, multiple of 32
-    const size_t smem = (size_t)M * (8 + 8 + 8 + 16 + 8 + 4 + 1);
+    const size_t smem = (size_t)M * (8 + 8 + 8 + 16 + 8 + 4 + 4 + 1);
     // lanes per agent: as many as one CTA of <= 1024 threads holds while all the
     // simulations' CTAs fit in half the GPU's thread slots (measured: C1 G = 32 3.0x
     // over G = 1; C3's 4096 simulations are best at G = 1)
@@ -779,8 +805,8 @@ extern "C" int am_replay_set_capacity(am_replay* rp, int64_t capacity, int32_t p
 extern "C" int am_replay_step(am_replay* rp, uint8_t* mask, int32_t* order, int32_t* labels, int32_t* n_ready)
 {
     if (!rp) return AM_E_ARG;
-    if (rp->r.K > 0) {
-        rp->ctx->err = "am_replay_step: not available with a finite capacity (use am_replay_run)";
+    if (rp->r.K > 0 || rp->r.sy.conflict) {
+        rp->ctx->err = "am_replay_step: not available with a finite capacity or exclusive tiles (use am_replay_run)";
         return AM_E_ARG;
     }
     int rc = enqueue_round(rp);

@@ -22,7 +22,7 @@ class Replay:
     def __init__(self, map_w, map_h, r_p, v, x0, y0, steps_target, *, n_sims=1, wall=None,
                  lat=None, cdf32=None, vals=None, base_us=5000, lat_seed=4, policy_seed=3,
                  dur_table=None, policy=0, quantum_us=0, cell=0, metric="l2", force=None,
-                 stats=False, capacity=0, priority=True, device="cuda"):
+                 stats=False, capacity=0, priority=True, conflict=0, device="cuda"):
         self.device = torch.device(device)
         n = len(x0)
         self.n = n
@@ -47,7 +47,7 @@ class Replay:
                         len(self._vals), int(base_us), int(lat_seed), int(policy_seed),
                         None if self._wall is None else self._wall.data_ptr(),
                         None if self._dur is None else self._dur.data_ptr(),
-                        0 if self._dur is None else self._dur.shape[1], int(policy))
+                        0 if self._dur is None else self._dur.shape[1], int(policy), int(conflict))
         torch.cuda.synchronize(dev)
         h = C.c_void_p()
         L = self.tracker.L

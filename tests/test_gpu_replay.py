@@ -248,3 +248,23 @@ def test_capacity_api_errors():
         _lib.check(rep.L.am_replay_set_capacity(rep.h, 4, 1), rep.tracker.ctx)
     assert e.value.code == _lib.E_ARG
     rep.close()
+
+
+@pytest.mark.parametrize("name,steps,n_sims,K", [("C1", 300, None, 0), ("C2", 60, None, 0), ("C3", 120, 16, 0),
+                                                 ("C1", 200, None, 4)])
+def test_exclusive_tiles_replay_vs_oracle(name, steps, n_sims, K):
+    """NEXT #4 exclusive tiles (per-cluster conflict resolution in the persistent kernel)
+    vs the oracle, bit for bit; the outcome equals lock-step's with the rule applied over
+    the whole simulation; also with a finite capacity."""
+    w = amgen.config(name, steps=steps, n=n_sims)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall, conflict=1)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, n_sims=w.n_sims)
+    r = O.replay(p, sy, w.x, w.y, Q=w.Q, capacity=K)
+    rep = Replay.from_workload(w, lm, conflict=1, capacity=K)
+    rep.run_to_end()
+    res = rep.results()
+    for k in ("T_ooo", "rounds", "x", "y", "traj"):
+        np.testing.assert_array_equal(res[k], r[k], err_msg=k)
+    np.testing.assert_array_equal(res["traj"], O.lockstep(p, sy, w.x, w.y, w.steps)["traj"])
+    rep.close()

@@ -349,3 +349,39 @@ def test_linf_eight_connected_walk_keeps_the_outcome():
     ls = O.lockstep(p, sy, w.x, w.y, w.steps)
     assert r["violations"] == 0
     np.testing.assert_array_equal(r["traj"], ls["traj"])
+
+
+def test_exclusive_tiles_keep_the_outcome():
+    """NEXT #4 variant: exclusive tiles (P:182 bathroom example; Alg. 3 l.20
+    resolve_conflict_and_commit).  Lock-step resolves over the whole simulation, the
+    out-of-order replay per cluster; the outcome is the same (P:27 + the cluster-locality
+    argument in oracle.c), no two agents ever share a tile (checked after every step of
+    a crowded run), and the rule does change the outcome against co-occupancy."""
+    w = amgen.config("C1", steps=80)
+    lm = amgen.latency_model(w.profile)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps)
+    ex = O.SynthTables.from_model(lm, wall=w.wall, conflict=1)
+    co = O.SynthTables.from_model(lm, wall=w.wall, conflict=0)
+    r = O.replay(p, ex, w.x, w.y, check=True)
+    ls = O.lockstep(p, ex, w.x, w.y, w.steps)
+    assert r["violations"] == 0
+    np.testing.assert_array_equal(r["traj"], ls["traj"])
+    assert not np.array_equal(ls["traj"], O.lockstep(p, co, w.x, w.y, w.steps)["traj"])
+    # crowded: 60 agents in a 12 x 12 open room, every step's positions distinct
+    rng = np.random.default_rng(5)
+    cells = rng.choice(144, 60, replace=False)
+    x0, y0 = (cells % 12).astype(np.int32), (cells // 12).astype(np.int32)
+    lm0 = amgen.latency_model()
+    ex0 = O.SynthTables.from_model(lm0, conflict=1)
+    co0 = O.SynthTables.from_model(lm0, conflict=0)
+    shared = 0
+    for T in range(1, 25):
+        pT = O.params(12, 12, 4, 1, target=T)
+        a = O.lockstep(pT, ex0, x0, y0, T)
+        assert len(set(zip(a["x"].tolist(), a["y"].tolist()))) == 60, T
+        b = O.lockstep(pT, co0, x0, y0, T)
+        shared += 60 - len(set(zip(b["x"].tolist(), b["y"].tolist())))
+    assert shared > 0, "co-occupancy happens without the rule"
+    pT = O.params(12, 12, 4, 1, target=24)
+    r = O.replay(pT, ex0, x0, y0, check=True)
+    np.testing.assert_array_equal(r["traj"], O.lockstep(pT, ex0, x0, y0, 24)["traj"])
