@@ -249,6 +249,12 @@ def other_configs(dev, budget_s: float = 2.0):
             res["sim_rounds_per_s"] = done * w.n_sims / (ms / 1e3)
             if act == 0:
                 res["T_ooo_s_mean"] = float(r["T_ooo"].mean()) / 1e6
+        if name == "C4":   # C4 snapshot rounds (full recompute, AM_PEEK)
+            fl = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+            sn = snapshot_rounds(rep, w, dev, fl, reps=20)
+            res["snapshot_rounds_per_s"] = sn["rounds_per_s"]
+            res["snapshot_ms_per_round"] = sn["ms_per_round_median"]
+            del fl
         out[name] = res
         rep.close()
     # finite LLM capacity, C2 = 500 agents busy hour: the paper's
