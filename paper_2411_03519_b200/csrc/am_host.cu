@@ -340,10 +340,10 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * kRadix);
         o_gh = take(4 * kMaxSortPasses * kRadix); o_gs = take(4 * kMaxSortPasses * kRadix);
         d.ecap = (int)(3 * N + 4096);
-        // the scan's work queue: stripes = block index mod 64 of k_scatter (kScatterItems
-        // agents per thread), so a stripe holds at most ceil(blocks / 64) x 256 x items records
-        const long long nbl = blocks(n, 256 * kScatterItems);
-        d.wq_cap = (int)(((nbl + kEdgeStripes - 1) / kEdgeStripes) * 256 * kScatterItems);
+        // the scan's work queue: stripes = block index mod 64 of k_scatter (one thread per
+        // agent), so a stripe holds at most ceil(blocks / 64) x 256 records
+        const long long nbl = blocks(n, 256);
+        d.wq_cap = (int)(((nbl + kEdgeStripes - 1) / kEdgeStripes) * 256);
         o_wit = take(4 * N); o_lrs = take(N);
         o_edges = take(8 * 4 * (size_t)d.ecap); o_ectr = take(4 * kEdgeStripes);
         o_wq = take(16 * (size_t)kEdgeStripes * d.wq_cap);
@@ -547,7 +547,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         if (!c->bin_pending) LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, nb, 256, 0, d)));
         c->bin_pending = false;
         LAUNCH(K_CELLS, CK(c, launch_k(c->pdl, s, k_cells, c->ntiles_cells, c->cells_threads, 0, d)));
-        LAUNCH(K_SCATTER, CK(c, launch_k(c->pdl, s, k_scatter, blocks(d.n, 256 * kScatterItems), 256, 0, d)));
+        LAUNCH(K_SCATTER, CK(c, launch_k(c->pdl, s, k_scatter, nb, 256, 0, d)));
         if (d.flags & AM_SCAN_THREAD)   // ablation: everything recomputed, no witnesses
             LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_thread, nb, 256, 0, d)));
         else

@@ -36,9 +36,6 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #ifndef AM_SCAN_DYN
 #define AM_SCAN_DYN 0
 #endif
-#ifndef AM_SCATTER_ITEMS
-#define AM_SCATTER_ITEMS 1
-#endif
 #ifndef AM_INGEST_ITEMS
 #define AM_INGEST_ITEMS 4
 #endif
@@ -52,7 +49,6 @@ constexpr int kRadixBits = 9;            // radix digit width of the priority so
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kFinItems = AM_FIN_ITEMS;
 constexpr int kCommitItems = AM_COMMIT_ITEMS;   // agents per thread in the driver's k_commit         // agents per thread in k_finalize
-constexpr int kScatterItems = AM_SCATTER_ITEMS;   // agents per thread in k_scatter
 constexpr int kIngestItems = AM_INGEST_ITEMS;   // agents per thread in k_ingest / k_commit
 constexpr int kEdgeStripes = 64;          // striped queues (one atomic counter per stripe)
 constexpr int kEdgeStage = 128;           // coupling edges staged per warp before appending

@@ -295,60 +295,42 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
 {
     pdl_begin();
     __shared__ uint32_t s_w[9];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t c = d.ctl->cur;
-    const bool full = round_full(d);
-    const uint32_t epoch = d.ctl->epoch;
-    // kScatterItems agents per thread: every independent load of all items is issued
-    // first (memory-level parallelism), then the dependent slot atomics / dirty marks
-    uint32_t key[kScatterItems], w[kScatterItems];
-    int2 p[kScatterItems];
-    int s[kScatterItems], lab[kScatterItems];
-    uint8_t st[kScatterItems];
-    bool ch[kScatterItems];
-#pragma unroll
-    for (int k = 0; k < kScatterItems; k++) {
-        const int i = blockIdx.x * (256 * kScatterItems) + k * 256 + threadIdx.x;
-        key[k] = kSentinel; w[k] = kSentinel; p[k] = make_int2(0, 0); s[k] = 0; lab[k] = -1; st[k] = 0; ch[k] = false;
-        if (i < d.n) {
-            key[k] = d.key[i];
-            p[k] = d.pos[c][i];
-            s[k] = d.step[c][i];
-            st[k] = d.status[c][i];
-            ch[k] = d.chg8[i] != 0;
-            lab[k] = d.labels[i];
-            w[k] = d.witness[i];
+    bool work = false;
+    int4 q = make_int4(0, 0, 0, 0);
+    if (i < d.n) {
+        const uint32_t key = d.key[i];
+        const int2 p = d.pos[c][i];
+        const int s = d.step[c][i];
+        const uint8_t st = d.status[c][i];
+        const bool ch = d.chg8[i] != 0;
+        const int lab = d.labels[i];
+        const uint32_t w = d.witness[i];
+        const bool full = round_full(d);
+        if (key == kSentinel) {   // DONE: counts as changed for the carried edges (k_efilter)
+            d.agflag[i] = 1;
+        } else {
+            const bool chg = full || ch;
+            // slot: the cell's start + its count taken back down (returns the counts to 0)
+            const uint32_t r = (uint32_t)d.ctab[key].x + (atomicSub(d.cnt + key, 1u) - 1u);
+            d.rec[r] = make_int4(p.x | (p.y << 16), s, i, st | (chg ? kRecChanged : 0));
+            // union-find forest of this round: an agent whose last-round cluster has no
+            // changed member keeps that cluster (all its coupling edges are unchanged: it
+            // is still connected, and it can only grow through an edge of a changed
+            // agent), so it hangs under the old root (= min id = its label); members of
+            // dirty clusters start alone
+            const bool dirty = full || lab < 0 || d.dirty[lab] == d.ctl->epoch;
+            d.parent[i] = dirty ? (uint32_t)i : (uint32_t)lab;
+            d.agflag[i] = (uint8_t)((chg ? 1 : 0) | (dirty ? 2 : 0));
+            // the scan's work queue (incremental scan): changed
+            // agents, and IDLE agents whose recorded blocker (witness) changed
+            work = chg || (st == ST_IDLE && w != kSentinel && agent_changed(d, c, w));
+            q = make_int4(p.x | (p.y << 16), s, (int)((uint32_t)i | (chg ? 0x80000000u : 0u)), st);
         }
     }
-#pragma unroll
-    for (int k = 0; k < kScatterItems; k++) {
-        const int i = blockIdx.x * (256 * kScatterItems) + k * 256 + threadIdx.x;
-        bool work = false;
-        int4 q = make_int4(0, 0, 0, 0);
-        if (i < d.n) {
-            if (key[k] == kSentinel) {   // DONE: counts as changed for the carried edges (k_efilter)
-                d.agflag[i] = 1;
-            } else {
-                const bool chg = full || ch[k];
-                // slot: the cell's start + its count taken back down (returns the counts to 0)
-                const uint32_t r = (uint32_t)d.ctab[key[k]].x + (atomicSub(d.cnt + key[k], 1u) - 1u);
-                d.rec[r] = make_int4(p[k].x | (p[k].y << 16), s[k], i, st[k] | (chg ? kRecChanged : 0));
-                // union-find forest of this round: an agent whose last-round cluster has no
-                // changed member keeps that cluster (all its coupling edges are unchanged: it
-                // is still connected, and it can only grow through an edge of a changed
-                // agent), so it hangs under the old root (= min id = its label); members of
-                // dirty clusters start alone
-                const bool dirty = full || lab[k] < 0 || d.dirty[lab[k]] == epoch;
-                d.parent[i] = dirty ? (uint32_t)i : (uint32_t)lab[k];
-                d.agflag[i] = (uint8_t)((chg ? 1 : 0) | (dirty ? 2 : 0));
-                // the scan's work queue (incremental scan): changed
-                // agents, and IDLE agents whose recorded blocker (witness) changed
-                work = chg || (st[k] == ST_IDLE && w[k] != kSentinel && agent_changed(d, c, w[k]));
-                q = make_int4(p[k].x | (p[k].y << 16), s[k], (int)((uint32_t)i | (chg ? 0x80000000u : 0u)), st[k]);
-            }
-        }
-        // stripe = block index mod 64, one atomic per block and item
-        block_append(d.wq, d.wq_cap, d.wq_ctr, (int)(blockIdx.x & (kEdgeStripes - 1)), work, q, s_w);
-    }
+    // stripe = block index mod 64, one atomic per block
+    block_append(d.wq, d.wq_cap, d.wq_ctr, (int)(blockIdx.x & (kEdgeStripes - 1)), work, q, s_w);
 }
 
 // test every record of cell `key` against agent A; returns true if A got blocked.
