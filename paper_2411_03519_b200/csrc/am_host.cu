@@ -19,6 +19,7 @@ __global__ void k_scan_thread(Dev d);
 __global__ void k_finalize(Dev d);
 __global__ void k_union(Dev d);
 __global__ void k_scan_hw(Dev d);
+__global__ void k_scan_hw_full(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
 __global__ void k_sort_pass(Dev d, int pass, int32_t* order, int ntiles);
@@ -417,6 +418,7 @@ static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, co
     if (!pos || !steps || (mode == 2 && !st)) return set_err(c, AM_E_ARG, "NULL array");
     if (c->bin_pending) return set_err(c, AM_E_STATE, "update after a binned update without a round");
     am_join_side(c);
+    if (mode != 0) c->full_hint = true;   // initial state / set state: the next round recomputes everything
     am_prof_begin(c, K_INGEST);
     CK(c, launch_k(c->pdl, c->stream, k_ingest, blocks(c->d.n, 256 * kIngestItems), 256, 0, c->d, (const int2*)pos, steps, st, mode, bin ? 1 : 0));
     CK(c, launch_k(c->pdl, c->stream, k_ingest_done, 1, 1, 0, c->d, mode, bin ? 1 : 0));
@@ -565,7 +567,21 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
                 c->stream = ms;
             }
             CK(c, cudaEventRecord(c->ev_efil, c->side));
-            LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw, std::min(blocks(d.n, 16), (unsigned)c->scan_blocks), 256, 0, d)));
+            {
+                // a round the host knows is a full recompute (initial / set state, no commit
+                // validation) outside a graph capture takes the smaller direct box; every
+                // other round (the replay's incremental rounds, device-detected full rounds)
+                // the incremental kernel.  Both are exact; only the pruning granularity differs.
+                cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                CK(c, cudaStreamIsCapturing(s, &cs));
+                const bool full = (c->full_hint || !(d.flags & AM_VALIDATE)) && cs == cudaStreamCaptureStatusNone;
+                const unsigned g = std::min(blocks(d.n, 16), (unsigned)c->scan_blocks);
+                if (full)
+                    LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw_full, g, 256, 0, d)));
+                else
+                    LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw, g, 256, 0, d)));
+                c->full_hint = false;
+            }
             CK(c, cudaStreamWaitEvent(s, c->ev_efil, 0));
             if (!AM_SCAN_UNITE)   // else the scan united its new edges as it flushed them
                 LAUNCH(K_UNION, CK(c, launch_k(c->pdl, s, k_union, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
@@ -674,6 +690,7 @@ extern "C" int am_set_flags(am_ctx* c, uint32_t flags)
     if (c->path == 1 && ((flags ^ c->d.flags) & AM_SCAN_THREAD)) {
         // the ablation scan keeps no blocking witnesses: recompute everything next round
         const int32_t one = 1;
+        c->full_hint = true;
         CK(c, cudaMemcpyAsync(&c->d.ctl->full, &one, sizeof one, cudaMemcpyHostToDevice, c->stream));
         CK(c, cudaStreamSynchronize(c->stream));
     }

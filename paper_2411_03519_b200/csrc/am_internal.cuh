@@ -36,6 +36,15 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #ifndef AM_SCAN_DYN
 #define AM_SCAN_DYN 0
 #endif
+#ifndef AM_DIRECT
+#define AM_DIRECT 64        // direct query box (cells) of the incremental scan
+#endif
+#ifndef AM_SCAN_MINB
+#define AM_SCAN_MINB 5      // k_scan_hw: 5 resident CTAs per SM (<= 51 registers; A/B: -6% round time)
+#endif
+#ifndef AM_DIRECT_FULL
+#define AM_DIRECT_FULL 16   // ... of full-recompute rounds (C5 snapshot A/B: 777 / 649 / 624 us at 64 / 32 / 16)
+#endif
 #ifndef AM_INGEST_ITEMS
 #define AM_INGEST_ITEMS 4
 #endif
@@ -202,6 +211,7 @@ struct am_ctx {
     int small_threads = 32;
     int num_sms = 148;
     int scan_blocks = 148 * 4;       // resident blocks of k_scan_hw (occupancy x SMs)
+    bool full_hint = true;           // the host knows the next round is a full recompute
     int sort_ctas = 16;              // persistent CTAs of each radix pass
     int sort_passes_max = 1;
     cudaStream_t side = nullptr;     // edge filter (beside the scan) and priority sort (beside

@@ -778,13 +778,8 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
 // The records of the listed cells are flattened over the 16 lanes (prefix sum of the
 // cell counts, 4-step shuffle search per lane) and tested 16 at a time; the first
 // blocker becomes A's witness.
-#ifndef AM_DIRECT
-#define AM_DIRECT 64
-#endif
-#ifndef AM_SCAN_MINB
-#define AM_SCAN_MINB 5   // 5 resident CTAs per SM (<= 51 registers; A/B: -6% round time)
-#endif
-constexpr int kDirect = AM_DIRECT;   // cells of the query box resolved with one table fetch
+constexpr int kDirect = AM_DIRECT;          // cells of the query box resolved with one table fetch
+constexpr int kDirectFull = AM_DIRECT_FULL; // the same for rounds the host knows are full recomputes
 
 // test the records of the cells in `list[0..nl)` (near cells first: nn of them) against
 // A; returns (in nblk/wit) the first blocker; stages coupling edges for a changed A
@@ -854,11 +849,12 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
     }
 }
 
-__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
+template <int KD>
+__device__ __forceinline__ void scan_hw(const Dev& d)
 {
     pdl_begin();
     __shared__ EdgeStage s_all[8];
-    __shared__ int2 s_list[16][kDirect];
+    __shared__ int2 s_list[16][KD];
     __shared__ int s_pref[kEdgeStripes + 1];
     const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4, hw = threadIdx.x >> 4;
     const unsigned hm = 0xFFFFu << (16 * h);
@@ -903,7 +899,7 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
             const int Rf = far ? (int)rb32(as - W, d.lagcap, d.v, d.r_p) : (int)Rc;
             int cx0 = max(0, (ax - Rf) >> cl), cx1 = min(Gx - 1, (ax + Rf) >> cl);
             int cy0 = max(0, (ay - Rf) >> cl), cy1 = min(Gy - 1, (ay + Rf) >> cl);
-            const bool direct = (cx1 - cx0 + 1) * (cy1 - cy0 + 1) <= kDirect;
+            const bool direct = (cx1 - cx0 + 1) * (cy1 - cy0 + 1) <= KD;
             if (!direct) {   // near cells only; the far test walks the pyramid below
                 cx0 = max(0, (ax - (int)Rc) >> cl); cx1 = min(Gx - 1, (ax + (int)Rc) >> cl);
                 cy0 = max(0, (ay - (int)Rc) >> cl); cy1 = min(Gy - 1, (ay + (int)Rc) >> cl);
@@ -916,13 +912,13 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
             auto krow = [&](int k) { return ncx == 1 ? k : (mulhi ? (int)__umulhi((uint32_t)k, rcx) : k / ncx); };
             bool nblk = false;
             uint32_t wit = kSentinel;
-            for (int cb = 0; cb < ncell; cb += kDirect) {   // one chunk unless cells are tiny
+            for (int cb = 0; cb < ncell; cb += KD) {   // one chunk unless cells are tiny
                 if ((nblk || !idle) && !chg) break;
                 // one round trip: the entries of the chunk's cells (<= 4 per lane)
-                int2 ent[kDirect / 16];
-                int nxt[kDirect / 16];
+                int2 ent[KD / 16];
+                int nxt[KD / 16];
 #pragma unroll
-                for (int j = 0; j < kDirect / 16; j++) {
+                for (int j = 0; j < KD / 16; j++) {
                     const int k = cb + j * 16 + l;
                     ent[j] = make_int2(0, INT_MAX);
                     nxt[j] = 0;
@@ -940,7 +936,7 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
 #pragma unroll
                 for (int pass = 0; pass < 2; pass++) {
 #pragma unroll
-                    for (int j = 0; j < kDirect / 16; j++) {
+                    for (int j = 0; j < KD / 16; j++) {
                         const int k = cb + j * 16 + l;
                         bool ok = false;
                         if (k < ncell && nxt[j] > ent[j].x) {
@@ -987,6 +983,9 @@ __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d)
     if (lane == 0 && nf) atomicAdd((unsigned*)&d.ctl->n_far, nf);
     hw_flush_stats(d, hs, lane);
 }
+// the incremental rounds' scan and the full-recompute rounds' scan (host-selected)
+__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d) { scan_hw<kDirect>(d); }
+__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw_full(Dev d) { scan_hw<kDirectFull>(d); }
 
 // k_union: unite this round's coupling edges (carried-over + new), one thread per edge
 // (ECL-CC style hooking of the larger root under the smaller, so roots stay the
