@@ -260,6 +260,10 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan_hw, 256, 0) == cudaSuccess && per > 0)
             x->scan_blocks = per * x->num_sms;
         cudaGetLastError();
+        x->scan_blocks_full = x->scan_blocks;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan_hw_full, 256, 0) == cudaSuccess && per > 0)
+            x->scan_blocks_full = per * x->num_sms;
+        cudaGetLastError();
     }
 
     // path selection
@@ -575,7 +579,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
                 cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
                 CK(c, cudaStreamIsCapturing(s, &cs));
                 const bool full = (c->full_hint || !(d.flags & AM_VALIDATE)) && cs == cudaStreamCaptureStatusNone;
-                const unsigned g = std::min(blocks(d.n, 16), (unsigned)c->scan_blocks);
+                const unsigned g = std::min(blocks(d.n, 16), (unsigned)(full ? c->scan_blocks_full : c->scan_blocks));
                 if (full)
                     LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw_full, g, 256, 0, d)));
                 else

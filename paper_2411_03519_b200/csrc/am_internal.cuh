@@ -42,6 +42,9 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #ifndef AM_SCAN_MINB
 #define AM_SCAN_MINB 5      // k_scan_hw: 5 resident CTAs per SM (<= 51 registers; A/B: -6% round time)
 #endif
+#ifndef AM_SCAN_MINB_FULL
+#define AM_SCAN_MINB_FULL AM_SCAN_MINB
+#endif
 #ifndef AM_DIRECT_FULL
 #define AM_DIRECT_FULL 16   // ... of full-recompute rounds (C5 snapshot A/B: 777 / 649 / 624 us at 64 / 32 / 16)
 #endif
@@ -211,6 +214,7 @@ struct am_ctx {
     int small_threads = 32;
     int num_sms = 148;
     int scan_blocks = 148 * 4;       // resident blocks of k_scan_hw (occupancy x SMs)
+    int scan_blocks_full = 148 * 4;  // ... of k_scan_hw_full
     bool full_hint = true;           // the host knows the next round is a full recompute
     int sort_ctas = 16;              // persistent CTAs of each radix pass
     int sort_passes_max = 1;

@@ -985,7 +985,7 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
 }
 // the incremental rounds' scan and the full-recompute rounds' scan (host-selected)
 __global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d) { scan_hw<kDirect>(d); }
-__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw_full(Dev d) { scan_hw<kDirectFull>(d); }
+__global__ void __launch_bounds__(256, AM_SCAN_MINB_FULL) k_scan_hw_full(Dev d) { scan_hw<kDirectFull>(d); }
 
 // k_union: unite this round's coupling edges (carried-over + new), one thread per edge
 // (ECL-CC style hooking of the larger root under the smaller, so roots stay the
