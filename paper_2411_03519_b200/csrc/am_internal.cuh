@@ -45,6 +45,9 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #ifndef AM_SCAN_MINB_FULL
 #define AM_SCAN_MINB_FULL AM_SCAN_MINB
 #endif
+#ifndef AM_SCAN_FULL_REC
+#define AM_SCAN_FULL_REC 1   // full rounds take their agents from the cell-sorted records
+#endif
 #ifndef AM_DIRECT_FULL
 #define AM_DIRECT_FULL 16   // ... of full-recompute rounds (C5 snapshot A/B: 777 / 649 / 624 us at 64 / 32 / 16)
 #endif

@@ -849,7 +849,10 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
     }
 }
 
-template <int KD>
+// kRec (full-recompute rounds, where the queue holds every binned agent): the agents are
+// taken from the cell-sorted records instead of the id-ordered queue, so neighbouring
+// half-warps scan neighbouring cells (cell-table and record reads shared in L1/L2)
+template <int KD, bool kRec>
 __device__ __forceinline__ void scan_hw(const Dev& d)
 {
     pdl_begin();
@@ -861,8 +864,8 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
     EdgeStage& sm = s_all[threadIdx.x >> 5];
     int2* list = s_list[hw];
     if (lane == 0) sm.ne = 0;
-    stripe_prefix(d.wq_ctr, 1 << 30, s_pref);
-    const int nq = s_pref[kEdgeStripes];
+    if (!kRec) stripe_prefix(d.wq_ctr, 1 << 30, s_pref);
+    const int nq = kRec ? d.ctab[d.ncells].x : s_pref[kEdgeStripes];
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_work = nq;
     const int W = d.ctl->W;
     const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
@@ -886,12 +889,17 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
         if (q < nq) {                                                  // half-warp uniform
             // stripe of queue entry q: the number of stripe starts <= q among stripes
             // 1..63 (prefixes are non-decreasing), counted by the 16 lanes at once
-            const int lo = (int)__reduce_add_sync(hm, (unsigned)((s_pref[1 + l] <= q) + (s_pref[17 + l] <= q) +
-                                                                 (s_pref[33 + l] <= q) + (s_pref[49 + l] <= q)));
-            const int4 A = d.wq[(size_t)lo * d.wq_cap + (q - s_pref[lo])];
+            int4 A;
+            if (kRec) {
+                A = d.rec[q];
+            } else {
+                const int lo = (int)__reduce_add_sync(hm, (unsigned)((s_pref[1 + l] <= q) + (s_pref[17 + l] <= q) +
+                                                                     (s_pref[33 + l] <= q) + (s_pref[49 + l] <= q)));
+                A = d.wq[(size_t)lo * d.wq_cap + (q - s_pref[lo])];
+            }
             const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
-            const uint32_t aid = (uint32_t)A.z & 0x7FFFFFFFu;
-            const bool chg = ((uint32_t)A.z >> 31) != 0;
+            const uint32_t aid = kRec ? (uint32_t)A.z : ((uint32_t)A.z & 0x7FFFFFFFu);
+            const bool chg = kRec ? (A.w & kRecChanged) != 0 : ((uint32_t)A.z >> 31) != 0;
             const bool idle = (A.w & 3) == ST_IDLE;
             const bool far = idle && as > W && !(d.flags & AM_DBG_SKIP_FAR);
             nfar += (far && l == 0) ? 1u : 0u;
@@ -984,8 +992,8 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
     hw_flush_stats(d, hs, lane);
 }
 // the incremental rounds' scan and the full-recompute rounds' scan (host-selected)
-__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d) { scan_hw<kDirect>(d); }
-__global__ void __launch_bounds__(256, AM_SCAN_MINB_FULL) k_scan_hw_full(Dev d) { scan_hw<kDirectFull>(d); }
+__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d) { scan_hw<kDirect, false>(d); }
+__global__ void __launch_bounds__(256, AM_SCAN_MINB_FULL) k_scan_hw_full(Dev d) { scan_hw<kDirectFull, AM_SCAN_FULL_REC != 0>(d); }
 
 // k_union: unite this round's coupling edges (carried-over + new), one thread per edge
 // (ECL-CC style hooking of the larger root under the smaller, so roots stay the
