@@ -12,8 +12,13 @@ restates in oracle.c.  Parity status per function:
   tests/golden, BFS components, invariants, brute force on tiny maps).
 * replay / lockstep: pinned by the closed forms D1-D5 and the OoO == lock-step
   outcome invariant.
-* duration / policy_move / digest (synthetic driver, Q16): the paper is silent;
-  parity unpinned by the paper (pinned only by splitmix64's published value).
+* duration / policy_move / digest / key3 / the trajectory hash (synthetic driver,
+  Q16): the paper is silent -- our own constructs; pinned against an
+  independent pure-Python implementation of the c.4 definitions built on splitmix64's
+  published outputs, plus structural pins (tests/test_oracle_pins.py).
+* round_mt / labels_steps / blocked_list / round_at_scale / lockstep_grid
+  (oracle_scale.c, the same predicates with threaded outer loops for the 100k / 1M
+  configs): pinned by equality with round_ / lockstep on random and workload states.
 """
 from __future__ import annotations
 
@@ -26,6 +31,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
+_SRC_SCALE = os.path.join(_HERE, "oracle_scale.c")   # the same definitions at BASELINE sizes
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -36,13 +42,24 @@ OK, E_ARG, E_BOUNDS, E_PROTOCOL, E_VELOCITY, E_LIVENESS = 0, -1, -2, -3, -4, -8
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c into liboracle.so with gcc (plain -O2, no vectorisation tricks)."""
+    """Compile oracle.c + oracle_scale.c into liboracle.so with gcc (plain -O2, no
+    vectorisation tricks; pthreads for the at-scale drivers' outer loops)."""
     with _lock:
-        if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC_SCALE))
+        if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
             tmp = _LIB + f".tmp{os.getpid()}"
-            subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC])
+            subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-pthread", "-o", tmp,
+                                   _SRC, _SRC_SCALE])
             os.replace(tmp, _LIB)
     return _LIB
+
+
+def host_threads() -> int:
+    """Host cores this process may use (the at-scale oracle's thread count)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:
+        return max(1, os.cpu_count() or 1)
 
 
 class Params(C.Structure):
@@ -97,6 +114,11 @@ def lib():
                                  C.POINTER(Log)]
         L.orc_replay_cap.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int64, C.c_int64, C.c_int32,
                                      vp, vp, vp, vp, vp, C.POINTER(Log)]
+        # oracle_scale.c
+        L.orc_round_mt.argtypes = [P, C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp, vp, vp, vp, C.c_int32]
+        L.orc_labels_steps.argtypes = [P, C.c_int32, vp, vp, vp, vp, vp, C.c_int32]
+        L.orc_blocked_list.argtypes = [P, C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp, C.c_int32]
+        L.orc_lockstep_grid.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int32, vp, vp, vp, vp, C.c_int32]
         _lib = L
     return _lib
 
@@ -272,3 +294,86 @@ def replay(p: Params, sy: SynthTables, x0, y0, Q: int = 0, log_rounds: int = 0,
                 log_id=eid[:ne].copy(), log_label=elab[:ne].copy(),
                 log_complete=(lg.n_rounds <= log_rounds and lg.n_entries <= log_entries),
                 violations=int(lg.violations), max_spread=int(lg.max_spread))
+
+
+# ------------------------------------------------------------------ at BASELINE sizes
+# (oracle_scale.c: the same predicates of oracle.c with threaded outer loops)
+def round_mt(p: Params, x, y, step, status, peek=False, threads: int | None = None):
+    """orc_round (one simulation) with the outer loops over agents split across host
+    threads; every pair is still tested.  Same outputs as round_()."""
+    x, y, step = _i32(x), _i32(y), _i32(step)
+    n = len(x)
+    assert status.dtype == np.uint8 and status.flags.c_contiguous
+    blocked = np.zeros(n, np.uint8)
+    label = np.zeros(n, np.int32)
+    mask = np.zeros(n, np.uint8)
+    order = np.zeros(max(n, 1), np.int32)
+    nr = np.zeros(1, np.int32)
+    rc = lib().orc_round_mt(C.byref(p), n, _p(x), _p(y), _p(step), _p(status), int(bool(peek)),
+                            _p(blocked), _p(label), _p(mask), _p(order), _p(nr), int(threads or host_threads()))
+    if rc != OK:
+        raise RuntimeError(f"orc_round_mt rc={rc}")
+    return dict(blocked=blocked, label=label, mask=mask, order=order[: nr[0]].copy())
+
+
+def labels_steps(p: Params, x, y, step, status, threads: int | None = None) -> np.ndarray:
+    """Cluster label (min id, -1 DONE) of every agent: all same-step pairs tested."""
+    x, y, step = _i32(x), _i32(y), _i32(step)
+    status = np.ascontiguousarray(status, np.uint8)
+    label = np.zeros(len(x), np.int32)
+    rc = lib().orc_labels_steps(C.byref(p), len(x), _p(x), _p(y), _p(step), _p(status), _p(label),
+                                int(threads or host_threads()))
+    if rc != OK:
+        raise RuntimeError(f"orc_labels_steps rc={rc}")
+    return label
+
+
+def blocked_list(p: Params, x, y, step, status, idx, threads: int | None = None) -> np.ndarray:
+    """Blocking verdict of the listed agents, each by a scan over all agents."""
+    x, y, step = _i32(x), _i32(y), _i32(step)
+    status = np.ascontiguousarray(status, np.uint8)
+    idx = _i32(idx)
+    out = np.zeros(len(idx), np.uint8)
+    rc = lib().orc_blocked_list(C.byref(p), len(x), _p(x), _p(y), _p(step), _p(status), len(idx), _p(idx),
+                                _p(out), int(threads or host_threads()))
+    if rc != OK:
+        raise RuntimeError(f"orc_blocked_list rc={rc}")
+    return out
+
+
+def round_at_scale(p: Params, x, y, step, status, sample, threads: int | None = None):
+    """The round's outputs where they can be computed exactly at 1M agents: the label
+    of EVERY agent (labels_steps), and for the sampled agents the blocking verdict and
+    the ready bit -- the latter from the blocking verdicts of every member of the
+    agent's cluster (cluster-ready rule P:162 / P:184) and the members' statuses."""
+    status = np.ascontiguousarray(status, np.uint8)
+    label = labels_steps(p, x, y, step, status, threads)
+    sample = _i32(sample)
+    comp = np.isin(label, np.unique(label[sample][label[sample] >= 0]))
+    members = np.flatnonzero(comp).astype(np.int32)
+    blk_m = blocked_list(p, x, y, step, status, members, threads)
+    blocked = np.zeros(len(x), np.uint8)
+    blocked[members] = blk_m
+    bad = {}
+    for i, b in zip(members.tolist(), blk_m.tolist()):
+        lab = int(label[i])
+        bad[lab] = bad.get(lab, False) or bool(b) or int(status[i]) == RUNNING
+    mask = np.array([int(status[i]) == IDLE and not bad.get(int(label[i]), False) if label[i] >= 0 else False
+                     for i in sample.tolist()], np.uint8)
+    return dict(label=label, blocked=blocked[sample], mask=mask, members=members)
+
+
+def lockstep_grid(p: Params, sy: SynthTables, x0, y0, T: int, threads: int | None = None):
+    """orc_lockstep (one simulation, co-occupancy) with the perceived sets gathered
+    through an oracle-private hash grid (perception only; outputs identical)."""
+    if sy.s.conflict:
+        raise ValueError("lockstep_grid: co-occupancy only (use lockstep for exclusive tiles)")
+    x, y = _i32(x0).copy(), _i32(y0).copy()
+    n = len(x)
+    traj = np.zeros(n, np.uint64)
+    tsync = np.zeros(1, np.int64)
+    rc = lib().orc_lockstep_grid(C.byref(p), C.byref(sy.s), n, int(T), _p(x), _p(y), _p(traj), _p(tsync),
+                                 int(threads or host_threads()))
+    if rc != OK:
+        raise RuntimeError(f"orc_lockstep_grid rc={rc}")
+    return dict(x=x, y=y, traj=traj, T_sync=tsync)

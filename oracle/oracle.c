@@ -17,10 +17,14 @@
  * Pins (tests/test_oracle.py): hand-worked vectors V1..V14 (tests/golden/),
  * closed-form driver vectors D1..D5, invariants I1..I7, connected components
  * cross-checked against a BFS written independently in the test, brute-force
- * enumeration of tiny maps.  The synthetic latency/policy functions (mix64,
- * key3, orc_duration, orc_policy_move) are our own constructs (the paper is
- * silent, Q16): parity unpinned by the paper; pinned only by splitmix64's
- * published test value and by the closed forms D1..D5.
+ * enumeration of tiny maps; orc_validity_violations by exact counts on hand states
+ * at the strict P:156 boundary (tests/test_oracle_pins.py).  The synthetic
+ * latency/policy functions (mix64, key3, orc_duration, orc_digest, orc_policy_move,
+ * the trajectory hash) are our own constructs (the paper is silent, Q16): pinned
+ * against an independent Python implementation of SURVEY 8(c.4) built on
+ * splitmix64's published outputs, structural cases, and the closed forms D1..D5.
+ * oracle_scale.c drives the same predicates at BASELINE sizes (threads, per-step
+ * pair enumeration, hash-grid perception for the lock-step run).
  */
 #include <stdint.h>
 #include <stdlib.h>
