@@ -137,51 +137,84 @@ def _dist():
 
 
 # ------------------------------------------------------------------ CPU oracle baseline
-def oracle_sample(w, seconds: float, seed: int = 0):
+def oracle_sample(w, state, seconds: float, seed: int = 0):
     """The oracle as it stands (single-threaded C, brute force) on a bounded sample of
-    the workload: sampled agents of the workload's initial round state, each resolved
-    one by one (blocked test O(N), component walk O(N*|C|)).  Returns
-    (ready agent-steps resolved per second, agents sampled, seconds)."""
+    the workload: sampled agents of ``state`` -- the pre-rolled round the GPU is timed
+    on (``prerolled_state``) -- each resolved one by one (blocking test O(N), cluster
+    walk O(N*|C|)).  Returns (ready agent-steps resolved per second, agents sampled,
+    seconds)."""
     import numpy as np
 
     import oracle as O
-    n = len(w.x)
+    x, y, steps, status = state
+    n = len(x)
     p = O.params(w.map_w, w.map_h, w.r_p, w.v, w.steps)
-    steps = np.zeros(n, np.int32)
-    status = np.zeros(n, np.uint8)
     rng = np.random.default_rng(seed)
     ready = sampled = 0
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < seconds:
         smp = rng.integers(0, n, 4).astype(np.int32)
-        r = O.round_sampled(p, w.x, w.y, steps, status, smp)
+        r = O.round_sampled(p, x, y, steps, status, smp)
         ready += int(r["mask"].sum())
         sampled += len(smp)
     dt = time.perf_counter() - t0
     return ready / dt, sampled, dt
 
 
-def oracle_sample_threads(w, seconds: float, threads: int):
+def oracle_sample_threads(w, state, seconds: float, threads: int):
     """the same oracle, as it stands, on `threads` host cores at once --
     an outer loop over sampled agents split across threads (each thread its own seed;
     ctypes releases the GIL around every oracle.c call).  Returns (aggregate ready
     agent-steps per second, agents sampled, seconds)."""
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(threads) as ex:
-        res = list(ex.map(lambda k: oracle_sample(w, seconds, seed=1000 + k), range(threads)))
+        res = list(ex.map(lambda k: oracle_sample(w, state, seconds, seed=1000 + k), range(threads)))
     return sum(r[0] for r in res), sum(r[1] for r in res), max(r[2] for r in res)
 
 
-def run_reference(args, w):
+def take_round_state(rep):
+    """Runs one replay round with its outputs and returns the state that round resolved:
+    (x, y, steps, status) as the round saw them -- the world arrays after the last
+    commits, and the statuses with the agents it dispatched still IDLE."""
+    import numpy as np
+    import torch
+    x = rep.pos[:, 0].cpu().numpy().copy()
+    y = rep.pos[:, 1].cpu().numpy().copy()
+    s = rep.steps.cpu().numpy().copy()
+    mask, _, _ = rep.step()
+    st = rep.tracker.status().cpu().numpy().copy()
+    torch.cuda.synchronize()
+    st[mask.cpu().numpy() == 1] = 0   # IDLE
+    return x, y, s, st.astype(np.uint8)
+
+
+def prerolled_state(w, lm, preroll: int):
+    """The input state of the timed rounds, for the oracle arm: the workload's replay
+    pre-rolled `preroll` rounds (deterministic: a pure function of the seeds), then the
+    state of the next round.  The pre-roll itself is input preparation, untimed."""
+    import torch
+
+    from paper_2411_03519_b200 import Replay
+    dev = torch.device("cuda", _dist()[2])
+    torch.cuda.set_device(dev)
+    rep = Replay.from_workload(w, lm, device=dev)
+    rep.run(preroll)
+    st = take_round_state(rep)
+    rep.close()
+    return st
+
+
+def run_reference(args, w, lm):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
     import oracle as O
     O.build()
+    state = prerolled_state(w, lm, args.preroll)
     times, resolved, sampled = [], 0, 0
     nt = max(1, len(os.sched_getaffinity(0)))
     for k in range(args.warmup + args.steps):
-        v, sm, dt = oracle_sample_threads(w, args.ref_step_seconds, nt)
+        v, sm, dt = oracle_sample_threads(w, state, args.ref_step_seconds, nt)
         if k >= args.warmup:
             times.append(dt)
             resolved += v * dt
@@ -194,9 +227,9 @@ def run_reference(args, w):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic", "config": _config(w, ws),
         "cpu_baseline": {"kind": "oracle", "value": value, "unit": UNIT, "cores": nt,
-                         "sample": f"{sampled} sampled agents of the {w.name} initial round "
-                                   f"({len(w.x)} agents), resolved one by one by oracle.c "
-                                   f"on {nt} threads"},
+                         "sample": f"{sampled} sampled agents of the {w.name} round after a "
+                                   f"{args.preroll}-round pre-roll ({len(w.x)} agents; the state the GPU "
+                                   f"arm times), resolved one by one by oracle.c on {nt} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -400,6 +433,10 @@ def run_ours(args, w, lm):
         rep.sync()
     prof_w = rep.profile_read()
     dom = max((k for k in prof_w if prof_w[k][1] > 0), key=lambda k: prof_w[k][0])
+    # the state of the next round: the CPU oracle baseline samples exactly this state
+    # (SURVEY 8(d.4) "same inputs, same run"); the round itself is one more warm-up
+    rep.profile(0)
+    cpu_state = take_round_state(rep)
     shares = {k: v[0] / v[1] for k, v in prof_w.items() if v[1] > 0}
     # timed region: only the dominant kernel bracketed by events
     rep.profile(1 << names.index(dom))
@@ -572,13 +609,14 @@ def run_ours(args, w, lm):
     # the oracle on the host cores, bounded sample (rank 0, N = 1 only)
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
-        v, sm, dt = oracle_sample(w, args.cpu_seconds)
+        v, sm, dt = oracle_sample(w, cpu_state, args.cpu_seconds)
         nt = max(1, len(os.sched_getaffinity(0)))
-        vt, smt, dtt = oracle_sample_threads(w, args.cpu_seconds / 2, nt) if nt > 1 else (v, sm, dt)
+        vt, smt, dtt = oracle_sample_threads(w, cpu_state, args.cpu_seconds / 2, nt) if nt > 1 else (v, sm, dt)
         cpu = {"value": vt, "unit": UNIT, "cores": nt, "kind": "oracle",
-               "sample": f"{smt} sampled agents of the {w.name} initial round ({n} agents) resolved "
-                         f"one by one by oracle.c in {dtt:.1f} s on {nt} threads (outer loop over "
-                         f"sampled agents, one seed per thread)",
+               "sample": f"{smt} sampled agents of the pre-rolled {w.name} round the GPU is timed on "
+                         f"({n} agents, after {args.preroll} + {args.warmup} rounds) resolved one by one "
+                         f"by oracle.c in {dtt:.1f} s on {nt} threads (outer loop over sampled agents, "
+                         f"one seed per thread)",
                "single_thread": {"value": v, "cores": 1,
                                  "sample": f"{sm} sampled agents in {dt:.1f} s"},
                "host_cores_available": os.cpu_count()}
@@ -641,7 +679,7 @@ def main():
     w = amgen.config(args.workload, n=args.agents)
     lm = amgen.latency_model(w.profile)
     if args.impl == "reference":
-        return run_reference(args, w)
+        return run_reference(args, w, lm)
     return run_ours(args, w, lm)
 
 

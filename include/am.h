@@ -26,10 +26,15 @@
  * tensors' data_ptr()) owned by the caller, unless marked "host".  Work is enqueued
  * on the context's stream (am_config.stream, a cudaStream_t; NULL = legacy default
  * stream) and is asynchronous: the caller keeps every input/output array alive and
- * untouched until that stream work completes (am_ready / am_sync synchronise).  The
- * context owns its own device workspace (allocated in am_init, freed in am_destroy;
- * am_workspace_bytes reports its size) and small host state.  Nothing is allocated
- * after am_init.  A context is not thread-safe: one host thread at a time.
+ * untouched until that stream work completes (am_ready / am_sync synchronise).
+ * DEVICE WORKSPACE (two-phase idiom): am_workspace_size() gives the bytes a context
+ * with these arguments needs; the caller allocates them (e.g. a torch uint8 CUDA
+ * tensor, so PyTorch's allocator serves all device memory), passes the pointer in
+ * am_config.workspace and keeps it alive until am_destroy.  With workspace == NULL the
+ * context allocates its own (cudaMalloc in am_init, cudaFree in am_destroy).  The
+ * context otherwise owns only small host state, a pinned control-block mirror, and
+ * its side streams / events.  Nothing is allocated after am_init.  A context is not
+ * thread-safe: one host thread at a time.
  *
  * ERRORS.  Every call returns AM_OK (0) or a negative AM_E_* code; no exception
  * crosses the ABI.  Commit validation happens on the device inside am_update; its
@@ -57,6 +62,7 @@ extern "C" {
 #define AM_E_CUDA       -5   /* CUDA runtime error (message in am_last_error)             */
 #define AM_E_NCCL       -6   /* reserved for the multi-GPU exchange                       */
 #define AM_E_STATE      -11  /* call out of order (e.g. am_ready before any am_update)    */
+#define AM_E_WORKSPACE  -13  /* caller workspace too small or not 256-byte aligned         */
 #define AM_E_LIVENESS   -12  /* replay driver: nothing running but agents not DONE        */
 
 /* agent status values (am_set_state / am_status) */
@@ -90,6 +96,9 @@ typedef struct {
     int32_t  metric;       /* AM_METRIC_L2 or AM_METRIC_LINF                              */
     uint32_t flags;        /* AM_* flags                                                  */
     void*    stream;       /* cudaStream_t                                                */
+    void*    workspace;    /* caller-owned device memory of >= am_workspace_size() bytes, */
+                           /* 256-byte aligned; NULL = the context allocates its own       */
+    size_t   workspace_bytes;
 } am_config;
 
 /* Round statistics of the most recent am_ready (host copy, filled at its sync). */
@@ -109,10 +118,17 @@ typedef struct {
     int32_t n_passes;      /* binned: radix passes the priority order needed              */
 } am_round_stats;
 
+/* Device workspace bytes am_init needs for these arguments (the same validation as
+ * am_init; 0 if they are invalid).  No CUDA call: usable before any device work. */
+size_t am_workspace_size(int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max, int32_t n_agents,
+                         const am_config* cfg);
+
 /* Create a tracker for n_agents agents on a map_w x map_h tile map (1..32768 each),
  * perception radius radius_p >= 0 and max speed v_max >= 0 tiles per step.
- * cfg may be NULL (defaults: no target, 1 sim, auto cell, L2, AM_VALIDATE).
- * *out receives the context.  Allocates the device workspace on the current device. */
+ * cfg may be NULL (defaults: no target, 1 sim, auto cell, L2, AM_VALIDATE, own workspace).
+ * *out receives the context.  Radii >= 46340 tiles are clamped (they already cover
+ * every distance on a <= 32768^2 map; no result changes).  Errors: AM_E_ARG, AM_E_WORKSPACE,
+ * AM_E_CUDA. */
 int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max,
             int32_t n_agents, const am_config* cfg);
 
@@ -167,7 +183,7 @@ int am_set_stream(am_ctx* ctx, void* stream);
 /* Forget the state: the next am_update is an initial state again. */
 int am_reset(am_ctx* ctx);
 
-/* Device bytes owned by the context. */
+/* Device workspace bytes of the context (caller-provided or its own). */
 size_t am_workspace_bytes(const am_ctx* ctx);
 
 /* Device pointer of the round's device-side ready count (int32), for graph capture. */

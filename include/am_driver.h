@@ -66,12 +66,21 @@ typedef struct {
 
 typedef struct am_replay am_replay;
 
+/* Device workspace bytes of a replay on ctx (event clock, dispatch times, moves,
+ * trajectory hashes, round outputs, the host-loop shadow): the two-phase idiom of am.h. */
+size_t am_replay_workspace_size(const am_ctx* ctx);
+
 /* Create a replay on ctx (which must have been created with target_step > 0; the
  * replay sets AM_DIGEST and clears AM_PEEK/AM_ASYNC on it as needed).
  * positions int32 [n][2] and steps int32 [n] are the world state, updated in place
- * by commits; the replay starts from the current contents (steps normally all 0). */
+ * by commits; the replay starts from the current contents (steps normally all 0).
+ * workspace: caller-owned device memory of >= am_replay_workspace_size(ctx) bytes,
+ * 256-byte aligned, alive until am_replay_destroy (NULL: the replay allocates its own).
+ * Nothing is allocated after creation (am_replay_io included).  Errors: AM_E_ARG,
+ * AM_E_WORKSPACE, AM_E_CUDA. */
 int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* synth,
-                     int64_t quantum_us, int32_t* positions, int32_t* steps);
+                     int64_t quantum_us, int32_t* positions, int32_t* steps, void* workspace,
+                     size_t workspace_bytes);
 
 /* Run up to max_rounds rounds without host synchronisation, then synchronise.  On the
  * cell-binned path the rounds are a CUDA graph of one round replayed; when every

@@ -119,6 +119,10 @@ def lib():
         L.orc_labels_steps.argtypes = [P, C.c_int32, vp, vp, vp, vp, vp, C.c_int32]
         L.orc_blocked_list.argtypes = [P, C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp, C.c_int32]
         L.orc_lockstep_grid.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int32, vp, vp, vp, vp, C.c_int32]
+        L.orc_replay_sim_logged.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int64, C.c_int32, vp, vp, vp,
+                                            vp, vp, C.POINTER(Log)]
+        L.orc_replay_mt.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int64, C.c_int64, C.c_int32,
+                                    vp, vp, vp, vp, vp, C.c_int32]
         _lib = L
     return _lib
 
@@ -377,3 +381,51 @@ def lockstep_grid(p: Params, sy: SynthTables, x0, y0, T: int, threads: int | Non
     if rc != OK:
         raise RuntimeError(f"orc_lockstep_grid rc={rc}")
     return dict(x=x, y=y, traj=traj, T_sync=tsync)
+
+
+def replay_mt(p: Params, sy: SynthTables, x0, y0, Q: int = 0, capacity: int = 0, priority: bool = True,
+              threads: int | None = None):
+    """orc_replay_cap with the simulations of a batch replayed concurrently (final states,
+    T_ooo and round counts only; identical to replay())."""
+    x, y = _i32(x0).copy(), _i32(y0).copy()
+    n = len(x)
+    traj = np.zeros(n, np.uint64)
+    tooo = np.zeros(p.n_sims, np.int64)
+    rounds = np.zeros(p.n_sims, np.int64)
+    rc = lib().orc_replay_mt(C.byref(p), C.byref(sy.s), n, int(Q), int(capacity), int(bool(priority)), _p(x), _p(y),
+                             _p(traj), _p(tooo), _p(rounds), int(threads or host_threads()))
+    if rc != OK:
+        raise RuntimeError(f"orc_replay_mt rc={rc}")
+    return dict(x=x, y=y, traj=traj, T_ooo=tooo, rounds=rounds)
+
+
+def replay_sims_logged(p: Params, sy: SynthTables, x0, y0, sims, Q: int = 0, log_rounds: int = 10**6,
+                       log_entries: int = 10**6):
+    """The replay of selected simulations of a batch, each with its own round log (the
+    loop body of orc_replay for simulation b, run alone).  Returns {b: dict(log_nready,
+    log_id, log_label, T_ooo, rounds, traj of the simulation's agents)}."""
+    x, y = _i32(x0).copy(), _i32(y0).copy()
+    n = len(x)
+    out = {}
+    for b in sims:
+        traj = np.zeros(n, np.uint64)
+        tooo = np.zeros(p.n_sims, np.int64)
+        rounds = np.zeros(p.n_sims, np.int64)
+        rt = np.zeros(log_rounds, np.int64)
+        rs = np.zeros(log_rounds, np.int32)
+        rn = np.zeros(log_rounds, np.int32)
+        eid = np.zeros(log_entries, np.int32)
+        elab = np.zeros(log_entries, np.int32)
+        lg = Log(log_rounds, log_entries, _p(rt).value, _p(rs).value, _p(rn).value, _p(eid).value,
+                 _p(elab).value, 0, 0, 0, 0, 0)
+        xb, yb = x.copy(), y.copy()
+        rc = lib().orc_replay_sim_logged(C.byref(p), C.byref(sy.s), n, int(Q), int(b), _p(xb), _p(yb), _p(traj),
+                                         _p(tooo), _p(rounds), C.byref(lg))
+        if rc != OK:
+            raise RuntimeError(f"orc_replay_sim_logged rc={rc}")
+        assert lg.n_rounds <= log_rounds and lg.n_entries <= log_entries
+        lo, hi = b * n // p.n_sims, (b + 1) * n // p.n_sims
+        out[b] = dict(log_nready=rn[: lg.n_rounds].copy(), log_id=eid[: lg.n_entries].copy(),
+                      log_label=elab[: lg.n_entries].copy(), T_ooo=int(tooo[b]), rounds=int(rounds[b]),
+                      traj=traj[lo:hi].copy(), x=xb[lo:hi].copy(), y=yb[lo:hi].copy())
+    return out

@@ -512,22 +512,31 @@ int orc_replay(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q,
     return orc_replay_cap(p, sy, n, Q, 0, 1, x, y, traj, T_ooo, rounds, log);
 }
 
-int orc_replay_cap(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q, int64_t K, int32_t priority,
-                   int32_t* x, int32_t* y, uint64_t* traj, int64_t* T_ooo, int64_t* rounds, orc_log* log)
-{
-    if (p->target <= 0 || K < 0) return ORC_E_ARG;
-    uint64_t* qkey = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));   /* queued members' keys */
-    int32_t* step = (int32_t*)calloc(n ? n : 1, sizeof(int32_t));
-    uint8_t* status = (uint8_t*)calloc(n ? n : 1, 1);
-    int64_t* tc = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
-    int32_t* mvx = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
-    int32_t* mvy = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
-    int64_t* cmax = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
-    int rc = ORC_OK;
-    if (log) { log->n_rounds = 0; log->n_entries = 0; log->violations = 0; log->max_spread = 0; }
-    for (int32_t i = 0; i < n; i++) traj[i] = 0;
+/* work arrays of a replay, indexed by agent id; simulation b only touches its slice
+ * [lo, hi), so simulations may be replayed one after another or concurrently */
+typedef struct {
+    uint64_t* qkey;   /* queued members' keys (finite capacity) */
+    int32_t* step;
+    uint8_t* status;
+    int64_t* tc;      /* completion time of the agent's dispatched step */
+    int32_t *mvx, *mvy;   /* move computed at dispatch */
+    int64_t* cmax;    /* cluster completion time, by label */
+} orc_replay_work;
 
-    for (int32_t b = 0; b < p->n_sims && rc == ORC_OK; b++) {
+/* the replay of simulation b (the loop body of orc_replay_cap) */
+int orc_replay_sim(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q, int64_t K, int32_t priority,
+                   int32_t b, const orc_replay_work* wk, int32_t* x, int32_t* y, uint64_t* traj, int64_t* T_ooo,
+                   int64_t* rounds, orc_log* log)
+{
+    uint64_t* qkey = wk->qkey;
+    int32_t* step = wk->step;
+    uint8_t* status = wk->status;
+    int64_t* tc = wk->tc;
+    int32_t* mvx = wk->mvx;
+    int32_t* mvy = wk->mvy;
+    int64_t* cmax = wk->cmax;
+    int rc = ORC_OK;
+    {
         int32_t lo = sim_lo(n, p->n_sims, b), hi = sim_lo(n, p->n_sims, b + 1);
         int32_t m = hi - lo;
         orc_params ps = *p; ps.n_sims = 1;
@@ -654,9 +663,26 @@ int orc_replay_cap(const orc_params* p, const orc_synth* sy, int32_t n, int64_t 
         rounds[b] = nr_b;
         free(lab); free(msk); free(ord); free(blk);
     }
-    free(step); free(status); free(tc); free(mvx); free(mvy); free(cmax); free(qkey);
-    if (rc == ORC_OK && log && log->n_rounds >= log->cap_rounds && log->cap_rounds > 0) {
-        /* log truncated is not an error; callers compare n_rounds with cap */
-    }
+    return rc;
+}
+
+int orc_replay_cap(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q, int64_t K, int32_t priority,
+                   int32_t* x, int32_t* y, uint64_t* traj, int64_t* T_ooo, int64_t* rounds, orc_log* log)
+{
+    if (p->target <= 0 || K < 0) return ORC_E_ARG;
+    orc_replay_work wk;
+    wk.qkey = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+    wk.step = (int32_t*)calloc(n ? n : 1, sizeof(int32_t));
+    wk.status = (uint8_t*)calloc(n ? n : 1, 1);
+    wk.tc = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    wk.mvx = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
+    wk.mvy = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
+    wk.cmax = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    int rc = ORC_OK;
+    if (log) { log->n_rounds = 0; log->n_entries = 0; log->violations = 0; log->max_spread = 0; }
+    for (int32_t i = 0; i < n; i++) traj[i] = 0;
+    for (int32_t b = 0; b < p->n_sims && rc == ORC_OK; b++)
+        rc = orc_replay_sim(p, sy, n, Q, K, priority, b, &wk, x, y, traj, T_ooo, rounds, log);
+    free(wk.step); free(wk.status); free(wk.tc); free(wk.mvx); free(wk.mvy); free(wk.cmax); free(wk.qkey);
     return rc;
 }

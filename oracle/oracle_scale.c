@@ -399,3 +399,80 @@ int orc_lockstep_grid(const orc_params* p, const orc_synth* sy, int32_t n, int32
     free(cstart); free(cidx); free(nx); free(ny); free(dmax); free(fill);
     return 0;
 }
+
+/* ============================================================ orc_replay_mt
+ * orc_replay_cap (oracle.c) with the simulations of a batch (C3) replayed concurrently:
+ * each simulation's replay (orc_replay_sim, the loop body of orc_replay_cap) only
+ * touches its own slice of the work arrays, so the per-simulation results are those
+ * of the sequential loop.  No round log. */
+typedef struct {
+    uint64_t* qkey;
+    int32_t* step;
+    uint8_t* status;
+    int64_t* tc;
+    int32_t *mvx, *mvy;
+    int64_t* cmax;
+} orc_replay_work;
+typedef struct orc_log orc_log;
+int orc_replay_sim(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q, int64_t K, int32_t priority,
+                   int32_t b, const orc_replay_work* wk, int32_t* x, int32_t* y, uint64_t* traj, int64_t* T_ooo,
+                   int64_t* rounds, orc_log* log);
+typedef struct {
+    const orc_params* p;
+    const orc_synth* sy;
+    int32_t n;
+    int64_t Q, K;
+    int32_t prio;
+    const orc_replay_work* wk;
+    int32_t *x, *y;
+    uint64_t* traj;
+    int64_t *T_ooo, *rounds;
+    int32_t* rc;
+} rp_t;
+static void rp_body(void* a, int64_t lo, int64_t hi)
+{
+    rp_t* r = (rp_t*)a;
+    for (int64_t b = lo; b < hi; b++)
+        r->rc[b] = orc_replay_sim(r->p, r->sy, r->n, r->Q, r->K, r->prio, (int32_t)b, r->wk, r->x, r->y, r->traj,
+                                  r->T_ooo, r->rounds, NULL);
+}
+int orc_replay_mt(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q, int64_t K, int32_t priority,
+                  int32_t* x, int32_t* y, uint64_t* traj, int64_t* T_ooo, int64_t* rounds, int32_t nthreads)
+{
+    if (p->target <= 0 || K < 0) return -1;
+    orc_replay_work wk;
+    wk.qkey = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+    wk.step = (int32_t*)calloc(n ? n : 1, sizeof(int32_t));
+    wk.status = (uint8_t*)calloc(n ? n : 1, 1);
+    wk.tc = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    wk.mvx = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
+    wk.mvy = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
+    wk.cmax = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    int32_t* rc = (int32_t*)calloc(p->n_sims, sizeof(int32_t));
+    for (int32_t i = 0; i < n; i++) traj[i] = 0;
+    rp_t r = {p, sy, n, Q, K, priority, &wk, x, y, traj, T_ooo, rounds, rc};
+    parallel_for(nthreads, p->n_sims, rp_body, &r);
+    int out = 0;
+    for (int32_t b = 0; b < p->n_sims; b++) if (rc[b]) out = rc[b];
+    free(wk.step); free(wk.status); free(wk.tc); free(wk.mvx); free(wk.mvy); free(wk.cmax); free(wk.qkey); free(rc);
+    return out;
+}
+
+/* the replay of simulation b alone, with its round log (infinite capacity) */
+int orc_replay_sim_logged(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q, int32_t b, int32_t* x,
+                          int32_t* y, uint64_t* traj, int64_t* T_ooo, int64_t* rounds, orc_log* log)
+{
+    if (p->target <= 0 || b < 0 || b >= p->n_sims) return -1;
+    orc_replay_work wk;
+    wk.qkey = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+    wk.step = (int32_t*)calloc(n ? n : 1, sizeof(int32_t));
+    wk.status = (uint8_t*)calloc(n ? n : 1, 1);
+    wk.tc = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    wk.mvx = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
+    wk.mvy = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
+    wk.cmax = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    for (int32_t i = 0; i < n; i++) traj[i] = 0;
+    const int rc = orc_replay_sim(p, sy, n, Q, 0, 1, b, &wk, x, y, traj, T_ooo, rounds, log);
+    free(wk.step); free(wk.status); free(wk.tc); free(wk.mvx); free(wk.mvy); free(wk.cmax); free(wk.qkey);
+    return rc;
+}

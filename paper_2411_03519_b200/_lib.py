@@ -14,7 +14,7 @@ _lib = None
 
 OK = 0
 E_ARG, E_BOUNDS, E_PROTOCOL, E_VELOCITY, E_CUDA, E_NCCL = -1, -2, -3, -4, -5, -6
-E_STATE, E_LIVENESS = -11, -12
+E_STATE, E_LIVENESS, E_WORKSPACE = -11, -12, -13
 IDLE, RUNNING, DONE = 0, 1, 2
 METRIC_L2, METRIC_LINF = 0, 1
 VALIDATE, PEEK, DIGEST, ASYNC, FORCE_BINNED, FORCE_SMALL, STATS, SCAN_THREAD = (
@@ -22,7 +22,7 @@ VALIDATE, PEEK, DIGEST, ASYNC, FORCE_BINNED, FORCE_SMALL, STATS, SCAN_THREAD = (
 
 ERROR_NAMES = {E_ARG: "AM_E_ARG", E_BOUNDS: "AM_E_BOUNDS", E_PROTOCOL: "AM_E_PROTOCOL",
                E_VELOCITY: "AM_E_VELOCITY", E_CUDA: "AM_E_CUDA", E_NCCL: "AM_E_NCCL",
-               E_STATE: "AM_E_STATE", E_LIVENESS: "AM_E_LIVENESS"}
+               E_STATE: "AM_E_STATE", E_LIVENESS: "AM_E_LIVENESS", E_WORKSPACE: "AM_E_WORKSPACE"}
 
 
 class AmError(RuntimeError):
@@ -33,7 +33,8 @@ class AmError(RuntimeError):
 
 class Config(C.Structure):
     _fields_ = [("target_step", C.c_int32), ("n_sims", C.c_int32), ("cell", C.c_int32),
-                ("metric", C.c_int32), ("flags", C.c_uint32), ("stream", C.c_void_p)]
+                ("metric", C.c_int32), ("flags", C.c_uint32), ("stream", C.c_void_p),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t)]
 
 
 class RoundStats(C.Structure):
@@ -61,6 +62,7 @@ class Synth(C.Structure):
 _vp, _i32, _i64, _u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
 SIGNATURES = {
     "am_init": (C.c_int, [C.POINTER(_vp), _i32, _i32, _i32, _i32, _i32, C.POINTER(Config)]),
+    "am_workspace_size": (C.c_size_t, [_i32, _i32, _i32, _i32, _i32, C.POINTER(Config)]),
     "am_update": (C.c_int, [_vp, _vp, _vp]),
     "am_set_state": (C.c_int, [_vp, _vp, _vp, _vp]),
     "am_ready": (C.c_int, [_vp, _vp, _vp, C.POINTER(_i32)]),
@@ -82,7 +84,8 @@ SIGNATURES = {
     "am_scan_stats": (C.c_int, [_vp, _vp]),
     "am_profile_read": (C.c_int, [_vp, _vp, _vp, _i32]),
     "am_profile_name": (C.c_char_p, [_i32]),
-    "am_replay_create": (C.c_int, [C.POINTER(_vp), _vp, C.POINTER(Synth), _i64, _vp, _vp]),
+    "am_replay_create": (C.c_int, [C.POINTER(_vp), _vp, C.POINTER(Synth), _i64, _vp, _vp, _vp, C.c_size_t]),
+    "am_replay_workspace_size": (C.c_size_t, [_vp]),
     "am_replay_run": (C.c_int, [_vp, _i64, C.POINTER(_i64)]),
     "am_replay_step": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(_i32)]),
     "am_replay_results": (C.c_int, [_vp, _vp, _vp, _vp]),

@@ -495,6 +495,7 @@ struct am_replay {
     am_ctx* ctx = nullptr;
     RepDev r{};
     void* mem = nullptr;
+    bool mem_owned = false;             // allocated here (no caller workspace)
     uint8_t* mask = nullptr;
     int32_t* order = nullptr;
     cudaStream_t stream = nullptr;      // own stream (graph capture)
@@ -534,7 +535,9 @@ static int enqueue_round(am_replay* rp)
     const unsigned nb = (unsigned)((n + 255) / 256);
     int rc = am_update_binned(c, (const int32_t*)rp->r.pos, rp->r.steps);
     if (rc) return rc;
+    c->defer_join = true;   // the sort overlaps dispatch + commit; joined below
     rc = am_ready(c, rp->mask, rp->order, nullptr);
+    c->defer_join = false;
     if (rc) return rc;
     rp->r.d = c->d;
     am_prof_begin(c, K_DISP_A);
@@ -553,8 +556,29 @@ static int enqueue_round(am_replay* rp)
     return AM_OK;
 }
 
+// device workspace layout of a replay (caller-owned, am_replay_workspace_size)
+struct RepLayout {
+    size_t total, tc, np, tr, tcl, ts, tn, td, rd, af, disp, live, chain, qk, mask, order, shadow;
+};
+static RepLayout rep_layout(const am_ctx* ctx)
+{
+    RepLayout L{};
+    const long long n = std::max(1, ctx->d.n), S = ctx->d.n_sims;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~size_t(255); return o; };
+    L.tc = take(8 * n); L.np = take(8 * n); L.tr = take(8 * n); L.tcl = take(8 * n);
+    L.ts = take(8 * S); L.tn = take(8 * S); L.td = take(8 * S); L.rd = take(8 * S); L.af = take(4 * S);
+    L.disp = take(8); L.live = take(4); L.chain = take(sizeof(Chain)); L.qk = take(8 * n);
+    L.mask = take(n); L.order = take(4 * n);
+    L.shadow = take(4 * n);   // am_replay_io: the steps as copied in (delta write-back)
+    L.total = off;
+    return L;
+}
+
+extern "C" size_t am_replay_workspace_size(const am_ctx* ctx) { return ctx ? rep_layout(ctx).total : 0; }
+
 extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* synth, int64_t quantum_us,
-                                int32_t* positions, int32_t* steps)
+                                int32_t* positions, int32_t* steps, void* workspace, size_t workspace_bytes)
 {
     if (!out || !ctx || !synth || !positions || !steps) return AM_E_ARG;
     if (ctx->d.target <= 0) {
@@ -571,42 +595,49 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
         ctx->err = "am_replay_create: exclusive tiles need the fused per-simulation path and r_p >= 2 v";
         return AM_E_ARG;
     }
+    const RepLayout L = rep_layout(ctx);
+    if (workspace && (workspace_bytes < L.total || ((uintptr_t)workspace & 255))) {
+        ctx->err = "am_replay_create: workspace smaller than am_replay_workspace_size() or not 256-byte aligned";
+        return AM_E_WORKSPACE;
+    }
     am_replay* rp = new (std::nothrow) am_replay();
     if (!rp) return AM_E_ARG;
     rp->ctx = ctx;
     rp->user_stream = ctx->stream;
-    const long long n = std::max(1, ctx->d.n), S = ctx->d.n_sims;
-    size_t off = 0;
-    auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~size_t(255); return o; };
-    size_t o_tc = take(8 * n), o_np = take(8 * n), o_tr = take(8 * n), o_tcl = take(8 * n);
-    size_t o_ts = take(8 * S), o_tn = take(8 * S), o_td = take(8 * S), o_rd = take(8 * S), o_af = take(4 * S);
-    size_t o_disp = take(8), o_live = take(4), o_chain = take(sizeof(Chain)), o_qk = take(8 * n);
-    size_t o_mask = take(n), o_order = take(4 * n);
-    cudaError_t e = cudaMalloc(&rp->mem, off);
-    if (e != cudaSuccess) { delete rp; return rp_err(nullptr, e, "cudaMalloc"); }
+    const long long S = ctx->d.n_sims;
+    const size_t off = L.total;
+    if (workspace) {
+        rp->mem = workspace;
+        rp->mem_owned = false;
+    } else {   // no caller workspace: the replay allocates (and frees) its own
+        cudaError_t e = cudaMalloc(&rp->mem, off);
+        if (e != cudaSuccess) { delete rp; return rp_err(nullptr, e, "cudaMalloc"); }
+        rp->mem_owned = true;
+    }
     char* b = (char*)rp->mem;
     RepDev& r = rp->r;
     r.sy = *synth;
     r.Q = quantum_us;
     r.pos = (int2*)positions;
     r.steps = steps;
-    r.tcommit = (long long*)(b + o_tc);
-    r.newpos = (int2*)(b + o_np);
-    r.traj = (unsigned long long*)(b + o_tr);
-    r.tcl = (long long*)(b + o_tcl);
-    r.t_sim = (long long*)(b + o_ts);
-    r.tnext = (long long*)(b + o_tn);
-    r.tdone = (long long*)(b + o_td);
-    r.rounds = (long long*)(b + o_rd);
-    r.active_flag = (int32_t*)(b + o_af);
-    r.dispatched = (long long*)(b + o_disp);
-    r.liveness = (int32_t*)(b + o_live);
-    r.chain = (Chain*)(b + o_chain);
-    r.qkey = (unsigned long long*)(b + o_qk);
+    r.tcommit = (long long*)(b + L.tc);
+    r.newpos = (int2*)(b + L.np);
+    r.traj = (unsigned long long*)(b + L.tr);
+    r.tcl = (long long*)(b + L.tcl);
+    r.t_sim = (long long*)(b + L.ts);
+    r.tnext = (long long*)(b + L.tn);
+    r.tdone = (long long*)(b + L.td);
+    r.rounds = (long long*)(b + L.rd);
+    r.active_flag = (int32_t*)(b + L.af);
+    r.dispatched = (long long*)(b + L.disp);
+    r.liveness = (int32_t*)(b + L.live);
+    r.chain = (Chain*)(b + L.chain);
+    r.qkey = (unsigned long long*)(b + L.qk);
     r.K = 0;
     r.prio = 1;
-    rp->mask = (uint8_t*)(b + o_mask);
-    rp->order = (int32_t*)(b + o_order);
+    rp->mask = (uint8_t*)(b + L.mask);
+    rp->order = (int32_t*)(b + L.order);
+    rp->shadow = (int32_t*)(b + L.shadow);
     r.order = ctx->path == 1 ? ctx->d.rid : rp->order;
     RK(cudaStreamCreateWithFlags(&rp->stream, cudaStreamNonBlocking));
     RK(cudaMallocHost((void**)&rp->h_buf, 64));
@@ -850,7 +881,6 @@ extern "C" int am_replay_io(am_replay* rp, const int32_t* h_pos_in, const int32_
     void *dpos = nullptr, *dsteps = nullptr;
     const bool delta = h_pos_out == h_pos_in && h_steps_out == h_steps_in && mapped(h_pos_out, &dpos) &&
                        mapped(h_steps_out, &dsteps);
-    if (delta && !rp->shadow) RK(cudaMalloc(&rp->shadow, 4 * std::max<size_t>(n, 1)));
     RK(cudaMemcpyAsync(rp->r.pos, h_pos_in, 8 * n, cudaMemcpyHostToDevice, rp->stream));
     RK(cudaMemcpyAsync(rp->r.steps, h_steps_in, 4 * n, cudaMemcpyHostToDevice, rp->stream));
     if (delta) RK(cudaMemcpyAsync(rp->shadow, rp->r.steps, 4 * n, cudaMemcpyDeviceToDevice, rp->stream));
@@ -946,13 +976,12 @@ extern "C" int am_replay_destroy(am_replay* rp)
     }
     if (rp->stream) cudaStreamDestroy(rp->stream);
     if (rp->h_buf) cudaFreeHost(rp->h_buf);
-    if (rp->shadow) cudaFree(rp->shadow);
     if (rp->copy) {
         cudaStreamSynchronize(rp->copy);
         cudaStreamDestroy(rp->copy);
         cudaEventDestroy(rp->ev_copy);
     }
-    cudaFree(rp->mem);
+    if (rp->mem_owned) cudaFree(rp->mem);
     delete rp;
     return AM_OK;
 }

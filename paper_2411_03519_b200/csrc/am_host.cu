@@ -175,11 +175,19 @@ extern "C" const char* am_profile_name(int32_t id)
 
 extern "C" const char* am_version(void) { return "ametro-b200 0.1 (sm_100a)"; }
 
-extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max,
-                       int32_t n_agents, const am_config* cfg)
+// The context's configuration and its device workspace layout -- a pure function of
+// the arguments (no CUDA call), shared by am_workspace_size and am_init.
+struct Layout {
+    size_t total = 0;
+    size_t ctl, pos0, pos1, st0, st1, ss0, ss1, labels, digest, blkid, tiles_s;
+    size_t key = 0, cnt = 0, cmin = 0, ctab = 0, l1 = 0, l2 = 0, rec = 0, blk = 0, par = 0, bad = 0, rk0 = 0,
+           rk1 = 0, rv0 = 0, rv1 = 0, tc = 0, tr = 0, tsort = 0, gh = 0, gs = 0, edges = 0, ectr = 0, wit = 0,
+           lrs = 0, wq = 0, dirty = 0, agf = 0, rid = 0;
+};
+
+static int plan(am_ctx* x, int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max, int32_t n_agents,
+                const am_config* cfg, Layout& L)
 {
-    if (!out) return set_err(nullptr, AM_E_ARG, "am_init: out is NULL");
-    *out = nullptr;
     if (map_w < 1 || map_h < 1 || map_w > 32768 || map_h > 32768)
         return set_err(nullptr, AM_E_ARG, "am_init: map dims must be in [1, 32768]");
     if (radius_p < 0 || v_max < 0 || n_agents < 0 || n_agents > (1 << 28))
@@ -196,8 +204,6 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         return set_err(nullptr, AM_E_ARG, "am_init: cell must be 0 or a power of two");
     if (c.target_step < 0) return set_err(nullptr, AM_E_ARG, "am_init: negative target_step");
 
-    am_ctx* x = new (std::nothrow) am_ctx();
-    if (!x) return set_err(nullptr, AM_E_ARG, "am_init: out of host memory");
     const long long n = n_agents;
     const int per_sim_max = (int)((n + c.n_sims - 1) / c.n_sims);
     Dev& d = x->d;
@@ -205,12 +211,128 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     d.n_sims = c.n_sims;
     d.map_w = map_w;
     d.map_h = map_h;
-    d.r_p = radius_p;
-    d.v = v_max;
+    // radii at or above kRClamp already cover every distance on a <= 32768^2 map (their
+    // squares stay < 2^31 and sums like r_p + v cannot wrap): clamping changes no result
+    d.r_p = (int32_t)std::min<long long>(radius_p, kRClamp);
+    d.v = (int32_t)std::min<long long>(v_max, kRClamp);
     d.target = c.target_step;
     d.metric = c.metric;
     d.flags = c.flags;
     x->stream = (cudaStream_t)c.stream;
+
+    // path selection
+    bool small = (c.n_sims > 1) || (n <= kSmallMax);
+    if (c.flags & AM_FORCE_BINNED) small = false;
+    if (c.flags & AM_FORCE_SMALL) small = true;
+    if (small && per_sim_max > kSmallMax)
+        return set_err(nullptr, AM_E_ARG, "am_init: fused path needs <= 1024 agents per simulation");
+    if (!small && c.n_sims > 1) return set_err(nullptr, AM_E_ARG, "am_init: the binned path takes one simulation");
+    x->path = small ? 0 : 1;
+    x->small_threads = std::max(32, ((per_sim_max + 31) / 32) * 32);
+
+    // cell size: >= R_c = r_p + v (coupling needs <= 2x2 cells), grown until the Morton
+    // grid has at most max(4N, 4096) cells and at most 4096 cells per side.  The grid is
+    // rectangular (2^gxlog x 2^gylog cells, each side >= 64 cells, mkey): a long thin map
+    // -- e.g. one spatial slab of a wide map -- gets a long thin cell table.
+    long long Rc = (long long)d.r_p + d.v;
+    auto gl = [&](long long extent, int cl) {
+        return ilog2_ceil(std::max(64LL, (extent + (1LL << cl) - 1) >> cl));
+    };
+    int clog;
+    if (c.cell) {
+        clog = ilog2_ceil(c.cell);
+    } else {
+        clog = ilog2_ceil(std::max(1LL, Rc));
+        for (;;) {
+            const long long g = 1LL << (gl(map_w, clog) + gl(map_h, clog));
+            if (g <= std::max(4 * n, 4096LL) || clog >= 15) break;
+            clog++;
+        }
+    }
+    while (std::max(gl(map_w, clog), gl(map_h, clog)) > 12 && clog < 15) clog++;   // <= 4096 cells per side
+    d.gxlog = gl(map_w, clog);
+    d.gylog = gl(map_h, clog);
+    d.mbits = std::min(d.gxlog, d.gylog);
+    d.mxhi = d.gxlog > d.gylog ? 1 : 0;
+    d.clog = clog;
+    d.ncells = 1 << (d.gxlog + d.gylog);
+    x->cell = 1 << clog;
+    d.idbits = std::max(1, ilog2_ceil(std::max(2LL, n)));
+    d.lagcap = (int32_t)(kRClamp / (uint32_t)std::max(1, d.v)) + 1;
+    {
+        int lagbits = c.target_step > 0 ? ilog2_ceil((long long)c.target_step + 1) : 31;
+        int bits = lagbits + d.idbits;
+        x->sort_passes_max = std::min(kMaxSortPasses, std::max(1, (bits + kRadixBits - 1) / kRadixBits));
+    }
+    x->ntiles_sort = (int)blocks(n, kSortTile);
+    x->ntiles_ready = (int)blocks(n, kReadyTile);
+    x->cells_threads = (int)std::min<long long>(kCellsThreads, d.ncells / 16);
+    x->ntiles_cells = (int)(d.ncells / (16LL * x->cells_threads));
+
+    // workspace layout
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    const size_t N = (size_t)std::max(1LL, n);
+    L.ctl = take(sizeof(Ctl));
+    L.pos0 = take(8 * N); L.pos1 = take(8 * N);
+    L.st0 = take(4 * N); L.st1 = take(4 * N);
+    L.ss0 = take(N); L.ss1 = take(N);
+    L.labels = take(4 * N); L.digest = take(8 * N); L.blkid = take(N);
+    L.tiles_s = take(8 * (size_t)c.n_sims);
+    const size_t NC = (size_t)d.ncells;
+    if (x->path == 1) {
+        L.key = take(4 * N);
+        L.cnt = take(4 * NC); L.cmin = take(4 * NC);
+        L.ctab = take(8 * (NC + 1)); L.l1 = take(4 * (NC / 16)); L.l2 = take(4 * (NC / 256));
+        L.rec = take(16 * N); L.blk = take(N);
+        L.par = take(4 * N); L.bad = take(N); L.dirty = take(4 * N); L.agf = take(N);
+        L.rk0 = take(8 * N); L.rk1 = take(8 * N); L.rid = take(4 * N); L.rv0 = take(4 * N); L.rv1 = take(4 * N);
+        L.tc = take(8 * (size_t)x->ntiles_cells); L.tr = take(8 * (size_t)x->ntiles_ready);
+        L.tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * kRadix);
+        L.gh = take(4 * kMaxSortPasses * kRadix); L.gs = take(4 * kMaxSortPasses * kRadix);
+        d.ecap = (int)(3 * N + 4096);
+        // the scan's work queue: stripes = block index mod 64 of k_scatter (one thread per
+        // agent), so a stripe holds at most ceil(blocks / 64) x 256 records
+        const long long nbl = blocks(n, 256);
+        d.wq_cap = (int)(((nbl + kEdgeStripes - 1) / kEdgeStripes) * 256);
+        L.wit = take(4 * N); L.lrs = take(N);
+        L.edges = take(8 * 4 * (size_t)d.ecap); L.ectr = take(4 * kEdgeStripes);
+        L.wq = take(16 * (size_t)kEdgeStripes * d.wq_cap);
+    }
+    L.total = off;
+    return AM_OK;
+}
+
+extern "C" size_t am_workspace_size(int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max,
+                                    int32_t n_agents, const am_config* cfg)
+{
+    am_ctx tmp;
+    Layout L;
+    if (plan(&tmp, map_w, map_h, radius_p, v_max, n_agents, cfg, L) != AM_OK) return 0;
+    return L.total;
+}
+
+extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max,
+                       int32_t n_agents, const am_config* cfg)
+{
+    if (!out) return set_err(nullptr, AM_E_ARG, "am_init: out is NULL");
+    *out = nullptr;
+    am_ctx* x = new (std::nothrow) am_ctx();
+    if (!x) return set_err(nullptr, AM_E_ARG, "am_init: out of host memory");
+    Layout L;
+    {
+        const int rc = plan(x, map_w, map_h, radius_p, v_max, n_agents, cfg, L);
+        if (rc != AM_OK) { delete x; return rc; }
+    }
+    if (cfg && cfg->workspace) {   // caller-owned device workspace (e.g. a torch uint8 tensor)
+        if (cfg->workspace_bytes < L.total || ((uintptr_t)cfg->workspace & 255)) {
+            delete x;
+            return set_err(nullptr, AM_E_WORKSPACE, "am_init: workspace smaller than am_workspace_size() or "
+                                                    "not 256-byte aligned");
+        }
+    }
+    Dev& d = x->d;
+    const long long n = n_agents;
     cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
     if (const char* e = getenv("AM_SORT_CTAS")) x->sort_ctas = std::max(1, atoi(e));   // tuning knob
     if (const char* e = getenv("AM_PDL")) x->pdl = atoi(e) != 0;                      // ablation
@@ -266,96 +388,23 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         cudaGetLastError();
     }
 
-    // path selection
-    bool small = (c.n_sims > 1) || (n <= kSmallMax);
-    if (c.flags & AM_FORCE_BINNED) small = false;
-    if (c.flags & AM_FORCE_SMALL) small = true;
-    if (small && per_sim_max > kSmallMax) {
-        delete x;
-        return set_err(nullptr, AM_E_ARG, "am_init: fused path needs <= 1024 agents per simulation");
-    }
-    if (!small && c.n_sims > 1) {
-        delete x;
-        return set_err(nullptr, AM_E_ARG, "am_init: the binned path takes one simulation");
-    }
-    x->path = small ? 0 : 1;
-    x->small_threads = std::max(32, ((per_sim_max + 31) / 32) * 32);
-
-    // cell size: >= R_c = r_p + v (coupling needs <= 2x2 cells), grown until the Morton
-    // grid has at most max(4N, 4096) cells and at most 4096 cells per side.  The grid is
-    // rectangular (2^gxlog x 2^gylog cells, each side >= 64 cells, mkey): a long thin map
-    // -- e.g. one spatial slab of a wide map -- gets a long thin cell table.
-    long long Rc = (long long)radius_p + v_max;
-    auto gl = [&](long long extent, int cl) {
-        return ilog2_ceil(std::max(64LL, (extent + (1LL << cl) - 1) >> cl));
-    };
-    int clog;
-    if (c.cell) {
-        clog = ilog2_ceil(c.cell);
-    } else {
-        clog = ilog2_ceil(std::max(1LL, Rc));
-        for (;;) {
-            const long long g = 1LL << (gl(map_w, clog) + gl(map_h, clog));
-            if (g <= std::max(4 * n, 4096LL) || clog >= 15) break;
-            clog++;
-        }
-    }
-    while (std::max(gl(map_w, clog), gl(map_h, clog)) > 12 && clog < 15) clog++;   // <= 4096 cells per side
-    d.gxlog = gl(map_w, clog);
-    d.gylog = gl(map_h, clog);
-    d.mbits = std::min(d.gxlog, d.gylog);
-    d.mxhi = d.gxlog > d.gylog ? 1 : 0;
-    d.clog = clog;
-    d.ncells = 1 << (d.gxlog + d.gylog);
-    x->cell = 1 << clog;
-    d.idbits = std::max(1, ilog2_ceil(std::max(2LL, n)));
-    d.lagcap = (int32_t)(kRClamp / (uint32_t)std::max(1, v_max)) + 1;
-    {
-        int lagbits = c.target_step > 0 ? ilog2_ceil((long long)c.target_step + 1) : 31;
-        int bits = lagbits + d.idbits;
-        x->sort_passes_max = std::min(kMaxSortPasses, std::max(1, (bits + kRadixBits - 1) / kRadixBits));
-    }
-    x->ntiles_sort = (int)blocks(n, kSortTile);
-    x->ntiles_ready = (int)blocks(n, kReadyTile);
-    x->cells_threads = (int)std::min<long long>(kCellsThreads, d.ncells / 16);
-    x->ntiles_cells = (int)(d.ncells / (16LL * x->cells_threads));
-
-    // workspace layout
-    size_t off = 0;
-    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
-    const size_t N = (size_t)std::max(1LL, n);
-    size_t o_ctl = take(sizeof(Ctl));
-    size_t o_pos0 = take(8 * N), o_pos1 = take(8 * N);
-    size_t o_st0 = take(4 * N), o_st1 = take(4 * N);
-    size_t o_ss0 = take(N), o_ss1 = take(N);
-    size_t o_labels = take(4 * N), o_digest = take(8 * N), o_blkid = take(N);
-    size_t o_tiles_s = take(8 * (size_t)c.n_sims);
-    size_t o_key = 0, o_cnt = 0, o_cmin = 0, o_ctab = 0, o_l1 = 0, o_l2 = 0, o_rec = 0,
-           o_blk = 0, o_par = 0, o_bad = 0, o_rk0 = 0, o_rk1 = 0, o_rv0 = 0, o_rv1 = 0, o_tc = 0, o_tr = 0,
-           o_tsort = 0, o_gh = 0, o_gs = 0, o_edges = 0, o_ectr = 0, o_wit = 0, o_lrs = 0, o_wq = 0, o_dirty = 0, o_agf = 0, o_rid = 0;
-    const size_t NC = (size_t)d.ncells;
-    if (x->path == 1) {
-        o_key = take(4 * N);
-        o_cnt = take(4 * NC); o_cmin = take(4 * NC);
-        o_ctab = take(8 * (NC + 1)); o_l1 = take(4 * (NC / 16)); o_l2 = take(4 * (NC / 256));
-        o_rec = take(16 * N); o_blk = take(N);
-        o_par = take(4 * N); o_bad = take(N); o_dirty = take(4 * N); o_agf = take(N);
-        o_rk0 = take(8 * N); o_rk1 = take(8 * N); o_rid = take(4 * N); o_rv0 = take(4 * N); o_rv1 = take(4 * N);
-        o_tc = take(8 * (size_t)x->ntiles_cells); o_tr = take(8 * (size_t)x->ntiles_ready);
-        o_tsort = take(8 * (size_t)kMaxSortPasses * x->ntiles_sort * kRadix);
-        o_gh = take(4 * kMaxSortPasses * kRadix); o_gs = take(4 * kMaxSortPasses * kRadix);
-        d.ecap = (int)(3 * N + 4096);
-        // the scan's work queue: stripes = block index mod 64 of k_scatter (one thread per
-        // agent), so a stripe holds at most ceil(blocks / 64) x 256 records
-        const long long nbl = blocks(n, 256);
-        d.wq_cap = (int)(((nbl + kEdgeStripes - 1) / kEdgeStripes) * 256);
-        o_wit = take(4 * N); o_lrs = take(N);
-        o_edges = take(8 * 4 * (size_t)d.ecap); o_ectr = take(4 * kEdgeStripes);
-        o_wq = take(16 * (size_t)kEdgeStripes * d.wq_cap);
-    }
+    const size_t off = L.total;
     x->ws_bytes = off;
-    cudaError_t e = cudaMalloc(&x->ws, off);
-    if (e != cudaSuccess) { delete x; return cuda_err(nullptr, e, "am_init: cudaMalloc"); }
+    cudaError_t e = cudaSuccess;
+    if (cfg && cfg->workspace) {
+        x->ws = cfg->workspace;
+        x->ws_owned = false;
+    } else {   // no caller workspace: the context allocates (and frees) its own
+        e = cudaMalloc(&x->ws, off);
+        if (e != cudaSuccess) { delete x; return cuda_err(nullptr, e, "am_init: cudaMalloc"); }
+        x->ws_owned = true;
+    }
+    auto fail = [&](cudaError_t err, const char* where) {
+        if (x->ws_owned) cudaFree(x->ws);
+        if (x->h_ctl) cudaFreeHost(x->h_ctl);
+        delete x;
+        return cuda_err(nullptr, err, where);
+    };
     if (x->path == 1) {
         e = cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming);
@@ -364,32 +413,34 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&x->side2, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_dig, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ev_mask, cudaEventDisableTiming);
-        if (e != cudaSuccess) { cudaFree(x->ws); delete x; return cuda_err(nullptr, e, "am_init: side stream"); }
+        if (e != cudaSuccess) return fail(e, "am_init: side stream");
     }
     e = cudaMallocHost((void**)&x->h_ctl, sizeof(Ctl));
-    if (e != cudaSuccess) { cudaFree(x->ws); delete x; return cuda_err(nullptr, e, "am_init: cudaMallocHost"); }
+    if (e != cudaSuccess) { x->h_ctl = nullptr; return fail(e, "am_init: cudaMallocHost"); }
     char* b = (char*)x->ws;
-    d.ctl = (Ctl*)(b + o_ctl);
-    d.pos[0] = (int2*)(b + o_pos0); d.pos[1] = (int2*)(b + o_pos1);
-    d.step[0] = (int32_t*)(b + o_st0); d.step[1] = (int32_t*)(b + o_st1);
-    d.status[0] = (uint8_t*)(b + o_ss0); d.status[1] = (uint8_t*)(b + o_ss1);
-    d.labels = (int32_t*)(b + o_labels);
-    d.blkid = (uint8_t*)(b + o_blkid);
-    d.digest = (unsigned long long*)(b + o_digest);
-    d.tiles_s = (unsigned long long*)(b + o_tiles_s);
+    d.ctl = (Ctl*)(b + L.ctl);
+    d.pos[0] = (int2*)(b + L.pos0); d.pos[1] = (int2*)(b + L.pos1);
+    d.step[0] = (int32_t*)(b + L.st0); d.step[1] = (int32_t*)(b + L.st1);
+    d.status[0] = (uint8_t*)(b + L.ss0); d.status[1] = (uint8_t*)(b + L.ss1);
+    d.labels = (int32_t*)(b + L.labels);
+    d.blkid = (uint8_t*)(b + L.blkid);
+    d.digest = (unsigned long long*)(b + L.digest);
+    d.tiles_s = (unsigned long long*)(b + L.tiles_s);
+    const size_t NC = (size_t)d.ncells;
+    const size_t N = (size_t)std::max(1LL, n);
     if (x->path == 1) {
-        d.key = (uint32_t*)(b + o_key);
-        d.cnt = (uint32_t*)(b + o_cnt); d.cmin = (int32_t*)(b + o_cmin);
-        d.ctab = (int2*)(b + o_ctab); d.lmin1 = (int32_t*)(b + o_l1); d.lmin2 = (int32_t*)(b + o_l2);
-        d.rec = (int4*)(b + o_rec); d.v8 = (uint8_t*)(b + o_blk);
-        d.parent = (uint32_t*)(b + o_par); d.bad = (uint8_t*)(b + o_bad); d.dirty = (uint32_t*)(b + o_dirty); d.agflag = (uint8_t*)(b + o_agf);
-        d.rid = (int32_t*)(b + o_rid); d.rkey[0] = (unsigned long long*)(b + o_rk0); d.rkey[1] = (unsigned long long*)(b + o_rk1);
-        d.rval[0] = (uint32_t*)(b + o_rv0); d.rval[1] = (uint32_t*)(b + o_rv1);
-        d.tiles_c = (unsigned long long*)(b + o_tc); d.tiles_r = (unsigned long long*)(b + o_tr);
-        d.tiles_sort = (unsigned long long*)(b + o_tsort);
-        d.ghist = (uint32_t*)(b + o_gh); d.gstart = (uint32_t*)(b + o_gs);
-        d.cedges = (uint2*)(b + o_edges); d.nedges = d.cedges + 2 * (size_t)d.ecap; d.wq_ctr = (uint32_t*)(b + o_ectr); d.wq = (int4*)(b + o_wq);
-        d.witness = (uint32_t*)(b + o_wit); d.chg8 = (uint8_t*)(b + o_lrs);
+        d.key = (uint32_t*)(b + L.key);
+        d.cnt = (uint32_t*)(b + L.cnt); d.cmin = (int32_t*)(b + L.cmin);
+        d.ctab = (int2*)(b + L.ctab); d.lmin1 = (int32_t*)(b + L.l1); d.lmin2 = (int32_t*)(b + L.l2);
+        d.rec = (int4*)(b + L.rec); d.v8 = (uint8_t*)(b + L.blk);
+        d.parent = (uint32_t*)(b + L.par); d.bad = (uint8_t*)(b + L.bad); d.dirty = (uint32_t*)(b + L.dirty); d.agflag = (uint8_t*)(b + L.agf);
+        d.rid = (int32_t*)(b + L.rid); d.rkey[0] = (unsigned long long*)(b + L.rk0); d.rkey[1] = (unsigned long long*)(b + L.rk1);
+        d.rval[0] = (uint32_t*)(b + L.rv0); d.rval[1] = (uint32_t*)(b + L.rv1);
+        d.tiles_c = (unsigned long long*)(b + L.tc); d.tiles_r = (unsigned long long*)(b + L.tr);
+        d.tiles_sort = (unsigned long long*)(b + L.tsort);
+        d.ghist = (uint32_t*)(b + L.gh); d.gstart = (uint32_t*)(b + L.gs);
+        d.cedges = (uint2*)(b + L.edges); d.nedges = d.cedges + 2 * (size_t)d.ecap; d.wq_ctr = (uint32_t*)(b + L.ectr); d.wq = (int4*)(b + L.wq);
+        d.witness = (uint32_t*)(b + L.wit); d.chg8 = (uint8_t*)(b + L.lrs);
     }
     // initial contents: everything zero except the min-step table
     e = cudaMemsetAsync(x->ws, 0, off, x->stream);
@@ -403,10 +454,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     h.full = 1;
     if (e == cudaSuccess) e = cudaMemcpyAsync(d.ctl, &h, sizeof h, cudaMemcpyHostToDevice, x->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
-    if (e != cudaSuccess) {
-        cudaFree(x->ws); cudaFreeHost(x->h_ctl); delete x;
-        return cuda_err(nullptr, e, "am_init: workspace init");
-    }
+    if (e != cudaSuccess) return fail(e, "am_init: workspace init");
     x->stats.path = x->path;
     x->stats.cell = x->cell;
     *out = x;
@@ -565,10 +613,15 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             CK(c, cudaEventRecord(c->ev_fork, s));
             CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
             {
+                // the profiling events of k_efilter go on its stream; the context's stream is
+                // restored before any error is returned
                 cudaStream_t ms = c->stream;
                 c->stream = c->side;
-                LAUNCH(K_NEAR, CK(c, launch_k(false, c->side, k_efilter, std::min(blocks(2LL * d.ecap, 256), pers), 256, 0, d)));
+                am_prof_begin(c, K_NEAR);
+                const cudaError_t le = launch_k(false, c->side, k_efilter, std::min(blocks(2LL * d.ecap, 256), pers), 256, 0, d);
+                am_prof_end(c, K_NEAR);
                 c->stream = ms;
+                if (le != cudaSuccess) return cuda_err(c, le, "k_efilter launch");
             }
             CK(c, cudaEventRecord(c->ev_efil, c->side));
             {
@@ -644,8 +697,12 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
 #undef LAUNCH
     CK(c, cudaGetLastError());
     c->have_round = true;
+    // the caller's stream waits for the side-stream priority sort (an event wait, no host
+    // synchronisation): `order` is complete for any later work on the context's stream.
+    // The replay driver's own round (defer_join) joins it after dispatch and commit
+    // instead, which do not read `order`, so the sort overlaps them.
+    if (!c->defer_join) am_join_side(c);
     if (async) return AM_OK;
-    am_join_side(c);
     int rc = am_sync(c);
     *n_ready = rc == AM_OK ? c->h_ctl->n_ready : 0;
     return rc;
@@ -714,6 +771,8 @@ extern "C" int am_reset(am_ctx* c)
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
     c->first = true;
     c->have_round = false;
+    c->bin_pending = false;   // a replay capture that failed between update and round
+    c->full_hint = true;
     return AM_OK;
 }
 
@@ -739,7 +798,7 @@ extern "C" int am_destroy(am_ctx* c)
         cudaEventDestroy(c->ev_dig);
         cudaEventDestroy(c->ev_mask);
     }
-    cudaFree(c->ws);
+    if (c->ws_owned) cudaFree(c->ws);
     cudaFreeHost(c->h_ctl);
     delete c;
     return AM_OK;

@@ -231,6 +231,7 @@ struct am_ctx {
     bool mask_event = false;
     bool dig_pending = false;
     bool bin_pending = false;        // am_update_binned ran the round's k_bin already
+    bool defer_join = false;         // am_ready inside a replay round: the driver joins the sort
     bool pdl = true;                 // programmatic dependent launch between round kernels
     int csort_ctas = 0;              // cluster size of the one-kernel priority sort (0 = onesweep)
     int csort_cap = 0;               // dynamic shared memory bytes per CTA of k_csort
@@ -242,6 +243,7 @@ struct am_ctx {
     bool have_round = false;
     void* ws = nullptr;
     size_t ws_bytes = 0;
+    bool ws_owned = false;           // allocated by am_init (no caller workspace in am_config)
     am_round_stats stats{};
     std::string err;
 };

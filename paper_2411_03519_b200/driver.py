@@ -51,8 +51,12 @@ class Replay:
         torch.cuda.synchronize(dev)
         h = C.c_void_p()
         L = self.tracker.L
+        # the replay's device workspace from PyTorch's allocator (two-phase idiom)
+        nbytes = int(L.am_replay_workspace_size(self.tracker.ctx))
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+        ws = (self.workspace.data_ptr() + 255) & ~255
         check(L.am_replay_create(C.byref(h), self.tracker.ctx, C.byref(sy), int(quantum_us),
-                                 self.pos.data_ptr(), self.steps.data_ptr()), self.tracker.ctx)
+                                 self.pos.data_ptr(), self.steps.data_ptr(), ws, nbytes), self.tracker.ctx)
         self.h = h
         self.L = L
         self.n_sims = n_sims

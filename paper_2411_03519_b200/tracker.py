@@ -62,7 +62,17 @@ class Tracker:
             self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
             cfg = _lib.Config(int(target), int(n_sims), int(cell),
                               _lib.METRIC_LINF if metric == "linf" else _lib.METRIC_L2, flags,
-                              self.stream.cuda_stream)
+                              self.stream.cuda_stream, None, 0)
+            # two-phase workspace: the library sizes it, PyTorch's allocator provides it
+            nbytes = int(self.L.am_workspace_size(self.map_w, self.map_h, self.r_p, self.v, self.n,
+                                                  C.byref(cfg)))
+            if nbytes == 0:
+                check(self.L.am_init(C.byref(C.c_void_p()), self.map_w, self.map_h, self.r_p, self.v,
+                                     self.n, C.byref(cfg)), None)   # reports the argument error
+            self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+            base = self.workspace.data_ptr()
+            cfg.workspace = (base + 255) & ~255
+            cfg.workspace_bytes = nbytes
             h = C.c_void_p()
             rc = self.L.am_init(C.byref(h), self.map_w, self.map_h, self.r_p, self.v, self.n, C.byref(cfg))
             check(rc, None)

@@ -57,12 +57,33 @@ def test_version_and_init_errors_without_gpu(lib):
     assert lib.am_init(C.byref(h), 0, 10, 4, 1, 10, None) == _lib.E_ARG
     assert b"map dims" in lib.am_last_error(None)
     assert lib.am_init(C.byref(h), 10, 10, -1, 1, 10, None) == _lib.E_ARG
-    cfg = _lib.Config(0, 3, 0, 0, 0, None)
+    cfg = _lib.Config(0, 3, 0, 0, 0, None, None, 0)
     assert lib.am_init(C.byref(h), 10, 10, 4, 1, 2, C.byref(cfg)) == _lib.E_ARG   # n_sims > n
-    cfg = _lib.Config(0, 1, 6, 0, 0, None)
+    assert lib.am_workspace_size(10, 10, 4, 1, 2, C.byref(cfg)) == 0
+    cfg = _lib.Config(0, 1, 6, 0, 0, None, None, 0)
     assert lib.am_init(C.byref(h), 10, 10, 4, 1, 2, C.byref(cfg)) == _lib.E_ARG   # cell not pow2
     assert lib.am_update(None, None, None) == _lib.E_ARG
     assert lib.am_destroy(None) == _lib.OK
+
+
+def test_workspace_size_two_phase_idiom(lib):
+    """am_workspace_size (no CUDA call): the caller-owned workspace of am_config.  It
+    grows with the agent count, the binned path needs the cell table, and a workspace
+    that is too small or misaligned is refused before any device work."""
+    cfg = _lib.Config(0, 1, 0, 0, _lib.VALIDATE, None, None, 0)
+    small = lib.am_workspace_size(140, 100, 4, 1, 25, C.byref(cfg))
+    big = lib.am_workspace_size(16384, 16384, 4, 1, 1_000_000, C.byref(cfg))
+    c4 = lib.am_workspace_size(4096, 4096, 4, 1, 100_000, C.byref(cfg))
+    assert 0 < small < c4 < big
+    assert big >= 1_000_000 * (8 + 8 + 4 + 4 + 16)     # double-buffered state + sorted records at least
+    assert lib.am_workspace_size(140, 100, 4, 1, 25, None) == small   # defaults = AM_VALIDATE
+    h = C.c_void_p()
+    cfg.workspace = 256
+    cfg.workspace_bytes = small - 1
+    assert lib.am_init(C.byref(h), 140, 100, 4, 1, 25, C.byref(cfg)) == _lib.E_WORKSPACE
+    cfg.workspace = 257
+    cfg.workspace_bytes = small
+    assert lib.am_init(C.byref(h), 140, 100, 4, 1, 25, C.byref(cfg)) == _lib.E_WORKSPACE
 
 
 def test_package_does_not_import_the_oracle():

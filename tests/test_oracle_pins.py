@@ -340,3 +340,43 @@ def test_lockstep_grid_radius_edge_cases(r_p, v, metric):
     b = O.lockstep_grid(p, sy, x, y, 12, threads=3)
     for k in ("x", "y", "traj", "T_sync"):
         np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_replay_mt_equals_replay():
+    """Concurrent simulations of a batch (C3 shape) give the sequential replay's results."""
+    w = amgen.config("C3", steps=80, n=24)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, n_sims=w.n_sims)
+    a = O.replay(p, sy, w.x, w.y)
+    b = O.replay_mt(p, sy, w.x, w.y, threads=5)
+    for k in ("x", "y", "traj", "T_ooo", "rounds"):
+        np.testing.assert_array_equal(a[k], b[k])
+    a = O.replay(p, sy, w.x, w.y, capacity=3, priority=False)
+    b = O.replay_mt(p, sy, w.x, w.y, capacity=3, priority=False, threads=3)
+    for k in ("traj", "T_ooo", "rounds"):
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_replay_sims_logged_equals_batched_log():
+    """One simulation replayed alone logs exactly its part of the batched replay's log."""
+    w = amgen.config("C3", steps=40, n=5)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, n_sims=w.n_sims)
+    full = O.replay(p, sy, w.x, w.y, log_rounds=10**5, log_entries=10**5)
+    one = O.replay_sims_logged(p, sy, w.x, w.y, [1, 3])
+    k = 0
+    per = {b: ([], [], []) for b in range(5)}
+    for b, nr in zip(full["log_sim"], full["log_nready"]):
+        per[b][0].append(nr)
+        per[b][1].extend(full["log_id"][k:k + nr])
+        per[b][2].extend(full["log_label"][k:k + nr])
+        k += nr
+    for b in (1, 3):
+        np.testing.assert_array_equal(one[b]["log_nready"], per[b][0])
+        np.testing.assert_array_equal(one[b]["log_id"], per[b][1])
+        np.testing.assert_array_equal(one[b]["log_label"], per[b][2])
+        assert one[b]["T_ooo"] == full["T_ooo"][b] and one[b]["rounds"] == full["rounds"][b]
+        lo, hi = b * 125 // 5, (b + 1) * 125 // 5
+        np.testing.assert_array_equal(one[b]["traj"], full["traj"][lo:hi])
