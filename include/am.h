@@ -116,6 +116,10 @@ typedef struct {
     int32_t n_items;       /* binned: 4x4-cell blocks the far test walked in the pyramid   */
     int32_t n_edges;       /* binned: coupling edges of this round (carried + new)        */
     int32_t n_passes;      /* binned: radix passes the priority order needed              */
+    int32_t rebuilt;       /* binned: 1 if the round rebuilt the cell binning, 0 if it kept  */
+                           /* the loose cells of the last rebuild (records updated in place) */
+    int32_t drift;         /* binned: tiles any agent lies outside its record's cell (D)     */
+    int32_t n_rebuilds;    /* binned: cell-binning rebuilds since am_init                    */
 } am_round_stats;
 
 /* Device workspace bytes am_init needs for these arguments (the same validation as

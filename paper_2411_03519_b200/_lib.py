@@ -42,7 +42,8 @@ class RoundStats(C.Structure):
                 ("watermark", C.c_int32), ("max_step", C.c_int32), ("n_clusters", C.c_int32),
                 ("path", C.c_int32), ("cell", C.c_int32), ("n_work", C.c_int32),
                 ("n_far", C.c_int32), ("n_items", C.c_int32), ("n_edges", C.c_int32),
-                ("n_passes", C.c_int32)]
+                ("n_passes", C.c_int32), ("rebuilt", C.c_int32), ("drift", C.c_int32),
+                ("n_rebuilds", C.c_int32)]
 
 
 class SlabGeom(C.Structure):

@@ -182,7 +182,7 @@ struct Layout {
     size_t ctl, pos0, pos1, st0, st1, ss0, ss1, labels, digest, blkid, tiles_s;
     size_t key = 0, cnt = 0, cmin = 0, ctab = 0, l1 = 0, l2 = 0, rec = 0, blk = 0, par = 0, bad = 0, rk0 = 0,
            rk1 = 0, rv0 = 0, rv1 = 0, tc = 0, tr = 0, tsort = 0, gh = 0, gs = 0, edges = 0, ectr = 0, wit = 0,
-           lrs = 0, wq = 0, dirty = 0, agf = 0, rid = 0;
+           lrs = 0, wq = 0, dirty = 0, agf = 0, rid = 0, slot = 0;
 };
 
 static int plan(am_ctx* x, int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max, int32_t n_agents,
@@ -295,7 +295,7 @@ static int plan(am_ctx* x, int32_t map_w, int32_t map_h, int32_t radius_p, int32
         // agent), so a stripe holds at most ceil(blocks / 64) x 256 records
         const long long nbl = blocks(n, 256);
         d.wq_cap = (int)(((nbl + kEdgeStripes - 1) / kEdgeStripes) * 256);
-        L.wit = take(4 * N); L.lrs = take(N);
+        L.wit = take(4 * N); L.lrs = take(N); L.slot = take(4 * N);
         L.edges = take(8 * 4 * (size_t)d.ecap); L.ectr = take(4 * kEdgeStripes);
         L.wq = take(16 * (size_t)kEdgeStripes * d.wq_cap);
     }
@@ -441,11 +441,18 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.ghist = (uint32_t*)(b + L.gh); d.gstart = (uint32_t*)(b + L.gs);
         d.cedges = (uint2*)(b + L.edges); d.nedges = d.cedges + 2 * (size_t)d.ecap; d.wq_ctr = (uint32_t*)(b + L.ectr); d.wq = (int4*)(b + L.wq);
         d.witness = (uint32_t*)(b + L.wit); d.chg8 = (uint8_t*)(b + L.lrs);
+        d.slot = (uint32_t*)(b + L.slot);
+        // loose-cell rebuild policy (tuning knobs)
+        d.rebuild_d = AM_REBUILD_D;
+        d.rebuild_k = AM_REBUILD_K;
+        if (const char* q = getenv("AM_REBUILD_D")) d.rebuild_d = atoi(q);
+        if (const char* q = getenv("AM_REBUILD_K")) d.rebuild_k = atoi(q);
     }
     // initial contents: everything zero except the min-step table
     e = cudaMemsetAsync(x->ws, 0, off, x->stream);
     if (e == cudaSuccess && x->path == 1) e = cudaMemsetAsync(d.cmin, 0x7F, 4 * NC, x->stream);  // ~INT_MAX
     if (e == cudaSuccess && x->path == 1) e = cudaMemsetAsync(d.witness, 0xFF, 4 * N, x->stream);
+    if (e == cudaSuccess && x->path == 1) e = cudaMemsetAsync(d.slot, 0xFF, 4 * N, x->stream);
     Ctl h{};
     h.acc_W = INT_MAX;
     h.acc_S = INT_MIN;
@@ -532,6 +539,9 @@ static void fill_stats(am_ctx* c)
     c->stats.n_items = h.n_items;
     c->stats.n_edges = h.n_edges;
     c->stats.n_passes = h.npasses;
+    c->stats.rebuilt = h.rebuild;
+    c->stats.drift = h.D;
+    c->stats.n_rebuilds = h.n_rebuilds;
 }
 
 // the main stream waits for the perception digests of the last round (side2)
@@ -598,7 +608,9 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         LAUNCH(K_SMALL, CK(c, launch_k(c->pdl, s, k_small, d.n_sims, c->small_threads, 0, d, mask, order)));
     } else {
         const unsigned nb = blocks(d.n, 256);
-        if (!c->bin_pending) LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, nb, 256, 0, d)));
+        // k_bin / k_cells return at once on loose-cell rounds (the device decides: a rebuild
+        // is due after a full recompute, a drift beyond rebuild_d, or rebuild_k rounds)
+        LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, nb, 256, 0, d)));
         c->bin_pending = false;
         LAUNCH(K_CELLS, CK(c, launch_k(c->pdl, s, k_cells, c->ntiles_cells, c->cells_threads, 0, d)));
         LAUNCH(K_SCATTER, CK(c, launch_k(c->pdl, s, k_scatter, nb, 256, 0, d)));

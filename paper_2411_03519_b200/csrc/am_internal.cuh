@@ -68,7 +68,16 @@ constexpr int kIngestItems = AM_INGEST_ITEMS;   // agents per thread in k_ingest
 constexpr int kEdgeStripes = 64;          // striped queues (one atomic counter per stripe)
 constexpr int kEdgeStage = 128;           // coupling edges staged per warp before appending
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
-constexpr int kRecChanged = 0x10;         // record status byte: agent's step changed since last round
+// record word w = status (bits 0-1) | change tag << 8: the 24-bit round epoch in which
+// the agent's step last changed ("changed this round" <=> tag == epoch & kTagMask)
+constexpr int kTagShift = 8;
+constexpr uint32_t kTagMask = 0xFFFFFFu;
+#ifndef AM_REBUILD_D
+#define AM_REBUILD_D 4      // rebuild the cell binning once an agent drifted this far out of its cell
+#endif
+#ifndef AM_REBUILD_K
+#define AM_REBUILD_K 32     // ... or after this many incremental rounds (cell minima go stale)
+#endif
 constexpr uint32_t kRClamp = 46340u;      // >= every distance on a 32768^2 map; R^2 < 2^31
 
 enum : int32_t { ERR_BOUNDS = 1, ERR_PROTOCOL = 2, ERR_VELOCITY = 4 };
@@ -98,6 +107,11 @@ struct Ctl {
     uint32_t ccnt[2];      // edges in each carried list (k_efilter output)
     uint32_t ncnt[2];      // edges in each new list (k_scan_hw output)
     int32_t  n_work, n_far, n_items, n_edges;   // this round's scan work (stats)
+    // incremental binning ("loose cells"): between rebuilds the records stay in their
+    // cells and committed agents update their record in place; D = max over agents of
+    // the L-inf distance from the agent to its record's cell box (every cell-pruning
+    // box is widened by D), acc_D its per-update accumulator
+    int32_t  D, acc_D, since_rebuild, rebuild, n_rebuilds;
     uint32_t scan_next;    // dynamic work distribution of k_scan_hw (AM_SCAN_DYN)
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
@@ -131,7 +145,10 @@ struct Dev {
     int2* ctab;            // [ncells+1] {start, min step}
     int32_t* lmin1;        // [ncells/16]  min step per 4x4-cell block
     int32_t* lmin2;        // [ncells/256] min step per 16x16-cell block
-    int4* rec;             // [n] sorted records {x | y<<16, step, id, status}
+    int4* rec;             // [n] records sorted by cell at the last rebuild {x | y<<16, step, id, w};
+                           // positions / steps are kept current (in place) between rebuilds
+    uint32_t* slot;        // [n] per id: index of its record (kSentinel: not binned, DONE)
+    int32_t rebuild_d, rebuild_k;   // rebuild policy (drift tiles, incremental rounds)
     uint8_t* v8;           // [n] per id: blocking verdict (0 no, 1 yes, 2 far phase pending)
     uint32_t* witness;     // [n] per id: the blocker found last time it was computed
     uint8_t* chg8;         // [n] per id: step changed since the last round (set by am_update)
@@ -300,6 +317,16 @@ __device__ __forceinline__ uint32_t mkey(const Dev& d, uint32_t cx, uint32_t cy,
     return part1by1(cx & lo) | (part1by1(cy & lo) << 1) | (hi << (2 * m));
 }
 
+__device__ __forceinline__ void mkey_decode(const Dev& d, uint32_t key, int& cx, int& cy)
+{
+    const int m = d.mbits;
+    const uint32_t lo = m >= 16 ? 0xFFFFFFFFu : ((1u << (2 * m)) - 1u);
+    const int xl = (int)part_compact(key & lo), yl = (int)part_compact((key & lo) >> 1);
+    const int hi = (int)(key >> (2 * m));
+    cx = d.mxhi ? (hi << m) | xl : xl;
+    cy = d.mxhi ? yl : (hi << m) | yl;
+}
+
 // blocking radius clamped so that R^2 fits in 31 bits; exact because the
 // clamp exceeds every distance on a <= 32768^2 map.
 __device__ __forceinline__ uint32_t rb_radius(long long lag, int v, int r_p)
@@ -336,6 +363,20 @@ __device__ __forceinline__ bool box_within(int x, int y, int x0, int y0, int x1,
     int dy = y < y0 ? y0 - y : (y > y1 ? y - y1 : 0);
     return within(dx, dy, R, metric);
 }
+
+// cell (cx, cy) of edge 2^sh, its tile box widened by D on every side (loose cells:
+// every agent recorded in the cell lies inside the widened box), within R of (x, y)
+__device__ __forceinline__ bool cell_within(int x, int y, int cx, int cy, int sh, int D, uint32_t R, int metric)
+{
+    return box_within(x, y, (cx << sh) - D, (cy << sh) - D, ((cx + 1) << sh) - 1 + D, ((cy + 1) << sh) - 1 + D, R,
+                      metric);
+}
+
+// record word: changed this round (tag == the round's epoch)
+__device__ __forceinline__ bool rec_changed(int w, uint32_t ep) { return (((uint32_t)w >> kTagShift) & kTagMask) == ep; }
+
+// inverse of mkey at level 0: the cell coordinates of a key
+__device__ __forceinline__ void mkey_decode(const Dev& d, uint32_t key, int& cx, int& cy);
 
 __device__ __forceinline__ bool box_dist_within(int ax0, int ay0, int ax1, int ay1, int bx0, int by0,
                                                 int bx1, int by1, uint32_t R, int metric)

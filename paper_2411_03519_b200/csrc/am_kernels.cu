@@ -31,8 +31,9 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
     pdl_begin();
     Ctl* ctl = d.ctl;
     const uint32_t c = ctl->cur;
-    int err = 0, act = 0, run = 0, smin = INT_MAX, smax = INT_MIN;
+    int err = 0, act = 0, run = 0, smin = INT_MAX, smax = INT_MIN, dmax = 0;
     const bool validate = (d.flags & AM_VALIDATE) != 0;
+    const uint32_t tag = (ctl->epoch + 1u) & kTagMask;   // the epoch of the round this update feeds
     // every load of the thread's items is issued before any compute or store, so the
     // thread keeps kIngestItems independent load chains in flight (memory-level
     // parallelism; the state buffers and the caller's arrays may not alias)
@@ -101,38 +102,37 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
             smax = max(smax, s[k]);
         }
         run += st == ST_RUNNING;
-        if (bin) {
-            // fused k_bin (replay rounds): cell key, slot, cell min step of the new state.
-            // A rejected update leaves the round's ready set empty and forces a full
-            // recompute next round (k_ingest_done), so bins of a rejected state are harmless.
-            // (no returning atomic: k_scatter takes each record's slot by counting the
-            // cell back down, which also leaves the counts zero for the next round)
-            uint32_t key = kSentinel;
-            if (st != ST_DONE) {
-                key = mkey(d, (uint32_t)p[k].x >> d.clog, (uint32_t)p[k].y >> d.clog, 0);
-                atomicAdd(d.cnt + key, 1u);
-                atomicMin(d.cmin + key, s[k]);
+        if (mode == 0 && s[k] != os[k] && d.slot) {
+            // loose cells: a committed agent keeps its record (cell of the last rebuild) and
+            // updates it in place; its distance outside that cell's box bounds the drift D
+            const uint32_t r = d.slot[i];
+            if (r != kSentinel) {
+                d.rec[r] = make_int4(p[k].x | (p[k].y << 16), s[k], i, (int)st | (int)(tag << kTagShift));
+                int cx, cy;
+                mkey_decode(d, d.key[i], cx, cy);
+                const int x0 = cx << d.clog, y0 = cy << d.clog;
+                const int x1 = x0 + (1 << d.clog) - 1, y1 = y0 + (1 << d.clog) - 1;
+                dmax = max(dmax, max(max(x0 - p[k].x, p[k].x - x1), max(y0 - p[k].y, p[k].y - y1)));
             }
-            d.key[i] = key;
-            d.bad[i] = 0;
-            d.blkid[i] = 0;
         }
     }
     // block reduction, then one atomic per quantity per block
-    __shared__ int r_err[8], r_min[8], r_max[8], r_act[8], r_run[8];
+    __shared__ int r_err[8], r_min[8], r_max[8], r_act[8], r_run[8], r_d[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     err = (int)__reduce_or_sync(0xFFFFFFFFu, (unsigned)err);
     smin = __reduce_min_sync(0xFFFFFFFFu, smin);
     smax = __reduce_max_sync(0xFFFFFFFFu, smax);
     act = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)act);
     run = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)run);
-    if (lane == 0) { r_err[w] = err; r_min[w] = smin; r_max[w] = smax; r_act[w] = act; r_run[w] = run; }
+    dmax = __reduce_max_sync(0xFFFFFFFFu, dmax);
+    if (lane == 0) { r_err[w] = err; r_min[w] = smin; r_max[w] = smax; r_act[w] = act; r_run[w] = run; r_d[w] = dmax; }
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int q = 1; q < 8; q++) {
             err |= r_err[q]; smin = min(smin, r_min[q]); smax = max(smax, r_max[q]);
-            act += r_act[q]; run += r_run[q];
+            act += r_act[q]; run += r_run[q]; dmax = max(dmax, r_d[q]);
         }
+        if (dmax > 0) atomicMax(&ctl->acc_D, dmax);
         if (err) atomicOr(&ctl->err_new, err);
         if (act) {
             atomicMin(&ctl->acc_W, smin);
@@ -154,7 +154,10 @@ __global__ void k_ingest_done(Dev d, int mode, int bin)
     if (threadIdx.x != 0) return;
     Ctl* ctl = d.ctl;
     const int e = ctl->err_new;
-    if (e != 0 && bin) ctl->full_next = 1;   // the fused bins and incremental state saw a rejected update
+    // a rejected update may have touched records and incremental state: recompute all
+    if (e != 0) ctl->full_next = 1;
+    ctl->D = max(ctl->D, ctl->acc_D);   // (a rejected update is followed by a full rebuild)
+    ctl->acc_D = 0;
     if (e == 0) {
         if (mode != 0) ctl->full = 1;
         ctl->cur ^= 1u;
@@ -199,6 +202,7 @@ __device__ __forceinline__ void block_append(T* q, int cap, uint32_t* ctr, int s
 __global__ void __launch_bounds__(256) k_bin(Dev d)
 {
     pdl_begin();
+    if (!d.ctl->rebuild) return;   // loose cells: the records of the last rebuild serve this round
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t c = d.ctl->cur;
     if (i < d.n) {
@@ -213,8 +217,6 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
             atomicMin(d.cmin + key, s);
         }
         d.key[i] = key;
-        d.bad[i] = 0;
-        d.blkid[i] = 0;
     }
 }
 
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(kCellsThreads) k_cells(Dev d)
 {
     pdl_begin();
     Ctl* ctl = d.ctl;
+    if (!ctl->rebuild) return;        // loose cells: the cell table of the last rebuild serves
     const int kW = blockDim.x >> 5;   // tile = blockDim.x threads x 16 cells (host: <= kCellsThreads)
     __shared__ uint32_t wsum[kCellsThreads / 32];
     __shared__ uint32_t tile_excl;
@@ -297,10 +300,11 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
     __shared__ uint32_t s_w[9];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t c = d.ctl->cur;
+    const bool rebuild = d.ctl->rebuild != 0;
+    const uint32_t ep = d.ctl->epoch & kTagMask;
     bool work = false;
     int4 q = make_int4(0, 0, 0, 0);
     if (i < d.n) {
-        const uint32_t key = d.key[i];
         const int2 p = d.pos[c][i];
         const int s = d.step[c][i];
         const uint8_t st = d.status[c][i];
@@ -308,13 +312,21 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
         const int lab = d.labels[i];
         const uint32_t w = d.witness[i];
         const bool full = round_full(d);
-        if (key == kSentinel) {   // DONE: counts as changed for the carried edges (k_efilter)
+        d.bad[i] = 0;     // per-root flags of this round (k_finalize)
+        d.blkid[i] = 0;
+        if (st == ST_DONE) {   // DONE: counts as changed for the carried edges (k_efilter)
             d.agflag[i] = 1;
+            if (rebuild) d.slot[i] = kSentinel;
         } else {
             const bool chg = full || ch;
-            // slot: the cell's start + its count taken back down (returns the counts to 0)
-            const uint32_t r = (uint32_t)d.ctab[key].x + (atomicSub(d.cnt + key, 1u) - 1u);
-            d.rec[r] = make_int4(p.x | (p.y << 16), s, i, st | (chg ? kRecChanged : 0));
+            if (rebuild) {
+                // slot: the cell's start + its count taken back down (returns the counts to 0)
+                const uint32_t key = d.key[i];
+                const uint32_t r = (uint32_t)d.ctab[key].x + (atomicSub(d.cnt + key, 1u) - 1u);
+                const uint32_t tag = chg ? ep : ((ep + 0x800000u) & kTagMask);   // never this epoch
+                d.rec[r] = make_int4(p.x | (p.y << 16), s, i, (int)st | (int)(tag << kTagShift));
+                d.slot[i] = r;
+            }
             // union-find forest of this round: an agent whose last-round cluster has no
             // changed member keeps that cluster (all its coupling edges are unchanged: it
             // is still connected, and it can only grow through an edge of a changed
@@ -664,8 +676,8 @@ __device__ __forceinline__ void hw_flush_stats(const Dev& d, const HwStats& hs, 
 // nothing inside can block A); cells within R_c of A are tested by the near phase.  The
 // records of the surviving cells are flattened over the lanes and tested 16 at a time.
 // Returns a blocker's id or kSentinel.
-__device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as, int W, int l, int h, unsigned hm,
-                                           int ox_l, int oy_l, HwStats& hs)
+__device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as, int W, int D, int l, int h,
+                                           unsigned hm, int ox_l, int oy_l, HwStats& hs)
 {
     const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2x = (1 << d.gxlog) >> 4, G2y = (1 << d.gylog) >> 4;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
@@ -676,8 +688,8 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
     uint32_t& nb1 = hs.nb1;
     uint32_t& nitems = hs.nitems;
     const int R = (int)rb32(as - W, d.lagcap, d.v, d.r_p);
-    const int bx0 = max(0, (ax - R) >> l2), bx1 = min(G2x - 1, (ax + R) >> l2);
-    const int by0 = max(0, (ay - R) >> l2), by1 = min(G2y - 1, (ay + R) >> l2);
+    const int bx0 = max(0, (ax - R - D) >> l2), bx1 = min(G2x - 1, (ax + R + D) >> l2);
+    const int by0 = max(0, (ay - R - D) >> l2), by1 = min(G2y - 1, (ay + R + D) >> l2);
     const int nbx = bx1 - bx0 + 1, nb = nbx * (by1 - by0 + 1);
     uint32_t wit = kSentinel;
     nb2 += l == 0 ? (uint32_t)nb : 0u;
@@ -688,8 +700,7 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
         bool ok2 = false;
         if (j < nb) {
             const int m2 = __ldg(d.lmin2 + mkey(d, bx, by, 4));
-            ok2 = m2 < as && box_within(ax, ay, bx << l2, by << l2, ((bx + 1) << l2) - 1, ((by + 1) << l2) - 1,
-                                        rb32(as - m2, d.lagcap, d.v, d.r_p), d.metric);
+            ok2 = m2 < as && cell_within(ax, ay, bx, by, l2, D, rb32(as - m2, d.lagcap, d.v, d.r_p), d.metric);
         }
         unsigned mask2 = (__ballot_sync(hm, ok2) >> (16 * h)) & 0xFFFFu;
         while (mask2 && wit == kSentinel) {
@@ -701,9 +712,7 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
             // level 1: lane l tests child l (4x4 cells)
             const int qx = bxj * 4 + ox_l, qy = byj * 4 + oy_l;
             const int m1 = __ldg(d.lmin1 + k2 * 16 + l);
-            const bool ok1 = m1 < as && box_within(ax, ay, qx << l1, qy << l1, ((qx + 1) << l1) - 1,
-                                                   ((qy + 1) << l1) - 1, rb32(as - m1, d.lagcap, d.v, d.r_p),
-                                                   d.metric);
+            const bool ok1 = m1 < as && cell_within(ax, ay, qx, qy, l1, D, rb32(as - m1, d.lagcap, d.v, d.r_p), d.metric);
             unsigned mask1 = (__ballot_sync(hm, ok1) >> (16 * h)) & 0xFFFFu;
             while (mask1 && wit == kSentinel) {
                 const int ii = __ffs(mask1) - 1;
@@ -716,10 +725,9 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
                 int nx = __shfl_down_sync(hm, e.x, 1, 16);
                 if (l == 15) nx = d.ctab[(size_t)k1g * 16 + 16].x;
                 const int cx = qxi * 4 + ox_l, cy = qyi * 4 + oy_l;
-                const int X0 = cx << cl, Y0 = cy << cl, X1 = ((cx + 1) << cl) - 1, Y1 = ((cy + 1) << cl) - 1;
-                const bool okc = nx > e.x && e.y < as && !box_within(ax, ay, X0, Y0, X1, Y1, Rc, d.metric) &&
-                                 box_within(ax, ay, X0, Y0, X1, Y1, rb32(as - e.y, d.lagcap, d.v, d.r_p),
-                                            d.metric);
+                // cells within R_c of A (widened boxes) were tested by the near phase
+                const bool okc = nx > e.x && e.y < as && !cell_within(ax, ay, cx, cy, cl, D, Rc, d.metric) &&
+                                 cell_within(ax, ay, cx, cy, cl, D, rb32(as - e.y, d.lagcap, d.v, d.r_p), d.metric);
                 const int cnt = okc ? nx - e.x : 0;
                 ncells += nx > e.x ? 1u : 0u;
                 // flatten the candidate records over the 16 lanes
@@ -784,8 +792,8 @@ constexpr int kDirectFull = AM_DIRECT_FULL; // the same for rounds the host know
 // test the records of the cells in `list[0..nl)` (near cells first: nn of them) against
 // A; returns (in nblk/wit) the first blocker; stages coupling edges for a changed A
 __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const int2* list, int nl, int nn, int ax,
-                                           int ay, int as, uint32_t aid, bool chg, bool idle, int l, int h,
-                                           unsigned hm, bool& nblk, uint32_t& wit, HwStats& hs)
+                                           int ay, int as, uint32_t aid, bool chg, bool idle, uint32_t ep, int l,
+                                           int h, unsigned hm, bool& nblk, uint32_t& wit, HwStats& hs)
 {
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
     const uint32_t Rc2 = Rc * Rc;
@@ -831,7 +839,7 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
                     const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
                     if (B.y == as) {
                         // B's record carries its changed bit (k_scatter)
-                        if (chg && bnear && within2(dx, dy, Rc2, Rc, d.metric) && (!(B.w & kRecChanged) || aid < bid))
+                        if (chg && bnear && within2(dx, dy, Rc2, Rc, d.metric) && (!rec_changed(B.w, ep) || aid < bid))
                             stage_edge(d, sm, min(aid, bid), max(aid, bid));
                     } else if (idle && !nblk && B.y < as) {
                         const uint32_t R =
@@ -868,6 +876,8 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
     const int nq = kRec ? d.ctab[d.ncells].x : s_pref[kEdgeStripes];
     if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->n_work = nq;
     const int W = d.ctl->W;
+    const int D = d.ctl->D;                      // loose-cell drift: every cell box widened by D
+    const uint32_t ep = d.ctl->epoch & kTagMask;
     const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
     int ox_l, oy_l;
@@ -899,18 +909,18 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
             }
             const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
             const uint32_t aid = kRec ? (uint32_t)A.z : ((uint32_t)A.z & 0x7FFFFFFFu);
-            const bool chg = kRec ? (A.w & kRecChanged) != 0 : ((uint32_t)A.z >> 31) != 0;
+            const bool chg = kRec ? rec_changed(A.w, ep) : ((uint32_t)A.z >> 31) != 0;
             const bool idle = (A.w & 3) == ST_IDLE;
             const bool far = idle && as > W && !(d.flags & AM_DBG_SKIP_FAR);
             nfar += (far && l == 0) ? 1u : 0u;
             // query box: far radius when the far test is due and the box is small enough
             const int Rf = far ? (int)rb32(as - W, d.lagcap, d.v, d.r_p) : (int)Rc;
-            int cx0 = max(0, (ax - Rf) >> cl), cx1 = min(Gx - 1, (ax + Rf) >> cl);
-            int cy0 = max(0, (ay - Rf) >> cl), cy1 = min(Gy - 1, (ay + Rf) >> cl);
+            int cx0 = max(0, (ax - Rf - D) >> cl), cx1 = min(Gx - 1, (ax + Rf + D) >> cl);
+            int cy0 = max(0, (ay - Rf - D) >> cl), cy1 = min(Gy - 1, (ay + Rf + D) >> cl);
             const bool direct = (cx1 - cx0 + 1) * (cy1 - cy0 + 1) <= KD;
             if (!direct) {   // near cells only; the far test walks the pyramid below
-                cx0 = max(0, (ax - (int)Rc) >> cl); cx1 = min(Gx - 1, (ax + (int)Rc) >> cl);
-                cy0 = max(0, (ay - (int)Rc) >> cl); cy1 = min(Gy - 1, (ay + (int)Rc) >> cl);
+                cx0 = max(0, (ax - (int)Rc - D) >> cl); cx1 = min(Gx - 1, (ax + (int)Rc + D) >> cl);
+                cy0 = max(0, (ay - (int)Rc - D) >> cl); cy1 = min(Gy - 1, (ay + (int)Rc + D) >> cl);
             }
             const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
             // row k / ncx of cell k of the box: a multiply-high by ceil(2^32 / ncx), exact
@@ -952,15 +962,13 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
                             if (pass == 0) {
                                 const int ky = krow(k);
                                 const int cx = cx0 + (k - ky * ncx), cy = cy0 + ky;
-                                const bool isnear = box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1,
-                                                               ((cy + 1) << cl) - 1, Rc, d.metric);
+                                const bool isnear = cell_within(ax, ay, cx, cy, cl, D, Rc, d.metric);
                                 nearbits |= isnear ? 1u << j : 0u;
                                 ok = isnear && (chg ? mn <= as : (idle && mn < as));
                             } else if (!((nearbits >> j) & 1u) && far && direct && mn < as) {
                                 const int ky = krow(k);
                                 const int cx = cx0 + (k - ky * ncx), cy = cy0 + ky;
-                                ok = box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1,
-                                                rb32(as - mn, d.lagcap, d.v, d.r_p), d.metric);
+                                ok = cell_within(ax, ay, cx, cy, cl, D, rb32(as - mn, d.lagcap, d.v, d.r_p), d.metric);
                             }
                         }
                         const unsigned bm = (__ballot_sync(hm, ok) >> (16 * h)) & 0xFFFFu;
@@ -971,12 +979,12 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
                 }
                 hs.ncells += l == 0 ? (uint32_t)nl : 0u;
                 __syncwarp(hm);
-                hw_records(d, sm, list, nl, nn, ax, ay, as, aid, chg, idle, l, h, hm, nblk, wit, hs);
+                hw_records(d, sm, list, nl, nn, ax, ay, as, aid, chg, idle, ep, l, h, hm, nblk, wit, hs);
                 __syncwarp(hm);   // the list is rewritten by the next chunk / agent
             }
             if (idle) {
                 if (far && !direct && !nblk) {
-                    wit = hw_far(d, ax, ay, as, W, l, h, hm, ox_l, oy_l, hs);
+                    wit = hw_far(d, ax, ay, as, W, D, l, h, hm, ox_l, oy_l, hs);
                     nblk = wit != kSentinel;
                 }
                 if (l == 0) {
@@ -1071,13 +1079,14 @@ __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict
     const unsigned hm = 0xFFFFu << (16 * h);
     const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
     const uint32_t Rp = (uint32_t)d.r_p, Rp2 = Rp * Rp;
+    const int D = d.ctl->D;   // loose cells (widened boxes)
     const int hw0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 4, nhw = (gridDim.x * blockDim.x) >> 4;
     for (int k = hw0; k < nr; k += nhw) {   // half-warp uniform
         const uint32_t aid = (uint32_t)ids[k];
         const int2 P = d.pos[c][aid];
         const int ax = P.x, ay = P.y, as = d.step[c][aid];
-        const int cx0 = max(0, (ax - (int)Rp) >> cl), cx1 = min(Gx - 1, (ax + (int)Rp) >> cl);
-        const int cy0 = max(0, (ay - (int)Rp) >> cl), cy1 = min(Gy - 1, (ay + (int)Rp) >> cl);
+        const int cx0 = max(0, (ax - (int)Rp - D) >> cl), cx1 = min(Gx - 1, (ax + (int)Rp + D) >> cl);
+        const int cy0 = max(0, (ay - (int)Rp - D) >> cl), cy1 = min(Gy - 1, (ay + (int)Rp + D) >> cl);
         const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
         unsigned long long dig = 0;
         for (int cb = 0; cb < ncell; cb += 16) {
@@ -1085,7 +1094,7 @@ __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict
             int st0 = 0, cnt = 0;
             if (q < ncell) {
                 const int cx = cx0 + q % ncx, cy = cy0 + q / ncx;
-                if (box_within(ax, ay, cx << cl, cy << cl, ((cx + 1) << cl) - 1, ((cy + 1) << cl) - 1, Rp, d.metric)) {
+                if (cell_within(ax, ay, cx, cy, cl, D, Rp, d.metric)) {
                     const uint32_t key = mkey(d, cx, cy, 0);
                     const int2 e = d.ctab[key];
                     if (e.y <= as) {
@@ -1506,6 +1515,18 @@ __device__ void round_begin(const Dev& d)
     ctl->cells.ticket = 0;
     ctl->full |= ctl->full_next;
     ctl->full_next = 0;
+    if (d.slot) {   // binned path: rebuild the cell binning, or keep the loose cells
+        const bool rb = ctl->full != 0 || ctl->D > d.rebuild_d || ctl->since_rebuild >= d.rebuild_k ||
+                        !(d.flags & AM_VALIDATE);
+        ctl->rebuild = rb ? 1 : 0;
+        if (rb) {
+            ctl->D = 0;
+            ctl->since_rebuild = 0;
+            ctl->n_rebuilds += 1;
+        } else {
+            ctl->since_rebuild += 1;
+        }
+    }
     if (ctl->epoch > 1) ctl->ecur ^= 1u;   // last round's edge lists become current
     ctl->ccnt[ctl->ecur ^ 1u] = 0;
     ctl->ncnt[ctl->ecur ^ 1u] = 0;

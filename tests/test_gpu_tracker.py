@@ -358,3 +358,46 @@ def test_interleaved_pair_clusters_closed_form(pairs, sort, wide, monkeypatch):
     np.testing.assert_array_equal(g["label"], label)
     np.testing.assert_array_equal(g["order"], np.lexsort((ids, label, s)))
     tr.close()
+
+
+@pytest.mark.parametrize("knobs", [{}, {"AM_REBUILD_D": "1000", "AM_REBUILD_K": "1000"},
+                                   {"AM_REBUILD_D": "0", "AM_REBUILD_K": "0"}])
+def test_loose_cells_every_round_vs_oracle(knobs, monkeypatch):
+    """Incremental binning ("loose cells"): between rebuilds the
+    records keep their cells, committed agents update theirs in place and every cell
+    box is widened by the drift D.  A C4-shaped replay (5000 agents at C4 density,
+    hotspots, busy hour, 50 ms quantum) compared with the brute-force oracle round by
+    round for 300 rounds: default policy, never rebuilding (D grows to tens of tiles:
+    the widening carries everything), and rebuilding every round."""
+    import amgen
+    from paper_2411_03519_b200 import Replay
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    w = amgen.config("C4", n=5000)
+    lm = amgen.latency_model(w.profile)
+    rep = Replay.from_workload(w, lm, force="binned")
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, w.steps)
+    rebuilt, loose, dmax = 0, 0, 0
+    for r in range(300):
+        x = rep.pos[:, 0].cpu().numpy().copy()
+        y = rep.pos[:, 1].cpu().numpy().copy()
+        s = rep.steps.cpu().numpy().copy()
+        mask_t, order_t, labels_t = rep.step()
+        st = rep.tracker.status().cpu().numpy()
+        mask = mask_t.cpu().numpy()
+        st[mask == 1] = O.IDLE
+        ref = O.round_mt(p, x, y, s, st.copy(), peek=True)
+        np.testing.assert_array_equal(mask, ref["mask"], err_msg=f"round {r}")
+        np.testing.assert_array_equal(order_t.cpu().numpy(), ref["order"], err_msg=f"round {r}")
+        np.testing.assert_array_equal(labels_t.cpu().numpy(), ref["label"], err_msg=f"round {r}")
+        stt = rep.tracker.stats()
+        rebuilt += stt["rebuilt"]
+        loose += 1 - stt["rebuilt"]
+        dmax = max(dmax, stt["drift"])
+    if knobs.get("AM_REBUILD_K") == "0":
+        assert loose == 0
+    else:
+        assert loose > 200 and rebuilt >= 1
+    if knobs.get("AM_REBUILD_K") == "1000":
+        assert dmax > 8, dmax          # the drift really grew past the cell edge
+    rep.close()
