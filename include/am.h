@@ -152,6 +152,17 @@ int am_update(am_ctx* ctx, const int32_t* positions, const int32_t* sim_steps);
 int am_set_state(am_ctx* ctx, const int32_t* positions, const int32_t* sim_steps,
                  const uint8_t* status);
 
+/* Replica update (the spatial-slab window of am_slab.h): the full state including
+ * statuses (uint8 [n_agents]; AM_DONE also marks an absent slot), diffed against the
+ * current one without commit validation.  An agent whose position or step changed, that
+ * arrived (absent -> present) or departed (present -> absent) is re-examined by the next
+ * round; every other verdict, coupling edge and cluster is reused (the incremental
+ * round).  Status changes IDLE <-> RUNNING alone are not changes.
+ * Stream-ordered (no synchronisation); errors (bounds, status values) surface at the
+ * next synchronising call.  The first call after am_init / am_reset acts as am_set_state. */
+int am_update_replica(am_ctx* ctx, const int32_t* positions, const int32_t* sim_steps,
+                      const uint8_t* status);
+
 /* One scheduling round (geo_clustering + ready filter + priority order, Alg. 3 l.8-9).
  * mask:  uint8 [n_agents]   1 iff the agent is ready (IDLE and its cluster unblocked).
  * order: int32 [n_agents]   capacity; the first *n_ready entries are the ready agents

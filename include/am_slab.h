@@ -1,99 +1,164 @@
 /*
- * am_slab.h -- spatial-slab decomposition of the tracker round across GPUs
- * (the paper runs one controller, and scales workers
- * "beyond a single machine", P:194 -- the slab exchange is this repo's design).
+ * am_slab.h -- the tracker and the trace-replay driver split across GPUs by spatial
+ * slabs (the paper runs one controller process, and
+ * scales its workers "beyond a single machine", P:194 -- the slab exchange is this
+ * repo's design).  Implemented by libametro.so (am_slab.cu); driven round by round by
+ * paper_2411_03519_b200/slabs.py, which only marshals pointers and runs the three
+ * collectives through torch.distributed (NCCL over NVLink) or an in-process loopback.
  *
- * The map's rows are split into G horizontal slabs; slab k owns rows
- * [k*map_h/G, (k+1)*map_h/G) and every agent whose y lies there.  One distributed
- * round (driven by paper_2411_03519_b200/slabs.py over an exchange: NCCL via
- * torch.distributed, or an in-process loopback for virtual slabs):
- *   1. am_slab_watermark on owned agents; all-reduce min of {W, -S};
- *   2. am_slab_halo: owned agent B is sent to every slab within R_b(S - s_B) rows
- *      (P:406 with the global max step: covers every agent B can block or couple
- *      with, since R_b(0) = r_p + v = R_c); all-to-all of the records;
- *   3. a local tracker round (am_set_state + am_ready, AM_PEEK) over owned agents
- *      (sorted by global id) followed by the received ghosts; am_clusters /
- *      am_blocked;  am_slab_links emits, for every boundary agent (a ghost here, or
- *      owned and sent elsewhere), a link {gid, gid of its local cluster label}, and
- *      for every local cluster with a boundary member whose OWNED members include a
- *      RUNNING or blocked agent, a bad record {gid of the label};  all-gather;
- *   4. am_slab_merge (identical on every rank): union-find over all links in a dense
- *      global-id forest (roots = minimum id), bad flags OR-ed per merged root; final
- *      outputs for the owned agents: global label (min id of the global cluster,
- *      P:139, Q10), ready mask (IDLE and cluster not bad) and a priority
- *      key ((step - W), label, id) (Q9) for the ready ones.
- * Every coupling edge is seen on the owner of one endpoint (the other is within
- * R_c <= the halo radius), every blocker of an owned agent is present as owned or
- * ghost, and every agent is owned once, so the merged result equals the
- * single-GPU round bit for bit (tests/test_gpu_slabs.py).
+ * PARTITION.  The map's rows are split into G horizontal slabs; slab k owns the rows
+ * [k*H/G, (k+1)*H/G) and every agent whose y lies there (ownership follows the agent).
+ * Rank k keeps a WINDOW: every agent whose y lies within `halo` rows of its slab, in
+ * stable slots (a global-id -> slot map; departures free a slot, arrivals take one).
+ * Owned agents carry their real status; the other window agents ("ghosts") are
+ * tracked as RUNNING (their blocking verdicts are their owner's business; DONE ones as
+ * DONE).  With halo >= R_b(S - W) + v (P:406 at the global step spread, plus one move)
+ * every agent that can block or couple with an owned agent (R_c = R_b(0)) is in
+ * the window, and an agent entering the window cannot affect an owned verdict, so the
+ * window's tracker runs the INCREMENTAL round (am_update_replica: only changed agents
+ * are re-examined).
  *
- * All arrays are DEVICE pointers owned by the caller; counts are device int32.
- * Work is enqueued on `stream`.  Returns AM_OK or AM_E_ARG / AM_E_CUDA.
+ * ONE DISTRIBUTED ROUND (Alg. 3 controller + workers, replay mode P:228):
+ *   am_slab_round_local   replica update + tracker round (PEEK) on the window; per local
+ *                         cluster: min global id, OR of (owned member RUNNING or
+ *                         blocked), max duration of the owned IDLE members; records for
+ *                         every cluster that touches the boundary (a ghost, or an owned
+ *                         agent inside another rank's window): links {gid, cluster min
+ *                         gid} and cluster records {min gid, bad, max duration};
+ *     -> all-gather of the records (fixed capacity per rank, device counts)
+ *   am_slab_merge         identical on every rank: union-find over the link records in a
+ *                         global-id forest (roots = min id, Q10), bad OR-ed and durations
+ *                         max-ed per root; for the owned agents the global cluster label,
+ *                         the ready bit (IDLE and cluster not bad, P:162 / P:184), dispatch
+ *                         of the ready ones (completion time t + the cluster's max
+ *                         duration, the move from the perception digest -- all perceived
+ *                         agents are in the window), the priority order of the rank's
+ *                         ready agents by (step, label, id) (Q9; the global order is
+ *                         the merge of the ranks' orders), and this rank's next event and
+ *                         activity;
+ *     -> all-reduce MIN of {next event, W, -S, no agent active}
+ *   am_slab_commit        the common clock advances to the global next event (rounded up
+ *                         to the quantum); owned agents whose cluster completed commit their
+ *                         move (step + 1, trajectory hash); every commit inside another
+ *                         rank's window (old or new position) becomes a delta record for it;
+ *     -> all-to-all of the delta records (fixed capacity per peer, device counts)
+ *   am_slab_apply         the received deltas update the window: moved agents, arrivals
+ *                         (new slots), departures (freed slots); ownership changes with y.
+ * The merged result equals the single-GPU round bit for bit (tests/test_gpu_slabs.py),
+ * and the replay equals the single-GPU replay and the oracle's.
+ *
+ * All arrays are DEVICE pointers; every call is stream-ordered on the slab's stream and
+ * none synchronises the host.  Capacity overflows and a halo narrower than the step
+ * spread needs are reported through am_slab_flags (checked by the caller every few
+ * rounds; the spread grows by at most one step per round, so a check every K rounds
+ * with K v of margin keeps every round exact).  Errors: AM_E_ARG, AM_E_WORKSPACE,
+ * AM_E_CUDA.
  */
 #ifndef AM_SLAB_H_
 #define AM_SLAB_H_
 
+#include <stddef.h>
 #include <stdint.h>
 #include "am.h"
+#include "am_driver.h"
 
 #ifdef __cplusplus
 extern "C" {
 #endif
 
 typedef struct {
-    int32_t map_w, map_h;     /* map (tiles)                                          */
-    int32_t r_p, v_max;       /* radius_p, max_vel                            */
-    int32_t metric;           /* AM_METRIC_L2 / AM_METRIC_LINF                        */
-    int32_t n_slabs;          /* G >= 1                                               */
-    int32_t my_slab;          /* this rank's slab                                     */
-    int32_t n_total;          /* agents over all slabs (global ids are 0..n_total-1)  */
+    int32_t map_w, map_h;     /* map (tiles)                                                 */
+    int32_t r_p, v_max;       /* radius_p, max_vel                                   */
+    int32_t metric;           /* AM_METRIC_L2 / AM_METRIC_LINF                               */
+    int32_t n_slabs;          /* G >= 1                                                      */
+    int32_t my_slab;          /* this rank's slab                                            */
+    int32_t n_total;          /* agents over all slabs (global ids 0..n_total-1, < 2^28)     */
+    int32_t target_step;      /* agents reaching it become DONE (> 0)                        */
+    int32_t halo;             /* window rows beyond the slab on each side (>= r_p + 2 v)     */
+    int32_t cap_window;       /* window slots                                                */
+    int32_t cap_peer;         /* delta records per peer per round                            */
+    int32_t cap_merge;        /* link records and cluster records (each) per rank per round, even */
+    int32_t check_rounds;     /* K: the caller checks am_slab_flags at least every K rounds  */
 } am_slab_geom;
 
-/* out[0] = min step over owned non-DONE agents (INT32_MAX if none),
- * out[1] = -(max step) (INT32_MAX if none): ready for an all-reduce MIN. */
-int am_slab_watermark(int32_t n, const int32_t* steps, const uint8_t* status, int32_t* out,
-                      void* stream);
+typedef struct am_slab am_slab;
 
-/* Halo records.  ws: device int32[2] = global {W, -S} after the all-reduce.
- * send: int32 [n_slabs][cap][4] records {gid, x | y<<16, step, status};
- * counts: int32 [n_slabs] (zeroed by the call); sent: uint8 [n] (1 = sent anywhere).
- * Records beyond cap are dropped and counts[j] > cap reports it (caller retries). */
-int am_slab_halo(const am_slab_geom* g, int32_t n, const int32_t* gid, const int32_t* pos,
-                 const int32_t* steps, const uint8_t* status, const int32_t* ws, int32_t cap,
-                 int32_t* send, int32_t* counts, uint8_t* sent, void* stream);
+/* flags (am_slab_flags) */
+#define AM_SLAB_OVF_WINDOW  0x1   /* no free window slot for an arrival                     */
+#define AM_SLAB_OVF_PEER    0x2   /* more delta records for a peer than cap_peer            */
+#define AM_SLAB_OVF_MERGE   0x4   /* more link / cluster records than cap_merge             */
+#define AM_SLAB_HALO        0x8   /* R_b(S - W) + (K + 1) v > halo: re-window before K rounds */
+#define AM_SLAB_LIVENESS    0x10  /* agents not DONE but nothing running                    */
+#define AM_SLAB_LAG         0x20  /* the step spread exceeds the priority key's lag field    */
 
-/* The local tracker's input arrays (capacity cap >= n + m): slots [0, n) the owned
- * agents (gid/pos int32[n][2]/steps/status), slots [n, n + m) the received halo
- * records ghosts int32 [m][4] {gid, x | y<<16, step, status}, the rest DONE padding;
- * every y translated by -y0 (the slab's window).  Outputs lpos int32 [cap][2], lsteps
- * int32 [cap], lstatus uint8 [cap], lgid int32 [cap]. */
-int am_slab_assemble(int32_t n, const int32_t* gid, const int32_t* pos, const int32_t* steps,
-                     const uint8_t* status, int32_t m, const int32_t* ghosts, int32_t cap, int32_t y0,
-                     int32_t* lpos, int32_t* lsteps, uint8_t* lstatus, int32_t* lgid, void* stream);
+/* Exchange buffers (int32 words; fixed capacity, counts inside, so a collective moves
+ * them without any host synchronisation):
+ *   merge buffer of one rank, AM_SLAB_MERGE_WORDS(cap_merge) words (cap_merge even):
+ *     [0] link count, [1] cluster count, [2..3] 0, then cap_merge links {gid, cluster min
+ *     gid}, then cap_merge cluster records {min gid, bad, max duration lo, hi};
+ *   delta block for one peer, AM_SLAB_DELTA_WORDS(cap_peer) words:
+ *     [0] record count, [1..5] 0, then cap_peer records {gid, x, y, step, traj lo, traj hi};
+ *   stats: int64 [4] {next event, W, -S, no agent active} (all-reduce MIN). */
+#define AM_SLAB_MERGE_WORDS(cap) (4 + 6 * (int64_t)(cap))
+#define AM_SLAB_DELTA_WORDS(cap) (6 + 6 * (int64_t)(cap))
 
-/* Merge records of the local round over n_local agents (owned first, then ghosts).
- * labels/blocked: am_clusters / am_blocked output (local indices); sent: from
- * am_slab_halo (owned part).  links: int32 [cap][2]; bads: int32 [cap];
- * n_links, n_bads: device int32 (zeroed by the call); badlocal: uint8 [n_local]
- * scratch that receives, per local root, "an owned member is RUNNING or blocked";
- * bnd: uint8 [n_local] scratch. */
-int am_slab_links(int32_t n_local, int32_t n_owned, const int32_t* gid, const int32_t* labels,
-                  const uint8_t* status, const uint8_t* blocked, const uint8_t* sent,
-                  int32_t cap, int32_t* links, int32_t* n_links, int32_t* bads, int32_t* n_bads,
-                  uint8_t* badlocal, uint8_t* bnd, void* stream);
+/* Device workspace bytes of a slab (window arrays, its tracker's workspace, the global-id
+ * map and merge forest, exchange buffers). */
+size_t am_slab_workspace_size(const am_slab_geom* g);
 
-/* Merge and final outputs for the n_owned owned agents.
- * links [n_links_all][2], bads [n_bads_all]: every rank's records concatenated
- * (host counts).  forest: uint32 [n_total] that must hold the identity (parent[x] =
- * x) and badm/touched: uint8 [n_total] zero on entry; all three are restored on exit.
- * ws: global {W, -S}.  Outputs: out_label int32 [n_owned] (-1 DONE), out_mask uint8
- * [n_owned], out_key int64 [n_owned] = ((step-W) << 42) | (label << 21) | gid for
- * ready agents (n_total <= 2^21), INT64_MAX otherwise. */
-int am_slab_merge(const am_slab_geom* g, int32_t n_owned, const int32_t* gid, const int32_t* steps,
-                  const uint8_t* status, const int32_t* labels, const uint8_t* badlocal,
-                  const int32_t* links, int32_t n_links_all, const int32_t* bads, int32_t n_bads_all,
-                  const int32_t* ws, uint32_t* forest, uint8_t* badm, uint8_t* touched,
-                  int32_t* out_label, uint8_t* out_mask, int64_t* out_key, void* stream);
+/* Create rank g->my_slab's slab.  synth: the synthetic policy / latency model
+ * (am_driver.h), quantum_us: the event quantum.  workspace: >= am_slab_workspace_size
+ * bytes, 256-byte aligned, caller-owned (NULL: the slab allocates its own).  stream:
+ * cudaStream_t of every call. */
+int am_slab_create(am_slab** out, const am_slab_geom* g, const am_synth* synth, int64_t quantum_us,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* (Re)load the window: m agents (global ids, positions int32 [m][2] in GLOBAL map
+ * coordinates, steps, statuses -- real ones for owned agents --, trajectory hashes,
+ * completion times and moves of owned RUNNING agents), clock t.  Device arrays.  The
+ * next round recomputes the window from scratch. */
+int am_slab_load(am_slab* s, int32_t m, const int32_t* gid, const int32_t* pos, const int32_t* steps,
+                 const uint8_t* status, const uint64_t* traj, const int64_t* tcommit, const int32_t* newpos,
+                 int64_t t);
+
+/* Step 1: the window's tracker round; this rank's merge buffer (mbuf). */
+int am_slab_round_local(am_slab* s, int32_t* mbuf);
+
+/* Step 2: merge the G ranks' all-gathered merge buffers (mbufs, G consecutive buffers),
+ * dispatch this rank's ready agents, write their global ids in priority order to
+ * order_out (int32, capacity cap_window) and their count to n_order (device int32), and
+ * this rank's stats (int64 [4]). */
+int am_slab_merge(am_slab* s, const int32_t* mbufs, int32_t* order_out, int32_t* n_order, int64_t* stats);
+
+/* Step 3: commit at the global next event (stats_global: the all-reduced MIN of the
+ * ranks' stats) and pack the deltas: dsend = G delta blocks (block j for rank j; this
+ * rank's own block stays empty). */
+int am_slab_commit(am_slab* s, const int64_t* stats_global, int32_t* dsend);
+
+/* Step 4: apply the received delta blocks (drecv: block r from rank r). */
+int am_slab_apply(am_slab* s, const int32_t* drecv);
+
+/* Per window slot, after the last merge (device pointers owned by the slab): the global
+ * id (-1 free), the global cluster label (-1 for DONE agents and ghosts), the ready bit
+ * (owned agents). */
+int am_slab_outputs(am_slab* s, const int32_t** slot_gid, const int32_t** slot_label, const uint8_t** slot_ready);
+
+/* The window state (device pointers owned by the slab): positions int32 [L][2] (global
+ * coordinates), steps, statuses (owned: real; ghosts: RUNNING / DONE), owned flags,
+ * trajectory hashes; and device counters int64 [4]: {clock t, time of the last commit
+ * that finished an agent, agent-steps dispatched by this rank, rounds}. */
+int am_slab_state(am_slab* s, const int32_t** pos, const int32_t** steps, const uint8_t** status,
+                  const uint64_t** traj, const int64_t** tcommit, const int32_t** newpos, const int64_t** counters);
+
+/* Sticky flags (AM_SLAB_*) and the window occupancy; synchronises the slab's stream and
+ * clears the flags. */
+int am_slab_flags(am_slab* s, int32_t* flags, int32_t* window_used);
+
+/* The slab's tracker context (statistics, profiling) and its stream. */
+am_ctx* am_slab_tracker(am_slab* s);
+void* am_slab_stream(am_slab* s);
+
+int am_slab_destroy(am_slab* s);
 
 #ifdef __cplusplus
 }

@@ -49,7 +49,9 @@ class RoundStats(C.Structure):
 class SlabGeom(C.Structure):
     _fields_ = [("map_w", C.c_int32), ("map_h", C.c_int32), ("r_p", C.c_int32), ("v_max", C.c_int32),
                 ("metric", C.c_int32), ("n_slabs", C.c_int32), ("my_slab", C.c_int32),
-                ("n_total", C.c_int32)]
+                ("n_total", C.c_int32), ("target_step", C.c_int32), ("halo", C.c_int32),
+                ("cap_window", C.c_int32), ("cap_peer", C.c_int32), ("cap_merge", C.c_int32),
+                ("check_rounds", C.c_int32)]
 
 
 class Synth(C.Structure):
@@ -66,6 +68,7 @@ SIGNATURES = {
     "am_workspace_size": (C.c_size_t, [_i32, _i32, _i32, _i32, _i32, C.POINTER(Config)]),
     "am_update": (C.c_int, [_vp, _vp, _vp]),
     "am_set_state": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "am_update_replica": (C.c_int, [_vp, _vp, _vp, _vp]),
     "am_ready": (C.c_int, [_vp, _vp, _vp, C.POINTER(_i32)]),
     "am_clusters": (C.c_int, [_vp, _vp]),
     "am_status": (C.c_int, [_vp, _vp]),
@@ -93,13 +96,21 @@ SIGNATURES = {
     "am_replay_dispatched": (C.c_int, [_vp, C.POINTER(_i64)]),
     "am_replay_destroy": (C.c_int, [_vp]),
     "am_replay_stream": (_vp, [_vp]),
-    "am_slab_watermark": (C.c_int, [_i32, _vp, _vp, _vp, _vp]),
-    "am_slab_halo": (C.c_int, [C.POINTER(SlabGeom), _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp]),
     "am_replay_set_capacity": (C.c_int, [_vp, C.c_int64, _i32]),
-    "am_slab_assemble": (C.c_int, [_i32, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
-    "am_slab_links": (C.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "am_slab_merge": (C.c_int, [C.POINTER(SlabGeom), _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i32,
-                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "am_slab_workspace_size": (C.c_size_t, [C.POINTER(SlabGeom)]),
+    "am_slab_create": (C.c_int, [C.POINTER(_vp), C.POINTER(SlabGeom), C.POINTER(Synth), _i64, _vp, C.c_size_t,
+                                 _vp]),
+    "am_slab_load": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64]),
+    "am_slab_round_local": (C.c_int, [_vp, _vp]),
+    "am_slab_merge": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "am_slab_commit": (C.c_int, [_vp, _vp, _vp]),
+    "am_slab_apply": (C.c_int, [_vp, _vp]),
+    "am_slab_outputs": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "am_slab_state": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "am_slab_flags": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
+    "am_slab_tracker": (_vp, [_vp]),
+    "am_slab_stream": (_vp, [_vp]),
+    "am_slab_destroy": (C.c_int, [_vp]),
     "am_replay_launch": (C.c_int, [_vp, _i64]),
     "am_replay_sync": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i32)]),
     "am_replay_io": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i32)]),

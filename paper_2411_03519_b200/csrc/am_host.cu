@@ -26,7 +26,8 @@ __global__ void k_sort_pass(Dev d, int pass, int32_t* order, int ntiles);
 __global__ void k_small(Dev d, uint8_t* mask, int32_t* order);
 __global__ void k_round_begin(Dev d);
 __global__ void k_efilter(Dev d);
-__global__ void k_digest(Dev d, const int32_t* order);
+__global__ void k_digest(Dev d, const int32_t* ids, const int32_t* count, const int32_t* gidmap,
+                         unsigned long long* out);
 __global__ void k_csort(Dev d, int32_t* order, int smem_bytes);
 size_t csort_smem_fixed();
 size_t csort_smem_need();
@@ -474,10 +475,10 @@ static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, co
 {
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
     if (c->d.n == 0) return AM_OK;
-    if (!pos || !steps || (mode == 2 && !st)) return set_err(c, AM_E_ARG, "NULL array");
+    if (!pos || !steps || ((mode == 2 || mode == 3) && !st)) return set_err(c, AM_E_ARG, "NULL array");
     if (c->bin_pending) return set_err(c, AM_E_STATE, "update after a binned update without a round");
     am_join_side(c);
-    if (mode != 0) c->full_hint = true;   // initial state / set state: the next round recomputes everything
+    if (mode == 1 || mode == 2) c->full_hint = true;   // initial / set state: the next round recomputes everything
     am_prof_begin(c, K_INGEST);
     CK(c, launch_k(c->pdl, c->stream, k_ingest, blocks(c->d.n, 256 * kIngestItems), 256, 0, c->d, (const int2*)pos, steps, st, mode, bin ? 1 : 0));
     CK(c, launch_k(c->pdl, c->stream, k_ingest_done, 1, 1, 0, c->d, mode, bin ? 1 : 0));
@@ -508,6 +509,14 @@ int am_update_binned(am_ctx* c, const int32_t* positions, const int32_t* sim_ste
     const int rc = launch_ingest(c, positions, sim_steps, nullptr, 0, true);
     if (rc == AM_OK) c->bin_pending = true;
     return rc;
+}
+
+extern "C" int am_update_replica(am_ctx* c, const int32_t* positions, const int32_t* sim_steps,
+                                 const uint8_t* status)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (c->first) return am_set_state(c, positions, sim_steps, status);
+    return launch_ingest(c, positions, sim_steps, status, 3);   // stream-ordered; errors at the next sync
 }
 
 extern "C" int am_set_state(am_ctx* c, const int32_t* positions, const int32_t* sim_steps,
@@ -701,7 +710,8 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             CK(c, cudaEventRecord(c->ev_fork, s));
             CK(c, cudaStreamWaitEvent(c->side2, c->ev_fork, 0));
             CK(c, launch_k(false, c->side2, k_digest, std::min(blocks(d.n, 16), (unsigned)c->num_sms * 8), 256, 0, d,
-                           (const int32_t*)d.rid));
+                           (const int32_t*)d.rid, (const int32_t*)nullptr, (const int32_t*)nullptr,
+                           (unsigned long long*)nullptr));
             CK(c, cudaEventRecord(c->ev_dig, c->side2));
             c->dig_pending = true;
         }
@@ -817,3 +827,33 @@ extern "C" int am_destroy(am_ctx* c)
 }
 
 extern "C" const char* am_last_error(const am_ctx* c) { return c ? c->err.c_str() : g_init_err.c_str(); }
+
+// ---------------------------------------------------------------- for am_slab.cu
+// perception digests of the listed agents (ids[0 .. *count)) from the context's last
+// round (records, cell table), perceived ids mapped through gidmap; into out[id]
+int am_internal_digest(am_ctx* c, const int32_t* ids, const int32_t* count, const int32_t* gidmap,
+                       unsigned long long* out, int max_ids, cudaStream_t s)
+{
+    if (c->path != 1) return set_err(c, AM_E_ARG, "digest list: binned path only");
+    CK(c, launch_k(false, s, k_digest, std::min(blocks(std::max(1, max_ids), 16), (unsigned)c->num_sms * 8), 256, 0,
+                   c->d, ids, count, gidmap, out));
+    return AM_OK;
+}
+
+// the context's one-kernel cluster sort on another key set (sd: rkey / rval ping-pong
+// buffers and a control block holding n_ready and sort_or): order[k] = rval of the k-th key
+int am_internal_csort(am_ctx* c, const Dev& sd, int32_t* order, cudaStream_t s)
+{
+    if (!c->csort_ctas) return set_err(c, AM_E_ARG, "cluster sort unavailable on this device");
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(c->csort_ctas);
+    lc.blockDim = dim3(csort_threads());
+    lc.dynamicSmemBytes = (size_t)c->csort_cap;
+    lc.stream = s;
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = c->csort_ctas; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+    lc.attrs = &at; lc.numAttrs = 1;
+    CK(c, cudaLaunchKernelEx(&lc, k_csort, sd, order, c->csort_cap));
+    return AM_OK;
+}

@@ -112,6 +112,7 @@ struct Ctl {
     // the L-inf distance from the agent to its record's cell box (every cell-pruning
     // box is widened by D), acc_D its per-update accumulator
     int32_t  D, acc_D, since_rebuild, rebuild, n_rebuilds;
+    int32_t  rebuild_req;  // a replica update brought an agent that has no record (arrival)
     uint32_t scan_next;    // dynamic work distribution of k_scan_hw (AM_SCAN_DYN)
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;

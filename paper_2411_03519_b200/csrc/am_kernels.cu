@@ -39,11 +39,11 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
     // parallelism; the state buffers and the caller's arrays may not alias)
     int2 p[kIngestItems], op[kIngestItems];
     int s[kIngestItems], os[kIngestItems];
-    uint8_t ost[kIngestItems];
+    uint8_t ost[kIngestItems], nst[kIngestItems];
 #pragma unroll
     for (int k = 0; k < kIngestItems; k++) {
         const int i = blockIdx.x * (256 * kIngestItems) + k * 256 + threadIdx.x;
-        p[k] = make_int2(0, 0); op[k] = make_int2(0, 0); s[k] = 0; os[k] = 0; ost[k] = 0;
+        p[k] = make_int2(0, 0); op[k] = make_int2(0, 0); s[k] = 0; os[k] = 0; ost[k] = 0; nst[k] = 0;
         if (i < d.n) {
             p[k] = __ldcs(npos + i);
             s[k] = __ldcs(nstep + i);
@@ -53,6 +53,11 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
                 if (validate) op[k] = d.pos[c][i];
             } else if (mode == 2) {
                 ost[k] = nstat[i];
+            } else if (mode == 3) {   // replica update: the old state to diff against
+                os[k] = d.step[c][i];
+                ost[k] = d.status[c][i];
+                op[k] = d.pos[c][i];
+                nst[k] = nstat[i];
             }
         }
     }
@@ -89,6 +94,38 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
         } else if (mode == 1) {
             if (s[k] < 0 || (d.target > 0 && s[k] > d.target)) err |= ERR_PROTOCOL;
             st = (d.target > 0 && s[k] == d.target) ? ST_DONE : ST_IDLE;
+        } else if (mode == 3) {
+            // replica update (spatial-slab window, am_slab.h): statuses are given, DONE marks
+            // an absent slot.  An agent CHANGED if it is present and its position or step
+            // differs, or it just arrived; it DEPARTED if it was present and is absent now.
+            st = nst[k];
+            if (st > ST_DONE || s[k] < 0) err |= ERR_PROTOCOL;
+            const bool pres = st != ST_DONE, was = ost[k] != ST_DONE;
+            const bool moved = pres && (!was || s[k] != os[k] || p[k].x != op[k].x || p[k].y != op[k].y);
+            if (moved || (was && !pres)) {
+                if (d.chg8) d.chg8[i] = 1;
+                if (d.dirty) {
+                    const int lab = d.labels[i];
+                    if (lab >= 0) d.dirty[lab] = ctl->epoch + 1u;
+                }
+                if (d.slot) {
+                    const uint32_t r = d.slot[i];
+                    if (r == kSentinel) {
+                        if (pres) atomicOr(&ctl->rebuild_req, 1);   // an arrival has no record yet
+                    } else if (pres) {
+                        d.rec[r] = make_int4(p[k].x | (p[k].y << 16), s[k], i, (int)st | (int)(tag << kTagShift));
+                        int cx, cy;
+                        mkey_decode(d, d.key[i], cx, cy);
+                        const int x0 = cx << d.clog, y0 = cy << d.clog;
+                        const int x1 = x0 + (1 << d.clog) - 1, y1 = y0 + (1 << d.clog) - 1;
+                        dmax = max(dmax, max(max(x0 - p[k].x, p[k].x - x1), max(y0 - p[k].y, p[k].y - y1)));
+                    } else {
+                        // departed: its record stays in its cell until the next rebuild with
+                        // a step that no agent's test matches (never behind, never equal)
+                        d.rec[r] = make_int4(op[k].x | (op[k].y << 16), INT_MAX, i, (int)ST_DONE);
+                    }
+                }
+            }
         } else {
             st = ost[k];
             if (st > ST_DONE || s[k] < 0) err |= ERR_PROTOCOL;
@@ -159,7 +196,7 @@ __global__ void k_ingest_done(Dev d, int mode, int bin)
     ctl->D = max(ctl->D, ctl->acc_D);   // (a rejected update is followed by a full rebuild)
     ctl->acc_D = 0;
     if (e == 0) {
-        if (mode != 0) ctl->full = 1;
+        if (mode == 1 || mode == 2) ctl->full = 1;   // modes 0 and 3 are incremental
         ctl->cur ^= 1u;
         ctl->W = ctl->acc_W;
         ctl->S = ctl->acc_S;
@@ -1070,10 +1107,15 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
 // agents within r_p of mix64(id<<32 ^ (u16)dx<<16 ^ (u16)dy) (order-independent).
 // One HALF-WARP per dispatched agent: lanes take the cells within r_p (one table fetch),
 // the records of the cells are flattened over the 16 lanes, partial sums are reduced.
-__global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict__ ids)
+__global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict__ ids, const int32_t* count,
+                                                const int32_t* __restrict__ gidmap, unsigned long long* out)
 {
     pdl_begin();
-    const int nr = d.ctl->n_ready;
+    // ids: the agents (slots) whose digest is due; count: their number (NULL: this round's
+    // ready count); gidmap: slot -> global id of the perceived agents' terms (NULL:
+    // identity; the spatial-slab window passes its slot map); out: NULL -> d.digest
+    const int nr = count ? *count : d.ctl->n_ready;
+    unsigned long long* dst = out ? out : d.digest;
     const uint32_t c = d.ctl->cur;
     const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4;
     const unsigned hm = 0xFFFFu << (16 * h);
@@ -1124,14 +1166,15 @@ __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict
                     const int4 B = d.rec[rs + (tq - rx)];
                     if (B.y == as && (uint32_t)B.z != aid) {
                         const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
-                        if (within2(dx, dy, Rp2, Rp, d.metric)) dig += digest_term((uint32_t)B.z, dx, dy);
+                        if (within2(dx, dy, Rp2, Rp, d.metric))
+                            dig += digest_term(gidmap ? (uint32_t)gidmap[B.z] : (uint32_t)B.z, dx, dy);
                     }
                 }
             }
         }
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) dig += __shfl_xor_sync(hm, dig, o, 16);
-        if (l == 0) d.digest[aid] = dig;
+        if (l == 0) dst[aid] = dig;
     }
 }
 
@@ -1517,7 +1560,8 @@ __device__ void round_begin(const Dev& d)
     ctl->full_next = 0;
     if (d.slot) {   // binned path: rebuild the cell binning, or keep the loose cells
         const bool rb = ctl->full != 0 || ctl->D > d.rebuild_d || ctl->since_rebuild >= d.rebuild_k ||
-                        !(d.flags & AM_VALIDATE);
+                        ctl->rebuild_req != 0 || !(d.flags & AM_VALIDATE);
+        ctl->rebuild_req = 0;
         ctl->rebuild = rb ? 1 : 0;
         if (rb) {
             ctl->D = 0;

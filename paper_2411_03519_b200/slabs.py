@@ -1,255 +1,537 @@
-"""Spatial-slab decomposition of the tracker round across GPUs (include/am_slab.h,
-SURVEY.md section 8(e)) -- marshalling and collectives only.
+"""Spatial-slab decomposition of the tracker and the replay driver across GPUs
+(include/am_slab.h) -- marshalling and collectives only.
 
-Every data-path step runs in libametro.so's kernels (am_slab.cu + the tracker);
-torch provides device memory, the exchange (NCCL through torch.distributed, or an
-in-process loopback for "virtual slabs" on one GPU) and two plumbing primitives:
-concatenating owned + received ghost records into the local tracker's input, and the
-final per-rank sort of the ready agents' priority keys (a library sort of at most
-n_owned int64 keys).
+Every data-path step runs in libametro.so's kernels (am_slab.cu + the window's
+incremental tracker); this module passes device pointers and runs the three collectives
+of a round on fixed-capacity buffers whose counts travel inside them, so no round
+synchronises the host:
 
-Round (identical result to the single-GPU round, tests/test_gpu_slabs.py):
-  1. am_slab_watermark            -> all-reduce MIN of {W, -S}
-  2. am_slab_halo                 -> all-to-all of halo records (counts first)
-  3. local round over owned + ghosts (am_set_state, am_ready PEEK, am_clusters,
-     am_blocked) -> am_slab_links  -> all-gather of link / bad records
-  4. am_slab_merge                -> global labels, ready mask, priority keys
+  1. am_slab_round_local  -> ALL-GATHER of the merge buffers (link / cluster records)
+  2. am_slab_merge        -> ALL-REDUCE MIN of the stats {next event, W, -S, inactive}
+  3. am_slab_commit       -> ALL-TO-ALL of the delta blocks (commits in other windows)
+  4. am_slab_apply
+
+The exchange is torch.distributed (NCCL over NVLink, one process per GPU:
+``DistWorld``) or an in-process loopback of G virtual slabs on one GPU
+(``LoopbackWorld``); both drive the identical library calls.  Every K rounds (and at
+the end) the flags are read (one host synchronisation): capacity overflows raise,
+a halo that the step spread is about to outgrow triggers a re-window (the global state
+is gathered once and every rank reloads a wider window) -- the spread grows by at most
+one step per round and the library raises the flag K rounds early, so every round is
+exact.
 """
 from __future__ import annotations
 
 import ctypes as C
-
+import numpy as np
 import torch
 
 from . import _lib
 from ._lib import check
-from .tracker import DONE, Tracker
 
-INT32_MAX = 2**31 - 1
+IDLE, RUNNING, DONE = _lib.IDLE, _lib.RUNNING, _lib.DONE
+OVF_WINDOW, OVF_PEER, OVF_MERGE, HALO, LIVENESS, LAG = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+NEVER = 2**63 - 1
 
 
 def slab_of_rows(map_h: int, n_slabs: int):
-    """Row range [lo, hi) of every slab (same formula as the kernels)."""
+    """Row range [lo, hi) of every slab (the kernels' formula)."""
     return [(k * map_h // n_slabs, (k + 1) * map_h // n_slabs) for k in range(n_slabs)]
 
 
 def partition(y: torch.Tensor, map_h: int, n_slabs: int) -> torch.Tensor:
-    """Slab of each agent (its row's slab)."""
-    # slab k holds rows [floor(k*H/G), floor((k+1)*H/G)): the last k with floor(k*H/G) <= y
+    """Slab of each agent (its row's slab): the last k with floor(k*H/G) <= y."""
     return ((y.to(torch.int64) + 1) * n_slabs - 1) // map_h
 
 
-class SlabRank:
-    """One slab's share of a distributed round."""
+class _DevArray:
+    """Zero-copy view of a device array owned by the library (__cuda_array_interface__)."""
 
-    def __init__(self, map_w, map_h, r_p, v, n_total, n_slabs, my_slab, gid, pos, steps, status, *,
-                 metric="l2", cell=0, ghost_cap=None, device="cuda"):
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _view(ptr, shape, dtype, device):
+    ts = {torch.int32: "<i4", torch.int64: "<i8", torch.uint8: "|u1"}[dtype]
+    return torch.as_tensor(_DevArray(ptr, shape, ts), device=device)
+
+
+def halo_needed(spread: int, r_p: int, v: int, K: int) -> int:
+    """Window rows that keep the next K rounds exact: R_b(spread + 1) + (K + 1) v."""
+    return (spread + 2) * v + r_p + (K + 1) * v
+
+
+class SlabRank:
+    """One rank's slab: its window, the window's tracker and the exchange buffers."""
+
+    def __init__(self, map_w, map_h, r_p, v, n_total, n_slabs, my_slab, target, synth, quantum_us, *,
+                 halo, cap_window, cap_peer, cap_merge, check_rounds=16, metric="l2", device="cuda",
+                 stream=None):
         self.L = _lib.load()
         self.dev = torch.device(device)
-        self.g = _lib.SlabGeom(int(map_w), int(map_h), int(r_p), int(v),
-                               _lib.METRIC_LINF if metric == "linf" else _lib.METRIC_L2,
-                               int(n_slabs), int(my_slab), int(n_total))
-        self.map_w, self.map_h, self.r_p, self.v, self.metric, self.cell = map_w, map_h, r_p, v, metric, cell
-        self.G = n_slabs
-        self.n_total = n_total
-        order = torch.argsort(gid.to(self.dev))
-        self.gid = gid.to(self.dev)[order].to(torch.int32).contiguous()   # owned, sorted by global id
-        self.pos = pos.to(self.dev)[order].to(torch.int32).contiguous()
-        self.steps = steps.to(self.dev)[order].to(torch.int32).contiguous()
-        self.status = status.to(self.dev)[order].to(torch.uint8).contiguous()
-        self.n = int(self.gid.numel())
-        self.ghost_cap = int(ghost_cap or max(4096, self.n // 2))
-        self.halo_cap = max(1024, self.n)
-        # the local tracker spans only this slab's rows plus a halo window of H rows on
-        # each side (slab-local cell table); H grows when the round's halo radius does
-        self.lo, self.hi = slab_of_rows(map_h, n_slabs)[my_slab]
-        self.H = 0
-        self.tracker = None
-        self._alloc()
-        self.stream = torch.cuda.current_stream(self.dev).cuda_stream
+        self.G, self.k = int(n_slabs), int(my_slab)
+        self.map_w, self.map_h, self.r_p, self.v = int(map_w), int(map_h), int(r_p), int(v)
+        self.n_total, self.target = int(n_total), int(target)
+        self.cap_merge = int(cap_merge) + (int(cap_merge) & 1)
+        self.g = _lib.SlabGeom(self.map_w, self.map_h, self.r_p, self.v,
+                               _lib.METRIC_LINF if metric == "linf" else _lib.METRIC_L2, self.G, self.k,
+                               self.n_total, self.target, int(halo), int(cap_window), int(cap_peer),
+                               self.cap_merge, int(check_rounds))
+        self.halo, self.cap_window, self.cap_peer = int(halo), int(cap_window), int(cap_peer)
+        self.lo, self.hi = slab_of_rows(self.map_h, self.G)[self.k]
+        self.y0, self.y1 = max(0, self.lo - self.halo), min(self.map_h, self.hi + self.halo)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        nbytes = int(self.L.am_slab_workspace_size(C.byref(self.g)))
+        if nbytes == 0:
+            raise ValueError("am_slab_workspace_size: invalid slab geometry")
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.dev)
+        ws = (self.workspace.data_ptr() + 255) & ~255
+        self.synth = synth   # keeps the tables alive
+        h = C.c_void_p()
+        check(self.L.am_slab_create(C.byref(h), C.byref(self.g), C.byref(synth.s), int(quantum_us), ws, nbytes,
+                                    self.stream.cuda_stream))
+        self.h = h
+        d = self.dev
+        self.mwords = 4 + 6 * self.cap_merge
+        self.dwords = 6 + 6 * self.cap_peer
+        self.mbuf = torch.zeros(self.mwords, dtype=torch.int32, device=d)
+        self.dsend = torch.zeros((self.G, self.dwords), dtype=torch.int32, device=d)
+        self.stats = torch.zeros(4, dtype=torch.int64, device=d)
+        self.order = torch.zeros(self.cap_window, dtype=torch.int32, device=d)
+        self.n_order = torch.zeros(1, dtype=torch.int32, device=d)
+        # zero-copy views of the library's window arrays
+        pp = [C.c_void_p() for _ in range(7)]
+        check(self.L.am_slab_state(h, *[C.byref(p) for p in pp]))
+        Lw = self.cap_window
+        self.w_pos = _view(pp[0].value, (Lw, 2), torch.int32, d)
+        self.w_step = _view(pp[1].value, (Lw,), torch.int32, d)
+        self.w_stat = _view(pp[2].value, (Lw,), torch.uint8, d)
+        self.w_traj = _view(pp[3].value, (Lw,), torch.int64, d)
+        self.w_tc = _view(pp[4].value, (Lw,), torch.int64, d)
+        self.w_np = _view(pp[5].value, (Lw, 2), torch.int32, d)
+        self.counters = _view(pp[6].value, (4,), torch.int64, d)
+        oo = [C.c_void_p() for _ in range(3)]
+        check(self.L.am_slab_outputs(h, *[C.byref(p) for p in oo]))
+        self.w_gid = _view(oo[0].value, (Lw,), torch.int32, d)
+        self.w_label = _view(oo[1].value, (Lw,), torch.int32, d)
+        self.w_ready = _view(oo[2].value, (Lw,), torch.uint8, d)
 
-    def _alloc(self):
-        d, G = self.dev, self.G
-        self.n_cap = self.n + self.ghost_cap
-        self._make_tracker()
-        self.ws = torch.empty(2, dtype=torch.int32, device=d)
-        self.send = torch.empty((G, self.halo_cap, 4), dtype=torch.int32, device=d)
-        self.counts = torch.zeros(G, dtype=torch.int32, device=d)
-        self.sent = torch.zeros(max(self.n, 1), dtype=torch.uint8, device=d)
-        self.lcap = self.n_cap
-        self.links = torch.empty((self.lcap, 2), dtype=torch.int32, device=d)
-        self.bads = torch.empty(self.lcap, dtype=torch.int32, device=d)
-        self.nl = torch.zeros(2, dtype=torch.int32, device=d)
-        self.badlocal = torch.zeros(self.n_cap, dtype=torch.uint8, device=d)
-        self.bnd = torch.zeros(self.n_cap, dtype=torch.uint8, device=d)
-        self.forest = torch.arange(self.n_total, dtype=torch.int64, device=d).to(torch.int32)
-        self.badm = torch.zeros(self.n_total, dtype=torch.uint8, device=d)
-        self.touched = torch.zeros(self.n_total, dtype=torch.uint8, device=d)
-        self.lpos = torch.zeros((self.n_cap, 2), dtype=torch.int32, device=d)
-        self.lsteps = torch.zeros(self.n_cap, dtype=torch.int32, device=d)
-        self.lstatus = torch.full((self.n_cap,), DONE, dtype=torch.uint8, device=d)
-        self.lgid = torch.zeros(self.n_cap, dtype=torch.int32, device=d)
-        self.lblocked = torch.zeros(self.n_cap, dtype=torch.uint8, device=d)
-        self.out_label = torch.empty(max(self.n, 1), dtype=torch.int32, device=d)
-        self.out_mask = torch.empty(max(self.n, 1), dtype=torch.uint8, device=d)
-        self.out_key = torch.empty(max(self.n, 1), dtype=torch.int64, device=d)
+    # ------------------------------------------------------------------ library steps
+    def load(self, gid, pos, steps, status, traj=None, tcommit=None, newpos=None, t: int = 0):
+        m = int(gid.numel())
+        if m > self.cap_window:
+            raise ValueError("window capacity exceeded")
+        args = [gid, pos, steps, status, traj, tcommit, newpos]
+        self._keep = [a.contiguous() if a is not None else None for a in args]
+        ptrs = [a.data_ptr() if a is not None else None for a in self._keep]
+        check(self.L.am_slab_load(self.h, m, *ptrs, int(t)))
 
-    def _make_tracker(self):
-        """Local tracker over rows [y0, y1) = this slab +- H halo rows (translated to
-        y - y0: distances, hence every result, are translation invariant)."""
-        if self.tracker is not None:
-            self.tracker.close()
-        self.y0 = max(0, self.lo - self.H)
-        self.y1 = min(self.map_h, self.hi + self.H)
-        self.tracker = Tracker(self.map_w, max(1, self.y1 - self.y0), self.r_p, self.v, self.n_cap, cell=self.cell,
-                               metric=self.metric, validate=False, peek=True, force="binned", device=self.dev)
+    def round_local(self):
+        check(self.L.am_slab_round_local(self.h, self.mbuf.data_ptr()))
+        return self.mbuf
 
-    def _window(self, ws_global: torch.Tensor):
-        """Grow the halo window to the round's halo radius R_b(S - W) (every ghost lies
-        within it of this slab, am_slab.h) with 2x slack."""
-        W, negS = ws_global.tolist()
-        if W == INT32_MAX:
-            return
-        lag = max(0, -negS - W)
-        rh = min(self.map_h, (lag + 1) * self.v + self.r_p + 1)
-        if rh > self.H and (self.lo - self.H > 0 or self.hi + self.H < self.map_h):
-            self.H = min(self.map_h, 2 * rh)
-            self._make_tracker()
+    def merge(self, mbufs: torch.Tensor):
+        check(self.L.am_slab_merge(self.h, mbufs.data_ptr(), self.order.data_ptr(), self.n_order.data_ptr(),
+                                   self.stats.data_ptr()))
+        return self.stats
 
-    # ------------------------------------------------------------------ phases
-    def p1_watermark(self) -> torch.Tensor:
-        check(self.L.am_slab_watermark(self.n, self.steps.data_ptr(), self.status.data_ptr(),
-                                       self.ws.data_ptr(), self.stream))
-        return self.ws
+    def commit(self, stats_global: torch.Tensor):
+        check(self.L.am_slab_commit(self.h, stats_global.data_ptr(), self.dsend.data_ptr()))
+        return self.dsend
 
-    def p2_halo(self, ws_global: torch.Tensor):
-        """-> list of G record tensors [count_j, 4] to send (own slab empty)."""
-        self.ws.copy_(ws_global)
-        check(self.L.am_slab_halo(C.byref(self.g), self.n, self.gid.data_ptr(), self.pos.data_ptr(),
-                                  self.steps.data_ptr(), self.status.data_ptr(), self.ws.data_ptr(),
-                                  self.halo_cap, self.send.data_ptr(), self.counts.data_ptr(),
-                                  self.sent.data_ptr(), self.stream))
-        cnt = self.counts.tolist()
-        if max(cnt) > self.halo_cap:
-            raise RuntimeError("halo buffer overflow")   # capacity is n_owned: cannot happen
-        return [self.send[j, : cnt[j]] for j in range(self.G)]
+    def apply(self, drecv: torch.Tensor):
+        check(self.L.am_slab_apply(self.h, drecv.data_ptr()))
 
-    def p3_local(self, ghosts: torch.Tensor):
-        """ghosts: [m, 4] received records.  -> (links [k, 2], bads [b]) to all-gather."""
-        m = int(ghosts.shape[0])
-        if self.n + m > self.n_cap:
-            self.ghost_cap = 2 * (self.n + m)
-            self._alloc()
-        n, nl = self.n, self.n + m
-        self._window(self.ws)
-        ghosts = ghosts.contiguous()
-        check(self.L.am_slab_assemble(n, self.gid.data_ptr(), self.pos.data_ptr(), self.steps.data_ptr(),
-                                      self.status.data_ptr(), m, ghosts.data_ptr() if m else None, self.n_cap,
-                                      self.y0, self.lpos.data_ptr(), self.lsteps.data_ptr(),
-                                      self.lstatus.data_ptr(), self.lgid.data_ptr(), self.stream))
-        tr = self.tracker
-        # stream-ordered local round (AM_ASYNC): no host synchronisation until the link
-        # counts; a rejected state would surface at the next synchronising call
-        self.L.am_set_flags(tr.ctx, tr.flags | _lib.ASYNC)
+    def flags(self):
+        f, used = C.c_int32(0), C.c_int32(0)
+        check(self.L.am_slab_flags(self.h, C.byref(f), C.byref(used)))
+        return f.value, used.value
+
+    def tracker_ctx(self):
+        return self.L.am_slab_tracker(self.h)
+
+    # ------------------------------------------------------------------ views
+    def owned_mask(self) -> torch.Tensor:
+        y = self.w_pos[:, 1]
+        return (self.w_gid >= 0) & (y >= self.lo) & (y < self.hi)
+
+    def owned_state(self):
+        """The owned agents (every field needed to reload them anywhere)."""
+        m = self.owned_mask()
+        return dict(gid=self.w_gid[m].clone(), pos=self.w_pos[m].clone(), steps=self.w_step[m].clone(),
+                    status=self.w_stat[m].clone(), traj=self.w_traj[m].clone(), tcommit=self.w_tc[m].clone(),
+                    newpos=self.w_np[m].clone())
+
+    def round_outputs(self):
+        """This rank's ready agents (global ids in priority order) and, for every owned
+        agent, (gid, global label, ready bit)."""
+        n = int(self.n_order.item())
+        m = self.owned_mask()
+        return dict(order=self.order[:n].clone(), gid=self.w_gid[m].clone(), label=self.w_label[m].clone(),
+                    ready=self.w_ready[m].clone(), step=self.w_step[m].clone())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.am_slab_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
         try:
-            tr.set_state(self.lpos, self.lsteps, self.lstatus)
-        finally:
-            self.L.am_set_flags(tr.ctx, tr.flags)
-        tr.ready_async()
-        labels = tr.clusters()
-        check(self.L.am_blocked(tr.ctx, self.lblocked.data_ptr()), tr.ctx)
-        check(self.L.am_slab_links(nl, n, self.lgid.data_ptr(), labels.data_ptr(), self.lstatus.data_ptr(),
-                                   self.lblocked.data_ptr(), self.sent.data_ptr(), self.lcap,
-                                   self.links.data_ptr(), self.nl.data_ptr(), self.bads.data_ptr(),
-                                   self.nl.data_ptr() + 4, self.badlocal.data_ptr(), self.bnd.data_ptr(),
-                                   self.stream))
-        k, b = self.nl.tolist()
-        tr.sync()   # reports a rejected local state (bounds, statuses)
-        if k > self.lcap or b > self.lcap:
-            raise RuntimeError("link buffer overflow")   # <= one record per local agent
-        self.labels_local = labels
-        return self.links[:k], self.bads[:b]
-
-    def p4_merge(self, links_all: torch.Tensor, bads_all: torch.Tensor, ws_global: torch.Tensor):
-        """-> dict(mask, labels (global), order (global ids by (step, label, id)), n_ready)."""
-        links_all = links_all.contiguous()
-        bads_all = bads_all.contiguous()
-        check(self.L.am_slab_merge(C.byref(self.g), self.n, self.gid.data_ptr(), self.steps.data_ptr(),
-                                   self.status.data_ptr(), self.labels_local.data_ptr(),
-                                   self.badlocal.data_ptr(), links_all.data_ptr(), int(links_all.shape[0]),
-                                   bads_all.data_ptr(), int(bads_all.shape[0]), ws_global.data_ptr(),
-                                   self.forest.data_ptr(), self.badm.data_ptr(), self.touched.data_ptr(),
-                                   self.out_label.data_ptr(), self.out_mask.data_ptr(),
-                                   self.out_key.data_ptr(), self.stream))
-        mask = self.out_mask[: self.n]
-        keys = self.out_key[: self.n]
-        sel = keys[mask.bool()]
-        skeys, _ = torch.sort(sel)
-        order = (skeys & ((1 << 21) - 1)).to(torch.int32)
-        return dict(mask=mask, labels=self.out_label[: self.n], order=order, gid=self.gid,
-                    n_ready=int(order.numel()))
+            self.close()
+        except Exception:
+            pass
 
 
-# ---------------------------------------------------------------------- drivers
-def round_loopback(ranks: list[SlabRank], timings: list | None = None):
-    """Virtual slabs in one process: the exchanges are in-device copies.  With
-    `timings` (a list), the device time of every slab's local round (phase 3) is
-    appended to it in ms (CUDA events; what one GPU would spend on its slab)."""
-    ws = torch.stack([r.p1_watermark() for r in ranks]).min(0).values
-    outgoing = [r.p2_halo(ws) for r in ranks]
-    recs = []
-    for r in ranks:
-        k = r.g.my_slab
-        parts = [outgoing[j][k] for j in range(len(ranks)) if j != k]
-        recs.append(torch.cat(parts) if parts else torch.empty((0, 4), dtype=torch.int32, device=r.dev))
-    lb = []
-    for r, g in zip(ranks, recs):
-        if timings is not None:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            lb.append(r.p3_local(g))
-            e1.record()
-            e1.synchronize()
-            timings.append(e0.elapsed_time(e1))
-        else:
-            lb.append(r.p3_local(g))
-    links = torch.cat([x[0] for x in lb])
-    bads = torch.cat([x[1] for x in lb])
-    return [r.p4_merge(links, bads, ws) for r in ranks]
+# ---------------------------------------------------------------------- worlds
+class _World:
+    """Common driver: setup from a global initial state, rounds, checks, re-windows."""
+
+    def _geometry(self, y_all: torch.Tensor, spread: int, K: int, halo: int | None = None):
+        H = halo if halo is not None else halo_needed(spread, self.r_p, self.v, K)
+        H = min(H, self.map_h)
+        # capacities from the actual distribution, with slack for migration
+        rows = slab_of_rows(self.map_h, self.G)
+        y = y_all.to(torch.int64)
+        wins, bands = [], []
+        for lo, hi in rows:
+            y0, y1 = max(0, lo - H), min(self.map_h, hi + H)
+            wins.append(int(((y >= y0) & (y < y1)).sum()))
+            bnd = ((y >= lo - H) & (y < lo + H)) | ((y >= hi - H) & (y < hi + H))
+            bands.append(int(bnd.sum()))
+        cap_window = int(max(wins) * 1.25) + 2048
+        cap_merge = int(max(bands) * 1.5) + 2048
+        cap_peer = int(max(bands) * 0.5) + 2048
+        return H, cap_window, cap_merge, cap_peer
+
+    @staticmethod
+    def _window_select(st: dict, lo: int, hi: int, H: int, map_h: int):
+        y = st["pos"][:, 1]
+        sel = (y >= max(0, lo - H)) & (y < min(map_h, hi + H))
+        return {k: v[sel].contiguous() for k, v in st.items()}
 
 
-def round_distributed(rank: SlabRank, dist):
-    """One slab per process; dist = torch.distributed with an initialised group
-    (NCCL on GPUs; the tensors are device tensors)."""
-    ws = rank.p1_watermark().clone()
-    dist.all_reduce(ws, op=dist.ReduceOp.MIN)
-    out = rank.p2_halo(ws)
-    G = rank.G
-    send_counts = torch.tensor([int(t.shape[0]) for t in out], dtype=torch.int64, device=rank.dev)
-    recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts)
-    rc = recv_counts.tolist()
-    sendbuf = torch.cat(out) if sum(int(t.shape[0]) for t in out) else torch.empty((0, 4), dtype=torch.int32,
-                                                                                      device=rank.dev)
-    recvbuf = torch.empty((sum(rc), 4), dtype=torch.int32, device=rank.dev)
-    dist.all_to_all_single(recvbuf, sendbuf.contiguous(), output_split_sizes=rc,
-                           input_split_sizes=send_counts.tolist())
-    links, bads = rank.p3_local(recvbuf)
-    links_all = _all_gather_var(dist, links, G, rank.dev)
-    bads_all = _all_gather_var(dist, bads, G, rank.dev)
-    return rank.p4_merge(links_all, bads_all, ws)
+def _spread(steps0, status0) -> int:
+    """S - W over the agents that are not DONE (0 for the all-at-step-0 start)."""
+    if steps0 is None:
+        return 0
+    s = np.asarray(steps0)
+    if status0 is not None:
+        s = s[np.asarray(status0) != DONE]
+    return int(s.max() - s.min()) if len(s) else 0
 
 
-def _all_gather_var(dist, t: torch.Tensor, G: int, dev):
-    """All-gather of a variable-length tensor (length first, then padded payload)."""
-    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)
-    ns = [torch.empty_like(n) for _ in range(G)]
-    dist.all_gather(ns, n)
-    ns = [int(x.item()) for x in ns]
-    mx = max(ns) if ns else 0
-    shape = (mx,) + tuple(t.shape[1:])
-    pad = torch.zeros(shape, dtype=t.dtype, device=dev)
-    pad[: t.shape[0]] = t
-    outs = [torch.empty(shape, dtype=t.dtype, device=dev) for _ in range(G)]
-    dist.all_gather(outs, pad)
-    return torch.cat([o[:k] for o, k in zip(outs, ns)])
+def _initial_state(x0, y0, steps0, status0, dev):
+    """Every agent's replay state at time 0 (all IDLE at step 0 unless given)."""
+    n = len(x0)
+    pos = torch.as_tensor(np.stack([np.asarray(x0), np.asarray(y0)], 1).reshape(n, 2), dtype=torch.int32,
+                          device=dev)
+    return dict(gid=torch.arange(n, dtype=torch.int32, device=dev), pos=pos,
+                steps=(torch.zeros(n, dtype=torch.int32, device=dev) if steps0 is None else
+                       torch.as_tensor(np.asarray(steps0), dtype=torch.int32, device=dev)),
+                status=(torch.zeros(n, dtype=torch.uint8, device=dev) if status0 is None else
+                        torch.as_tensor(np.asarray(status0), dtype=torch.uint8, device=dev)),
+                traj=torch.zeros(n, dtype=torch.int64, device=dev),
+                tcommit=torch.full((n,), NEVER, dtype=torch.int64, device=dev), newpos=pos.clone())
+
+
+class LoopbackWorld(_World):
+    """G virtual slabs in one process on one GPU (the exchanges are device copies on one
+    stream): the same library calls as the NCCL run, bit-exact against it by design."""
+
+    def __init__(self, map_w, map_h, r_p, v, x0, y0, target, synth, quantum_us, n_slabs, *, metric="l2",
+                 check_rounds=16, device="cuda", halo=None, steps0=None, status0=None):
+        self.map_w, self.map_h, self.r_p, self.v = int(map_w), int(map_h), int(r_p), int(v)
+        self.G, self.target, self.synth, self.Q = int(n_slabs), int(target), synth, int(quantum_us)
+        self.metric, self.K, self.dev = metric, int(check_rounds), torch.device(device)
+        st = _initial_state(x0, y0, steps0, status0, self.dev)
+        self.n = len(x0)
+        self.ranks = []
+        self.rounds_done = 0
+        self.rewindows = 0
+        self._setup(st, 0, spread=_spread(steps0, status0), halo=halo)
+
+    def _setup(self, st: dict, t: int, spread: int, halo=None):
+        for r in self.ranks:
+            r.close()
+        H, cw, cm, cp = self._geometry(st["pos"][:, 1], spread, self.K, halo)
+        self.halo = H
+        self.ranks = []
+        for k in range(self.G):
+            r = SlabRank(self.map_w, self.map_h, self.r_p, self.v, self.n, self.G, k, self.target, self.synth,
+                         self.Q, halo=H, cap_window=cw, cap_peer=cp, cap_merge=cm, check_rounds=self.K,
+                         metric=self.metric, device=self.dev)
+            w = self._window_select(st, r.lo, r.hi, H, self.map_h)
+            r.load(w["gid"], w["pos"], w["steps"], w["status"], w["traj"], w["tcommit"], w["newpos"], t)
+            self.ranks.append(r)
+
+    def round(self, log: list | None = None):
+        """One distributed round of all virtual slabs (no host synchronisation unless
+        `log` asks for the round's outputs)."""
+        mb = torch.stack([r.round_local() for r in self.ranks])            # all-gather
+        for r in self.ranks:
+            r.merge(mb)
+        if log is not None:
+            log.append([r.round_outputs() for r in self.ranks])
+        sg = torch.stack([r.stats for r in self.ranks]).min(0).values       # all-reduce MIN
+        ds = torch.stack([r.commit(sg) for r in self.ranks])                # [src, dst, words]
+        for k, r in enumerate(self.ranks):
+            r.apply(ds[:, k].contiguous())                                  # all-to-all
+        self.rounds_done += 1
+        self._last_stats = sg
+
+    def check(self) -> bool:
+        """Reads every rank's flags (one synchronisation).  Raises on an overflow or a
+        liveness failure, re-windows when the halo is about to be outgrown.  Returns True
+        when every agent is DONE."""
+        flags = 0
+        for r in self.ranks:
+            f, _ = r.flags()
+            flags |= f
+        if flags & (OVF_WINDOW | OVF_PEER | OVF_MERGE | LAG):
+            raise RuntimeError(f"slab exchange overflow (flags {flags:#x})")
+        if flags & LIVENESS:
+            raise RuntimeError("replay: agents not DONE but nothing running (liveness)")
+        sg = self._last_stats.tolist()
+        if flags & HALO:
+            self.rewindow(spread=-sg[2] - sg[1])
+        return sg[3] == 1
+
+    def rewindow(self, spread: int):
+        """Gathers the global state and reloads every rank with a window twice as wide as
+        the spread needs now."""
+        parts = [r.owned_state() for r in self.ranks]
+        st = {k: torch.cat([p[k] for p in parts]) for k in parts[0]}
+        t = int(self.ranks[0].counters[0].item())
+        need = halo_needed(spread, self.r_p, self.v, self.K)
+        self._setup(st, t, spread, halo=2 * need)
+        self.rewindows += 1
+
+    def run(self, max_rounds: int) -> int:
+        """Rounds until every agent is DONE (checked every K rounds); returns the rounds run."""
+        done = 0
+        while done < max_rounds:
+            for _ in range(min(self.K, max_rounds - done)):
+                self.round()
+                done += 1
+            if self.check():
+                break
+        return done
+
+    def results(self):
+        """The final (or current) state of every agent, in global-id order, T_ooo, rounds."""
+        parts = [r.owned_state() for r in self.ranks]
+        gid = torch.cat([p["gid"] for p in parts]).long()
+        n = self.n
+        out = {}
+        for k in ("pos", "steps", "traj"):
+            v = torch.cat([p[k] for p in parts])
+            o = torch.zeros((n,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
+            o[gid] = v
+            out[k] = o.cpu().numpy()
+        cnt = torch.stack([r.counters for r in self.ranks]).cpu().numpy()
+        assert len(np.unique(gid.cpu().numpy())) == n, "every agent owned exactly once"
+        return dict(x=out["pos"][:, 0], y=out["pos"][:, 1], steps=out["steps"],
+                    traj=out["traj"].view(np.uint64), T_ooo=int(cnt[:, 1].max()), rounds=int(cnt[0, 3]),
+                    dispatched=int(cnt[:, 2].sum()))
+
+    def close(self):
+        for r in self.ranks:
+            r.close()
+        self.ranks = []
+
+
+class DistWorld(_World):
+    """One slab per process over torch.distributed (NCCL on GPUs; every collective runs on
+    the current stream with fixed-size device buffers -- no host synchronisation per
+    round).  `dist` may be torch.distributed or any object with the same four calls
+    (tests stage gloo through the host)."""
+
+    def __init__(self, dist, map_w, map_h, r_p, v, x0, y0, target, synth, quantum_us, *, metric="l2",
+                 check_rounds=16, device="cuda", halo=None, steps0=None, status0=None):
+        self.dist = dist
+        self.G, self.k = dist.get_world_size(), dist.get_rank()
+        self.map_w, self.map_h, self.r_p, self.v = int(map_w), int(map_h), int(r_p), int(v)
+        self.target, self.synth, self.Q = int(target), synth, int(quantum_us)
+        self.metric, self.K, self.dev = metric, int(check_rounds), torch.device(device)
+        st = _initial_state(x0, y0, steps0, status0, self.dev)
+        self.n = len(x0)
+        self.rank = None
+        self.rounds_done = 0
+        self.rewindows = 0
+        self._setup(st, 0, spread=_spread(steps0, status0), halo=halo)
+
+    def _setup(self, st: dict, t: int, spread: int, halo=None):
+        if self.rank is not None:
+            self.rank.close()
+        H, cw, cm, cp = self._geometry(st["pos"][:, 1], spread, self.K, halo)
+        self.halo = H
+        r = SlabRank(self.map_w, self.map_h, self.r_p, self.v, self.n, self.G, self.k, self.target, self.synth,
+                     self.Q, halo=H, cap_window=cw, cap_peer=cp, cap_merge=cm, check_rounds=self.K,
+                     metric=self.metric, device=self.dev)
+        w = self._window_select(st, r.lo, r.hi, H, self.map_h)
+        r.load(w["gid"], w["pos"], w["steps"], w["status"], w["traj"], w["tcommit"], w["newpos"], t)
+        self.rank = r
+        self.mball = torch.empty((self.G, r.mwords), dtype=torch.int32, device=self.dev)
+        self.drecv = torch.empty((self.G, r.dwords), dtype=torch.int32, device=self.dev)
+
+    def round(self, log: list | None = None):
+        r, dist = self.rank, self.dist
+        mb = r.round_local()
+        dist.all_gather_into_tensor(self.mball.view(-1), mb)
+        r.merge(self.mball)
+        if log is not None:
+            log.append(r.round_outputs())
+        sg = r.stats.clone()
+        dist.all_reduce(sg, op=dist.ReduceOp.MIN)
+        ds = r.commit(sg)
+        dist.all_to_all_single(self.drecv, ds)
+        r.apply(self.drecv)
+        self.rounds_done += 1
+        self._last_stats = sg
+
+    def check(self) -> bool:
+        f, _ = self.rank.flags()
+        ft = torch.tensor([f], dtype=torch.int32, device=self.dev)
+        fall = torch.empty(self.G, dtype=torch.int32, device=self.dev)
+        self.dist.all_gather_into_tensor(fall, ft)   # flags of every rank, OR-ed below
+        flags = 0
+        for x in fall.tolist():
+            flags |= int(x)
+        if flags & (OVF_WINDOW | OVF_PEER | OVF_MERGE | LAG):
+            raise RuntimeError(f"slab exchange overflow (flags {flags:#x})")
+        if flags & LIVENESS:
+            raise RuntimeError("replay: agents not DONE but nothing running (liveness)")
+        sg = self._last_stats.tolist()
+        if flags & HALO:
+            self.rewindow(spread=-sg[2] - sg[1])
+        return sg[3] == 1
+
+    def _gather_state(self):
+        mine = self.rank.owned_state()
+        cnt = torch.tensor([mine["gid"].numel()], dtype=torch.int64, device=self.dev)
+        cnts = [torch.empty_like(cnt) for _ in range(self.G)]
+        self.dist.all_gather(cnts, cnt)
+        cnts = [int(c.item()) for c in cnts]
+        mx = max(cnts)
+        out = {}
+        for k, v in mine.items():
+            pad = torch.zeros((mx,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
+            pad[: v.shape[0]] = v
+            parts = [torch.empty_like(pad) for _ in range(self.G)]
+            self.dist.all_gather(parts, pad)
+            out[k] = torch.cat([p[:c] for p, c in zip(parts, cnts)])
+        return out
+
+    def rewindow(self, spread: int):
+        st = self._gather_state()
+        t = int(self.rank.counters[0].item())
+        need = halo_needed(spread, self.r_p, self.v, self.K)
+        self._setup(st, t, spread, halo=2 * need)
+        self.rewindows += 1
+
+    def run(self, max_rounds: int) -> int:
+        done = 0
+        while done < max_rounds:
+            for _ in range(min(self.K, max_rounds - done)):
+                self.round()
+                done += 1
+            if self.check():
+                break
+        return done
+
+    def results(self):
+        st = self._gather_state()
+        n = self.n
+        gid = st["gid"].long()
+        out = {}
+        for k in ("pos", "steps", "traj"):
+            v = st[k]
+            o = torch.zeros((n,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
+            o[gid] = v
+            out[k] = o.cpu().numpy()
+        cnt = self.rank.counters.clone()
+        c1 = cnt[1:2].clone()
+        self.dist.all_reduce(c1, op=self.dist.ReduceOp.MAX)
+        c2 = cnt[2:3].clone()
+        self.dist.all_reduce(c2, op=self.dist.ReduceOp.SUM)
+        return dict(x=out["pos"][:, 0], y=out["pos"][:, 1], steps=out["steps"],
+                    traj=out["traj"].view(np.uint64), T_ooo=int(c1.item()), rounds=int(cnt[3].item()),
+                    dispatched=int(c2.item()))
+
+    def close(self):
+        if self.rank is not None:
+            self.rank.close()
+            self.rank = None
+
+
+class Synth:
+    """The synthetic replay model's tables (am_driver.h am_synth) as device tensors,
+    kept alive with the ctypes struct that points into them."""
+
+    def __init__(self, lm, *, wall=None, dur_table=None, policy=0, device="cuda"):
+        dev = torch.device(device)
+        self.lat = torch.as_tensor(np.asarray(lm.lat, np.int64).astype(np.uint32).view(np.int32), device=dev)
+        self.cdf = torch.as_tensor(np.asarray(lm.cdf32, np.uint64).view(np.int64), device=dev)
+        self.vals = torch.as_tensor(np.asarray(lm.vals, np.int32), device=dev)
+        self.wall = None if wall is None else torch.as_tensor(np.ascontiguousarray(wall, np.uint8), device=dev)
+        self.dur = None if dur_table is None else torch.as_tensor(np.asarray(dur_table, np.int64), device=dev)
+        self.s = _lib.Synth(self.lat.data_ptr(), self.cdf.data_ptr(), self.vals.data_ptr(), len(self.vals),
+                            int(lm.base_us), int(lm.lat_seed), int(lm.policy_seed),
+                            None if self.wall is None else self.wall.data_ptr(),
+                            None if self.dur is None else self.dur.data_ptr(),
+                            0 if self.dur is None else self.dur.shape[1], int(policy), 0)
+
+
+def merged_order(outs: list) -> tuple[np.ndarray, np.ndarray]:
+    """One round's ready agents over all ranks (test / logging helper, host side): the
+    ranks' orders -- each sorted by (step, label, id) -- merged into the global order,
+    with the dispatched agents' labels."""
+    ids, keys, labs = [], [], []
+    for o in outs:
+        g = o["gid"].cpu().numpy()
+        lab = dict(zip(g.tolist(), o["label"].cpu().numpy().tolist()))
+        stp = dict(zip(g.tolist(), o["step"].cpu().numpy().tolist()))
+        for i in o["order"].cpu().numpy().tolist():
+            ids.append(i)
+            labs.append(lab[i])
+            keys.append((stp[i], lab[i], i))
+    idx = sorted(range(len(ids)), key=lambda k: keys[k])
+    return np.array([ids[k] for k in idx], np.int32), np.array([labs[k] for k in idx], np.int32)
+
+
+class HostStagedDist:
+    """torch.distributed calls of DistWorld over a gloo group with CUDA tensors staged
+    through host memory -- for running several ranks on ONE GPU (NCCL refuses two ranks
+    per device): multi-process tests of the distributed round.  Synchronous, slow, exact."""
+
+    def __init__(self, dist):
+        self.d = dist
+        self.ReduceOp = dist.ReduceOp
+
+    def get_rank(self):
+        return self.d.get_rank()
+
+    def get_world_size(self):
+        return self.d.get_world_size()
+
+    def all_gather_into_tensor(self, out, inp):
+        parts = [torch.empty_like(inp, device="cpu") for _ in range(self.get_world_size())]
+        self.d.all_gather(parts, inp.cpu())
+        out.copy_(torch.cat([p.reshape(-1) for p in parts]).reshape(out.shape))
+
+    def all_gather(self, outs, inp):
+        parts = [torch.empty_like(inp, device="cpu") for _ in outs]
+        self.d.all_gather(parts, inp.cpu())
+        for o, p in zip(outs, parts):
+            o.copy_(p)
+
+    def all_reduce(self, t, op):
+        c = t.cpu()
+        self.d.all_reduce(c, op=op)
+        t.copy_(c)
+
+    def all_to_all_single(self, out, inp):
+        c = torch.empty_like(out, device="cpu")
+        self.d.all_to_all_single(c, inp.cpu().contiguous())
+        out.copy_(c)

@@ -91,6 +91,12 @@ class Tracker:
                                   _ptr(steps, torch.int32, (self.n,)),
                                   _ptr(status, torch.uint8, (self.n,))), self.ctx)
 
+    def update_replica(self, pos: torch.Tensor, steps: torch.Tensor, status: torch.Tensor) -> None:
+        """am_update_replica: full state diffed against the current one (incremental)."""
+        check(self.L.am_update_replica(self.ctx, _ptr(pos, torch.int32, (self.n, 2)),
+                                       _ptr(steps, torch.int32, (self.n,)),
+                                       _ptr(status, torch.uint8, (self.n,))), self.ctx)
+
     def ready(self, mask: torch.Tensor | None = None, order: torch.Tensor | None = None):
         """One round.  Returns (mask, order[:n_ready]) device tensors."""
         mask = self.mask if mask is None else mask

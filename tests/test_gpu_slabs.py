@@ -1,6 +1,15 @@
-"""S7 multi-GPU spatial slabs, virtual slabs on one GPU (loopback exchange): the
-distributed round equals the oracle's single round bit for bit (mask, labels,
-per-rank order) for several slab counts, including multi-hop halos."""
+"""S7 / S8 across spatial slabs (include/am_slab.h), run as virtual slabs on one GPU
+(LoopbackWorld: the same library calls as the NCCL run, the exchanges are device copies).
+
+* one distributed round on random and banded states equals the oracle's single round bit
+  for bit: ready mask, cluster labels of every agent, and the global priority order (the
+  ranks' orders merged), for G = 1 .. 16 slabs including multi-hop windows;
+* the distributed REPLAY (incremental window trackers, deltas, migration across slab
+  edges, arrivals / departures, cross-slab cluster completion times, the global event
+  clock, re-windowing as the step spread grows) equals the oracle's replay round by round
+  (every round's dispatched ids in priority order and their labels) and in its final
+  state (positions, trajectory hashes, T_ooo, rounds) on C1, C2 and a C4-shaped map at
+  G = 2 / 4 / 8."""
 import numpy as np
 import pytest
 import torch
@@ -12,60 +21,55 @@ from paper_2411_03519_b200 import slabs
 pytestmark = pytest.mark.gpu
 
 
-def _run(x, y, s, st, W, H, G, r_p=4, v=1, metric="l2"):
+def _world(w, lm, G, steps0=None, status0=None, **kw):
+    sy = slabs.Synth(lm, wall=w.wall)
+    return slabs.LoopbackWorld(w.map_w, w.map_h, w.r_p, w.v, w.x, w.y, w.steps, sy, w.Q, G, steps0=steps0,
+                               status0=status0, **kw)
+
+
+def _round_vs_oracle(x, y, s, st, W, H, G, r_p=4, v=1, metric="l2", check_rounds=4):
     n = len(x)
-    gid = np.arange(n, dtype=np.int32)
-    part = slabs.partition(torch.as_tensor(y), H, G).numpy()
-    ranks = []
-    for k in range(G):
-        sel = np.nonzero(part == k)[0]
-        t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a[sel]), dtype=dt, device="cuda")
-        pos = torch.as_tensor(np.stack([x[sel], y[sel]], 1), dtype=torch.int32, device="cuda")
-        ranks.append(slabs.SlabRank(W, H, r_p, v, n, G, k, t(gid, torch.int32), pos, t(s, torch.int32),
-                                    t(st, torch.uint8), metric=metric))
-    outs = slabs.round_loopback(ranks)
+    lm = amgen.latency_model()
+    w = amgen.Workload("rand", W, H, None, x, y, 1, 1000, r_p=r_p, v=v)
+    sy = slabs.Synth(lm)
+    wd = slabs.LoopbackWorld(W, H, r_p, v, x, y, 1000, sy, 0, G, steps0=s, status0=st, metric=metric,
+                             check_rounds=check_rounds)
+    log = []
+    wd.round(log)
+    outs = log[0]
+    p = O.params(W, H, r_p, v, 1000, O.LINF if metric == "linf" else O.L2)
+    ref = O.round_(p, x, y, s, st.copy(), peek=True)
     mask = np.zeros(n, np.uint8)
-    label = np.zeros(n, np.int32)
-    orders = []
+    lab = np.full(n, -7, np.int32)
     for o in outs:
         g = o["gid"].cpu().numpy()
-        mask[g] = o["mask"].cpu().numpy()
-        label[g] = o["labels"].cpu().numpy()
-        orders.append(o["order"].cpu().numpy())
-    return mask, label, orders
-
-
-def _check(x, y, s, st, W, H, G, **kw):
-    p = O.params(W, H, kw.get("r_p", 4), kw.get("v", 1), 0,
-                 O.LINF if kw.get("metric") == "linf" else O.L2)
-    r = O.round_(p, x, y, s, st.copy(), peek=True)
-    mask, label, orders = _run(x, y, s, st, W, H, G, **kw)
-    np.testing.assert_array_equal(mask, r["mask"])
-    np.testing.assert_array_equal(label, r["label"])
-    # each rank's order = the global order restricted to its agents
-    part = slabs.partition(torch.as_tensor(y), H, G).numpy()
-    for k, ok in enumerate(orders):
-        exp = np.array([i for i in r["order"] if part[i] == k], np.int32)
-        np.testing.assert_array_equal(ok, exp)
-    assert sum(len(o) for o in orders) == len(r["order"])
+        mask[g] = o["ready"].cpu().numpy()
+        lab[g] = o["label"].cpu().numpy()
+    np.testing.assert_array_equal(mask, ref["mask"])
+    np.testing.assert_array_equal(lab, ref["label"])
+    order, olab = slabs.merged_order(outs)
+    np.testing.assert_array_equal(order, ref["order"])
+    np.testing.assert_array_equal(olab, ref["label"][ref["order"]])
+    wd.close()
+    del w
 
 
 @pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
-def test_random_state_slabs(G):
+def test_random_state_round(G):
     n, m = 12000, 900
     x, y, s, st = amgen.random_state(n, m, m, 40 + G, max_step=6, p_running=0.3)
     st[np.random.default_rng(G).random(n) < 0.05] = O.DONE
-    _check(x, y, s, st, m, m, G)
+    s[st == O.DONE] = 1000
+    _round_vs_oracle(x, y, s, st, m, m, G)
 
 
 @pytest.mark.parametrize("G", [2, 8, 16])
 def test_banded_large_spread_multihop(G):
-    """Spread ~60 steps -> halo radius > slab height for G=16 (multi-hop halo)."""
+    """Spread ~60 steps: the window reaches past the neighbouring slabs for G = 16."""
     n, w = 10000, 1500
     x, y, s, st = amgen.banded_state(n, w, 480, 3, p_running=0.3)
-    # rotate so that the step gradient runs across the slabs (bands along y)
-    x, y = y.copy(), x.copy()
-    _check(x, y, s, st, 480, w, G)
+    x, y = y.copy(), x.copy()          # the step gradient across the slabs
+    _round_vs_oracle(x, y, s, st, 480, w, G)
 
 
 def test_linf_and_coupled_chain_across_all_slabs():
@@ -76,6 +80,82 @@ def test_linf_and_coupled_chain_across_all_slabs():
     s = np.zeros(len(ys), np.int32)
     st = np.zeros(len(ys), np.uint8)
     st[len(ys) // 2] = O.RUNNING        # poisons the whole chain
-    mask, label, _ = _run(x, ys, s, st, 64, H, G)
-    assert np.all(label == 0) and mask.sum() == 0
-    _check(x, ys, s, st, 64, H, G, metric="linf")
+    _round_vs_oracle(x, ys, s, st, 64, H, G)
+    _round_vs_oracle(x, ys, s, st, 64, H, G, metric="linf")
+
+
+def _oracle_logs(r):
+    logs, k = [], 0
+    for nr in r["log_nready"]:
+        if nr:
+            logs.append((r["log_id"][k:k + nr], r["log_label"][k:k + nr]))
+        k += nr
+    return logs
+
+
+def _replay_logged(wd, max_rounds=10**6):
+    logs = []
+    for k in range(max_rounds):
+        log = []
+        wd.round(log)
+        ids, lab = slabs.merged_order(log[0])
+        if len(ids):
+            logs.append((ids, lab))
+        if (k + 1) % wd.K == 0 and wd.check():
+            break
+    return logs
+
+
+@pytest.mark.parametrize("name,steps,n,G", [
+    ("C1", 300, None, 2), ("C1", 300, None, 4),
+    ("C2", 25, None, 2), ("C2", 25, None, 4), ("C2", 25, None, 8),
+    ("C4", 12, 2000, 2), ("C4", 12, 2000, 8),
+])
+def test_slab_replay_round_logs_vs_oracle(name, steps, n, G):
+    w = amgen.config(name, steps=steps, n=n)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps)
+    r = O.replay(p, sy, w.x, w.y, Q=w.Q, log_rounds=10**6, log_entries=len(w.x) * w.steps + 10)
+    assert r["log_complete"]
+    wd = _world(w, lm, G, check_rounds=4)
+    glogs = _replay_logged(wd)
+    ologs = _oracle_logs(r)
+    assert len(glogs) == len(ologs), (len(glogs), len(ologs))
+    for k, ((gi, gl), (oi, ol)) in enumerate(zip(glogs, ologs)):
+        np.testing.assert_array_equal(gi, oi, err_msg=f"round {k}")
+        np.testing.assert_array_equal(gl, ol, err_msg=f"round {k}")
+    res = wd.results()
+    np.testing.assert_array_equal(res["x"], r["x"])
+    np.testing.assert_array_equal(res["y"], r["y"])
+    np.testing.assert_array_equal(res["traj"], r["traj"])
+    assert res["T_ooo"] == int(r["T_ooo"][0])
+    assert res["rounds"] == int(r["rounds"][0])
+    assert res["dispatched"] == len(w.x) * w.steps
+    assert np.all(res["steps"] == w.steps)
+    wd.close()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_slab_replay_c4_shape_final_state_vs_lockstep(G):
+    """20k agents at C4 density over 120 steps (re-windows as the spread grows, agents
+    migrate across slab edges): the final state equals the oracle's lock-step run
+    and the single-GPU replay's completion time and round count."""
+    from paper_2411_03519_b200 import Replay
+    w = amgen.config("C4", steps=120, n=20000)
+    lm = amgen.latency_model(w.profile)
+    wd = _world(w, lm, G, check_rounds=8)
+    wd.run(10**6)
+    res = wd.results()
+    assert wd.rewindows >= 1
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, w.steps)
+    ls = O.lockstep_grid(p, O.SynthTables.from_model(lm), w.x, w.y, w.steps)
+    np.testing.assert_array_equal(res["x"], ls["x"])
+    np.testing.assert_array_equal(res["y"], ls["y"])
+    np.testing.assert_array_equal(res["traj"], ls["traj"])
+    one = Replay.from_workload(w, lm)
+    one.run_to_end(chunk=512)
+    r1 = one.results()
+    assert res["T_ooo"] == int(r1["T_ooo"][0]) and res["rounds"] == int(r1["rounds"][0])
+    one.close()
+    wd.close()

@@ -1,6 +1,8 @@
-"""The multi-GPU exchange layer (slabs.round_distributed's collectives) on CPU with
-gloo, world size 2: the variable-size all-gather and the counts-then-payload
-all-to-all deliver exactly the records the slab kernels would send."""
+"""The multi-GPU exchange layer on CPU with gloo, world size 2: the three collectives of
+a distributed round (slabs.DistWorld) on fixed-capacity buffers whose counts travel
+inside them -- all-gather of merge buffers, all-reduce MIN of the int64 stats, equal-split
+all-to-all of delta blocks -- deliver exactly what the slab kernels expect, through the
+host-staged wrapper the multi-process GPU test uses (slabs.HostStagedDist)."""
 import os
 import socket
 
@@ -25,26 +27,32 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        dev = torch.device("cpu")
-        # variable all-gather of link records: rank k contributes k+1 pairs
-        t = torch.arange(2 * (rank + 1), dtype=torch.int32).reshape(-1, 2) + 100 * rank
-        g = slabs._all_gather_var(dist, t, world, dev)
-        exp = torch.cat([torch.arange(2 * (k + 1), dtype=torch.int32).reshape(-1, 2) + 100 * k
-                         for k in range(world)])
-        ok1 = torch.equal(g, exp)
-        # counts then payload (halo records): rank k sends k+2 records to every other rank
-        out = [torch.full((0 if j == rank else rank + 2, 4), rank, dtype=torch.int32) for j in range(world)]
-        sc = torch.tensor([int(o.shape[0]) for o in out], dtype=torch.int64)
-        rc = torch.empty_like(sc)
-        dist.all_to_all_single(rc, sc)
-        recv = torch.empty((int(rc.sum()), 4), dtype=torch.int32)
-        dist.all_to_all_single(recv, torch.cat(out), output_split_sizes=rc.tolist(),
-                               input_split_sizes=sc.tolist())
-        exp2 = torch.cat([torch.full((0 if j == rank else j + 2, 4), j, dtype=torch.int32) for j in range(world)])
-        ok2 = torch.equal(recv, exp2)
-        ws = torch.tensor([5 + rank, -(10 + rank)], dtype=torch.int32)
-        dist.all_reduce(ws, op=dist.ReduceOp.MIN)
-        ok3 = ws.tolist() == [5, -(10 + world - 1)]
+        hd = slabs.HostStagedDist(dist)
+        # merge buffers: [count links, count clusters, 0, 0, records ...] per rank
+        cap = 4
+        mb = torch.zeros(4 + 6 * cap, dtype=torch.int32)
+        mb[0] = rank + 1
+        mb[4:4 + 2 * (rank + 1)] = torch.arange(2 * (rank + 1), dtype=torch.int32) + 100 * rank
+        mall = torch.empty((world, 4 + 6 * cap), dtype=torch.int32)
+        hd.all_gather_into_tensor(mall.view(-1), mb)
+        ok1 = all(int(mall[r, 0]) == r + 1 and
+                  torch.equal(mall[r, 4:4 + 2 * (r + 1)], torch.arange(2 * (r + 1), dtype=torch.int32) + 100 * r)
+                  for r in range(world))
+        # stats: int64 MIN (next event, W, -S, inactive)
+        st = torch.tensor([1000 + rank, 5 + rank, -(10 + rank), 1 - rank], dtype=torch.int64)
+        hd.all_reduce(st, op=dist.ReduceOp.MIN)
+        ok2 = st.tolist() == [1000, 5, -(10 + world - 1), 0]
+        # delta blocks: block j of rank r goes to rank j; header = record count
+        capp = 3
+        ds = torch.zeros((world, 6 + 6 * capp), dtype=torch.int32)
+        for j in range(world):
+            if j != rank:
+                ds[j, 0] = rank + 1
+                ds[j, 6] = 1000 * rank + j
+        dr = torch.empty_like(ds)
+        hd.all_to_all_single(dr, ds)
+        ok3 = all((int(dr[r, 0]) == (r + 1 if r != rank else 0)) and
+                  (r == rank or int(dr[r, 6]) == 1000 * r + rank) for r in range(world))
         q.put((rank, ok1, ok2, ok3))
     finally:
         dist.destroy_process_group()
@@ -64,8 +72,11 @@ def test_gloo_world2_exchange():
         assert ok1 and ok2 and ok3, (rank, ok1, ok2, ok3)
 
 
-def test_partition_rows():
+def test_partition_rows_and_halo():
     rows = slabs.slab_of_rows(100, 3)
     assert rows == [(0, 33), (33, 66), (66, 100)]
     y = torch.tensor([0, 32, 33, 65, 66, 99])
     assert slabs.partition(y, 100, 3).tolist() == [0, 0, 1, 1, 2, 2]
+    # R_b(spread + 1) + (K + 1) v  (P:406 plus K rounds of growth at one step per round)
+    assert slabs.halo_needed(0, 4, 1, 16) == (0 + 2) * 1 + 4 + 17
+    assert slabs.halo_needed(80, 4, 1, 16) == 82 + 4 + 17
