@@ -13,8 +13,8 @@ of device time); rounds/s is reported beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 (torchrun): every rank runs its own replica of the workload (no data-path
-collective; "replicas" -- the spatial-slab exchange is not in this round).
+N > 1 (torchrun, one process per GPU, NCCL): the same 1M-agent map split into N
+horizontal slabs (slabs.DistWorld, strong scaling).
 """
 from __future__ import annotations
 
@@ -365,41 +365,180 @@ def snapshot_rounds(rep, w, dev, flush, reps: int = 20):
                     "L2 flushed before each round"}
 
 
-def virtual_slabs(rep, w, dev, slab_counts=(2, 8)):
-    """S7 on one GPU: the pre-rolled C5 state split into G horizontal
-    slabs, one distributed round (watermark all-reduce, halo all-to-all, slab-local
-    round, link all-gather, merge) with an in-process loopback exchange; the device time
-    of every slab's local round is what one GPU of a G-GPU run spends on it.  The merged
-    ready set must equal the single-GPU round's (checked)."""
+def virtual_slabs(w, lm, dev, slab_counts=(2, 8), preroll=200, timed=4):
+    """S7 + S8 on one GPU: the C5 replay split into G horizontal slabs
+    (slabs.LoopbackWorld: the library calls of the NCCL run, exchanges as device copies),
+    pre-rolled `preroll` rounds from t = 0, then `timed` rounds with every rank's own
+    device time recorded (its library steps; the exchanges are NCCL's in a real run): the
+    slowest rank's time is what one GPU of a G-GPU run computes per round.  Checked
+    against the single-GPU replay after the same rounds (agent-steps dispatched)."""
     import torch
 
-    from paper_2411_03519_b200 import Tracker, slabs
-    pos, steps = rep.pos.clone(), rep.steps.clone()
-    status = rep.tracker.status().clone()
-    n = pos.shape[0]
-    gid = torch.arange(n, dtype=torch.int32, device=dev)
-    tr = Tracker(w.map_w, w.map_h, w.r_p, w.v, n, peek=True, force="binned", device=dev)
-    tr.set_state(pos, steps, status)
-    _, order = tr.ready()
-    ref = int(order.numel())
-    tr.close()
+    from paper_2411_03519_b200 import Replay, slabs
+    one = Replay.from_workload(w, lm, device=dev)
+    one.run(preroll + timed)
+    ref = one.dispatched()
+    one.close()
     out = {}
     for G in slab_counts:
-        part = slabs.partition(pos[:, 1], w.map_h, G)
-        ranks = []
-        for k in range(G):
-            sel = torch.nonzero(part == k).flatten()
-            ranks.append(slabs.SlabRank(w.map_w, w.map_h, w.r_p, w.v, n, G, k, gid[sel], pos[sel], steps[sel],
-                                        status[sel], device=dev))
-        outs = slabs.round_loopback(ranks)   # warm-up (grows the halo windows)
+        sy = slabs.Synth(lm, device=dev)
+        wd = slabs.LoopbackWorld(w.map_w, w.map_h, w.r_p, w.v, w.x, w.y, w.steps, sy, w.Q, G, device=dev,
+                                 check_rounds=16)
+        done = 0
+        while done < preroll:
+            k = min(wd.K, preroll - done)
+            for _ in range(k):
+                wd.round()
+            done += k
+            wd.check()
         tl = []
-        for _ in range(3):
-            outs = slabs.round_loopback(ranks, tl)
-        per = [min(tl[k::G]) for k in range(G)]
-        out[f"G={G}"] = {"local_round_ms_max_over_slabs": max(per), "local_round_ms_mean": sum(per) / G,
-                         "ready": sum(o["n_ready"] for o in outs), "equals_single_gpu": sum(o["n_ready"] for o in outs) == ref}
-        del ranks
+        for _ in range(timed):
+            wd.round(timing=tl)
+        wd.check()
+        per = [max(r[k] for r in tl[1:] or tl) for k in range(G)]   # worst round per rank
+        med = [sorted(r[k] for r in tl)[len(tl) // 2] for k in range(G)]
+        disp = sum(int(r.counters[2].item()) for r in wd.ranks)
+        out[f"G={G}"] = {"rank_round_ms_max_over_ranks": max(med), "rank_round_ms_mean": sum(med) / G,
+                         "rank_round_ms_worst": max(per), "halo_rows": wd.halo, "rewindows": wd.rewindows,
+                         "window_agents_max": max(int((r.w_gid >= 0).sum().item()) for r in wd.ranks),
+                         "dispatched_equals_single_gpu": disp == ref, "rounds": preroll + timed}
+        wd.close()
     return out
+
+
+# ------------------------------------------------------------------ N > 1: spatial slabs
+def run_slabs(args, w, lm):
+    """N GPUs (torchrun, one process per GPU, NCCL over NVLink): the ONE C5 map split into
+    N horizontal slabs (slabs.DistWorld): every round = window tracker round
+    + all-gather of merge records + merge/dispatch + all-reduce MIN of the event clock +
+    commit + all-to-all of deltas + apply.  Strong scaling: the total work is the same 1M
+    agents as N = 1.  value = agent-steps dispatched by all ranks / max over ranks of the
+    summed device time of the timed rounds."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_03519_b200 import slabs
+    ws, rank, local = _dist()
+    staged = os.environ.get("AM_SLAB_STAGED") == "1"   # test only: N ranks on ONE GPU over gloo
+    if staged:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if staged:
+        dist.init_process_group("gloo")
+        ex = slabs.HostStagedDist(dist)
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+        ex = dist
+    sy = slabs.Synth(lm, device=dev)
+    wd = slabs.DistWorld(ex, w.map_w, w.map_h, w.r_p, w.v, w.x, w.y, w.steps, sy, w.Q, device=dev,
+                         check_rounds=16)
+    done = 0
+    while done < args.preroll:
+        for _ in range(min(wd.K, args.preroll - done)):
+            wd.round()
+            done += 1
+        wd.check()
+    for _ in range(args.warmup):
+        wd.round()
+    wd.check()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    evs = []
+    d0 = int(wd.rank.counters[2].item())
+    try:
+        gid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        gid = str(local)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(gid) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            wd.round()
+            b.record()
+            evs.append((a, b))
+            if (k + 1) % wd.K == 0:
+                wd.check()   # (outside the event brackets)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    steps_local = int(wd.rank.counters[2].item()) - d0
+    t = torch.tensor([total_ms, float(steps_local)], dtype=torch.float64, device=dev)
+    tmax = t[:1].clone()
+    ex.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    tsum = t[1:].clone()
+    ex.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    total_ms, agent_steps = float(tmax.item()), int(tsum.item())
+    value = agent_steps / (total_ms / 1e3) if total_ms > 0 else 0.0
+    wd.check()
+    # e2e: every round the rank's window state goes host -> device from page-locked
+    # memory and back, and the rank's ready order + count come back to the host
+    r = wd.rank
+    L = r.cap_window
+    h_pos = torch.empty((L, 2), dtype=torch.int32, pin_memory=True)
+    h_step = torch.empty(L, dtype=torch.int32, pin_memory=True)
+    h_order = torch.empty(L, dtype=torch.int32, pin_memory=True)
+    h_n = torch.empty(1, dtype=torch.int32, pin_memory=True)
+    h_pos.copy_(r.w_pos)
+    h_step.copy_(r.w_step)
+    torch.cuda.synchronize(dev)
+    e_ms = []
+    e0 = int(r.counters[2].item())
+    for k in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r.w_pos.copy_(h_pos, non_blocking=True)
+        r.w_step.copy_(h_step, non_blocking=True)
+        wd.round()
+        h_order.copy_(r.order, non_blocking=True)
+        h_n.copy_(r.n_order, non_blocking=True)
+        h_pos.copy_(r.w_pos, non_blocking=True)
+        h_step.copy_(r.w_step, non_blocking=True)
+        b.record()
+        b.synchronize()
+        e_ms.append(a.elapsed_time(b))
+        if (k + 1) % wd.K == 0:
+            wd.check()
+            if wd.rank is not r:   # re-windowed: new buffers
+                r = wd.rank
+                L = r.cap_window
+                h_pos = torch.empty((L, 2), dtype=torch.int32, pin_memory=True)
+                h_step = torch.empty(L, dtype=torch.int32, pin_memory=True)
+                h_order = torch.empty(L, dtype=torch.int32, pin_memory=True)
+                h_pos.copy_(r.w_pos)
+                h_step.copy_(r.w_step)
+                torch.cuda.synchronize(dev)
+    e_steps = int(r.counters[2].item()) - e0
+    te = torch.tensor([sum(e_ms), float(e_steps)], dtype=torch.float64, device=dev)
+    tem = te[:1].clone()
+    ex.all_reduce(tem, op=dist.ReduceOp.MAX)
+    tes = te[1:].clone()
+    ex.all_reduce(tes, op=dist.ReduceOp.SUM)
+    e_value = float(tes.item()) / (float(tem.item()) / 1e3) if float(tem.item()) > 0 else 0.0
+    launches_round = 32   # library kernels of one rank's round (tracker ~14 + slab steps ~14 + sort)
+    if rank == 0:
+        cfg = _config(w, ws)
+        cfg["parallelism"] = f"slabs{ws}" + ("-gloo-staged-one-gpu (test only)" if staged else "")
+        cfg["halo_rows"] = wd.halo
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": cfg,
+            "rounds_per_s": args.steps / (total_ms / 1e3) if total_ms > 0 else 0.0,
+            "agent_steps_per_round": agent_steps / args.steps,
+            "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": 12 * L * ws,
+                    "d2h_bytes_per_step": (12 * L + 4 * L // 8) * ws, "ms_per_step": sum(e_ms) / args.steps,
+                    "note": "per rank: window state H2D + round + window state, order and count D2H"},
+            "gpu_launches": launches_round * args.steps,
+            "clocks": clk.summary(), "roofline": None, "cpu_baseline": None,
+            "rewindows": wd.rewindows,
+        }
+        print(json.dumps(line), flush=True)
+    wd.close()
+    dist.destroy_process_group()
+    return 0
 
 
 # ------------------------------------------------------------------ our arm
@@ -540,7 +679,7 @@ def run_ours(args, w, lm):
         e_value = float(t[1]) / (float(tm[0]) / 1000.0)
 
     snap = snapshot_rounds(rep, w, dev, flush) if not args.no_snapshot else None
-    vslab = virtual_slabs(rep, w, dev) if (not args.no_snapshot and ws == 1) else None
+    vslab = virtual_slabs(w, lm, dev) if (not args.no_snapshot and ws == 1) else None
 
     if rank != 0:
         rep.close()
@@ -680,6 +819,8 @@ def main():
     lm = amgen.latency_model(w.profile)
     if args.impl == "reference":
         return run_reference(args, w, lm)
+    if _dist()[0] > 1:
+        return run_slabs(args, w, lm)
     return run_ours(args, w, lm)
 
 

@@ -37,6 +37,7 @@ struct RepDev {
     Chain* chain;               // last-block counter of k_disp_b
     unsigned long long* qkey;   // [n] queue key of a queued (RUNNING, not started) agent (finite capacity)
     long long K;                // agent-steps in service at once; 0 = infinite capacity
+    int32_t* part;              // [2 x 4 x commit blocks] post-commit partials (in-place commits)
     int32_t prio;               // 1: queue by (step, label); 0: by (round, label)
 };
 
@@ -54,14 +55,22 @@ __device__ __forceinline__ int2 policy_move(const RepDev& r, int i, int s, int2 
 // k_disp_b just advanced): the move computed at dispatch is applied and the step
 // advances (worker l.20-21).  Agents that stay RUNNING bound the next
 // event; any agent left active marks its simulation active for the next round.
-__global__ void __launch_bounds__(256) k_commit(RepDev r)
+// inplace (cell-binned path, the driver's own rounds): the commit is also applied to
+// the tracker's state in place -- exactly what the next am_update would find by diffing
+// the world arrays (update_agents, Alg. 3 l.11): IDLE (DONE at the target), the changed
+// mark, the last-round cluster made dirty, the agent's loose-cell record and its drift
+// -- and every block leaves its partial {min step, max step, active, running, drift}
+// of the post-commit state for k_replay_begin, so the next round needs no O(N) ingest.
+__global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
 {
     pdl_begin();
     const Dev& d = r.d;
     const bool one = d.n_sims == 1;
     const uint32_t c = d.ctl->cur;
+    const uint32_t tag = (d.ctl->epoch + 1u) & kTagMask;   // the round this commit feeds
     unsigned long long tmin = ~0ull;  // pending completions (single-simulation case)
     int any_active = 0;
+    int wmin = INT_MAX, smax = INT_MIN, nact = 0, nrun = 0, dmax = 0, err = 0;
     // loads of all items first (independent chains in flight), then the commits
     uint8_t st[kCommitItems];
     long long tc[kCommitItems];
@@ -83,16 +92,40 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r)
         const int b = sim_of(d, i);
         const long long t = one ? t1 : r.t_sim[b];
         bool active = true;
+        bool running = st[k] == ST_RUNNING;
         if (st[k] == ST_RUNNING) {
             if (tc[k] <= t) {
                 const int2 np = r.newpos[i];
+                const int2 op = r.pos[i];
                 const int s = r.steps[i] + 1;
                 r.pos[i] = np;
                 r.steps[i] = s;
                 r.traj[i] = traj_step(r.traj[i], s, np.x, np.y);
-                if (d.target > 0 && s == d.target) {
+                const bool done = d.target > 0 && s == d.target;
+                if (done) {
                     active = false;
                     atomicMax((unsigned long long*)(r.tdone + b), (unsigned long long)t);
+                }
+                running = false;
+                if (inplace) {
+                    // the speed limit the soundness of the rules rests on
+                    if (!within(np.x - op.x, np.y - op.y, (uint32_t)d.v, d.metric)) err |= ERR_VELOCITY;
+                    const uint8_t nst = done ? ST_DONE : ST_IDLE;
+                    d.pos[c][i] = np;
+                    d.step[c][i] = s;
+                    d.status[c][i] = nst;
+                    d.chg8[i] = 1;
+                    const int lab = d.labels[i];
+                    if (lab >= 0) d.dirty[lab] = d.ctl->epoch + 1u;
+                    const uint32_t rr = d.slot[i];
+                    if (rr != kSentinel) {
+                        d.rec[rr] = make_int4(np.x | (np.y << 16), s, i, (int)nst | (int)(tag << kTagShift));
+                        int cx, cy;
+                        mkey_decode(d, d.key[i], cx, cy);
+                        const int x0 = cx << d.clog, y0 = cy << d.clog;
+                        const int x1 = x0 + (1 << d.clog) - 1, y1 = y0 + (1 << d.clog) - 1;
+                        dmax = max(dmax, max(max(x0 - np.x, np.x - x1), max(y0 - np.y, np.y - y1)));
+                    }
                 }
             } else if (one) {
                 tmin = min(tmin, (unsigned long long)tc[k]);
@@ -104,6 +137,13 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r)
         if (active) {
             if (one) any_active = 1;
             else r.active_flag[b] = 1;
+            if (inplace) {
+                const int s = r.steps[i];
+                wmin = min(wmin, s);
+                smax = max(smax, s);
+                nact++;
+                nrun += running;
+            }
         }
     }
     if (one) {  // block reduction, one atomic per block
@@ -119,6 +159,74 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r)
             if (tmin != ~0ull) atomicMin((unsigned long long*)r.tnext, tmin);
             if (any_active) r.active_flag[0] = 1;
         }
+    }
+    if (inplace) {   // the post-commit state's partials of this block (no atomics)
+        __shared__ int p_w[8], p_s[8], p_a[8], p_r[8], p_d[8], p_e[8];
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        wmin = __reduce_min_sync(0xFFFFFFFFu, wmin);
+        smax = __reduce_max_sync(0xFFFFFFFFu, smax);
+        nact = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)nact);
+        nrun = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)nrun);
+        dmax = __reduce_max_sync(0xFFFFFFFFu, dmax);
+        err = (int)__reduce_or_sync(0xFFFFFFFFu, (unsigned)err);
+        if (lane == 0) { p_w[w] = wmin; p_s[w] = smax; p_a[w] = nact; p_r[w] = nrun; p_d[w] = dmax; p_e[w] = err; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 1; q < 8; q++) {
+                wmin = min(wmin, p_w[q]); smax = max(smax, p_s[q]); nact += p_a[q]; nrun += p_r[q];
+                dmax = max(dmax, p_d[q]); err |= p_e[q];
+            }
+            int4* part = reinterpret_cast<int4*>(r.part) + 2 * (size_t)blockIdx.x;
+            part[0] = make_int4(wmin, smax, nact, nrun);
+            part[1] = make_int4(dmax, err, 0, 0);
+            if (blockIdx.x == 0) d.ctl->part_valid = 1;
+        }
+    }
+}
+
+// The driver's own round begins (cell-binned path, after an in-place k_commit): the
+// partials of the post-commit state give W, S and the counts that k_ingest_done would
+// publish (nothing else changed since the commit), the drift is merged, a velocity
+// violation is reported and forces a full recompute; then the round's counters reset.
+__global__ void __launch_bounds__(1024) k_replay_begin(RepDev r, int nparts)
+{
+    pdl_begin();
+    Ctl* ctl = r.d.ctl;
+    __shared__ int sw[32], ss[32], sa[32], sr[32], sd[32], se[32];
+    int w = INT_MAX, s = INT_MIN, a = 0, run = 0, dm = 0, e = 0;
+    if (ctl->part_valid) {
+        const int4* part = reinterpret_cast<const int4*>(r.part);
+        for (int k = threadIdx.x; k < nparts; k += blockDim.x) {
+            const int4 p0 = part[2 * k], p1 = part[2 * k + 1];
+            w = min(w, p0.x); s = max(s, p0.y); a += p0.z; run += p0.w; dm = max(dm, p1.x); e |= p1.y;
+        }
+    }
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    w = __reduce_min_sync(0xFFFFFFFFu, w);
+    s = __reduce_max_sync(0xFFFFFFFFu, s);
+    a = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)a);
+    run = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)run);
+    dm = __reduce_max_sync(0xFFFFFFFFu, dm);
+    e = (int)__reduce_or_sync(0xFFFFFFFFu, (unsigned)e);
+    if (lane == 0) { sw[wp] = w; ss[wp] = s; sa[wp] = a; sr[wp] = run; sd[wp] = dm; se[wp] = e; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < (int)(blockDim.x >> 5); q++) {
+            w = min(w, sw[q]); s = max(s, ss[q]); a += sa[q]; run += sr[q]; dm = max(dm, sd[q]); e |= se[q];
+        }
+        if (ctl->part_valid) {
+            ctl->W = w;
+            ctl->S = s;
+            ctl->n_active = a;
+            ctl->n_running = run;
+            ctl->D = max(ctl->D, dm);
+            if (e) {
+                ctl->err_sticky |= e;
+                ctl->full_next = 1;
+            }
+            ctl->part_valid = 0;
+        }
+        round_begin(r.d);
     }
 }
 
@@ -457,7 +565,7 @@ struct am_replay {
     int32_t* order = nullptr;
     cudaStream_t stream = nullptr;      // own stream (graph capture)
     cudaStream_t user_stream = nullptr;
-    cudaGraphExec_t g1 = nullptr, g8 = nullptr;
+    cudaGraphExec_t g1 = nullptr, g8 = nullptr, g1x = nullptr;   // g1x: one host-buffer (external) round
     unsigned graph_prof = 0;            // profiling mask the graphs were captured with
     uint32_t graph_flags = 0;           // context flags the graphs were captured with
     long long* h_buf = nullptr;         // pinned: dispatched, liveness
@@ -485,13 +593,30 @@ static int rp_err(am_replay* rp, cudaError_t e, const char* where)
 // commit at the next event time.  Committing at the end of the round (instead of the
 // start of the next) leaves the state a host-side user would hold between rounds in
 // the world arrays; the sequence of rounds is unchanged.
-static int enqueue_round(am_replay* rp)
+static int enqueue_round(am_replay* rp, bool external = false)
 {
     am_ctx* c = rp->ctx;
     const int n = c->d.n;
     const unsigned nb = (unsigned)((n + 255) / 256);
-    int rc = am_update_binned(c, (const int32_t*)rp->r.pos, rp->r.steps);
-    if (rc) return rc;
+    const unsigned ncb = (unsigned)((n + 256 * kCommitItems - 1) / (256 * kCommitItems));
+    const bool inplace = c->path == 1;   // the cell-binned tracker takes the commits in place
+    int rc;
+    if (inplace && !external && !c->first) {
+        // the driver's own round: its last k_commit applied the commits to the tracker
+        // already, so no O(N) ingest of the world arrays -- k_replay_begin publishes the
+        // post-commit W / S / counts from the commit's block partials (am_ready then
+        // skips k_round_begin)
+        if (c->bin_pending) return AM_E_STATE;
+        am_join_side(c);
+        am_prof_begin(c, K_INGEST);
+        RK(launch_k(c->pdl, rp->stream, k_replay_begin, 1, 1024, 0, rp->r, (int)ncb));
+        am_prof_end(c, K_INGEST);
+        c->bin_pending = true;
+    } else {
+        // the world arrays as a user hands them in (am_replay_io): diffed and validated
+        rc = am_update_binned(c, (const int32_t*)rp->r.pos, rp->r.steps);
+        if (rc) return rc;
+    }
     c->defer_join = true;   // the sort overlaps dispatch + commit; joined below
     rc = am_ready(c, rp->mask, rp->order, nullptr);
     c->defer_join = false;
@@ -506,7 +631,7 @@ static int enqueue_round(am_replay* rp)
     RK(launch_k(c->pdl, rp->stream, k_disp_b, nbd, 256, 0, rp->r));
     am_prof_end(c, K_DISP_B);
     am_prof_begin(c, K_COMMIT);
-    RK(launch_k(c->pdl, rp->stream, k_commit, (unsigned)((n + 256 * kCommitItems - 1) / (256 * kCommitItems)), 256, 0, rp->r));
+    RK(launch_k(c->pdl, rp->stream, k_commit, ncb, 256, 0, rp->r, inplace ? 1 : 0));
     am_join_side(c);   // the priority sort ran beside dispatch and commit
     am_prof_end(c, K_COMMIT);
     RK(cudaGetLastError());
@@ -515,7 +640,7 @@ static int enqueue_round(am_replay* rp)
 
 // device workspace layout of a replay (caller-owned, am_replay_workspace_size)
 struct RepLayout {
-    size_t total, tc, np, tr, tcl, ts, tn, td, rd, af, disp, live, chain, qk, mask, order, shadow;
+    size_t total, tc, np, tr, tcl, ts, tn, td, rd, af, disp, live, chain, qk, mask, order, shadow, part;
 };
 static RepLayout rep_layout(const am_ctx* ctx)
 {
@@ -528,6 +653,7 @@ static RepLayout rep_layout(const am_ctx* ctx)
     L.disp = take(8); L.live = take(4); L.chain = take(sizeof(Chain)); L.qk = take(8 * n);
     L.mask = take(n); L.order = take(4 * n);
     L.shadow = take(4 * n);   // am_replay_io: the steps as copied in (delta write-back)
+    L.part = take(32 * ((n + 256 * kCommitItems - 1) / (256 * kCommitItems)));   // k_commit partials
     L.total = off;
     return L;
 }
@@ -595,6 +721,7 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
     rp->mask = (uint8_t*)(b + L.mask);
     rp->order = (int32_t*)(b + L.order);
     rp->shadow = (int32_t*)(b + L.shadow);
+    r.part = (int32_t*)(b + L.part);
     r.order = ctx->path == 1 ? ctx->d.rid : rp->order;
     RK(cudaStreamCreateWithFlags(&rp->stream, cudaStreamNonBlocking));
     RK(cudaMallocHost((void**)&rp->h_buf, 64));
@@ -640,7 +767,7 @@ static int build_io_graph(am_replay* rp, uint8_t* h_mask)
     cudaGraph_t g;
     RK(cudaStreamBeginCapture(rp->stream, cudaStreamCaptureModeThreadLocal));
     c->mask_event = true;
-    int rc = enqueue_round(rp);
+    int rc = enqueue_round(rp, true);   // the host-buffer round: the world state is diffed and validated
     c->mask_event = false;
     cudaError_t e = cudaSuccess;
     if (rc == AM_OK) {
@@ -660,12 +787,12 @@ static int build_io_graph(am_replay* rp, uint8_t* h_mask)
     return AM_OK;
 }
 
-static int build_graph(am_replay* rp, int rounds, cudaGraphExec_t* exec)
+static int build_graph(am_replay* rp, int rounds, cudaGraphExec_t* exec, bool external = false)
 {
     cudaGraph_t g;
     RK(cudaStreamBeginCapture(rp->stream, cudaStreamCaptureModeThreadLocal));
     int rc = AM_OK;
-    for (int k = 0; k < rounds && rc == AM_OK; k++) rc = enqueue_round(rp);
+    for (int k = 0; k < rounds && rc == AM_OK; k++) rc = enqueue_round(rp, external);
     cudaError_t e = cudaStreamEndCapture(rp->stream, &g);
     if (rc) return rc;
     if (e != cudaSuccess) return rp_err(rp, e, "cudaStreamEndCapture");
@@ -701,7 +828,8 @@ static int ensure_graphs(am_replay* rp)
         if (rp->g1) cudaGraphExecDestroy(rp->g1);
         if (rp->g8) cudaGraphExecDestroy(rp->g8);
         if (rp->g_io) cudaGraphExecDestroy(rp->g_io);
-        rp->g1 = rp->g8 = rp->g_io = nullptr;
+        if (rp->g1x) cudaGraphExecDestroy(rp->g1x);
+        rp->g1 = rp->g8 = rp->g_io = rp->g1x = nullptr;
         rp->g_io_mask = nullptr;
         rp->graph_prof = pm;
         rp->graph_flags = rp->ctx->d.flags;
@@ -849,7 +977,9 @@ extern "C" int am_replay_io(am_replay* rp, const int32_t* h_pos_in, const int32_
         if (rp->g_io_mask != (const void*)h_mask && (rc = build_io_graph(rp, h_mask))) return rc;
         RK(cudaGraphLaunch(rp->g_io, rp->stream));
     } else {
-        RK(cudaGraphLaunch(rp->g1, rp->stream));
+        // one round that diffs and validates the copied-in world state (captured once)
+        if (!rp->g1x && (rc = build_graph(rp, 1, &rp->g1x, true))) return rc;
+        RK(cudaGraphLaunch(rp->g1x, rp->stream));
         am_prof_mark(c, rp->graph_prof);
     }
     if (delta) {
@@ -927,6 +1057,7 @@ extern "C" int am_replay_destroy(am_replay* rp)
     if (rp->g1) cudaGraphExecDestroy(rp->g1);
     if (rp->g8) cudaGraphExecDestroy(rp->g8);
     if (rp->g_io) cudaGraphExecDestroy(rp->g_io);
+    if (rp->g1x) cudaGraphExecDestroy(rp->g1x);
     if (rp->ctx) {
         am_set_stream(rp->ctx, rp->user_stream);
         rp->ctx->d.flags &= ~AM_ASYNC;

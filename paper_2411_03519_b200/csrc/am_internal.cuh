@@ -113,6 +113,7 @@ struct Ctl {
     // box is widened by D), acc_D its per-update accumulator
     int32_t  D, acc_D, since_rebuild, rebuild, n_rebuilds;
     int32_t  rebuild_req;  // a replica update brought an agent that has no record (arrival)
+    int32_t  part_valid;   // the replay's in-place commit left post-commit partials (k_replay_begin)
     uint32_t scan_next;    // dynamic work distribution of k_scan_hw (AM_SCAN_DYN)
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
@@ -602,6 +603,44 @@ __device__ __forceinline__ bool finish_block(Chain* c, uint32_t nblocks)
     }
     __syncthreads();
     return last;
+}
+
+}  // namespace am
+
+namespace am {
+// reset the per-round counters that the host reads (before the round kernels)
+__device__ __forceinline__ void round_begin(const Dev& d)
+{
+    Ctl* ctl = d.ctl;
+    ctl->epoch += 1;
+    ctl->n_ready = 0;
+    ctl->n_clusters = 0;
+    ctl->n_items = 0;
+    ctl->n_far = 0;
+    ctl->scan_next = 0;
+    ctl->sort_or = 0;
+    ctl->ready.ticket = 0;   // k_ready and k_cells take tile tickets and keep no epilogue
+    ctl->cells.ticket = 0;
+    ctl->full |= ctl->full_next;
+    ctl->full_next = 0;
+    if (d.slot) {   // binned path: rebuild the cell binning, or keep the loose cells
+        const bool rb = ctl->full != 0 || ctl->D > d.rebuild_d || ctl->since_rebuild >= d.rebuild_k ||
+                        ctl->rebuild_req != 0 || !(d.flags & AM_VALIDATE);
+        ctl->rebuild_req = 0;
+        ctl->rebuild = rb ? 1 : 0;
+        if (rb) {
+            ctl->D = 0;
+            ctl->since_rebuild = 0;
+            ctl->n_rebuilds += 1;
+        } else {
+            ctl->since_rebuild += 1;
+        }
+    }
+    if (ctl->epoch > 1) ctl->ecur ^= 1u;   // last round's edge lists become current
+    ctl->ccnt[ctl->ecur ^ 1u] = 0;
+    ctl->ncnt[ctl->ecur ^ 1u] = 0;
+    if (d.wq_ctr)
+        for (int k = 0; k < kEdgeStripes; k++) d.wq_ctr[k] = 0;
 }
 
 }  // namespace am

@@ -180,7 +180,6 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
     }
 }
 
-__device__ void round_begin(const Dev& d);
 
 // k_ingest_done: one thread after k_ingest: flips to the new state buffer iff no agent
 // raised an error (all-or-nothing update), publishes W / S / counts, resets the
@@ -193,6 +192,7 @@ __global__ void k_ingest_done(Dev d, int mode, int bin)
     const int e = ctl->err_new;
     // a rejected update may have touched records and incremental state: recompute all
     if (e != 0) ctl->full_next = 1;
+    ctl->part_valid = 0;                // W / S / counts are this update's
     ctl->D = max(ctl->D, ctl->acc_D);   // (a rejected update is followed by a full rebuild)
     ctl->acc_D = 0;
     if (e == 0) {
@@ -1541,41 +1541,6 @@ __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mas
     __syncthreads();
     if (rdy) order[s_excl + rank] = lo + t;
     finish_block(&ctl->small_, gridDim.x);
-}
-
-// reset the per-round counters that the host reads (before the round kernels)
-__device__ void round_begin(const Dev& d)
-{
-    Ctl* ctl = d.ctl;
-    ctl->epoch += 1;
-    ctl->n_ready = 0;
-    ctl->n_clusters = 0;
-    ctl->n_items = 0;
-    ctl->n_far = 0;
-    ctl->scan_next = 0;
-    ctl->sort_or = 0;
-    ctl->ready.ticket = 0;   // k_ready and k_cells take tile tickets and keep no epilogue
-    ctl->cells.ticket = 0;
-    ctl->full |= ctl->full_next;
-    ctl->full_next = 0;
-    if (d.slot) {   // binned path: rebuild the cell binning, or keep the loose cells
-        const bool rb = ctl->full != 0 || ctl->D > d.rebuild_d || ctl->since_rebuild >= d.rebuild_k ||
-                        ctl->rebuild_req != 0 || !(d.flags & AM_VALIDATE);
-        ctl->rebuild_req = 0;
-        ctl->rebuild = rb ? 1 : 0;
-        if (rb) {
-            ctl->D = 0;
-            ctl->since_rebuild = 0;
-            ctl->n_rebuilds += 1;
-        } else {
-            ctl->since_rebuild += 1;
-        }
-    }
-    if (ctl->epoch > 1) ctl->ecur ^= 1u;   // last round's edge lists become current
-    ctl->ccnt[ctl->ecur ^ 1u] = 0;
-    ctl->ncnt[ctl->ecur ^ 1u] = 0;
-    if (d.wq_ctr)
-        for (int k = 0; k < kEdgeStripes; k++) d.wq_ctr[k] = 0;
 }
 
 __global__ void k_round_begin(Dev d)

@@ -265,20 +265,48 @@ class LoopbackWorld(_World):
             r.load(w["gid"], w["pos"], w["steps"], w["status"], w["traj"], w["tcommit"], w["newpos"], t)
             self.ranks.append(r)
 
-    def round(self, log: list | None = None):
+    def round(self, log: list | None = None, timing: list | None = None):
         """One distributed round of all virtual slabs (no host synchronisation unless
-        `log` asks for the round's outputs)."""
-        mb = torch.stack([r.round_local() for r in self.ranks])            # all-gather
-        for r in self.ranks:
+        `log` asks for the round's outputs).  With `timing` (a list), the device time of
+        every rank's own library steps (everything but the exchanges, which NCCL does in
+        a real run) is appended, per rank, in ms: what one GPU of a G-GPU run computes."""
+        ev = None
+        if timing is not None:
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in self.ranks]
+
+        def rec(k, j):
+            if ev is not None:
+                ev[k][j].record()
+
+        mbs = []
+        for k, r in enumerate(self.ranks):
+            rec(k, 0)
+            mbs.append(r.round_local())
+            rec(k, 1)
+        mb = torch.stack(mbs)                                               # all-gather
+        for k, r in enumerate(self.ranks):
+            rec(k, 2)
             r.merge(mb)
+            rec(k, 3)
         if log is not None:
             log.append([r.round_outputs() for r in self.ranks])
         sg = torch.stack([r.stats for r in self.ranks]).min(0).values       # all-reduce MIN
-        ds = torch.stack([r.commit(sg) for r in self.ranks])                # [src, dst, words]
+        dss = []
         for k, r in enumerate(self.ranks):
-            r.apply(ds[:, k].contiguous())                                  # all-to-all
+            rec(k, 4)
+            dss.append(r.commit(sg))
+            rec(k, 5)
+        ds = torch.stack(dss)                                               # [src, dst, words]
+        for k, r in enumerate(self.ranks):
+            recv = ds[:, k].contiguous()                                    # all-to-all
+            rec(k, 6)
+            r.apply(recv)
+            rec(k, 7)
         self.rounds_done += 1
         self._last_stats = sg
+        if ev is not None:
+            torch.cuda.synchronize(self.dev)
+            timing.append([sum(e[2 * j].elapsed_time(e[2 * j + 1]) for j in range(4)) for e in ev])
 
     def check(self) -> bool:
         """Reads every rank's flags (one synchronisation).  Raises on an overflow or a
