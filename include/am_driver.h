@@ -112,6 +112,19 @@ int am_replay_results(am_replay* r, int64_t* T_ooo, int64_t* rounds, uint64_t* t
  * already ran). */
 int am_replay_set_capacity(am_replay* r, int64_t capacity, int32_t priority);
 
+/* LLM busy time dispatched so far per simulation (host int64 [n_sims], microseconds):
+ * the sum over dispatched agent-steps of dur(i, s) - base_us (the time spent in LLM
+ * calls; calls of one agent-step are sequential, one outstanding request at a time).
+ * Divided by T_ooo it is the achieved parallelism of the paper's evaluation (average
+ * outstanding LLM requests over the execution time).  Synchronises. */
+int am_replay_llm_time(am_replay* r, int64_t* llm_us);
+
+/* The parallel-sync baseline (Algorithm 1's barrier per step): T_sync[b]
+ * = sum_{s < T} max_{i in simulation b} dur(i, s) for n agents in n_sims simulations
+ * under the synthetic latency model, computed on the device (host int64 [n_sims] out;
+ * temporary device memory from the stream-ordered allocator).  Synchronises. */
+int am_lockstep_time(const am_synth* synth, int32_t n, int32_t n_sims, int32_t T, int64_t* T_sync, void* stream);
+
 /* Total agent-steps dispatched so far (host). */
 int am_replay_dispatched(am_replay* r, int64_t* agent_steps);
 

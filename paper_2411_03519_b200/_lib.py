@@ -94,6 +94,8 @@ SIGNATURES = {
     "am_replay_step": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(_i32)]),
     "am_replay_results": (C.c_int, [_vp, _vp, _vp, _vp]),
     "am_replay_dispatched": (C.c_int, [_vp, C.POINTER(_i64)]),
+    "am_replay_llm_time": (C.c_int, [_vp, _vp]),
+    "am_lockstep_time": (C.c_int, [C.POINTER(Synth), _i32, _i32, _i32, _vp, _vp]),
     "am_replay_destroy": (C.c_int, [_vp]),
     "am_replay_stream": (_vp, [_vp]),
     "am_replay_set_capacity": (C.c_int, [_vp, C.c_int64, _i32]),

@@ -38,6 +38,7 @@ struct RepDev {
     unsigned long long* qkey;   // [n] queue key of a queued (RUNNING, not started) agent (finite capacity)
     long long K;                // agent-steps in service at once; 0 = infinite capacity
     int32_t* part;              // [2 x 4 x commit blocks] post-commit partials (in-place commits)
+    long long* llm;             // [S] LLM busy time dispatched so far: sum of (duration - base_us), us
     int32_t prio;               // 1: queue by (step, label); 0: by (round, label)
 };
 
@@ -59,8 +60,9 @@ __device__ __forceinline__ int2 policy_move(const RepDev& r, int i, int s, int2 
 // the tracker's state in place -- exactly what the next am_update would find by diffing
 // the world arrays (update_agents, Alg. 3 l.11): IDLE (DONE at the target), the changed
 // mark, the last-round cluster made dirty, the agent's loose-cell record and its drift
-// -- and every block leaves its partial {min step, max step, active, running, drift}
-// of the post-commit state for k_replay_begin, so the next round needs no O(N) ingest.
+// -- and every block adds its {min step, max step, active, running} of the post-commit
+// state to one of 64 reduction stripes for k_replay_begin, so the next round needs no
+// O(N) ingest.
 __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
 {
     pdl_begin();
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
             if (any_active) r.active_flag[0] = 1;
         }
     }
-    if (inplace) {   // the post-commit state's partials of this block (no atomics)
+    if (inplace) {   // the post-commit state's reduction: one atomic per quantity per block, 64 stripes
         __shared__ int p_w[8], p_s[8], p_a[8], p_r[8], p_d[8], p_e[8];
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         wmin = __reduce_min_sync(0xFFFFFFFFu, wmin);
@@ -176,55 +178,57 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
                 wmin = min(wmin, p_w[q]); smax = max(smax, p_s[q]); nact += p_a[q]; nrun += p_r[q];
                 dmax = max(dmax, p_d[q]); err |= p_e[q];
             }
-            int4* part = reinterpret_cast<int4*>(r.part) + 2 * (size_t)blockIdx.x;
-            part[0] = make_int4(wmin, smax, nact, nrun);
-            part[1] = make_int4(dmax, err, 0, 0);
+            int32_t* st = d.cstripe + 32 * (blockIdx.x & (kCommitStripes - 1));   // its own 128-byte line
+            if (wmin != INT_MAX) atomicMin(st, wmin);
+            if (smax != INT_MIN) atomicMax(st + 1, smax);
+            if (nact) atomicAdd(st + 2, nact);
+            if (nrun) atomicAdd(st + 3, nrun);
             if (blockIdx.x == 0) d.ctl->part_valid = 1;
+            // the drift and a velocity violation go to the accumulators both round starts
+            // merge (k_replay_begin, or k_ingest_done after a host-buffer ingest)
+            if (dmax > 0) atomicMax(&d.ctl->acc_D, dmax);
+            if (err) atomicOr(&d.ctl->err_new, err);
         }
     }
 }
 
 // The driver's own round begins (cell-binned path, after an in-place k_commit): the
-// partials of the post-commit state give W, S and the counts that k_ingest_done would
-// publish (nothing else changed since the commit), the drift is merged, a velocity
+// 64 reduction stripes of the post-commit state give W, S and the counts k_ingest_done
+// would publish (nothing else changed since the commit), the drift is merged, a velocity
 // violation is reported and forces a full recompute; then the round's counters reset.
-__global__ void __launch_bounds__(1024) k_replay_begin(RepDev r, int nparts)
+__global__ void __launch_bounds__(32) k_replay_begin(RepDev r, int nparts)
 {
     pdl_begin();
+    (void)nparts;
     Ctl* ctl = r.d.ctl;
-    __shared__ int sw[32], ss[32], sa[32], sr[32], sd[32], se[32];
-    int w = INT_MAX, s = INT_MIN, a = 0, run = 0, dm = 0, e = 0;
-    if (ctl->part_valid) {
-        const int4* part = reinterpret_cast<const int4*>(r.part);
-        for (int k = threadIdx.x; k < nparts; k += blockDim.x) {
-            const int4 p0 = part[2 * k], p1 = part[2 * k + 1];
-            w = min(w, p0.x); s = max(s, p0.y); a += p0.z; run += p0.w; dm = max(dm, p1.x); e |= p1.y;
-        }
+    const Dev& d = r.d;
+    // one warp reduces the 64 stripes (two per lane) and resets them
+    const int lane = threadIdx.x;
+    int w = INT_MAX, s = INT_MIN, a = 0, run = 0;
+    const bool valid = ctl->part_valid != 0;
+    for (int k = lane; k < kCommitStripes; k += 32) {
+        int32_t* c = d.cstripe + 32 * k;
+        w = min(w, c[0]); s = max(s, c[1]); a += c[2]; run += c[3];
+        c[0] = INT_MAX; c[1] = INT_MIN; c[2] = 0; c[3] = 0;
     }
-    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     w = __reduce_min_sync(0xFFFFFFFFu, w);
     s = __reduce_max_sync(0xFFFFFFFFu, s);
     a = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)a);
     run = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)run);
-    dm = __reduce_max_sync(0xFFFFFFFFu, dm);
-    e = (int)__reduce_or_sync(0xFFFFFFFFu, (unsigned)e);
-    if (lane == 0) { sw[wp] = w; ss[wp] = s; sa[wp] = a; sr[wp] = run; sd[wp] = dm; se[wp] = e; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int q = 1; q < (int)(blockDim.x >> 5); q++) {
-            w = min(w, sw[q]); s = max(s, ss[q]); a += sa[q]; run += sr[q]; dm = max(dm, sd[q]); e |= se[q];
-        }
-        if (ctl->part_valid) {
+    if (lane == 0) {
+        if (valid) {
             ctl->W = w;
             ctl->S = s;
             ctl->n_active = a;
             ctl->n_running = run;
-            ctl->D = max(ctl->D, dm);
-            if (e) {
-                ctl->err_sticky |= e;
-                ctl->full_next = 1;
-            }
             ctl->part_valid = 0;
+        }
+        ctl->D = max(ctl->D, ctl->acc_D);
+        ctl->acc_D = 0;
+        if (ctl->err_new) {   // a commit broke the speed limit: reported, full recompute next
+            ctl->err_sticky |= ctl->err_new;
+            ctl->full_next = 1;
+            ctl->err_new = 0;
         }
         round_begin(r.d);
     }
@@ -238,11 +242,19 @@ __global__ void __launch_bounds__(256) k_disp_a(RepDev r)
     const Dev& d = r.d;
     const int nr = d.ctl->n_ready;
     if (blockIdx.x == 0 && threadIdx.x == 0) *r.dispatched += nr;
+    unsigned long long busy = 0;   // LLM time of the dispatched agent-steps (one simulation)
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x) {
         const int i = r.order[k];
         const int b = sim_of(d, i);
-        const long long tc = r.t_sim[b] + duration(r.sy, i, r.steps[i]);
+        const long long du = duration(r.sy, i, r.steps[i]);
+        const long long tc = r.t_sim[b] + du;
         atomicMax((unsigned long long*)(r.tcl + d.labels[i]), (unsigned long long)tc);
+        if (d.n_sims > 1) atomicAdd((unsigned long long*)(r.llm + b), (unsigned long long)(du - r.sy.base_us));
+        else busy += (unsigned long long)(du - r.sy.base_us);
+    }
+    if (d.n_sims == 1) {   // one atomic per warp
+        for (int o = 16; o > 0; o >>= 1) busy += __shfl_xor_sync(0xFFFFFFFFu, busy, o);
+        if ((threadIdx.x & 31) == 0 && busy) atomicAdd((unsigned long long*)r.llm, busy);
     }
 }
 
@@ -345,7 +357,7 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
         sq[t] = r.qkey[i];
         traj = r.traj[i];
     }
-    long long tsim = r.t_sim[b], tdone = r.tdone[b], nrounds = r.rounds[b], disp = 0;
+    long long tsim = r.t_sim[b], tdone = r.tdone[b], nrounds = r.rounds[b], disp = 0, busy = 0;
     int act = r.active_flag[b], live_err = 0, lab = -1;
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
     const uint32_t Rc2 = Rc * Rc, Rp = (uint32_t)d.r_p, Rp2 = Rp * Rp;
@@ -392,7 +404,11 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
         const bool rdy = lead && st == ST_IDLE && !sbad[lab];
         if (mine && lead) slab[t] = rdy ? lab : -1;   // ready clusters' members (exclusive tiles)
         // ---- dispatch part a (k_disp_a): cluster completion time
-        if (rdy) atomicMax(stcl + lab, (unsigned long long)(tsim + duration(r.sy, i, A.z)));
+        if (rdy) {
+            const long long du = duration(r.sy, i, A.z);
+            atomicMax(stcl + lab, (unsigned long long)(tsim + du));
+            busy += du - r.sy.base_us;
+        }
         __syncthreads();
         // ---- dispatch part b (k_disp_b): member completion times and moves
         if (rdy) snp[t] = policy_move(r, i, A.z, make_int2(A.x, A.y), dig);
@@ -501,6 +517,7 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
     __syncthreads();
     if (mine && lead && S.w == ST_RUNNING && stc[t] != LLONG_MAX) atomicMin(&s_tmin, (unsigned long long)stc[t]);
     if (mine && lead && S.w != ST_DONE) atomicAdd(&s_any, 1);
+    if (busy) atomicAdd((unsigned long long*)(r.llm + b), (unsigned long long)busy);   // LLM time dispatched
     __syncthreads();
     if (threadIdx.x == 0) {
         r.t_sim[b] = tsim;
@@ -609,7 +626,7 @@ static int enqueue_round(am_replay* rp, bool external = false)
         if (c->bin_pending) return AM_E_STATE;
         am_join_side(c);
         am_prof_begin(c, K_INGEST);
-        RK(launch_k(c->pdl, rp->stream, k_replay_begin, 1, 1024, 0, rp->r, (int)ncb));
+        RK(launch_k(c->pdl, rp->stream, k_replay_begin, 1, 32, 0, rp->r, (int)ncb));
         am_prof_end(c, K_INGEST);
         c->bin_pending = true;
     } else {
@@ -640,7 +657,7 @@ static int enqueue_round(am_replay* rp, bool external = false)
 
 // device workspace layout of a replay (caller-owned, am_replay_workspace_size)
 struct RepLayout {
-    size_t total, tc, np, tr, tcl, ts, tn, td, rd, af, disp, live, chain, qk, mask, order, shadow, part;
+    size_t total, tc, np, tr, tcl, ts, tn, td, rd, af, disp, live, chain, qk, mask, order, shadow, part, llm;
 };
 static RepLayout rep_layout(const am_ctx* ctx)
 {
@@ -654,6 +671,7 @@ static RepLayout rep_layout(const am_ctx* ctx)
     L.mask = take(n); L.order = take(4 * n);
     L.shadow = take(4 * n);   // am_replay_io: the steps as copied in (delta write-back)
     L.part = take(32 * ((n + 256 * kCommitItems - 1) / (256 * kCommitItems)));   // k_commit partials
+    L.llm = take(8 * S);
     L.total = off;
     return L;
 }
@@ -722,6 +740,7 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
     rp->order = (int32_t*)(b + L.order);
     rp->shadow = (int32_t*)(b + L.shadow);
     r.part = (int32_t*)(b + L.part);
+    r.llm = (long long*)(b + L.llm);
     r.order = ctx->path == 1 ? ctx->d.rid : rp->order;
     RK(cudaStreamCreateWithFlags(&rp->stream, cudaStreamNonBlocking));
     RK(cudaMallocHost((void**)&rp->h_buf, 64));
@@ -1039,6 +1058,75 @@ extern "C" int am_replay_results(am_replay* rp, int64_t* T_ooo, int64_t* rounds,
     if (rounds) RK(cudaMemcpy(rounds, rp->r.rounds, 8 * S, cudaMemcpyDeviceToHost));
     if (traj) RK(cudaMemcpy(traj, rp->r.traj, 8 * (size_t)rp->ctx->d.n, cudaMemcpyDeviceToDevice));
     return AM_OK;
+}
+
+extern "C" int am_replay_llm_time(am_replay* rp, int64_t* llm_us)
+{
+    if (!rp || !llm_us) return AM_E_ARG;
+    RK(cudaStreamSynchronize(rp->stream));
+    RK(cudaMemcpy(llm_us, rp->r.llm, 8 * (size_t)rp->ctx->d.n_sims, cudaMemcpyDeviceToHost));
+    return AM_OK;
+}
+
+// T_sync[b] = sum over steps s < T of max over the agents i of simulation b of dur(i, s):
+// Algorithm 1's global barrier per step, the parallel-sync baseline.
+// Index k = s * n + i: a warp's lanes share the step (and mostly the simulation), so the
+// max is warp-reduced before one atomic.
+__global__ void k_lockstep_time(am_synth sy, int n, int n_sims, int T, unsigned long long* mx)
+{
+    const long long total = (long long)n * T;
+    for (long long k0 = (long long)blockIdx.x * blockDim.x; k0 < total; k0 += (long long)gridDim.x * blockDim.x) {
+        const long long k = k0 + threadIdx.x;
+        int b = -1, s = 0;
+        unsigned long long du = 0;
+        if (k < total) {
+            s = (int)(k / n);
+            const int i = (int)(k % n);
+            b = n_sims == 1 ? 0 : (int)(((long long)i * n_sims + n_sims - 1) / n);
+            du = (unsigned long long)duration(sy, i, s);
+        }
+        const long long key = b < 0 ? -1 : (long long)b * T + s;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+        unsigned long long m = du;
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+            const int src = (threadIdx.x & 31) ^ o;
+            if ((peers >> src) & 1u) m = max(m, y);
+        }
+        // lanes of one key may not be a contiguous power-of-two group: finish with atomics
+        if (b >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicMax(mx + key, m);
+        else if (b >= 0) atomicMax(mx + key, du);
+    }
+}
+
+__global__ void k_lockstep_sum(const unsigned long long* mx, int n_sims, int T, long long* out)
+{
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n_sims; b += gridDim.x * blockDim.x) {
+        long long acc = 0;
+        for (int s = 0; s < T; s++) acc += (long long)mx[(long long)b * T + s];
+        out[b] = acc;
+    }
+}
+
+extern "C" int am_lockstep_time(const am_synth* synth, int32_t n, int32_t n_sims, int32_t T, int64_t* T_sync,
+                                void* stream)
+{
+    if (!synth || n < 1 || n_sims < 1 || n_sims > n || T < 0 || !T_sync) return AM_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* mx = nullptr;
+    long long* d_out = nullptr;
+    const size_t cells = (size_t)n_sims * (size_t)std::max(1, T);
+    if (cudaMallocAsync((void**)&mx, 8 * cells, st) != cudaSuccess) return AM_E_CUDA;
+    if (cudaMallocAsync((void**)&d_out, 8 * (size_t)n_sims, st) != cudaSuccess) { cudaFreeAsync(mx, st); return AM_E_CUDA; }
+    cudaMemsetAsync(mx, 0, 8 * cells, st);
+    if (T > 0) k_lockstep_time<<<1184, 256, 0, st>>>(*synth, n, n_sims, T, mx);
+    k_lockstep_sum<<<(n_sims + 255) / 256, 256, 0, st>>>(mx, n_sims, T, d_out);
+    cudaError_t e = cudaMemcpyAsync(T_sync, d_out, 8 * (size_t)n_sims, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFreeAsync(mx, st);
+    cudaFreeAsync(d_out, st);
+    cudaStreamSynchronize(st);
+    return e == cudaSuccess ? AM_OK : AM_E_CUDA;
 }
 
 extern "C" int am_replay_dispatched(am_replay* rp, int64_t* agent_steps)

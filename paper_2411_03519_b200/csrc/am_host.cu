@@ -183,7 +183,7 @@ struct Layout {
     size_t ctl, pos0, pos1, st0, st1, ss0, ss1, labels, digest, blkid, tiles_s;
     size_t key = 0, cnt = 0, cmin = 0, ctab = 0, l1 = 0, l2 = 0, rec = 0, blk = 0, par = 0, bad = 0, rk0 = 0,
            rk1 = 0, rv0 = 0, rv1 = 0, tc = 0, tr = 0, tsort = 0, gh = 0, gs = 0, edges = 0, ectr = 0, wit = 0,
-           lrs = 0, wq = 0, dirty = 0, agf = 0, rid = 0, slot = 0;
+           lrs = 0, wq = 0, dirty = 0, agf = 0, rid = 0, slot = 0, cstripe = 0;
 };
 
 static int plan(am_ctx* x, int32_t map_w, int32_t map_h, int32_t radius_p, int32_t v_max, int32_t n_agents,
@@ -296,7 +296,7 @@ static int plan(am_ctx* x, int32_t map_w, int32_t map_h, int32_t radius_p, int32
         // agent), so a stripe holds at most ceil(blocks / 64) x 256 records
         const long long nbl = blocks(n, 256);
         d.wq_cap = (int)(((nbl + kEdgeStripes - 1) / kEdgeStripes) * 256);
-        L.wit = take(4 * N); L.lrs = take(N); L.slot = take(4 * N);
+        L.wit = take(4 * N); L.lrs = take(N); L.slot = take(4 * N); L.cstripe = take(4 * 32 * kCommitStripes);
         L.edges = take(8 * 4 * (size_t)d.ecap); L.ectr = take(4 * kEdgeStripes);
         L.wq = take(16 * (size_t)kEdgeStripes * d.wq_cap);
     }
@@ -443,6 +443,7 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
         d.cedges = (uint2*)(b + L.edges); d.nedges = d.cedges + 2 * (size_t)d.ecap; d.wq_ctr = (uint32_t*)(b + L.ectr); d.wq = (int4*)(b + L.wq);
         d.witness = (uint32_t*)(b + L.wit); d.chg8 = (uint8_t*)(b + L.lrs);
         d.slot = (uint32_t*)(b + L.slot);
+        d.cstripe = (int32_t*)(b + L.cstripe);
         // loose-cell rebuild policy (tuning knobs)
         d.rebuild_d = AM_REBUILD_D;
         d.rebuild_k = AM_REBUILD_K;
@@ -454,6 +455,10 @@ extern "C" int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radiu
     if (e == cudaSuccess && x->path == 1) e = cudaMemsetAsync(d.cmin, 0x7F, 4 * NC, x->stream);  // ~INT_MAX
     if (e == cudaSuccess && x->path == 1) e = cudaMemsetAsync(d.witness, 0xFF, 4 * N, x->stream);
     if (e == cudaSuccess && x->path == 1) e = cudaMemsetAsync(d.slot, 0xFF, 4 * N, x->stream);
+    int32_t h_stripes[32 * kCommitStripes] = {};
+    for (int k = 0; k < kCommitStripes; k++) { h_stripes[32 * k] = INT_MAX; h_stripes[32 * k + 1] = INT_MIN; }
+    if (e == cudaSuccess && x->path == 1)
+        e = cudaMemcpyAsync(d.cstripe, h_stripes, sizeof h_stripes, cudaMemcpyHostToDevice, x->stream);
     Ctl h{};
     h.acc_W = INT_MAX;
     h.acc_S = INT_MIN;

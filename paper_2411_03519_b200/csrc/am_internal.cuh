@@ -4,6 +4,7 @@
 // Citations "P:<line>" refer to /root/reference/PAPER.md.
 #pragma once
 
+#include <climits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -66,6 +67,7 @@ constexpr int kFinItems = AM_FIN_ITEMS;
 constexpr int kCommitItems = AM_COMMIT_ITEMS;   // agents per thread in the driver's k_commit         // agents per thread in k_finalize
 constexpr int kIngestItems = AM_INGEST_ITEMS;   // agents per thread in k_ingest / k_commit
 constexpr int kEdgeStripes = 64;          // striped queues (one atomic counter per stripe)
+constexpr int kCommitStripes = 64;        // post-commit reductions (block index mod 64)
 constexpr int kEdgeStage = 128;           // coupling edges staged per warp before appending
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
 // record word w = status (bits 0-1) | change tag << 8: the 24-bit round epoch in which
@@ -150,6 +152,8 @@ struct Dev {
     int4* rec;             // [n] records sorted by cell at the last rebuild {x | y<<16, step, id, w};
                            // positions / steps are kept current (in place) between rebuilds
     uint32_t* slot;        // [n] per id: index of its record (kSentinel: not binned, DONE)
+    int32_t* cstripe;      // [64][32] post-commit {min step, max step, active, running} per stripe
+                           // (one 128-byte line each; the replay's in-place commits, k_replay_begin)
     int32_t rebuild_d, rebuild_k;   // rebuild policy (drift tiles, incremental rounds)
     uint8_t* v8;           // [n] per id: blocking verdict (0 no, 1 yes, 2 far phase pending)
     uint32_t* witness;     // [n] per id: the blocker found last time it was computed
@@ -643,4 +647,16 @@ __device__ __forceinline__ void round_begin(const Dev& d)
         for (int k = 0; k < kEdgeStripes; k++) d.wq_ctr[k] = 0;
 }
 
+}  // namespace am
+
+namespace am {
+// neutral values of the post-commit reduction stripes (one thread)
+__device__ __forceinline__ void cstripe_reset(const Dev& d)
+{
+    if (!d.cstripe) return;
+    for (int k = 0; k < kCommitStripes; k++) {
+        int32_t* c = d.cstripe + 32 * k;
+        c[0] = INT_MAX; c[1] = INT_MIN; c[2] = 0; c[3] = 0;
+    }
+}
 }  // namespace am

@@ -193,6 +193,7 @@ __global__ void k_ingest_done(Dev d, int mode, int bin)
     // a rejected update may have touched records and incremental state: recompute all
     if (e != 0) ctl->full_next = 1;
     ctl->part_valid = 0;                // W / S / counts are this update's
+    cstripe_reset(d);
     ctl->D = max(ctl->D, ctl->acc_D);   // (a rejected update is followed by a full rebuild)
     ctl->acc_D = 0;
     if (e == 0) {

@@ -49,6 +49,7 @@ class Replay:
                         None if self._dur is None else self._dur.data_ptr(),
                         0 if self._dur is None else self._dur.shape[1], int(policy), int(conflict))
         torch.cuda.synchronize(dev)
+        self._sy = sy
         h = C.c_void_p()
         L = self.tracker.L
         # the replay's device workspace from PyTorch's allocator (two-phase idiom)
@@ -143,6 +144,21 @@ class Replay:
         # into the update and k_round_begin into k_ingest_done (am_update_binned)
         fused = 2 if self.tracker.stats()["path"] == 1 else 0
         return int(self.L.am_launches_per_round(self.tracker.ctx)) + 3 - fused
+
+    def llm_time(self):
+        """LLM busy time dispatched per simulation (us): the numerator of the achieved
+        parallelism (P:249)."""
+        out = np.zeros(self.n_sims, np.int64)
+        check(self.L.am_replay_llm_time(self.h, out.ctypes.data), self.tracker.ctx)
+        return out
+
+    def lockstep_time(self, T: int):
+        """T_sync per simulation of the parallel-sync schedule (Alg. 1) under the same
+        latency model, computed on the device."""
+        out = np.zeros(self.n_sims, np.int64)
+        check(self.L.am_lockstep_time(C.byref(self._sy), int(self.n), int(self.n_sims), int(T), out.ctypes.data,
+                                      self.tracker.stream.cuda_stream), self.tracker.ctx)
+        return out
 
     def dispatched(self) -> int:
         v = C.c_int64(0)

@@ -249,6 +249,7 @@ class LoopbackWorld(_World):
         self.ranks = []
         self.rounds_done = 0
         self.rewindows = 0
+        self._carry = (0, 0, 0)   # counters of the slabs before the last re-window
         self._setup(st, 0, spread=_spread(steps0, status0), halo=halo)
 
     def _setup(self, st: dict, t: int, spread: int, halo=None):
@@ -330,7 +331,10 @@ class LoopbackWorld(_World):
         the spread needs now."""
         parts = [r.owned_state() for r in self.ranks]
         st = {k: torch.cat([p[k] for p in parts]) for k in parts[0]}
-        t = int(self.ranks[0].counters[0].item())
+        cnt = torch.stack([r.counters for r in self.ranks]).cpu().numpy()
+        self._carry = (max(self._carry[0], int(cnt[:, 1].max())), self._carry[1] + int(cnt[:, 2].sum()),
+                       self._carry[2] + int(cnt[0, 3]))   # finishing time, dispatched, rounds
+        t = int(cnt[0, 0])
         need = halo_needed(spread, self.r_p, self.v, self.K)
         self._setup(st, t, spread, halo=2 * need)
         self.rewindows += 1
@@ -360,8 +364,12 @@ class LoopbackWorld(_World):
         cnt = torch.stack([r.counters for r in self.ranks]).cpu().numpy()
         assert len(np.unique(gid.cpu().numpy())) == n, "every agent owned exactly once"
         return dict(x=out["pos"][:, 0], y=out["pos"][:, 1], steps=out["steps"],
-                    traj=out["traj"].view(np.uint64), T_ooo=int(cnt[:, 1].max()), rounds=int(cnt[0, 3]),
-                    dispatched=int(cnt[:, 2].sum()))
+                    traj=out["traj"].view(np.uint64), T_ooo=max(self._carry[0], int(cnt[:, 1].max())),
+                    rounds=self._carry[2] + int(cnt[0, 3]), dispatched=self._carry[1] + int(cnt[:, 2].sum()))
+
+    def dispatched(self) -> int:
+        """Agent-steps dispatched so far by all ranks (synchronises)."""
+        return self._carry[1] + int(torch.stack([r.counters for r in self.ranks])[:, 2].sum().item())
 
     def close(self):
         for r in self.ranks:
@@ -387,6 +395,7 @@ class DistWorld(_World):
         self.rank = None
         self.rounds_done = 0
         self.rewindows = 0
+        self._carry = (0, 0, 0)   # this rank's counters before the last re-window
         self._setup(st, 0, spread=_spread(steps0, status0), halo=halo)
 
     def _setup(self, st: dict, t: int, spread: int, halo=None):
@@ -453,7 +462,9 @@ class DistWorld(_World):
 
     def rewindow(self, spread: int):
         st = self._gather_state()
-        t = int(self.rank.counters[0].item())
+        cnt = self.rank.counters.cpu().numpy()
+        self._carry = (max(self._carry[0], int(cnt[1])), self._carry[1] + int(cnt[2]), self._carry[2] + int(cnt[3]))
+        t = int(cnt[0])
         need = halo_needed(spread, self.r_p, self.v, self.K)
         self._setup(st, t, spread, halo=2 * need)
         self.rewindows += 1
@@ -480,12 +491,13 @@ class DistWorld(_World):
             out[k] = o.cpu().numpy()
         cnt = self.rank.counters.clone()
         c1 = cnt[1:2].clone()
+        c1[0] = max(int(c1[0].item()), self._carry[0])
         self.dist.all_reduce(c1, op=self.dist.ReduceOp.MAX)
-        c2 = cnt[2:3].clone()
+        c2 = cnt[2:3].clone() + self._carry[1]
         self.dist.all_reduce(c2, op=self.dist.ReduceOp.SUM)
         return dict(x=out["pos"][:, 0], y=out["pos"][:, 1], steps=out["steps"],
-                    traj=out["traj"].view(np.uint64), T_ooo=int(c1.item()), rounds=int(cnt[3].item()),
-                    dispatched=int(c2.item()))
+                    traj=out["traj"].view(np.uint64), T_ooo=int(c1.item()),
+                    rounds=self._carry[2] + int(cnt[3].item()), dispatched=int(c2.item()))
 
     def close(self):
         if self.rank is not None:

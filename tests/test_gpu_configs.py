@@ -85,18 +85,18 @@ def _round_state(rep):
 
 
 def _take_round(rep):
-    """Run one round with outputs; returns (x, y, s, st_seen, mask, order, labels, blocked)."""
+    """Run one round with outputs; returns (x, y, s, st_seen, mask, order, labels, blocked).
+    The state the round sees: the world arrays and the tracker's statuses before it (the
+    last round's commits were applied in place at its end)."""
     x, y, s = _round_state(rep)
-    mask_t, order_t, labels_t = rep.step()
     tr = rep.tracker
+    st = tr.status().cpu().numpy().copy()
+    mask_t, order_t, labels_t = rep.step()
     n = rep.n
     blk_t = torch.empty(n, dtype=torch.uint8, device="cuda")
     assert tr.L.am_blocked(tr.ctx, C.c_void_p(blk_t.data_ptr())) == 0
-    st_after = tr.status().cpu().numpy()
     torch.cuda.synchronize()
     mask = mask_t.cpu().numpy()
-    st = st_after.copy()
-    st[mask == 1] = O.IDLE          # dispatched agents were IDLE when the round saw them
     return x, y, s, st, mask, order_t.cpu().numpy(), labels_t.cpu().numpy(), blk_t.cpu().numpy()
 
 

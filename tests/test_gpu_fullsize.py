@@ -47,20 +47,18 @@ def test_full_size_round_sampled_vs_oracle(name, preroll):
     x = rep.pos[:, 0].cpu().numpy().copy()
     y = rep.pos[:, 1].cpu().numpy().copy()
     s = rep.steps.cpu().numpy().copy()
-    mask_t, order_t, labels_t = rep.step()
     tr = rep.tracker
+    # the statuses the round sees (the last round's commits were applied in place)
+    st = tr.status().cpu().numpy().copy()
+    mask_t, order_t, labels_t = rep.step()
     n = rep.n
     blk_t = torch.empty(n, dtype=torch.uint8, device="cuda")
     assert tr.L.am_blocked(tr.ctx, C.c_void_p(blk_t.data_ptr())) == 0
-    st_after = tr.status().cpu().numpy()
     torch.cuda.synchronize()
     mask = mask_t.cpu().numpy()
     order = order_t.cpu().numpy()
     labels = labels_t.cpu().numpy()
     blocked = blk_t.cpu().numpy()
-    # the statuses the round saw: dispatched agents were IDLE before it
-    st = st_after.copy()
-    st[mask == 1] = O.IDLE
     assert mask.sum() > 1000, "the pre-roll must reach a round that dispatches work"
     assert len(np.unique(s[st != O.DONE])) > 10, "expected a spread of steps"
 

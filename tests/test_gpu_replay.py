@@ -268,3 +268,28 @@ def test_exclusive_tiles_replay_vs_oracle(name, steps, n_sims, K):
         np.testing.assert_array_equal(res[k], r[k], err_msg=k)
     np.testing.assert_array_equal(res["traj"], O.lockstep(p, sy, w.x, w.y, w.steps)["traj"])
     rep.close()
+
+
+@pytest.mark.parametrize("name,steps,n,path", [("C1", 300, None, None), ("C3", 120, 16, None),
+                                               ("C4", 15, 2000, "binned"), ("C2", 30, None, "binned")])
+def test_llm_time_and_lockstep_time(name, steps, n, path):
+    """Achieved parallelism and the parallel-sync baseline: the LLM busy
+    time the replay dispatched equals the schedule-independent sum over every agent-step
+    of dur - base_us (each agent-step runs exactly once), and the device lock-step time
+    equals the oracle's T_sync = sum_s max_i dur(i, s)."""
+    w = amgen.config(name, steps=steps, n=n)
+    lm = amgen.latency_model(w.profile)
+    rep = Replay.from_workload(w, lm, force=path)
+    rep.run_to_end(chunk=512)
+    llm = rep.llm_time()
+    tsync = rep.lockstep_time(w.steps)
+    sy = O.SynthTables.from_model(lm, wall=w.wall)
+    nn = len(w.x)
+    durs = np.array([[O.duration(sy, i, s) for s in range(w.steps)] for i in range(nn)], np.int64)
+    per_sim = (durs - lm.base_us).sum(1).reshape(w.n_sims, -1).sum(1)
+    np.testing.assert_array_equal(llm, per_sim)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, n_sims=w.n_sims)
+    ls = O.lockstep(p, sy, w.x, w.y, w.steps)
+    np.testing.assert_array_equal(tsync, ls["T_sync"])
+    assert np.all(rep.results()["T_ooo"] <= tsync + (w.Q * w.steps if w.Q else 0))
+    rep.close()
