@@ -407,7 +407,7 @@ def virtual_slabs(w, lm, dev, slab_counts=(2, 8), preroll=200, timed=4):
         wd.check()
         per = [max(r[k] for r in tl[1:] or tl) for k in range(G)]   # worst round per rank
         med = [sorted(r[k] for r in tl)[len(tl) // 2] for k in range(G)]
-        disp = sum(int(r.counters[2].item()) for r in wd.ranks)
+        disp = wd.dispatched()
         out[f"G={G}"] = {"rank_round_ms_max_over_ranks": max(med), "rank_round_ms_mean": sum(med) / G,
                          "rank_round_ms_worst": max(per), "halo_rows": wd.halo, "rewindows": wd.rewindows,
                          "window_agents_max": max(int((r.w_gid >= 0).sum().item()) for r in wd.ranks),

@@ -252,9 +252,15 @@ __global__ void __launch_bounds__(256) k_disp_a(RepDev r)
         if (d.n_sims > 1) atomicAdd((unsigned long long*)(r.llm + b), (unsigned long long)(du - r.sy.base_us));
         else busy += (unsigned long long)(du - r.sy.base_us);
     }
-    if (d.n_sims == 1) {   // one atomic per warp
+    if (d.n_sims == 1) {   // block reduction, one atomic per block on one of 64 stripes
+        __shared__ unsigned long long s_b[8];
         for (int o = 16; o > 0; o >>= 1) busy += __shfl_xor_sync(0xFFFFFFFFu, busy, o);
-        if ((threadIdx.x & 31) == 0 && busy) atomicAdd((unsigned long long*)r.llm, busy);
+        if ((threadIdx.x & 31) == 0) s_b[threadIdx.x >> 5] = busy;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 1; q < 8; q++) busy += s_b[q];
+            if (busy) atomicAdd((unsigned long long*)(r.llm + 16 * (blockIdx.x & 63)), busy);
+        }
     }
 }
 
@@ -671,7 +677,7 @@ static RepLayout rep_layout(const am_ctx* ctx)
     L.mask = take(n); L.order = take(4 * n);
     L.shadow = take(4 * n);   // am_replay_io: the steps as copied in (delta write-back)
     L.part = take(32 * ((n + 256 * kCommitItems - 1) / (256 * kCommitItems)));   // k_commit partials
-    L.llm = take(8 * S);
+    L.llm = take(8 * std::max(S, 16LL * 64));   // one simulation: 64 stripes of 128 bytes
     L.total = off;
     return L;
 }
@@ -1064,6 +1070,14 @@ extern "C" int am_replay_llm_time(am_replay* rp, int64_t* llm_us)
 {
     if (!rp || !llm_us) return AM_E_ARG;
     RK(cudaStreamSynchronize(rp->stream));
+    if (rp->ctx->d.n_sims == 1) {   // one simulation: 64 stripes (k_disp_a); the persistent kernel adds to stripe 0
+        long long h[16 * 64];
+        RK(cudaMemcpy(h, rp->r.llm, sizeof h, cudaMemcpyDeviceToHost));
+        long long acc = 0;
+        for (int k = 0; k < 64; k++) acc += h[16 * k];
+        llm_us[0] = acc;
+        return AM_OK;
+    }
     RK(cudaMemcpy(llm_us, rp->r.llm, 8 * (size_t)rp->ctx->d.n_sims, cudaMemcpyDeviceToHost));
     return AM_OK;
 }

@@ -436,7 +436,10 @@ __device__ __forceinline__ uint32_t suf_find(volatile uint32_t* parent, uint32_t
     if (cur != x) {
         uint32_t prev = x, next;
         while (cur > (next = parent[cur])) {
-            parent[prev] = next;
+            // path halving as a shared-memory atomicMin: parent pointers only ever decrease
+            // (hooks and halving both move toward the smaller root), so the min keeps the
+            // forest valid under concurrent finds and unions without a data race
+            atomicMin((uint32_t*)&parent[prev], next);
             prev = cur;
             cur = next;
         }

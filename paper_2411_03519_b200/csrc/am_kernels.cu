@@ -310,6 +310,7 @@ __global__ void __launch_bounds__(kCellsThreads) k_cells(Dev d)
         for (int k = 0; k < kW; k++) acc += wsum[k];
         const uint32_t ex = gridDim.x <= kScanAllTiles ? chain_scan_all(d.tiles_c, tile, tag, acc)
                                                          : chain_scan_warp(d.tiles_c, tile, tag, acc);
+        __syncwarp();   // every lane has read wsum before lane 0 rewrites it
         if (t == 0) {
             tile_excl = ex;
             uint32_t a2 = 0;
@@ -1249,6 +1250,7 @@ __global__ void __launch_bounds__(kReadyThreads) k_ready(Dev d, uint8_t* __restr
         for (int k = 0; k < kW; k++) acc += wsum[k];
         const uint32_t ex = gridDim.x <= kScanAllTiles ? chain_scan_all(d.tiles_r, tile, tag, acc)
                                                          : chain_scan_warp(d.tiles_r, tile, tag, acc);
+        __syncwarp();   // every lane has read wsum before lane 0 rewrites it
         if (t == 0) {
             tile_excl = ex;
             uint32_t a2 = 0;

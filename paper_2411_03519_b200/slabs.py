@@ -277,6 +277,11 @@ class LoopbackWorld(_World):
 
         def rec(k, j):
             if ev is not None:
+                if j % 2 == 0:
+                    # the device sleeps while the host enqueues the rank's phase, so the
+                    # events bracket its kernels running back to back (device time, not
+                    # the host's launch rate)
+                    torch.cuda._sleep(3_000_000)
                 ev[k][j].record()
 
         mbs = []
