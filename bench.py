@@ -40,8 +40,10 @@ UNIT = "agent-steps/s"
 def algorithmic_bytes(kernel: str, s: dict) -> float:
     n, a, c, r, p = s["n"], s["n_active"], s["ncells"], s["n_ready"], s["passes"]
     table = {
-        # read pos 8 + step 4 (new) + old step 4 + status 1 + old pos 8; write pos 8 + step 4 + status 1
-        "k_ingest": 38.0 * n,
+        # replay rounds: k_replay_begin (timed as k_ingest) reads / resets the 64 post-commit
+        # reduction stripes (128 B each); a host-buffer round's k_ingest reads pos 8 + step 4
+        # (new) + old step 4 + status 1 + old pos 8 and writes pos 8 + step 4 + status 1
+        "k_ingest": 64 * 128 * 2.0,
         # read status 1 + pos 8 + step 4; write key 4 + bad 1 + blkid 1; cell count + min 8
         "k_bin": 27.0 * n,
         # read count 4 + min 4; write start/min 8 + min reset 4 + pyramid 0.27
@@ -67,8 +69,10 @@ def algorithmic_bytes(kernel: str, s: dict) -> float:
         "k_disp_a": 20.0 * r,
         # ready: order 4 + label 4 + cluster time 8 + step 4 + pos 8 + digest 8; write tcommit 8 + newpos 8
         "k_disp_b": 52.0 * r,
-        # read status 1 (+ tcommit 8 for RUNNING); commit: pos/step/traj r+w
-        "k_commit": 1.0 * n + 8.0 * s["n_running"],
+        # read status 1 (+ tcommit 8 for RUNNING, world step 4 for the post-commit W / S);
+        # per commit (~ the ready count at steady state): world pos / step / traj r+w 32 +
+        # move 8 + label 4 + slot 4 + key 4, tracker state 13, record 16, dirty 4, changed 1
+        "k_commit": 1.0 * n + 12.0 * s["n_running"] + 4.0 * a + 86.0 * r,
         # read edge 8 + two parent words per edge
         "k_union": 16.0 * s["n_edges"],
     }

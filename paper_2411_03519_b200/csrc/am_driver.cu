@@ -76,14 +76,17 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
     // loads of all items first (independent chains in flight), then the commits
     uint8_t st[kCommitItems];
     long long tc[kCommitItems];
+    int sw[kCommitItems];
 #pragma unroll
     for (int k = 0; k < kCommitItems; k++) {
         const int i = blockIdx.x * (256 * kCommitItems) + k * 256 + threadIdx.x;
         st[k] = ST_DONE;
         tc[k] = 0;
+        sw[k] = 0;
         if (i < d.n) {
             st[k] = d.status[c][i];  // after this round's dispatch
             tc[k] = r.tcommit[i];
+            if (inplace) sw[k] = r.steps[i];   // (post-commit W / S: issued with the others)
         }
     }
     const long long t1 = one ? r.t_sim[0] : 0;
@@ -99,7 +102,8 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
             if (tc[k] <= t) {
                 const int2 np = r.newpos[i];
                 const int2 op = r.pos[i];
-                const int s = r.steps[i] + 1;
+                const int s = (inplace ? sw[k] : r.steps[i]) + 1;
+                sw[k] = s;
                 r.pos[i] = np;
                 r.steps[i] = s;
                 r.traj[i] = traj_step(r.traj[i], s, np.x, np.y);
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
             if (one) any_active = 1;
             else r.active_flag[b] = 1;
             if (inplace) {
-                const int s = r.steps[i];
+                const int s = sw[k];
                 wmin = min(wmin, s);
                 smax = max(smax, s);
                 nact++;

@@ -29,4 +29,7 @@ def test_sanitizer_clean(tool, case):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "workload ok" in out, out[-2000:]
-    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+    if tool == "racecheck":
+        assert "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" in out, out[-4000:]
+    else:
+        assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
