@@ -179,6 +179,59 @@ def random_state(n: int, w: int, h: int, seed: int, max_step: int = 4, p_running
     return x, y, s, st
 
 
+# ----------------------------------------------------------------------------- graphs
+def social_graph(V: int = 200, k: int = 4, p_rewire: float = 0.1, seed: int = 5):
+    """A small-world "social network" (Watts-Strogatz: a ring where every node links to
+    its k/2 nearest neighbours on each side, each link rewired with probability
+    p_rewire; regenerated until connected) for the non-Euclidean variant.
+    Returns (offsets int32 [V+1], neighbours int32 [E2]) -- CSR, neighbours sorted."""
+    for attempt in range(100):
+        rng = np.random.default_rng([seed, attempt])
+        edges = set()
+        for u in range(V):
+            for j in range(1, k // 2 + 1):
+                w = (u + j) % V
+                if rng.random() < p_rewire:
+                    w = int(rng.integers(0, V))
+                    while w == u or (min(u, w), max(u, w)) in edges:
+                        w = int(rng.integers(0, V))
+                edges.add((min(u, w), max(u, w)))
+        nbr = [[] for _ in range(V)]
+        for a, b in edges:
+            nbr[a].append(b)
+            nbr[b].append(a)
+        off = np.zeros(V + 1, np.int32)
+        for u in range(V):
+            off[u + 1] = off[u] + len(nbr[u])
+        adj = np.concatenate([np.array(sorted(x), np.int32) for x in nbr]) if edges else np.zeros(0, np.int32)
+        d = graph_distances(off, adj)
+        if (d != 0xFFFF).all():
+            return off, adj
+    raise RuntimeError("social graph generator failed")
+
+
+def graph_distances(off: np.ndarray, adj: np.ndarray) -> np.ndarray:
+    """Hop distances between all node pairs by breadth-first search from every node:
+    uint16 [V][V], 0xFFFF = unreachable.  Data for both sides (the metric's table)."""
+    V = len(off) - 1
+    out = np.full((V, V), 0xFFFF, np.uint16)
+    for src in range(V):
+        dist = out[src]
+        dist[src] = 0
+        frontier = [src]
+        h = 0
+        while frontier:
+            h += 1
+            nxt = []
+            for u in frontier:
+                for w in adj[off[u]:off[u + 1]]:
+                    if dist[w] == 0xFFFF:
+                        dist[w] = h
+                        nxt.append(int(w))
+            frontier = nxt
+    return out
+
+
 # ----------------------------------------------------------------------------- configs
 @dataclass
 class Workload:
@@ -194,6 +247,8 @@ class Workload:
     v: int = 1
     profile: str = "fullday"
     Q: int = 0
+    graph: tuple | None = None        # (offsets, neighbours): the graph-metric variant
+    gdist: np.ndarray | None = None   # uint16 [V][V] hop distances
 
 
 def config(name: str, steps: int | None = None, n: int | None = None) -> Workload:
@@ -223,6 +278,16 @@ def config(name: str, steps: int | None = None, n: int | None = None) -> Workloa
             ys.append(y)
         return Workload("C3", TOWN_W, TOWN_H, wall, np.concatenate(xs), np.concatenate(ys), sims,
                         steps or 1000)
+    if name == "G1":
+        # NEXT #4 variant ("non-Euclidean spaces such as social networks"): agents
+        # on the nodes of a 600-node small-world graph (ring lattice k = 4, 2% of the links
+        # rewired: diameter 39, mean distance 14 hops), hop metric, r_p = 2 hops, v = 1
+        off, adj = social_graph(600, 4, 0.02, seed=5)
+        V = len(off) - 1
+        rng = np.random.default_rng(2)
+        nodes = rng.integers(0, V, n or 60).astype(np.int32)
+        return Workload("G1", V, 1, None, nodes, np.zeros(len(nodes), np.int32), 1, steps or 300, r_p=2, v=1,
+                        graph=(off, adj), gdist=graph_distances(off, adj))
     if name in ("C4", "C5"):
         big = name == "C5"
         N = n or (1_000_000 if big else 100_000)

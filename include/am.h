@@ -73,6 +73,9 @@ extern "C" {
 /* distance metric */
 #define AM_METRIC_L2    0    /* Euclidean, compared as squared integers (default)        */
 #define AM_METRIC_LINF  1    /* Chebyshev variant                                         */
+#define AM_METRIC_GRAPH 2    /* hop count on a graph (am_set_graph; "non-Euclidean spaces   */
+                             /* such as social networks"): positions are nodes        */
+                             /* (x = node in [0, map_w), map_h = 1); fused path only         */
 
 /* flags (am_config.flags, am_set_flags) */
 #define AM_VALIDATE     0x1u /* validate commits in am_update (protocol + velocity)       */
@@ -83,6 +86,9 @@ extern "C" {
 #define AM_FORCE_SMALL  0x20u/* always use the fused per-simulation kernel (<=1024/sim)    */
 #define AM_STATS        0x40u/* count scan work (cells, candidate pairs) for am_scan_stats  */
 #define AM_SCAN_THREAD  0x80u/* one thread per agent neighbour scan (ablation baseline)    */
+#define AM_NO_ORDER     0x100u/* am_ready leaves `order` unwritten (the mask, labels and the  */
+                              /* ready count are computed; the spatial-slab window tracker   */
+                              /* orders its ranks' ready agents itself)                      */
 #define AM_DBG_SKIP_NEAR 0x1000u /* PROFILING ONLY: skip the scan's near phase (wrong results) */
 #define AM_DBG_SKIP_FAR  0x2000u /* PROFILING ONLY: skip the scan's far phase (wrong results)  */
 
@@ -144,6 +150,12 @@ int am_init(am_ctx** out, int32_t map_w, int32_t map_h, int32_t radius_p, int32_
  * App. A); it then becomes IDLE (DONE at target_step).  Unchanged agents keep
  * their status.  Validation (AM_VALIDATE) is reported by the next am_ready/am_sync. */
 int am_update(am_ctx* ctx, const int32_t* positions, const int32_t* sim_steps);
+
+/* The graph of AM_METRIC_GRAPH: dist = uint16 [n_nodes][n_nodes] hop distances (device,
+ * caller-owned, 0xFFFF = unreachable; a shortest-path metric, so App. A's derivation --
+ * triangle inequality and at most v hops per step -- holds), n_nodes == map_w.  Call
+ * before the first am_update.  Errors: AM_E_ARG (wrong metric / size / path). */
+int am_set_graph(am_ctx* ctx, const uint16_t* dist, int32_t n_nodes);
 
 /* Set the full state, including statuses (uint8 [n_agents], AM_IDLE/RUNNING/DONE),
  * without commit validation (snapshots).  Bounds and status values are checked; the call

@@ -26,7 +26,8 @@
  *              perceived = same-step non-DONE j != i with dist <= radius_p
  *   h = mix64(key3(policy_seed, i, s) + digest_i); move = {0,+x,-x,+y,-y}[h % 5]
  *       (policy 2, the 8-connected walk for the L-infinity metric: those five then
- *       (+1,+1), (-1,+1), (+1,-1), (-1,-1), [h % 9]),
+ *       (+1,+1), (-1,+1), (+1,-1), (-1,-1), [h % 9]; policy 3, the graph walk:
+ *       {stay, neighbour 0, ..., neighbour deg-1}[h % (deg + 1)]),
  *       cancelled if the target tile is a wall or off the map
  *   K = vals[min{m : (key3(lat_seed,i,s) >> 32) < cdf32[m]}]
  *   dur(i,s) = base_us + sum_{k<K} lat[key3(lat_seed ^ 0xC0FFEE, (i<<20) ^ s, k) >> 54]
@@ -62,6 +63,9 @@ typedef struct {
                                    a lower-id cluster-mate proposes it (Alg. 3 l.20;
                                    needs r_p >= 2 v; fused per-simulation path only,
                                    through am_replay_run / am_replay_launch)              */
+    const int32_t* graph_off;   /* policy 3 (graph walk, AM_METRIC_GRAPH): CSR adjacency,  */
+    const int32_t* graph_adj;   /* [n_nodes + 1] offsets and the neighbour lists; a move is
+                                   {stay, neighbour 0..deg-1}[h % (deg + 1)]              */
 } am_synth;
 
 typedef struct am_replay am_replay;

@@ -37,7 +37,7 @@ _lock = threading.Lock()
 _lib = None
 
 IDLE, RUNNING, DONE = 0, 1, 2
-L2, LINF = 0, 1
+L2, LINF, GRAPH = 0, 1, 2
 OK, E_ARG, E_BOUNDS, E_PROTOCOL, E_VELOCITY, E_LIVENESS = 0, -1, -2, -3, -4, -8
 
 
@@ -65,7 +65,7 @@ def host_threads() -> int:
 class Params(C.Structure):
     _fields_ = [("map_w", C.c_int32), ("map_h", C.c_int32), ("r_p", C.c_int32),
                 ("v", C.c_int32), ("target", C.c_int32), ("metric", C.c_int32),
-                ("n_sims", C.c_int32)]
+                ("n_sims", C.c_int32), ("gdist", C.c_void_p), ("gV", C.c_int32)]
 
 
 class Synth(C.Structure):
@@ -73,7 +73,7 @@ class Synth(C.Structure):
                 ("n_vals", C.c_int32), ("base_us", C.c_int32), ("lat_seed", C.c_uint64),
                 ("policy_seed", C.c_uint64), ("wall", C.c_void_p),
                 ("dur_table", C.c_void_p), ("dur_T", C.c_int32), ("policy", C.c_int32),
-                ("conflict", C.c_int32)]
+                ("conflict", C.c_int32), ("graph_off", C.c_void_p), ("graph_adj", C.c_void_p)]
 
 
 class Log(C.Structure):
@@ -131,8 +131,15 @@ def _p(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def params(map_w, map_h, r_p, v, target=0, metric=L2, n_sims=1) -> Params:
-    return Params(int(map_w), int(map_h), int(r_p), int(v), int(target), int(metric), int(n_sims))
+def params(map_w, map_h, r_p, v, target=0, metric=L2, n_sims=1, graph_dist=None) -> Params:
+    """graph_dist: uint16 [V][V] hop distances (metric GRAPH; positions are nodes)."""
+    if graph_dist is None:
+        return Params(int(map_w), int(map_h), int(r_p), int(v), int(target), int(metric), int(n_sims), None, 0)
+    gd = np.ascontiguousarray(graph_dist, np.uint16)
+    p = Params(int(map_w), int(map_h), int(r_p), int(v), int(target), int(GRAPH), int(n_sims), _p(gd).value,
+               int(gd.shape[0]))
+    p._keep = gd
+    return p
 
 
 def _i32(a):
@@ -222,22 +229,27 @@ class SynthTables:
     """Keeps the numpy arrays alive while the C struct points into them."""
 
     def __init__(self, lat, cdf32, vals, base_us, lat_seed, policy_seed, wall=None,
-                 dur_table=None, policy=0, conflict=0):
+                 dur_table=None, policy=0, conflict=0, graph=None):
         self.lat = np.ascontiguousarray(lat, np.uint32)
         self.cdf32 = np.ascontiguousarray(cdf32, np.uint64)
         self.vals = np.ascontiguousarray(vals, np.int32)
         self.wall = None if wall is None else np.ascontiguousarray(wall, np.uint8)
         self.dur = None if dur_table is None else np.ascontiguousarray(dur_table, np.int64)
+        self.goff = None if graph is None else np.ascontiguousarray(graph[0], np.int32)
+        self.gadj = None if graph is None else np.ascontiguousarray(graph[1], np.int32)
         self.s = Synth(_p(self.lat).value, _p(self.cdf32).value, _p(self.vals).value,
                        len(self.vals), int(base_us), int(lat_seed), int(policy_seed),
                        None if self.wall is None else _p(self.wall).value,
                        None if self.dur is None else _p(self.dur).value,
-                       0 if self.dur is None else self.dur.shape[1], int(policy), int(conflict))
+                       0 if self.dur is None else self.dur.shape[1], int(policy), int(conflict),
+                       None if graph is None else _p(self.goff).value,
+                       None if graph is None else _p(self.gadj).value)
 
     @classmethod
-    def from_model(cls, lm, wall=None, dur_table=None, policy=0, conflict=0):
+    def from_model(cls, lm, wall=None, dur_table=None, policy=0, conflict=0, graph=None):
+        """graph: (offsets, neighbours) CSR adjacency for the graph walk (policy 3)."""
         return cls(lm.lat, lm.cdf32, lm.vals, lm.base_us, lm.lat_seed, lm.policy_seed, wall,
-                   dur_table, policy, conflict)
+                   dur_table, policy, conflict, graph)
 
 
 def duration(sy: SynthTables, i: int, s: int) -> int:

@@ -33,7 +33,7 @@
 enum { ORC_IDLE = 0, ORC_RUNNING = 1, ORC_DONE = 2 };
 enum { ORC_OK = 0, ORC_E_ARG = -1, ORC_E_BOUNDS = -2, ORC_E_PROTOCOL = -3,
        ORC_E_VELOCITY = -4, ORC_E_LIVENESS = -8, ORC_E_INVARIANT = -9, ORC_E_CAPACITY = -10 };
-enum { ORC_L2 = 0, ORC_LINF = 1 };
+enum { ORC_L2 = 0, ORC_LINF = 1, ORC_GRAPH = 2 };
 
 typedef struct {
     int32_t map_w, map_h;   /* x in [0,map_w), y in [0,map_h)              (Q14) */
@@ -42,6 +42,12 @@ typedef struct {
     int32_t target;         /* target_step (Alg. 1/3 P:108); 0 = unbounded      */
     int32_t metric;         /* ORC_L2 (Euclidean, Q1) or ORC_LINF        */
     int32_t n_sims;         /* >=1 independent simulations, agents partitioned  */
+    /* ORC_GRAPH ("non-Euclidean spaces such as social networks",
+     * P:309): positions are graph nodes (x = node, y = 0) and dist(A,B) is the hop
+     * count gdist[x_A * gV + x_B] (0xFFFF = unreachable), the shortest-path metric the
+     * App. A derivation needs (triangle inequality + at most v hops per step). */
+    const uint16_t* gdist;
+    int32_t gV;
 } orc_params;
 
 /* agents of simulation b are [b*n/n_sims, (b+1)*n/n_sims) */
@@ -60,12 +66,23 @@ static int within(const orc_params* p, int64_t dx, int64_t dy, int64_t R)
     return dx * dx + dy * dy <= R * R;
 }
 
+/* dist(A,B) <= R for the positions of A and B under the metric */
+static int within_pts(const orc_params* p, int64_t xa, int64_t ya, int64_t xb, int64_t yb, int64_t R)
+{
+    if (p->metric == ORC_GRAPH) {
+        if (R < 0) return 0;
+        const uint16_t d = p->gdist[xa * p->gV + xb];
+        return d != 0xFFFF && (int64_t)d <= R;
+    }
+    return within(p, xa - xb, ya - yb, R);
+}
+
 /* P:160 (section 3.2) and App. A: A and B are coupled iff
  * Step_A == Step_B and dist(A,B) <= radius_p + max_vel. */
 int orc_coupled(const orc_params* p, int32_t xa, int32_t ya, int32_t sa,
                 int32_t xb, int32_t yb, int32_t sb)
 {
-    return sa == sb && within(p, (int64_t)xa - xb, (int64_t)ya - yb, (int64_t)p->r_p + p->v);
+    return sa == sb && within_pts(p, xa, ya, xb, yb, (int64_t)p->r_p + p->v);
 }
 
 /* P:161 (section 3.2; the minus sign is lost there) restated from App. A P:406:
@@ -78,7 +95,7 @@ int orc_blocked_by(const orc_params* p, int32_t xa, int32_t ya, int32_t sa,
 {
     if (!(sb < sa)) return 0;
     int64_t R = ((int64_t)sa - sb + 1) * p->v + p->r_p;
-    return within(p, (int64_t)xa - xb, (int64_t)ya - yb, R);
+    return within_pts(p, xa, ya, xb, yb, R);
 }
 
 /* ---- sequential union-find; the root of every tree is its minimum id (Q10) ---- */
@@ -249,7 +266,7 @@ int orc_update(const orc_params* p, int32_t n, int32_t first, int32_t* x, int32_
             if (nx[i] != x[i] || ny[i] != y[i]) err_p = 1;
         } else if (ds == 1) {
             if (status[i] != ORC_RUNNING) err_p = 1;
-            else if (!within(p, (int64_t)nx[i] - x[i], (int64_t)ny[i] - y[i], p->v)) err_v = 1;
+            else if (!within_pts(p, x[i], y[i], nx[i], ny[i], p->v)) err_v = 1;
         } else {
             err_p = 1;
         }
@@ -283,7 +300,7 @@ int64_t orc_validity_violations(const orc_params* p, int32_t n, const int32_t* x
                 int64_t g = (int64_t)step[i] - step[j];
                 if (g < 0) g = -g;
                 /* dist > R  <=>  !(dist <= R) */
-                if (within(p, (int64_t)x[i] - x[j], (int64_t)y[i] - y[j], (int64_t)p->r_p + (g - 1) * p->v))
+                if (within_pts(p, x[i], y[i], x[j], y[j], (int64_t)p->r_p + (g - 1) * p->v))
                     bad++;
             }
     }
@@ -320,8 +337,11 @@ typedef struct {
     const uint8_t* wall;      /* [map_h*map_w] row-major, 1 = wall; NULL = open map   */
     const int64_t* dur_table; /* optional explicit durations [n][dur_T] (closed forms)  */
     int32_t dur_T;
-    int32_t policy;           /* 0 = random walk, 1 = always stay, 2 = 8-connected     */
+    int32_t policy;           /* 0 = random walk, 1 = always stay, 2 = 8-connected,    */
+                              /* 3 = graph walk (ORC_GRAPH)                             */
     int32_t conflict;         /* 0 = co-occupancy allowed; 1 = exclusive tiles (below)  */
+    const int32_t* graph_off; /* policy 3: CSR adjacency of the graph, [gV + 1] offsets  */
+    const int32_t* graph_adj; /*           and the neighbour lists                      */
 } orc_synth;
 
 /*
@@ -385,7 +405,7 @@ uint64_t orc_digest(const orc_params* p, int32_t lo, int32_t hi, const int32_t* 
     for (int32_t j = lo; j < hi; j++) {
         if (j == i || status[j] == ORC_DONE || step[j] != step[i]) continue;
         int32_t dx = x[j] - x[i], dy = y[j] - y[i];
-        if (!within(p, dx, dy, p->r_p)) continue;
+        if (!within_pts(p, x[i], y[i], x[j], y[j], p->r_p)) continue;
         uint64_t w = ((uint64_t)(uint32_t)j << 32) ^ ((uint64_t)(uint16_t)dx << 16) ^ (uint64_t)(uint16_t)dy;
         dig += orc_mix64(w);
     }
@@ -403,6 +423,15 @@ void orc_policy_move(const orc_params* p, const orc_synth* sy, int32_t i, int32_
     static const int32_t MX[9] = {0, 1, -1, 0, 0, 1, -1, 1, -1};
     static const int32_t MY[9] = {0, 0, 0, 1, -1, 1, 1, -1, -1};
     uint64_t h = orc_mix64(orc_key3(sy->policy_seed, (uint64_t)(uint32_t)i, (uint64_t)(uint32_t)s) + digest);
+    if (sy->policy == 3) {
+        /* graph walk: {stay, neighbour 0, ..., neighbour deg-1}[h % (deg + 1)] -- one hop,
+         * within v >= 1 under the hop metric */
+        const int32_t deg = sy->graph_off[px + 1] - sy->graph_off[px];
+        const int32_t m = (int32_t)(h % (uint64_t)(deg + 1));
+        *nx = m == 0 ? px : sy->graph_adj[sy->graph_off[px] + m - 1];
+        *ny = py;
+        return;
+    }
     int32_t m = sy->policy == 1 ? 0 : sy->policy == 2 ? (int32_t)(h % 9) : (int32_t)(h % 5);
     int32_t qx = px + MX[m], qy = py + MY[m];
     int ok = qx >= 0 && qx < p->map_w && qy >= 0 && qy < p->map_h;

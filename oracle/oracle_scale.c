@@ -35,6 +35,8 @@ enum { S_IDLE = 0, S_RUNNING = 1, S_DONE = 2 };
 /* the parameter / synth structs of oracle.c (same layout) */
 typedef struct {
     int32_t map_w, map_h, r_p, v, target, metric, n_sims;
+    const uint16_t* gdist;   /* ORC_GRAPH (oracle.c) */
+    int32_t gV;
 } orc_params;
 typedef struct orc_synth orc_synth;
 
@@ -364,7 +366,7 @@ static void lsg_body(void* a, int64_t lo, int64_t hi)
 int orc_lockstep_grid(const orc_params* p, const orc_synth* sy, int32_t n, int32_t T, int32_t* x, int32_t* y,
                       uint64_t* traj, int64_t* T_sync, int32_t nthreads)
 {
-    if (p->n_sims != 1 || n < 0) return -1;
+    if (p->n_sims != 1 || n < 0 || p->metric == 2) return -1;   /* spatial maps only (no graph metric) */
     const int32_t cell = p->r_p > 0 ? p->r_p : 1;
     const int32_t gw = (p->map_w + cell - 1) / cell, gh = (p->map_h + cell - 1) / cell;
     const int64_t nc = (int64_t)gw * gh;

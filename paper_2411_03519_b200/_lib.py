@@ -16,9 +16,10 @@ OK = 0
 E_ARG, E_BOUNDS, E_PROTOCOL, E_VELOCITY, E_CUDA, E_NCCL = -1, -2, -3, -4, -5, -6
 E_STATE, E_LIVENESS, E_WORKSPACE = -11, -12, -13
 IDLE, RUNNING, DONE = 0, 1, 2
-METRIC_L2, METRIC_LINF = 0, 1
+METRIC_L2, METRIC_LINF, METRIC_GRAPH = 0, 1, 2
 VALIDATE, PEEK, DIGEST, ASYNC, FORCE_BINNED, FORCE_SMALL, STATS, SCAN_THREAD = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80)
+NO_ORDER = 0x100
 
 ERROR_NAMES = {E_ARG: "AM_E_ARG", E_BOUNDS: "AM_E_BOUNDS", E_PROTOCOL: "AM_E_PROTOCOL",
                E_VELOCITY: "AM_E_VELOCITY", E_CUDA: "AM_E_CUDA", E_NCCL: "AM_E_NCCL",
@@ -58,7 +59,8 @@ class Synth(C.Structure):
     _fields_ = [("lat", C.c_void_p), ("cdf32", C.c_void_p), ("vals", C.c_void_p),
                 ("n_vals", C.c_int32), ("base_us", C.c_int32), ("lat_seed", C.c_uint64),
                 ("policy_seed", C.c_uint64), ("wall", C.c_void_p), ("dur_table", C.c_void_p),
-                ("dur_T", C.c_int32), ("policy", C.c_int32), ("conflict", C.c_int32)]
+                ("dur_T", C.c_int32), ("policy", C.c_int32), ("conflict", C.c_int32),
+                ("graph_off", C.c_void_p), ("graph_adj", C.c_void_p)]
 
 
 # name -> (restype, argtypes); every symbol include/*.h declares
@@ -69,6 +71,7 @@ SIGNATURES = {
     "am_update": (C.c_int, [_vp, _vp, _vp]),
     "am_set_state": (C.c_int, [_vp, _vp, _vp, _vp]),
     "am_update_replica": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "am_set_graph": (C.c_int, [_vp, _vp, _i32]),
     "am_ready": (C.c_int, [_vp, _vp, _vp, C.POINTER(_i32)]),
     "am_clusters": (C.c_int, [_vp, _vp]),
     "am_status": (C.c_int, [_vp, _vp]),

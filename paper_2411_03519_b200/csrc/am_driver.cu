@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
                 running = false;
                 if (inplace) {
                     // the speed limit the soundness of the rules rests on
-                    if (!within(np.x - op.x, np.y - op.y, (uint32_t)d.v, d.metric)) err |= ERR_VELOCITY;
+                    if (!within_pts(d, op.x, op.y, np.x, np.y, (uint32_t)d.v)) err |= ERR_VELOCITY;
                     const uint8_t nst = done ? ST_DONE : ST_IDLE;
                     d.pos[c][i] = np;
                     d.step[c][i] = s;
@@ -389,14 +389,19 @@ __global__ void __launch_bounds__(1024) k_small_replay(RepDev r, long long max_r
                 const int4 B = sa[j];
                 if (j == t || B.w == ST_DONE) continue;
                 const int dx = B.x - A.x, dy = B.y - A.y;
+                // the metric (template): coordinates, or the graph's hop table
+                const uint32_t hop = kMetric == AM_METRIC_GRAPH ? (uint32_t)d.gdist[(size_t)A.x * d.gV + B.x] : 0u;
+                auto in = [&](uint32_t R2, uint32_t R) {
+                    return kMetric == AM_METRIC_GRAPH ? (hop != 0xFFFFu && hop <= R) : within2(dx, dy, R2, R, kMetric);
+                };
                 if (B.z == A.z) {
-                    if (within2(dx, dy, Rc2, Rc, kMetric)) {
+                    if (in(Rc2, Rc)) {
                         if (t < j) suf_unite(par, (uint32_t)t, (uint32_t)j);
-                        if (within2(dx, dy, Rp2, Rp, kMetric)) dig += digest_term((uint32_t)(lo + j), dx, dy);
+                        if (in(Rp2, Rp)) dig += digest_term((uint32_t)(lo + j), dx, dy);
                     }
                 } else if (!blocked && B.z < A.z) {
                     const uint32_t R = min((uint32_t)min(A.z - B.z, lagcap) * vv + vr, kRClamp);
-                    blocked = within2(dx, dy, R * R, R, kMetric);
+                    blocked = in(R * R, R);
                 }
             }
         }
@@ -702,6 +707,11 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
             return AM_E_ARG;
         }
     }
+    if ((synth->policy == 3) != (ctx->d.metric == AM_METRIC_GRAPH) ||
+        (synth->policy == 3 && (!synth->graph_off || !synth->graph_adj || !ctx->d.gdist))) {
+        ctx->err = "am_replay_create: the graph walk (policy 3) goes with AM_METRIC_GRAPH and am_set_graph";
+        return AM_E_ARG;
+    }
     if (synth->conflict && (ctx->path != 0 || ctx->d.r_p < 2 * ctx->d.v)) {
         ctx->err = "am_replay_create: exclusive tiles need the fused per-simulation path and r_p >= 2 v";
         return AM_E_ARG;
@@ -898,13 +908,17 @@ static int launch_small_replay(am_replay* rp, int64_t rounds)
     static bool attr = [] {   // > 48 KB of dynamic shared memory for 1024-agent simulations
         cudaFuncSetAttribute(k_small_replay<AM_METRIC_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         cudaFuncSetAttribute(k_small_replay<AM_METRIC_LINF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(k_small_replay<AM_METRIC_GRAPH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         cudaGetLastError();
         return true;
     }();
     (void)attr;
     RK(cudaMemsetAsync(&c->d.ctl->n_active, 0, sizeof(int32_t), rp->stream));
     rp->r.d = c->d;
-    if (c->d.metric == AM_METRIC_LINF)
+    if (c->d.metric == AM_METRIC_GRAPH)
+        RK(launch_k(false, rp->stream, k_small_replay<AM_METRIC_GRAPH>, (unsigned)c->d.n_sims, (unsigned)(M * G), smem,
+                    rp->r, (long long)rounds, M, G));
+    else if (c->d.metric == AM_METRIC_LINF)
         RK(launch_k(false, rp->stream, k_small_replay<AM_METRIC_LINF>, (unsigned)c->d.n_sims, (unsigned)(M * G), smem,
                     rp->r, (long long)rounds, M, G));
     else

@@ -199,8 +199,10 @@ static int plan(am_ctx* x, int32_t map_w, int32_t map_h, int32_t radius_p, int32
     if (cfg) c = *cfg;
     if (c.n_sims < 1 || (n_agents > 0 && c.n_sims > n_agents))
         return set_err(nullptr, AM_E_ARG, "am_init: n_sims must be in [1, n_agents]");
-    if (c.metric != AM_METRIC_L2 && c.metric != AM_METRIC_LINF)
+    if (c.metric != AM_METRIC_L2 && c.metric != AM_METRIC_LINF && c.metric != AM_METRIC_GRAPH)
         return set_err(nullptr, AM_E_ARG, "am_init: unknown metric");
+    if (c.metric == AM_METRIC_GRAPH && (map_h != 1 || (c.flags & AM_FORCE_BINNED)))
+        return set_err(nullptr, AM_E_ARG, "am_init: the graph metric takes map_h == 1 (x = node) and the fused path");
     if (c.cell < 0 || (c.cell & (c.cell - 1)))
         return set_err(nullptr, AM_E_ARG, "am_init: cell must be 0 or a power of two");
     if (c.target_step < 0) return set_err(nullptr, AM_E_ARG, "am_init: negative target_step");
@@ -228,6 +230,8 @@ static int plan(am_ctx* x, int32_t map_w, int32_t map_h, int32_t radius_p, int32
     if (small && per_sim_max > kSmallMax)
         return set_err(nullptr, AM_E_ARG, "am_init: fused path needs <= 1024 agents per simulation");
     if (!small && c.n_sims > 1) return set_err(nullptr, AM_E_ARG, "am_init: the binned path takes one simulation");
+    if (!small && c.metric == AM_METRIC_GRAPH)
+        return set_err(nullptr, AM_E_ARG, "am_init: the graph metric runs on the fused path (<= 1024 agents/sim)");
     x->path = small ? 0 : 1;
     x->small_threads = std::max(32, ((per_sim_max + 31) / 32) * 32);
 
@@ -482,6 +486,7 @@ static int launch_ingest(am_ctx* c, const int32_t* pos, const int32_t* steps, co
     if (c->d.n == 0) return AM_OK;
     if (!pos || !steps || ((mode == 2 || mode == 3) && !st)) return set_err(c, AM_E_ARG, "NULL array");
     if (c->bin_pending) return set_err(c, AM_E_STATE, "update after a binned update without a round");
+    if (c->d.metric == AM_METRIC_GRAPH && !c->d.gdist) return set_err(c, AM_E_STATE, "am_set_graph first");
     am_join_side(c);
     if (mode == 1 || mode == 2) c->full_hint = true;   // initial / set state: the next round recomputes everything
     am_prof_begin(c, K_INGEST);
@@ -514,6 +519,16 @@ int am_update_binned(am_ctx* c, const int32_t* positions, const int32_t* sim_ste
     const int rc = launch_ingest(c, positions, sim_steps, nullptr, 0, true);
     if (rc == AM_OK) c->bin_pending = true;
     return rc;
+}
+
+extern "C" int am_set_graph(am_ctx* c, const uint16_t* dist, int32_t n_nodes)
+{
+    if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");
+    if (c->d.metric != AM_METRIC_GRAPH || !dist || n_nodes != c->d.map_w)
+        return set_err(c, AM_E_ARG, "am_set_graph: needs AM_METRIC_GRAPH and an n_nodes == map_w distance table");
+    c->d.gdist = dist;
+    c->d.gV = n_nodes;
+    return AM_OK;
 }
 
 extern "C" int am_update_replica(am_ctx* c, const int32_t* positions, const int32_t* sim_steps,
@@ -674,7 +689,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         // the mask is final here: a caller may copy it out beside the rest of the round
         if (c->mask_event && c->ev_mask) CK(c, cudaEventRecord(c->ev_mask, s));
         static const bool dbg_nosort = [] { const char* e = getenv("AM_DBG_NOSORT"); return e && atoi(e); }();
-        if (dbg_nosort) {
+        if (dbg_nosort || (d.flags & AM_NO_ORDER)) {
             // PROFILING ONLY (wrong `order`): measures how much of the round the sort holds up
         } else if (c->csort_ctas) {
             // one cluster of csort_ctas CTAs sorts the whole ready set (am_sort.cu), on the

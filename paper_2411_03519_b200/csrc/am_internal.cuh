@@ -155,6 +155,8 @@ struct Dev {
     int32_t* cstripe;      // [64][32] post-commit {min step, max step, active, running} per stripe
                            // (one 128-byte line each; the replay's in-place commits, k_replay_begin)
     int32_t rebuild_d, rebuild_k;   // rebuild policy (drift tiles, incremental rounds)
+    const uint16_t* gdist;          // AM_METRIC_GRAPH: [gV][gV] hop distances (0xFFFF: unreachable)
+    int32_t gV;
     uint8_t* v8;           // [n] per id: blocking verdict (0 no, 1 yes, 2 far phase pending)
     uint32_t* witness;     // [n] per id: the blocker found last time it was computed
     uint8_t* chg8;         // [n] per id: step changed since the last round (set by am_update)
@@ -355,6 +357,18 @@ __device__ __forceinline__ bool within(int dx, int dy, uint32_t R, int metric)
     }
     uint32_t d2 = (uint32_t)(dx * dx) + (uint32_t)(dy * dy);
     return d2 <= R * R;
+}
+
+// dist(A, B) <= R for positions A, B under the context's metric (the graph metric looks
+// the hop count up; the others use the coordinate differences)
+__device__ __forceinline__ bool within(int dx, int dy, uint32_t R, int metric);
+__device__ __forceinline__ bool within_pts(const Dev& d, int ax, int ay, int bx, int by, uint32_t R)
+{
+    if (d.metric == AM_METRIC_GRAPH) {
+        const uint32_t h = d.gdist[(size_t)ax * d.gV + bx];
+        return h != 0xFFFFu && h <= R;
+    }
+    return within(bx - ax, by - ay, R, d.metric);
 }
 
 // distance between the tile boxes [ax0,ax1]x[ay0,ay1] and [bx0,bx1]x[by0,by1] within R

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) k_ingest(Dev d, const int2* __restrict__ 
                 if (ost[k] != ST_RUNNING) {
                     err |= ERR_PROTOCOL;
                 } else {
-                    if (validate && !within(p[k].x - op[k].x, p[k].y - op[k].y, (uint32_t)d.v, d.metric))
+                    if (validate && !within_pts(d, op[k].x, op[k].y, p[k].x, p[k].y, (uint32_t)d.v))
                         err |= ERR_VELOCITY;
                     st = (d.target > 0 && s[k] == d.target) ? ST_DONE : ST_IDLE;
                 }
@@ -1496,13 +1496,13 @@ __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mas
             if (j == t || sst[j] == ST_DONE) continue;
             const int dx = sx[j] - ax, dy = sy[j] - ay, bs = ss[j];
             if (bs == as) {
-                if (within(dx, dy, Rc, d.metric)) {
+                if (within_pts(d, ax, ay, sx[j], sy[j], Rc)) {
                     if (t < j) suf_unite(par, (uint32_t)t, (uint32_t)j);
-                    if ((d.flags & AM_DIGEST) && within(dx, dy, (uint32_t)d.r_p, d.metric))
+                    if ((d.flags & AM_DIGEST) && within_pts(d, ax, ay, sx[j], sy[j], (uint32_t)d.r_p))
                         dig += digest_term((uint32_t)(lo + j), dx, dy);
                 }
             } else if (!blocked && bs < as) {
-                blocked = within(dx, dy, rb32(as - bs, d.lagcap, d.v, d.r_p), d.metric);
+                blocked = within_pts(d, ax, ay, sx[j], sy[j], rb32(as - bs, d.lagcap, d.v, d.r_p));
             }
         }
     }

@@ -224,14 +224,13 @@ __device__ __forceinline__ int4 mcluster(const SlabDev& s, const int32_t* mb, in
     return reinterpret_cast<const int4*>(mb + 4 + 2 * (size_t)s.g.cap_merge)[j];
 }
 
+// merge kernels: blockIdx.y = the rank whose records a block walks, up to their count
 __global__ void k_sl_unite(SlabDev s, const int32_t* __restrict__ mbufs)
 {
-    const int G = s.g.n_slabs, cap = s.g.cap_merge;
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < (long long)G * cap;
-         k += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(k / cap), j = (int)(k % cap);
-        const int32_t* mb = mbuf_of(s, mbufs, r);
-        if (j >= min(mb[0], cap)) continue;
+    const int r = blockIdx.y;
+    const int32_t* mb = mbuf_of(s, mbufs, r);
+    const int nl = min(mb[0], s.g.cap_merge);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nl; j += gridDim.x * blockDim.x) {
         const int2 e = mlink(s, mb, j);
         s.touched[e.x] = 1;
         s.touched[e.y] = 1;
@@ -241,12 +240,10 @@ __global__ void k_sl_unite(SlabDev s, const int32_t* __restrict__ mbufs)
 
 __global__ void k_sl_cbad(SlabDev s, const int32_t* __restrict__ mbufs)
 {
-    const int G = s.g.n_slabs, cap = s.g.cap_merge;
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < (long long)G * cap;
-         k += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(k / cap), j = (int)(k % cap);
-        const int32_t* mb = mbuf_of(s, mbufs, r);
-        if (j >= min(mb[1], cap)) continue;
+    const int r = blockIdx.y;
+    const int32_t* mb = mbuf_of(s, mbufs, r);
+    const int nc = min(mb[1], s.g.cap_merge);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nc; j += gridDim.x * blockDim.x) {
         const int4 c = mcluster(s, mb, j);
         const uint32_t f = uf_find(s.forest, (uint32_t)c.x);
         if (c.y) s.badm[f] = 1;
@@ -355,11 +352,10 @@ __global__ void __launch_bounds__(256) k_sl_final(SlabDev s, long long* stats)
 // the forest, bad, duration and touched marks back to their neutral values
 __global__ void k_sl_restore(SlabDev s, const int32_t* __restrict__ mbufs)
 {
-    const int G = s.g.n_slabs, cap = s.g.cap_merge;
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < (long long)G * cap;
-         k += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(k / cap), j = (int)(k % cap);
-        const int32_t* mb = mbuf_of(s, mbufs, r);
+    const int r = blockIdx.y, cap = s.g.cap_merge;
+    const int32_t* mb = mbuf_of(s, mbufs, r);
+    const int nmax = max(min(mb[0], cap), min(mb[1], cap));
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nmax; j += gridDim.x * blockDim.x) {
         if (j < min(mb[0], cap)) {
             const int2 e = mlink(s, mb, j);
             s.forest[e.x] = (uint32_t)e.x; s.forest[e.y] = (uint32_t)e.y;
@@ -458,12 +454,11 @@ __global__ void k_sl_commit(SlabDev s, int32_t* __restrict__ dsend)
 // departures first (their slots return to the free stack) ...
 __global__ void k_sl_depart(SlabDev s, const int32_t* __restrict__ drecv)
 {
-    const int G = s.g.n_slabs, cap = s.g.cap_peer;
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < (long long)G * cap;
-         k += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(k / cap), j = (int)(k % cap);
-        const int32_t* blk = dblock(s, drecv, r);
-        if (r == s.g.my_slab || j >= min(blk[0], cap)) continue;
+    const int r = blockIdx.y;   // the sender
+    if (r == s.g.my_slab) return;
+    const int32_t* blk = dblock(s, drecv, r);
+    const int nd = min(blk[0], s.g.cap_peer);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += gridDim.x * blockDim.x) {
         const int32_t* d = blk + 6 + (size_t)j * 6;
         const int g = d[0], y = d[2];
         const int i = s.map[g];
@@ -480,12 +475,11 @@ __global__ void k_sl_depart(SlabDev s, const int32_t* __restrict__ drecv)
 // ... then moved agents and arrivals (a free slot each)
 __global__ void k_sl_arrive(SlabDev s, const int32_t* __restrict__ drecv)
 {
-    const int G = s.g.n_slabs, cap = s.g.cap_peer;
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < (long long)G * cap;
-         k += (long long)gridDim.x * blockDim.x) {
-        const int r = (int)(k / cap), j = (int)(k % cap);
-        const int32_t* blk = dblock(s, drecv, r);
-        if (r == s.g.my_slab || j >= min(blk[0], cap)) continue;
+    const int r = blockIdx.y;   // the sender
+    if (r == s.g.my_slab) return;
+    const int32_t* blk = dblock(s, drecv, r);
+    const int nd = min(blk[0], s.g.cap_peer);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += gridDim.x * blockDim.x) {
         const int32_t* d = blk + 6 + (size_t)j * 6;
         const int g = d[0], x = d[1], y = d[2], stp = d[3];
         if (!in_window(s, y)) continue;
@@ -555,7 +549,7 @@ am_config tracker_cfg(const am_slab_geom& g)
     c.cell = 0;
     c.metric = g.metric;
     // mode-3 replica updates ignore AM_VALIDATE (it keeps the incremental round on)
-    c.flags = AM_VALIDATE | AM_PEEK | AM_ASYNC | AM_FORCE_BINNED;
+    c.flags = AM_VALIDATE | AM_PEEK | AM_ASYNC | AM_FORCE_BINNED | AM_NO_ORDER;
     return c;
 }
 
@@ -744,8 +738,11 @@ extern "C" int am_slab_merge(am_slab* sl, const int32_t* mbufs, int32_t* order_o
 {
     if (!sl || !mbufs || !order_out || !n_order || !stats) return AM_E_ARG;
     SlabDev& s = sl->s;
-    const long long nrec = (long long)s.g.n_slabs * s.g.cap_merge;
-    const unsigned gm = grid_for(sl, nrec), gr = grid_for(sl, s.L);
+    // one row of blocks per rank's records (each walks its rank's records up to their count)
+    const dim3 gm(std::max(1u, std::min((unsigned)((s.g.cap_merge + 255) / 256), (unsigned)(sl->num_sms * 8) /
+                                                                                   (unsigned)s.g.n_slabs)),
+                  (unsigned)s.g.n_slabs);
+    const unsigned gr = grid_for(sl, s.L);
     k_sl_unite<<<gm, 256, 0, sl->stream>>>(s, mbufs);
     k_sl_cbad<<<gm, 256, 0, sl->stream>>>(s, mbufs);
     k_sl_stats_init<<<1, 32, 0, sl->stream>>>(s, (long long*)stats);
@@ -776,7 +773,9 @@ extern "C" int am_slab_apply(am_slab* sl, const int32_t* drecv)
 {
     if (!sl || !drecv) return AM_E_ARG;
     SlabDev& s = sl->s;
-    const unsigned g = grid_for(sl, (long long)s.g.n_slabs * s.g.cap_peer);
+    const dim3 g(std::max(1u, std::min((unsigned)((s.g.cap_peer + 255) / 256), (unsigned)(sl->num_sms * 4) /
+                                                                               (unsigned)s.g.n_slabs)),
+                 (unsigned)s.g.n_slabs);
     k_sl_depart<<<g, 256, 0, sl->stream>>>(s, drecv);
     k_sl_arrive<<<g, 256, 0, sl->stream>>>(s, drecv);
     SK(cudaGetLastError());

@@ -47,6 +47,12 @@ __device__ __forceinline__ bool within2(int dx, int dy, uint32_t R2, uint32_t R,
 __device__ __forceinline__ int2 policy_move_g(const am_synth& sy, int map_w, int map_h, int i, int s, int2 p,
                                               unsigned long long dig)
 {
+    if (sy.policy == 3) {   // graph walk (AM_METRIC_GRAPH: x = node, one hop <= v)
+        const unsigned long long h = mix64(key3(sy.policy_seed, (uint32_t)i, (uint32_t)s) + dig);
+        const int deg = sy.graph_off[p.x + 1] - sy.graph_off[p.x];
+        const int m = (int)(h % (unsigned long long)(deg + 1));
+        return m == 0 ? p : make_int2(sy.graph_adj[sy.graph_off[p.x] + m - 1], p.y);
+    }
     int mv = 0;
     if (sy.policy == 0 || sy.policy == 2) {
         const unsigned long long h = mix64(key3(sy.policy_seed, (uint32_t)i, (uint32_t)s) + dig);

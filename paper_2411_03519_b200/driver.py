@@ -22,13 +22,17 @@ class Replay:
     def __init__(self, map_w, map_h, r_p, v, x0, y0, steps_target, *, n_sims=1, wall=None,
                  lat=None, cdf32=None, vals=None, base_us=5000, lat_seed=4, policy_seed=3,
                  dur_table=None, policy=0, quantum_us=0, cell=0, metric="l2", force=None,
-                 stats=False, capacity=0, priority=True, conflict=0, device="cuda"):
+                 stats=False, capacity=0, priority=True, conflict=0, device="cuda", graph=None,
+                 gdist=None):
         self.device = torch.device(device)
         n = len(x0)
         self.n = n
+        gd = None
+        if gdist is not None:   # uint16 hop table as int16 storage (the kernels read uint16)
+            gd = torch.as_tensor(np.ascontiguousarray(gdist, np.uint16).view(np.int16), device=self.device)
         self.tracker = Tracker(map_w, map_h, r_p, v, n, target=steps_target, n_sims=n_sims,
                                cell=cell, metric=metric, validate=True, digest=True, force=force,
-                               stats=stats, device=self.device)
+                               stats=stats, device=self.device, graph_dist=gd)
         dev = self.device
         self.pos = torch.tensor(np.stack([np.asarray(x0), np.asarray(y0)], 1), dtype=torch.int32,
                                 device=dev).contiguous()
@@ -43,11 +47,15 @@ class Replay:
                                                                device=dev).contiguous()
         self._dur = None if dur_table is None else torch.as_tensor(np.asarray(dur_table, np.int64),
                                                                    device=dev).contiguous()
+        self._goff = None if graph is None else torch.as_tensor(np.asarray(graph[0], np.int32), device=dev)
+        self._gadj = None if graph is None else torch.as_tensor(np.asarray(graph[1], np.int32), device=dev)
         sy = _lib.Synth(self._lat.data_ptr(), self._cdf.data_ptr(), self._vals.data_ptr(),
                         len(self._vals), int(base_us), int(lat_seed), int(policy_seed),
                         None if self._wall is None else self._wall.data_ptr(),
                         None if self._dur is None else self._dur.data_ptr(),
-                        0 if self._dur is None else self._dur.shape[1], int(policy), int(conflict))
+                        0 if self._dur is None else self._dur.shape[1], int(policy), int(conflict),
+                        None if self._goff is None else self._goff.data_ptr(),
+                        None if self._gadj is None else self._gadj.data_ptr())
         torch.cuda.synchronize(dev)
         self._sy = sy
         h = C.c_void_p()
@@ -67,6 +75,11 @@ class Replay:
     @classmethod
     def from_workload(cls, w, lm, **kw):
         """w: amgen.Workload, lm: amgen.LatencyModel."""
+        if getattr(w, "graph", None) is not None:   # the graph-metric variant (NEXT #4, P:309)
+            kw.setdefault("metric", "graph")
+            kw.setdefault("policy", 3)
+            kw.setdefault("graph", w.graph)
+            kw.setdefault("gdist", w.gdist)
         return cls(w.map_w, w.map_h, w.r_p, w.v, w.x, w.y, w.steps, n_sims=w.n_sims, wall=w.wall,
                    lat=lm.lat, cdf32=lm.cdf32, vals=lm.vals, base_us=lm.base_us, lat_seed=lm.lat_seed,
                    policy_seed=lm.policy_seed, quantum_us=kw.pop("quantum_us", w.Q), **kw)

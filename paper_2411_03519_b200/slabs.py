@@ -525,7 +525,7 @@ class Synth:
                             int(lm.base_us), int(lm.lat_seed), int(lm.policy_seed),
                             None if self.wall is None else self.wall.data_ptr(),
                             None if self.dur is None else self.dur.data_ptr(),
-                            0 if self.dur is None else self.dur.shape[1], int(policy), 0)
+                            0 if self.dur is None else self.dur.shape[1], int(policy), 0, None, None)
 
 
 def merged_order(outs: list) -> tuple[np.ndarray, np.ndarray]:

@@ -37,7 +37,7 @@ class Tracker:
                  n_sims: int = 1, cell: int = 0, metric: str = "l2", validate: bool = True,
                  peek: bool = False, digest: bool = False, force: str | None = None,
                  stats: bool = False, scan_thread: bool = False, device=None,
-                 stream: torch.cuda.Stream | None = None):
+                 stream: torch.cuda.Stream | None = None, graph_dist: torch.Tensor | None = None):
         self.L = _lib.load()
         self.device = torch.device(device if device is not None else "cuda")
         self.n = int(n)
@@ -60,9 +60,8 @@ class Tracker:
         self.flags = flags
         with torch.cuda.device(self.device):
             self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-            cfg = _lib.Config(int(target), int(n_sims), int(cell),
-                              _lib.METRIC_LINF if metric == "linf" else _lib.METRIC_L2, flags,
-                              self.stream.cuda_stream, None, 0)
+            mcode = {"l2": _lib.METRIC_L2, "linf": _lib.METRIC_LINF, "graph": _lib.METRIC_GRAPH}[metric]
+            cfg = _lib.Config(int(target), int(n_sims), int(cell), mcode, flags, self.stream.cuda_stream, None, 0)
             # two-phase workspace: the library sizes it, PyTorch's allocator provides it
             nbytes = int(self.L.am_workspace_size(self.map_w, self.map_h, self.r_p, self.v, self.n,
                                                   C.byref(cfg)))
@@ -77,6 +76,12 @@ class Tracker:
             rc = self.L.am_init(C.byref(h), self.map_w, self.map_h, self.r_p, self.v, self.n, C.byref(cfg))
             check(rc, None)
         self.ctx = h
+        if metric == "graph":
+            # the hop-distance table of AM_METRIC_GRAPH (uint16 [V][V] as int16 storage)
+            if graph_dist is None:
+                raise ValueError("metric='graph' needs graph_dist")
+            self.graph_dist = graph_dist.to(self.device).contiguous()
+            check(self.L.am_set_graph(self.ctx, self.graph_dist.data_ptr(), int(self.graph_dist.shape[0])), self.ctx)
         self.mask = torch.zeros(self.n, dtype=torch.uint8, device=self.device)
         self.order = torch.zeros(max(self.n, 1), dtype=torch.int32, device=self.device)
         self.labels = torch.zeros(max(self.n, 1), dtype=torch.int32, device=self.device)

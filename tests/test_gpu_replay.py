@@ -293,3 +293,64 @@ def test_llm_time_and_lockstep_time(name, steps, n, path):
     np.testing.assert_array_equal(tsync, ls["T_sync"])
     assert np.all(rep.results()["T_ooo"] <= tsync + (w.Q * w.steps if w.Q else 0))
     rep.close()
+
+
+@pytest.mark.parametrize("Q", [0, 30_000])
+def test_graph_metric_replay_vs_oracle(Q):
+    """NEXT #4 variant, graph-distance dependencies: agents on the nodes of a
+    600-node small-world graph, hop metric, the graph walk.  Every round's log (ids in
+    priority order + labels) of the multi-kernel rounds, and the persistent kernel's
+    final state, equal the oracle's replay; the outcome equals lock-step."""
+    w = amgen.config("G1", steps=150)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, policy=3, graph=w.graph)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, graph_dist=w.gdist)
+    r = O.replay(p, sy, w.x, w.y, Q=Q, log_rounds=10**6, log_entries=len(w.x) * w.steps + 10, check=True)
+    assert r["violations"] == 0
+    rep = Replay.from_workload(w, lm, quantum_us=Q)
+    glogs = _gpu_logged(rep, 1, len(w.x))
+    ologs = _split_oracle_log(r, 1)
+    assert len(glogs[0]) == len(ologs[0])
+    for (gi, gl), (oi, ol) in zip(glogs[0], ologs[0]):
+        np.testing.assert_array_equal(gi, oi)
+        np.testing.assert_array_equal(gl, ol)
+    res = rep.results()
+    for k in ("T_ooo", "rounds", "x", "traj"):
+        np.testing.assert_array_equal(res[k], r[k], err_msg=k)
+    rep.close()
+    rep = Replay.from_workload(w, lm, quantum_us=Q)   # the persistent per-simulation kernel
+    rep.run_to_end(chunk=4096)
+    res = rep.results()
+    for k in ("T_ooo", "rounds", "x", "traj"):
+        np.testing.assert_array_equal(res[k], r[k], err_msg=k)
+    ls = O.lockstep(p, sy, w.x, w.y, w.steps)
+    np.testing.assert_array_equal(res["traj"], ls["traj"])
+    rep.close()
+
+
+def test_graph_metric_round_vs_oracle():
+    """One round on random states of the graph (RUNNING / DONE mixes, a spread of steps)."""
+    from paper_2411_03519_b200 import Tracker
+    off, adj = amgen.social_graph(600, 4, 0.02, seed=5)
+    gd = amgen.graph_distances(off, adj)
+    rng = np.random.default_rng(4)
+    n = 800
+    x = rng.integers(0, 600, n).astype(np.int32)
+    y = np.zeros(n, np.int32)
+    s = rng.integers(0, 8, n).astype(np.int32)
+    st = (rng.random(n) < 0.2).astype(np.uint8)
+    st[rng.random(n) < 0.05] = O.DONE
+    p = O.params(600, 1, 2, 1, graph_dist=gd)
+    ref = O.round_(p, x, y, s, st.copy())
+    tr = Tracker(600, 1, 2, 1, n, metric="graph",
+                 graph_dist=torch.as_tensor(gd.view(np.int16)), device="cuda")
+    dev = torch.device("cuda")
+    tr.set_state(torch.as_tensor(np.stack([x, y], 1), dtype=torch.int32, device=dev), torch.as_tensor(s, device=dev),
+                 torch.as_tensor(st, device=dev))
+    mask, order = tr.ready()
+    labels = tr.clusters()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(mask.cpu().numpy(), ref["mask"])
+    np.testing.assert_array_equal(order.cpu().numpy(), ref["order"])
+    np.testing.assert_array_equal(labels.cpu().numpy(), ref["label"])
+    tr.close()
