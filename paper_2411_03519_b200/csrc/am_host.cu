@@ -639,7 +639,7 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         const unsigned nb = blocks(d.n, 256);
         // k_bin / k_cells return at once on loose-cell rounds (the device decides: a rebuild
         // is due after a full recompute, a drift beyond rebuild_d, or rebuild_k rounds)
-        LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, nb, 256, 0, d)));
+        LAUNCH(K_BIN, CK(c, launch_k(c->pdl, s, k_bin, std::min(nb, (unsigned)c->num_sms * 8), 256, 0, d)));
         c->bin_pending = false;
         LAUNCH(K_CELLS, CK(c, launch_k(c->pdl, s, k_cells, c->ntiles_cells, c->cells_threads, 0, d)));
         LAUNCH(K_SCATTER, CK(c, launch_k(c->pdl, s, k_scatter, nb, 256, 0, d)));

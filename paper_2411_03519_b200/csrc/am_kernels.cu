@@ -241,9 +241,9 @@ __global__ void __launch_bounds__(256) k_bin(Dev d)
 {
     pdl_begin();
     if (!d.ctl->rebuild) return;   // loose cells: the records of the last rebuild serve this round
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t c = d.ctl->cur;
-    if (i < d.n) {
+    // grid-stride over a resident-sized grid: a loose round's early exit costs one wave
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x) {
         // independent loads first (one round trip), then the atomics
         const uint8_t st = d.status[c][i];
         const int2 p = d.pos[c][i];
@@ -974,12 +974,14 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
                 // one round trip: the entries of the chunk's cells (<= 4 per lane)
                 int2 ent[KD / 16];
                 int nxt[KD / 16];
+                // only the 16-cell groups the box has (half-warp uniform: one agent)
+                const int ngrp = min(KD / 16, (ncell - cb + 15) >> 4);
 #pragma unroll
                 for (int j = 0; j < KD / 16; j++) {
                     const int k = cb + j * 16 + l;
                     ent[j] = make_int2(0, INT_MAX);
                     nxt[j] = 0;
-                    if (k < ncell) {
+                    if (j < ngrp && k < ncell) {
                         const int ky = krow(k), kx = k - ky * ncx;
                         const uint32_t key = mkey(d, cx0 + kx, cy0 + ky, 0);
                         ent[j] = d.ctab[key];
@@ -992,8 +994,10 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
                 unsigned nearbits = 0;
 #pragma unroll
                 for (int pass = 0; pass < 2; pass++) {
+                    if (pass == 1 && !(far && direct)) break;   // no far cells in this box
 #pragma unroll
                     for (int j = 0; j < KD / 16; j++) {
+                        if (j >= ngrp) break;                    // half-warp uniform
                         const int k = cb + j * 16 + l;
                         bool ok = false;
                         if (k < ncell && nxt[j] > ent[j].x) {
