@@ -39,6 +39,7 @@ struct RepDev {
     long long K;                // agent-steps in service at once; 0 = infinite capacity
     int32_t* part;              // [2 x 4 x commit blocks] post-commit partials (in-place commits)
     long long* llm;             // [S] LLM busy time dispatched so far: sum of (duration - base_us), us
+    int32_t* clist;             // [n] this round's committing agents (AM_COMMIT_SPLIT)
     int32_t prio;               // 1: queue by (step, label); 0: by (round, label)
 };
 
@@ -193,6 +194,132 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
             if (dmax > 0) atomicMax(&d.ctl->acc_D, dmax);
             if (err) atomicOr(&d.ctl->err_new, err);
         }
+    }
+}
+
+// ---- the commit as two passes (AM_COMMIT_SPLIT, one simulation, binned path) ----
+// k_commit_scan: the O(N) part only -- statuses, completion times and steps, read
+// coalesced with no dependent chain: which agents commit (appended to a list), the next
+// event from the agents that stay RUNNING, activity, and the post-commit {min step, max
+// step, active, running} into the reduction stripes.  k_commit_apply then commits the
+// listed agents densely, one thread each (world state, trajectory hash, the tracker's
+// state in place, loose-cell record and drift) -- the scattered work leaves the O(N) pass.
+__global__ void __launch_bounds__(256) k_commit_scan(RepDev r)
+{
+    pdl_begin();
+    const Dev& d = r.d;
+    const uint32_t c = d.ctl->cur;
+    const long long t = r.t_sim[0];
+    unsigned long long tmin = ~0ull;
+    int wmin = INT_MAX, smax = INT_MIN, nact = 0, nrun = 0, any_active = 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = blockIdx.x * blockDim.x; base < d.n; base += gridDim.x * blockDim.x) {   // block uniform
+        const int i = base + threadIdx.x;
+        bool com = false;
+        if (i < d.n) {
+            const uint8_t st = d.status[c][i];
+            if (st != ST_DONE) {
+                const int s0 = r.steps[i];
+                int s = s0;
+                bool run = st == ST_RUNNING;
+                if (run) {
+                    const long long tc = r.tcommit[i];
+                    if (tc <= t) {
+                        com = true;
+                        run = false;
+                        s = s0 + 1;
+                    } else {
+                        tmin = min(tmin, (unsigned long long)tc);
+                    }
+                }
+                const bool done = com && d.target > 0 && s == d.target;
+                if (!done) {
+                    any_active = 1;
+                    wmin = min(wmin, s);
+                    smax = max(smax, s);
+                    nact++;
+                    nrun += run;
+                } else {
+                    atomicMax((unsigned long long*)r.tdone, (unsigned long long)t);
+                }
+            }
+        }
+        // warp-aggregated append of the committing agents
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, com);
+        int b0 = 0;
+        if (lane == 0 && m) b0 = atomicAdd(&d.ctl->n_commit, __popc(m));
+        b0 = __shfl_sync(0xFFFFFFFFu, b0, 0);
+        if (com) r.clist[b0 + __popc(m & ((1u << lane) - 1u))] = i;
+    }
+    __shared__ unsigned long long s_min[8];
+    __shared__ int p_w[8], p_s[8], p_a[8], p_r[8], p_y[8];
+    for (int o = 16; o > 0; o >>= 1) tmin = min(tmin, __shfl_xor_sync(0xFFFFFFFFu, tmin, o));
+    wmin = __reduce_min_sync(0xFFFFFFFFu, wmin);
+    smax = __reduce_max_sync(0xFFFFFFFFu, smax);
+    nact = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)nact);
+    nrun = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)nrun);
+    any_active = (int)__reduce_or_sync(0xFFFFFFFFu, (unsigned)any_active);
+    if (lane == 0) { s_min[w] = tmin; p_w[w] = wmin; p_s[w] = smax; p_a[w] = nact; p_r[w] = nrun; p_y[w] = any_active; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < 8; q++) {
+            tmin = min(tmin, s_min[q]); wmin = min(wmin, p_w[q]); smax = max(smax, p_s[q]);
+            nact += p_a[q]; nrun += p_r[q]; any_active |= p_y[q];
+        }
+        if (tmin != ~0ull) atomicMin((unsigned long long*)r.tnext, tmin);
+        if (any_active) r.active_flag[0] = 1;
+        int32_t* sp = d.cstripe + 32 * (blockIdx.x & (kCommitStripes - 1));
+        if (wmin != INT_MAX) atomicMin(sp, wmin);
+        if (smax != INT_MIN) atomicMax(sp + 1, smax);
+        if (nact) atomicAdd(sp + 2, nact);
+        if (nrun) atomicAdd(sp + 3, nrun);
+        if (blockIdx.x == 0) d.ctl->part_valid = 1;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_commit_apply(RepDev r)
+{
+    pdl_begin();
+    const Dev& d = r.d;
+    const uint32_t c = d.ctl->cur;
+    const uint32_t tag = (d.ctl->epoch + 1u) & kTagMask;
+    const int nc = d.ctl->n_commit;
+    int dmax = 0, err = 0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+        const int i = r.clist[k];
+        // every load first (independent), then the stores
+        const int2 np = r.newpos[i];
+        const int2 op = r.pos[i];
+        const int s = r.steps[i] + 1;
+        const unsigned long long th = r.traj[i];
+        const int lab = d.labels[i];
+        const uint32_t rr = d.slot[i];
+        const uint32_t key = d.key[i];
+        const bool done = d.target > 0 && s == d.target;
+        const uint8_t nst = done ? ST_DONE : ST_IDLE;
+        r.pos[i] = np;
+        r.steps[i] = s;
+        r.traj[i] = traj_step(th, s, np.x, np.y);
+        if (!within_pts(d, op.x, op.y, np.x, np.y, (uint32_t)d.v)) err |= ERR_VELOCITY;
+        d.pos[c][i] = np;
+        d.step[c][i] = s;
+        d.status[c][i] = nst;
+        d.chg8[i] = 1;
+        if (lab >= 0) d.dirty[lab] = d.ctl->epoch + 1u;
+        if (rr != kSentinel) {
+            d.rec[rr] = make_int4(np.x | (np.y << 16), s, i, (int)nst | (int)(tag << kTagShift));
+            int cx, cy;
+            mkey_decode(d, key, cx, cy);
+            const int x0 = cx << d.clog, y0 = cy << d.clog;
+            const int x1 = x0 + (1 << d.clog) - 1, y1 = y0 + (1 << d.clog) - 1;
+            dmax = max(dmax, max(max(x0 - np.x, np.x - x1), max(y0 - np.y, np.y - y1)));
+        }
+    }
+    dmax = __reduce_max_sync(0xFFFFFFFFu, dmax);
+    err = (int)__reduce_or_sync(0xFFFFFFFFu, (unsigned)err);
+    if ((threadIdx.x & 31) == 0) {
+        if (dmax > 0) atomicMax(&d.ctl->acc_D, dmax);
+        if (err) atomicOr(&d.ctl->err_new, err);
     }
 }
 
@@ -663,7 +790,14 @@ static int enqueue_round(am_replay* rp, bool external = false)
     RK(launch_k(c->pdl, rp->stream, k_disp_b, nbd, 256, 0, rp->r));
     am_prof_end(c, K_DISP_B);
     am_prof_begin(c, K_COMMIT);
-    RK(launch_k(c->pdl, rp->stream, k_commit, ncb, 256, 0, rp->r, inplace ? 1 : 0));
+    if (inplace && c->d.n_sims == 1 && AM_COMMIT_SPLIT) {
+        // the O(N) scan and the dense commit of the listed agents (two passes)
+        const unsigned g = std::min(ncb, (unsigned)c->num_sms * 8);
+        RK(launch_k(c->pdl, rp->stream, k_commit_scan, g, 256, 0, rp->r));
+        RK(launch_k(c->pdl, rp->stream, k_commit_apply, std::min(nb, (unsigned)c->num_sms * 4), 256, 0, rp->r));
+    } else {
+        RK(launch_k(c->pdl, rp->stream, k_commit, ncb, 256, 0, rp->r, inplace ? 1 : 0));
+    }
     am_join_side(c);   // the priority sort ran beside dispatch and commit
     am_prof_end(c, K_COMMIT);
     RK(cudaGetLastError());
@@ -672,7 +806,7 @@ static int enqueue_round(am_replay* rp, bool external = false)
 
 // device workspace layout of a replay (caller-owned, am_replay_workspace_size)
 struct RepLayout {
-    size_t total, tc, np, tr, tcl, ts, tn, td, rd, af, disp, live, chain, qk, mask, order, shadow, part, llm;
+    size_t total, tc, np, tr, tcl, ts, tn, td, rd, af, disp, live, chain, qk, mask, order, shadow, part, llm, clist;
 };
 static RepLayout rep_layout(const am_ctx* ctx)
 {
@@ -687,6 +821,7 @@ static RepLayout rep_layout(const am_ctx* ctx)
     L.shadow = take(4 * n);   // am_replay_io: the steps as copied in (delta write-back)
     L.part = take(32 * ((n + 256 * kCommitItems - 1) / (256 * kCommitItems)));   // k_commit partials
     L.llm = take(8 * std::max(S, 16LL * 64));   // one simulation: 64 stripes of 128 bytes
+    L.clist = take(4 * n);
     L.total = off;
     return L;
 }
@@ -761,6 +896,7 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
     rp->shadow = (int32_t*)(b + L.shadow);
     r.part = (int32_t*)(b + L.part);
     r.llm = (long long*)(b + L.llm);
+    r.clist = (int32_t*)(b + L.clist);
     r.order = ctx->path == 1 ? ctx->d.rid : rp->order;
     RK(cudaStreamCreateWithFlags(&rp->stream, cudaStreamNonBlocking));
     RK(cudaMallocHost((void**)&rp->h_buf, 64));

@@ -52,6 +52,9 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #ifndef AM_DIRECT_FULL
 #define AM_DIRECT_FULL 16   // ... of full-recompute rounds (C5 snapshot A/B: 777 / 649 / 624 us at 64 / 32 / 16)
 #endif
+#ifndef AM_COMMIT_SPLIT
+#define AM_COMMIT_SPLIT 1   // the replay's commit as an O(N) scan + a dense pass over the committing agents
+#endif
 #ifndef AM_INGEST_ITEMS
 #define AM_INGEST_ITEMS 4
 #endif
@@ -116,6 +119,7 @@ struct Ctl {
     int32_t  D, acc_D, since_rebuild, rebuild, n_rebuilds;
     int32_t  rebuild_req;  // a replica update brought an agent that has no record (arrival)
     int32_t  part_valid;   // the replay's in-place commit left post-commit partials (k_replay_begin)
+    int32_t  n_commit;     // committing agents listed by k_commit_scan (reset by round_begin)
     uint32_t scan_next;    // dynamic work distribution of k_scan_hw (AM_SCAN_DYN)
     // accumulators of am_update (reset by its last block)
     int32_t  acc_W, acc_S, acc_active, acc_running;
@@ -635,6 +639,7 @@ __device__ __forceinline__ void round_begin(const Dev& d)
     Ctl* ctl = d.ctl;
     ctl->epoch += 1;
     ctl->n_ready = 0;
+    ctl->n_commit = 0;
     ctl->n_clusters = 0;
     ctl->n_items = 0;
     ctl->n_far = 0;
