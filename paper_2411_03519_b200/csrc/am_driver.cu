@@ -13,6 +13,8 @@
 #include "am_internal.cuh"
 #include "am_synth.cuh"
 
+int am_internal_csort(am_ctx* c, const am::Dev& sd, int32_t* order, cudaStream_t s);
+
 namespace am {
 
 struct RepDev {
@@ -40,6 +42,23 @@ struct RepDev {
     int32_t* part;              // [2 x 4 x commit blocks] post-commit partials (in-place commits)
     long long* llm;             // [S] LLM busy time dispatched so far: sum of (duration - base_us), us
     int32_t* clist;             // [n] this round's committing agents (AM_COMMIT_SPLIT)
+    // finite capacity on the cell-binned path (one simulation): the queue of ready clusters
+    // waiting to start, one entry each {key, label, size, max duration}
+    int32_t* qsz;               // [n] members of this round's ready cluster, by label
+    unsigned long long* qe_key[2];   // [n] entry keys (ping-pong)
+    int32_t* qe_lab[2];
+    int32_t* qe_size[2];
+    long long* qe_dur[2];
+    int32_t* qn;                // [2] entries in each buffer
+    int32_t* qcur;              // [1] the current buffer
+    long long* qstart_t;        // [n] by label: completion time of a cluster started this round
+    uint32_t* qstart_ep;        // [n] by label: the epoch it started in
+    long long* busy;            // [1] agent-steps in service
+    int32_t* qorder;            // [n] entry indices in key order (the queue's sort)
+    Ctl* qctl;                  // the queue sort's control block (n_ready = entries, sort_or)
+    unsigned long long* qrk[2]; // the queue sort's ping-pong keys / values
+    uint32_t* qrv[2];
+    int32_t qidb;               // bits of an agent id in the compact entry key
     int32_t prio;               // 1: queue by (step, label); 0: by (round, label)
 };
 
@@ -91,10 +110,19 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
         }
     }
     const long long t1 = one ? r.t_sim[0] : 0;
+    int ncommit = 0;
 #pragma unroll
     for (int k = 0; k < kCommitItems; k++) {
         const int i = blockIdx.x * (256 * kCommitItems) + k * 256 + threadIdx.x;
         if (st[k] == ST_DONE) continue;
+        if (r.K > 0 && st[k] == ST_RUNNING && tc[k] == LLONG_MAX) {
+            // queued: did its cluster start this round (k_qstart)?
+            const int lab = (int)(r.qkey[i] & ((1ull << r.qidb) - 1ull));
+            if (r.qstart_ep[lab] == d.ctl->epoch) {
+                tc[k] = r.qstart_t[lab];
+                r.tcommit[i] = tc[k];
+            }
+        }
         const int b = sim_of(d, i);
         const long long t = one ? t1 : r.t_sim[b];
         bool active = true;
@@ -114,6 +142,7 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
                     atomicMax((unsigned long long*)(r.tdone + b), (unsigned long long)t);
                 }
                 running = false;
+                ncommit++;
                 if (inplace) {
                     // the speed limit the soundness of the rules rests on
                     if (!within_pts(d, op.x, op.y, np.x, np.y, (uint32_t)d.v)) err |= ERR_VELOCITY;
@@ -152,6 +181,10 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
                 nrun += running;
             }
         }
+    }
+    if (r.K > 0 && one) {   // agent-steps leaving service (finite capacity)
+        ncommit = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)ncommit);
+        if ((threadIdx.x & 31) == 0 && ncommit) atomicAdd((unsigned long long*)r.busy, (unsigned long long)(-(long long)ncommit));
     }
     if (one) {  // block reduction, one atomic per block
         __shared__ unsigned long long s_min[8];
@@ -365,6 +398,114 @@ __global__ void __launch_bounds__(32) k_replay_begin(RepDev r, int nparts)
     }
 }
 
+// ---- finite capacity on the cell-binned path (one simulation) ---------------------
+// k_qprep: the queue's entries become the sort's input (compact keys, entry indices)
+__global__ void __launch_bounds__(256) k_qprep(RepDev r)
+{
+    pdl_begin();
+    const int q = *r.qcur, n = r.qn[q];
+    unsigned long long kor = 0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const unsigned long long key = r.qe_key[q][k];
+        r.qrk[0][k] = key;
+        r.qrv[0][k] = (uint32_t)k;
+        kor |= key;
+    }
+    for (int o = 16; o > 0; o >>= 1) kor |= __shfl_xor_sync(0xFFFFFFFFu, kor, o);
+    if ((threadIdx.x & 31) == 0 && kor) atomicOr(&r.qctl->sort_or, kor);
+    if (blockIdx.x == 0 && threadIdx.x == 0) r.qctl->n_ready = n;
+}
+
+// k_qstart (one block): start the queued clusters in key order while they fit -- strict
+// order, no bypass; a cluster larger than the capacity starts only when nothing is in
+// service (the oracle's orc_replay_cap) -- then the event clock (k_disp_b's last block
+// without capacity): the next event is the earliest completion of what is in service.
+__global__ void __launch_bounds__(1024) k_qstart(RepDev r)
+{
+    pdl_begin();
+    __shared__ int s_wsum[32];
+    __shared__ long long s_base;
+    __shared__ int s_cut, s_keep;
+    __shared__ unsigned long long s_tmin;
+    const int q = *r.qcur, n = r.qn[q];
+    const long long t = r.t_sim[0];
+    const uint32_t ep = r.d.ctl->epoch;
+    const long long busy0 = *r.busy;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) { s_base = 0; s_cut = n; s_keep = 0; s_tmin = ~0ull; }
+    __syncthreads();
+    // pass 1: the cutoff in key order (sizes' prefix sums, chunk by chunk)
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+        if (s_cut < c0) break;   // block uniform (written before the last barrier)
+        const int k = c0 + threadIdx.x;
+        const int e = k < n ? (int)r.qorder[k] : 0;
+        const int sz = k < n ? r.qe_size[q][e] : 0;
+        int incl = sz;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_wsum[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            const int v = lane < (int)(blockDim.x >> 5) ? s_wsum[lane] : 0;
+            int sc = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, sc, o);
+                if (lane >= o) sc += y;
+            }
+            s_wsum[lane] = sc - v;
+        }
+        __syncthreads();
+        const long long P = s_base + s_wsum[w] + incl;   // sizes of entries [0, k]
+        const bool fits = (busy0 + P <= r.K) || (k == 0 && busy0 == 0);
+        if (k < n && !fits) atomicMin(&s_cut, k);
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_base = P;
+        __syncthreads();
+    }
+    const int cut = s_cut;
+    // pass 2: start the prefix, keep the rest (any order: the queue is re-sorted next round)
+    long long started = 0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int e = (int)r.qorder[k];
+        if (k < cut) {
+            const int lab = r.qe_lab[q][e];
+            const long long tc = t + r.qe_dur[q][e];
+            r.qstart_t[lab] = tc;
+            r.qstart_ep[lab] = ep;
+            started += r.qe_size[q][e];
+            atomicMin(&s_tmin, (unsigned long long)tc);
+        } else {
+            const int j = atomicAdd(&s_keep, 1);
+            r.qe_key[q ^ 1][j] = r.qe_key[q][e];
+            r.qe_lab[q ^ 1][j] = r.qe_lab[q][e];
+            r.qe_size[q ^ 1][j] = r.qe_size[q][e];
+            r.qe_dur[q ^ 1][j] = r.qe_dur[q][e];
+        }
+    }
+    started = __reduce_add_sync(0xFFFFFFFFu, (unsigned)started);
+    if (lane == 0 && started) atomicAdd((unsigned long long*)r.busy, (unsigned long long)started);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        r.qn[q ^ 1] = s_keep;
+        r.qn[q] = 0;
+        *r.qcur = q ^ 1;
+        r.qctl->sort_or = 0;
+        // the clock (k_disp_b's last block without capacity)
+        unsigned long long tn = *(volatile unsigned long long*)r.tnext;
+        tn = min(tn, s_tmin);
+        const int act = *(volatile int32_t*)r.active_flag;
+        if (act) {
+            r.rounds[0] += 1;
+            if (tn == (unsigned long long)LLONG_MAX || tn == ~0ull) *r.liveness = 1;
+            else r.t_sim[0] = r.Q > 0 ? (((long long)tn + r.Q - 1) / r.Q) * r.Q : (long long)tn;
+        }
+        r.tnext[0] = LLONG_MAX;
+        r.active_flag[0] = 0;
+    }
+}
+
 // dispatch, part a: cluster completion time = t + max member duration (atomicMax at
 // the cluster's root label; a stale value is <= t).
 __global__ void __launch_bounds__(256) k_disp_a(RepDev r)
@@ -380,6 +521,7 @@ __global__ void __launch_bounds__(256) k_disp_a(RepDev r)
         const long long du = duration(r.sy, i, r.steps[i]);
         const long long tc = r.t_sim[b] + du;
         atomicMax((unsigned long long*)(r.tcl + d.labels[i]), (unsigned long long)tc);
+        if (r.K > 0) atomicAdd(r.qsz + d.labels[i], 1);   // the cluster's size (finite capacity)
         if (d.n_sims > 1) atomicAdd((unsigned long long*)(r.llm + b), (unsigned long long)(du - r.sy.base_us));
         else busy += (unsigned long long)(du - r.sy.base_us);
     }
@@ -403,15 +545,37 @@ __global__ void __launch_bounds__(256) k_disp_b(RepDev r)
     const Dev& d = r.d;
     const int nr = d.ctl->n_ready;
     unsigned long long tmin = ~0ull;
+    const bool cap = r.K > 0;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x) {
         const int i = r.order[k];
         const int b = sim_of(d, i);
-        const long long tc = r.tcl[d.labels[i]];
-        r.tcommit[i] = tc;
+        const int lab = d.labels[i];
+        const long long tc = r.tcl[lab];
         r.newpos[i] = policy_move(r, i, r.steps[i], r.pos[i], d.digest[i]);
+        if (cap) {
+            // queued (members RUNNING, moves computed now): key (step, label) in step-priority
+            // order (section 3.5) or (round, label) in FIFO order
+            const unsigned long long hi = r.prio ? (unsigned long long)(uint32_t)r.steps[i]
+                                                 : (unsigned long long)r.rounds[0];
+            const unsigned long long key = (hi << r.qidb) | (unsigned long long)(uint32_t)lab;
+            r.tcommit[i] = LLONG_MAX;
+            r.qkey[i] = key;
+            if (i == lab) {   // the cluster's entry, from its min-id member
+                const int q = *r.qcur;
+                const int e = atomicAdd(r.qn + q, 1);
+                r.qe_key[q][e] = key;
+                r.qe_lab[q][e] = lab;
+                r.qe_size[q][e] = r.qsz[lab];
+                r.qe_dur[q][e] = tc - r.t_sim[0];
+                r.qsz[lab] = 0;
+            }
+            continue;
+        }
+        r.tcommit[i] = tc;
         if (d.n_sims > 1) atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc);
         else tmin = min(tmin, (unsigned long long)tc);
     }
+    if (cap) return;   // the queue's starts and the clock: k_qprep / k_csort / k_qstart
     if (d.n_sims == 1) {  // block reduction, one atomic per block
         __shared__ unsigned long long s_min[8];
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -725,6 +889,7 @@ struct am_replay {
     cudaStream_t stream = nullptr;      // own stream (graph capture)
     cudaStream_t user_stream = nullptr;
     cudaGraphExec_t g1 = nullptr, g8 = nullptr, g1x = nullptr;   // g1x: one host-buffer (external) round
+    Dev qsd{};                          // finite capacity, binned path: the queue sort's view
     unsigned graph_prof = 0;            // profiling mask the graphs were captured with
     uint32_t graph_flags = 0;           // context flags the graphs were captured with
     long long* h_buf = nullptr;         // pinned: dispatched, liveness
@@ -788,6 +953,13 @@ static int enqueue_round(am_replay* rp, bool external = false)
     am_join_digest(c);   // part b reads the digests (computed beside part a)
     am_prof_begin(c, K_DISP_B);
     RK(launch_k(c->pdl, rp->stream, k_disp_b, nbd, 256, 0, rp->r));
+    if (rp->r.K > 0 && c->path == 1) {
+        // finite capacity: the queued clusters sorted by key, started while they fit
+        RK(launch_k(c->pdl, rp->stream, k_qprep, nbd, 256, 0, rp->r));
+        const int qrc = am_internal_csort(c, rp->qsd, rp->r.qorder, rp->stream);
+        if (qrc) return qrc;
+        RK(launch_k(false, rp->stream, k_qstart, 1, 1024, 0, rp->r));
+    }
     am_prof_end(c, K_DISP_B);
     am_prof_begin(c, K_COMMIT);
     if (inplace && c->d.n_sims == 1 && AM_COMMIT_SPLIT) {
@@ -807,6 +979,8 @@ static int enqueue_round(am_replay* rp, bool external = false)
 // device workspace layout of a replay (caller-owned, am_replay_workspace_size)
 struct RepLayout {
     size_t total, tc, np, tr, tcl, ts, tn, td, rd, af, disp, live, chain, qk, mask, order, shadow, part, llm, clist;
+    size_t qsz = 0, qek[2] = {}, qel[2] = {}, qes[2] = {}, qed[2] = {}, qrk[2] = {}, qrv[2] = {}, qn = 0, qcur = 0,
+           qst = 0, qsep = 0, busy = 0, qorder = 0, qctl = 0;
 };
 static RepLayout rep_layout(const am_ctx* ctx)
 {
@@ -822,6 +996,15 @@ static RepLayout rep_layout(const am_ctx* ctx)
     L.part = take(32 * ((n + 256 * kCommitItems - 1) / (256 * kCommitItems)));   // k_commit partials
     L.llm = take(8 * std::max(S, 16LL * 64));   // one simulation: 64 stripes of 128 bytes
     L.clist = take(4 * n);
+    if (ctx->path == 1) {   // finite capacity on the cell-binned path: the cluster queue
+        L.qsz = take(4 * n);
+        for (int b = 0; b < 2; b++) {
+            L.qek[b] = take(8 * n); L.qel[b] = take(4 * n); L.qes[b] = take(4 * n); L.qed[b] = take(8 * n);
+            L.qrk[b] = take(8 * n); L.qrv[b] = take(4 * n);
+        }
+        L.qn = take(8); L.qcur = take(4); L.qst = take(8 * n); L.qsep = take(4 * n); L.busy = take(8);
+        L.qorder = take(4 * n); L.qctl = take(sizeof(Ctl));
+    }
     L.total = off;
     return L;
 }
@@ -897,12 +1080,29 @@ extern "C" int am_replay_create(am_replay** out, am_ctx* ctx, const am_synth* sy
     r.part = (int32_t*)(b + L.part);
     r.llm = (long long*)(b + L.llm);
     r.clist = (int32_t*)(b + L.clist);
+    if (ctx->path == 1) {
+        r.qsz = (int32_t*)(b + L.qsz);
+        for (int q = 0; q < 2; q++) {
+            r.qe_key[q] = (unsigned long long*)(b + L.qek[q]); r.qe_lab[q] = (int32_t*)(b + L.qel[q]);
+            r.qe_size[q] = (int32_t*)(b + L.qes[q]); r.qe_dur[q] = (long long*)(b + L.qed[q]);
+            r.qrk[q] = (unsigned long long*)(b + L.qrk[q]); r.qrv[q] = (uint32_t*)(b + L.qrv[q]);
+        }
+        r.qn = (int32_t*)(b + L.qn); r.qcur = (int32_t*)(b + L.qcur);
+        r.qstart_t = (long long*)(b + L.qst); r.qstart_ep = (uint32_t*)(b + L.qsep);
+        r.busy = (long long*)(b + L.busy); r.qorder = (int32_t*)(b + L.qorder); r.qctl = (Ctl*)(b + L.qctl);
+        r.qidb = ctx->d.idbits;
+        rp->qsd = ctx->d;   // the queue sort's view: its keys / ids and control block
+        rp->qsd.ctl = r.qctl;
+        rp->qsd.rkey[0] = r.qrk[0]; rp->qsd.rkey[1] = r.qrk[1];
+        rp->qsd.rval[0] = r.qrv[0]; rp->qsd.rval[1] = r.qrv[1];
+    }
     r.order = ctx->path == 1 ? ctx->d.rid : rp->order;
     RK(cudaStreamCreateWithFlags(&rp->stream, cudaStreamNonBlocking));
     RK(cudaMallocHost((void**)&rp->h_buf, 64));
     RK(cudaStreamSynchronize(rp->user_stream));
     RK(cudaMemsetAsync(rp->mem, 0, off, rp->stream));
     RK(cudaMemsetAsync(r.tnext, 0x7F, 8 * S, rp->stream));  // "no pending" marker
+    if (ctx->path == 1) RK(cudaMemsetAsync(r.qstart_ep, 0xFF, 4 * (size_t)std::max(1, ctx->d.n), rp->stream));
     RK(cudaStreamSynchronize(rp->stream));
     // tnext must be exactly LLONG_MAX: fill with a tiny copy
     {
@@ -993,7 +1193,7 @@ static int finish_check(am_replay* rp, int64_t* active)
 
 static int ensure_graphs(am_replay* rp)
 {
-    if (rp->r.K > 0 || rp->r.sy.conflict) {   // only the persistent per-simulation kernel has these
+    if ((rp->r.K > 0 && rp->ctx->path == 0) || rp->r.sy.conflict) {   // only the persistent per-simulation kernel has these
         rp->ctx->err = "finite LLM capacity and exclusive tiles run through am_replay_run / am_replay_launch "
                        "on the fused per-simulation path (<= 1024 agents per simulation, tracing off)";
         return AM_E_ARG;
@@ -1020,7 +1220,7 @@ static int ensure_graphs(am_replay* rp)
 static bool small_persistent(am_replay* rp)
 {
     am_ctx* c = rp->ctx;
-    if (rp->r.K > 0 || rp->r.sy.conflict) return c->path == 0;   // only the persistent kernel has them
+    if ((rp->r.K > 0 && c->path == 0) || rp->r.sy.conflict) return c->path == 0;   // only the persistent kernel has them
     if (c->path != 0 || c->prof.on) return false;
     static const int off = [] { const char* e = getenv("AM_SMALL_PERSIST"); return e && atoi(e) == 0; }();
     return !off;   // AM_SMALL_PERSIST=0: the multi-kernel rounds (ablation)
@@ -1088,8 +1288,8 @@ extern "C" int am_replay_set_capacity(am_replay* rp, int64_t capacity, int32_t p
         rp->ctx->err = "am_replay_set_capacity: only before the first round";
         return AM_E_STATE;
     }
-    if (capacity > 0 && !(rp->ctx->path == 0)) {
-        rp->ctx->err = "am_replay_set_capacity: finite capacity needs the fused per-simulation path";
+    if (capacity > 0 && rp->ctx->path == 1 && rp->ctx->d.n_sims != 1) {
+        rp->ctx->err = "am_replay_set_capacity: the cell-binned path takes one simulation";
         return AM_E_ARG;
     }
     rp->r.K = capacity;
@@ -1100,8 +1300,9 @@ extern "C" int am_replay_set_capacity(am_replay* rp, int64_t capacity, int32_t p
 extern "C" int am_replay_step(am_replay* rp, uint8_t* mask, int32_t* order, int32_t* labels, int32_t* n_ready)
 {
     if (!rp) return AM_E_ARG;
-    if (rp->r.K > 0 || rp->r.sy.conflict) {
-        rp->ctx->err = "am_replay_step: not available with a finite capacity or exclusive tiles (use am_replay_run)";
+    if ((rp->r.K > 0 && rp->ctx->path == 0) || rp->r.sy.conflict) {
+        rp->ctx->err = "am_replay_step: not available with a finite capacity on the fused path or exclusive tiles "
+                       "(use am_replay_run)";
         return AM_E_ARG;
     }
     int rc = enqueue_round(rp);

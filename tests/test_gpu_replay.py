@@ -181,24 +181,30 @@ def test_persistent_small_replay_equals_round_kernels(name, n_sims):
     b.close()
 
 
-@pytest.mark.parametrize("name,steps,n_sims,K,prio", [
-    ("C1", 300, None, 1, True),
-    ("C1", 300, None, 4, False),
-    ("C1", 300, None, 8, True),
-    ("C2", 60, None, 32, True),
-    ("C2", 60, None, 32, False),
-    ("C3", 120, 16, 3, True),
+@pytest.mark.parametrize("name,steps,n_sims,K,prio,path", [
+    ("C1", 300, None, 1, True, None),
+    ("C1", 300, None, 4, False, None),
+    ("C1", 300, None, 8, True, None),
+    ("C2", 60, None, 32, True, None),
+    ("C2", 60, None, 32, False, None),
+    ("C3", 120, 16, 3, True, None),
+    ("C2", 60, None, 32, True, "binned"),
+    ("C2", 60, None, 32, False, "binned"),
+    ("C1", 200, None, 2, True, "binned"),
+    ("C4", 15, 1500, 64, True, "binned"),
+    ("C4", 15, 1500, 64, False, "binned"),
 ])
-def test_capacity_replay_vs_oracle(name, steps, n_sims, K, prio):
-    """Finite LLM capacity (am_replay_set_capacity, persistent per-simulation kernel) vs
-    orc_replay_cap: T_ooo, round counts, final positions and trajectory hashes, bit for
-    bit; the outcome equals lock-step's."""
+def test_capacity_replay_vs_oracle(name, steps, n_sims, K, prio, path):
+    """Finite LLM capacity (am_replay_set_capacity: the persistent per-simulation kernel,
+    or on the cell-binned path the device queue of ready clusters sorted by key and started
+    while they fit) vs orc_replay_cap: T_ooo, round counts, final positions and trajectory
+    hashes, bit for bit; the outcome equals lock-step's."""
     w = amgen.config(name, steps=steps, n=n_sims)
     lm = amgen.latency_model(w.profile)
     sy = O.SynthTables.from_model(lm, wall=w.wall)
     p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps, n_sims=w.n_sims)
     r = O.replay(p, sy, w.x, w.y, Q=w.Q, capacity=K, priority=prio)
-    rep = Replay.from_workload(w, lm, capacity=K, priority=prio)
+    rep = Replay.from_workload(w, lm, capacity=K, priority=prio, force=path)
     rep.run_to_end()
     res = rep.results()
     for k in ("T_ooo", "rounds", "x", "y", "traj"):
@@ -206,8 +212,30 @@ def test_capacity_replay_vs_oracle(name, steps, n_sims, K, prio):
     ls = O.lockstep(p, sy, w.x, w.y, w.steps)
     np.testing.assert_array_equal(res["traj"], ls["traj"])
     assert rep.dispatched() == len(w.x) * w.steps
-    with pytest.raises(Exception):
-        rep.step()   # finite capacity exists only in the persistent kernel
+    if path is None:
+        with pytest.raises(Exception):
+            rep.step()   # on the fused path finite capacity exists only in the persistent kernel
+
+
+def test_capacity_binned_round_logs_vs_oracle():
+    """The binned path with a finite capacity, round by round: the dispatched (queued)
+    agents' ids and labels of every round equal orc_replay_cap's log."""
+    w = amgen.config("C2", steps=30)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps)
+    r = O.replay(p, sy, w.x, w.y, Q=w.Q, capacity=24, priority=True, log_rounds=10**6,
+                 log_entries=len(w.x) * w.steps + 10)
+    rep = Replay.from_workload(w, lm, capacity=24, priority=True, force="binned")
+    glogs = _gpu_logged(rep, 1, len(w.x))
+    ologs = _split_oracle_log(r, 1)
+    assert len(glogs[0]) == len(ologs[0])
+    for (gi, gl), (oi, ol) in zip(glogs[0], ologs[0]):
+        np.testing.assert_array_equal(gi, oi)
+        np.testing.assert_array_equal(gl, ol)
+    res = rep.results()
+    np.testing.assert_array_equal(res["traj"], r["traj"])
+    rep.close()
     rep.close()
 
 
