@@ -110,10 +110,11 @@ int am_replay_results(am_replay* r, int64_t* T_ooo, int64_t* rounds, uint64_t* t
  * start + max member duration -- in the order of the key (step << 32 | label) when
  * priority != 0 (the paper's step-priority ready_queue, section 3.5),
  * else (round << 32 | label) (FIFO); strict order, a cluster larger than the capacity
- * starts only when nothing is in service.  Only the fused per-simulation path
- * (<= 1024 agents per simulation) supports it, through am_replay_run / am_replay_launch
- * (am_replay_step / am_replay_io return AM_E_ARG).  Errors: AM_E_ARG, AM_E_STATE (rounds
- * already ran). */
+ * starts only when nothing is in service.  The fused per-simulation path runs it in the
+ * persistent kernel (am_replay_run / am_replay_launch; am_replay_step / am_replay_io
+ * return AM_E_ARG there); the cell-binned path (one simulation) keeps a device queue of
+ * ready clusters, sorted each round by the one-kernel cluster sort and started in key
+ * order while they fit (every call).  Errors: AM_E_ARG, AM_E_STATE (rounds already ran). */
 int am_replay_set_capacity(am_replay* r, int64_t capacity, int32_t priority);
 
 /* LLM busy time dispatched so far per simulation (host int64 [n_sims], microseconds):

@@ -259,9 +259,9 @@ def test_linf_eight_connected_replay_vs_oracle(path):
 
 
 def test_capacity_api_errors():
-    """am_replay_set_capacity: only before the first round (AM_E_STATE), only on the fused
-    per-simulation path (AM_E_ARG); the multi-kernel entry points refuse a finite
-    capacity."""
+    """am_replay_set_capacity: only before the first round (AM_E_STATE) and with a
+    non-negative capacity (AM_E_ARG); both paths accept it before the first round (the
+    cell-binned path keeps its device queue)."""
     from paper_2411_03519_b200 import AmError, _lib
     w = amgen.config("C1", steps=20)
     lm = amgen.latency_model(w.profile)
@@ -273,8 +273,13 @@ def test_capacity_api_errors():
     rep.close()
     rep = Replay.from_workload(w, lm, force="binned")
     with pytest.raises(AmError) as e:
-        _lib.check(rep.L.am_replay_set_capacity(rep.h, 4, 1), rep.tracker.ctx)
+        _lib.check(rep.L.am_replay_set_capacity(rep.h, -1, 1), rep.tracker.ctx)
     assert e.value.code == _lib.E_ARG
+    _lib.check(rep.L.am_replay_set_capacity(rep.h, 4, 1), rep.tracker.ctx)
+    rep.run(3)
+    with pytest.raises(AmError) as e:
+        _lib.check(rep.L.am_replay_set_capacity(rep.h, 8, 1), rep.tracker.ctx)
+    assert e.value.code == _lib.E_STATE
     rep.close()
 
 
