@@ -12,6 +12,9 @@ restates in oracle.c.  Parity status per function:
   tests/golden, BFS components, invariants, brute force on tiny maps).
 * replay / lockstep: pinned by the closed forms D1-D5 and the OoO == lock-step
   outcome invariant.
+* replay_stale (stale-halo slabs, NEXT #3): pinned by P = 1 == replay round for round,
+  zero I1/I2 violations and OoO == lock-step for every P and G, and hand states where a
+  stale ghost must defer (tests/test_oracle_stale.py).
 * duration / policy_move / digest / key3 / the trajectory hash (synthetic driver,
   Q16): the paper is silent -- our own constructs; pinned against an
   independent pure-Python implementation of the c.4 definitions built on splitmix64's
@@ -114,6 +117,8 @@ def lib():
                                  C.POINTER(Log)]
         L.orc_replay_cap.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int64, C.c_int64, C.c_int32,
                                      vp, vp, vp, vp, vp, C.POINTER(Log)]
+        L.orc_replay_stale.argtypes = [P, C.POINTER(Synth), C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                       vp, vp, vp, vp, vp, C.POINTER(Log)]
         # oracle_scale.c
         L.orc_round_mt.argtypes = [P, C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp, vp, vp, vp, C.c_int32]
         L.orc_labels_steps.argtypes = [P, C.c_int32, vp, vp, vp, vp, vp, C.c_int32]
@@ -282,6 +287,28 @@ def lockstep(p: Params, sy: SynthTables, x0, y0, T: int):
     return dict(x=x, y=y, traj=traj, T_sync=tsync)
 
 
+class _LogBufs:
+    """The per-round log arrays of a replay (orc_log)."""
+
+    def __init__(self, log_rounds: int, log_entries: int, check: bool):
+        self.caps = (log_rounds, log_entries)
+        self.rt = np.zeros(max(log_rounds, 1), np.int64)
+        self.rs = np.zeros(max(log_rounds, 1), np.int32)
+        self.rn = np.zeros(max(log_rounds, 1), np.int32)
+        self.eid = np.zeros(max(log_entries, 1), np.int32)
+        self.elab = np.zeros(max(log_entries, 1), np.int32)
+        self.lg = Log(log_rounds, log_entries, _p(self.rt).value, _p(self.rs).value, _p(self.rn).value,
+                      _p(self.eid).value, _p(self.elab).value, 0, 0, int(check), 0, 0)
+
+    def result(self, **kw):
+        lg, (cr, ce) = self.lg, self.caps
+        nr, ne = min(lg.n_rounds, cr), min(lg.n_entries, ce)
+        return dict(kw, log_t=self.rt[:nr].copy(), log_sim=self.rs[:nr].copy(), log_nready=self.rn[:nr].copy(),
+                    log_id=self.eid[:ne].copy(), log_label=self.elab[:ne].copy(),
+                    log_complete=(lg.n_rounds <= cr and lg.n_entries <= ce),
+                    violations=int(lg.violations), max_spread=int(lg.max_spread))
+
+
 def replay(p: Params, sy: SynthTables, x0, y0, Q: int = 0, log_rounds: int = 0,
            log_entries: int = 0, check: bool = False, capacity: int = 0, priority: bool = True):
     """Out-of-order replay (orc_replay; orc_replay_cap with a finite capacity of
@@ -292,24 +319,29 @@ def replay(p: Params, sy: SynthTables, x0, y0, Q: int = 0, log_rounds: int = 0,
     traj = np.zeros(n, np.uint64)
     tooo = np.zeros(p.n_sims, np.int64)
     rounds = np.zeros(p.n_sims, np.int64)
-    rt = np.zeros(max(log_rounds, 1), np.int64)
-    rs = np.zeros(max(log_rounds, 1), np.int32)
-    rn = np.zeros(max(log_rounds, 1), np.int32)
-    eid = np.zeros(max(log_entries, 1), np.int32)
-    elab = np.zeros(max(log_entries, 1), np.int32)
-    lg = Log(log_rounds, log_entries, _p(rt).value, _p(rs).value, _p(rn).value, _p(eid).value,
-             _p(elab).value, 0, 0, int(check), 0, 0)
+    lb = _LogBufs(log_rounds, log_entries, check)
     rc = lib().orc_replay_cap(C.byref(p), C.byref(sy.s), n, int(Q), int(capacity), int(bool(priority)), _p(x),
-                              _p(y), _p(traj), _p(tooo), _p(rounds), C.byref(lg))
+                              _p(y), _p(traj), _p(tooo), _p(rounds), C.byref(lb.lg))
     if rc != OK:
         raise RuntimeError(f"orc_replay rc={rc}")
-    nr = min(lg.n_rounds, log_rounds)
-    ne = min(lg.n_entries, log_entries)
-    return dict(x=x, y=y, traj=traj, T_ooo=tooo, rounds=rounds,
-                log_t=rt[:nr].copy(), log_sim=rs[:nr].copy(), log_nready=rn[:nr].copy(),
-                log_id=eid[:ne].copy(), log_label=elab[:ne].copy(),
-                log_complete=(lg.n_rounds <= log_rounds and lg.n_entries <= log_entries),
-                violations=int(lg.violations), max_spread=int(lg.max_spread))
+    return lb.result(x=x, y=y, traj=traj, T_ooo=tooo, rounds=rounds)
+
+
+def replay_stale(p: Params, sy: SynthTables, x0, y0, G: int, P: int, Q: int = 0, log_rounds: int = 0,
+                 log_entries: int = 0, check: bool = False):
+    """Stale-halo replay over G horizontal slabs with a sync round every P rounds
+    (orc_replay_stale, SURVEY 8(f) NEXT #3).  One simulation; P = 1 is replay()."""
+    x, y = _i32(x0).copy(), _i32(y0).copy()
+    n = len(x)
+    traj = np.zeros(n, np.uint64)
+    tooo = np.zeros(1, np.int64)
+    rounds = np.zeros(1, np.int64)
+    lb = _LogBufs(log_rounds, log_entries, check)
+    rc = lib().orc_replay_stale(C.byref(p), C.byref(sy.s), n, int(Q), int(G), int(P), _p(x), _p(y), _p(traj),
+                                _p(tooo), _p(rounds), C.byref(lb.lg))
+    if rc != OK:
+        raise RuntimeError(f"orc_replay_stale rc={rc}")
+    return lb.result(x=x, y=y, traj=traj, T_ooo=tooo, rounds=rounds)
 
 
 # ------------------------------------------------------------------ at BASELINE sizes

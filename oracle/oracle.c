@@ -715,3 +715,163 @@ int orc_replay_cap(const orc_params* p, const orc_synth* sy, int32_t n, int64_t 
     free(wk.step); free(wk.status); free(wk.tc); free(wk.mvx); free(wk.mvy); free(wk.cmax); free(wk.qkey);
     return rc;
 }
+
+/*
+ * Stale-halo replay over G horizontal slabs (derived from App. A:
+ * the blocking radius shrinks by exactly the blocker's progress, so a
+ * blocker seen at an older step and position still blocks whenever the real one does;
+ * the slab exchange itself is this repo's design, include/am_slab.h).  One simulation,
+ * infinite capacity, no exclusive tiles.  Slab k owns the rows [k*H/G, (k+1)*H/G).
+ * Rounds are counted from 0 while some agent is not DONE; round r is a SYNC round when
+ * r % P == 0, else a STALE round.  At the start of every sync round (after its commits)
+ * the snapshot (x, y, step, DONE) of every agent is kept and every agent's owner becomes
+ * the slab of its row; owners stay fixed until the next sync round.
+ *   sync round:  orc_replay's round (global, with dispatch).
+ *   stale round: for every slab k, the agents k owns at their current state and every
+ *     other agent at its snapshot, as RUNNING unless DONE: orc_round (peek) over that
+ *     mixed state; the agents k owns that are ready in it are dispatched, labelled with
+ *     their mixed-state label; the round's order is every dispatched agent by
+ *     (step, label, id) (Q9).
+ * The rest is orc_replay_sim's loop: cluster completion times, moves from the perception
+ * digest of the current state, commits, the clock.  A stale round after which nothing is
+ * pending leaves the clock where it is (the rounds up to the next sync round may then be
+ * idle); only a sync round with nothing pending is a liveness failure.  P = 1 is
+ * orc_replay.  That every dispatch is safe and the final state equals lock-step for any P
+ * is tested (tests/test_oracle_stale.py), not assumed here.
+ */
+static int32_t slab_of_row(int32_t yy, int32_t G, int32_t H)
+{
+    int32_t k = 0;
+    while (k + 1 < G && (int64_t)(k + 1) * H / G <= yy) k++;
+    return k;
+}
+
+int orc_replay_stale(const orc_params* p, const orc_synth* sy, int32_t n, int64_t Q, int32_t G, int32_t P,
+                     int32_t* x, int32_t* y, uint64_t* traj, int64_t* T_ooo, int64_t* rounds, orc_log* log)
+{
+    if (p->target <= 0 || p->n_sims != 1 || G < 1 || P < 1 || sy->conflict || p->metric == ORC_GRAPH) return ORC_E_ARG;
+    size_t nn = (size_t)(n ? n : 1);
+    int32_t* step = (int32_t*)calloc(nn, sizeof(int32_t));
+    uint8_t* status = (uint8_t*)calloc(nn, 1);
+    int64_t* tc = (int64_t*)malloc(sizeof(int64_t) * nn);
+    int32_t* mvx = (int32_t*)malloc(sizeof(int32_t) * nn);
+    int32_t* mvy = (int32_t*)malloc(sizeof(int32_t) * nn);
+    int64_t* cmax = (int64_t*)calloc(nn, sizeof(int64_t));
+    int32_t* owner = (int32_t*)calloc(nn, sizeof(int32_t));
+    int32_t *x0 = (int32_t*)malloc(sizeof(int32_t) * nn), *y0 = (int32_t*)malloc(sizeof(int32_t) * nn);
+    int32_t* s0 = (int32_t*)malloc(sizeof(int32_t) * nn);
+    uint8_t* d0 = (uint8_t*)malloc(nn);
+    int32_t *xm = (int32_t*)malloc(sizeof(int32_t) * nn), *ym = (int32_t*)malloc(sizeof(int32_t) * nn);
+    int32_t* sm = (int32_t*)malloc(sizeof(int32_t) * nn);
+    uint8_t* stm = (uint8_t*)malloc(nn);
+    int32_t* lab = (int32_t*)malloc(sizeof(int32_t) * nn);
+    int32_t* labk = (int32_t*)malloc(sizeof(int32_t) * nn);
+    uint8_t* msk = (uint8_t*)malloc(nn);
+    uint8_t* blk = (uint8_t*)malloc(nn);
+    int32_t* ord = (int32_t*)malloc(sizeof(int32_t) * nn);
+    ord_key* keys = (ord_key*)malloc(sizeof(ord_key) * nn);
+    int rc = ORC_OK;
+    int64_t t = 0, r = 0;
+    if (log) { log->n_rounds = 0; log->n_entries = 0; log->violations = 0; log->max_spread = 0; }
+    for (int32_t i = 0; i < n; i++) { traj[i] = 0; tc[i] = INT64_MAX; }
+    for (;;) {
+        /* commit (Alg. 3 worker l.20 + controller l.11-12) */
+        for (int32_t i = 0; i < n; i++) {
+            if (status[i] == ORC_RUNNING && tc[i] <= t) {
+                x[i] = mvx[i]; y[i] = mvy[i]; step[i] += 1;
+                status[i] = (step[i] == p->target) ? ORC_DONE : ORC_IDLE;
+                traj[i] = traj_step(traj[i], step[i], x[i], y[i]);
+            }
+        }
+        if (log && log->check && orc_validity_violations(p, n, x, y, step) != 0) log->violations++;
+        int32_t all_done = 1, W = INT32_MAX, S = INT32_MIN;
+        for (int32_t i = 0; i < n; i++)
+            if (status[i] != ORC_DONE) {
+                all_done = 0;
+                if (step[i] < W) W = step[i];
+                if (step[i] > S) S = step[i];
+            }
+        if (all_done) break;
+        if (log && (int64_t)S - W > log->max_spread) log->max_spread = (int64_t)S - W;
+        const int sync = (r % P) == 0;
+        int32_t nr = 0;
+        if (sync) {
+            /* the snapshot and the owners of the rounds up to the next sync round */
+            for (int32_t i = 0; i < n; i++) {
+                x0[i] = x[i]; y0[i] = y[i]; s0[i] = step[i]; d0[i] = status[i] == ORC_DONE;
+                owner[i] = slab_of_row(y[i], G, p->map_h);
+            }
+            orc_round(p, n, x, y, step, status, 0, blk, lab, msk, ord, &nr);
+        } else {
+            for (int32_t k = 0; k < G; k++) {
+                for (int32_t i = 0; i < n; i++) {
+                    if (owner[i] == k) { xm[i] = x[i]; ym[i] = y[i]; sm[i] = step[i]; stm[i] = status[i]; }
+                    else { xm[i] = x0[i]; ym[i] = y0[i]; sm[i] = s0[i]; stm[i] = d0[i] ? ORC_DONE : ORC_RUNNING; }
+                }
+                int32_t nk = 0;
+                orc_round(p, n, xm, ym, sm, stm, 1, blk, labk, msk, ord, &nk);
+                for (int32_t i = 0; i < n; i++)
+                    if (owner[i] == k && msk[i]) {
+                        lab[i] = labk[i];
+                        keys[nr].sim = 0; keys[nr].step = step[i]; keys[nr].label = labk[i]; keys[nr].id = i;
+                        nr++;
+                    }
+            }
+            qsort(keys, (size_t)nr, sizeof(ord_key), ord_cmp);
+            for (int32_t q = 0; q < nr; q++) { ord[q] = keys[q].id; status[ord[q]] = ORC_RUNNING; }
+        }
+        r++;
+        if (log && log->n_rounds < log->cap_rounds) {
+            if (log->round_t) log->round_t[log->n_rounds] = t;
+            if (log->round_sim) log->round_sim[log->n_rounds] = 0;
+            if (log->round_nready) log->round_nready[log->n_rounds] = nr;
+            log->n_rounds++;
+            for (int32_t q = 0; q < nr; q++) {
+                if (log->n_entries < log->cap_entries) {
+                    if (log->entry_id) log->entry_id[log->n_entries] = ord[q];
+                    if (log->entry_label) log->entry_label[log->n_entries] = lab[ord[q]];
+                    log->n_entries++;
+                }
+            }
+        }
+        /* I1 safety at dispatch, on the real state */
+        if (log && log->check) {
+            for (int32_t q = 0; q < nr; q++) {
+                int32_t a = ord[q];
+                for (int32_t j = 0; j < n; j++)
+                    if (j != a && status[j] != ORC_DONE &&
+                        orc_blocked_by(p, x[a], y[a], step[a], x[j], y[j], step[j]))
+                        log->violations++;
+            }
+        }
+        /* dispatch: cluster completion time and the members' moves */
+        for (int32_t q = 0; q < nr; q++) cmax[lab[ord[q]]] = 0;
+        for (int32_t q = 0; q < nr; q++) {
+            int32_t a = ord[q];
+            int64_t d = orc_duration(sy, a, step[a]);
+            if (d > cmax[lab[a]]) cmax[lab[a]] = d;
+        }
+        for (int32_t q = 0; q < nr; q++) {
+            int32_t a = ord[q];
+            tc[a] = t + cmax[lab[a]];
+            uint64_t dg = orc_digest(p, 0, n, x, y, step, status, a);
+            orc_policy_move(p, sy, a, step[a], x[a], y[a], dg, &mvx[a], &mvy[a]);
+        }
+        /* next event */
+        int64_t tn = INT64_MAX;
+        for (int32_t i = 0; i < n; i++)
+            if (status[i] == ORC_RUNNING && tc[i] < tn) tn = tc[i];
+        if (tn == INT64_MAX) {
+            if (sync) { rc = ORC_E_LIVENESS; break; }
+            continue;   /* nothing pending after a stale round: the clock stays */
+        }
+        if (Q > 0) tn = ((tn + Q - 1) / Q) * Q;
+        t = tn;
+    }
+    T_ooo[0] = t;
+    rounds[0] = r;
+    free(step); free(status); free(tc); free(mvx); free(mvy); free(cmax); free(owner);
+    free(x0); free(y0); free(s0); free(d0); free(xm); free(ym); free(sm); free(stm);
+    free(lab); free(labk); free(msk); free(blk); free(ord); free(keys);
+    return rc;
+}
