@@ -379,13 +379,15 @@ def snapshot_rounds(rep, w, dev, flush, reps: int = 20):
                     "L2 flushed before each round"}
 
 
-def virtual_slabs(w, lm, dev, slab_counts=(2, 8), preroll=200, timed=4):
+def virtual_slabs(w, lm, dev, slab_counts=((2, 1), (8, 1), (8, 4)), preroll=200, timed=8):
     """S7 + S8 on one GPU: the C5 replay split into G horizontal slabs
     (slabs.LoopbackWorld: the library calls of the NCCL run, exchanges as device copies),
     pre-rolled `preroll` rounds from t = 0, then `timed` rounds with every rank's own
     device time recorded (its library steps; the exchanges are NCCL's in a real run): the
-    slowest rank's time is what one GPU of a G-GPU run computes per round.  Checked
-    against the single-GPU replay after the same rounds (agent-steps dispatched)."""
+    slowest rank's time is what one GPU of a G-GPU run computes per round.  (G, P): P > 1
+    = stale-halo rounds (NEXT #3), a sync round every P rounds, reported as the mean over
+    whole periods.  Synchronous runs are checked against the single-GPU replay after the
+    same rounds (agent-steps dispatched)."""
     import torch
 
     from paper_2411_03519_b200 import Replay, slabs
@@ -394,10 +396,10 @@ def virtual_slabs(w, lm, dev, slab_counts=(2, 8), preroll=200, timed=4):
     ref = one.dispatched()
     one.close()
     out = {}
-    for G in slab_counts:
+    for G, P in slab_counts:
         sy = slabs.Synth(lm, device=dev)
         wd = slabs.LoopbackWorld(w.map_w, w.map_h, w.r_p, w.v, w.x, w.y, w.steps, sy, w.Q, G, device=dev,
-                                 check_rounds=16)
+                                 check_rounds=16, stale_rounds=P)
         done = 0
         while done < preroll:
             k = min(wd.K, preroll - done)
@@ -411,11 +413,19 @@ def virtual_slabs(w, lm, dev, slab_counts=(2, 8), preroll=200, timed=4):
         wd.check()
         per = [max(r[k] for r in tl[1:] or tl) for k in range(G)]   # worst round per rank
         med = [sorted(r[k] for r in tl)[len(tl) // 2] for k in range(G)]
+        mean = [sum(r[k] for r in tl) / len(tl) for k in range(G)]    # whole periods (timed % P == 0)
         disp = wd.dispatched()
-        out[f"G={G}"] = {"rank_round_ms_max_over_ranks": max(med), "rank_round_ms_mean": sum(med) / G,
-                         "rank_round_ms_worst": max(per), "halo_rows": wd.halo, "rewindows": wd.rewindows,
-                         "window_agents_max": max(int((r.w_gid >= 0).sum().item()) for r in wd.ranks),
-                         "dispatched_equals_single_gpu": disp == ref, "rounds": preroll + timed}
+        key = f"G={G}" if P == 1 else f"G={G},P={P}"
+        out[key] = {"rank_round_ms_max_over_ranks": max(med) if P == 1 else max(mean),
+                    "rank_round_ms_mean": sum(med) / G if P == 1 else sum(mean) / G,
+                    "rank_round_ms_worst": max(per), "halo_rows": wd.halo, "rewindows": wd.rewindows,
+                    "window_agents_max": max(int((r.w_gid >= 0).sum().item()) for r in wd.ranks),
+                    "rounds": preroll + timed, "stale_rounds": P}
+        if P == 1:
+            out[key]["dispatched_equals_single_gpu"] = disp == ref
+        else:
+            out[key]["dispatched"] = disp
+            out[key]["dispatched_single_gpu_same_rounds"] = ref
         wd.close()
     return out
 
@@ -446,7 +456,7 @@ def run_slabs(args, w, lm):
         ex = dist
     sy = slabs.Synth(lm, device=dev)
     wd = slabs.DistWorld(ex, w.map_w, w.map_h, w.r_p, w.v, w.x, w.y, w.steps, sy, w.Q, device=dev,
-                         check_rounds=16)
+                         check_rounds=16, stale_rounds=args.slab_stale)
     done = 0
     while done < args.preroll:
         for _ in range(min(wd.K, args.preroll - done)):
@@ -536,6 +546,7 @@ def run_slabs(args, w, lm):
         cfg = _config(w, ws)
         cfg["parallelism"] = f"slabs{ws}" + ("-gloo-staged-one-gpu (test only)" if staged else "")
         cfg["halo_rows"] = wd.halo
+        cfg["stale_rounds"] = args.slab_stale
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -826,6 +837,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--no-snapshot", action="store_true")
+    ap.add_argument("--slab-stale", type=int, default=1, choices=[1, 2, 4, 8, 16],
+                    help="N > 1: a sync round every P rounds (stale-halo rounds between)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     import amgen

@@ -47,6 +47,21 @@
  * The merged result equals the single-GPU round bit for bit (tests/test_gpu_slabs.py),
  * and the replay equals the single-GPU replay and the oracle's.
  *
+ * STALE-HALO ROUNDS (stale_rounds = P > 1).  Only every P-th round
+ * is a sync round as above; the exchange (all-to-all + apply) happens only after the
+ * commits of the round before a sync round, and ownership changes only there.  In the
+ * P - 1 rounds in between each rank runs am_slab_round_stale: its window's tracker round
+ * with the ghosts at their state of the last exchange (RUNNING), the local clusters, and
+ * the dispatch of the owned agents whose cluster holds no ghost and no owned RUNNING or
+ * blocked member -- no merge records, no all-gather; the all-reduce of the stats stays
+ * (the common clock).  Exact by App. A: the blocking radius shrinks by v per
+ * step the blocker advances and the blocker moves at most v per step, so a stale ghost
+ * blocks whenever the real agent does, and a real same-step neighbour is either
+ * blocked-on through its stale copy or that copy sits in the cluster (deferred).  The
+ * schedule equals oracle/orc_replay_stale round for round (tests/test_gpu_slabs.py); the
+ * outcome equals lock-step.  A stale round may leave nothing pending: the clock
+ * then stays and the rounds up to the next sync round are idle.
+ *
  * All arrays are DEVICE pointers; every call is stream-ordered on the slab's stream and
  * none synchronises the host.  Capacity overflows and a halo narrower than the step
  * spread needs are reported through am_slab_flags (checked by the caller every few
@@ -79,6 +94,8 @@ typedef struct {
     int32_t cap_peer;         /* delta records per peer per round                            */
     int32_t cap_merge;        /* link records and cluster records (each) per rank per round, even */
     int32_t check_rounds;     /* K: the caller checks am_slab_flags at least every K rounds  */
+    int32_t stale_rounds;     /* P: a sync round (and exchange) every P rounds; 0 or 1 = every
+                                 round.  halo >= r_p + (P + 1) v                              */
 } am_slab_geom;
 
 typedef struct am_slab am_slab;
@@ -88,7 +105,7 @@ typedef struct am_slab am_slab;
 #define AM_SLAB_OVF_PEER    0x2   /* more delta records for a peer than cap_peer            */
 #define AM_SLAB_OVF_MERGE   0x4   /* more link / cluster records than cap_merge             */
 #define AM_SLAB_HALO        0x8   /* R_b(S - W) + (K + 1) v > halo: re-window before K rounds */
-#define AM_SLAB_LIVENESS    0x10  /* agents not DONE but nothing running                    */
+#define AM_SLAB_LIVENESS    0x10  /* agents not DONE but nothing running after a sync round  */
 #define AM_SLAB_LAG         0x20  /* the step spread exceeds the priority key's lag field    */
 
 /* Exchange buffers (int32 words; fixed capacity, counts inside, so a collective moves
@@ -97,10 +114,12 @@ typedef struct am_slab am_slab;
  *     [0] link count, [1] cluster count, [2..3] 0, then cap_merge links {gid, cluster min
  *     gid}, then cap_merge cluster records {min gid, bad, max duration lo, hi};
  *   delta block for one peer, AM_SLAB_DELTA_WORDS(cap_peer) words:
- *     [0] record count, [1..5] 0, then cap_peer records {gid, x, y, step, traj lo, traj hi};
+ *     [0] record count, [1..5] 0, then cap_peer records {gid, x, y, step, traj lo, traj hi,
+ *     status, completion time lo, hi, move x, move y, 0} (the owner's state: a RUNNING
+ *     agent that changes owner carries its completion time and move);
  *   stats: int64 [4] {next event, W, -S, no agent active} (all-reduce MIN). */
 #define AM_SLAB_MERGE_WORDS(cap) (4 + 6 * (int64_t)(cap))
-#define AM_SLAB_DELTA_WORDS(cap) (6 + 6 * (int64_t)(cap))
+#define AM_SLAB_DELTA_WORDS(cap) (6 + 12 * (int64_t)(cap))
 
 /* Device workspace bytes of a slab (window arrays, its tracker's workspace, the global-id
  * map and merge forest, exchange buffers). */
@@ -130,9 +149,17 @@ int am_slab_round_local(am_slab* s, int32_t* mbuf);
  * this rank's stats (int64 [4]). */
 int am_slab_merge(am_slab* s, const int32_t* mbufs, int32_t* order_out, int32_t* n_order, int64_t* stats);
 
+/* The round of a stale-halo round (instead of round_local + all-gather + merge):
+ * dispatch of the owned agents whose local cluster holds no ghost and no owned RUNNING
+ * or blocked member; outputs as am_slab_merge. */
+int am_slab_round_stale(am_slab* s, int32_t* order_out, int32_t* n_order, int64_t* stats);
+
 /* Step 3: commit at the global next event (stats_global: the all-reduced MIN of the
- * ranks' stats) and pack the deltas: dsend = G delta blocks (block j for rank j; this
- * rank's own block stays empty). */
+ * ranks' stats).  dsend non-NULL (an exchange follows): pack the delta records of every
+ * owned agent committed since the last exchange -- dsend = G delta blocks (block j for
+ * rank j; this rank's own block stays empty) -- and hand the agents that left the slab
+ * over (ghosts here from now on).  dsend NULL: the commits stay local until the next
+ * exchange (stale-halo rounds). */
 int am_slab_commit(am_slab* s, const int64_t* stats_global, int32_t* dsend);
 
 /* Step 4: apply the received delta blocks (drecv: block r from rank r). */
@@ -149,6 +176,9 @@ int am_slab_outputs(am_slab* s, const int32_t** slot_gid, const int32_t** slot_l
  * that finished an agent, agent-steps dispatched by this rank, rounds}. */
 int am_slab_state(am_slab* s, const int32_t** pos, const int32_t** steps, const uint8_t** status,
                   const uint64_t** traj, const int64_t** tcommit, const int32_t** newpos, const int64_t** counters);
+
+/* Per window slot: 1 if this rank owns the agent (device pointer owned by the slab). */
+int am_slab_owned(am_slab* s, const uint8_t** own);
 
 /* Sticky flags (AM_SLAB_*) and the window occupancy; synchronises the slab's stream and
  * clears the flags. */

@@ -52,7 +52,7 @@ class SlabGeom(C.Structure):
                 ("metric", C.c_int32), ("n_slabs", C.c_int32), ("my_slab", C.c_int32),
                 ("n_total", C.c_int32), ("target_step", C.c_int32), ("halo", C.c_int32),
                 ("cap_window", C.c_int32), ("cap_peer", C.c_int32), ("cap_merge", C.c_int32),
-                ("check_rounds", C.c_int32)]
+                ("check_rounds", C.c_int32), ("stale_rounds", C.c_int32)]
 
 
 class Synth(C.Structure):
@@ -108,6 +108,8 @@ SIGNATURES = {
     "am_slab_load": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64]),
     "am_slab_round_local": (C.c_int, [_vp, _vp]),
     "am_slab_merge": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "am_slab_round_stale": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "am_slab_owned": (C.c_int, [_vp, _vp]),
     "am_slab_commit": (C.c_int, [_vp, _vp, _vp]),
     "am_slab_apply": (C.c_int, [_vp, _vp]),
     "am_slab_outputs": (C.c_int, [_vp, _vp, _vp, _vp]),

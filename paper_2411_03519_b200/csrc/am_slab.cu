@@ -19,6 +19,7 @@ int am_internal_csort(am_ctx* c, const am::Dev& sd, int32_t* order, cudaStream_t
 namespace am {
 
 constexpr long long kNever = LLONG_MAX;
+constexpr int kDeltaRec = 12;   // words of a delta record (am_slab.h)
 
 // everything a slab kernel needs, by value
 struct SlabDev {
@@ -29,12 +30,16 @@ struct SlabDev {
     int y0, y1;            // the window's rows [y0, y1)
     int idb;               // bits of a global id (priority keys)
     int L;                 // window slots
+    int P;                 // a sync round every P rounds (stale_rounds; 1 = every round)
     // window (slot-indexed)
     int32_t* gid;          // -1 = free slot
     int2* pos;             // GLOBAL coordinates
     int2* tpos;            // the tracker's input: window coordinates (y - y0)
     int32_t* step;
     uint8_t* stat;         // the tracker's input status: owned real, ghost RUNNING, absent/finished DONE
+    uint8_t* own;          // owned by this rank: the slab of its row at the last exchange (fixed in between)
+    uint8_t* dirty;        // owned and committed since the last exchange
+    int32_t* ly;           // row at the last exchange
     unsigned long long* traj;
     long long* tc;         // completion time of the dispatched step (owned RUNNING)
     int2* np;              // move computed at dispatch (global coordinates)
@@ -95,7 +100,11 @@ __global__ void k_sl_load(SlabDev s, int m, const int32_t* __restrict__ gid, con
             const int g = gid[i];
             const int2 p = pos[i];
             uint8_t st = status[i];
-            if (!in_slab(s, p.y) && st != ST_DONE) st = ST_RUNNING;   // ghost
+            const bool own = in_slab(s, p.y);
+            if (!own && st != ST_DONE) st = ST_RUNNING;   // ghost
+            s.own[i] = own;
+            s.dirty[i] = 0;
+            s.ly[i] = p.y;
             s.gid[i] = g;
             s.pos[i] = p;
             s.step[i] = steps[i];
@@ -109,6 +118,9 @@ __global__ void k_sl_load(SlabDev s, int m, const int32_t* __restrict__ gid, con
             s.pos[i] = make_int2(0, s.y0);
             s.step[i] = 0;
             s.stat[i] = ST_DONE;
+            s.own[i] = 0;
+            s.dirty[i] = 0;
+            s.ly[i] = s.y0;
             s.traj[i] = 0ull;
             s.tc[i] = kNever;
             s.np[i] = make_int2(0, s.y0);
@@ -134,12 +146,13 @@ __global__ void k_sl_prep(SlabDev s, int32_t* mbuf)
         s.bndl[i] = 0;
         s.maxd[i] = 0;
     }
-    if (blockIdx.x == 0 && threadIdx.x < 4) mbuf[threadIdx.x] = 0;   // link / cluster counts
+    if (mbuf && blockIdx.x == 0 && threadIdx.x < 4) mbuf[threadIdx.x] = 0;   // link / cluster counts
 }
 
-// per local cluster: min global id, size, bad (an OWNED member RUNNING or blocked),
-// max duration of the owned IDLE members, boundary flag
-__global__ void k_sl_clusters(SlabDev s)
+// per local cluster: min global id, size, bad (an OWNED member RUNNING or blocked; in a
+// stale round also any ghost member: its owner's verdict is not exchanged), max duration
+// of the owned IDLE members, boundary flag
+__global__ void k_sl_clusters(SlabDev s, int stale)
 {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.L; i += gridDim.x * blockDim.x) {
         const uint8_t st = s.stat[i];
@@ -147,13 +160,15 @@ __global__ void k_sl_clusters(SlabDev s)
         const int l = s.labels[i];
         const int g = s.gid[i];
         const int y = s.pos[i].y;
-        const bool own = in_slab(s, y);
+        const bool own = s.own[i] != 0;
         atomicMin(s.mingid + l, g);
         atomicAdd(s.csize + l, 1);
         if (own) {
             if (st == ST_RUNNING || s.blocked[i]) s.badl[l] = 1;
             if (st == ST_IDLE)
                 atomicMax((unsigned long long*)(s.maxd + l), (unsigned long long)duration(s.sy, g, s.step[i]));
+        } else if (stale) {
+            s.badl[l] = 1;
         }
         if (!own || in_other_window(s, y)) s.bndl[l] = 1;
     }
@@ -176,7 +191,7 @@ __global__ void k_sl_records(SlabDev s, int32_t* __restrict__ mbuf)
             const int l = s.labels[i];
             if (s.bndl[l]) {
                 const int y = s.pos[i].y;
-                const bool bnd = !in_slab(s, y) || in_other_window(s, y);
+                const bool bnd = !s.own[i] || in_other_window(s, y);
                 if (bnd && s.csize[l] > 1) {
                     lk = true;
                     lv = make_int2(s.gid[i], s.mingid[l]);
@@ -277,8 +292,7 @@ __global__ void __launch_bounds__(256) k_sl_final(SlabDev s, long long* stats)
     unsigned long long kor = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.L; i += gridDim.x * blockDim.x) {
         uint8_t st = s.stat[i];
-        const int y = s.pos[i].y;
-        const bool own = st != ST_DONE && in_slab(s, y);
+        const bool own = st != ST_DONE && s.own[i];
         int lab = -1;
         bool rdy = false;
         if (own) {
@@ -397,55 +411,88 @@ __device__ __forceinline__ const int32_t* dblock(const SlabDev& s, const int32_t
     return d + (size_t)r * (size_t)AM_SLAB_DELTA_WORDS(s.g.cap_peer);
 }
 
-__global__ void k_sl_clock(SlabDev s, const long long* __restrict__ gstats, int32_t* dsend)
+// (after a stale round nothing may be pending: the clock stays, the rounds up to the next
+// sync round may be idle; only a sync round with nothing pending is a liveness failure)
+__global__ void k_sl_clock(SlabDev s, const long long* __restrict__ gstats, int32_t* dsend, int stale)
 {
-    for (int r = threadIdx.x; r < s.g.n_slabs; r += blockDim.x)
-        for (int q = 0; q < 6; q++) dblock(s, dsend, r)[q] = 0;   // counts (headers)
+    if (dsend)
+        for (int r = threadIdx.x; r < s.g.n_slabs; r += blockDim.x)
+            for (int q = 0; q < 6; q++) dblock(s, dsend, r)[q] = 0;   // counts (headers)
     if (threadIdx.x != 0) return;
     const long long tn = gstats[0];
     const bool active = gstats[3] == 0;
     if (active) {
         s.counters[3] += 1;
-        if (tn == kNever) atomicOr(s.flags, AM_SLAB_LIVENESS);
-        else s.counters[0] = s.Q > 0 ? ((tn + s.Q - 1) / s.Q) * s.Q : tn;
+        if (tn == kNever) {
+            if (!stale) atomicOr(s.flags, AM_SLAB_LIVENESS);
+        } else {
+            s.counters[0] = s.Q > 0 ? ((tn + s.Q - 1) / s.Q) * s.Q : tn;
+        }
+        // the owned agents drift up to P v outside the slab between exchanges, and the
+        // ghosts' snapshot is up to P rounds old: 2 P v more rows
         const long long spread = -gstats[2] - gstats[1] + 1;
-        const long long need = (spread + 1) * s.g.v_max + s.g.r_p + (long long)(s.g.check_rounds + 1) * s.g.v_max;
+        const long long need = (spread + 1) * s.g.v_max + s.g.r_p + (long long)(s.g.check_rounds + 1) * s.g.v_max +
+                               (s.P > 1 ? 2LL * s.P * s.g.v_max : 0LL);
         if (need > s.g.halo) atomicOr(s.flags, AM_SLAB_HALO);
     }
 }
 
 // owned RUNNING agents whose cluster completed commit their move (worker l.20-21,
-// controller l.11-12); commits inside another rank's window become delta records
-__global__ void k_sl_commit(SlabDev s, int32_t* __restrict__ dsend)
+// controller l.11-12); they stay owned (IDLE, or DONE at the target) until the next
+// exchange, which sends them to every rank whose window they were or are in
+__global__ void k_sl_commit(SlabDev s)
 {
     const long long t = s.counters[0];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.L; i += gridDim.x * blockDim.x) {
-        if (s.stat[i] != ST_RUNNING) continue;
-        const int2 op = s.pos[i];
-        if (!in_slab(s, op.y) || s.tc[i] > t) continue;   // ghosts are committed by their owner
+        if (s.stat[i] != ST_RUNNING || !s.own[i] || s.tc[i] > t) continue;   // ghosts are committed by their owner
         const int2 np = s.np[i];
         const int stp = s.step[i] + 1;
-        const unsigned long long th = traj_step(s.traj[i], stp, np.x, np.y);
         s.pos[i] = np;
         s.step[i] = stp;
-        s.traj[i] = th;
+        s.traj[i] = traj_step(s.traj[i], stp, np.x, np.y);
         s.tc[i] = kNever;
         const bool done = s.g.target_step > 0 && stp == s.g.target_step;
         if (done) atomicMax((unsigned long long*)(s.counters + 1), (unsigned long long)t);
-        // my view: IDLE (or DONE) if still mine, a ghost (RUNNING) if it left the slab
-        s.stat[i] = done ? ST_DONE : (in_slab(s, np.y) ? ST_IDLE : ST_RUNNING);
+        s.stat[i] = done ? ST_DONE : ST_IDLE;
+        s.dirty[i] = 1;
+    }
+}
+
+// the exchange's send side: every owned agent that committed since the last exchange, to
+// every other rank whose window holds its row then or now -- its whole state (a RUNNING
+// agent changing owner carries its completion time and move) -- and ownership follows
+// the row: an agent that left the slab becomes a ghost here
+__global__ void k_sl_flush(SlabDev s, int32_t* __restrict__ dsend)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.L; i += gridDim.x * blockDim.x) {
+        if (!s.dirty[i]) continue;
+        s.dirty[i] = 0;
+        const int2 p = s.pos[i];
+        const int y_old = s.ly[i];
+        const uint8_t st = s.stat[i];
+        const unsigned long long th = s.traj[i];
+        const long long tc = s.tc[i];
+        const int2 np = s.np[i];
         for (int j = 0; j < s.g.n_slabs; j++) {
             if (j == s.g.my_slab) continue;
-            if (!in_window_of(s, j, op.y) && !in_window_of(s, j, np.y)) continue;
+            if (!in_window_of(s, j, y_old) && !in_window_of(s, j, p.y)) continue;
             int32_t* blk = dblock(s, dsend, j);
             const int k = atomicAdd(blk, 1);
             if (k < s.g.cap_peer) {
-                int32_t* r = blk + 6 + (size_t)k * 6;
-                r[0] = s.gid[i]; r[1] = np.x; r[2] = np.y; r[3] = stp;
+                int32_t* r = blk + 6 + (size_t)k * kDeltaRec;
+                r[0] = s.gid[i]; r[1] = p.x; r[2] = p.y; r[3] = s.step[i];
                 r[4] = (int32_t)(uint32_t)th; r[5] = (int32_t)(uint32_t)(th >> 32);
+                r[6] = st; r[7] = (int32_t)(uint32_t)tc; r[8] = (int32_t)(uint32_t)((unsigned long long)tc >> 32);
+                r[9] = np.x; r[10] = np.y; r[11] = 0;
             } else {
                 atomicOr(s.flags, AM_SLAB_OVF_PEER);
             }
+        }
+        s.ly[i] = p.y;
+        if (!in_slab(s, p.y)) {
+            s.own[i] = 0;
+            s.stat[i] = st == ST_DONE ? ST_DONE : ST_RUNNING;
+            s.tc[i] = kNever;
         }
     }
 }
@@ -459,13 +506,14 @@ __global__ void k_sl_depart(SlabDev s, const int32_t* __restrict__ drecv)
     const int32_t* blk = dblock(s, drecv, r);
     const int nd = min(blk[0], s.g.cap_peer);
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += gridDim.x * blockDim.x) {
-        const int32_t* d = blk + 6 + (size_t)j * 6;
+        const int32_t* d = blk + 6 + (size_t)j * kDeltaRec;
         const int g = d[0], y = d[2];
         const int i = s.map[g];
         if (i < 0 || in_window(s, y)) continue;
         s.map[g] = -1;
         s.gid[i] = -1;
         s.stat[i] = ST_DONE;
+        s.own[i] = 0;
         s.pos[i] = make_int2(0, s.y0);
         const int f = atomicAdd(s.ftop, 1);
         s.fstack[f] = i;
@@ -480,7 +528,7 @@ __global__ void k_sl_arrive(SlabDev s, const int32_t* __restrict__ drecv)
     const int32_t* blk = dblock(s, drecv, r);
     const int nd = min(blk[0], s.g.cap_peer);
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += gridDim.x * blockDim.x) {
-        const int32_t* d = blk + 6 + (size_t)j * 6;
+        const int32_t* d = blk + 6 + (size_t)j * kDeltaRec;
         const int g = d[0], x = d[1], y = d[2], stp = d[3];
         if (!in_window(s, y)) continue;
         int i = s.map[g];
@@ -497,12 +545,20 @@ __global__ void k_sl_arrive(SlabDev s, const int32_t* __restrict__ drecv)
             s.tc[i] = kNever;
         }
         s.pos[i] = make_int2(x, y);
-        s.np[i] = make_int2(x, y);
         s.step[i] = stp;
         s.traj[i] = (unsigned long long)(uint32_t)d[4] | ((unsigned long long)(uint32_t)d[5] << 32);
-        const bool done = s.g.target_step > 0 && stp == s.g.target_step;
-        // the owner's commit: IDLE (DONE at the target) if it moved into my slab
-        s.stat[i] = done ? ST_DONE : (in_slab(s, y) ? ST_IDLE : ST_RUNNING);
+        s.ly[i] = y;
+        s.dirty[i] = 0;
+        // mine if it is in my slab now: the owner's status (IDLE, DONE, or RUNNING with its
+        // completion time and move); else a ghost
+        const uint8_t st = (uint8_t)d[6];
+        const bool own = in_slab(s, y);
+        s.own[i] = own;
+        s.stat[i] = st == ST_DONE ? ST_DONE : (own ? st : ST_RUNNING);
+        s.tc[i] = own && st == ST_RUNNING ? (long long)((unsigned long long)(uint32_t)d[7] |
+                                                        ((unsigned long long)(uint32_t)d[8] << 32))
+                                          : kNever;
+        s.np[i] = own && st == ST_RUNNING ? make_int2(d[9], d[10]) : make_int2(x, y);
     }
 }
 
@@ -522,12 +578,14 @@ struct am_slab {
     Dev sd{};                     // the order sort's view (keys, ids, control block)
     int32_t* order = nullptr;
     int num_sms = 148;
+    bool last_stale = false;      // the last round was a stale round
 };
 
 namespace {
 struct SlabLayout {
     size_t total = 0, tracker = 0, trk_bytes = 0;
-    size_t gid, pos, tpos, step, stat, traj, tc, np, dig, map, fstack, ftop, mingid, csize, badl, bndl, maxd;
+    size_t gid, pos, tpos, step, stat, own, dirty, ly, traj, tc, np, dig, map, fstack, ftop, mingid, csize, badl, bndl,
+        maxd;
     size_t forest, badm, touched, maxdm, glabel, ready, rlist, sctl, rk0, rk1, rv0, rv1, counters, flags, tmask,
         torder, order;
 };
@@ -558,7 +616,8 @@ bool geom_ok(const am_slab_geom* g)
     return g && g->n_slabs >= 1 && g->my_slab >= 0 && g->my_slab < g->n_slabs && g->n_total > 0 &&
            g->n_total < (1 << 28) && g->target_step > 0 && g->halo >= g->r_p + 2 * g->v_max && g->cap_window > 0 &&
            g->cap_peer > 0 && g->cap_merge > 0 && (g->cap_merge % 2) == 0 && g->map_w >= 1 && g->map_h >= 1 && g->map_w <= 32768 &&
-           g->map_h <= 32768 && g->check_rounds >= 1 && g->n_slabs <= 1024;
+           g->map_h <= 32768 && g->check_rounds >= 1 && g->n_slabs <= 1024 && g->stale_rounds >= 0 &&
+           g->halo >= g->r_p + (std::max(1, g->stale_rounds) + 1) * g->v_max;
 }
 
 SlabLayout slab_layout(const am_slab_geom& g)
@@ -573,6 +632,7 @@ SlabLayout slab_layout(const am_slab_geom& g)
     Ly.trk_bytes = am_workspace_size(g.map_w, std::max(1, y1 - y0), g.r_p, g.v_max, (int32_t)L, &c);
     Ly.tracker = take(Ly.trk_bytes);
     Ly.gid = take(4 * L); Ly.pos = take(8 * L); Ly.tpos = take(8 * L); Ly.step = take(4 * L); Ly.stat = take(L);
+    Ly.own = take(L); Ly.dirty = take(L); Ly.ly = take(4 * L);
     Ly.traj = take(8 * L); Ly.tc = take(8 * L); Ly.np = take(8 * L); Ly.dig = take(8 * L);
     Ly.map = take(4 * N); Ly.fstack = take(4 * L); Ly.ftop = take(4);
     Ly.mingid = take(4 * L); Ly.csize = take(4 * L); Ly.badl = take(L); Ly.bndl = take(L); Ly.maxd = take(8 * L);
@@ -652,6 +712,7 @@ extern "C" int am_slab_create(am_slab** out, const am_slab_geom* g, const am_syn
     s.Q = quantum_us;
     s.lo = lo; s.hi = hi; s.y0 = y0; s.y1 = y1;
     s.L = g->cap_window;
+    s.P = std::max(1, g->stale_rounds);
     {
         int idb = 1;
         while ((1LL << idb) < (long long)g->n_total) idb++;
@@ -659,6 +720,7 @@ extern "C" int am_slab_create(am_slab** out, const am_slab_geom* g, const am_syn
     }
     s.gid = (int32_t*)(b + Ly.gid); s.pos = (int2*)(b + Ly.pos); s.tpos = (int2*)(b + Ly.tpos);
     s.step = (int32_t*)(b + Ly.step); s.stat = (uint8_t*)(b + Ly.stat);
+    s.own = (uint8_t*)(b + Ly.own); s.dirty = (uint8_t*)(b + Ly.dirty); s.ly = (int32_t*)(b + Ly.ly);
     s.traj = (unsigned long long*)(b + Ly.traj); s.tc = (long long*)(b + Ly.tc); s.np = (int2*)(b + Ly.np);
     s.dig = (unsigned long long*)(b + Ly.dig);
     s.map = (int32_t*)(b + Ly.map); s.fstack = (int32_t*)(b + Ly.fstack); s.ftop = (int32_t*)(b + Ly.ftop);
@@ -726,10 +788,32 @@ extern "C" int am_slab_round_local(am_slab* sl, int32_t* mbuf)
     if (rc) return rc;
     rc = am_ready(sl->tr, sl->tmask, sl->torder, nullptr);   // AM_PEEK | AM_ASYNC
     if (rc) return rc;
-    k_sl_clusters<<<gr, 256, 0, sl->stream>>>(s);
+    k_sl_clusters<<<gr, 256, 0, sl->stream>>>(s, 0);
     k_sl_records<<<gr, 256, 0, sl->stream>>>(s, mbuf);
     SK(cudaGetLastError());
+    sl->last_stale = false;
     return AM_OK;
+}
+
+// the dispatch of the ready agents of a round (local clusters, or merged through the
+// records of `mbufs`): ready bits, dispatch, digests, moves, the rank's order
+static int slab_finish(am_slab* sl, const int32_t* mbufs, int32_t* order_out, int32_t* n_order, int64_t* stats);
+
+extern "C" int am_slab_round_stale(am_slab* sl, int32_t* order_out, int32_t* n_order, int64_t* stats)
+{
+    if (!sl || !order_out || !n_order || !stats) return AM_E_ARG;
+    SlabDev& s = sl->s;
+    const unsigned gr = grid_for(sl, s.L);
+    k_sl_prep<<<gr, 256, 0, sl->stream>>>(s, nullptr);
+    SK(cudaGetLastError());
+    int rc = am_update_replica(sl->tr, (const int32_t*)s.tpos, s.step, s.stat);
+    if (rc) return rc;
+    rc = am_ready(sl->tr, sl->tmask, sl->torder, nullptr);   // AM_PEEK | AM_ASYNC
+    if (rc) return rc;
+    k_sl_clusters<<<gr, 256, 0, sl->stream>>>(s, 1);
+    SK(cudaGetLastError());
+    sl->last_stale = true;
+    return slab_finish(sl, nullptr, order_out, n_order, stats);
 }
 
 __global__ void k_sl_norder(const Ctl* c, int32_t* n) { *n = c->n_ready; }
@@ -737,17 +821,24 @@ __global__ void k_sl_norder(const Ctl* c, int32_t* n) { *n = c->n_ready; }
 extern "C" int am_slab_merge(am_slab* sl, const int32_t* mbufs, int32_t* order_out, int32_t* n_order, int64_t* stats)
 {
     if (!sl || !mbufs || !order_out || !n_order || !stats) return AM_E_ARG;
+    return slab_finish(sl, mbufs, order_out, n_order, stats);
+}
+
+static int slab_finish(am_slab* sl, const int32_t* mbufs, int32_t* order_out, int32_t* n_order, int64_t* stats)
+{
     SlabDev& s = sl->s;
     // one row of blocks per rank's records (each walks its rank's records up to their count)
     const dim3 gm(std::max(1u, std::min((unsigned)((s.g.cap_merge + 255) / 256), (unsigned)(sl->num_sms * 8) /
                                                                                    (unsigned)s.g.n_slabs)),
                   (unsigned)s.g.n_slabs);
     const unsigned gr = grid_for(sl, s.L);
-    k_sl_unite<<<gm, 256, 0, sl->stream>>>(s, mbufs);
-    k_sl_cbad<<<gm, 256, 0, sl->stream>>>(s, mbufs);
+    if (mbufs) {
+        k_sl_unite<<<gm, 256, 0, sl->stream>>>(s, mbufs);
+        k_sl_cbad<<<gm, 256, 0, sl->stream>>>(s, mbufs);
+    }
     k_sl_stats_init<<<1, 32, 0, sl->stream>>>(s, (long long*)stats);
     k_sl_final<<<gr, 256, 0, sl->stream>>>(s, (long long*)stats);
-    k_sl_restore<<<gm, 256, 0, sl->stream>>>(s, mbufs);
+    if (mbufs) k_sl_restore<<<gm, 256, 0, sl->stream>>>(s, mbufs);
     k_sl_norder<<<1, 1, 0, sl->stream>>>(s.sctl, n_order);
     SK(cudaGetLastError());
     // perception digests of the dispatched agents (global ids in the terms), their moves
@@ -761,10 +852,11 @@ extern "C" int am_slab_merge(am_slab* sl, const int32_t* mbufs, int32_t* order_o
 
 extern "C" int am_slab_commit(am_slab* sl, const int64_t* stats_global, int32_t* dsend)
 {
-    if (!sl || !stats_global || !dsend) return AM_E_ARG;
+    if (!sl || !stats_global) return AM_E_ARG;
     SlabDev& s = sl->s;
-    k_sl_clock<<<1, 256, 0, sl->stream>>>(s, (const long long*)stats_global, dsend);
-    k_sl_commit<<<grid_for(sl, s.L), 256, 0, sl->stream>>>(s, dsend);
+    k_sl_clock<<<1, 256, 0, sl->stream>>>(s, (const long long*)stats_global, dsend, sl->last_stale ? 1 : 0);
+    k_sl_commit<<<grid_for(sl, s.L), 256, 0, sl->stream>>>(s);
+    if (dsend) k_sl_flush<<<grid_for(sl, s.L), 256, 0, sl->stream>>>(s, dsend);
     SK(cudaGetLastError());
     return AM_OK;
 }
@@ -818,6 +910,13 @@ extern "C" int am_slab_flags(am_slab* sl, int32_t* flags, int32_t* window_used)
     if (window_used) *window_used = sl->s.L - sl->h_flags[1];
     const int rc = am_sync(sl->tr);   // the window tracker's pending errors
     return rc;
+}
+
+extern "C" int am_slab_owned(am_slab* sl, const uint8_t** own)
+{
+    if (!sl || !own) return AM_E_ARG;
+    *own = sl->s.own;
+    return AM_OK;
 }
 
 extern "C" am_ctx* am_slab_tracker(am_slab* sl) { return sl ? sl->tr : nullptr; }

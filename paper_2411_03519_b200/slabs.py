@@ -11,6 +11,11 @@ synchronises the host:
   3. am_slab_commit       -> ALL-TO-ALL of the delta blocks (commits in other windows)
   4. am_slab_apply
 
+With stale_rounds = P > 1 (stale-halo rounds, NEXT #3) only every P-th round is such a
+sync round; the rounds in between run am_slab_round_stale (no all-gather, no merge)
+against the ghosts of the last exchange, and the all-to-all runs only before a sync
+round -- one all-reduce per stale round (the common clock).
+
 The exchange is torch.distributed (NCCL over NVLink, one process per GPU:
 ``DistWorld``) or an in-process loopback of G virtual slabs on one GPU
 (``LoopbackWorld``); both drive the identical library calls.  Every K rounds (and at
@@ -57,9 +62,11 @@ def _view(ptr, shape, dtype, device):
     return torch.as_tensor(_DevArray(ptr, shape, ts), device=device)
 
 
-def halo_needed(spread: int, r_p: int, v: int, K: int) -> int:
-    """Window rows that keep the next K rounds exact: R_b(spread + 1) + (K + 1) v."""
-    return (spread + 2) * v + r_p + (K + 1) * v
+def halo_needed(spread: int, r_p: int, v: int, K: int, P: int = 1) -> int:
+    """Window rows that keep the next K rounds exact: R_b(spread + 1) + (K + 1) v,
+    plus 2 P v with stale-halo rounds (owned agents drift up to P v out of the slab and
+    the ghosts' snapshot is up to P rounds old)."""
+    return (spread + 2) * v + r_p + (K + 1) * v + (2 * P * v if P > 1 else 0)
 
 
 class SlabRank:
@@ -67,7 +74,7 @@ class SlabRank:
 
     def __init__(self, map_w, map_h, r_p, v, n_total, n_slabs, my_slab, target, synth, quantum_us, *,
                  halo, cap_window, cap_peer, cap_merge, check_rounds=16, metric="l2", device="cuda",
-                 stream=None):
+                 stream=None, stale_rounds=1):
         self.L = _lib.load()
         self.dev = torch.device(device)
         self.G, self.k = int(n_slabs), int(my_slab)
@@ -77,7 +84,7 @@ class SlabRank:
         self.g = _lib.SlabGeom(self.map_w, self.map_h, self.r_p, self.v,
                                _lib.METRIC_LINF if metric == "linf" else _lib.METRIC_L2, self.G, self.k,
                                self.n_total, self.target, int(halo), int(cap_window), int(cap_peer),
-                               self.cap_merge, int(check_rounds))
+                               self.cap_merge, int(check_rounds), int(stale_rounds))
         self.halo, self.cap_window, self.cap_peer = int(halo), int(cap_window), int(cap_peer)
         self.lo, self.hi = slab_of_rows(self.map_h, self.G)[self.k]
         self.y0, self.y1 = max(0, self.lo - self.halo), min(self.map_h, self.hi + self.halo)
@@ -94,7 +101,7 @@ class SlabRank:
         self.h = h
         d = self.dev
         self.mwords = 4 + 6 * self.cap_merge
-        self.dwords = 6 + 6 * self.cap_peer
+        self.dwords = 6 + 12 * self.cap_peer
         self.mbuf = torch.zeros(self.mwords, dtype=torch.int32, device=d)
         self.dsend = torch.zeros((self.G, self.dwords), dtype=torch.int32, device=d)
         self.stats = torch.zeros(4, dtype=torch.int64, device=d)
@@ -116,6 +123,9 @@ class SlabRank:
         self.w_gid = _view(oo[0].value, (Lw,), torch.int32, d)
         self.w_label = _view(oo[1].value, (Lw,), torch.int32, d)
         self.w_ready = _view(oo[2].value, (Lw,), torch.uint8, d)
+        ow = C.c_void_p()
+        check(self.L.am_slab_owned(h, C.byref(ow)))
+        self.w_own = _view(ow.value, (Lw,), torch.uint8, d)
 
     # ------------------------------------------------------------------ library steps
     def load(self, gid, pos, steps, status, traj=None, tcommit=None, newpos=None, t: int = 0):
@@ -136,8 +146,14 @@ class SlabRank:
                                    self.stats.data_ptr()))
         return self.stats
 
-    def commit(self, stats_global: torch.Tensor):
-        check(self.L.am_slab_commit(self.h, stats_global.data_ptr(), self.dsend.data_ptr()))
+    def round_stale(self):
+        check(self.L.am_slab_round_stale(self.h, self.order.data_ptr(), self.n_order.data_ptr(),
+                                         self.stats.data_ptr()))
+        return self.stats
+
+    def commit(self, stats_global: torch.Tensor, exchange: bool = True):
+        """exchange=False: the commits stay local until the next exchange (stale rounds)."""
+        check(self.L.am_slab_commit(self.h, stats_global.data_ptr(), self.dsend.data_ptr() if exchange else None))
         return self.dsend
 
     def apply(self, drecv: torch.Tensor):
@@ -153,8 +169,7 @@ class SlabRank:
 
     # ------------------------------------------------------------------ views
     def owned_mask(self) -> torch.Tensor:
-        y = self.w_pos[:, 1]
-        return (self.w_gid >= 0) & (y >= self.lo) & (y < self.hi)
+        return (self.w_gid >= 0) & (self.w_own != 0)
 
     def owned_state(self):
         """The owned agents (every field needed to reload them anywhere)."""
@@ -188,7 +203,8 @@ class _World:
     """Common driver: setup from a global initial state, rounds, checks, re-windows."""
 
     def _geometry(self, y_all: torch.Tensor, spread: int, K: int, halo: int | None = None):
-        H = halo if halo is not None else halo_needed(spread, self.r_p, self.v, K)
+        H = halo if halo is not None else halo_needed(spread, self.r_p, self.v, K, self.P)
+        H = max(H, self.r_p + (self.P + 1) * self.v)
         H = min(H, self.map_h)
         # capacities from the actual distribution, with slack for migration
         rows = slab_of_rows(self.map_h, self.G)
@@ -201,8 +217,19 @@ class _World:
             bands.append(int(bnd.sum()))
         cap_window = int(max(wins) * 1.25) + 2048
         cap_merge = int(max(bands) * 1.5) + 2048
-        cap_peer = int(max(bands) * 0.5) + 2048
+        cap_peer = int(max(bands) * min(1.0, 0.5 * self.P)) + 2048   # one record per agent per exchange
         return H, cap_window, cap_merge, cap_peer
+
+    def _schedule(self):
+        """(sync, exchange) of the next round: a sync round every P rounds, the exchange
+        after the commits of the round before one."""
+        r = self.rounds_done
+        return r % self.P == 0, (r + 1) % self.P == 0
+
+    def _set_period(self, K: int, stale_rounds: int):
+        self.P = max(1, int(stale_rounds))
+        if K % self.P:
+            raise ValueError("check_rounds must be a multiple of stale_rounds (re-windows happen at exchanges)")
 
     @staticmethod
     def _window_select(st: dict, lo: int, hi: int, H: int, map_h: int):
@@ -240,10 +267,11 @@ class LoopbackWorld(_World):
     stream): the same library calls as the NCCL run, bit-exact against it by design."""
 
     def __init__(self, map_w, map_h, r_p, v, x0, y0, target, synth, quantum_us, n_slabs, *, metric="l2",
-                 check_rounds=16, device="cuda", halo=None, steps0=None, status0=None):
+                 check_rounds=16, device="cuda", halo=None, steps0=None, status0=None, stale_rounds=1):
         self.map_w, self.map_h, self.r_p, self.v = int(map_w), int(map_h), int(r_p), int(v)
         self.G, self.target, self.synth, self.Q = int(n_slabs), int(target), synth, int(quantum_us)
         self.metric, self.K, self.dev = metric, int(check_rounds), torch.device(device)
+        self._set_period(self.K, stale_rounds)
         st = _initial_state(x0, y0, steps0, status0, self.dev)
         self.n = len(x0)
         self.ranks = []
@@ -261,7 +289,7 @@ class LoopbackWorld(_World):
         for k in range(self.G):
             r = SlabRank(self.map_w, self.map_h, self.r_p, self.v, self.n, self.G, k, self.target, self.synth,
                          self.Q, halo=H, cap_window=cw, cap_peer=cp, cap_merge=cm, check_rounds=self.K,
-                         metric=self.metric, device=self.dev)
+                         metric=self.metric, device=self.dev, stale_rounds=self.P)
             w = self._window_select(st, r.lo, r.hi, H, self.map_h)
             r.load(w["gid"], w["pos"], w["steps"], w["status"], w["traj"], w["tcommit"], w["newpos"], t)
             self.ranks.append(r)
@@ -271,48 +299,45 @@ class LoopbackWorld(_World):
         `log` asks for the round's outputs).  With `timing` (a list), the device time of
         every rank's own library steps (everything but the exchanges, which NCCL does in
         a real run) is appended, per rank, in ms: what one GPU of a G-GPU run computes."""
-        ev = None
-        if timing is not None:
-            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in self.ranks]
+        sync, exchange = self._schedule()
+        ev = [[] for _ in self.ranks]
 
-        def rec(k, j):
-            if ev is not None:
-                if j % 2 == 0:
-                    # the device sleeps while the host enqueues the rank's phase, so the
-                    # events bracket its kernels running back to back (device time, not
-                    # the host's launch rate)
-                    torch.cuda._sleep(3_000_000)
-                ev[k][j].record()
+        def phase(k, fn):
+            if timing is None:
+                return fn()
+            # the device sleeps while the host enqueues the rank's phase, so the events
+            # bracket its kernels running back to back (device time, not the host's
+            # launch rate)
+            torch.cuda._sleep(3_000_000)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = fn()
+            e1.record()
+            ev[k].append((e0, e1))
+            return out
 
-        mbs = []
-        for k, r in enumerate(self.ranks):
-            rec(k, 0)
-            mbs.append(r.round_local())
-            rec(k, 1)
-        mb = torch.stack(mbs)                                               # all-gather
-        for k, r in enumerate(self.ranks):
-            rec(k, 2)
-            r.merge(mb)
-            rec(k, 3)
+        if sync:
+            mbs = [phase(k, r.round_local) for k, r in enumerate(self.ranks)]
+            mb = torch.stack(mbs)                                           # all-gather
+            for k, r in enumerate(self.ranks):
+                phase(k, lambda r=r: r.merge(mb))
+        else:
+            for k, r in enumerate(self.ranks):
+                phase(k, r.round_stale)
         if log is not None:
             log.append([r.round_outputs() for r in self.ranks])
         sg = torch.stack([r.stats for r in self.ranks]).min(0).values       # all-reduce MIN
-        dss = []
-        for k, r in enumerate(self.ranks):
-            rec(k, 4)
-            dss.append(r.commit(sg))
-            rec(k, 5)
-        ds = torch.stack(dss)                                               # [src, dst, words]
-        for k, r in enumerate(self.ranks):
-            recv = ds[:, k].contiguous()                                    # all-to-all
-            rec(k, 6)
-            r.apply(recv)
-            rec(k, 7)
+        dss = [phase(k, lambda r=r: r.commit(sg, exchange)) for k, r in enumerate(self.ranks)]
+        if exchange:
+            ds = torch.stack(dss)                                           # [src, dst, words]
+            for k, r in enumerate(self.ranks):
+                recv = ds[:, k].contiguous()                                # all-to-all
+                phase(k, lambda r=r, recv=recv: r.apply(recv))
         self.rounds_done += 1
         self._last_stats = sg
-        if ev is not None:
+        if timing is not None:
             torch.cuda.synchronize(self.dev)
-            timing.append([sum(e[2 * j].elapsed_time(e[2 * j + 1]) for j in range(4)) for e in ev])
+            timing.append([sum(a.elapsed_time(b) for a, b in e) for e in ev])
 
     def check(self) -> bool:
         """Reads every rank's flags (one synchronisation).  Raises on an overflow or a
@@ -340,7 +365,7 @@ class LoopbackWorld(_World):
         self._carry = (max(self._carry[0], int(cnt[:, 1].max())), self._carry[1] + int(cnt[:, 2].sum()),
                        self._carry[2] + int(cnt[0, 3]))   # finishing time, dispatched, rounds
         t = int(cnt[0, 0])
-        need = halo_needed(spread, self.r_p, self.v, self.K)
+        need = halo_needed(spread, self.r_p, self.v, self.K, self.P)
         self._setup(st, t, spread, halo=2 * need)
         self.rewindows += 1
 
@@ -389,12 +414,13 @@ class DistWorld(_World):
     (tests stage gloo through the host)."""
 
     def __init__(self, dist, map_w, map_h, r_p, v, x0, y0, target, synth, quantum_us, *, metric="l2",
-                 check_rounds=16, device="cuda", halo=None, steps0=None, status0=None):
+                 check_rounds=16, device="cuda", halo=None, steps0=None, status0=None, stale_rounds=1):
         self.dist = dist
         self.G, self.k = dist.get_world_size(), dist.get_rank()
         self.map_w, self.map_h, self.r_p, self.v = int(map_w), int(map_h), int(r_p), int(v)
         self.target, self.synth, self.Q = int(target), synth, int(quantum_us)
         self.metric, self.K, self.dev = metric, int(check_rounds), torch.device(device)
+        self._set_period(self.K, stale_rounds)
         st = _initial_state(x0, y0, steps0, status0, self.dev)
         self.n = len(x0)
         self.rank = None
@@ -410,7 +436,7 @@ class DistWorld(_World):
         self.halo = H
         r = SlabRank(self.map_w, self.map_h, self.r_p, self.v, self.n, self.G, self.k, self.target, self.synth,
                      self.Q, halo=H, cap_window=cw, cap_peer=cp, cap_merge=cm, check_rounds=self.K,
-                     metric=self.metric, device=self.dev)
+                     metric=self.metric, device=self.dev, stale_rounds=self.P)
         w = self._window_select(st, r.lo, r.hi, H, self.map_h)
         r.load(w["gid"], w["pos"], w["steps"], w["status"], w["traj"], w["tcommit"], w["newpos"], t)
         self.rank = r
@@ -419,16 +445,21 @@ class DistWorld(_World):
 
     def round(self, log: list | None = None):
         r, dist = self.rank, self.dist
-        mb = r.round_local()
-        dist.all_gather_into_tensor(self.mball.view(-1), mb)
-        r.merge(self.mball)
+        sync, exchange = self._schedule()
+        if sync:
+            mb = r.round_local()
+            dist.all_gather_into_tensor(self.mball.view(-1), mb)
+            r.merge(self.mball)
+        else:
+            r.round_stale()
         if log is not None:
             log.append(r.round_outputs())
         sg = r.stats.clone()
         dist.all_reduce(sg, op=dist.ReduceOp.MIN)
-        ds = r.commit(sg)
-        dist.all_to_all_single(self.drecv, ds)
-        r.apply(self.drecv)
+        ds = r.commit(sg, exchange)
+        if exchange:
+            dist.all_to_all_single(self.drecv, ds)
+            r.apply(self.drecv)
         self.rounds_done += 1
         self._last_stats = sg
 
@@ -470,7 +501,7 @@ class DistWorld(_World):
         cnt = self.rank.counters.cpu().numpy()
         self._carry = (max(self._carry[0], int(cnt[1])), self._carry[1] + int(cnt[2]), self._carry[2] + int(cnt[3]))
         t = int(cnt[0])
-        need = halo_needed(spread, self.r_p, self.v, self.K)
+        need = halo_needed(spread, self.r_p, self.v, self.K, self.P)
         self._setup(st, t, spread, halo=2 * need)
         self.rewindows += 1
 

@@ -9,7 +9,11 @@
   clock, re-windowing as the step spread grows) equals the oracle's replay round by round
   (every round's dispatched ids in priority order and their labels) and in its final
   state (positions, trajectory hashes, T_ooo, rounds) on C1, C2 and a C4-shaped map at
-  G = 2 / 4 / 8."""
+  G = 2 / 4 / 8;
+* with stale-halo rounds (NEXT #3: a sync round every P rounds, the rounds between
+  decided against the last exchange's ghosts) the replay equals the oracle's
+  orc_replay_stale round by round and in its final state, and a long C4-shaped run
+  (re-windows, migration) ends in the lock-step state."""
 import numpy as np
 import pytest
 import torch
@@ -21,7 +25,7 @@ from paper_2411_03519_b200 import slabs
 pytestmark = pytest.mark.gpu
 
 
-def _world(w, lm, G, steps0=None, status0=None, **kw):
+def _world(w, lm, G, steps0=None, status0=None, **kw):   # kw: check_rounds, stale_rounds
     sy = slabs.Synth(lm, wall=w.wall)
     return slabs.LoopbackWorld(w.map_w, w.map_h, w.r_p, w.v, w.x, w.y, w.steps, sy, w.Q, G, steps0=steps0,
                                status0=status0, **kw)
@@ -159,3 +163,59 @@ def test_slab_replay_c4_shape_final_state_vs_lockstep(G):
     assert res["T_ooo"] == int(r1["T_ooo"][0]) and res["rounds"] == int(r1["rounds"][0])
     one.close()
     wd.close()
+
+
+@pytest.mark.parametrize("name,steps,n,G,P", [
+    ("C1", 300, None, 2, 2), ("C1", 300, None, 4, 4),
+    ("C2", 8, None, 4, 2), ("C2", 8, None, 8, 4),
+    ("C4", 6, 2000, 4, 4),
+])
+def test_stale_slab_replay_round_logs_vs_oracle(name, steps, n, G, P):
+    w = amgen.config(name, steps=steps, n=n)
+    lm = amgen.latency_model(w.profile)
+    sy = O.SynthTables.from_model(lm, wall=w.wall)
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps)
+    r = O.replay_stale(p, sy, w.x, w.y, G=G, P=P, Q=w.Q, log_rounds=10**6, log_entries=len(w.x) * w.steps + 10)
+    assert r["log_complete"]
+    wd = _world(w, lm, G, check_rounds=2 * P, stale_rounds=P)
+    glogs = _replay_logged(wd)
+    ologs = _oracle_logs(r)
+    assert len(glogs) == len(ologs), (len(glogs), len(ologs))
+    for k, ((gi, gl), (oi, ol)) in enumerate(zip(glogs, ologs)):
+        np.testing.assert_array_equal(gi, oi, err_msg=f"round {k}")
+        np.testing.assert_array_equal(gl, ol, err_msg=f"round {k}")
+    res = wd.results()
+    np.testing.assert_array_equal(res["x"], r["x"])
+    np.testing.assert_array_equal(res["y"], r["y"])
+    np.testing.assert_array_equal(res["traj"], r["traj"])
+    assert res["T_ooo"] == int(r["T_ooo"][0])
+    assert res["rounds"] == int(r["rounds"][0])
+    assert res["dispatched"] == len(w.x) * w.steps
+    wd.close()
+
+
+@pytest.mark.parametrize("G,P", [(4, 2), (8, 4)])
+def test_stale_slab_replay_c4_shape_final_state_vs_lockstep(G, P):
+    """20k agents at C4 density over 120 steps with stale-halo rounds: re-windows at
+    exchanges, agents handed over (RUNNING ones with their completion times) -- the final
+    state is lock-step's (P:27)."""
+    w = amgen.config("C4", steps=120, n=20000)
+    lm = amgen.latency_model(w.profile)
+    wd = _world(w, lm, G, check_rounds=2 * P, stale_rounds=P)
+    wd.run(10**6)
+    res = wd.results()
+    assert wd.rewindows >= 1
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, w.steps)
+    ls = O.lockstep_grid(p, O.SynthTables.from_model(lm), w.x, w.y, w.steps)
+    np.testing.assert_array_equal(res["x"], ls["x"])
+    np.testing.assert_array_equal(res["y"], ls["y"])
+    np.testing.assert_array_equal(res["traj"], ls["traj"])
+    assert res["dispatched"] == len(w.x) * w.steps
+    wd.close()
+
+
+def test_stale_period_must_divide_the_check_period():
+    w = amgen.config("C1", steps=10)
+    lm = amgen.latency_model(w.profile)
+    with pytest.raises(ValueError):
+        _world(w, lm, 2, check_rounds=6, stale_rounds=4)

@@ -2,7 +2,8 @@
 two processes (two ranks, two slabs) on ONE GPU: torch.distributed over gloo with the
 CUDA buffers staged through the host (NCCL refuses two ranks per device).  The replay of
 C2 (500 agents, 25 steps) equals the oracle's round by round (the ranks' orders merged)
-and in its final state."""
+and in its final state -- synchronous, and with stale-halo rounds (a sync round every
+P = 4 rounds, orc_replay_stale)."""
 import os
 import socket
 
@@ -20,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, P):
     import torch
     import torch.distributed as dist
 
@@ -35,7 +36,7 @@ def _worker(rank, world, port, q):
         lm = amgen.latency_model(w.profile)
         sy = slabs.Synth(lm, wall=w.wall)
         wd = slabs.DistWorld(slabs.HostStagedDist(dist), w.map_w, w.map_h, w.r_p, w.v, w.x, w.y, w.steps, sy, w.Q,
-                             check_rounds=4)
+                             check_rounds=4, stale_rounds=P)
         logs = []
         k = 0
         while True:
@@ -56,7 +57,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_dist_world_two_ranks_one_gpu_vs_oracle():
+@pytest.mark.parametrize("P", [1, 4])
+def test_dist_world_two_ranks_one_gpu_vs_oracle(P):
     import torch.multiprocessing as mp
 
     import amgen
@@ -65,7 +67,7 @@ def test_dist_world_two_ranks_one_gpu_vs_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, P)) for r in range(2)]
     for p in ps:
         p.start()
     got = {}
@@ -79,7 +81,10 @@ def test_dist_world_two_ranks_one_gpu_vs_oracle():
     lm = amgen.latency_model(w.profile)
     sy = O.SynthTables.from_model(lm, wall=w.wall)
     p = O.params(w.map_w, w.map_h, w.r_p, w.v, target=w.steps)
-    r = O.replay(p, sy, w.x, w.y, Q=w.Q, log_rounds=10**6, log_entries=len(w.x) * w.steps + 10)
+    if P == 1:
+        r = O.replay(p, sy, w.x, w.y, Q=w.Q, log_rounds=10**6, log_entries=len(w.x) * w.steps + 10)
+    else:
+        r = O.replay_stale(p, sy, w.x, w.y, G=2, P=P, Q=w.Q, log_rounds=10**6, log_entries=len(w.x) * w.steps + 10)
     ologs, k = [], 0
     for nr in r["log_nready"]:
         if nr:

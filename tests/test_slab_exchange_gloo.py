@@ -44,7 +44,7 @@ def _worker(rank, world, port, q):
         ok2 = st.tolist() == [1000, 5, -(10 + world - 1), 0]
         # delta blocks: block j of rank r goes to rank j; header = record count
         capp = 3
-        ds = torch.zeros((world, 6 + 6 * capp), dtype=torch.int32)
+        ds = torch.zeros((world, 6 + 12 * capp), dtype=torch.int32)
         for j in range(world):
             if j != rank:
                 ds[j, 0] = rank + 1
