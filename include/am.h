@@ -207,6 +207,12 @@ int am_sync(am_ctx* ctx);
 int am_set_flags(am_ctx* ctx, uint32_t flags);
 int am_set_stream(am_ctx* ctx, void* stream);
 
+/* The stream the context's work is ordered on now (a replay driver moves its context
+ * onto the replay's own stream, am_driver.h): a caller reading an output of a
+ * stream-ordered getter (am_status, am_clusters, am_blocked) from another stream makes
+ * that stream wait on this one first. */
+void* am_get_stream(const am_ctx* ctx);
+
 /* Forget the state: the next am_update is an initial state again. */
 int am_reset(am_ctx* ctx);
 

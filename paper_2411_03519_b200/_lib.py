@@ -80,6 +80,7 @@ SIGNATURES = {
     "am_sync": (C.c_int, [_vp]),
     "am_set_flags": (C.c_int, [_vp, _u32]),
     "am_set_stream": (C.c_int, [_vp, _vp]),
+    "am_get_stream": (_vp, [_vp]),
     "am_reset": (C.c_int, [_vp]),
     "am_workspace_bytes": (C.c_size_t, [_vp]),
     "am_ready_count_device": (_vp, [_vp]),

@@ -808,6 +808,8 @@ extern "C" int am_set_stream(am_ctx* c, void* stream)
     return AM_OK;
 }
 
+extern "C" void* am_get_stream(const am_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
 extern "C" int am_reset(am_ctx* c)
 {
     if (!c) return set_err(nullptr, AM_E_ARG, "NULL context");

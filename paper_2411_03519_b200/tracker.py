@@ -123,14 +123,25 @@ class Tracker:
             self.L.am_set_flags(self.ctx, self.flags)
         return mask, order
 
+    def _join(self) -> None:
+        """Make torch's current stream wait for the context's stream (a replay runs the
+        context on its own stream): outputs of stream-ordered getters are then safe to read
+        from torch."""
+        ptr = self.L.am_get_stream(self.ctx)
+        cur = torch.cuda.current_stream(self.device)
+        if ptr and int(ptr) != cur.cuda_stream:
+            cur.wait_stream(torch.cuda.ExternalStream(int(ptr), device=self.device))
+
     def clusters(self, out: torch.Tensor | None = None) -> torch.Tensor:
         out = self.labels[: self.n] if out is None else out
         check(self.L.am_clusters(self.ctx, _ptr(out, torch.int32)), self.ctx)
+        self._join()
         return out
 
     def status(self) -> torch.Tensor:
         out = torch.empty(self.n, dtype=torch.uint8, device=self.device)
         check(self.L.am_status(self.ctx, _ptr(out, torch.uint8)), self.ctx)
+        self._join()
         return out
 
     def sync(self) -> None:
