@@ -236,7 +236,10 @@ static int plan(am_ctx* x, int32_t map_w, int32_t map_h, int32_t radius_p, int32
     x->small_threads = std::max(32, ((per_sim_max + 31) / 32) * 32);
 
     // cell size: >= R_c = r_p + v (coupling needs <= 2x2 cells), grown until the Morton
-    // grid has at most max(4N, 4096) cells and at most 4096 cells per side.  The grid is
+    // grid has at most max(N/2, 4096) cells (>= 2 agents per cell on average) and at most
+    // 4096 cells per side.  (A/B on the replay round, tools/ab_round.py AM_CELL: C5 cells
+    // of 8 / 16 / 32 / 64 tiles -> 167 / 167 / 146 / 173 us, C4 73 / 67 / 63 / 73 us; the
+    // scan's per-cell box work shrinks while the cells stay small enough to prune.)  The grid is
     // rectangular (2^gxlog x 2^gylog cells, each side >= 64 cells, mkey): a long thin map
     // -- e.g. one spatial slab of a wide map -- gets a long thin cell table.
     long long Rc = (long long)d.r_p + d.v;
@@ -244,13 +247,16 @@ static int plan(am_ctx* x, int32_t map_w, int32_t map_h, int32_t radius_p, int32
         return ilog2_ceil(std::max(64LL, (extent + (1LL << cl) - 1) >> cl));
     };
     int clog;
-    if (c.cell) {
-        clog = ilog2_ceil(c.cell);
+    int cell_knob = 0;   // tuning knob (A/B of the grid density): a forced cell edge
+    if (!c.cell)
+        if (const char* e = getenv("AM_CELL")) cell_knob = std::max(0, atoi(e));
+    if (c.cell || cell_knob) {
+        clog = ilog2_ceil(c.cell ? c.cell : cell_knob);
     } else {
         clog = ilog2_ceil(std::max(1LL, Rc));
         for (;;) {
             const long long g = 1LL << (gl(map_w, clog) + gl(map_h, clog));
-            if (g <= std::max(4 * n, 4096LL) || clog >= 15) break;
+            if (g <= std::max(n / 2, 4096LL) || clog >= 15) break;
             clog++;
         }
     }
