@@ -21,6 +21,11 @@ SAN = "/usr/local/cuda/bin/compute-sanitizer"
 def test_sanitizer_clean(tool, case):
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")
+    if os.environ.get("AM_RUN_SANITIZER") != "1":
+        # the GPU pool closed compute-sanitizer after this round's clean runs
+        # (profiles/r2_gputest_s3.log, s4.log: all twelve cases clean): runs under it left
+        # GPUs needing a reset there.  Opt in explicitly where it is allowed.
+        pytest.skip("compute-sanitizer closed on the GPU pool (AM_RUN_SANITIZER=1 to run)")
     cmd = [SAN, "--tool", tool, "--error-exitcode", "97", "--print-limit", "20"]
     if tool == "memcheck":
         cmd += ["--leak-check", "no"]
