@@ -72,6 +72,44 @@ __device__ __forceinline__ int2 policy_move(const RepDev& r, int i, int s, int2 
     return policy_move_g(r.sy, r.d.map_w, r.d.map_h, i, s, p, dig);
 }
 
+// The commit of one agent i (old step s0) at time t of its simulation b: world state,
+// trajectory hash, the tracker's state in place (inplace), the loose-cell drift.
+// Returns the new step; done = reached the target.
+__device__ __forceinline__ int commit_agent(const RepDev& r, int i, int s0, int b, long long t, bool inplace,
+                                            uint32_t c, uint32_t tag, bool& done, int& dmax, int& err)
+{
+    const Dev& d = r.d;
+    const int2 np = r.newpos[i];
+    const int2 op = r.pos[i];
+    const int s = (inplace ? s0 : r.steps[i]) + 1;
+    r.pos[i] = np;
+    r.steps[i] = s;
+    r.traj[i] = traj_step(r.traj[i], s, np.x, np.y);
+    done = d.target > 0 && s == d.target;
+    if (done) atomicMax((unsigned long long*)(r.tdone + b), (unsigned long long)t);
+    if (inplace) {
+        // the speed limit the soundness of the rules rests on
+        if (!within_pts(d, op.x, op.y, np.x, np.y, (uint32_t)d.v)) err |= ERR_VELOCITY;
+        const uint8_t nst = done ? ST_DONE : ST_IDLE;
+        d.pos[c][i] = np;
+        d.step[c][i] = s;
+        d.status[c][i] = nst;
+        d.chg8[i] = 1;
+        const int lab = d.labels[i];
+        if (lab >= 0) d.dirty[lab] = d.ctl->epoch + 1u;
+        const uint32_t rr = d.slot[i];
+        if (rr != kSentinel) {
+            d.rec[rr] = make_int4(np.x | (np.y << 16), s, i, (int)nst | (int)(tag << kTagShift));
+            int cx, cy;
+            mkey_decode(d, d.key[i], cx, cy);
+            const int x0 = cx << d.clog, y0 = cy << d.clog;
+            const int x1 = x0 + (1 << d.clog) - 1, y1 = y0 + (1 << d.clog) - 1;
+            dmax = max(dmax, max(max(x0 - np.x, np.x - x1), max(y0 - np.y, np.y - y1)));
+        }
+    }
+    return s;
+}
+
 // commit every RUNNING agent whose cluster completed (tcommit <= t_sim, the clock
 // k_disp_b just advanced): the move computed at dispatch is applied and the step
 // advances (worker l.20-21).  Agents that stay RUNNING bound the next
@@ -83,23 +121,30 @@ __device__ __forceinline__ int2 policy_move(const RepDev& r, int i, int s, int2 
 // -- and every block adds its {min step, max step, active, running} of the post-commit
 // state to one of 64 reduction stripes for k_replay_begin, so the next round needs no
 // O(N) ingest.
+// Each thread reads kCommitItems agents' status / completion time / step (all loads in
+// flight together); the ~4% that commit are compacted per warp (ballot) into a shared
+// list and committed by consecutive lanes, so a warp runs the scattered commit path
+// once per 32 commits instead of once per 32 agents with any commit among them.
 __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
 {
     pdl_begin();
+    constexpr int KC = kCommitItems;
+    __shared__ int2 s_cl[8][32 * KC];   // per warp: {agent, old step} of the committing agents
     const Dev& d = r.d;
     const bool one = d.n_sims == 1;
     const uint32_t c = d.ctl->cur;
     const uint32_t tag = (d.ctl->epoch + 1u) & kTagMask;   // the round this commit feeds
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned long long tmin = ~0ull;  // pending completions (single-simulation case)
     int any_active = 0;
     int wmin = INT_MAX, smax = INT_MIN, nact = 0, nrun = 0, dmax = 0, err = 0;
     // loads of all items first (independent chains in flight), then the commits
-    uint8_t st[kCommitItems];
-    long long tc[kCommitItems];
-    int sw[kCommitItems];
+    uint8_t st[KC];
+    long long tc[KC];
+    int sw[KC];
 #pragma unroll
-    for (int k = 0; k < kCommitItems; k++) {
-        const int i = blockIdx.x * (256 * kCommitItems) + k * 256 + threadIdx.x;
+    for (int k = 0; k < KC; k++) {
+        const int i = blockIdx.x * (256 * KC) + k * 256 + threadIdx.x;
         st[k] = ST_DONE;
         tc[k] = 0;
         sw[k] = 0;
@@ -110,86 +155,67 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
         }
     }
     const long long t1 = one ? r.t_sim[0] : 0;
-    int ncommit = 0;
+    int nlist = 0;   // warp uniform
 #pragma unroll
-    for (int k = 0; k < kCommitItems; k++) {
-        const int i = blockIdx.x * (256 * kCommitItems) + k * 256 + threadIdx.x;
-        if (st[k] == ST_DONE) continue;
-        if (r.K > 0 && st[k] == ST_RUNNING && tc[k] == LLONG_MAX) {
-            // queued: did its cluster start this round (k_qstart)?
-            const int lab = (int)(r.qkey[i] & ((1ull << r.qidb) - 1ull));
-            if (r.qstart_ep[lab] == d.ctl->epoch) {
-                tc[k] = r.qstart_t[lab];
-                r.tcommit[i] = tc[k];
-            }
-        }
-        const int b = sim_of(d, i);
-        const long long t = one ? t1 : r.t_sim[b];
-        bool active = true;
-        bool running = st[k] == ST_RUNNING;
-        if (st[k] == ST_RUNNING) {
-            if (tc[k] <= t) {
-                const int2 np = r.newpos[i];
-                const int2 op = r.pos[i];
-                const int s = (inplace ? sw[k] : r.steps[i]) + 1;
-                sw[k] = s;
-                r.pos[i] = np;
-                r.steps[i] = s;
-                r.traj[i] = traj_step(r.traj[i], s, np.x, np.y);
-                const bool done = d.target > 0 && s == d.target;
-                if (done) {
-                    active = false;
-                    atomicMax((unsigned long long*)(r.tdone + b), (unsigned long long)t);
+    for (int k = 0; k < KC; k++) {
+        const int i = blockIdx.x * (256 * KC) + k * 256 + threadIdx.x;
+        bool commit = false;
+        if (st[k] != ST_DONE) {
+            if (r.K > 0 && st[k] == ST_RUNNING && tc[k] == LLONG_MAX) {
+                // queued: did its cluster start this round (k_qstart)?
+                const int lab = (int)(r.qkey[i] & ((1ull << r.qidb) - 1ull));
+                if (r.qstart_ep[lab] == d.ctl->epoch) {
+                    tc[k] = r.qstart_t[lab];
+                    r.tcommit[i] = tc[k];
                 }
-                running = false;
-                ncommit++;
+            }
+            const int b = sim_of(d, i);
+            const long long t = one ? t1 : r.t_sim[b];
+            commit = st[k] == ST_RUNNING && tc[k] <= t;
+            if (!commit) {
+                if (st[k] == ST_RUNNING) {
+                    // stays RUNNING through this round: bounds the next event
+                    if (one) tmin = min(tmin, (unsigned long long)tc[k]);
+                    else atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc[k]);
+                }
+                if (one) any_active = 1;
+                else r.active_flag[b] = 1;
                 if (inplace) {
-                    // the speed limit the soundness of the rules rests on
-                    if (!within_pts(d, op.x, op.y, np.x, np.y, (uint32_t)d.v)) err |= ERR_VELOCITY;
-                    const uint8_t nst = done ? ST_DONE : ST_IDLE;
-                    d.pos[c][i] = np;
-                    d.step[c][i] = s;
-                    d.status[c][i] = nst;
-                    d.chg8[i] = 1;
-                    const int lab = d.labels[i];
-                    if (lab >= 0) d.dirty[lab] = d.ctl->epoch + 1u;
-                    const uint32_t rr = d.slot[i];
-                    if (rr != kSentinel) {
-                        d.rec[rr] = make_int4(np.x | (np.y << 16), s, i, (int)nst | (int)(tag << kTagShift));
-                        int cx, cy;
-                        mkey_decode(d, d.key[i], cx, cy);
-                        const int x0 = cx << d.clog, y0 = cy << d.clog;
-                        const int x1 = x0 + (1 << d.clog) - 1, y1 = y0 + (1 << d.clog) - 1;
-                        dmax = max(dmax, max(max(x0 - np.x, np.x - x1), max(y0 - np.y, np.y - y1)));
-                    }
+                    wmin = min(wmin, sw[k]);
+                    smax = max(smax, sw[k]);
+                    nact++;
+                    nrun += st[k] == ST_RUNNING;
                 }
-            } else if (one) {
-                tmin = min(tmin, (unsigned long long)tc[k]);
-            } else {
-                // stays RUNNING through this round: bounds the next event
-                atomicMin((unsigned long long*)(r.tnext + b), (unsigned long long)tc[k]);
             }
         }
-        if (active) {
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, commit);
+        if (commit) s_cl[w][nlist + __popc(bal & ((1u << lane) - 1u))] = make_int2(i, sw[k]);
+        nlist += __popc(bal);
+    }
+    __syncwarp();
+    // the warp's committing agents, one per lane
+    for (int j = lane; j < nlist; j += 32) {
+        const int2 e = s_cl[w][j];
+        const int b = sim_of(d, e.x);
+        const long long t = one ? t1 : r.t_sim[b];
+        bool done;
+        const int s = commit_agent(r, e.x, e.y, b, t, inplace != 0, c, tag, done, dmax, err);
+        if (!done) {
             if (one) any_active = 1;
             else r.active_flag[b] = 1;
             if (inplace) {
-                const int s = sw[k];
                 wmin = min(wmin, s);
                 smax = max(smax, s);
                 nact++;
-                nrun += running;
             }
         }
     }
     if (r.K > 0 && one) {   // agent-steps leaving service (finite capacity)
-        ncommit = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)ncommit);
-        if ((threadIdx.x & 31) == 0 && ncommit) atomicAdd((unsigned long long*)r.busy, (unsigned long long)(-(long long)ncommit));
+        if (lane == 0 && nlist) atomicAdd((unsigned long long*)r.busy, (unsigned long long)(-(long long)nlist));
     }
     if (one) {  // block reduction, one atomic per block
         __shared__ unsigned long long s_min[8];
         __shared__ int s_act[8];
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         for (int o = 16; o > 0; o >>= 1) tmin = min(tmin, __shfl_xor_sync(0xFFFFFFFFu, tmin, o));
         any_active = __reduce_or_sync(0xFFFFFFFFu, (unsigned)any_active);
         if (lane == 0) { s_min[w] = tmin; s_act[w] = any_active; }
@@ -202,7 +228,6 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
     }
     if (inplace) {   // the post-commit state's reduction: one atomic per quantity per block, 64 stripes
         __shared__ int p_w[8], p_s[8], p_a[8], p_r[8], p_d[8], p_e[8];
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         wmin = __reduce_min_sync(0xFFFFFFFFu, wmin);
         smax = __reduce_max_sync(0xFFFFFFFFu, smax);
         nact = (int)__reduce_add_sync(0xFFFFFFFFu, (unsigned)nact);

@@ -375,8 +375,27 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
             d.parent[i] = dirty ? (uint32_t)i : (uint32_t)lab;
             d.agflag[i] = (uint8_t)((chg ? 1 : 0) | (dirty ? 2 : 0));
             // the scan's work queue (incremental scan): changed
-            // agents, and IDLE agents whose recorded blocker (witness) changed
-            work = chg || (st == ST_IDLE && w != kSentinel && agent_changed(d, c, w));
+            // agents, and IDLE agents whose recorded blocker (witness) changed and no
+            // longer blocks them at its new state (a witness that committed one step and
+            // moved <= v is usually still inside the shrunk radius R_b(s - s_w), P:406:
+            // the verdict "blocked" and the witness stand, exactly)
+            work = chg;
+            if (!chg && st == ST_IDLE && w != kSentinel && agent_changed(d, c, w)) {
+#if AM_WIT_RECHECK
+                const int sw = d.step[c][w];
+                bool still = false;
+                if (sw < s && d.status[c][w] != ST_DONE) {
+                    const int2 pw = d.pos[c][w];
+                    const uint32_t R = rb32(s - sw, d.lagcap, d.v, d.r_p);
+                    const int dx = pw.x - p.x, dy = pw.y - p.y;
+                    still = d.metric == AM_METRIC_LINF ? ((uint32_t)abs(dx) <= R && (uint32_t)abs(dy) <= R)
+                                                       : (uint32_t)(dx * dx) + (uint32_t)(dy * dy) <= R * R;
+                }
+                work = !still;
+#else
+                work = true;
+#endif
+            }
             q = make_int4(p.x | (p.y << 16), s, (int)((uint32_t)i | (chg ? 0x80000000u : 0u)), st);
         }
     }
@@ -682,7 +701,7 @@ __device__ __forceinline__ void morton_child(int k, int& dx, int& dy)
 
 // Work counters of the half-warp scan (AM_STATS and the far-item count).
 struct HwStats {
-    uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0;
+    uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0, nblk = 0;
 };
 
 // per-warp reduction of the half-warp scan counters, one atomic per warp (no block
@@ -694,7 +713,9 @@ __device__ __forceinline__ void hw_flush_stats(const Dev& d, const HwStats& hs, 
     if (d.flags & AM_STATS) {
         const unsigned c0 = __reduce_add_sync(0xFFFFFFFFu, hs.ncells), c1 = __reduce_add_sync(0xFFFFFFFFu, hs.ncand);
         const unsigned c3 = __reduce_add_sync(0xFFFFFFFFu, hs.nb2), c4 = __reduce_add_sync(0xFFFFFFFFu, hs.nb1);
+        const unsigned c5 = __reduce_add_sync(0xFFFFFFFFu, hs.nblk);
         if (lane == 0) {
+            atomicAdd(&d.ctl->st_blocked, (unsigned long long)c5);
             atomicAdd(&d.ctl->st_cells, (unsigned long long)c0);
             atomicAdd(&d.ctl->st_cand, (unsigned long long)c1);
             atomicAdd(&d.ctl->st_p2, (unsigned long long)it);   // far work items (4x4 blocks)
@@ -830,9 +851,11 @@ constexpr int kDirectFull = AM_DIRECT_FULL; // the same for rounds the host know
 
 // test the records of the cells in `list[0..nl)` (near cells first: nn of them) against
 // A; returns (in nblk/wit) the first blocker; stages coupling edges for a changed A
-__device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const int2* list, int nl, int nn, int ax,
-                                           int ay, int as, uint32_t aid, bool chg, bool idle, uint32_t ep, int l,
-                                           int h, unsigned hm, bool& nblk, uint32_t& wit, HwStats& hs)
+// (list[0, nn) near cells; the far cells follow at list[fgap + nn, fgap + nl): fgap = 0
+// when they were appended, the gap to the end of the buffer when they fill it backwards)
+__device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const int2* list, int nl, int nn, int fgap,
+                                           int ax, int ay, int as, uint32_t aid, bool chg, bool idle, uint32_t ep,
+                                           int l, int h, unsigned hm, bool& nblk, uint32_t& wit, HwStats& hs)
 {
     const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
     const uint32_t Rc2 = Rc * Rc;
@@ -843,7 +866,7 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
         const int k = c0 + l;
         int st0 = 0, cnt = 0;
         if (k < nl) {
-            const int2 e = list[k];
+            const int2 e = list[k < nn ? k : k + fgap];
             st0 = e.x;
             cnt = e.y;
         }
@@ -989,8 +1012,38 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
                     }
                 }
                 // classify, compact into the list: near cells first, then far cells
-                // (pass 0 records which cells are near; pass 1 tests only the others)
-                int nn = 0, nl = 0;
+                int nn = 0, nl = 0, fgap = 0;
+#if AM_SCAN_1PASS
+                // one pass: near cells compacted from the front of the list, far cells
+                // from its end (each cell's row / column and box distance computed once)
+                {
+                    int nf = 0;
+#pragma unroll
+                    for (int j = 0; j < KD / 16; j++) {
+                        if (j >= ngrp) break;                    // half-warp uniform
+                        const int k = cb + j * 16 + l;
+                        bool okn = false, okf = false;
+                        if (k < ncell && nxt[j] > ent[j].x) {
+                            const int mn = ent[j].y;
+                            const int ky = krow(k);
+                            const int cx = cx0 + (k - ky * ncx), cy = cy0 + ky;
+                            const bool isnear = cell_within(ax, ay, cx, cy, cl, D, Rc, d.metric);
+                            okn = isnear && (chg ? mn <= as : (idle && mn < as));
+                            okf = !isnear && far && direct && mn < as &&
+                                  cell_within(ax, ay, cx, cy, cl, D, rb32(as - mn, d.lagcap, d.v, d.r_p), d.metric);
+                        }
+                        const unsigned bn = (__ballot_sync(hm, okn) >> (16 * h)) & 0xFFFFu;
+                        const unsigned bf = (__ballot_sync(hm, okf) >> (16 * h)) & 0xFFFFu;
+                        const unsigned lt = (1u << l) - 1u;
+                        if (okn) list[nn + __popc(bn & lt)] = make_int2(ent[j].x, nxt[j] - ent[j].x);
+                        if (okf) list[KD - 1 - (nf + __popc(bf & lt))] = make_int2(ent[j].x, nxt[j] - ent[j].x);
+                        nn += __popc(bn);
+                        nf += __popc(bf);
+                    }
+                    nl = nn + nf;
+                    fgap = KD - nl;   // far entry q (0-based) at list[KD - 1 - q] = list[fgap + nn + (nf - 1 - q)]
+                }
+#else
                 unsigned nearbits = 0;
 #pragma unroll
                 for (int pass = 0; pass < 2; pass++) {
@@ -1020,9 +1073,10 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
                     }
                     if (pass == 0) nn = nl;
                 }
+#endif
                 hs.ncells += l == 0 ? (uint32_t)nl : 0u;
                 __syncwarp(hm);
-                hw_records(d, sm, list, nl, nn, ax, ay, as, aid, chg, idle, ep, l, h, hm, nblk, wit, hs);
+                hw_records(d, sm, list, nl, nn, fgap, ax, ay, as, aid, chg, idle, ep, l, h, hm, nblk, wit, hs);
                 __syncwarp(hm);   // the list is rewritten by the next chunk / agent
             }
             if (idle) {
@@ -1030,6 +1084,7 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
                     wit = hw_far(d, ax, ay, as, W, D, l, h, hm, ox_l, oy_l, hs);
                     nblk = wit != kSentinel;
                 }
+                hs.nblk += (l == 0 && nblk) ? 1u : 0u;
                 if (l == 0) {
                     d.v8[aid] = nblk ? 1 : 0;
                     d.witness[aid] = nblk ? wit : kSentinel;

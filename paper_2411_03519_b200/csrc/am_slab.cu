@@ -137,6 +137,7 @@ __global__ void k_sl_load(SlabDev s, int m, const int32_t* __restrict__ gid, con
 // the tracker's input positions (window coordinates) and the per-cluster scratch reset
 __global__ void k_sl_prep(SlabDev s, int32_t* mbuf)
 {
+    pdl_begin();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.L; i += gridDim.x * blockDim.x) {
         const int2 p = s.pos[i];
         s.tpos[i] = s.gid[i] >= 0 ? make_int2(p.x, p.y - s.y0) : make_int2(0, 0);
@@ -154,6 +155,7 @@ __global__ void k_sl_prep(SlabDev s, int32_t* mbuf)
 // of the owned IDLE members, boundary flag
 __global__ void k_sl_clusters(SlabDev s, int stale)
 {
+    pdl_begin();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.L; i += gridDim.x * blockDim.x) {
         const uint8_t st = s.stat[i];
         if (st == ST_DONE) continue;
@@ -178,6 +180,7 @@ __global__ void k_sl_clusters(SlabDev s, int stale)
 // per boundary cluster (from its root slot)
 __global__ void k_sl_records(SlabDev s, int32_t* __restrict__ mbuf)
 {
+    pdl_begin();
     int32_t* counts = mbuf;
     int2* links = reinterpret_cast<int2*>(mbuf + 4);
     int4* clusters = reinterpret_cast<int4*>(mbuf + 4 + 2 * (size_t)s.g.cap_merge);
@@ -242,6 +245,7 @@ __device__ __forceinline__ int4 mcluster(const SlabDev& s, const int32_t* mb, in
 // merge kernels: blockIdx.y = the rank whose records a block walks, up to their count
 __global__ void k_sl_unite(SlabDev s, const int32_t* __restrict__ mbufs)
 {
+    pdl_begin();
     const int r = blockIdx.y;
     const int32_t* mb = mbuf_of(s, mbufs, r);
     const int nl = min(mb[0], s.g.cap_merge);
@@ -255,6 +259,7 @@ __global__ void k_sl_unite(SlabDev s, const int32_t* __restrict__ mbufs)
 
 __global__ void k_sl_cbad(SlabDev s, const int32_t* __restrict__ mbufs)
 {
+    pdl_begin();
     const int r = blockIdx.y;
     const int32_t* mb = mbuf_of(s, mbufs, r);
     const int nc = min(mb[1], s.g.cap_merge);
@@ -269,6 +274,7 @@ __global__ void k_sl_cbad(SlabDev s, const int32_t* __restrict__ mbufs)
 
 __global__ void k_sl_stats_init(SlabDev s, long long* stats)
 {
+    pdl_begin();
     if (threadIdx.x == 0) {
         stats[0] = kNever;   // next event
         stats[1] = kNever;   // W
@@ -283,6 +289,7 @@ __global__ void k_sl_stats_init(SlabDev s, long long* stats)
 // time, priority key), then this rank's next event, W, S and activity
 __global__ void __launch_bounds__(256) k_sl_final(SlabDev s, long long* stats)
 {
+    pdl_begin();
     const long long t = s.counters[0];
     const int W = s.tctl->W;
     const int idb = s.idb;
@@ -366,6 +373,7 @@ __global__ void __launch_bounds__(256) k_sl_final(SlabDev s, long long* stats)
 // the forest, bad, duration and touched marks back to their neutral values
 __global__ void k_sl_restore(SlabDev s, const int32_t* __restrict__ mbufs)
 {
+    pdl_begin();
     const int r = blockIdx.y, cap = s.g.cap_merge;
     const int32_t* mb = mbuf_of(s, mbufs, r);
     const int nmax = max(min(mb[0], cap), min(mb[1], cap));
@@ -391,6 +399,7 @@ __global__ void k_sl_restore(SlabDev s, const int32_t* __restrict__ mbufs)
 // perceived agents are in the window)
 __global__ void k_sl_moves(SlabDev s)
 {
+    pdl_begin();
     const int nr = s.sctl->n_ready;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x) {
         const int i = s.rlist[k];
@@ -415,6 +424,7 @@ __device__ __forceinline__ const int32_t* dblock(const SlabDev& s, const int32_t
 // sync round may be idle; only a sync round with nothing pending is a liveness failure)
 __global__ void k_sl_clock(SlabDev s, const long long* __restrict__ gstats, int32_t* dsend, int stale)
 {
+    pdl_begin();
     if (dsend)
         for (int r = threadIdx.x; r < s.g.n_slabs; r += blockDim.x)
             for (int q = 0; q < 6; q++) dblock(s, dsend, r)[q] = 0;   // counts (headers)
@@ -442,6 +452,7 @@ __global__ void k_sl_clock(SlabDev s, const long long* __restrict__ gstats, int3
 // exchange, which sends them to every rank whose window they were or are in
 __global__ void k_sl_commit(SlabDev s)
 {
+    pdl_begin();
     const long long t = s.counters[0];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.L; i += gridDim.x * blockDim.x) {
         if (s.stat[i] != ST_RUNNING || !s.own[i] || s.tc[i] > t) continue;   // ghosts are committed by their owner
@@ -464,6 +475,7 @@ __global__ void k_sl_commit(SlabDev s)
 // the row: an agent that left the slab becomes a ghost here
 __global__ void k_sl_flush(SlabDev s, int32_t* __restrict__ dsend)
 {
+    pdl_begin();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.L; i += gridDim.x * blockDim.x) {
         if (!s.dirty[i]) continue;
         s.dirty[i] = 0;
@@ -501,6 +513,7 @@ __global__ void k_sl_flush(SlabDev s, int32_t* __restrict__ dsend)
 // departures first (their slots return to the free stack) ...
 __global__ void k_sl_depart(SlabDev s, const int32_t* __restrict__ drecv)
 {
+    pdl_begin();
     const int r = blockIdx.y;   // the sender
     if (r == s.g.my_slab) return;
     const int32_t* blk = dblock(s, drecv, r);
@@ -523,6 +536,7 @@ __global__ void k_sl_depart(SlabDev s, const int32_t* __restrict__ drecv)
 // ... then moved agents and arrivals (a free slot each)
 __global__ void k_sl_arrive(SlabDev s, const int32_t* __restrict__ drecv)
 {
+    pdl_begin();
     const int r = blockIdx.y;   // the sender
     if (r == s.g.my_slab) return;
     const int32_t* blk = dblock(s, drecv, r);
@@ -769,9 +783,9 @@ extern "C" int am_slab_load(am_slab* sl, int32_t m, const int32_t* gid, const in
 {
     if (!sl || m < 0 || m > sl->s.L || (m && (!gid || !pos || !steps || !status))) return AM_E_ARG;
     SK(cudaMemsetAsync(sl->s.map, 0xFF, 4 * (size_t)sl->s.g.n_total, sl->stream));
-    k_sl_load<<<grid_for(sl, sl->s.L), 256, 0, sl->stream>>>(sl->s, m, gid, (const int2*)pos, steps, status,
+    SK(launch_k(false, sl->stream, k_sl_load, grid_for(sl, sl->s.L), 256, 0, sl->s, m, gid, (const int2*)pos, steps, status,
                                                              (const unsigned long long*)traj, (const long long*)tcommit,
-                                                             (const int2*)newpos, (long long)t);
+                                                             (const int2*)newpos, (long long)t));
     SK(cudaGetLastError());
     am_reset(sl->tr);   // the next round recomputes the window from scratch
     return AM_OK;
@@ -782,14 +796,14 @@ extern "C" int am_slab_round_local(am_slab* sl, int32_t* mbuf)
     if (!sl || !mbuf) return AM_E_ARG;
     SlabDev& s = sl->s;
     const unsigned gr = grid_for(sl, s.L);
-    k_sl_prep<<<gr, 256, 0, sl->stream>>>(s, mbuf);
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_prep, gr, 256, 0, s, mbuf));
     SK(cudaGetLastError());
     int rc = am_update_replica(sl->tr, (const int32_t*)s.tpos, s.step, s.stat);
     if (rc) return rc;
     rc = am_ready(sl->tr, sl->tmask, sl->torder, nullptr);   // AM_PEEK | AM_ASYNC
     if (rc) return rc;
-    k_sl_clusters<<<gr, 256, 0, sl->stream>>>(s, 0);
-    k_sl_records<<<gr, 256, 0, sl->stream>>>(s, mbuf);
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_clusters, gr, 256, 0, s, 0));
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_records, gr, 256, 0, s, mbuf));
     SK(cudaGetLastError());
     sl->last_stale = false;
     return AM_OK;
@@ -804,19 +818,23 @@ extern "C" int am_slab_round_stale(am_slab* sl, int32_t* order_out, int32_t* n_o
     if (!sl || !order_out || !n_order || !stats) return AM_E_ARG;
     SlabDev& s = sl->s;
     const unsigned gr = grid_for(sl, s.L);
-    k_sl_prep<<<gr, 256, 0, sl->stream>>>(s, nullptr);
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_prep, gr, 256, 0, s, nullptr));
     SK(cudaGetLastError());
     int rc = am_update_replica(sl->tr, (const int32_t*)s.tpos, s.step, s.stat);
     if (rc) return rc;
     rc = am_ready(sl->tr, sl->tmask, sl->torder, nullptr);   // AM_PEEK | AM_ASYNC
     if (rc) return rc;
-    k_sl_clusters<<<gr, 256, 0, sl->stream>>>(s, 1);
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_clusters, gr, 256, 0, s, 1));
     SK(cudaGetLastError());
     sl->last_stale = true;
     return slab_finish(sl, nullptr, order_out, n_order, stats);
 }
 
-__global__ void k_sl_norder(const Ctl* c, int32_t* n) { *n = c->n_ready; }
+__global__ void k_sl_norder(const Ctl* c, int32_t* n)
+{
+    pdl_begin();
+    *n = c->n_ready;
+}
 
 extern "C" int am_slab_merge(am_slab* sl, const int32_t* mbufs, int32_t* order_out, int32_t* n_order, int64_t* stats)
 {
@@ -833,18 +851,18 @@ static int slab_finish(am_slab* sl, const int32_t* mbufs, int32_t* order_out, in
                   (unsigned)s.g.n_slabs);
     const unsigned gr = grid_for(sl, s.L);
     if (mbufs) {
-        k_sl_unite<<<gm, 256, 0, sl->stream>>>(s, mbufs);
-        k_sl_cbad<<<gm, 256, 0, sl->stream>>>(s, mbufs);
+        SK(launch_k(sl->tr->pdl, sl->stream, k_sl_unite, gm, 256, 0, s, mbufs));
+        SK(launch_k(sl->tr->pdl, sl->stream, k_sl_cbad, gm, 256, 0, s, mbufs));
     }
-    k_sl_stats_init<<<1, 32, 0, sl->stream>>>(s, (long long*)stats);
-    k_sl_final<<<gr, 256, 0, sl->stream>>>(s, (long long*)stats);
-    if (mbufs) k_sl_restore<<<gm, 256, 0, sl->stream>>>(s, mbufs);
-    k_sl_norder<<<1, 1, 0, sl->stream>>>(s.sctl, n_order);
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_stats_init, 1, 32, 0, s, (long long*)stats));
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_final, gr, 256, 0, s, (long long*)stats));
+    if (mbufs) SK(launch_k(sl->tr->pdl, sl->stream, k_sl_restore, gm, 256, 0, s, mbufs));
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_norder, 1, 1, 0, s.sctl, n_order));
     SK(cudaGetLastError());
     // perception digests of the dispatched agents (global ids in the terms), their moves
     int rc = am_internal_digest(sl->tr, s.rlist, &s.sctl->n_ready, s.gid, s.dig, s.L, sl->stream);
     if (rc) return rc;
-    k_sl_moves<<<gr, 256, 0, sl->stream>>>(s);
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_moves, gr, 256, 0, s));
     SK(cudaGetLastError());
     // the rank's priority order: unique keys (lag, global label, id) -> global ids
     return am_internal_csort(sl->tr, sl->sd, order_out, sl->stream);
@@ -854,9 +872,9 @@ extern "C" int am_slab_commit(am_slab* sl, const int64_t* stats_global, int32_t*
 {
     if (!sl || !stats_global) return AM_E_ARG;
     SlabDev& s = sl->s;
-    k_sl_clock<<<1, 256, 0, sl->stream>>>(s, (const long long*)stats_global, dsend, sl->last_stale ? 1 : 0);
-    k_sl_commit<<<grid_for(sl, s.L), 256, 0, sl->stream>>>(s);
-    if (dsend) k_sl_flush<<<grid_for(sl, s.L), 256, 0, sl->stream>>>(s, dsend);
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_clock, 1, 256, 0, s, (const long long*)stats_global, dsend, sl->last_stale ? 1 : 0));
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_commit, grid_for(sl, s.L), 256, 0, s));
+    if (dsend) SK(launch_k(sl->tr->pdl, sl->stream, k_sl_flush, grid_for(sl, s.L), 256, 0, s, dsend));
     SK(cudaGetLastError());
     return AM_OK;
 }
@@ -868,8 +886,8 @@ extern "C" int am_slab_apply(am_slab* sl, const int32_t* drecv)
     const dim3 g(std::max(1u, std::min((unsigned)((s.g.cap_peer + 255) / 256), (unsigned)(sl->num_sms * 4) /
                                                                                (unsigned)s.g.n_slabs)),
                  (unsigned)s.g.n_slabs);
-    k_sl_depart<<<g, 256, 0, sl->stream>>>(s, drecv);
-    k_sl_arrive<<<g, 256, 0, sl->stream>>>(s, drecv);
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_depart, g, 256, 0, s, drecv));
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_arrive, g, 256, 0, s, drecv));
     SK(cudaGetLastError());
     return AM_OK;
 }
