@@ -34,12 +34,6 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #ifndef AM_COMMIT_ITEMS
 #define AM_COMMIT_ITEMS 8   // k_commit: agents per thread (commits compacted per warp)
 #endif
-#ifndef AM_WIT_RECHECK
-#define AM_WIT_RECHECK 1   // k_scatter re-tests a changed witness before queueing its agent
-#endif
-#ifndef AM_CSORT_SMALL
-#define AM_CSORT_SMALL 1   // k_csort: ready sets <= 8192 sorted by one CTA (bitonic, shared memory)
-#endif
 #ifndef AM_SCAN_1PASS
 #define AM_SCAN_1PASS 1   // scan_hw: near and far cells classified in one pass
 #endif

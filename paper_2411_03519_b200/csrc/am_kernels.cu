@@ -375,27 +375,8 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
             d.parent[i] = dirty ? (uint32_t)i : (uint32_t)lab;
             d.agflag[i] = (uint8_t)((chg ? 1 : 0) | (dirty ? 2 : 0));
             // the scan's work queue (incremental scan): changed
-            // agents, and IDLE agents whose recorded blocker (witness) changed and no
-            // longer blocks them at its new state (a witness that committed one step and
-            // moved <= v is usually still inside the shrunk radius R_b(s - s_w), P:406:
-            // the verdict "blocked" and the witness stand, exactly)
-            work = chg;
-            if (!chg && st == ST_IDLE && w != kSentinel && agent_changed(d, c, w)) {
-#if AM_WIT_RECHECK
-                const int sw = d.step[c][w];
-                bool still = false;
-                if (sw < s && d.status[c][w] != ST_DONE) {
-                    const int2 pw = d.pos[c][w];
-                    const uint32_t R = rb32(s - sw, d.lagcap, d.v, d.r_p);
-                    const int dx = pw.x - p.x, dy = pw.y - p.y;
-                    still = d.metric == AM_METRIC_LINF ? ((uint32_t)abs(dx) <= R && (uint32_t)abs(dy) <= R)
-                                                       : (uint32_t)(dx * dx) + (uint32_t)(dy * dy) <= R * R;
-                }
-                work = !still;
-#else
-                work = true;
-#endif
-            }
+            // agents, and IDLE agents whose recorded blocker (witness) changed
+            work = chg || (st == ST_IDLE && w != kSentinel && agent_changed(d, c, w));
             q = make_int4(p.x | (p.y << 16), s, (int)((uint32_t)i | (chg ? 0x80000000u : 0u)), st);
         }
     }

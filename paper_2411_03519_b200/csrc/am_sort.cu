@@ -313,38 +313,6 @@ __device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned ch
     }
 }
 
-// Small ready sets (n <= kCsSmall: a slab's ready set, C4's): CTA 0 alone, no passes,
-// no cluster barriers.  Every key is made unique by appending its input position (the
-// compaction is in id order, so ties resolve to the stable order the LSD passes give),
-// the n composite keys are sorted by a bitonic network in shared memory (keys padded
-// with ~0 to a power of two), and the ids are read back by position.  The multi-pass
-// cluster sort costs ~11 us per 9-bit pass whatever n is; this costs log2(P)(log2(P)+1)/2
-// block barriers.
-constexpr int kCsSmallLog = 13;
-constexpr int kCsSmall = 1 << kCsSmallLog;
-
-__device__ void csort_small(const Dev& d, int32_t* __restrict__ order, unsigned char* smem, int n)
-{
-    unsigned long long* sk = reinterpret_cast<unsigned long long*>(smem);
-    const int t = threadIdx.x;
-    int P = 2;
-    while (P < n) P <<= 1;
-    for (int i = t; i < P; i += kCsThreads)
-        sk[i] = i < n ? (d.rkey[0][i] << kCsSmallLog) | (unsigned long long)i : ~0ull;
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = t; i < (P >> 1); i += kCsThreads) {
-                const int a = ((i & ~(j - 1)) << 1) | (i & (j - 1)), b = a + j;
-                const unsigned long long x = sk[a], y = sk[b];
-                if ((x > y) == ((a & k) == 0)) { sk[a] = y; sk[b] = x; }
-            }
-            __syncthreads();
-        }
-    }
-    for (int i = t; i < n; i += kCsThreads) order[i] = (int32_t)d.rval[0][(int)(sk[i] & (kCsSmall - 1))];
-}
-
 __global__ void __launch_bounds__(kCsThreads, 1) k_csort(Dev d, int32_t* __restrict__ order, int smem_bytes)
 {
     pdl_begin();
@@ -361,10 +329,6 @@ __global__ void __launch_bounds__(kCsThreads, 1) k_csort(Dev d, int32_t* __restr
     if (np == 0) {   // every key equal: the compaction order (id) is the order
         const int me = (int)cg::this_cluster().block_rank();
         for (int k = me * kCsThreads + threadIdx.x; k < n; k += C * kCsThreads) order[k] = (int32_t)d.rval[0][k];
-        return;
-    }
-    if (AM_CSORT_SMALL && n <= kCsSmall && bits + kCsSmallLog <= 64) {
-        if (cg::this_cluster().block_rank() == 0) csort_small(d, order, cs_smem, n);
         return;
     }
     // elements per thread per tile: as few as the chunk needs (shorter serial work)
