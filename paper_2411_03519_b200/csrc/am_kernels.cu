@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(256) k_scan_thread(Dev d)
         const int ax = A.x & 0xFFFF, ay = A.x >> 16, as = A.y;
         const uint32_t aid = (uint32_t)A.z;
         const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
-        const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+        const uint32_t Rc = min((uint32_t)(d.r_p + d.v), kRClamp);   // r_p, v <= kRClamp (am_init)
         unsigned long long dig = 0;
         // ---- phase 1
         {
@@ -721,8 +721,8 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
                                            unsigned hm, int ox_l, int oy_l, HwStats& hs)
 {
     const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2x = (1 << d.gxlog) >> 4, G2y = (1 << d.gylog) >> 4;
-    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
-    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+    const uint32_t Rc = min((uint32_t)(d.r_p + d.v), kRClamp);   // r_p, v <= kRClamp (am_init)
+    const int lagcap = d.lagcap;   // host-computed kRClamp / v + 1
     uint32_t& ncells = hs.ncells;
     uint32_t& ncand = hs.ncand;
     uint32_t& nb2 = hs.nb2;
@@ -838,9 +838,9 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
                                            int ax, int ay, int as, uint32_t aid, bool chg, bool idle, uint32_t ep,
                                            int l, int h, unsigned hm, bool& nblk, uint32_t& wit, HwStats& hs)
 {
-    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const uint32_t Rc = min((uint32_t)(d.r_p + d.v), kRClamp);   // r_p, v <= kRClamp (am_init)
     const uint32_t Rc2 = Rc * Rc;
-    const int lagcap = (int)(kRClamp / (uint32_t)max(1, d.v)) + 1;
+    const int lagcap = d.lagcap;   // host-computed kRClamp / v + 1
     for (int c0 = 0; c0 < nl; c0 += 16) {
         // nothing left to decide: blocked (or not IDLE) and no coupling in the rest
         if ((nblk || !idle) && (!chg || c0 >= nn)) break;
@@ -911,7 +911,7 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
     __shared__ int2 s_list[16][KD];
     __shared__ int s_pref[kEdgeStripes + 1];
     const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4, hw = threadIdx.x >> 4;
-    const unsigned hm = 0xFFFFu << (16 * h);
+    const unsigned hm = 0xFFFFu << (threadIdx.x & 16);   // this half-warp's lanes
     EdgeStage& sm = s_all[threadIdx.x >> 5];
     int2* list = s_list[hw];
     if (lane == 0) sm.ne = 0;
@@ -922,7 +922,7 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
     const int D = d.ctl->D;                      // loose-cell drift: every cell box widened by D
     const uint32_t ep = d.ctl->epoch & kTagMask;
     const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
-    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const uint32_t Rc = min((uint32_t)(d.r_p + d.v), kRClamp);   // r_p, v <= kRClamp (am_init)
     int ox_l, oy_l;
     morton_child(l, ox_l, oy_l);
     HwStats hs;
@@ -1159,8 +1159,8 @@ __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict
     const int nr = count ? *count : d.ctl->n_ready;
     unsigned long long* dst = out ? out : d.digest;
     const uint32_t c = d.ctl->cur;
-    const int lane = threadIdx.x & 31, l = lane & 15, h = lane >> 4;
-    const unsigned hm = 0xFFFFu << (16 * h);
+    const int lane = threadIdx.x & 31, l = lane & 15;
+    const unsigned hm = 0xFFFFu << (threadIdx.x & 16);   // this half-warp's lanes
     const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
     const uint32_t Rp = (uint32_t)d.r_p, Rp2 = Rp * Rp;
     const int D = d.ctl->D;   // loose cells (widened boxes)
@@ -1527,7 +1527,7 @@ __global__ void __launch_bounds__(1024) k_small(Dev d, uint8_t* __restrict__ mas
         par[t] = (uint32_t)t;
     }
     __syncthreads();
-    const uint32_t Rc = (uint32_t)min((long long)d.r_p + d.v, (long long)kRClamp);
+    const uint32_t Rc = min((uint32_t)(d.r_p + d.v), kRClamp);   // r_p, v <= kRClamp (am_init)
     bool blocked = false;
     unsigned long long dig = 0;
     if (t < m && sst[t] != ST_DONE) {
