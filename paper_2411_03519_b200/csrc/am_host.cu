@@ -20,6 +20,8 @@ __global__ void k_finalize(Dev d);
 __global__ void k_union(Dev d);
 __global__ void k_scan_hw(Dev d);
 __global__ void k_scan_hw_full(Dev d);
+__global__ void k_scan_hw_st(Dev d);
+__global__ void k_scan_hw_full_st(Dev d);
 __global__ void k_ready(Dev d, uint8_t* mask);
 __global__ void k_sort_hist(Dev d, int max_passes);
 __global__ void k_sort_pass(Dev d, int pass, int32_t* order, int ntiles);
@@ -680,10 +682,11 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
                 CK(c, cudaStreamIsCapturing(s, &cs));
                 const bool full = (c->full_hint || !(d.flags & AM_VALIDATE)) && cs == cudaStreamCaptureStatusNone;
                 const unsigned g = std::min(blocks(d.n, 16), (unsigned)(full ? c->scan_blocks_full : c->scan_blocks));
+                const bool st = (d.flags & AM_STATS) != 0;   // the instantiation with work counters
                 if (full)
-                    LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw_full, g, 256, 0, d)));
+                    LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, st ? k_scan_hw_full_st : k_scan_hw_full, g, 256, 0, d)));
                 else
-                    LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, k_scan_hw, g, 256, 0, d)));
+                    LAUNCH(K_SCAN, CK(c, launch_k(c->pdl, s, st ? k_scan_hw_st : k_scan_hw, g, 256, 0, d)));
                 c->full_hint = false;
             }
             CK(c, cudaStreamWaitEvent(s, c->ev_efil, 0));

@@ -44,10 +44,10 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #define AM_DIRECT 64        // direct query box (cells) of the incremental scan
 #endif
 #ifndef AM_SCAN_MINB
-#define AM_SCAN_MINB 5      // k_scan_hw: 5 resident CTAs per SM (<= 51 registers; A/B: -6% round time)
+#define AM_SCAN_MINB 4      // k_scan_hw: 4 resident CTAs per SM (64 registers; A/B after the stats registers left: 4 / 5 / 6 CTAs 130.7 / 131.1 / 135.9 us)
 #endif
 #ifndef AM_SCAN_MINB_FULL
-#define AM_SCAN_MINB_FULL AM_SCAN_MINB
+#define AM_SCAN_MINB_FULL 5   // k_scan_hw_full (full-recompute rounds)
 #endif
 #ifndef AM_SCAN_FULL_REC
 #define AM_SCAN_FULL_REC 1   // full rounds take their agents from the cell-sorted records

@@ -681,13 +681,26 @@ __device__ __forceinline__ void morton_child(int k, int& dx, int& dy)
 }
 
 // Work counters of the half-warp scan (AM_STATS and the far-item count).
-struct HwStats {
+// A counter compiled out (the scan without AM_STATS): adding does nothing, reads give 0,
+// so the statistics cost no registers in the kernel that runs every round.
+struct StatSink {
+    __device__ __forceinline__ StatSink& operator+=(uint32_t) { return *this; }
+    __device__ __forceinline__ operator uint32_t() const { return 0u; }
+};
+template <bool kOn>
+struct HwStatsT {
     uint32_t ncells = 0, ncand = 0, nb2 = 0, nb1 = 0, nitems = 0, nblk = 0;
+};
+template <>
+struct HwStatsT<false> {
+    StatSink ncells, ncand, nb2, nb1, nblk;
+    uint32_t nitems = 0;   // the far-item count is always kept (n_items)
 };
 
 // per-warp reduction of the half-warp scan counters, one atomic per warp (no block
 // barrier: a warp that is done leaves at once)
-__device__ __forceinline__ void hw_flush_stats(const Dev& d, const HwStats& hs, int lane)
+template <class HS>
+__device__ __forceinline__ void hw_flush_stats(const Dev& d, const HS& hs, int lane)
 {
     const unsigned it = __reduce_add_sync(0xFFFFFFFFu, hs.nitems);
     if (lane == 0 && it) atomicAdd(&d.ctl->n_items, (int)it);
@@ -717,17 +730,20 @@ __device__ __forceinline__ void hw_flush_stats(const Dev& d, const HwStats& hs, 
 // nothing inside can block A); cells within R_c of A are tested by the near phase.  The
 // records of the surviving cells are flattened over the lanes and tested 16 at a time.
 // Returns a blocker's id or kSentinel.
+template <class HS>
 __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as, int W, int D, int l, int h,
-                                           unsigned hm, int ox_l, int oy_l, HwStats& hs)
+                                           unsigned hm, HS& hs)
 {
+    int ox_l, oy_l;   // lane l's Morton child offsets in a 4x4 block
+    morton_child(l, ox_l, oy_l);
     const int cl = d.clog, l1 = cl + 2, l2 = cl + 4, G2x = (1 << d.gxlog) >> 4, G2y = (1 << d.gylog) >> 4;
     const uint32_t Rc = min((uint32_t)(d.r_p + d.v), kRClamp);   // r_p, v <= kRClamp (am_init)
     const int lagcap = d.lagcap;   // host-computed kRClamp / v + 1
-    uint32_t& ncells = hs.ncells;
-    uint32_t& ncand = hs.ncand;
-    uint32_t& nb2 = hs.nb2;
-    uint32_t& nb1 = hs.nb1;
-    uint32_t& nitems = hs.nitems;
+    auto& ncells = hs.ncells;
+    auto& ncand = hs.ncand;
+    auto& nb2 = hs.nb2;
+    auto& nb1 = hs.nb1;
+    auto& nitems = hs.nitems;
     const int R = (int)rb32(as - W, d.lagcap, d.v, d.r_p);
     const int bx0 = max(0, (ax - R - D) >> l2), bx1 = min(G2x - 1, (ax + R + D) >> l2);
     const int by0 = max(0, (ay - R - D) >> l2), by1 = min(G2y - 1, (ay + R + D) >> l2);
@@ -834,9 +850,10 @@ constexpr int kDirectFull = AM_DIRECT_FULL; // the same for rounds the host know
 // A; returns (in nblk/wit) the first blocker; stages coupling edges for a changed A
 // (list[0, nn) near cells; the far cells follow at list[fgap + nn, fgap + nl): fgap = 0
 // when they were appended, the gap to the end of the buffer when they fill it backwards)
+template <class HS>
 __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const int2* list, int nl, int nn, int fgap,
                                            int ax, int ay, int as, uint32_t aid, bool chg, bool idle, uint32_t ep,
-                                           int l, int h, unsigned hm, bool& nblk, uint32_t& wit, HwStats& hs)
+                                           int l, int h, unsigned hm, bool& nblk, uint32_t& wit, HS& hs)
 {
     const uint32_t Rc = min((uint32_t)(d.r_p + d.v), kRClamp);   // r_p, v <= kRClamp (am_init)
     const uint32_t Rc2 = Rc * Rc;
@@ -903,7 +920,7 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
 // kRec (full-recompute rounds, where the queue holds every binned agent): the agents are
 // taken from the cell-sorted records instead of the id-ordered queue, so neighbouring
 // half-warps scan neighbouring cells (cell-table and record reads shared in L1/L2)
-template <int KD, bool kRec>
+template <int KD, bool kRec, bool kStats>
 __device__ __forceinline__ void scan_hw(const Dev& d)
 {
     pdl_begin();
@@ -923,9 +940,7 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
     const uint32_t ep = d.ctl->epoch & kTagMask;
     const int cl = d.clog, Gx = 1 << d.gxlog, Gy = 1 << d.gylog;
     const uint32_t Rc = min((uint32_t)(d.r_p + d.v), kRClamp);   // r_p, v <= kRClamp (am_init)
-    int ox_l, oy_l;
-    morton_child(l, ox_l, oy_l);
-    HwStats hs;
+    HwStatsT<kStats> hs;
     uint32_t nfar = 0;
 #if AM_SCAN_DYN
     // dynamic distribution: each warp takes the next two queue entries (one per half-warp)
@@ -1062,7 +1077,7 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
             }
             if (idle) {
                 if (far && !direct && !nblk) {
-                    wit = hw_far(d, ax, ay, as, W, D, l, h, hm, ox_l, oy_l, hs);
+                    wit = hw_far(d, ax, ay, as, W, D, l, h, hm, hs);
                     nblk = wit != kSentinel;
                 }
                 hs.nblk += (l == 0 && nblk) ? 1u : 0u;
@@ -1079,8 +1094,12 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
     hw_flush_stats(d, hs, lane);
 }
 // the incremental rounds' scan and the full-recompute rounds' scan (host-selected)
-__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d) { scan_hw<kDirect, false>(d); }
-__global__ void __launch_bounds__(256, AM_SCAN_MINB_FULL) k_scan_hw_full(Dev d) { scan_hw<kDirectFull, AM_SCAN_FULL_REC != 0>(d); }
+// (the _st instantiations keep the AM_STATS work counters; the host picks them when the
+// flag is set)
+__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw(Dev d) { scan_hw<kDirect, false, false>(d); }
+__global__ void __launch_bounds__(256, AM_SCAN_MINB_FULL) k_scan_hw_full(Dev d) { scan_hw<kDirectFull, AM_SCAN_FULL_REC != 0, false>(d); }
+__global__ void __launch_bounds__(256, AM_SCAN_MINB) k_scan_hw_st(Dev d) { scan_hw<kDirect, false, true>(d); }
+__global__ void __launch_bounds__(256, AM_SCAN_MINB_FULL) k_scan_hw_full_st(Dev d) { scan_hw<kDirectFull, AM_SCAN_FULL_REC != 0, true>(d); }
 
 // k_union: unite this round's coupling edges (carried-over + new), one thread per edge
 // (ECL-CC style hooking of the larger root under the smaller, so roots stay the
