@@ -297,6 +297,15 @@ def config(name: str, steps: int | None = None, n: int | None = None) -> Workloa
         side = max(64, int(round(side * (N / full) ** 0.5)))
         x, y = hotspot_positions(N, side, side, seed=2)
         return Workload(name, side, side, None, x, y, 1, steps or 1000, profile="busy", Q=50_000)
+    if name == "C5T":
+        # C5's density and recipe on a TALL map (width 16384, height 16384 * N / 1M): the
+        # slab-distributed replay beyond one tracker's 32768 rows (weak scaling, one 1M-agent
+        # 16384^2 slab per rank at N = G * 1M; each window keeps its own 16-bit row frame)
+        N = n or 2_000_000
+        w_ = 16384
+        h_ = max(64, int(round(16384 * N / 1_000_000)))
+        x, y = hotspot_positions(N, w_, h_, seed=2)
+        return Workload(name, w_, h_, None, x, y, 1, steps or 1000, profile="busy", Q=50_000)
     raise KeyError(name)
 
 

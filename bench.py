@@ -430,6 +430,45 @@ def virtual_slabs(w, lm, dev, slab_counts=((2, 1), (8, 1), (8, 4)), preroll=200,
     return out
 
 
+def virtual_slabs_tall(lm, dev, slab_counts=(4, 16), preroll=200, timed=8):
+    """Weak scaling on virtual slabs: C5's density and recipe on a tall map of G x 1M
+    agents (16384 wide, G x 16384 rows: beyond one tracker's 32768 rows from G = 2, so
+    only the slab decomposition holds it), one 1M-agent 16384^2 slab per rank.  Per rank:
+    its own device time of a round (as in virtual_slabs); aggregate: the agent-steps all
+    ranks dispatch per round over the slowest rank's round time -- what G GPUs would
+    resolve per second, before the cost of the three collectives."""
+    import amgen
+    from paper_2411_03519_b200 import slabs
+    out = {}
+    for G in slab_counts:
+        w = amgen.config("C5T", n=G * 1_000_000)
+        sy = slabs.Synth(lm, device=dev)
+        wd = slabs.LoopbackWorld(w.map_w, w.map_h, w.r_p, w.v, w.x, w.y, w.steps, sy, w.Q, G, device=dev,
+                                 check_rounds=16)
+        done = 0
+        while done < preroll:
+            k = min(wd.K, preroll - done)
+            for _ in range(k):
+                wd.round()
+            done += k
+            wd.check()
+        d0 = wd.dispatched()
+        tl = []
+        for _ in range(timed):
+            wd.round(timing=tl)
+        wd.check()
+        per_round = (wd.dispatched() - d0) / timed
+        med = [sorted(r[k] for r in tl)[len(tl) // 2] for k in range(G)]
+        t = max(med)
+        out[f"G={G}"] = {"agents": len(w.x), "map": [w.map_w, w.map_h], "rank_round_ms_max_over_ranks": t,
+                         "rank_round_ms_mean": sum(med) / G, "agent_steps_per_round": per_round,
+                         "agent_steps_per_s_if_one_gpu_per_slab": per_round / (t / 1000.0),
+                         "halo_rows": wd.halo, "rewindows": wd.rewindows, "rounds": preroll + timed}
+        wd.close()
+        del w
+    return out
+
+
 # ------------------------------------------------------------------ N > 1: spatial slabs
 def run_slabs(args, w, lm):
     """N GPUs (torchrun, one process per GPU, NCCL over NVLink): the ONE C5 map split into
@@ -705,6 +744,7 @@ def run_ours(args, w, lm):
 
     snap = snapshot_rounds(rep, w, dev, flush) if not args.no_snapshot else None
     vslab = virtual_slabs(w, lm, dev) if (not args.no_snapshot and ws == 1) else None
+    vtall = virtual_slabs_tall(lm, dev) if (not args.no_snapshot and ws == 1 and w.name == "C5") else None
 
     if rank != 0:
         rep.close()
@@ -802,6 +842,7 @@ def run_ours(args, w, lm):
         "issue_roofline": issue,
         "snapshot": snap,
         "virtual_slabs": vslab,
+        "virtual_slabs_weak": vtall,
         "kernel_share_warmup_us": {k: round(v * 1000.0, 2) for k, v in sorted(shares.items())},
         # D2H (am_replay_io, page-locked host arrays, state outputs aliasing the inputs):
         # position + step of every aligned 8-agent group holding a committed agent (96 B

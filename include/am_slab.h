@@ -82,7 +82,10 @@ extern "C" {
 #endif
 
 typedef struct {
-    int32_t map_w, map_h;     /* map (tiles)                                                 */
+    int32_t map_w, map_h;     /* map (tiles): map_w <= 32768, map_h <= 2^30 -- the map may be
+                                 taller than one tracker's 32768 rows as long as every window
+                                 (slab rows + 2 halo) fits in 32768 rows (its own frame,
+                                 y - y0); am_slab_create returns AM_E_ARG otherwise          */
     int32_t r_p, v_max;       /* radius_p, max_vel                                   */
     int32_t metric;           /* AM_METRIC_L2 / AM_METRIC_LINF                               */
     int32_t n_slabs;          /* G >= 1                                                      */
@@ -153,6 +156,21 @@ int am_slab_merge(am_slab* s, const int32_t* mbufs, int32_t* order_out, int32_t*
  * dispatch of the owned agents whose local cluster holds no ghost and no owned RUNNING
  * or blocked member; outputs as am_slab_merge. */
 int am_slab_round_stale(am_slab* s, int32_t* order_out, int32_t* n_order, int64_t* stats);
+
+/* order_out of am_slab_merge / am_slab_round_stale is written by the rank's priority sort
+ * on a library side stream, beside commit, exchange and apply (none of them reads it),
+ * after the merge forest's restore (which reads mbufs: the caller leaves mbufs untouched
+ * until the join); n_order and everything else are ordered on the slab's stream as
+ * usual.  The slab's stream waits for the side work (an event wait, no host
+ * synchronisation) at the start of the next am_slab_round_local / am_slab_round_stale /
+ * am_slab_load, or at am_slab_wait_order -- call it before reading order_out on the
+ * slab's stream. */
+int am_slab_wait_order(am_slab* s);
+
+/* Device time of the last side-stream work (forest restore + priority sort) in ms
+ * (timing events around it; blocks the host until it is done).  AM_E_STATE before the
+ * first round. */
+int am_slab_order_ms(am_slab* s, float* ms);
 
 /* Step 3: commit at the global next event (stats_global: the all-reduced MIN of the
  * ranks' stats).  dsend non-NULL (an exchange follows): pack the delta records of every

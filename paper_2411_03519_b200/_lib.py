@@ -110,6 +110,8 @@ SIGNATURES = {
     "am_slab_round_local": (C.c_int, [_vp, _vp]),
     "am_slab_merge": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "am_slab_round_stale": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "am_slab_wait_order": (C.c_int, [_vp]),
+    "am_slab_order_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "am_slab_owned": (C.c_int, [_vp, _vp]),
     "am_slab_commit": (C.c_int, [_vp, _vp, _vp]),
     "am_slab_apply": (C.c_int, [_vp, _vp]),

@@ -242,6 +242,17 @@ __device__ __forceinline__ int4 mcluster(const SlabDev& s, const int32_t* mb, in
     return reinterpret_cast<const int4*>(mb + 4 + 2 * (size_t)s.g.cap_merge)[j];
 }
 
+// neutral values of this round's stats and of the order sort's counters (one thread)
+__device__ __forceinline__ void stats_reset(const SlabDev& s, long long* stats)
+{
+    stats[0] = kNever;   // next event
+    stats[1] = kNever;   // W
+    stats[2] = kNever;   // -S
+    stats[3] = 1;        // no agent active
+    s.sctl->n_ready = 0;
+    s.sctl->sort_or = 0;
+}
+
 // merge kernels: blockIdx.y = the rank whose records a block walks, up to their count
 __global__ void k_sl_unite(SlabDev s, const int32_t* __restrict__ mbufs)
 {
@@ -257,9 +268,10 @@ __global__ void k_sl_unite(SlabDev s, const int32_t* __restrict__ mbufs)
     }
 }
 
-__global__ void k_sl_cbad(SlabDev s, const int32_t* __restrict__ mbufs)
+__global__ void k_sl_cbad(SlabDev s, const int32_t* __restrict__ mbufs, long long* stats)
 {
     pdl_begin();
+    if (stats && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) stats_reset(s, stats);   // for k_sl_final
     const int r = blockIdx.y;
     const int32_t* mb = mbuf_of(s, mbufs, r);
     const int nc = min(mb[1], s.g.cap_merge);
@@ -275,14 +287,7 @@ __global__ void k_sl_cbad(SlabDev s, const int32_t* __restrict__ mbufs)
 __global__ void k_sl_stats_init(SlabDev s, long long* stats)
 {
     pdl_begin();
-    if (threadIdx.x == 0) {
-        stats[0] = kNever;   // next event
-        stats[1] = kNever;   // W
-        stats[2] = kNever;   // -S
-        stats[3] = 1;        // no agent active
-        s.sctl->n_ready = 0;
-        s.sctl->sort_or = 0;
-    }
+    if (threadIdx.x == 0) stats_reset(s, stats);
 }
 
 // final outputs of the owned agents: global label, ready bit, dispatch (status, completion
@@ -397,10 +402,11 @@ __global__ void k_sl_restore(SlabDev s, const int32_t* __restrict__ mbufs)
 
 // moves of the dispatched agents from their perception digests (Alg. 2 "perceive"; all
 // perceived agents are in the window)
-__global__ void k_sl_moves(SlabDev s)
+__global__ void k_sl_moves(SlabDev s, int32_t* n_order)
 {
     pdl_begin();
     const int nr = s.sctl->n_ready;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_order = nr;   // the order's length
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nr; k += gridDim.x * blockDim.x) {
         const int i = s.rlist[k];
         s.np[i] = policy_move_g(s.sy, s.g.map_w, s.g.map_h, s.gid[i], s.step[i], s.pos[i], s.dig[i]);
@@ -422,38 +428,39 @@ __device__ __forceinline__ const int32_t* dblock(const SlabDev& s, const int32_t
 
 // (after a stale round nothing may be pending: the clock stays, the rounds up to the next
 // sync round may be idle; only a sync round with nothing pending is a liveness failure)
-__global__ void k_sl_clock(SlabDev s, const long long* __restrict__ gstats, int32_t* dsend, int stale)
-{
-    pdl_begin();
-    if (dsend)
-        for (int r = threadIdx.x; r < s.g.n_slabs; r += blockDim.x)
-            for (int q = 0; q < 6; q++) dblock(s, dsend, r)[q] = 0;   // counts (headers)
-    if (threadIdx.x != 0) return;
-    const long long tn = gstats[0];
-    const bool active = gstats[3] == 0;
-    if (active) {
-        s.counters[3] += 1;
-        if (tn == kNever) {
-            if (!stale) atomicOr(s.flags, AM_SLAB_LIVENESS);
-        } else {
-            s.counters[0] = s.Q > 0 ? ((tn + s.Q - 1) / s.Q) * s.Q : tn;
-        }
-        // the owned agents drift up to P v outside the slab between exchanges, and the
-        // ghosts' snapshot is up to P rounds old: 2 P v more rows
-        const long long spread = -gstats[2] - gstats[1] + 1;
-        const long long need = (spread + 1) * s.g.v_max + s.g.r_p + (long long)(s.g.check_rounds + 1) * s.g.v_max +
-                               (s.P > 1 ? 2LL * s.P * s.g.v_max : 0LL);
-        if (need > s.g.halo) atomicOr(s.flags, AM_SLAB_HALO);
-    }
-}
-
 // owned RUNNING agents whose cluster completed commit their move (worker l.20-21,
 // controller l.11-12); they stay owned (IDLE, or DONE at the target) until the next
 // exchange, which sends them to every rank whose window they were or are in
-__global__ void k_sl_commit(SlabDev s)
+// The common clock first (every block computes it from the all-reduced stats; block 0
+// records it with the round count, liveness and the halo check): the global next event
+// rounded up to the quantum.
+__global__ void k_sl_commit(SlabDev s, const long long* __restrict__ gstats, int32_t* dsend, int stale)
 {
     pdl_begin();
-    const long long t = s.counters[0];
+    const long long tn = gstats[0];
+    const bool active = gstats[3] == 0;
+    long long t = s.counters[0];
+    if (active && tn != kNever) t = s.Q > 0 ? ((tn + s.Q - 1) / s.Q) * s.Q : tn;
+    if (blockIdx.x == 0) {
+        if (dsend)
+            for (int r = threadIdx.x; r < s.g.n_slabs; r += blockDim.x)
+                for (int q = 0; q < 6; q++) dblock(s, dsend, r)[q] = 0;   // counts (headers)
+        if (threadIdx.x == 0 && active) {
+            s.counters[3] += 1;
+            if (tn == kNever) {
+                if (!stale) atomicOr(s.flags, AM_SLAB_LIVENESS);
+            } else {
+                s.counters[0] = t;
+            }
+            // the owned agents drift up to P v outside the slab between exchanges, and the
+            // ghosts' snapshot is up to P rounds old: 2 P v more rows
+            const long long spread = -gstats[2] - gstats[1] + 1;
+            const long long need = (spread + 1) * s.g.v_max + s.g.r_p +
+                                   (long long)(s.g.check_rounds + 1) * s.g.v_max +
+                                   (s.P > 1 ? 2LL * s.P * s.g.v_max : 0LL);
+            if (need > s.g.halo) atomicOr(s.flags, AM_SLAB_HALO);
+        }
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.L; i += gridDim.x * blockDim.x) {
         if (s.stat[i] != ST_RUNNING || !s.own[i] || s.tc[i] > t) continue;   // ghosts are committed by their owner
         const int2 np = s.np[i];
@@ -593,7 +600,21 @@ struct am_slab {
     int32_t* order = nullptr;
     int num_sms = 148;
     bool last_stale = false;      // the last round was a stale round
+    // the rank's priority sort runs on a side stream beside commit / exchange / apply;
+    // the slab's stream joins it before the next round rewrites its inputs
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+    bool order_pending = false, order_timed = false;
 };
+
+// the slab's stream waits for the last priority sort (an event wait, no host sync)
+static void slab_join(am_slab* sl)
+{
+    if (sl && sl->order_pending) {
+        cudaStreamWaitEvent(sl->stream, sl->ev_s1, 0);
+        sl->order_pending = false;
+    }
+}
 
 namespace {
 struct SlabLayout {
@@ -609,8 +630,9 @@ int window_rows(const am_slab_geom& g, int& lo, int& hi, int& y0, int& y1)
     lo = (int)((long long)g.my_slab * g.map_h / g.n_slabs);
     hi = (int)((long long)(g.my_slab + 1) * g.map_h / g.n_slabs);
     y0 = std::max(0, lo - g.halo);
-    y1 = std::min(g.map_h, hi + g.halo);
-    return y1 > y0 ? AM_OK : AM_E_ARG;
+    y1 = (int)std::min<long long>(g.map_h, (long long)hi + g.halo);
+    // the window's tracker packs window rows in 16 bits (one tracker map <= 32768 rows)
+    return y1 > y0 && y1 - y0 <= 32768 ? AM_OK : AM_E_ARG;
 }
 
 am_config tracker_cfg(const am_slab_geom& g)
@@ -630,7 +652,7 @@ bool geom_ok(const am_slab_geom* g)
     return g && g->n_slabs >= 1 && g->my_slab >= 0 && g->my_slab < g->n_slabs && g->n_total > 0 &&
            g->n_total < (1 << 28) && g->target_step > 0 && g->halo >= g->r_p + 2 * g->v_max && g->cap_window > 0 &&
            g->cap_peer > 0 && g->cap_merge > 0 && (g->cap_merge % 2) == 0 && g->map_w >= 1 && g->map_h >= 1 && g->map_w <= 32768 &&
-           g->map_h <= 32768 && g->check_rounds >= 1 && g->n_slabs <= 1024 && g->stale_rounds >= 0 &&
+           g->map_h <= (1 << 30) &&   // each window's height is checked by its tracker (<= 32768) g->check_rounds >= 1 && g->n_slabs <= 1024 && g->stale_rounds >= 0 &&
            g->halo >= g->r_p + (std::max(1, g->stale_rounds) + 1) * g->v_max;
 }
 
@@ -762,6 +784,10 @@ extern "C" int am_slab_create(am_slab** out, const am_slab_geom* g, const am_syn
     if (!rc) rc = ck(sl, cudaMemsetAsync(b + Ly.gid, 0, Ly.total - Ly.gid, st), "memset");
     if (!rc) rc = ck(sl, cudaMemsetAsync(s.map, 0xFF, 4 * (size_t)g->n_total, st), "memset map");
     if (!rc) rc = ck(sl, cudaMallocHost((void**)&sl->h_flags, 16), "cudaMallocHost");
+    if (!rc) rc = ck(sl, cudaStreamCreateWithFlags(&sl->side, cudaStreamNonBlocking), "side stream");
+    if (!rc) rc = ck(sl, cudaEventCreateWithFlags(&sl->ev_fork, cudaEventDisableTiming), "event");
+    if (!rc) rc = ck(sl, cudaEventCreate(&sl->ev_s0), "event");
+    if (!rc) rc = ck(sl, cudaEventCreate(&sl->ev_s1), "event");
     if (rc) { am_slab_destroy(sl); return rc; }
     // forest = identity: a tiny kernel-free init through the sort's control block is not
     // available, so fill from the host once (n_total words)
@@ -782,6 +808,7 @@ extern "C" int am_slab_load(am_slab* sl, int32_t m, const int32_t* gid, const in
                             int64_t t)
 {
     if (!sl || m < 0 || m > sl->s.L || (m && (!gid || !pos || !steps || !status))) return AM_E_ARG;
+    slab_join(sl);
     SK(cudaMemsetAsync(sl->s.map, 0xFF, 4 * (size_t)sl->s.g.n_total, sl->stream));
     SK(launch_k(false, sl->stream, k_sl_load, grid_for(sl, sl->s.L), 256, 0, sl->s, m, gid, (const int2*)pos, steps, status,
                                                              (const unsigned long long*)traj, (const long long*)tcommit,
@@ -794,6 +821,7 @@ extern "C" int am_slab_load(am_slab* sl, int32_t m, const int32_t* gid, const in
 extern "C" int am_slab_round_local(am_slab* sl, int32_t* mbuf)
 {
     if (!sl || !mbuf) return AM_E_ARG;
+    slab_join(sl);   // the last round's priority sort read the buffers this round rewrites
     SlabDev& s = sl->s;
     const unsigned gr = grid_for(sl, s.L);
     SK(launch_k(sl->tr->pdl, sl->stream, k_sl_prep, gr, 256, 0, s, mbuf));
@@ -816,6 +844,7 @@ static int slab_finish(am_slab* sl, const int32_t* mbufs, int32_t* order_out, in
 extern "C" int am_slab_round_stale(am_slab* sl, int32_t* order_out, int32_t* n_order, int64_t* stats)
 {
     if (!sl || !order_out || !n_order || !stats) return AM_E_ARG;
+    slab_join(sl);   // the last round's priority sort read the buffers this round rewrites
     SlabDev& s = sl->s;
     const unsigned gr = grid_for(sl, s.L);
     SK(launch_k(sl->tr->pdl, sl->stream, k_sl_prep, gr, 256, 0, s, nullptr));
@@ -830,11 +859,6 @@ extern "C" int am_slab_round_stale(am_slab* sl, int32_t* order_out, int32_t* n_o
     return slab_finish(sl, nullptr, order_out, n_order, stats);
 }
 
-__global__ void k_sl_norder(const Ctl* c, int32_t* n)
-{
-    pdl_begin();
-    *n = c->n_ready;
-}
 
 extern "C" int am_slab_merge(am_slab* sl, const int32_t* mbufs, int32_t* order_out, int32_t* n_order, int64_t* stats)
 {
@@ -852,28 +876,54 @@ static int slab_finish(am_slab* sl, const int32_t* mbufs, int32_t* order_out, in
     const unsigned gr = grid_for(sl, s.L);
     if (mbufs) {
         SK(launch_k(sl->tr->pdl, sl->stream, k_sl_unite, gm, 256, 0, s, mbufs));
-        SK(launch_k(sl->tr->pdl, sl->stream, k_sl_cbad, gm, 256, 0, s, mbufs));
+        SK(launch_k(sl->tr->pdl, sl->stream, k_sl_cbad, gm, 256, 0, s, mbufs, (long long*)stats));
+    } else {
+        SK(launch_k(sl->tr->pdl, sl->stream, k_sl_stats_init, 1, 32, 0, s, (long long*)stats));
     }
-    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_stats_init, 1, 32, 0, s, (long long*)stats));
     SK(launch_k(sl->tr->pdl, sl->stream, k_sl_final, gr, 256, 0, s, (long long*)stats));
-    if (mbufs) SK(launch_k(sl->tr->pdl, sl->stream, k_sl_restore, gm, 256, 0, s, mbufs));
-    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_norder, 1, 1, 0, s.sctl, n_order));
     SK(cudaGetLastError());
     // perception digests of the dispatched agents (global ids in the terms), their moves
     int rc = am_internal_digest(sl->tr, s.rlist, &s.sctl->n_ready, s.gid, s.dig, s.L, sl->stream);
     if (rc) return rc;
-    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_moves, gr, 256, 0, s));
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_moves, gr, 256, 0, s, n_order));
     SK(cudaGetLastError());
-    // the rank's priority order: unique keys (lag, global label, id) -> global ids
-    return am_internal_csort(sl->tr, sl->sd, order_out, sl->stream);
+    // on the side stream (nothing in commit / apply reads them; the next round joins it
+    // first): the merge forest's restore (reads mbufs: they stay untouched until then)
+    // and the rank's priority order -- unique keys (lag, global label, id) -> global ids
+    SK(cudaEventRecord(sl->ev_fork, sl->stream));
+    SK(cudaStreamWaitEvent(sl->side, sl->ev_fork, 0));
+    SK(cudaEventRecord(sl->ev_s0, sl->side));
+    if (mbufs) SK(launch_k(false, sl->side, k_sl_restore, gm, 256, 0, s, mbufs));
+    rc = am_internal_csort(sl->tr, sl->sd, order_out, sl->side);
+    if (rc) return rc;
+    SK(cudaEventRecord(sl->ev_s1, sl->side));
+    sl->order_pending = true;
+    sl->order_timed = true;
+    return AM_OK;
+}
+
+extern "C" int am_slab_wait_order(am_slab* sl)
+{
+    if (!sl) return AM_E_ARG;
+    slab_join(sl);
+    return AM_OK;
+}
+
+extern "C" int am_slab_order_ms(am_slab* sl, float* ms)
+{
+    if (!sl || !ms) return AM_E_ARG;
+    if (!sl->order_timed) return AM_E_STATE;
+    SK(cudaEventSynchronize(sl->ev_s1));
+    SK(cudaEventElapsedTime(ms, sl->ev_s0, sl->ev_s1));
+    return AM_OK;
 }
 
 extern "C" int am_slab_commit(am_slab* sl, const int64_t* stats_global, int32_t* dsend)
 {
     if (!sl || !stats_global) return AM_E_ARG;
     SlabDev& s = sl->s;
-    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_clock, 1, 256, 0, s, (const long long*)stats_global, dsend, sl->last_stale ? 1 : 0));
-    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_commit, grid_for(sl, s.L), 256, 0, s));
+    SK(launch_k(sl->tr->pdl, sl->stream, k_sl_commit, grid_for(sl, s.L), 256, 0, s, (const long long*)stats_global,
+                dsend, sl->last_stale ? 1 : 0));
     if (dsend) SK(launch_k(sl->tr->pdl, sl->stream, k_sl_flush, grid_for(sl, s.L), 256, 0, s, dsend));
     SK(cudaGetLastError());
     return AM_OK;
@@ -944,6 +994,13 @@ extern "C" int am_slab_destroy(am_slab* sl)
 {
     if (!sl) return AM_OK;
     if (sl->stream) cudaStreamSynchronize(sl->stream);
+    if (sl->side) {
+        cudaStreamSynchronize(sl->side);
+        cudaStreamDestroy(sl->side);
+    }
+    if (sl->ev_fork) cudaEventDestroy(sl->ev_fork);
+    if (sl->ev_s0) cudaEventDestroy(sl->ev_s0);
+    if (sl->ev_s1) cudaEventDestroy(sl->ev_s1);
     if (sl->tr) am_destroy(sl->tr);
     if (sl->h_flags) cudaFreeHost(sl->h_flags);
     if (sl->mem_owned) cudaFree(sl->mem);

@@ -159,6 +159,16 @@ class SlabRank:
     def apply(self, drecv: torch.Tensor):
         check(self.L.am_slab_apply(self.h, drecv.data_ptr()))
 
+    def wait_order(self):
+        """The slab's stream waits for the rank's priority sort (side stream)."""
+        check(self.L.am_slab_wait_order(self.h))
+
+    def order_ms(self) -> float:
+        """Device time of the last priority sort (ms; synchronises on it)."""
+        ms = C.c_float(0.0)
+        check(self.L.am_slab_order_ms(self.h, C.byref(ms)))
+        return float(ms.value)
+
     def flags(self):
         f, used = C.c_int32(0), C.c_int32(0)
         check(self.L.am_slab_flags(self.h, C.byref(f), C.byref(used)))
@@ -181,6 +191,7 @@ class SlabRank:
     def round_outputs(self):
         """This rank's ready agents (global ids in priority order) and, for every owned
         agent, (gid, global label, ready bit)."""
+        self.wait_order()
         n = int(self.n_order.item())
         m = self.owned_mask()
         return dict(order=self.order[:n].clone(), gid=self.w_gid[m].clone(), label=self.w_label[m].clone(),
@@ -298,7 +309,8 @@ class LoopbackWorld(_World):
         """One distributed round of all virtual slabs (no host synchronisation unless
         `log` asks for the round's outputs).  With `timing` (a list), the device time of
         every rank's own library steps (everything but the exchanges, which NCCL does in
-        a real run) is appended, per rank, in ms: what one GPU of a G-GPU run computes."""
+        a real run) is appended, per rank, in ms: what one GPU of a G-GPU run computes
+        (its side-stream restore + sort counted where they outlast commit + apply)."""
         sync, exchange = self._schedule()
         ev = [[] for _ in self.ranks]
 
@@ -337,7 +349,16 @@ class LoopbackWorld(_World):
         self._last_stats = sg
         if timing is not None:
             torch.cuda.synchronize(self.dev)
-            timing.append([sum(a.elapsed_time(b) for a, b in e) for e in ev])
+            # per rank: its phases on its stream, plus the part of its side-stream work
+            # (merge-forest restore + priority sort, started at the end of the merge /
+            # stale phase) that outlasts the phases after it (commit, apply) -- in a G-GPU
+            # run it also overlaps the all-reduce and the all-to-all, not counted here
+            tot = []
+            for k, r in enumerate(self.ranks):
+                ph = [a.elapsed_time(b) for a, b in ev[k]]
+                after = sum(ph[2:]) if sync else sum(ph[1:])
+                tot.append(sum(ph) + max(0.0, r.order_ms() - after))
+            timing.append(tot)
 
     def check(self) -> bool:
         """Reads every rank's flags (one synchronisation).  Raises on an overflow or a

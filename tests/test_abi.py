@@ -86,6 +86,22 @@ def test_workspace_size_two_phase_idiom(lib):
     assert lib.am_init(C.byref(h), 140, 100, 4, 1, 25, C.byref(cfg)) == _lib.E_WORKSPACE
 
 
+def test_slab_geometry_tall_maps(lib):
+    """am_slab_workspace_size (no CUDA call): a map taller than one tracker's 32768 rows is
+    accepted when every window (slab rows + 2 halo rows) fits 32768 rows -- each window
+    tracker works in its own row frame -- and refused (0) otherwise."""
+    def ws(H, G, k, halo=160):
+        g = _lib.SlabGeom(16384, H, 4, 1, _lib.METRIC_L2, G, k, 2_000_000, 1000, halo, 1_100_000, 20000, 40000,
+                          16, 1)
+        return lib.am_slab_workspace_size(C.byref(g))
+    assert ws(32768, 1, 0) > 0
+    assert ws(40000, 1, 0) == 0                       # one window of 40000 rows
+    assert ws(40000, 2, 0) > 0 and ws(40000, 2, 1) > 0
+    assert all(ws(262144, 16, k) > 0 for k in (0, 7, 15))
+    assert ws(262144, 8, 3) == 0                      # 32768 slab rows + 2 x 160 halo rows
+    assert ws(16384, 4, 0, halo=2) == 0               # halo < r_p + 2 v
+
+
 def test_package_does_not_import_the_oracle():
     src = ""
     pdir = os.path.dirname(pkg.__file__)

@@ -165,6 +165,30 @@ def test_slab_replay_c4_shape_final_state_vs_lockstep(G):
     wd.close()
 
 
+@pytest.mark.parametrize("G", [2, 4])
+def test_slab_replay_tall_map_final_state_vs_lockstep(G):
+    """A map taller than one tracker's 32768 rows (128 x 40000, 20k agents at C5 density in
+    hotspots, 60 steps): split into G slabs whose windows fit 32768 rows (each window keeps
+    its own row frame), the distributed replay ends in the oracle's lock-step state (P:27);
+    a single slab cannot hold the map."""
+    x, y = amgen.hotspot_positions(20000, 128, 40000, seed=3)
+    w = amgen.Workload("tall", 128, 40000, None, x, y, 1, 60, profile="busy", Q=50_000)
+    lm = amgen.latency_model(w.profile)
+    with pytest.raises(ValueError):
+        _world(w, lm, 1)
+    wd = _world(w, lm, G, check_rounds=8)
+    wd.run(10**6)
+    res = wd.results()
+    p = O.params(w.map_w, w.map_h, w.r_p, w.v, w.steps)
+    ls = O.lockstep_grid(p, O.SynthTables.from_model(lm), w.x, w.y, w.steps)
+    np.testing.assert_array_equal(res["x"], ls["x"])
+    np.testing.assert_array_equal(res["y"], ls["y"])
+    np.testing.assert_array_equal(res["traj"], ls["traj"])
+    assert np.all(res["steps"] == w.steps)
+    assert int(res["y"].max()) > 32767
+    wd.close()
+
+
 @pytest.mark.parametrize("name,steps,n,G,P", [
     ("C1", 300, None, 2, 2), ("C1", 300, None, 4, 4),
     ("C2", 8, None, 4, 2), ("C2", 8, None, 8, 4),

@@ -1,0 +1,15 @@
+#!/bin/bash
+# session 18: the slab clock folded into k_sl_commit, the stats reset into k_sl_cbad:
+# slab suites, bench, slab launch list
+cd "${GRAFT_REPO_ROOT:-$(pwd)}"
+mkdir -p gpurun_out
+export PYTHONPATH=$(pwd):$PYTHONPATH
+timeout 1500 python -m pytest tests/test_gpu_slabs.py tests/test_gpu_slabs_dist.py -q -x > gpurun_out/slab_tests.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/slab_tests.log
+tail -2 gpurun_out/slab_tests.log
+timeout 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+echo "bench rc=$?" >> gpurun_out/bench.err
+python -c "import json; d=json.load(open('gpurun_out/bench.json')); print(d['ms_per_step'], {k: v['rank_round_ms_max_over_ranks'] for k, v in d['virtual_slabs'].items()}, {k: v['rank_round_ms_max_over_ranks'] for k, v in d['virtual_slabs_weak'].items()})"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  --profile-from-start off --csv --log-file gpurun_out/launches_slabs_s18.csv python tools/profile_slabs.py --G 8 --preroll 200 --rounds 2 \
+  > gpurun_out/launches_slabs_s18.log 2>&1; echo "slab launch list rc=$?"
