@@ -311,7 +311,9 @@ int64_t orc_validity_violations(const orc_params* p, int32_t n, const int32_t* x
  * The paper replays recorded GenAgent traces; those are not available, so
  * actions come from a deterministic random-walk policy and per-step LLM latencies
  * from integer tables.  The paper is silent on all of
- * this: parity unpinned by the paper (pinned by D1..D5 closed forms only). */
+ * this, so SURVEY 8(c.4) defines it; pinned against that definition by independent
+ * pure-Python restatements and splitmix64's published outputs
+ * (tests/test_oracle_pins.py) and by the D1..D5 closed forms (tests/test_oracle.py). */
 
 /* splitmix64 finalizer (Steele/Lea/Flood 2014), with its golden-gamma increment. */
 uint64_t orc_mix64(uint64_t z)
