@@ -42,8 +42,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 def build_variant(name: str, defines: list[str]) -> str:
-    """Experiment builds (tools/ab_round.py): libametro_<name>.so with extra -D flags,
-    loaded when AM_LIB_VARIANT=<name> is set.  Never used by the product path."""
+    """Experiment builds (tools/ab_round.py) and the bounds-checked test build
+    (tests/test_gpu_bounds.py, -DAM_DEBUG_BOUNDS=1): libametro_<name>.so with extra -D
+    flags, loaded when AM_LIB_VARIANT=<name> is set.  Never used by the product path."""
     out = os.path.join(PKG, f"libametro_{name}.so")
     cmd = [NVCC, *FLAGS, *[f"-D{x}" for x in defines], "-o", out, *sources(), "-lcudart"]
     subprocess.check_call(cmd)

@@ -98,6 +98,7 @@ __device__ __forceinline__ int commit_agent(const RepDev& r, int i, int s0, int 
         const int lab = d.labels[i];
         if (lab >= 0) d.dirty[lab] = d.ctl->epoch + 1u;
         const uint32_t rr = d.slot[i];
+        AM_CHECK(rr == kSentinel || rr < (uint32_t)d.n);
         if (rr != kSentinel) {
             d.rec[rr] = make_int4(np.x | (np.y << 16), s, i, (int)nst | (int)(tag << kTagShift));
             int cx, cy;
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
             }
         }
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, commit);
+        AM_CHECK(!commit || (i < d.n && nlist + __popc(bal & ((1u << lane) - 1u)) < 32 * KC));
         if (commit) s_cl[w][nlist + __popc(bal & ((1u << lane) - 1u))] = make_int2(i, sw[k]);
         nlist += __popc(bal);
     }

@@ -34,6 +34,18 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #ifndef AM_COMMIT_ITEMS
 #define AM_COMMIT_ITEMS 8   // k_commit: agents per thread (commits compacted per warp)
 #endif
+// Bounds-checked experiment build (-DAM_DEBUG_BOUNDS=1, tools/ab_round.py build dbg=...):
+// device asserts on the index of every shared / global access the checks name; the GPU
+// suite runs against it with AM_LIB_VARIANT=dbg (compute-sanitizer is closed on the pool)
+#ifndef AM_DEBUG_BOUNDS
+#define AM_DEBUG_BOUNDS 0
+#endif
+#if AM_DEBUG_BOUNDS
+#include <cassert>
+#define AM_CHECK(c) assert(c)
+#else
+#define AM_CHECK(c) ((void)0)
+#endif
 #ifndef AM_SCAN_1PASS
 #define AM_SCAN_1PASS 1   // scan_hw: near and far cells classified in one pass
 #endif

@@ -361,7 +361,9 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
             if (rebuild) {
                 // slot: the cell's start + its count taken back down (returns the counts to 0)
                 const uint32_t key = d.key[i];
+                AM_CHECK(key < (uint32_t)d.ncells);
                 const uint32_t r = (uint32_t)d.ctab[key].x + (atomicSub(d.cnt + key, 1u) - 1u);
+                AM_CHECK(r < (uint32_t)d.n);
                 const uint32_t tag = chg ? ep : ((ep + 0x800000u) & kTagMask);   // never this epoch
                 d.rec[r] = make_int4(p.x | (p.y << 16), s, i, (int)st | (int)(tag << kTagShift));
                 d.slot[i] = r;
@@ -810,6 +812,7 @@ __device__ __forceinline__ uint32_t hw_far(const Dev& d, int ax, int ay, int as,
                     bool found = false;
                     uint32_t bid = 0;
                     if (tq < total) {
+                        AM_CHECK(rs + (tq - rx) >= 0 && rs + (tq - rx) < d.n);
                         const int4 B = d.rec[rs + (tq - rx)];
                         bid = (uint32_t)B.z;
                         if (B.y < as) {
@@ -864,6 +867,7 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
         const int k = c0 + l;
         int st0 = 0, cnt = 0;
         if (k < nl) {
+            AM_CHECK((k < nn ? k : k + fgap) >= 0 && (k < nn ? k : k + fgap) < (AM_DIRECT > AM_DIRECT_FULL ? AM_DIRECT : AM_DIRECT_FULL));
             const int2 e = list[k < nn ? k : k + fgap];
             st0 = e.x;
             cnt = e.y;
@@ -893,7 +897,8 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
             bool found = false;
             uint32_t bid = 0;
             if (tq < total) {
-                const int4 B = d.rec[rs + (tq - rx)];
+                AM_CHECK(rs + (tq - rx) >= 0 && rs + (tq - rx) < d.n);
+                        const int4 B = d.rec[rs + (tq - rx)];
                 bid = (uint32_t)B.z;
                 if (bid != aid) {
                     const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
@@ -920,6 +925,10 @@ __device__ __forceinline__ void hw_records(const Dev& d, EdgeStage& sm, const in
 // kRec (full-recompute rounds, where the queue holds every binned agent): the agents are
 // taken from the cell-sorted records instead of the id-ordered queue, so neighbouring
 // half-warps scan neighbouring cells (cell-table and record reads shared in L1/L2)
+// ceil(2^32 / n) for box widths n = 2..64 (0 for n <= 1): the scan's row of cell k of a
+// box is __umulhi(k, c_rcx[ncx]), without a per-agent division
+__constant__ uint32_t c_rcx[65] = {0u, 0u, 2147483648u, 1431655766u, 1073741824u, 858993460u, 715827883u, 613566757u, 536870912u, 477218589u, 429496730u, 390451573u, 357913942u, 330382100u, 306783379u, 286331154u, 268435456u, 252645136u, 238609295u, 226050911u, 214748365u, 204522253u, 195225787u, 186737709u, 178956971u, 171798692u, 165191050u, 159072863u, 153391690u, 148102321u, 143165577u, 138547333u, 134217728u, 130150525u, 126322568u, 122713352u, 119304648u, 116080198u, 113025456u, 110127367u, 107374183u, 104755300u, 102261127u, 99882961u, 97612894u, 95443718u, 93368855u, 91382283u, 89478486u, 87652394u, 85899346u, 84215046u, 82595525u, 81037119u, 79536432u, 78090315u, 76695845u, 75350304u, 74051161u, 72796056u, 71582789u, 70409300u, 69273667u, 68174085u, 67108864u};
+
 template <int KD, bool kRec, bool kStats>
 __device__ __forceinline__ void scan_hw(const Dev& d)
 {
@@ -983,7 +992,7 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
             const int ncx = cx1 - cx0 + 1, ncell = ncx * (cy1 - cy0 + 1);
             // row k / ncx of cell k of the box: a multiply-high by ceil(2^32 / ncx), exact
             // for k, ncx < 2^16 (a plain division for the rare larger boxes)
-            const uint32_t rcx = ncx > 1 ? 0xFFFFFFFFu / (uint32_t)ncx + 1u : 0u;
+            const uint32_t rcx = ncx <= 64 ? c_rcx[ncx] : 0xFFFFFFFFu / (uint32_t)ncx + 1u;
             const bool mulhi = ncx > 1 && ncell < 65536;
             auto krow = [&](int k) { return ncx == 1 ? k : (mulhi ? (int)__umulhi((uint32_t)k, rcx) : k / ncx); };
             bool nblk = false;
@@ -1003,6 +1012,7 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
                     if (j < ngrp && k < ncell) {
                         const int ky = krow(k), kx = k - ky * ncx;
                         const uint32_t key = mkey(d, cx0 + kx, cy0 + ky, 0);
+                        AM_CHECK(key < (uint32_t)d.ncells);
                         ent[j] = d.ctab[key];
                         nxt[j] = d.ctab[key + 1].x;
                     }
@@ -1031,6 +1041,8 @@ __device__ __forceinline__ void scan_hw(const Dev& d)
                         const unsigned bn = (__ballot_sync(hm, okn) >> (16 * h)) & 0xFFFFu;
                         const unsigned bf = (__ballot_sync(hm, okf) >> (16 * h)) & 0xFFFFu;
                         const unsigned lt = (1u << l) - 1u;
+                        AM_CHECK(!okn || nn + __popc(bn & lt) < KD);
+                        AM_CHECK(!okf || (KD - 1 - (nf + __popc(bf & lt)) >= 0 && KD - 1 - (nf + __popc(bf & lt)) >= nn));
                         if (okn) list[nn + __popc(bn & lt)] = make_int2(ent[j].x, nxt[j] - ent[j].x);
                         if (okf) list[KD - 1 - (nf + __popc(bf & lt))] = make_int2(ent[j].x, nxt[j] - ent[j].x);
                         nn += __popc(bn);
@@ -1224,7 +1236,8 @@ __global__ void __launch_bounds__(256) k_digest(Dev d, const int32_t* __restrict
                 }
                 const int rs = __shfl_sync(hm, st0, sl, 16), rx = __shfl_sync(hm, excl, sl, 16);
                 if (tq < total) {
-                    const int4 B = d.rec[rs + (tq - rx)];
+                    AM_CHECK(rs + (tq - rx) >= 0 && rs + (tq - rx) < d.n);
+                        const int4 B = d.rec[rs + (tq - rx)];
                     if (B.y == as && (uint32_t)B.z != aid) {
                         const int dx = (B.x & 0xFFFF) - ax, dy = (B.x >> 16) - ay;
                         if (within2(dx, dy, Rp2, Rp, d.metric))

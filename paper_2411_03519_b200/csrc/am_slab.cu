@@ -262,6 +262,7 @@ __global__ void k_sl_unite(SlabDev s, const int32_t* __restrict__ mbufs)
     const int nl = min(mb[0], s.g.cap_merge);
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nl; j += gridDim.x * blockDim.x) {
         const int2 e = mlink(s, mb, j);
+        AM_CHECK(e.x >= 0 && e.x < s.g.n_total && e.y >= 0 && e.y < s.g.n_total);
         s.touched[e.x] = 1;
         s.touched[e.y] = 1;
         if (e.x != e.y) uf_unite(s.forest, (uint32_t)e.x, (uint32_t)e.y);
@@ -528,7 +529,9 @@ __global__ void k_sl_depart(SlabDev s, const int32_t* __restrict__ drecv)
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += gridDim.x * blockDim.x) {
         const int32_t* d = blk + 6 + (size_t)j * kDeltaRec;
         const int g = d[0], y = d[2];
+        AM_CHECK(g >= 0 && g < s.g.n_total);
         const int i = s.map[g];
+        AM_CHECK(i < s.L);
         if (i < 0 || in_window(s, y)) continue;
         s.map[g] = -1;
         s.gid[i] = -1;
@@ -536,6 +539,7 @@ __global__ void k_sl_depart(SlabDev s, const int32_t* __restrict__ drecv)
         s.own[i] = 0;
         s.pos[i] = make_int2(0, s.y0);
         const int f = atomicAdd(s.ftop, 1);
+        AM_CHECK(f >= 0 && f < s.L);
         s.fstack[f] = i;
     }
 }
@@ -551,8 +555,10 @@ __global__ void k_sl_arrive(SlabDev s, const int32_t* __restrict__ drecv)
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += gridDim.x * blockDim.x) {
         const int32_t* d = blk + 6 + (size_t)j * kDeltaRec;
         const int g = d[0], x = d[1], y = d[2], stp = d[3];
+        AM_CHECK(g >= 0 && g < s.g.n_total);
         if (!in_window(s, y)) continue;
         int i = s.map[g];
+        AM_CHECK(i < s.L);
         if (i < 0) {   // arrival
             const int f = atomicSub(s.ftop, 1) - 1;
             if (f < 0) {
@@ -561,6 +567,7 @@ __global__ void k_sl_arrive(SlabDev s, const int32_t* __restrict__ drecv)
                 continue;
             }
             i = s.fstack[f];
+            AM_CHECK(i >= 0 && i < s.L);
             s.map[g] = i;
             s.gid[i] = g;
             s.tc[i] = kNever;

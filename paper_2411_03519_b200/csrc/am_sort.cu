@@ -298,6 +298,7 @@ __device__ void csort_run(const Dev& d, int32_t* __restrict__ order, unsigned ch
                 const E e = res[j];
                 const int dg = (int)((ekey(e) >> shift) & (kCsRadix - 1));
                 const uint32_t dst = base[dg] + run[dg] + (uint32_t)j - tstart[dg];
+                AM_CHECK(dst < (uint32_t)n);
                 if (last) order[dst] = (int32_t)e.v;
                 else gstore(d, (p + 1) & 1, (int)dst, e);
             }
