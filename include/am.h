@@ -89,6 +89,10 @@ extern "C" {
 #define AM_NO_ORDER     0x100u/* am_ready leaves `order` unwritten (the mask, labels and the  */
                               /* ready count are computed; the spatial-slab window tracker   */
                               /* orders its ranks' ready agents itself)                      */
+#define AM_LABELS_ONLY  0x200u/* binned path: am_ready stops after the labels and blocking   */
+                              /* verdicts (am_clusters, am_blocked): no mask, order, ready   */
+                              /* count or dispatch (mask / order may be NULL) -- the slab    */
+                              /* window tracker decides readiness in its merge               */
 #define AM_DBG_SKIP_NEAR 0x1000u /* PROFILING ONLY: skip the scan's near phase (wrong results) */
 #define AM_DBG_SKIP_FAR  0x2000u /* PROFILING ONLY: skip the scan's far phase (wrong results)  */
 

@@ -19,7 +19,7 @@ IDLE, RUNNING, DONE = 0, 1, 2
 METRIC_L2, METRIC_LINF, METRIC_GRAPH = 0, 1, 2
 VALIDATE, PEEK, DIGEST, ASYNC, FORCE_BINNED, FORCE_SMALL, STATS, SCAN_THREAD = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80)
-NO_ORDER = 0x100
+NO_ORDER, LABELS_ONLY = 0x100, 0x200
 
 ERROR_NAMES = {E_ARG: "AM_E_ARG", E_BOUNDS: "AM_E_BOUNDS", E_PROTOCOL: "AM_E_PROTOCOL",
                E_VELOCITY: "AM_E_VELOCITY", E_CUDA: "AM_E_CUDA", E_NCCL: "AM_E_NCCL",

@@ -630,7 +630,8 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
         if (n_ready) *n_ready = 0;
         return AM_OK;
     }
-    if (!mask || !order) return set_err(c, AM_E_ARG, "NULL mask/order");
+    const bool labels_only = c->path == 1 && (c->d.flags & AM_LABELS_ONLY);
+    if ((!mask || !order) && !labels_only) return set_err(c, AM_E_ARG, "NULL mask/order");
     am_join_side(c);   // the previous round's sort reads the buffers this round rewrites
     const Dev& d = c->d;
     cudaStream_t s = c->stream;
@@ -694,55 +695,57 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
                 LAUNCH(K_UNION, CK(c, launch_k(c->pdl, s, k_union, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
         }
         LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, blocks(d.n, 256 * kFinItems), 256, 0, d)));
-        LAUNCH(K_READY, CK(c, launch_k(c->pdl, s, k_ready, c->ntiles_ready, kReadyThreads, 0, d, mask)));
-        // the mask is final here: a caller may copy it out beside the rest of the round
-        if (c->mask_event && c->ev_mask) CK(c, cudaEventRecord(c->ev_mask, s));
-        static const bool dbg_nosort = [] { const char* e = getenv("AM_DBG_NOSORT"); return e && atoi(e); }();
-        if (dbg_nosort || (d.flags & AM_NO_ORDER)) {
-            // PROFILING ONLY (wrong `order`): measures how much of the round the sort holds up
-        } else if (c->csort_ctas) {
-            // one cluster of csort_ctas CTAs sorts the whole ready set (am_sort.cu), on the
-            // side stream: nothing else in the round reads `order` (digests and dispatch
-            // take the id-ordered ready list), so it overlaps the rest of the round and
-            // joins the main stream at am_join_side (end of a replay round, am_sync)
-            CK(c, cudaEventRecord(c->ev_fork, s));
-            CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-            cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3(c->csort_ctas);
-            lc.blockDim = dim3(csort_threads());
-            lc.dynamicSmemBytes = (size_t)c->csort_cap;
-            lc.stream = c->side;
-            cudaLaunchAttribute at{};
-            at.id = cudaLaunchAttributeClusterDimension;
-            at.val.clusterDim.x = c->csort_ctas; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
-            lc.attrs = &at; lc.numAttrs = 1;
-            cudaStream_t ms = c->stream;
-            c->stream = c->side;   // profiling events of the sort on its stream
-            am_prof_begin(c, K_SORT_PASS);
-            const cudaError_t le = cudaLaunchKernelEx(&lc, k_csort, d, order, c->csort_cap);
-            am_prof_end(c, K_SORT_PASS);
-            c->stream = ms;
-            if (le != cudaSuccess) return cuda_err(c, le, "k_csort launch");
-            CK(c, cudaEventRecord(c->ev_join, c->side));
-            c->join_pending = true;
-        } else {
-            LAUNCH(K_SORT_HIST, CK(c, launch_k(c->pdl, s, k_sort_hist, std::min(c->ntiles_sort, 32), 256, 0, d, c->sort_passes_max)));
-            am_prof_begin(c, K_SORT_PASS);
-            for (int p = 0; p < c->sort_passes_max; p++)   // persistent: <= 16 CTAs take tiles
-                CK(c, launch_k(c->pdl, s, k_sort_pass, std::min(c->ntiles_sort, c->sort_ctas), 1024, kSortSmem, d, p, order, c->ntiles_sort));
-            am_prof_end(c, K_SORT_PASS);
-        }
-        // perception digests of the dispatched agents (replay driver), on a second side
-        // stream forked after k_ready: they overlap the driver's dispatch part a, which
-        // does not read them; the driver joins them (am_join_digest) before part b
-        if (d.flags & AM_DIGEST) {
-            CK(c, cudaEventRecord(c->ev_fork, s));
-            CK(c, cudaStreamWaitEvent(c->side2, c->ev_fork, 0));
-            CK(c, launch_k(false, c->side2, k_digest, std::min(blocks(d.n, 16), (unsigned)c->num_sms * 8), 256, 0, d,
-                           (const int32_t*)d.rid, (const int32_t*)nullptr, (const int32_t*)nullptr,
-                           (unsigned long long*)nullptr));
-            CK(c, cudaEventRecord(c->ev_dig, c->side2));
-            c->dig_pending = true;
+        if (!labels_only) {   // else labels and verdicts are final (AM_LABELS_ONLY)
+            LAUNCH(K_READY, CK(c, launch_k(c->pdl, s, k_ready, c->ntiles_ready, kReadyThreads, 0, d, mask)));
+            // the mask is final here: a caller may copy it out beside the rest of the round
+            if (c->mask_event && c->ev_mask) CK(c, cudaEventRecord(c->ev_mask, s));
+            static const bool dbg_nosort = [] { const char* e = getenv("AM_DBG_NOSORT"); return e && atoi(e); }();
+            if (dbg_nosort || (d.flags & AM_NO_ORDER)) {
+                // PROFILING ONLY (wrong `order`): measures how much of the round the sort holds up
+            } else if (c->csort_ctas) {
+                // one cluster of csort_ctas CTAs sorts the whole ready set (am_sort.cu), on the
+                // side stream: nothing else in the round reads `order` (digests and dispatch
+                // take the id-ordered ready list), so it overlaps the rest of the round and
+                // joins the main stream at am_join_side (end of a replay round, am_sync)
+                CK(c, cudaEventRecord(c->ev_fork, s));
+                CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+                cudaLaunchConfig_t lc{};
+                lc.gridDim = dim3(c->csort_ctas);
+                lc.blockDim = dim3(csort_threads());
+                lc.dynamicSmemBytes = (size_t)c->csort_cap;
+                lc.stream = c->side;
+                cudaLaunchAttribute at{};
+                at.id = cudaLaunchAttributeClusterDimension;
+                at.val.clusterDim.x = c->csort_ctas; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+                lc.attrs = &at; lc.numAttrs = 1;
+                cudaStream_t ms = c->stream;
+                c->stream = c->side;   // profiling events of the sort on its stream
+                am_prof_begin(c, K_SORT_PASS);
+                const cudaError_t le = cudaLaunchKernelEx(&lc, k_csort, d, order, c->csort_cap);
+                am_prof_end(c, K_SORT_PASS);
+                c->stream = ms;
+                if (le != cudaSuccess) return cuda_err(c, le, "k_csort launch");
+                CK(c, cudaEventRecord(c->ev_join, c->side));
+                c->join_pending = true;
+            } else {
+                LAUNCH(K_SORT_HIST, CK(c, launch_k(c->pdl, s, k_sort_hist, std::min(c->ntiles_sort, 32), 256, 0, d, c->sort_passes_max)));
+                am_prof_begin(c, K_SORT_PASS);
+                for (int p = 0; p < c->sort_passes_max; p++)   // persistent: <= 16 CTAs take tiles
+                    CK(c, launch_k(c->pdl, s, k_sort_pass, std::min(c->ntiles_sort, c->sort_ctas), 1024, kSortSmem, d, p, order, c->ntiles_sort));
+                am_prof_end(c, K_SORT_PASS);
+            }
+            // perception digests of the dispatched agents (replay driver), on a second side
+            // stream forked after k_ready: they overlap the driver's dispatch part a, which
+            // does not read them; the driver joins them (am_join_digest) before part b
+            if (d.flags & AM_DIGEST) {
+                CK(c, cudaEventRecord(c->ev_fork, s));
+                CK(c, cudaStreamWaitEvent(c->side2, c->ev_fork, 0));
+                CK(c, launch_k(false, c->side2, k_digest, std::min(blocks(d.n, 16), (unsigned)c->num_sms * 8), 256, 0, d,
+                               (const int32_t*)d.rid, (const int32_t*)nullptr, (const int32_t*)nullptr,
+                               (unsigned long long*)nullptr));
+                CK(c, cudaEventRecord(c->ev_dig, c->side2));
+                c->dig_pending = true;
+            }
         }
     }
 #undef LAUNCH

@@ -1165,7 +1165,11 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
 #pragma unroll
     for (int k = 0; k < kFinItems; k++) {
         const int i = i0 + k * 256;
-        if (st[k] == ST_DONE) continue;
+        if (i < d.n) d.chg8[i] = 0;   // the round consumed this agent's change (nothing after reads it)
+        if (st[k] == ST_DONE) {
+            if (i < d.n) d.labels[i] = -1;
+            continue;
+        }
         uint32_t root = par[k];
         if (root != (uint32_t)i) root = uf_find(d.parent, (uint32_t)i);
         d.labels[i] = (int32_t)root;
@@ -1296,7 +1300,6 @@ __global__ void __launch_bounds__(kReadyThreads) k_ready(Dev d, uint8_t* __restr
     for (int k = 0; k < kReadyItems; k++) {
         const int i = i0 + k;
         if (i < d.n) {
-            if (d.chg8) d.chg8[i] = 0;     // the round consumed this agent's change
             if (st[k] == ST_DONE) {
                 d.labels[i] = -1;
                 lab[k] = -1;

@@ -650,7 +650,7 @@ am_config tracker_cfg(const am_slab_geom& g)
     c.cell = 0;
     c.metric = g.metric;
     // mode-3 replica updates ignore AM_VALIDATE (it keeps the incremental round on)
-    c.flags = AM_VALIDATE | AM_PEEK | AM_ASYNC | AM_FORCE_BINNED | AM_NO_ORDER;
+    c.flags = AM_VALIDATE | AM_PEEK | AM_ASYNC | AM_FORCE_BINNED | AM_NO_ORDER | AM_LABELS_ONLY;
     return c;
 }
 

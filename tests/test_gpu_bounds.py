@@ -36,5 +36,6 @@ def test_parity_subset_under_bounds_checks():
            "tests/test_gpu_tracker.py", "tests/test_gpu_replay.py", "tests/test_gpu_slabs.py", "-k", sel]
     r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=2400)
     out = r.stdout + r.stderr
+    print(out[-600:])   # the child's summary (pytest -rP shows it)
     assert r.returncode == 0, out[-4000:]
     assert " passed" in out and "failed" not in out, out[-2000:]
