@@ -102,3 +102,33 @@ def test_full_size_round_sampled_vs_oracle(name, preroll):
     np.testing.assert_array_equal(flabels.cpu().numpy(), labels)
     ft.close()
     rep.close()
+
+
+@pytest.mark.parametrize("name,rounds", [("C4", 300), ("C5", 60)])
+def test_replay_is_deterministic_at_full_size(name, rounds):
+    """Run-to-run determinism at BASELINE sizes (the kernels order their work with
+    atomics: slot count-downs, union-find hooks, stripe appends, sort ranks): two replays
+    of the same workload from the same initial state, in the launch configuration bench.py
+    times, dispatch the same agent-steps every round and end in the same world state
+    (positions, steps, trajectory hashes) -- every output that the oracle fixes is unique,
+    so any order dependence would show up here."""
+    w = amgen.config(name)
+    lm = amgen.latency_model(w.profile)
+    runs = []
+    for _ in range(2):
+        rep = Replay.from_workload(w, lm)
+        per_round = []
+        for _r in range(rounds // 20):
+            d0 = rep.dispatched()
+            rep.launch(20)
+            rep.sync()
+            per_round.append(rep.dispatched() - d0)
+        runs.append((per_round, rep.pos.cpu().numpy().copy(), rep.steps.cpu().numpy().copy(),
+                     rep.results()["traj"].copy()))
+        rep.close()
+    (d1, p1, s1, t1), (d2, p2, s2, t2) = runs
+    assert d1 == d2
+    assert sum(d1) > 0
+    np.testing.assert_array_equal(p1, p2)
+    np.testing.assert_array_equal(s1, s2)
+    np.testing.assert_array_equal(t1, t2)
