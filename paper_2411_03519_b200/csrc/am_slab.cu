@@ -609,9 +609,9 @@ struct am_slab {
     bool last_stale = false;      // the last round was a stale round
     // the rank's priority sort runs on a side stream beside commit / exchange / apply;
     // the slab's stream joins it before the next round rewrites its inputs
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
-    bool order_pending = false, order_timed = false;
+    cudaStream_t side = nullptr, side2 = nullptr;   // the sort; the merge forest's restore
+    cudaEvent_t ev_fork = nullptr, ev_s0 = nullptr, ev_s1 = nullptr, ev_r1 = nullptr;
+    bool order_pending = false, order_timed = false, restore_pending = false, last_restore = false;
 };
 
 // the slab's stream waits for the last priority sort (an event wait, no host sync)
@@ -620,6 +620,10 @@ static void slab_join(am_slab* sl)
     if (sl && sl->order_pending) {
         cudaStreamWaitEvent(sl->stream, sl->ev_s1, 0);
         sl->order_pending = false;
+    }
+    if (sl && sl->restore_pending) {
+        cudaStreamWaitEvent(sl->stream, sl->ev_r1, 0);
+        sl->restore_pending = false;
     }
 }
 
@@ -795,6 +799,8 @@ extern "C" int am_slab_create(am_slab** out, const am_slab_geom* g, const am_syn
     if (!rc) rc = ck(sl, cudaEventCreateWithFlags(&sl->ev_fork, cudaEventDisableTiming), "event");
     if (!rc) rc = ck(sl, cudaEventCreate(&sl->ev_s0), "event");
     if (!rc) rc = ck(sl, cudaEventCreate(&sl->ev_s1), "event");
+    if (!rc) rc = ck(sl, cudaStreamCreateWithFlags(&sl->side2, cudaStreamNonBlocking), "side stream");
+    if (!rc) rc = ck(sl, cudaEventCreate(&sl->ev_r1), "event");
     if (rc) { am_slab_destroy(sl); return rc; }
     // forest = identity: a tiny kernel-free init through the sort's control block is not
     // available, so fill from the host once (n_total words)
@@ -897,10 +903,17 @@ static int slab_finish(am_slab* sl, const int32_t* mbufs, int32_t* order_out, in
     // on the side stream (nothing in commit / apply reads them; the next round joins it
     // first): the merge forest's restore (reads mbufs: they stay untouched until then)
     // and the rank's priority order -- unique keys (lag, global label, id) -> global ids
+    // (two side streams: the restore and the sort touch disjoint buffers and run together)
     SK(cudaEventRecord(sl->ev_fork, sl->stream));
     SK(cudaStreamWaitEvent(sl->side, sl->ev_fork, 0));
     SK(cudaEventRecord(sl->ev_s0, sl->side));
-    if (mbufs) SK(launch_k(false, sl->side, k_sl_restore, gm, 256, 0, s, mbufs));
+    if (mbufs) {
+        SK(cudaStreamWaitEvent(sl->side2, sl->ev_fork, 0));
+        SK(launch_k(false, sl->side2, k_sl_restore, gm, 256, 0, s, mbufs));
+        SK(cudaEventRecord(sl->ev_r1, sl->side2));
+        sl->restore_pending = true;
+    }
+    sl->last_restore = mbufs != nullptr;
     rc = am_internal_csort(sl->tr, sl->sd, order_out, sl->side);
     if (rc) return rc;
     SK(cudaEventRecord(sl->ev_s1, sl->side));
@@ -922,6 +935,12 @@ extern "C" int am_slab_order_ms(am_slab* sl, float* ms)
     if (!sl->order_timed) return AM_E_STATE;
     SK(cudaEventSynchronize(sl->ev_s1));
     SK(cudaEventElapsedTime(ms, sl->ev_s0, sl->ev_s1));
+    if (sl->last_restore) {   // the restore beside it (same start): the longer of the two
+        float mr = 0.0f;
+        if (cudaEventSynchronize(sl->ev_r1) == cudaSuccess && cudaEventElapsedTime(&mr, sl->ev_s0, sl->ev_r1) == cudaSuccess)
+            *ms = std::max(*ms, mr);
+        cudaGetLastError();
+    }
     return AM_OK;
 }
 
@@ -1005,6 +1024,11 @@ extern "C" int am_slab_destroy(am_slab* sl)
         cudaStreamSynchronize(sl->side);
         cudaStreamDestroy(sl->side);
     }
+    if (sl->side2) {
+        cudaStreamSynchronize(sl->side2);
+        cudaStreamDestroy(sl->side2);
+    }
+    if (sl->ev_r1) cudaEventDestroy(sl->ev_r1);
     if (sl->ev_fork) cudaEventDestroy(sl->ev_fork);
     if (sl->ev_s0) cudaEventDestroy(sl->ev_s0);
     if (sl->ev_s1) cudaEventDestroy(sl->ev_s1);
