@@ -977,7 +977,10 @@ static int enqueue_round(am_replay* rp, bool external = false)
     const unsigned nbd = std::min(nb, (unsigned)c->num_sms * 4);   // grid-stride over the ready list
     RK(launch_k(c->pdl, rp->stream, k_disp_a, nbd, 256, 0, rp->r));
     am_prof_end(c, K_DISP_A);
-    am_join_digest(c);   // part b reads the digests (computed beside part a)
+    // PROFILING ONLY (AM_DBG_LATE_DIGEST=1, wrong moves): the join after the commit
+    // instead -- measures how much of the round the digests hold up beyond part a
+    static const bool late_dig = [] { const char* e = getenv("AM_DBG_LATE_DIGEST"); return e && atoi(e); }();
+    if (!late_dig) am_join_digest(c);   // part b reads the digests (computed beside part a)
     am_prof_begin(c, K_DISP_B);
     RK(launch_k(c->pdl, rp->stream, k_disp_b, nbd, 256, 0, rp->r));
     if (rp->r.K > 0 && c->path == 1) {
@@ -998,6 +1001,7 @@ static int enqueue_round(am_replay* rp, bool external = false)
         RK(launch_k(c->pdl, rp->stream, k_commit, ncb, 256, 0, rp->r, inplace ? 1 : 0));
     }
     am_join_side(c);   // the priority sort ran beside dispatch and commit
+    if (late_dig) am_join_digest(c);
     am_prof_end(c, K_COMMIT);
     RK(cudaGetLastError());
     return AM_OK;
