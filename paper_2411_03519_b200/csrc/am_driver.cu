@@ -128,7 +128,9 @@ __device__ __forceinline__ int commit_agent(const RepDev& r, int i, int s0, int 
 // once per 32 commits instead of once per 32 agents with any commit among them.
 __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
 {
+#if !(AM_PDL_EARLY & 2)
     pdl_begin();
+#endif
     constexpr int KC = kCommitItems;
     __shared__ int2 s_cl[8][32 * KC];   // per warp: {agent, old step} of the committing agents
     const Dev& d = r.d;
@@ -151,10 +153,23 @@ __global__ void __launch_bounds__(256) k_commit(RepDev r, int inplace)
         sw[k] = 0;
         if (i < d.n) {
             st[k] = d.status[c][i];  // after this round's dispatch
-            tc[k] = r.tcommit[i];
             if (inplace) sw[k] = r.steps[i];   // (post-commit W / S: issued with the others)
+#if !(AM_PDL_EARLY & 2)
+            tc[k] = r.tcommit[i];
+#endif
         }
     }
+#if AM_PDL_EARLY & 2
+    // statuses (k_ready) and steps (the last commit) were final before this kernel's
+    // predecessor began: loaded above while k_disp_b still runs (PDL); the completion
+    // times k_disp_b writes and the clock its last block sets, after the wait
+    pdl_begin();
+#pragma unroll
+    for (int k = 0; k < KC; k++) {
+        const int i = blockIdx.x * (256 * KC) + k * 256 + threadIdx.x;
+        if (i < d.n) tc[k] = r.tcommit[i];
+    }
+#endif
     const long long t1 = one ? r.t_sim[0] : 0;
     int nlist = 0;   // warp uniform
 #pragma unroll

@@ -16,7 +16,7 @@ __global__ void k_cells(Dev d);
 __global__ void k_scatter(Dev d);
 __global__ void k_scan(Dev d);
 __global__ void k_scan_thread(Dev d);
-__global__ void k_finalize(Dev d);
+__global__ void k_finalize(Dev d, int early);
 __global__ void k_union(Dev d);
 __global__ void k_scan_hw(Dev d);
 __global__ void k_scan_hw_full(Dev d);
@@ -694,7 +694,10 @@ extern "C" int am_ready(am_ctx* c, uint8_t* mask, int32_t* order, int32_t* n_rea
             if (!AM_SCAN_UNITE)   // else the scan united its new edges as it flushed them
                 LAUNCH(K_UNION, CK(c, launch_k(c->pdl, s, k_union, std::min(blocks(d.ecap, 256), pers), 256, 0, d)));
         }
-        LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, blocks(d.n, 256 * kFinItems), 256, 0, d)));
+        {   // early loads when k_union precedes it (not the ablation scan, not AM_SCAN_UNITE)
+            const int early = (c->pdl && !(d.flags & AM_SCAN_THREAD) && !AM_SCAN_UNITE) ? 1 : 0;
+            LAUNCH(K_FINALIZE, CK(c, launch_k(c->pdl, s, k_finalize, blocks(d.n, 256 * kFinItems), 256, 0, d, early)));
+        }
         if (!labels_only) {   // else labels and verdicts are final (AM_LABELS_ONLY)
             LAUNCH(K_READY, CK(c, launch_k(c->pdl, s, k_ready, c->ntiles_ready, kReadyThreads, 0, d, mask)));
             // the mask is final here: a caller may copy it out beside the rest of the round

@@ -46,6 +46,9 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #else
 #define AM_CHECK(c) ((void)0)
 #endif
+#ifndef AM_PDL_EARLY
+#define AM_PDL_EARLY 5   // bits: 1 k_finalize, 2 k_commit, 4 k_scatter load what their predecessor does not write before the PDL wait
+#endif
 #ifndef AM_SCAN_1PASS
 #define AM_SCAN_1PASS 1   // scan_hw: near and far cells classified in one pass
 #endif

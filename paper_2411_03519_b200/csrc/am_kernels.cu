@@ -335,7 +335,9 @@ __global__ void __launch_bounds__(kCellsThreads) k_cells(Dev d)
 // queue of this round.
 __global__ void __launch_bounds__(256) k_scatter(Dev d)
 {
+#if !(AM_PDL_EARLY & 4)
     pdl_begin();
+#endif
     __shared__ uint32_t s_w[9];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t c = d.ctl->cur;
@@ -343,21 +345,44 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
     const uint32_t ep = d.ctl->epoch & kTagMask;
     bool work = false;
     int4 q = make_int4(0, 0, 0, 0);
+    // every read but the binning's (the agent state, last round's labels, witnesses,
+    // dirty marks: final before k_bin began) first -- with AM_PDL_EARLY while k_cells
+    // still runs; the cell table, the counts and every write after the PDL wait
+    int2 p = make_int2(0, 0);
+    int s = 0, lab = -1;
+    uint8_t st = ST_DONE;
+    bool chg = false, dirty = false;
     if (i < d.n) {
-        const int2 p = d.pos[c][i];
-        const int s = d.step[c][i];
-        const uint8_t st = d.status[c][i];
+        p = d.pos[c][i];
+        s = d.step[c][i];
+        st = d.status[c][i];
         const bool ch = d.chg8[i] != 0;
-        const int lab = d.labels[i];
+        lab = d.labels[i];
         const uint32_t w = d.witness[i];
         const bool full = round_full(d);
+        if (st != ST_DONE) {
+            chg = full || ch;
+            // union-find forest of this round: an agent whose last-round cluster has no
+            // changed member keeps that cluster (all its coupling edges are unchanged: it
+            // is still connected, and it can only grow through an edge of a changed
+            // agent), so it hangs under the old root (= min id = its label); members of
+            // dirty clusters start alone
+            dirty = full || lab < 0 || d.dirty[lab] == d.ctl->epoch;
+            // the scan's work queue (incremental scan, DESIGN.md section 6): changed
+            // agents, and IDLE agents whose recorded blocker (witness) changed
+            work = chg || (st == ST_IDLE && w != kSentinel && agent_changed(d, c, w));
+        }
+    }
+#if AM_PDL_EARLY & 4
+    pdl_begin();
+#endif
+    if (i < d.n) {
         d.bad[i] = 0;     // per-root flags of this round (k_finalize)
         d.blkid[i] = 0;
         if (st == ST_DONE) {   // DONE: counts as changed for the carried edges (k_efilter)
             d.agflag[i] = 1;
             if (rebuild) d.slot[i] = kSentinel;
         } else {
-            const bool chg = full || ch;
             if (rebuild) {
                 // slot: the cell's start + its count taken back down (returns the counts to 0)
                 const uint32_t key = d.key[i];
@@ -368,17 +393,8 @@ __global__ void __launch_bounds__(256) k_scatter(Dev d)
                 d.rec[r] = make_int4(p.x | (p.y << 16), s, i, (int)st | (int)(tag << kTagShift));
                 d.slot[i] = r;
             }
-            // union-find forest of this round: an agent whose last-round cluster has no
-            // changed member keeps that cluster (all its coupling edges are unchanged: it
-            // is still connected, and it can only grow through an edge of a changed
-            // agent), so it hangs under the old root (= min id = its label); members of
-            // dirty clusters start alone
-            const bool dirty = full || lab < 0 || d.dirty[lab] == d.ctl->epoch;
             d.parent[i] = dirty ? (uint32_t)i : (uint32_t)lab;
             d.agflag[i] = (uint8_t)((chg ? 1 : 0) | (dirty ? 2 : 0));
-            // the scan's work queue (incremental scan, DESIGN.md section 6): changed
-            // agents, and IDLE agents whose recorded blocker (witness) changed
-            work = chg || (st == ST_IDLE && w != kSentinel && agent_changed(d, c, w));
             q = make_int4(p.x | (p.y << 16), s, (int)((uint32_t)i | (chg ? 0x80000000u : 0u)), st);
         }
     }
@@ -1134,11 +1150,14 @@ __global__ void __launch_bounds__(256) k_union(Dev d)
 // a blocked or RUNNING member makes its cluster not ready (Q7).
 // Id order: status / parent / verdict / label accesses are coalesced; only agents
 // whose parent is not themselves chase pointers (singletons are one load).
-__global__ void __launch_bounds__(256) k_finalize(Dev d)
+// early = 1: this kernel's predecessor is k_union, so the statuses and the scan's
+// verdicts were final before it began and are loaded before the PDL wait
+__global__ void __launch_bounds__(256) k_finalize(Dev d, int early)
 {
-    pdl_begin();
+    early = (AM_PDL_EARLY & 1) ? early : 0;
+    if (!early) pdl_begin();
     const int i0 = blockIdx.x * (256 * kFinItems) + threadIdx.x;
-    if (i0 == 0) {
+    if (i0 == 0 && !early) {
         d.ctl->full = 0;   // every kernel that reads the full-round flag has run
         if (AM_SCAN_UNITE) {   // (k_union's statistic)
             const uint32_t nxt = d.ctl->ecur ^ 1u;
@@ -1159,7 +1178,16 @@ __global__ void __launch_bounds__(256) k_finalize(Dev d)
         if (i < d.n) {
             st[k] = d.status[c][i];
             vb[k] = d.v8[i];
-            par[k] = ld_cg(d.parent + i);
+            if (!early) par[k] = ld_cg(d.parent + i);
+        }
+    }
+    if (early) {   // the forest k_union writes, after the wait
+        pdl_begin();
+        if (i0 == 0) d.ctl->full = 0;   // every kernel that reads the full-round flag has run
+#pragma unroll
+        for (int k = 0; k < kFinItems; k++) {
+            const int i = i0 + k * 256;
+            if (i < d.n) par[k] = ld_cg(d.parent + i);
         }
     }
 #pragma unroll
