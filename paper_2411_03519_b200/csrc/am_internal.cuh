@@ -68,7 +68,7 @@ constexpr int kScanAllTiles = 1024;       // chained scans sum all predecessors 
 #define AM_SCAN_FULL_REC 1   // full rounds take their agents from the cell-sorted records
 #endif
 #ifndef AM_DIRECT_FULL
-#define AM_DIRECT_FULL 16   // ... of full-recompute rounds (C5 snapshot A/B: 777 / 649 / 624 us at 64 / 32 / 16)
+#define AM_DIRECT_FULL 32   // ... of full-recompute rounds (C5 snapshot A/B with 16-tile cells: 777 / 649 / 624 us at 64 / 32 / 16; with 32-tile cells: 607 / 597 / 602 us, profiles/r2_sweep_s29)
 #endif
 #ifndef AM_COMMIT_SPLIT
 #define AM_COMMIT_SPLIT 0   // 1: the replay's commit as an O(N) scan + a dense pass over the committing
