@@ -227,7 +227,7 @@ def run_reference(args, w, lm):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / max(1, args.steps),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic", "config": _config(w, ws),
         "cpu_baseline": {"kind": "oracle", "value": value, "unit": UNIT, "cores": nt,
                          "sample": f"{sampled} sampled agents of the {w.name} round after a "
@@ -828,7 +828,8 @@ def run_ours(args, w, lm):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        # the same C5 map at every N (N > 1: split into slabs, run_slabs): total work fixed
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": _config(w, ws),
         "rounds_per_s": rounds_per_s,
         "agent_steps_per_round": agent_steps / args.steps / ws,
